@@ -1,0 +1,145 @@
+/*
+ * adamk.h -- C ABI of the B200 decode MegaKernel plugin (libadamk.so).
+ *
+ * Drop-in boundary.  The reference describes this call
+ * only in prose: "embed MegaKernel ... into TensorRT-LLM's execution topology
+ * via a Plugin mechanism", "replace only the core Transformer Block with a
+ * custom MegaKernel plugin", Prefill on native ops / Decode on the MegaKernel
+ * (/root/reference/PAPER.md:244-249), and its SPEC puts the plugin itself out
+ * of scope.  There is therefore no reference
+ * signature to copy; these entry points have the shape of a TensorRT
+ * IPluginV2::enqueue(inputs, outputs, workspace, stream) call and are what a
+ * maintainer of the reference's online half would bind (see INTEGRATION.md for
+ * the ctypes stub).  What the plugin consumes is the reference's own artifact:
+ * the SolidifiedTrace written by `mkplan search`
+ * (/root/reference/pkg/src/mkplan/search.py:79-107,138-171), lowered by
+ * paper_2605_11581_b200/task_table.py to the flat device task table passed to
+ * adamk_create().
+ *
+ * Conventions: every function returns 0 on success or a negative ADAMK_E_*
+ * code; adamk_last_error() returns a thread-local message.  No exceptions and
+ * no C++/torch types cross the boundary.  The caller owns every device buffer
+ * (weights, packed weights, KV cache, workspace, outputs); the library owns
+ * only its handle and the device copy of the task table.  decode_step is
+ * asynchronous on the given stream and not re-entrant per handle.
+ */
+#ifndef ADAMK_H_
+#define ADAMK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADAMK_ABI_VERSION 1
+
+#define ADAMK_OK 0
+#define ADAMK_E_INVALID (-1)     /* bad argument / malformed task table        */
+#define ADAMK_E_CUDA (-2)        /* a CUDA runtime call failed                 */
+#define ADAMK_E_UNSUPPORTED (-3) /* valid request this build cannot execute    */
+#define ADAMK_E_STATE (-4)       /* call order violated (e.g. step before bind) */
+#define ADAMK_E_DEVICE (-5)      /* the kernel reported an error (watchdog...) */
+
+typedef struct AdamkHandle_* adamk_handle;
+typedef void* adamk_stream; /* cudaStream_t */
+
+/* Decoder dimensions.  Mirrors paper_2605_11581_b200.model_config.ModelConfig. */
+typedef struct AdamkModelDesc {
+  int32_t hidden, n_layers, n_q_heads, n_kv_heads, head_dim, intermediate, vocab;
+  int32_t max_ctx;   /* KV-cache capacity in positions                          */
+  int32_t max_batch; /* sequences per step the task table was built for         */
+  int32_t qkv_bias;  /* Qwen2/Qwen2.5: 1                                        */
+  int32_t qk_norm;   /* Qwen3: 1                                                */
+  int32_t tied_embed;
+  float rms_eps;
+  float rope_theta;  /* informational; the kernel reads the cos/sin tables      */
+} AdamkModelDesc;
+
+/* Per-layer bf16 weights in Hugging Face layout ([out_features, in_features],
+ * row-major).  Optional pointers are NULL when the model has no such tensor. */
+typedef struct AdamkLayerWeights {
+  const void* ln1;    /* [hidden]                      */
+  const void* wq;     /* [q_dim, hidden]               */
+  const void* wk;     /* [kv_dim, hidden]              */
+  const void* wv;     /* [kv_dim, hidden]              */
+  const void* bq;     /* [q_dim]      or NULL          */
+  const void* bk;     /* [kv_dim]     or NULL          */
+  const void* bv;     /* [kv_dim]     or NULL          */
+  const void* q_norm; /* [head_dim]   or NULL (Qwen3)  */
+  const void* k_norm; /* [head_dim]   or NULL (Qwen3)  */
+  const void* wo;     /* [hidden, q_dim]               */
+  const void* ln2;    /* [hidden]                      */
+  const void* wgate;  /* [intermediate, hidden]        */
+  const void* wup;    /* [intermediate, hidden]        */
+  const void* wdown;  /* [hidden, intermediate]        */
+} AdamkLayerWeights;
+
+typedef struct AdamkWeightPtrs {
+  const void* embed;      /* bf16 [vocab, hidden]; must stay alive (row gather)  */
+  const void* final_norm; /* bf16 [hidden]                                       */
+  const void* lm_head;    /* bf16 [vocab, hidden]; NULL = tied to embed          */
+  const AdamkLayerWeights* layers; /* HOST array of n_layers entries             */
+  const float* rope_cos;  /* fp32 [max_ctx, head_dim/2] device                   */
+  const float* rope_sin;  /* fp32 [max_ctx, head_dim/2] device                   */
+} AdamkWeightPtrs;
+
+/* ABI / device queries (no handle needed). */
+int adamk_abi_version(void);
+int adamk_device_sm_count(int device, int* out_sms);
+const char* adamk_last_error(void);
+
+/* Create a plugin instance from the model description and the device task
+ * table blob (task_table.py: header, per-SM ranges, 64-byte task records).
+ * The table is validated against the description and the device, then copied
+ * to the GPU.  tp_rank/tp_size select the tensor-parallel shard (1 GPU: 0/1). */
+int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task_table_bytes,
+                 int tp_rank, int tp_size, adamk_handle* out);
+void adamk_destroy(adamk_handle h);
+
+/* Bytes of the caller-allocated packed-weight buffer (tile-major per-SM weight
+ * streams + fp32 copies of the norm/bias vectors). */
+size_t adamk_packed_bytes(adamk_handle h);
+/* Repack the HF-layout weights into `packed` (device, 256-byte aligned) on
+ * `stream` and remember the pointers.  The source matrices may be freed after
+ * the stream has drained, except `embed`. */
+int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, adamk_stream stream);
+
+/* Tensor parallelism only: peer workspace base pointers (device-mapped peer
+ * memory, one per rank, own rank included) for the in-kernel NVLink reduction. */
+int adamk_bind_peers(adamk_handle h, void* const* peer_workspaces, int n_peers);
+
+/* Workspace: activations, attention partials, per-SM argmax partials and the
+ * dependency counters.  Must be zero-initialised once with workspace_init. */
+size_t adamk_workspace_bytes(adamk_handle h);
+int adamk_workspace_init(adamk_handle h, void* workspace, adamk_stream stream);
+
+/* KV cache geometry: each of k_cache / v_cache is bf16
+ * [n_layers, max_batch, n_kv_heads, max_ctx, head_dim]. */
+size_t adamk_kv_cache_bytes(adamk_handle h);
+
+/* One decode step for `batch` sequences: ONE launch of the persistent kernel.
+ * token_ids / positions / next_token_out are DEVICE int32[batch]; logits_out is
+ * DEVICE fp32 [batch, vocab] or NULL.  Writes K/V of the new token at
+ * positions[b] and the greedy next token.  With auto_advance != 0 the kernel
+ * also stores next_token into token_ids and increments positions, so steps can
+ * be enqueued back to back with no host round trip. */
+int adamk_decode_step(adamk_handle h, int32_t* token_ids, int32_t* positions, int batch,
+                      void* k_cache, void* v_cache, void* workspace,
+                      float* logits_out, int32_t* next_token_out, int auto_advance,
+                      adamk_stream stream);
+
+/* Poll the device-written status block (host-mapped); 0 = no error recorded.
+ * Fills `info` (8 ints: code, sm, task, counter, seen, expected, ...) if not NULL. */
+int adamk_device_status(adamk_handle h, int32_t* info);
+
+/* Standalone weight-streaming probe used by the measurement harness: runs only
+ * the Loader/Consumer ring over the packed stream (no dependencies), to
+ * separate HBM streaming efficiency from dependency stalls. */
+int adamk_stream_probe(adamk_handle h, float* sink, adamk_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADAMK_H_ */

@@ -1,0 +1,1154 @@
+// adamk.cu -- persistent, warp-specialised decode MegaKernel for sm_100a + its C ABI.
+//
+// One launch = one decode step of the whole model (every layer + LM head + argmax).
+// grid = one CTA per SM; each CTA walks its static, program-ordered task list
+// (paper_2605_11581_b200/task_table.py).  Roles follow the reference's role split
+// (/root/reference/pkg/src/mkplan/planner.py:60-77):
+//   Loader   : warp 0, one elected lane.  Streams the CTA's weight sub-tiles with
+//              cp.async.bulk (TMA, SASS UBLKCP) into an n_stage-deep shared-memory
+//              ring; never looks at activations, so it runs ahead across operator
+//              and layer boundaries (the paper's "asynchronous prefetching and
+//              logical decoupling") limited only by free ring slots.
+//   Consumer : warps 1..C.  Wait on the operator's dependency counter, stage the
+//              fp32 activation vector in shared memory (fusing RMSNorm), then GEMV
+//              out of the ring with LDS.128 + FFMA and warp-shuffle reductions.
+//   Storer   : the consumers' epilogue (bias / residual / SiLU*up / argmax) and the
+//              release of the operator's global counter.
+// Page states Empty -> Locked -> Ready (planner.py:84-94) = ring slot `empty`
+// mbarrier phase -> TMA in flight -> `full` mbarrier phase.
+// Inter-SM dependencies are monotonically increasing global counters whose target
+// values are fixed in the task table ("path solidification").
+//
+// Numerical contract (shared with oracle/decode_ref.py): bf16 weights used exactly,
+// fp32 activations and accumulation, bf16 KV cache, fp32 RoPE tables from the host.
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/adamk.h"
+
+// ----------------------------------------------------------------------------------
+// task table format (keep in sync with task_table.py)
+// ----------------------------------------------------------------------------------
+namespace {
+
+constexpr int kMagic = 0x4B4D4441;
+constexpr int kVersion = 1;
+constexpr int kHeaderInts = 16;
+constexpr int kTaskInts = 16;
+constexpr int kChunk = 256;          // K elements per chunk
+constexpr int kSmemMax = 232448;
+constexpr int kSmemReserved = 1024;  // barriers + reduction scratch
+constexpr int kMaxStages = 16;
+constexpr int kAttnCLMax = 512;
+constexpr int kGMax = 8;             // max q heads per kv head
+
+enum TaskType { T_END = 0, T_QKV = 1, T_ATTN = 2, T_OPROJ = 3, T_GATEUP = 4, T_DOWN = 5, T_LMHEAD = 6 };
+enum Ctr { CTR_A = 0, CTR_B = 1, CTR_C = 2, CTR_D = 3, CTR_E = 4, CTR_F = 5, CTR_HEAD0 = 6 };
+
+struct Task {  // 64 bytes
+  int type, layer, a, b, k, kchunks, rt, ktc, n_tiles, n_ktiles, w_off, n_stages, wait_ctr, wait_val, sig_ctr, aux;
+};
+static_assert(sizeof(Task) == kTaskInts * 4, "task record is 64 bytes");
+
+// device error codes written to the host-mapped status block
+enum DevErr { DE_NONE = 0, DE_WATCHDOG_CTR = 1, DE_WATCHDOG_FULL = 2, DE_WATCHDOG_EMPTY = 3, DE_BAD_POS = 4 };
+
+struct KParams {
+  // model
+  int H, L, nq, nkv, D, I, V, G, q_dim, kv_dim, qkv_rows, max_ctx, batch;
+  int has_bias, qk_norm;
+  float eps;
+  // schedule
+  int C, n_stage, stage_bytes, attn_chunks, attn_min_chunk, scratch_bytes, n_lm_tasks, n_counters;
+  // task table
+  const Task* tasks;
+  const int* sm_begin;
+  // weights
+  const uint8_t* wpacked;   // tile-major bf16 weight streams
+  const float* fparams;     // fp32 norm gains / biases
+  int fp_layer_stride, fp_ln1, fp_ln2, fp_bias, fp_qn, fp_kn, fp_final;
+  const __nv_bfloat16* embed;
+  const float* rope_cos;
+  const float* rope_sin;
+  // per-step buffers
+  __nv_bfloat16* kcache;
+  __nv_bfloat16* vcache;
+  float* h_a;
+  float* h_b;
+  float* qkv;
+  float* attn;
+  float* act;
+  float* part;
+  float* lm_val;
+  int* lm_idx;
+  unsigned* counters;
+  float* logits;
+  int* tokens;
+  int* positions;
+  int* next_tokens;
+  int* status;  // host-mapped, 8 ints
+  int auto_advance;
+  int probe;    // 1 = stream probe: consumers skip dependencies and epilogues
+  float* probe_sink;
+};
+
+// ----------------------------------------------------------------------------------
+// PTX helpers
+// ----------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ uint32_t mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok;
+}
+// TMA bulk copy global -> shared, completion on an mbarrier (SASS: UBLKCP)
+__device__ __forceinline__ void tma_bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_acqrel_add(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+// named barrier over the consumer warps only (barrier 0 is __syncthreads)
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+__device__ __forceinline__ float4 lds128f(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128u(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+constexpr long long kWatchdogCycles = 6000000000LL;  // ~3 s at 2 GHz; a step takes < 1 ms
+
+__device__ __noinline__ void dev_fail(const KParams& p, int code, int task, int a, int b, int c) {
+  volatile int* s = p.status;
+  if (s) {
+    s[1] = blockIdx.x; s[2] = task; s[3] = a; s[4] = b; s[5] = c; s[6] = threadIdx.x;
+    __threadfence_system();
+    s[0] = code;
+    __threadfence_system();
+  }
+  __trap();
+}
+
+__device__ __forceinline__ void mbar_wait(const KParams& p, uint32_t bar, uint32_t parity, int code, int task) {
+  if (mbar_try_wait(bar, parity)) return;
+  long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > kWatchdogCycles) dev_fail(p, code, task, (int)bar, (int)parity, 0);
+  }
+}
+
+// ----------------------------------------------------------------------------------
+// shared-memory layout
+// ----------------------------------------------------------------------------------
+struct SmemHdr {
+  unsigned long long full[kMaxStages];
+  unsigned long long empty[kMaxStages];
+  float red[64];
+  int misc[32];
+};
+static_assert(sizeof(SmemHdr) <= kSmemReserved, "smem header too large");
+
+struct ConsumerCtx {
+  uint32_t it;        // ring stages consumed so far (slot = it % n_stage)
+  int cw;             // consumer warp index 0..C-1
+  int lane;
+  int ctid;           // thread index among consumers
+  int nct;            // number of consumer threads
+  float best_val;     // LM-head running argmax (lane 0 of each warp)
+  int best_idx;
+};
+
+// ----------------------------------------------------------------------------------
+// dependency wait / signal
+// ----------------------------------------------------------------------------------
+__device__ __forceinline__ void wait_counter(const KParams& p, const ConsumerCtx& c, int ctr, int val, int task) {
+  if (ctr >= 0 && !p.probe) {
+    if (c.ctid == 0) {
+      const unsigned* addr = p.counters + ctr;
+      if (ld_acquire_u32(addr) < (unsigned)val) {
+        long long t0 = clock64();
+        unsigned seen;
+        while ((seen = ld_acquire_u32(addr)) < (unsigned)val) {
+          if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_CTR, task, ctr, (int)seen, val);
+        }
+      }
+    }
+  }
+  consumer_sync(c.nct);
+}
+
+// all consumer threads have finished their global writes for this task
+__device__ __forceinline__ void signal_counter(const KParams& p, const ConsumerCtx& c, int ctr) {
+  consumer_sync(c.nct);
+  if (c.ctid == 0 && ctr >= 0 && !p.probe) red_release_add(p.counters + ctr, 1u);
+}
+
+// ----------------------------------------------------------------------------------
+// GEMV task
+// ----------------------------------------------------------------------------------
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + expf(-g)); }
+
+// fp32 hidden-state element of the layer input: layer 0 reads the embedding row
+__device__ __forceinline__ float4 load_h4(const KParams& p, int layer, bool mid, int tok, int i4) {
+  if (mid) return __ldcg(reinterpret_cast<const float4*>(p.h_b) + i4);
+  if (layer == 0) {
+    const uint2 raw = __ldg(reinterpret_cast<const uint2*>(p.embed + (size_t)tok * p.H) + i4);
+    return make_float4(bf_lo(raw.x), bf_hi(raw.x), bf_lo(raw.y), bf_hi(raw.y));
+  }
+  return __ldcg(reinterpret_cast<const float4*>(p.h_a) + i4);
+}
+__device__ __forceinline__ float load_h1(const KParams& p, int layer, int tok, int i) {
+  if (layer == 0) return __bfloat162float(p.embed[(size_t)tok * p.H + i]);
+  return __ldcg(p.h_a + i);
+}
+
+// Stage the activation vector of a GEMV in shared memory (fp32, zero padded to kpad).
+__device__ __forceinline__ void gemv_prologue(const KParams& p, const ConsumerCtx& c, const Task& t, float* xs,
+                                              SmemHdr* hdr, int tok) {
+  const int kpad = t.kchunks * kChunk;
+  const int type = t.type;
+  if (type == T_OPROJ || type == T_DOWN) {
+    const float* src = (type == T_OPROJ) ? p.attn : p.act;
+    const int k4 = t.k >> 2;
+    for (int i = c.ctid; i < (kpad >> 2); i += c.nct) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < k4) v = __ldcg(reinterpret_cast<const float4*>(src) + i);
+      reinterpret_cast<float4*>(xs)[i] = v;
+    }
+    consumer_sync(c.nct);
+    return;
+  }
+  // RMSNorm-fused prologues: QKV (ln1 over layer input), GATEUP (ln2 over h_mid), LMHEAD (final norm)
+  const bool mid = (type == T_GATEUP);
+  const int layer = (type == T_LMHEAD) ? p.L : t.layer;  // LM head reads h_a (layer index L > 0)
+  const float* gain = (type == T_LMHEAD) ? (p.fparams + p.fp_final)
+                                         : (p.fparams + (size_t)t.layer * p.fp_layer_stride + (mid ? p.fp_ln2 : p.fp_ln1));
+  const int h4 = p.H >> 2;
+  float ss = 0.f;
+  for (int i = c.ctid; i < (kpad >> 2); i += c.nct) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < h4) v = load_h4(p, layer, mid, tok, i);
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    reinterpret_cast<float4*>(xs)[i] = v;
+  }
+  ss = warp_sum(ss);
+  if (c.lane == 0) hdr->red[c.cw] = ss;
+  consumer_sync(c.nct);
+  float tot = 0.f;
+  for (int w = 0; w < p.C; ++w) tot += hdr->red[w];
+  const float rs = rsqrtf(tot / (float)p.H + p.eps);
+  for (int i = c.ctid; i < h4; i += c.nct) {
+    float4 v = reinterpret_cast<float4*>(xs)[i];
+    const float4 g = __ldg(reinterpret_cast<const float4*>(gain) + i);
+    v.x = v.x * rs * g.x; v.y = v.y * rs * g.y; v.z = v.z * rs * g.z; v.w = v.w * rs * g.w;
+    reinterpret_cast<float4*>(xs)[i] = v;
+  }
+  consumer_sync(c.nct);
+}
+
+__device__ __forceinline__ void gemv_epilogue(const KParams& p, ConsumerCtx& c, const Task& t, int vrow, float v,
+                                              float v_pair, int tok) {
+  switch (t.type) {
+    case T_QKV: {
+      if (p.has_bias) v += __ldg(p.fparams + (size_t)t.layer * p.fp_layer_stride + p.fp_bias + vrow);
+      p.qkv[vrow] = v;
+    } break;
+    case T_OPROJ: p.h_b[vrow] = load_h1(p, t.layer, tok, vrow) + v; break;
+    case T_GATEUP: p.act[vrow >> 1] = silu(v) * v_pair; break;  // vrow even = gate, pair = up
+    case T_DOWN: p.h_a[vrow] = __ldcg(p.h_b + vrow) + v; break;
+    case T_LMHEAD: {
+      if (p.logits) p.logits[vrow] = v;
+      if (v > c.best_val) { c.best_val = v; c.best_idx = vrow; }  // rows ascend: first max wins ties
+    } break;
+    default: break;
+  }
+}
+
+template <int RW>
+__device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx,
+                                           const float* xs, SmemHdr* hdr, uint8_t* ring, int tok) {
+  const uint32_t xs_addr = smem_u32(xs) + c.lane * 16;
+  const uint32_t ring_addr = smem_u32(ring);
+  const uint32_t full0 = smem_u32(&hdr->full[0]);
+  const uint32_t empty0 = smem_u32(&hdr->empty[0]);
+  for (int tile = 0; tile < t.n_tiles; ++tile) {
+    const int rows = min(t.rt, t.b - tile * t.rt);
+    float acc0[RW], acc1[RW];
+#pragma unroll
+    for (int i = 0; i < RW; ++i) { acc0[i] = 0.f; acc1[i] = 0.f; }
+    const int r0 = c.cw * RW;
+    for (int kt = 0; kt < t.n_ktiles; ++kt) {
+      const int chunks = min(t.ktc, t.kchunks - kt * t.ktc);
+      const uint32_t slot = c.it % (uint32_t)p.n_stage;
+      const uint32_t ph = (c.it / (uint32_t)p.n_stage) & 1u;
+      mbar_wait(p, full0 + slot * 8, ph, DE_WATCHDOG_FULL, task_idx);
+      if (r0 < rows) {
+        const uint32_t row_stride = (uint32_t)chunks * 512u;
+        const uint32_t wbase = ring_addr + slot * (uint32_t)p.stage_bytes + (uint32_t)r0 * row_stride + c.lane * 16;
+        const uint32_t xk = xs_addr + (uint32_t)(kt * t.ktc) * (kChunk * 4);
+#pragma unroll 2
+        for (int ch = 0; ch < chunks; ++ch) {
+          const float4 xa = lds128f(xk + ch * (kChunk * 4));
+          const float4 xb = lds128f(xk + ch * (kChunk * 4) + 512);
+#pragma unroll
+          for (int i = 0; i < RW; ++i) {
+            if (r0 + i < rows) {
+              const uint4 w = lds128u(wbase + i * row_stride + ch * 512);
+              acc0[i] = fmaf(bf_lo(w.x), xa.x, acc0[i]);
+              acc1[i] = fmaf(bf_hi(w.x), xa.y, acc1[i]);
+              acc0[i] = fmaf(bf_lo(w.y), xa.z, acc0[i]);
+              acc1[i] = fmaf(bf_hi(w.y), xa.w, acc1[i]);
+              acc0[i] = fmaf(bf_lo(w.z), xb.x, acc0[i]);
+              acc1[i] = fmaf(bf_hi(w.z), xb.y, acc1[i]);
+              acc0[i] = fmaf(bf_lo(w.w), xb.z, acc0[i]);
+              acc1[i] = fmaf(bf_hi(w.w), xb.w, acc1[i]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (c.lane == 0) mbar_arrive(empty0 + slot * 8);
+      ++c.it;
+    }
+    if (p.probe) {
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < RW; ++i) s += acc0[i] + acc1[i];
+      if (s == 1.2345678e-30f) p.probe_sink[blockIdx.x] = s;  // keep the math alive
+      continue;
+    }
+    if (r0 < rows) {
+      float v[RW];
+#pragma unroll
+      for (int i = 0; i < RW; ++i) v[i] = warp_sum(acc0[i] + acc1[i]);
+      if (c.lane == 0) {
+        const int vrow0 = t.a + tile * t.rt + r0;
+        if (t.type == T_GATEUP) {
+#pragma unroll
+          for (int i = 0; i < RW; i += 2)
+            if (r0 + i < rows) gemv_epilogue(p, c, t, vrow0 + i, v[i], v[(i + 1) % RW], tok);
+        } else {
+#pragma unroll
+          for (int i = 0; i < RW; ++i)
+            if (r0 + i < rows) gemv_epilogue(p, c, t, vrow0 + i, v[i], 0.f, tok);
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void lm_finish(const KParams& p, ConsumerCtx& c, SmemHdr* hdr) {
+  // per-warp best -> CTA best -> global partial -> last CTA reduces, publishes, resets counters
+  float bv = __shfl_sync(0xffffffffu, c.best_val, 0);
+  int bi = __shfl_sync(0xffffffffu, c.best_idx, 0);
+  if (c.lane == 0) { hdr->red[c.cw] = bv; hdr->misc[c.cw] = bi; }
+  consumer_sync(c.nct);
+  if (c.ctid == 0) {
+    float best = hdr->red[0];
+    int idx = hdr->misc[0];
+    for (int w = 1; w < p.C; ++w) {
+      const float v = hdr->red[w];
+      const int i = hdr->misc[w];
+      if (v > best || (v == best && i < idx)) { best = v; idx = i; }
+    }
+    p.lm_val[blockIdx.x] = best;
+    p.lm_idx[blockIdx.x] = idx;
+    __threadfence();
+    const unsigned old = atom_acqrel_add(p.counters + CTR_F, 1u);
+    hdr->misc[31] = (old == (unsigned)(p.n_lm_tasks - 1)) ? 1 : 0;
+  }
+  consumer_sync(c.nct);
+  if (hdr->misc[31] && c.cw == 0) {
+    __threadfence();
+    float best = -INFINITY;
+    int idx = 0x7fffffff;
+    for (int s = c.lane; s < (int)gridDim.x; s += 32) {
+      const int i = __ldcg(p.lm_idx + s);
+      const float v = __ldcg(p.lm_val + s);
+      if (i >= 0 && (v > best || (v == best && i < idx))) { best = v; idx = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ov > best || (ov == best && oi < idx)) { best = ov; idx = oi; }
+    }
+    if (c.lane == 0) {
+      p.next_tokens[0] = idx;
+      if (p.auto_advance) { p.tokens[0] = idx; p.positions[0] = p.positions[0] + 1; }
+    }
+    // every CTA has passed its last wait: reset the dependency counters for the next launch
+    for (int i = c.lane; i < p.n_counters; i += 32) p.counters[i] = 0u;
+  }
+}
+
+__device__ __forceinline__ void run_gemv(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* xs,
+                                         SmemHdr* hdr, uint8_t* ring, int tok) {
+  wait_counter(p, c, t.wait_ctr, t.wait_val, task_idx);
+  if (!p.probe) gemv_prologue(p, c, t, xs, hdr, tok);
+  const int rw = t.rt / p.C;
+  if (rw == 2) gemv_tiles<2>(p, c, t, task_idx, xs, hdr, ring, tok);
+  else gemv_tiles<4>(p, c, t, task_idx, xs, hdr, ring, tok);
+  if (p.probe) return;
+  if (t.type == T_LMHEAD) lm_finish(p, c, hdr);
+  else signal_counter(p, c, t.sig_ctr);
+}
+
+// ----------------------------------------------------------------------------------
+// attention task: one (kv head, context chunk) unit of split-KV decode attention
+// ----------------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ void rope_norm_head(const KParams& p, const float* raw, const float* gain, int pos,
+                                               float scale, int lane, float* out) {
+  // one warp, one head: optional RMSNorm over D, rotate-half RoPE, scale
+  constexpr int PER = D / 32;  // 4 (D=128) or 2 (D=64): elements lane, lane+32, ...
+  constexpr int HALF = D / 2;
+  float v[PER];
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) { v[j] = __ldcg(raw + lane + 32 * j); ss += v[j] * v[j]; }
+  if (gain) {
+    ss = warp_sum(ss);
+    const float rs = rsqrtf(ss / (float)D + p.eps);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) v[j] = v[j] * rs * __ldg(gain + lane + 32 * j);
+  }
+  const float* cs = p.rope_cos + (size_t)pos * HALF;
+  const float* sn = p.rope_sin + (size_t)pos * HALF;
+#pragma unroll
+  for (int j = 0; j < PER / 2; ++j) {
+    const int d1 = lane + 32 * j;  // < HALF
+    const float c1 = __ldg(cs + d1), s1 = __ldg(sn + d1);
+    const float x1 = v[j], x2 = v[j + PER / 2];
+    out[d1] = (x1 * c1 - x2 * s1) * scale;
+    out[d1 + HALF] = (x2 * c1 + x1 * s1) * scale;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* scratch,
+                                         SmemHdr* hdr, int pos) {
+  const int G = p.G;
+  const int kvh = t.a, slot = t.b, bidx = t.aux;
+  const int ctx = pos + 1;
+  int CL = max(p.attn_min_chunk, (ctx + p.attn_chunks - 1) / p.attn_chunks);
+  CL = (CL + 7) & ~7;
+  const int n_active = (ctx + CL - 1) / CL;
+  if (slot >= n_active || p.probe) return;  // uniform across the CTA's consumers
+  wait_counter(p, c, t.wait_ctr, t.wait_val, task_idx);
+
+  const int t0 = slot * CL;
+  const int n = min(ctx, t0 + CL) - t0;
+  // scratch carve-up (floats)
+  float* qs = scratch;                  // [G][D]
+  float* sc = qs + G * D;               // [G][kAttnCLMax]
+  float* red = sc + G * kAttnCLMax;     // [C][G][D]
+  float* ml = red + p.C * G * D;        // m[G], l[G]
+  float* knew = ml + 2 * kGMax;         // [D] staging for the new K row (bf16-rounded fp32)
+
+  const float* qkv = p.qkv + (size_t)bidx * p.qkv_rows;
+  const float* lay_fp = p.fparams + (size_t)t.layer * p.fp_layer_stride;
+  const float scale = rsqrtf((float)D);
+  const size_t head_base = ((size_t)(t.layer * p.batch + bidx) * p.nkv + kvh) * (size_t)p.max_ctx * D;
+  __nv_bfloat16* Kc = p.kcache + head_base;
+  __nv_bfloat16* Vc = p.vcache + head_base;
+
+  // 1. q heads of this group: (norm) + RoPE + 1/sqrt(D)
+  for (int g = c.cw; g < G; g += p.C)
+    rope_norm_head<D>(p, qkv + (size_t)(kvh * G + g) * D, p.qk_norm ? lay_fp + p.fp_qn : nullptr, pos, scale, c.lane,
+                      qs + g * D);
+  // 2. the unit that owns position `pos` appends the new K/V rows (bf16)
+  if (slot == n_active - 1) {
+    const int wk = (G % p.C);            // a warp that is not the busiest in step 1
+    const int wv = ((G + 1) % p.C);
+    if (c.cw == wk) {
+      rope_norm_head<D>(p, qkv + p.q_dim + (size_t)kvh * D, p.qk_norm ? lay_fp + p.fp_kn : nullptr, pos, 1.0f, c.lane,
+                        knew);
+      __syncwarp();
+      for (int d = c.lane; d < D; d += 32) Kc[(size_t)pos * D + d] = __float2bfloat16_rn(knew[d]);
+    }
+    if (c.cw == wv) {
+      const float* vraw = qkv + p.q_dim + p.kv_dim + (size_t)kvh * D;
+      for (int d = c.lane; d < D; d += 32) Vc[(size_t)pos * D + d] = __float2bfloat16_rn(__ldcg(vraw + d));
+    }
+  }
+  consumer_sync(c.nct);
+
+  // 3. scores: 8 lanes per position, 4 positions per warp step
+  {
+    constexpr int EPL = D / 8;  // elements per lane: 16 or 8
+    const int sub = c.lane >> 3, sl = c.lane & 7;
+    for (int base = c.cw * 4; base < n; base += p.C * 4) {
+      const int tt = base + sub;
+      const bool valid = tt < n;
+      float kf[EPL];
+      if (valid) {
+        const uint4* kp = reinterpret_cast<const uint4*>(Kc + (size_t)(t0 + tt) * D + sl * EPL);
+#pragma unroll
+        for (int q = 0; q < EPL / 8; ++q) {
+          const uint4 raw = __ldcg(kp + q);
+          kf[q * 8 + 0] = bf_lo(raw.x); kf[q * 8 + 1] = bf_hi(raw.x);
+          kf[q * 8 + 2] = bf_lo(raw.y); kf[q * 8 + 3] = bf_hi(raw.y);
+          kf[q * 8 + 4] = bf_lo(raw.z); kf[q * 8 + 5] = bf_hi(raw.z);
+          kf[q * 8 + 6] = bf_lo(raw.w); kf[q * 8 + 7] = bf_hi(raw.w);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) kf[e] = 0.f;
+      }
+      for (int g = 0; g < G; ++g) {
+        const float4* qp = reinterpret_cast<const float4*>(qs + g * D + sl * EPL);
+        float s = 0.f;
+#pragma unroll
+        for (int q = 0; q < EPL / 4; ++q) {
+          const float4 qv = qp[q];
+          s = fmaf(qv.x, kf[q * 4 + 0], s); s = fmaf(qv.y, kf[q * 4 + 1], s);
+          s = fmaf(qv.z, kf[q * 4 + 2], s); s = fmaf(qv.w, kf[q * 4 + 3], s);
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        if (valid && sl == 0) sc[g * kAttnCLMax + tt] = s;
+      }
+    }
+  }
+  consumer_sync(c.nct);
+
+  // 4. chunk-local softmax statistics per head
+  for (int g = c.cw; g < G; g += p.C) {
+    float m = -INFINITY;
+    for (int i = c.lane; i < n; i += 32) m = fmaxf(m, sc[g * kAttnCLMax + i]);
+    m = warp_max(m);
+    float l = 0.f;
+    for (int i = c.lane; i < n; i += 32) {
+      const float e = expf(sc[g * kAttnCLMax + i] - m);
+      sc[g * kAttnCLMax + i] = e;
+      l += e;
+    }
+    l = warp_sum(l);
+    if (c.lane == 0) { ml[g] = m; ml[kGMax + g] = l; }
+  }
+  consumer_sync(c.nct);
+
+  // 5. P.V: warps split positions, lanes split dims
+  {
+    constexpr int DPL = D / 32;  // 4 or 2
+    float acc[kGMax][DPL];
+#pragma unroll
+    for (int g = 0; g < kGMax; ++g)
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) acc[g][e] = 0.f;
+#pragma unroll 4
+    for (int tt = c.cw; tt < n; tt += p.C) {
+      float vf[DPL];
+      if constexpr (DPL == 4) {
+        const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(Vc + (size_t)(t0 + tt) * D) + c.lane);
+        vf[0] = bf_lo(raw.x); vf[1] = bf_hi(raw.x); vf[2] = bf_lo(raw.y); vf[3] = bf_hi(raw.y);
+      } else {
+        const uint32_t raw = __ldcg(reinterpret_cast<const uint32_t*>(Vc + (size_t)(t0 + tt) * D) + c.lane);
+        vf[0] = bf_lo(raw); vf[1] = bf_hi(raw);
+      }
+#pragma unroll
+      for (int g = 0; g < kGMax; ++g) {
+        if (g < G) {
+          const float pg = sc[g * kAttnCLMax + tt];
+#pragma unroll
+          for (int e = 0; e < DPL; ++e) acc[g][e] = fmaf(pg, vf[e], acc[g][e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < kGMax; ++g) {
+      if (g < G) {
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) red[(c.cw * G + g) * D + c.lane * DPL + e] = acc[g][e];
+      }
+    }
+  }
+  consumer_sync(c.nct);
+
+  // 6. cross-warp reduction, then either the final output (single chunk) or a partial
+  const int PS = D + 2;  // partial record: o[D], m, l
+  float* part = p.part + ((size_t)(bidx * p.nkv + kvh) * p.attn_chunks) * (size_t)G * PS;
+  float* out = p.attn + (size_t)bidx * p.q_dim + (size_t)kvh * G * D;
+  for (int i = c.ctid; i < G * D; i += c.nct) {
+    const int g = i / D, d = i - g * D;
+    float o = 0.f;
+    for (int w = 0; w < p.C; ++w) o += red[(w * G + g) * D + d];
+    if (n_active == 1) out[i] = o / ml[kGMax + g];
+    else part[((size_t)slot * G + g) * PS + d] = o;
+  }
+  if (n_active == 1) {
+    signal_counter(p, c, CTR_C);
+    return;
+  }
+  if (c.ctid < G) {
+    part[((size_t)slot * G + c.ctid) * PS + D] = ml[c.ctid];
+    part[((size_t)slot * G + c.ctid) * PS + D + 1] = ml[kGMax + c.ctid];
+  }
+  consumer_sync(c.nct);
+  if (c.ctid == 0) {
+    __threadfence();
+    const unsigned old = atom_acqrel_add(p.counters + t.sig_ctr, 1u);
+    hdr->misc[30] = (old == (unsigned)(t.layer * n_active + n_active - 1)) ? 1 : 0;
+  }
+  consumer_sync(c.nct);
+  if (!hdr->misc[30]) return;
+  // last unit of this head: merge the partials (flash-decoding combine)
+  __threadfence();
+  for (int i = c.ctid; i < G * D; i += c.nct) {
+    const int g = i / D, d = i - g * D;
+    float M = -INFINITY;
+    for (int s = 0; s < n_active; ++s) M = fmaxf(M, __ldcg(part + ((size_t)s * G + g) * PS + D));
+    float Lsum = 0.f, O = 0.f;
+    for (int s = 0; s < n_active; ++s) {
+      const float* rec = part + ((size_t)s * G + g) * PS;
+      const float wgt = expf(__ldcg(rec + D) - M);
+      Lsum = fmaf(__ldcg(rec + D + 1), wgt, Lsum);
+      O = fmaf(__ldcg(rec + d), wgt, O);
+    }
+    out[i] = O / Lsum;
+  }
+  signal_counter(p, c, CTR_C);
+}
+
+// ----------------------------------------------------------------------------------
+// the persistent kernel
+// ----------------------------------------------------------------------------------
+__global__ void __launch_bounds__(544, 1) adamk_decode_kernel(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  SmemHdr* hdr = reinterpret_cast<SmemHdr*>(smem);
+  float* scratch = reinterpret_cast<float*>(smem + kSmemReserved);
+  uint8_t* ring = smem + kSmemReserved + p.scratch_bytes;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.n_stage; ++s) {
+      mbar_init(smem_u32(&hdr->full[s]), 1);
+      mbar_init(smem_u32(&hdr->empty[s]), (uint32_t)p.C);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int tb = p.sm_begin[blockIdx.x], te = p.sm_begin[blockIdx.x + 1];
+
+  if (warp == 0) {
+    // ------------------------------ Loader ------------------------------
+    if (lane == 0) {
+      uint32_t it = 0;
+      const uint32_t ring_addr = smem_u32(ring);
+      for (int ti = tb; ti < te; ++ti) {
+        const int4* tp = reinterpret_cast<const int4*>(p.tasks + ti);
+        const int4 q0 = __ldg(tp), q1 = __ldg(tp + 1), q2 = __ldg(tp + 2);
+        const int type = q0.x, nrows = q0.w, kchunks = q1.y, rt = q1.z, ktc = q1.w;
+        const int n_tiles = q2.x, n_ktiles = q2.y;
+        if (type == T_ATTN || type == T_END) continue;
+        const uint8_t* src = p.wpacked + (size_t)(uint32_t)q2.z * 16u;
+        for (int tile = 0; tile < n_tiles; ++tile) {
+          const int rows = min(rt, nrows - tile * rt);
+          for (int kt = 0; kt < n_ktiles; ++kt) {
+            const int chunks = min(ktc, kchunks - kt * ktc);
+            const uint32_t bytes = (uint32_t)rows * (uint32_t)chunks * 512u;
+            const uint32_t slot = it % (uint32_t)p.n_stage;
+            const uint32_t ph = (it / (uint32_t)p.n_stage) & 1u;
+            mbar_wait(p, smem_u32(&hdr->empty[slot]), ph ^ 1u, DE_WATCHDOG_EMPTY, ti);
+            const uint32_t fb = smem_u32(&hdr->full[slot]);
+            mbar_arrive_expect_tx(fb, bytes);
+            tma_bulk_g2s(ring_addr + slot * (uint32_t)p.stage_bytes, src, bytes, fb);
+            src += bytes;
+            ++it;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------ Consumers ------------------------------
+  ConsumerCtx c;
+  c.it = 0; c.cw = warp - 1; c.lane = lane; c.ctid = threadIdx.x - 32; c.nct = p.C * 32;
+  c.best_val = -INFINITY; c.best_idx = -1;
+  int tok = 0, pos = 0;
+  if (!p.probe) {
+    tok = __ldcg(p.tokens);
+    pos = __ldcg(p.positions);
+    if (pos < 0 || pos >= p.max_ctx || tok < 0 || tok >= p.V) {
+      if (c.ctid == 0) dev_fail(p, DE_BAD_POS, -1, pos, tok, p.max_ctx);
+      return;
+    }
+  }
+  for (int ti = tb; ti < te; ++ti) {
+    Task t;
+    {
+      const int4* tp = reinterpret_cast<const int4*>(p.tasks + ti);
+      int4* dst = reinterpret_cast<int4*>(&t);
+      dst[0] = __ldg(tp); dst[1] = __ldg(tp + 1); dst[2] = __ldg(tp + 2); dst[3] = __ldg(tp + 3);
+    }
+    if (t.type == T_ATTN) {
+      if (p.D == 128) run_attn<128>(p, c, t, ti, scratch, hdr, pos);
+      else run_attn<64>(p, c, t, ti, scratch, hdr, pos);
+    } else if (t.type != T_END) {
+      run_gemv(p, c, t, ti, scratch, hdr, ring, tok);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------
+// weight packer: HF row-major bf16 -> per-SM tile-major streams (+ fp32 parameter tail)
+// ----------------------------------------------------------------------------------
+struct PackParams {
+  const Task* tasks;
+  int n_tasks;
+  const AdamkLayerWeights* layers;  // device copy
+  const void* lm_head;
+  uint8_t* wpacked;
+  int H, I, q_dim, kv_dim;
+};
+
+__device__ __forceinline__ const __nv_bfloat16* resolve_row(const PackParams& pp, const Task& t, int vrow, int* K) {
+  const AdamkLayerWeights* lw = (t.type == T_LMHEAD) ? nullptr : pp.layers + t.layer;
+  switch (t.type) {
+    case T_QKV:
+      *K = pp.H;
+      if (vrow < pp.q_dim) return (const __nv_bfloat16*)lw->wq + (size_t)vrow * pp.H;
+      if (vrow < pp.q_dim + pp.kv_dim) return (const __nv_bfloat16*)lw->wk + (size_t)(vrow - pp.q_dim) * pp.H;
+      return (const __nv_bfloat16*)lw->wv + (size_t)(vrow - pp.q_dim - pp.kv_dim) * pp.H;
+    case T_OPROJ: *K = pp.q_dim; return (const __nv_bfloat16*)lw->wo + (size_t)vrow * pp.q_dim;
+    case T_GATEUP:
+      *K = pp.H;
+      return ((vrow & 1) ? (const __nv_bfloat16*)lw->wup : (const __nv_bfloat16*)lw->wgate) + (size_t)(vrow >> 1) * pp.H;
+    case T_DOWN: *K = pp.I; return (const __nv_bfloat16*)lw->wdown + (size_t)vrow * pp.I;
+    default: *K = pp.H; return (const __nv_bfloat16*)pp.lm_head + (size_t)vrow * pp.H;
+  }
+}
+
+__global__ void adamk_pack_kernel(const PackParams pp) {
+  const int ti = blockIdx.x;
+  if (ti >= pp.n_tasks) return;
+  const Task t = pp.tasks[ti];
+  if (t.type == T_ATTN || t.type == T_END) return;
+  uint4* dst = reinterpret_cast<uint4*>(pp.wpacked + (size_t)(uint32_t)t.w_off * 16u);
+  size_t done = 0;  // 16-byte elements written so far
+  for (int tile = 0; tile < t.n_tiles; ++tile) {
+    const int rows = min(t.rt, t.b - tile * t.rt);
+    for (int kt = 0; kt < t.n_ktiles; ++kt) {
+      const int chunks = min(t.ktc, t.kchunks - kt * t.ktc);
+      const int n = rows * chunks * 32;
+      for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const int ln = e & 31;
+        const int ch = (e >> 5) % chunks;
+        const int r = (e >> 5) / chunks;
+        int K;
+        const __nv_bfloat16* row = resolve_row(pp, t, t.a + tile * t.rt + r, &K);
+        const int k0 = (kt * t.ktc + ch) * kChunk + ln * 4;
+        uint2 lo = make_uint2(0u, 0u), hi = make_uint2(0u, 0u);
+        if (k0 + 3 < K) lo = *reinterpret_cast<const uint2*>(row + k0);
+        else {
+          unsigned short v[4] = {0, 0, 0, 0};
+          for (int j = 0; j < 4; ++j) if (k0 + j < K) v[j] = reinterpret_cast<const unsigned short*>(row)[k0 + j];
+          lo = make_uint2(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16));
+        }
+        const int k1 = k0 + 128;
+        if (k1 + 3 < K) hi = *reinterpret_cast<const uint2*>(row + k1);
+        else {
+          unsigned short v[4] = {0, 0, 0, 0};
+          for (int j = 0; j < 4; ++j) if (k1 + j < K) v[j] = reinterpret_cast<const unsigned short*>(row)[k1 + j];
+          hi = make_uint2(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16));
+        }
+        dst[done + e] = make_uint4(lo.x, lo.y, hi.x, hi.y);
+      }
+      done += (size_t)n;
+    }
+  }
+}
+
+__global__ void adamk_cvt_kernel(const __nv_bfloat16* src, float* dst, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = __bfloat162float(src[i]);
+}
+
+// ----------------------------------------------------------------------------------
+// host side
+// ----------------------------------------------------------------------------------
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define CUDA_TRY(expr)                                                                                   \
+  do {                                                                                                   \
+    cudaError_t _e = (expr);                                                                             \
+    if (_e != cudaSuccess)                                                                               \
+      return fail(ADAMK_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));                     \
+  } while (0)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+struct AdamkHandle_ {
+  AdamkModelDesc desc{};
+  int n_sms = 0, C = 0, n_stage = 0, stage_bytes = 0, n_tasks = 0, batch = 0, n_counters = 0;
+  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0;
+  size_t packed_weight_bytes = 0;  // matrix streams only
+  size_t fparam_floats = 0;
+  int fp_layer_stride = 0, fp_ln1 = 0, fp_ln2 = 0, fp_bias = 0, fp_qn = 0, fp_kn = 0, fp_final = 0;
+  std::vector<int> host_table;
+  int* d_table = nullptr;  // sm_begin + tasks
+  const int* d_sm_begin = nullptr;
+  const Task* d_tasks = nullptr;
+  bool bound = false;
+  const uint8_t* wpacked = nullptr;
+  const float* fparams = nullptr;
+  AdamkWeightPtrs w{};
+  int* status_host = nullptr;
+  int* status_dev = nullptr;
+  int smem_bytes = 0;
+  // workspace layout (byte offsets)
+  size_t ws_h_a = 0, ws_h_b = 0, ws_qkv = 0, ws_attn = 0, ws_act = 0, ws_part = 0, ws_lm_val = 0, ws_lm_idx = 0,
+         ws_counters = 0, ws_total = 0;
+};
+
+extern "C" {
+
+int adamk_abi_version(void) { return ADAMK_ABI_VERSION; }
+
+const char* adamk_last_error(void) { return g_err.c_str(); }
+
+int adamk_device_sm_count(int device, int* out_sms) {
+  if (!out_sms) return fail(ADAMK_E_INVALID, "out_sms is NULL");
+  int n = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+  *out_sms = n;
+  return ADAMK_OK;
+}
+
+int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task_table_bytes, int tp_rank, int tp_size,
+                 adamk_handle* out) {
+  if (!desc || !task_table || !out) return fail(ADAMK_E_INVALID, "NULL argument");
+  if (tp_size != 1 || tp_rank != 0) return fail(ADAMK_E_UNSUPPORTED, "tensor parallel shards are not built yet (tp_size must be 1)");
+  if (task_table_bytes < (size_t)kHeaderInts * 4 || task_table_bytes % 4) return fail(ADAMK_E_INVALID, "task table too small");
+  const int* tt = static_cast<const int*>(task_table);
+  if (tt[0] != kMagic || tt[1] != kVersion) return fail(ADAMK_E_INVALID, "task table magic/version mismatch");
+  auto h = new AdamkHandle_();
+  h->desc = *desc;
+  h->n_sms = tt[2]; h->C = tt[3]; h->n_stage = tt[4]; h->stage_bytes = tt[5]; h->n_tasks = tt[6]; h->batch = tt[7];
+  h->n_counters = tt[8]; h->attn_chunks = tt[9]; h->attn_min_chunk = tt[10]; h->scratch_bytes = tt[11];
+  h->n_lm_tasks = tt[12];
+  auto bad = [&](const std::string& m) { delete h; return fail(ADAMK_E_INVALID, m); };
+  const AdamkModelDesc& d = *desc;
+  if (d.head_dim != 64 && d.head_dim != 128) return bad("head_dim must be 64 or 128");
+  if (d.n_kv_heads < 1 || d.n_q_heads % d.n_kv_heads) return bad("n_q_heads must be a multiple of n_kv_heads");
+  if (d.n_q_heads / d.n_kv_heads > kGMax) return bad("more than 8 q heads per kv head");
+  if (d.hidden % 8 || d.intermediate % 8) return bad("hidden/intermediate must be multiples of 8");
+  if (h->batch != 1 || d.max_batch != 1) { delete h; return fail(ADAMK_E_UNSUPPORTED, "batch > 1 is not built yet"); }
+  if (h->C != 4 && h->C != 8 && h->C != 16) return bad("consumer_warps must be 4, 8 or 16");
+  if (h->n_stage < 1 || h->n_stage > kMaxStages) return bad("n_stage out of range");
+  if (h->stage_bytes <= 0 || h->stage_bytes % 1024) return bad("stage_bytes must be a positive multiple of 1024");
+  if (h->n_sms < 1 || h->n_tasks < 1) return bad("empty task table");
+  const size_t need = ((size_t)kHeaderInts + (size_t)h->n_sms + 1 + (size_t)h->n_tasks * kTaskInts) * 4;
+  if (task_table_bytes != need) return bad("task table size does not match its header");
+  if (h->n_counters != CTR_HEAD0 + h->batch * d.n_kv_heads) return bad("counter count mismatch");
+  h->smem_bytes = kSmemReserved + h->scratch_bytes + h->n_stage * h->stage_bytes;
+  if (h->smem_bytes > kSmemMax) return bad("ring + scratch exceed 227 KB shared memory");
+  {  // the scratch region must hold the widest activation vector and the attention buffers
+    const int G = d.n_q_heads / d.n_kv_heads;
+    const int kmax = std::max(std::max(d.hidden, d.n_q_heads * d.head_dim), d.intermediate);
+    const size_t xb = align_up((size_t)kmax, kChunk) * 4;
+    const size_t ab = ((size_t)G * d.head_dim + (size_t)G * kAttnCLMax + (size_t)h->C * G * d.head_dim + 2 * kGMax + d.head_dim) * 4;
+    if ((size_t)h->scratch_bytes < std::max(xb, ab)) return bad("scratch_bytes too small for this model");
+  }
+  const int* sm_begin = tt + kHeaderInts;
+  const Task* tasks = reinterpret_cast<const Task*>(tt + kHeaderInts + h->n_sms + 1);
+  if (sm_begin[0] != 0 || sm_begin[h->n_sms] != h->n_tasks) return bad("sm_begin does not cover the task list");
+  size_t wbytes = 0;
+  for (int s = 0; s < h->n_sms; ++s)
+    if (sm_begin[s] > sm_begin[s + 1]) return bad("sm_begin not monotone");
+  const int qkv_rows = (d.n_q_heads + 2 * d.n_kv_heads) * d.head_dim;
+  for (int i = 0; i < h->n_tasks; ++i) {
+    const Task& t = tasks[i];
+    if (t.type == T_ATTN) {
+      if (t.a < 0 || t.a >= d.n_kv_heads || t.b < 0 || t.b >= h->attn_chunks || t.layer < 0 || t.layer >= d.n_layers)
+        return bad("attention task out of range");
+      continue;
+    }
+    if (t.type < T_QKV || t.type > T_LMHEAD) return bad("unknown task type");
+    int n_rows = 0, K = 0;
+    switch (t.type) {
+      case T_QKV: n_rows = qkv_rows; K = d.hidden; break;
+      case T_OPROJ: n_rows = d.hidden; K = d.n_q_heads * d.head_dim; break;
+      case T_GATEUP: n_rows = 2 * d.intermediate; K = d.hidden; break;
+      case T_DOWN: n_rows = d.hidden; K = d.intermediate; break;
+      default: n_rows = d.vocab; K = d.hidden; break;
+    }
+    if (t.k != K || t.kchunks != (K + kChunk - 1) / kChunk) return bad("task K mismatch");
+    if (t.a < 0 || t.b < 1 || t.a + t.b > n_rows) return bad("task rows out of range");
+    if (t.rt % h->C || (t.rt / h->C != 2 && t.rt / h->C != 4)) return bad("rows_per_tile / consumer_warps must be 2 or 4");
+    if (t.type == T_GATEUP && ((t.a | t.b) & 1)) return bad("gate/up rows must come in pairs");
+    if (t.ktc < 1 || t.n_ktiles != (t.kchunks + t.ktc - 1) / t.ktc || t.n_tiles != (t.b + t.rt - 1) / t.rt)
+      return bad("task tiling inconsistent");
+    if ((size_t)t.rt * t.ktc * 512 > (size_t)h->stage_bytes) return bad("stage larger than stage_bytes");
+    if (t.type != T_LMHEAD && (t.layer < 0 || t.layer >= d.n_layers)) return bad("task layer out of range");
+    if (t.wait_ctr >= h->n_counters || t.sig_ctr >= h->n_counters) return bad("counter index out of range");
+    const size_t bytes = (size_t)t.b * t.kchunks * 512;
+    const size_t off = (size_t)(uint32_t)t.w_off * 16;
+    wbytes = std::max(wbytes, off + bytes);
+  }
+  h->packed_weight_bytes = align_up(wbytes, 256);
+  // fp32 parameter tail
+  h->fp_ln1 = 0; h->fp_ln2 = d.hidden; h->fp_bias = 2 * d.hidden; h->fp_qn = h->fp_bias + qkv_rows;
+  h->fp_kn = h->fp_qn + d.head_dim; h->fp_layer_stride = (int)align_up((size_t)h->fp_kn + d.head_dim, 4);
+  h->fp_final = h->fp_layer_stride * d.n_layers;
+  h->fparam_floats = (size_t)h->fp_final + d.hidden;
+  // workspace layout
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+  const int G = d.n_q_heads / d.n_kv_heads;
+  h->ws_counters = take((size_t)h->n_counters * 4);
+  h->ws_h_a = take((size_t)d.hidden * 4);
+  h->ws_h_b = take((size_t)d.hidden * 4);
+  h->ws_qkv = take((size_t)qkv_rows * 4);
+  h->ws_attn = take((size_t)d.n_q_heads * d.head_dim * 4);
+  h->ws_act = take(align_up((size_t)d.intermediate, kChunk) * 4);
+  h->ws_part = take((size_t)d.n_kv_heads * h->attn_chunks * G * (d.head_dim + 2) * 4);
+  h->ws_lm_val = take((size_t)h->n_sms * 4);
+  h->ws_lm_idx = take((size_t)h->n_sms * 4);
+  h->ws_total = o;
+
+  // device copy: task records first (64-byte aligned for the int4 loads), then sm_begin
+  h->host_table.assign(reinterpret_cast<const int*>(tasks), reinterpret_cast<const int*>(tasks) + (size_t)h->n_tasks * kTaskInts);
+  h->host_table.insert(h->host_table.end(), sm_begin, sm_begin + h->n_sms + 1);
+  cudaError_t e = cudaMalloc(&h->d_table, h->host_table.size() * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(h->d_table, h->host_table.data(), h->host_table.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaHostAlloc(&h->status_host, 64, cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    memset(h->status_host, 0, 64);
+    e = cudaHostGetDevicePointer(&h->status_dev, h->status_host, 0);
+  }
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  if (e != cudaSuccess) {
+    std::string m = std::string("adamk_create: ") + cudaGetErrorString(e);
+    adamk_destroy(h);
+    return fail(ADAMK_E_CUDA, m);
+  }
+  h->d_tasks = reinterpret_cast<const Task*>(h->d_table);
+  h->d_sm_begin = h->d_table + (size_t)h->n_tasks * kTaskInts;
+  *out = h;
+  return ADAMK_OK;
+}
+
+void adamk_destroy(adamk_handle h) {
+  if (!h) return;
+  if (h->d_table) cudaFree(h->d_table);
+  if (h->status_host) cudaFreeHost(h->status_host);
+  delete h;
+}
+
+size_t adamk_packed_bytes(adamk_handle h) { return h ? h->packed_weight_bytes + align_up(h->fparam_floats * 4, 256) : 0; }
+
+size_t adamk_workspace_bytes(adamk_handle h) { return h ? h->ws_total : 0; }
+
+size_t adamk_kv_cache_bytes(adamk_handle h) {
+  if (!h) return 0;
+  const AdamkModelDesc& d = h->desc;
+  return (size_t)d.n_layers * d.max_batch * d.n_kv_heads * d.max_ctx * d.head_dim * 2;
+}
+
+int adamk_workspace_init(adamk_handle h, void* workspace, adamk_stream stream) {
+  if (!h || !workspace) return fail(ADAMK_E_INVALID, "NULL argument");
+  CUDA_TRY(cudaMemsetAsync(workspace, 0, h->ws_total, (cudaStream_t)stream));
+  return ADAMK_OK;
+}
+
+int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, adamk_stream stream_) {
+  if (!h || !w || !packed) return fail(ADAMK_E_INVALID, "NULL argument");
+  if (!w->embed || !w->final_norm || !w->layers || !w->rope_cos || !w->rope_sin) return fail(ADAMK_E_INVALID, "missing weight pointer");
+  if ((uintptr_t)packed % 256) return fail(ADAMK_E_INVALID, "packed buffer must be 256-byte aligned");
+  const AdamkModelDesc& d = h->desc;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  for (int l = 0; l < d.n_layers; ++l) {
+    const AdamkLayerWeights& lw = w->layers[l];
+    if (!lw.ln1 || !lw.wq || !lw.wk || !lw.wv || !lw.wo || !lw.ln2 || !lw.wgate || !lw.wup || !lw.wdown)
+      return fail(ADAMK_E_INVALID, "layer " + std::to_string(l) + ": missing matrix pointer");
+    if (d.qkv_bias && (!lw.bq || !lw.bk || !lw.bv)) return fail(ADAMK_E_INVALID, "qkv_bias set but bias pointer missing");
+    if (d.qk_norm && (!lw.q_norm || !lw.k_norm)) return fail(ADAMK_E_INVALID, "qk_norm set but norm pointer missing");
+  }
+  AdamkLayerWeights* d_layers = nullptr;
+  CUDA_TRY(cudaMalloc(&d_layers, sizeof(AdamkLayerWeights) * d.n_layers));
+  cudaError_t e = cudaMemcpyAsync(d_layers, w->layers, sizeof(AdamkLayerWeights) * d.n_layers, cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) { cudaFree(d_layers); return fail(ADAMK_E_CUDA, cudaGetErrorString(e)); }
+  PackParams pp{};
+  pp.tasks = h->d_tasks; pp.n_tasks = h->n_tasks; pp.layers = d_layers;
+  pp.lm_head = w->lm_head ? w->lm_head : w->embed;
+  pp.wpacked = static_cast<uint8_t*>(packed);
+  pp.H = d.hidden; pp.I = d.intermediate; pp.q_dim = d.n_q_heads * d.head_dim; pp.kv_dim = d.n_kv_heads * d.head_dim;
+  adamk_pack_kernel<<<h->n_tasks, 256, 0, stream>>>(pp);
+  // fp32 parameter tail
+  float* fp = reinterpret_cast<float*>(static_cast<uint8_t*>(packed) + h->packed_weight_bytes);
+  auto cvt = [&](const void* src, size_t off, int n) {
+    if (src && n > 0) adamk_cvt_kernel<<<(n + 255) / 256, 256, 0, stream>>>((const __nv_bfloat16*)src, fp + off, n);
+  };
+  e = cudaMemsetAsync(fp, 0, h->fparam_floats * 4, stream);
+  for (int l = 0; l < d.n_layers && e == cudaSuccess; ++l) {
+    const AdamkLayerWeights& lw = w->layers[l];
+    const size_t base = (size_t)l * h->fp_layer_stride;
+    cvt(lw.ln1, base + h->fp_ln1, d.hidden);
+    cvt(lw.ln2, base + h->fp_ln2, d.hidden);
+    if (d.qkv_bias) {
+      cvt(lw.bq, base + h->fp_bias, pp.q_dim);
+      cvt(lw.bk, base + h->fp_bias + pp.q_dim, pp.kv_dim);
+      cvt(lw.bv, base + h->fp_bias + pp.q_dim + pp.kv_dim, pp.kv_dim);
+    }
+    if (d.qk_norm) {
+      cvt(lw.q_norm, base + h->fp_qn, d.head_dim);
+      cvt(lw.k_norm, base + h->fp_kn, d.head_dim);
+    }
+  }
+  cvt(w->final_norm, h->fp_final, d.hidden);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  cudaFree(d_layers);
+  if (e != cudaSuccess) return fail(ADAMK_E_CUDA, std::string("adamk_bind_weights: ") + cudaGetErrorString(e));
+  h->w = *w;
+  h->w.layers = nullptr;
+  h->wpacked = static_cast<const uint8_t*>(packed);
+  h->fparams = fp;
+  h->bound = true;
+  return ADAMK_OK;
+}
+
+int adamk_bind_peers(adamk_handle h, void* const* peer_workspaces, int n_peers) {
+  (void)peer_workspaces;
+  if (!h) return fail(ADAMK_E_INVALID, "NULL handle");
+  if (n_peers == 1) return ADAMK_OK;
+  return fail(ADAMK_E_UNSUPPORTED, "tensor parallel shards are not built yet");
+}
+
+static int fill_params(adamk_handle h, KParams& p, void* workspace) {
+  const AdamkModelDesc& d = h->desc;
+  memset(&p, 0, sizeof(p));
+  p.H = d.hidden; p.L = d.n_layers; p.nq = d.n_q_heads; p.nkv = d.n_kv_heads; p.D = d.head_dim; p.I = d.intermediate;
+  p.V = d.vocab; p.G = d.n_q_heads / d.n_kv_heads; p.q_dim = d.n_q_heads * d.head_dim; p.kv_dim = d.n_kv_heads * d.head_dim;
+  p.qkv_rows = p.q_dim + 2 * p.kv_dim; p.max_ctx = d.max_ctx; p.batch = h->batch;
+  p.has_bias = d.qkv_bias; p.qk_norm = d.qk_norm; p.eps = d.rms_eps;
+  p.C = h->C; p.n_stage = h->n_stage; p.stage_bytes = h->stage_bytes; p.attn_chunks = h->attn_chunks;
+  p.attn_min_chunk = h->attn_min_chunk; p.scratch_bytes = h->scratch_bytes; p.n_lm_tasks = h->n_lm_tasks;
+  p.n_counters = h->n_counters;
+  p.tasks = h->d_tasks; p.sm_begin = h->d_sm_begin;
+  p.wpacked = h->wpacked; p.fparams = h->fparams;
+  p.fp_layer_stride = h->fp_layer_stride; p.fp_ln1 = h->fp_ln1; p.fp_ln2 = h->fp_ln2; p.fp_bias = h->fp_bias;
+  p.fp_qn = h->fp_qn; p.fp_kn = h->fp_kn; p.fp_final = h->fp_final;
+  p.embed = (const __nv_bfloat16*)h->w.embed; p.rope_cos = h->w.rope_cos; p.rope_sin = h->w.rope_sin;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  if (ws) {
+    p.counters = (unsigned*)(ws + h->ws_counters);
+    p.h_a = (float*)(ws + h->ws_h_a); p.h_b = (float*)(ws + h->ws_h_b); p.qkv = (float*)(ws + h->ws_qkv);
+    p.attn = (float*)(ws + h->ws_attn); p.act = (float*)(ws + h->ws_act); p.part = (float*)(ws + h->ws_part);
+    p.lm_val = (float*)(ws + h->ws_lm_val); p.lm_idx = (int*)(ws + h->ws_lm_idx);
+  }
+  p.status = h->status_dev;
+  return ADAMK_OK;
+}
+
+static int launch(adamk_handle h, const KParams& p, cudaStream_t stream) {
+  int dev = 0, sms = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (sms < h->n_sms) return fail(ADAMK_E_INVALID, "task table was built for more SMs than this device has");
+  void* args[] = {(void*)&p};
+  // cooperative launch: all CTAs must be co-resident (they wait on each other's counters)
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)adamk_decode_kernel, dim3(h->n_sms), dim3((h->C + 1) * 32), args,
+                                       (size_t)h->smem_bytes, stream));
+  return ADAMK_OK;
+}
+
+int adamk_decode_step(adamk_handle h, int32_t* token_ids, int32_t* positions, int batch, void* k_cache, void* v_cache,
+                      void* workspace, float* logits_out, int32_t* next_token_out, int auto_advance,
+                      adamk_stream stream) {
+  if (!h || !token_ids || !positions || !k_cache || !v_cache || !workspace || !next_token_out)
+    return fail(ADAMK_E_INVALID, "NULL argument");
+  if (!h->bound) return fail(ADAMK_E_STATE, "adamk_bind_weights has not been called");
+  if (batch != h->batch) return fail(ADAMK_E_INVALID, "batch does not match the task table");
+  if (h->status_host[0] != 0) return fail(ADAMK_E_DEVICE, "a previous step reported a device error; see adamk_device_status");
+  KParams p;
+  fill_params(h, p, workspace);
+  p.kcache = (__nv_bfloat16*)k_cache; p.vcache = (__nv_bfloat16*)v_cache;
+  p.logits = logits_out; p.tokens = token_ids; p.positions = positions; p.next_tokens = next_token_out;
+  p.auto_advance = auto_advance;
+  return launch(h, p, (cudaStream_t)stream);
+}
+
+int adamk_stream_probe(adamk_handle h, float* sink, adamk_stream stream) {
+  if (!h || !sink) return fail(ADAMK_E_INVALID, "NULL argument");
+  if (!h->bound) return fail(ADAMK_E_STATE, "adamk_bind_weights has not been called");
+  KParams p;
+  fill_params(h, p, nullptr);
+  p.probe = 1; p.probe_sink = sink;
+  return launch(h, p, (cudaStream_t)stream);
+}
+
+int adamk_device_status(adamk_handle h, int32_t* info) {
+  if (!h) return fail(ADAMK_E_INVALID, "NULL handle");
+  if (info) memcpy(info, h->status_host, 32);
+  return h->status_host[0];
+}
+
+}  // extern "C"

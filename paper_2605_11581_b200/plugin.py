@@ -1,0 +1,227 @@
+"""ctypes binding of libadamk.so: the MegaKernel plugin entry point.
+
+The reference describes this layer only in prose (``PAPER.md:244-249``: the
+MegaKernel is embedded "via a Plugin mechanism", Decode switches to it); see
+include/adamk.h for the C ABI and INTEGRATION.md for the binding a reference
+maintainer would add.  PyTorch is used for device-buffer ownership only.
+
+There is no CPU fallback: importing works without a GPU (so host logic can be
+tested), but constructing a plugin without the built library or without a CUDA
+device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from .build import LIB
+from .model_config import ModelConfig
+from .task_table import KernelSchedule, TaskTable, build_task_table
+from .weights import DecoderWeights, rope_table
+
+ABI_VERSION = 1
+
+
+class AdamkError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"adamk error {code}: {msg}")
+        self.code = code
+
+
+class _ModelDesc(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "hidden", "n_layers", "n_q_heads", "n_kv_heads", "head_dim", "intermediate", "vocab",
+        "max_ctx", "max_batch", "qkv_bias", "qk_norm", "tied_embed")] + [
+        ("rms_eps", C.c_float), ("rope_theta", C.c_float)]
+
+
+_LAYER_FIELDS = ("ln1", "wq", "wk", "wv", "bq", "bk", "bv", "q_norm", "k_norm", "wo", "ln2",
+                 "wgate", "wup", "wdown")
+
+
+class _LayerWeights(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in _LAYER_FIELDS]
+
+
+class _WeightPtrs(C.Structure):
+    _fields_ = [("embed", C.c_void_p), ("final_norm", C.c_void_p), ("lm_head", C.c_void_p),
+                ("layers", C.POINTER(_LayerWeights)), ("rope_cos", C.c_void_p), ("rope_sin", C.c_void_p)]
+
+
+EXPORTS = (
+    "adamk_abi_version", "adamk_device_sm_count", "adamk_last_error", "adamk_create", "adamk_destroy",
+    "adamk_packed_bytes", "adamk_bind_weights", "adamk_bind_peers", "adamk_workspace_bytes",
+    "adamk_workspace_init", "adamk_kv_cache_bytes", "adamk_decode_step", "adamk_device_status",
+    "adamk_stream_probe",
+)
+
+_lib = None
+
+
+def load_library() -> C.CDLL:
+    """dlopen libadamk.so (built in-tree by ``build.py``) and declare prototypes."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB.exists():
+        raise AdamkError(-100, f"{LIB} is not built; run `python -m paper_2605_11581_b200.build` "
+                               "(there is no CPU fallback for the decode path)")
+    lib = C.CDLL(str(LIB))
+    lib.adamk_abi_version.restype = C.c_int
+    lib.adamk_last_error.restype = C.c_char_p
+    lib.adamk_device_sm_count.argtypes = [C.c_int, C.POINTER(C.c_int)]
+    lib.adamk_create.argtypes = [C.POINTER(_ModelDesc), C.c_void_p, C.c_size_t, C.c_int, C.c_int,
+                                 C.POINTER(C.c_void_p)]
+    lib.adamk_destroy.argtypes = [C.c_void_p]
+    lib.adamk_destroy.restype = None
+    for name in ("adamk_packed_bytes", "adamk_workspace_bytes", "adamk_kv_cache_bytes"):
+        getattr(lib, name).argtypes = [C.c_void_p]
+        getattr(lib, name).restype = C.c_size_t
+    lib.adamk_bind_weights.argtypes = [C.c_void_p, C.POINTER(_WeightPtrs), C.c_void_p, C.c_void_p]
+    lib.adamk_bind_peers.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_int]
+    lib.adamk_workspace_init.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.adamk_decode_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+    lib.adamk_device_status.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
+    lib.adamk_stream_probe.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    if lib.adamk_abi_version() != ABI_VERSION:
+        raise AdamkError(-101, "libadamk.so ABI version mismatch; rebuild")
+    _lib = lib
+    return lib
+
+
+def _check(lib, code: int) -> None:
+    if code != 0:
+        raise AdamkError(code, (lib.adamk_last_error() or b"").decode())
+
+
+def device_sm_count(device: int = 0) -> int:
+    lib = load_library()
+    n = C.c_int(0)
+    _check(lib, lib.adamk_device_sm_count(device, C.byref(n)))
+    return n.value
+
+
+@dataclass
+class StepOutput:
+    next_token: torch.Tensor            # int32 [batch] (device)
+    logits: torch.Tensor | None         # fp32 [batch, vocab] (device) or None
+
+
+class MegaKernelPlugin:
+    """One decode MegaKernel instance bound to one GPU.
+
+    ``schedule`` carries the solidified pipeline parameters (from
+    ``KernelSchedule.from_plan(solidified_trace.plan)``); the whole-model task
+    table is derived from it and the model config at construction."""
+
+    def __init__(self, cfg: ModelConfig, schedule: KernelSchedule, max_ctx: int, device: int | str = 0,
+                 n_sms: int | None = None):
+        if not torch.cuda.is_available():
+            raise AdamkError(-102, "no CUDA device: the decode MegaKernel has no CPU fallback")
+        self.lib = load_library()
+        self.cfg, self.schedule, self.max_ctx = cfg, schedule, int(max_ctx)
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        torch.cuda.set_device(self.device)
+        self.n_sms = n_sms or device_sm_count(self.device.index or 0)
+        self.table: TaskTable = build_task_table(cfg, schedule, n_sms=self.n_sms, batch=1)
+        desc = _ModelDesc(cfg.hidden, cfg.n_layers, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim,
+                          cfg.intermediate, cfg.vocab, self.max_ctx, 1, int(cfg.qkv_bias), int(cfg.qk_norm),
+                          int(cfg.tied_embed), cfg.rms_eps, cfg.rope_theta)
+        blob = self.table.blob
+        self._blob = C.create_string_buffer(blob, len(blob))
+        h = C.c_void_p()
+        _check(self.lib, self.lib.adamk_create(C.byref(desc), self._blob, len(blob), 0, 1, C.byref(h)))
+        self._h = h
+        self._weights: DecoderWeights | None = None
+        self.packed: torch.Tensor | None = None
+        self.workspace = torch.empty(self.lib.adamk_workspace_bytes(h), dtype=torch.uint8, device=self.device)
+        self._stream_ptr = lambda: C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _check(self.lib, self.lib.adamk_workspace_init(h, C.c_void_p(self.workspace.data_ptr()), self._stream_ptr()))
+        kv_elems = self.lib.adamk_kv_cache_bytes(h) // 2
+        self.k_cache = torch.zeros(kv_elems, dtype=torch.bfloat16, device=self.device)
+        self.v_cache = torch.zeros(kv_elems, dtype=torch.bfloat16, device=self.device)
+        self.tokens = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.positions = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.next_token = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.logits = torch.zeros(1, cfg.vocab, dtype=torch.float32, device=self.device)
+        self.launches = 0
+
+    # -- weights -------------------------------------------------------------
+    def bind_weights(self, w: DecoderWeights, keep_source: bool = False) -> None:
+        """Repack HF-layout bf16 weights into the per-SM tile-major streams."""
+        cfg = self.cfg
+        w = w.to(self.device)
+        cos, sin = rope_table(cfg, self.max_ctx)
+        self._rope = (cos.to(self.device), sin.to(self.device))
+        layers = (_LayerWeights * cfg.n_layers)()
+        for i, lw in enumerate(w.layers):
+            for name in _LAYER_FIELDS:
+                t = getattr(lw, name)
+                if t is not None:
+                    assert t.dtype == torch.bfloat16 and t.is_contiguous()
+                setattr(layers[i], name, None if t is None else t.data_ptr())
+        ptrs = _WeightPtrs(w.embed.data_ptr(), w.final_norm.data_ptr(),
+                           None if w.lm_head is None else w.lm_head.data_ptr(),
+                           layers, self._rope[0].data_ptr(), self._rope[1].data_ptr())
+        self.packed = torch.empty(self.lib.adamk_packed_bytes(self._h), dtype=torch.uint8, device=self.device)
+        _check(self.lib, self.lib.adamk_bind_weights(self._h, C.byref(ptrs), C.c_void_p(self.packed.data_ptr()),
+                                                     self._stream_ptr()))
+        self._embed = w.embed                      # the kernel gathers embedding rows from the source table
+        self._weights = w if keep_source else None
+
+    # -- decode ----------------------------------------------------------------
+    def set_state(self, token: int, position: int) -> None:
+        self.tokens.fill_(int(token))
+        self.positions.fill_(int(position))
+
+    def enqueue(self, want_logits: bool = False, auto_advance: bool = True) -> None:
+        """Enqueue ONE decode step (one kernel launch) on the current stream using
+        the device-resident token/position state."""
+        _check(self.lib, self.lib.adamk_decode_step(
+            self._h, C.c_void_p(self.tokens.data_ptr()), C.c_void_p(self.positions.data_ptr()), 1,
+            C.c_void_p(self.k_cache.data_ptr()), C.c_void_p(self.v_cache.data_ptr()),
+            C.c_void_p(self.workspace.data_ptr()),
+            C.c_void_p(self.logits.data_ptr()) if want_logits else None,
+            C.c_void_p(self.next_token.data_ptr()), int(auto_advance), self._stream_ptr()))
+        self.launches += 1
+
+    def decode_step(self, token: int, position: int, want_logits: bool = True) -> StepOutput:
+        """Host-facing step: host token/position in, device outputs out (no sync)."""
+        self.set_state(token, position)
+        self.enqueue(want_logits=want_logits, auto_advance=False)
+        return StepOutput(self.next_token, self.logits if want_logits else None)
+
+    def check(self) -> None:
+        """Synchronise and raise if the kernel reported an error."""
+        try:
+            torch.cuda.synchronize(self.device)
+        finally:
+            info = (C.c_int32 * 8)()
+            code = self.lib.adamk_device_status(self._h, info)
+            if code != 0:
+                raise AdamkError(-5, f"device error {code}: sm={info[1]} task={info[2]} a={info[3]} "
+                                     f"b={info[4]} c={info[5]} tid={info[6]}")
+
+    def stream_probe(self) -> None:
+        sink = torch.zeros(self.n_sms, dtype=torch.float32, device=self.device)
+        _check(self.lib, self.lib.adamk_stream_probe(self._h, C.c_void_p(sink.data_ptr()), self._stream_ptr()))
+
+    def kv_view(self) -> tuple[torch.Tensor, torch.Tensor]:
+        cfg = self.cfg
+        shape = (cfg.n_layers, 1, cfg.n_kv_heads, self.max_ctx, cfg.head_dim)
+        return self.k_cache.view(shape), self.v_cache.view(shape)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self.lib.adamk_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass

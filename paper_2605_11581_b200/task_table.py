@@ -1,0 +1,362 @@
+"""Lower a solidified schedule to the static device task table.
+
+Ada-MK's offline half ends with a ``SolidifiedTrace`` (reference
+``pkg/src/mkplan/search.py:79-107``; plan fields ``tile``, ``n_stage``,
+``consumer_warps``, ``stride_eff``, ``programs``, ``page_plan`` at ``:138-171``).
+That artifact describes ONE SM running ONE layer's pipeline.  The online half
+(paper only, ``PAPER.md:84,177-197``) replays it: Loader warps stream weight
+sub-tiles into pages, Consumer warps compute, Storers publish, and "path
+solidification" means no scheduling decision is left for run time.
+
+This module is the bridge.  It maps the plan's pipeline parameters onto the
+persistent sm_100a kernel's ring (``KernelSchedule``) and expands the whole
+model -- every layer of every operator plus the LM head -- into a flat,
+per-SM, program-ordered list of 64-byte task records with *fixed* dependency
+counter targets.  The kernel (``csrc/adamk.cu``) only walks its list.
+
+Role mapping (reference ``planner.py:60-77`` -> kernel):
+  Loader   -> warp 0, one elected lane issuing ``cp.async.bulk`` (TMA) per stage
+  Consumer -> warps 1..C: GEMV over the staged sub-tile, fp32 accumulate
+  Storer   -> the epilogue of the consumer warps + the release of the counter
+  Launcher -> the task-record fetch at the top of every task
+Page states Empty/Locked/Ready (``planner.py:84-94``) are the ring slot's
+``empty`` mbarrier phase / in-flight TMA / ``full`` mbarrier phase.
+
+Stage geometry: a stage is ``rows_per_tile`` output rows by ``ktile_chunks``
+256-element K chunks of bf16 = the reference's weight sub-tile
+``block_n * sub_k * 2`` bytes (``graph_ir.py:308-311``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .model_config import ModelConfig
+
+MAGIC = 0x4B4D4441  # "ADMK"
+VERSION = 1
+HEADER_INTS = 16
+TASK_INTS = 16
+KCHUNK = 256           # K elements per chunk: 32 lanes x 8 bf16 (one LDS.128 per lane)
+SMEM_MAX = 232448      # 227 KB opt-in shared memory per CTA on sm_100
+SMEM_RESERVED = 1024   # mbarriers + reduction scratch ahead of the scratch/ring regions
+MAX_STAGES = 16
+MAX_RW = 4             # rows per consumer warp per tile the kernel is instantiated for
+ATTN_CLMAX = 512       # positions per attention chunk the scratch region holds
+
+T_END, T_QKV, T_ATTN, T_OPROJ, T_GATEUP, T_DOWN, T_LMHEAD = 0, 1, 2, 3, 4, 5, 6
+GEMV_TYPES = (T_QKV, T_OPROJ, T_GATEUP, T_DOWN, T_LMHEAD)
+TYPE_NAMES = {T_QKV: "qkv", T_ATTN: "attn", T_OPROJ: "oproj", T_GATEUP: "gateup",
+              T_DOWN: "down", T_LMHEAD: "lmhead"}
+
+CTR_A, CTR_B, CTR_C, CTR_D, CTR_E, CTR_F, CTR_HEAD0 = 0, 1, 2, 3, 4, 5, 6
+
+# field indices inside a task record
+F_TYPE, F_LAYER, F_A, F_B, F_K, F_KCHUNKS, F_RT, F_KTC, F_NTILES, F_NKTILES, \
+    F_WOFF, F_NSTAGES, F_WAITCTR, F_WAITVAL, F_SIGCTR, F_AUX = range(16)
+
+
+class ScheduleError(ValueError):
+    """The schedule cannot be executed by the kernel (geometry / smem)."""
+
+
+def _ceil_div(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+@dataclass(frozen=True)
+class KernelSchedule:
+    """Pipeline parameters of the persistent kernel, taken from the plan."""
+
+    consumer_warps: int = 8
+    n_stage: int = 6
+    rows_per_tile: int = 16   # plan tile block_n
+    ktile_chunks: int = 4     # plan tile sub_k / 256
+    attn_min_chunk: int = 64  # positions per split-KV unit before more SMs are used
+
+    def __post_init__(self) -> None:
+        if self.consumer_warps not in (4, 8, 16):
+            raise ScheduleError("consumer_warps must be 4, 8 or 16")
+        if not 1 <= self.n_stage <= MAX_STAGES:
+            raise ScheduleError(f"n_stage must be in 1..{MAX_STAGES}")
+        if self.rows_per_tile % self.consumer_warps:
+            raise ScheduleError("rows_per_tile (block_n) must be a multiple of consumer_warps")
+        rw = self.rows_per_tile // self.consumer_warps
+        if rw not in (2, 4):
+            # rw=1 would split a gate/up row pair across warps (SwiGLU is fused in-warp)
+            raise ScheduleError("block_n / consumer_warps must be 2 or 4")
+        if self.ktile_chunks < 1:
+            raise ScheduleError("sub_k must be a positive multiple of 256")
+        if self.attn_min_chunk < 8 or self.attn_min_chunk > ATTN_CLMAX:
+            raise ScheduleError("attn_min_chunk out of range")
+
+    @property
+    def rows_per_warp(self) -> int:
+        return self.rows_per_tile // self.consumer_warps
+
+    @property
+    def stage_bytes(self) -> int:
+        return self.rows_per_tile * self.ktile_chunks * KCHUNK * 2
+
+    @classmethod
+    def from_plan(cls, plan: dict, **overrides) -> "KernelSchedule":
+        """Read the ring parameters out of ``SolidifiedTrace.plan``.
+
+        tile = [block_m, block_n, block_k, k_split]; sub_k = block_k / k_split.
+        The ring depth is the plan's ``n_stage`` (the window of
+        ``n_stage * per_stage`` pages, reference ``planner.py:415``)."""
+        bm, bn, bk, ks = plan["tile"]
+        sub_k = bk // ks
+        if sub_k % KCHUNK:
+            raise ScheduleError(f"sub_k={sub_k} is not a multiple of {KCHUNK}")
+        kw = dict(consumer_warps=int(plan["consumer_warps"]), n_stage=int(plan["n_stage"]),
+                  rows_per_tile=int(bn), ktile_chunks=sub_k // KCHUNK)
+        kw.update(overrides)
+        return cls(**kw)
+
+
+def scratch_bytes(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> int:
+    """Shared-memory scratch: the fp32 activation vector of the widest GEMV, or
+    the attention unit's q / scores / cross-warp reduction buffers."""
+    kpad_max = max(_ceil_div(k, KCHUNK) * KCHUNK for k in (cfg.hidden, cfg.q_dim, cfg.intermediate))
+    x_bytes = batch * kpad_max * 4
+    g, d, c = cfg.group, cfg.head_dim, sched.consumer_warps
+    attn_bytes = (g * d + g * ATTN_CLMAX + c * g * d + 2 * 8 + d) * 4
+    return _ceil_div(max(x_bytes, attn_bytes), 1024) * 1024
+
+
+def max_stages_that_fit(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> int:
+    free = SMEM_MAX - SMEM_RESERVED - scratch_bytes(cfg, sched, batch)
+    return max(0, free // sched.stage_bytes)
+
+
+def split_rows(n_units: int, n_sms: int, rot: int) -> list[tuple[int, int]]:
+    """Contiguous, near-even split of ``n_units`` over ``n_sms`` SMs.
+
+    The ``n_units % n_sms`` SMs that take one extra unit start at SM ``rot`` so
+    consecutive operators put their remainder on different SMs and the per-SM
+    byte streams stay balanced.  Returns [(first_unit, count)] indexed by SM."""
+    base, rem = divmod(n_units, n_sms)
+    out = [(0, 0)] * n_sms
+    for jr in range(n_sms):
+        sm = (jr + rot) % n_sms
+        first = jr * base + min(jr, rem)
+        out[sm] = (first, base + (1 if jr < rem else 0))
+    return out
+
+
+@dataclass
+class TaskTable:
+    cfg: ModelConfig
+    sched: KernelSchedule
+    n_sms: int
+    batch: int
+    header: np.ndarray      # int32[HEADER_INTS]
+    sm_begin: np.ndarray    # int32[n_sms + 1]
+    tasks: np.ndarray       # int32[n_tasks, TASK_INTS]
+    packed_weight_bytes: int
+    n_counters: int
+    attn_chunks: int
+
+    @property
+    def blob(self) -> bytes:
+        return np.concatenate([self.header, self.sm_begin, self.tasks.reshape(-1)]).astype("<i4").tobytes()
+
+    def tasks_of(self, sm: int) -> np.ndarray:
+        return self.tasks[self.sm_begin[sm]:self.sm_begin[sm + 1]]
+
+    def stream_bytes_per_sm(self) -> np.ndarray:
+        out = np.zeros(self.n_sms, dtype=np.int64)
+        for sm in range(self.n_sms):
+            out[sm] = sum(task_weight_bytes(t) for t in self.tasks_of(sm))
+        return out
+
+    def summary(self) -> dict:
+        per_sm = self.stream_bytes_per_sm()
+        return {
+            "n_sms": self.n_sms, "n_tasks": int(self.tasks.shape[0]),
+            "consumer_warps": self.sched.consumer_warps, "n_stage": self.sched.n_stage,
+            "stage_bytes": self.sched.stage_bytes, "packed_weight_bytes": int(self.packed_weight_bytes),
+            "stream_bytes_min": int(per_sm.min()), "stream_bytes_max": int(per_sm.max()),
+            "attn_chunks": self.attn_chunks, "n_counters": self.n_counters,
+        }
+
+
+def stage_shapes(task: np.ndarray):
+    """Yield (tile, ktile, rows, chunks) for every ring stage of a GEMV task, in
+    the order the Loader issues them and the Consumers drain them."""
+    nrows, rt, ktc, kchunks = int(task[F_B]), int(task[F_RT]), int(task[F_KTC]), int(task[F_KCHUNKS])
+    for tile in range(int(task[F_NTILES])):
+        rows = min(rt, nrows - tile * rt)
+        for kt in range(int(task[F_NKTILES])):
+            yield tile, kt, rows, min(ktc, kchunks - kt * ktc)
+
+
+def task_weight_bytes(task: np.ndarray) -> int:
+    if int(task[F_TYPE]) not in GEMV_TYPES:
+        return 0
+    # rows * kchunks * 512, independent of tiling
+    return int(task[F_B]) * int(task[F_KCHUNKS]) * KCHUNK * 2
+
+
+def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, batch: int = 1) -> TaskTable:
+    if batch != 1:
+        raise ScheduleError("this build executes batch 1 only (batched path: SURVEY.md 8(f).1)")
+    if n_sms < 1:
+        raise ScheduleError("n_sms must be >= 1")
+    fit = max_stages_that_fit(cfg, sched, batch)
+    if sched.n_stage > fit:
+        raise ScheduleError(
+            f"n_stage={sched.n_stage} x {sched.stage_bytes} B stages + "
+            f"{scratch_bytes(cfg, sched, batch)} B scratch exceed {SMEM_MAX} B shared memory (max {fit})")
+    for k in (cfg.hidden, cfg.q_dim, cfg.intermediate):
+        if k % 8:
+            raise ScheduleError("reduction dims must be multiples of 8")
+
+    nkv = cfg.n_kv_heads
+    attn_chunks = max(1, min(n_sms // (batch * nkv), 128))
+    n_counters = CTR_HEAD0 + batch * nkv
+    per_sm: list[list[list[int]]] = [[] for _ in range(n_sms)]
+    rot = 0
+    done = {CTR_A: 0, CTR_B: 0, CTR_D: 0, CTR_E: 0}   # cumulative signal counts per counter
+
+    def gemv(ttype: int, layer: int, n_rows: int, k: int, unit: int, wait_ctr: int, wait_val: int,
+             sig_ctr: int) -> int:
+        """Emit one GEMV operator across all SMs; returns the number of tasks."""
+        nonlocal rot
+        assert n_rows % unit == 0
+        kchunks = _ceil_div(k, KCHUNK)
+        ktc = min(sched.ktile_chunks, kchunks)
+        n_kt = _ceil_div(kchunks, ktc)
+        ktc = _ceil_div(kchunks, n_kt)          # even out the k-tiles
+        n_kt = _ceil_div(kchunks, ktc)
+        split = split_rows(n_rows // unit, n_sms, rot)
+        rot = (rot + (n_rows // unit) % n_sms) % n_sms
+        emitted = 0
+        for sm, (first, cnt) in enumerate(split):
+            if cnt == 0:
+                continue
+            nrows = cnt * unit
+            n_tiles = _ceil_div(nrows, sched.rows_per_tile)
+            per_sm[sm].append([ttype, layer, first * unit, nrows, k, kchunks, sched.rows_per_tile, ktc,
+                               n_tiles, n_kt, 0, n_tiles * n_kt, wait_ctr, wait_val, sig_ctr, 0])
+            emitted += 1
+        return emitted
+
+    for layer in range(cfg.n_layers):
+        wa = (CTR_A, done[CTR_A]) if layer > 0 else (-1, 0)
+        done[CTR_B] += gemv(T_QKV, layer, cfg.qkv_rows, cfg.hidden, 1, wa[0], wa[1], CTR_B)
+        for b in range(batch):
+            for kvh in range(nkv):
+                for c in range(attn_chunks):
+                    sm = ((b * nkv + kvh) * attn_chunks + c) % n_sms
+                    per_sm[sm].append([T_ATTN, layer, kvh, c, 0, 0, 0, 0, 0, 0, 0, 0,
+                                       CTR_B, done[CTR_B], CTR_HEAD0 + b * nkv + kvh, b])
+        done[CTR_D] += gemv(T_OPROJ, layer, cfg.hidden, cfg.q_dim, 1, CTR_C, (layer + 1) * batch * nkv, CTR_D)
+        done[CTR_E] += gemv(T_GATEUP, layer, 2 * cfg.intermediate, cfg.hidden, 2, CTR_D, done[CTR_D], CTR_E)
+        done[CTR_A] += gemv(T_DOWN, layer, cfg.hidden, cfg.intermediate, 1, CTR_E, done[CTR_E], CTR_A)
+    n_lm = gemv(T_LMHEAD, cfg.n_layers, cfg.vocab, cfg.hidden, 1, CTR_A, done[CTR_A], CTR_F)
+
+    # weight offsets: each SM's stream is one contiguous run, SM-major
+    cursor = 0
+    sm_begin = np.zeros(n_sms + 1, dtype=np.int32)
+    flat: list[list[int]] = []
+    for sm in range(n_sms):
+        sm_begin[sm] = len(flat)
+        for t in per_sm[sm]:
+            if t[F_TYPE] in GEMV_TYPES:
+                t[F_WOFF] = cursor // 16
+                cursor += t[F_B] * t[F_KCHUNKS] * KCHUNK * 2
+            flat.append(t)
+    sm_begin[n_sms] = len(flat)
+    if cursor // 16 >= 2 ** 31:
+        raise ScheduleError("packed weights exceed the 32 GiB offset range of the task record")
+    tasks = np.asarray(flat, dtype=np.int32).reshape(-1, TASK_INTS)
+
+    header = np.zeros(HEADER_INTS, dtype=np.int32)
+    header[:13] = [MAGIC, VERSION, n_sms, sched.consumer_warps, sched.n_stage, sched.stage_bytes,
+                   tasks.shape[0], batch, n_counters, attn_chunks, sched.attn_min_chunk,
+                   scratch_bytes(cfg, sched, batch), n_lm]
+    header[13] = (cursor // 16) & 0x7FFFFFFF
+    return TaskTable(cfg=cfg, sched=sched, n_sms=n_sms, batch=batch, header=header, sm_begin=sm_begin,
+                     tasks=tasks, packed_weight_bytes=cursor, n_counters=n_counters,
+                     attn_chunks=attn_chunks)
+
+
+# ---------------------------------------------------------------------------
+# Host restatement of the device weight packer (tests: exact-cover + bit parity)
+# ---------------------------------------------------------------------------
+
+def virtual_row_source(cfg: ModelConfig, ttype: int, vrow: int) -> tuple[str, int]:
+    """(matrix name, row) a virtual output row of an operator reads."""
+    if ttype == T_QKV:
+        if vrow < cfg.q_dim:
+            return "wq", vrow
+        if vrow < cfg.q_dim + cfg.kv_dim:
+            return "wk", vrow - cfg.q_dim
+        return "wv", vrow - cfg.q_dim - cfg.kv_dim
+    if ttype == T_OPROJ:
+        return "wo", vrow
+    if ttype == T_GATEUP:      # gate/up rows interleaved so one warp owns a pair
+        return ("wup", vrow >> 1) if vrow & 1 else ("wgate", vrow >> 1)
+    if ttype == T_DOWN:
+        return "wdown", vrow
+    if ttype == T_LMHEAD:
+        return "lm_head", vrow
+    raise ValueError(ttype)
+
+
+def chunk_permutation() -> np.ndarray:
+    """Packed position -> original offset inside one 256-element K chunk.
+
+    Lane ``l`` owns packed elements ``8l..8l+7``; they hold original offsets
+    ``4l..4l+3`` and ``128+4l..128+4l+3`` so that the matching fp32 activations
+    are two conflict-free LDS.128 per lane."""
+    p = np.arange(KCHUNK)
+    lane, e = p // 8, p % 8
+    return (e >> 2) * 128 + lane * 4 + (e & 3)
+
+
+def pack_weights_reference(table: TaskTable, weights) -> np.ndarray:
+    """NumPy restatement of ``adamk_pack_kernel``: uint16 view of the packed bf16
+    weight stream (without the fp32 parameter tail)."""
+    import torch
+
+    cfg = table.cfg
+    perm = chunk_permutation()
+    out = np.zeros(table.packed_weight_bytes // 2, dtype=np.uint16)
+
+    def as_u16(t):
+        return t.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16)
+
+    mats: dict[tuple[int, str], np.ndarray] = {}
+
+    def mat(layer: int, name: str) -> np.ndarray:
+        key = (layer, name)
+        if key not in mats:
+            if name == "lm_head":
+                mats[key] = as_u16(weights.lm_head_matrix)
+            else:
+                mats[key] = as_u16(getattr(weights.layers[layer], name))
+        return mats[key]
+
+    for task in table.tasks:
+        ttype = int(task[F_TYPE])
+        if ttype not in GEMV_TYPES:
+            continue
+        layer, vrow0, k = int(task[F_LAYER]), int(task[F_A]), int(task[F_K])
+        rt, ktc = int(task[F_RT]), int(task[F_KTC])
+        pos = int(task[F_WOFF]) * 8  # uint16 elements
+        for tile, kt, rows, chunks in stage_shapes(task):
+            for r in range(rows):
+                name, row = virtual_row_source(cfg, ttype, vrow0 + tile * rt + r)
+                src = mat(layer, name)[row]
+                for c in range(chunks):
+                    kbase = (kt * ktc + c) * KCHUNK
+                    kidx = kbase + perm
+                    vals = np.where(kidx < k, src[np.minimum(kidx, k - 1)], 0).astype(np.uint16)
+                    out[pos:pos + KCHUNK] = vals
+                    pos += KCHUNK
+    return out
