@@ -136,8 +136,9 @@ int adamk_device_status(adamk_handle h, int32_t* info);
 
 /* Standalone weight-streaming probe used by the measurement harness: runs only
  * the Loader/Consumer ring over the packed stream (no dependencies), to
- * separate HBM streaming efficiency from dependency stalls. */
-int adamk_stream_probe(adamk_handle h, float* sink, adamk_stream stream);
+ * separate HBM streaming efficiency from dependency stalls.  mode 1: Loader +
+ * Consumer math; mode 2: Loader only (consumers release slots untouched). */
+int adamk_stream_probe(adamk_handle h, float* sink, int mode, adamk_stream stream);
 
 #ifdef __cplusplus
 }

@@ -95,7 +95,7 @@ struct KParams {
   int* next_tokens;
   int* status;  // host-mapped, 8 ints
   int auto_advance;
-  int probe;    // 1 = stream probe: consumers skip dependencies and epilogues
+  int probe;    // 1 = stream probe: consumers skip dependencies and epilogues; 2 = also skip the math
   float* probe_sink;
 };
 
@@ -337,7 +337,7 @@ __device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, con
       const uint32_t slot = c.it % (uint32_t)p.n_stage;
       const uint32_t ph = (c.it / (uint32_t)p.n_stage) & 1u;
       mbar_wait(p, full0 + slot * 8, ph, DE_WATCHDOG_FULL, task_idx);
-      if (r0 < rows) {
+      if (r0 < rows && p.probe != 2) {
         const uint32_t row_stride = (uint32_t)chunks * 512u;
         const uint32_t wbase = ring_addr + slot * (uint32_t)p.stage_bytes + (uint32_t)r0 * row_stride + c.lane * 16;
         const uint32_t xk = xs_addr + (uint32_t)(kt * t.ktc) * (kChunk * 4);
@@ -904,6 +904,11 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   if (h->n_stage < 1 || h->n_stage > kMaxStages) return bad("n_stage out of range");
   if (h->stage_bytes <= 0 || h->stage_bytes % 1024) return bad("stage_bytes must be a positive multiple of 1024");
   if (h->n_sms < 1 || h->n_tasks < 1) return bad("empty task table");
+  if (h->attn_chunks < 1 || h->attn_min_chunk < 8 || h->attn_min_chunk > kAttnCLMax) return bad("attention chunking out of range");
+  if ((long long)d.max_ctx > (long long)h->attn_chunks * kAttnCLMax) {
+    delete h;
+    return fail(ADAMK_E_UNSUPPORTED, "max_ctx exceeds attn_chunks * 512 positions");
+  }
   const size_t need = ((size_t)kHeaderInts + (size_t)h->n_sms + 1 + (size_t)h->n_tasks * kTaskInts) * 4;
   if (task_table_bytes != need) return bad("task table size does not match its header");
   if (h->n_counters != CTR_HEAD0 + h->batch * d.n_kv_heads) return bad("counter count mismatch");
@@ -1136,12 +1141,12 @@ int adamk_decode_step(adamk_handle h, int32_t* token_ids, int32_t* positions, in
   return launch(h, p, (cudaStream_t)stream);
 }
 
-int adamk_stream_probe(adamk_handle h, float* sink, adamk_stream stream) {
+int adamk_stream_probe(adamk_handle h, float* sink, int mode, adamk_stream stream) {
   if (!h || !sink) return fail(ADAMK_E_INVALID, "NULL argument");
   if (!h->bound) return fail(ADAMK_E_STATE, "adamk_bind_weights has not been called");
   KParams p;
   fill_params(h, p, nullptr);
-  p.probe = 1; p.probe_sink = sink;
+  p.probe = (mode == 2) ? 2 : 1; p.probe_sink = sink;
   return launch(h, p, (cudaStream_t)stream);
 }
 

@@ -86,7 +86,7 @@ def load_library() -> C.CDLL:
     lib.adamk_decode_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     lib.adamk_device_status.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
-    lib.adamk_stream_probe.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.adamk_stream_probe.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     if lib.adamk_abi_version() != ABI_VERSION:
         raise AdamkError(-101, "libadamk.so ABI version mismatch; rebuild")
     _lib = lib
@@ -206,9 +206,11 @@ class MegaKernelPlugin:
                 raise AdamkError(-5, f"device error {code}: sm={info[1]} task={info[2]} a={info[3]} "
                                      f"b={info[4]} c={info[5]} tid={info[6]}")
 
-    def stream_probe(self) -> None:
-        sink = torch.zeros(self.n_sms, dtype=torch.float32, device=self.device)
-        _check(self.lib, self.lib.adamk_stream_probe(self._h, C.c_void_p(sink.data_ptr()), self._stream_ptr()))
+    def stream_probe(self, mode: int = 1) -> None:
+        if not hasattr(self, "_sink"):
+            self._sink = torch.zeros(self.n_sms, dtype=torch.float32, device=self.device)
+        _check(self.lib, self.lib.adamk_stream_probe(self._h, C.c_void_p(self._sink.data_ptr()), mode,
+                                                     self._stream_ptr()))
 
     def kv_view(self) -> tuple[torch.Tensor, torch.Tensor]:
         cfg = self.cfg
