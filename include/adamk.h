@@ -134,6 +134,14 @@ int adamk_decode_step(adamk_handle h, int32_t* token_ids, int32_t* positions, in
  * Fills `info` (8 ints: code, sm, task, counter, seen, expected, ...) if not NULL. */
 int adamk_device_status(adamk_handle h, int32_t* info);
 
+/* Optional per-task timeline (the device analogue of the reference's
+ * chrome_trace_events, /root/reference/pkg/src/mkplan/simulator.py:381-411):
+ * when a device buffer of adamk_trace_bytes() is set, consumer thread 0 of every
+ * CTA stores four %globaltimer stamps per task (start, dependency met, prologue
+ * done, end).  NULL disables tracing. */
+size_t adamk_trace_bytes(adamk_handle h);
+int adamk_set_trace(adamk_handle h, void* trace_buf);
+
 /* Standalone weight-streaming probe used by the measurement harness: runs only
  * the Loader/Consumer ring over the packed stream (no dependencies), to
  * separate HBM streaming efficiency from dependency stalls.  mode 1: Loader +

@@ -46,7 +46,8 @@ constexpr int kChunk = 256;          // K elements per chunk
 constexpr int kSmemMax = 232448;
 constexpr int kSmemReserved = 1024;  // barriers + reduction scratch
 constexpr int kMaxStages = 16;
-constexpr int kAttnCLMax = 512;
+constexpr int kAttnPBMax = 128;      // positions per attention block (8 per consumer warp)
+constexpr int kAttnChunksMax = 128;  // split-KV units per (sequence, kv head)
 constexpr int kGMax = 8;             // max q heads per kv head
 
 enum TaskType { T_END = 0, T_QKV = 1, T_ATTN = 2, T_OPROJ = 3, T_GATEUP = 4, T_DOWN = 5, T_LMHEAD = 6 };
@@ -70,6 +71,8 @@ struct KParams {
   // task table
   const Task* tasks;
   const int* sm_begin;
+  const unsigned* sm_stream;  // [n_sms + 1] packed-stream range of every SM (16-byte units)
+  int pf_min_bytes, pf_max_bytes;  // L2 prefetch distance ahead of the ring: steady state / while stalled
   // weights
   const uint8_t* wpacked;   // tile-major bf16 weight streams
   const float* fparams;     // fp32 norm gains / biases
@@ -97,6 +100,7 @@ struct KParams {
   int auto_advance;
   int probe;    // 1 = stream probe: consumers skip dependencies and epilogues; 2 = also skip the math
   float* probe_sink;
+  unsigned long long* trace;  // optional [n_tasks][8] globaltimer stamps (0 start, 1 dependency met, 2 prologue done, 7 end, 3-6 op specific)
 };
 
 // ----------------------------------------------------------------------------------
@@ -130,10 +134,35 @@ __device__ __forceinline__ void tma_bulk_g2s(uint32_t dst, const void* src, uint
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void l2_prefetch_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -184,12 +213,25 @@ __device__ __noinline__ void dev_fail(const KParams& p, int code, int task, int 
   __trap();
 }
 
-__device__ __forceinline__ void mbar_wait(const KParams& p, uint32_t bar, uint32_t parity, int code, int task) {
-  if (mbar_try_wait(bar, parity)) return;
-  long long t0 = clock64();
-  while (!mbar_try_wait(bar, parity)) {
+__device__ __forceinline__ uint32_t mbar_try_wait_hint(uint32_t bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(ns)
+      : "memory");
+  return ok;
+}
+__device__ __noinline__ void mbar_wait_slow(const KParams& p, uint32_t bar, uint32_t parity, int code, int task) {
+  const long long t0 = clock64();
+  while (!mbar_try_wait_hint(bar, parity, 2000u)) {
     if (clock64() - t0 > kWatchdogCycles) dev_fail(p, code, task, (int)bar, (int)parity, 0);
   }
+}
+__device__ __forceinline__ void mbar_wait(const KParams& p, uint32_t bar, uint32_t parity, int code, int task) {
+  if (!mbar_try_wait(bar, parity)) mbar_wait_slow(p, bar, parity, code, task);
 }
 
 // ----------------------------------------------------------------------------------
@@ -204,29 +246,37 @@ struct SmemHdr {
 static_assert(sizeof(SmemHdr) <= kSmemReserved, "smem header too large");
 
 struct ConsumerCtx {
-  uint32_t it;        // ring stages consumed so far (slot = it % n_stage)
+  uint32_t slot;      // ring slot of the next stage to drain
+  uint32_t ph;        // its mbarrier phase parity
   int cw;             // consumer warp index 0..C-1
   int lane;
   int ctid;           // thread index among consumers
   int nct;            // number of consumer threads
+  float rs;           // RMSNorm scale of the current GEMV's input (applied in the epilogue), else 1
   float best_val;     // LM-head running argmax (lane 0 of each warp)
   int best_idx;
 };
 
+__device__ __forceinline__ void stamp(const KParams& p, const ConsumerCtx& c, int task, int k) {
+  if (p.trace && c.ctid == 0) p.trace[(size_t)task * 8 + k] = globaltimer_ns();
+}
+
 // ----------------------------------------------------------------------------------
 // dependency wait / signal
 // ----------------------------------------------------------------------------------
+__device__ __noinline__ void poll_counter_slow(const KParams& p, const unsigned* addr, int val, int ctr, int task) {
+  const long long t0 = clock64();
+  unsigned seen;
+  while ((seen = ld_relaxed_u32(addr)) < (unsigned)val) {
+    if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_CTR, task, ctr, (int)seen, val);
+  }
+}
 __device__ __forceinline__ void wait_counter(const KParams& p, const ConsumerCtx& c, int ctr, int val, int task) {
   if (ctr >= 0 && !p.probe) {
     if (c.ctid == 0) {
       const unsigned* addr = p.counters + ctr;
-      if (ld_acquire_u32(addr) < (unsigned)val) {
-        long long t0 = clock64();
-        unsigned seen;
-        while ((seen = ld_acquire_u32(addr)) < (unsigned)val) {
-          if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_CTR, task, ctr, (int)seen, val);
-        }
-      }
+      if (ld_relaxed_u32(addr) < (unsigned)val) poll_counter_slow(p, addr, val, ctr, task);
+      fence_acq_rel_gpu();  // one acquire for the whole poll loop (no per-poll L1 invalidate)
     }
   }
   consumer_sync(c.nct);
@@ -258,10 +308,11 @@ __device__ __forceinline__ float load_h1(const KParams& p, int layer, int tok, i
 }
 
 // Stage the activation vector of a GEMV in shared memory (fp32, zero padded to kpad).
-__device__ __forceinline__ void gemv_prologue(const KParams& p, const ConsumerCtx& c, const Task& t, float* xs,
+__device__ __forceinline__ void gemv_prologue(const KParams& p, ConsumerCtx& c, const Task& t, float* xs,
                                               SmemHdr* hdr, int tok) {
   const int kpad = t.kchunks * kChunk;
   const int type = t.type;
+  c.rs = 1.0f;
   if (type == T_OPROJ || type == T_DOWN) {
     const float* src = (type == T_OPROJ) ? p.attn : p.act;
     const int k4 = t.k >> 2;
@@ -280,10 +331,16 @@ __device__ __forceinline__ void gemv_prologue(const KParams& p, const ConsumerCt
                                          : (p.fparams + (size_t)t.layer * p.fp_layer_stride + (mid ? p.fp_ln2 : p.fp_ln1));
   const int h4 = p.H >> 2;
   float ss = 0.f;
+  // single pass: stage h * gain, accumulate sum(h^2); the scalar rsqrt(mean + eps) commutes
+  // with the dot products and is applied to each output row in the epilogue
   for (int i = c.ctid; i < (kpad >> 2); i += c.nct) {
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < h4) v = load_h4(p, layer, mid, tok, i);
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    if (i < h4) {
+      v = load_h4(p, layer, mid, tok, i);
+      const float4 g = __ldg(reinterpret_cast<const float4*>(gain) + i);
+      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+      v.x *= g.x; v.y *= g.y; v.z *= g.z; v.w *= g.w;
+    }
     reinterpret_cast<float4*>(xs)[i] = v;
   }
   ss = warp_sum(ss);
@@ -291,14 +348,7 @@ __device__ __forceinline__ void gemv_prologue(const KParams& p, const ConsumerCt
   consumer_sync(c.nct);
   float tot = 0.f;
   for (int w = 0; w < p.C; ++w) tot += hdr->red[w];
-  const float rs = rsqrtf(tot / (float)p.H + p.eps);
-  for (int i = c.ctid; i < h4; i += c.nct) {
-    float4 v = reinterpret_cast<float4*>(xs)[i];
-    const float4 g = __ldg(reinterpret_cast<const float4*>(gain) + i);
-    v.x = v.x * rs * g.x; v.y = v.y * rs * g.y; v.z = v.z * rs * g.z; v.w = v.w * rs * g.w;
-    reinterpret_cast<float4*>(xs)[i] = v;
-  }
-  consumer_sync(c.nct);
+  c.rs = rsqrtf(tot / (float)p.H + p.eps);
 }
 
 __device__ __forceinline__ void gemv_epilogue(const KParams& p, ConsumerCtx& c, const Task& t, int vrow, float v,
@@ -319,73 +369,82 @@ __device__ __forceinline__ void gemv_epilogue(const KParams& p, ConsumerCtx& c, 
   }
 }
 
+// One 256-element K chunk of RW rows: acc[i] += w[i][chunk] . x[chunk].  bf16 -> fp32 is a
+// shift / mask per element; the products go through the packed FFMA2 pipe (sm_100).
+template <int RW, bool ALL>
+__device__ __forceinline__ void gemv_chunk(uint32_t waddr, uint32_t row_stride, uint32_t xaddr, int nrows,
+                                           float2 (&accA)[RW], float2 (&accB)[RW]) {
+  const float4 xa = lds128f(xaddr);
+  const float4 xb = lds128f(xaddr + 512);
+#pragma unroll
+  for (int i = 0; i < RW; ++i) {
+    if (ALL || i < nrows) {
+      const uint4 w = lds128u(waddr + i * row_stride);
+      accA[i] = __ffma2_rn(make_float2(bf_lo(w.x), bf_hi(w.x)), make_float2(xa.x, xa.y), accA[i]);
+      accB[i] = __ffma2_rn(make_float2(bf_lo(w.y), bf_hi(w.y)), make_float2(xa.z, xa.w), accB[i]);
+      accA[i] = __ffma2_rn(make_float2(bf_lo(w.z), bf_hi(w.z)), make_float2(xb.x, xb.y), accA[i]);
+      accB[i] = __ffma2_rn(make_float2(bf_lo(w.w), bf_hi(w.w)), make_float2(xb.z, xb.w), accB[i]);
+    }
+  }
+}
+
 template <int RW>
 __device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx,
                                            const float* xs, SmemHdr* hdr, uint8_t* ring, int tok) {
   const uint32_t xs_addr = smem_u32(xs) + c.lane * 16;
-  const uint32_t ring_addr = smem_u32(ring);
+  const uint32_t ring_addr = smem_u32(ring) + c.lane * 16;
   const uint32_t full0 = smem_u32(&hdr->full[0]);
   const uint32_t empty0 = smem_u32(&hdr->empty[0]);
+  const int r0 = c.cw * RW;
+  const uint32_t n_stage = (uint32_t)p.n_stage;
   for (int tile = 0; tile < t.n_tiles; ++tile) {
     const int rows = min(t.rt, t.b - tile * t.rt);
-    float acc0[RW], acc1[RW];
+    const int nrows = min(RW, rows - r0);  // rows of this tile owned by this warp (<= 0: none)
+    float2 accA[RW], accB[RW];
 #pragma unroll
-    for (int i = 0; i < RW; ++i) { acc0[i] = 0.f; acc1[i] = 0.f; }
-    const int r0 = c.cw * RW;
-    for (int kt = 0; kt < t.n_ktiles; ++kt) {
-      const int chunks = min(t.ktc, t.kchunks - kt * t.ktc);
-      const uint32_t slot = c.it % (uint32_t)p.n_stage;
-      const uint32_t ph = (c.it / (uint32_t)p.n_stage) & 1u;
-      mbar_wait(p, full0 + slot * 8, ph, DE_WATCHDOG_FULL, task_idx);
-      if (r0 < rows && p.probe != 2) {
+    for (int i = 0; i < RW; ++i) { accA[i] = make_float2(0.f, 0.f); accB[i] = make_float2(0.f, 0.f); }
+    int kc0 = 0;
+    for (int kt = 0; kt < t.n_ktiles; ++kt, kc0 += t.ktc) {
+      const int chunks = min(t.ktc, t.kchunks - kc0);
+      mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);
+      if (nrows > 0 && p.probe != 2) {
         const uint32_t row_stride = (uint32_t)chunks * 512u;
-        const uint32_t wbase = ring_addr + slot * (uint32_t)p.stage_bytes + (uint32_t)r0 * row_stride + c.lane * 16;
-        const uint32_t xk = xs_addr + (uint32_t)(kt * t.ktc) * (kChunk * 4);
+        uint32_t wa = ring_addr + c.slot * (uint32_t)p.stage_bytes + (uint32_t)r0 * row_stride;
+        uint32_t xa = xs_addr + (uint32_t)kc0 * (kChunk * 4);
+        if (nrows == RW) {
 #pragma unroll 2
-        for (int ch = 0; ch < chunks; ++ch) {
-          const float4 xa = lds128f(xk + ch * (kChunk * 4));
-          const float4 xb = lds128f(xk + ch * (kChunk * 4) + 512);
-#pragma unroll
-          for (int i = 0; i < RW; ++i) {
-            if (r0 + i < rows) {
-              const uint4 w = lds128u(wbase + i * row_stride + ch * 512);
-              acc0[i] = fmaf(bf_lo(w.x), xa.x, acc0[i]);
-              acc1[i] = fmaf(bf_hi(w.x), xa.y, acc1[i]);
-              acc0[i] = fmaf(bf_lo(w.y), xa.z, acc0[i]);
-              acc1[i] = fmaf(bf_hi(w.y), xa.w, acc1[i]);
-              acc0[i] = fmaf(bf_lo(w.z), xb.x, acc0[i]);
-              acc1[i] = fmaf(bf_hi(w.z), xb.y, acc1[i]);
-              acc0[i] = fmaf(bf_lo(w.w), xb.z, acc0[i]);
-              acc1[i] = fmaf(bf_hi(w.w), xb.w, acc1[i]);
-            }
-          }
+          for (int ch = 0; ch < chunks; ++ch, wa += 512, xa += kChunk * 4)
+            gemv_chunk<RW, true>(wa, row_stride, xa, RW, accA, accB);
+        } else {
+          for (int ch = 0; ch < chunks; ++ch, wa += 512, xa += kChunk * 4)
+            gemv_chunk<RW, false>(wa, row_stride, xa, nrows, accA, accB);
         }
       }
       __syncwarp();
-      if (c.lane == 0) mbar_arrive(empty0 + slot * 8);
-      ++c.it;
+      if (c.lane == 0) mbar_arrive(empty0 + c.slot * 8);
+      if (++c.slot == n_stage) { c.slot = 0; c.ph ^= 1u; }
     }
     if (p.probe) {
       float s = 0.f;
 #pragma unroll
-      for (int i = 0; i < RW; ++i) s += acc0[i] + acc1[i];
+      for (int i = 0; i < RW; ++i) s += accA[i].x + accA[i].y + accB[i].x + accB[i].y;
       if (s == 1.2345678e-30f) p.probe_sink[blockIdx.x] = s;  // keep the math alive
       continue;
     }
-    if (r0 < rows) {
+    if (nrows > 0) {
       float v[RW];
 #pragma unroll
-      for (int i = 0; i < RW; ++i) v[i] = warp_sum(acc0[i] + acc1[i]);
+      for (int i = 0; i < RW; ++i) v[i] = c.rs * warp_sum((accA[i].x + accB[i].x) + (accA[i].y + accB[i].y));
       if (c.lane == 0) {
         const int vrow0 = t.a + tile * t.rt + r0;
         if (t.type == T_GATEUP) {
 #pragma unroll
           for (int i = 0; i < RW; i += 2)
-            if (r0 + i < rows) gemv_epilogue(p, c, t, vrow0 + i, v[i], v[(i + 1) % RW], tok);
+            if (i < nrows) gemv_epilogue(p, c, t, vrow0 + i, v[i], v[(i + 1) % RW], tok);
         } else {
 #pragma unroll
           for (int i = 0; i < RW; ++i)
-            if (r0 + i < rows) gemv_epilogue(p, c, t, vrow0 + i, v[i], 0.f, tok);
+            if (i < nrows) gemv_epilogue(p, c, t, vrow0 + i, v[i], 0.f, tok);
         }
       }
     }
@@ -439,14 +498,19 @@ __device__ __forceinline__ void lm_finish(const KParams& p, ConsumerCtx& c, Smem
 
 __device__ __forceinline__ void run_gemv(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* xs,
                                          SmemHdr* hdr, uint8_t* ring, int tok) {
+  stamp(p, c, task_idx, 0);
   wait_counter(p, c, t.wait_ctr, t.wait_val, task_idx);
+  stamp(p, c, task_idx, 1);
   if (!p.probe) gemv_prologue(p, c, t, xs, hdr, tok);
+  stamp(p, c, task_idx, 2);
   const int rw = t.rt / p.C;
   if (rw == 2) gemv_tiles<2>(p, c, t, task_idx, xs, hdr, ring, tok);
   else gemv_tiles<4>(p, c, t, task_idx, xs, hdr, ring, tok);
   if (p.probe) return;
+  stamp(p, c, task_idx, 3);
   if (t.type == T_LMHEAD) lm_finish(p, c, hdr);
   else signal_counter(p, c, t.sig_ctr);
+  stamp(p, c, task_idx, 7);
 }
 
 // ----------------------------------------------------------------------------------
@@ -480,9 +544,14 @@ __device__ __forceinline__ void rope_norm_head(const KParams& p, const float* ra
   }
 }
 
+// Layout of the attention scratch (floats); must match task_table.scratch_bytes / adamk_create.
+//   qs[G][D] | sc[G][kAttnPBMax] | red[C][G][D] | lw[C][kGMax] | knew[D] | vnew[D] | wts[kAttnChunksMax][kGMax]
 template <int D>
 __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* scratch,
                                          SmemHdr* hdr, int pos) {
+  constexpr int EPL = D / 8;   // K elements per lane in the score step (8 lanes per position)
+  constexpr int KQ = EPL / 8;  // uint4 loads per lane per position
+  constexpr int DPL = D / 32;  // V / output elements per lane in the P.V step
   const int G = p.G;
   const int kvh = t.a, slot = t.b, bidx = t.aux;
   const int ctx = pos + 1;
@@ -490,16 +559,21 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
   CL = (CL + 7) & ~7;
   const int n_active = (ctx + CL - 1) / CL;
   if (slot >= n_active || p.probe) return;  // uniform across the CTA's consumers
-  wait_counter(p, c, t.wait_ctr, t.wait_val, task_idx);
+  stamp(p, c, task_idx, 0);
 
   const int t0 = slot * CL;
   const int n = min(ctx, t0 + CL) - t0;
-  // scratch carve-up (floats)
-  float* qs = scratch;                  // [G][D]
-  float* sc = qs + G * D;               // [G][kAttnCLMax]
-  float* red = sc + G * kAttnCLMax;     // [C][G][D]
-  float* ml = red + p.C * G * D;        // m[G], l[G]
-  float* knew = ml + 2 * kGMax;         // [D] staging for the new K row (bf16-rounded fp32)
+  const int PB = 8 * p.C;  // positions per block; every warp owns 8 consecutive positions of a block
+  const int nblk = (n + PB - 1) / PB;
+  const bool owns_new = (slot == n_active - 1);  // this chunk contains position `pos`
+
+  float* qs = scratch;
+  float* sc = qs + G * D;
+  float* red = sc + G * kAttnPBMax;
+  float* lw = red + p.C * G * D;
+  float* knew = lw + p.C * kGMax;
+  float* vnew = knew + D;
+  float* wts = vnew + D;
 
   const float* qkv = p.qkv + (size_t)bidx * p.qkv_rows;
   const float* lay_fp = p.fparams + (size_t)t.layer * p.fp_layer_stride;
@@ -507,170 +581,244 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
   const size_t head_base = ((size_t)(t.layer * p.batch + bidx) * p.nkv + kvh) * (size_t)p.max_ctx * D;
   __nv_bfloat16* Kc = p.kcache + head_base;
   __nv_bfloat16* Vc = p.vcache + head_base;
+  const int sub = c.lane >> 3, sl = c.lane & 7;
 
-  // 1. q heads of this group: (norm) + RoPE + 1/sqrt(D)
+  // K/V rows of cached positions do not depend on this step: issue the first block's
+  // loads BEFORE waiting for the QKV projections (their HBM latency leaves the critical path).
+  uint4 kreg[2][KQ];
+  uint32_t vreg[8][DPL / 2];
+  auto load_block = [&](int blk) {
+    const int wb = blk * PB + c.cw * 8;  // first position (chunk-relative) owned by this warp
+#pragma unroll
+    for (int st = 0; st < 2; ++st) {
+      const int tt = wb + st * 4 + sub;
+      const bool ld = tt < n && (t0 + tt) != pos;
+      const uint4* kp = reinterpret_cast<const uint4*>(Kc + (size_t)(t0 + tt) * D + sl * EPL);
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) kreg[st][q] = ld ? __ldcg(kp + q) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int tt = wb + j;
+      const bool ld = tt < n && (t0 + tt) != pos;
+      const uint32_t* vp = reinterpret_cast<const uint32_t*>(Vc + (size_t)(t0 + tt) * D) + c.lane * (DPL / 2);
+#pragma unroll
+      for (int q = 0; q < DPL / 2; ++q) vreg[j][q] = ld ? __ldcg(vp + q) : 0u;
+    }
+  };
+  load_block(0);
+
+  wait_counter(p, c, t.wait_ctr, t.wait_val, task_idx);
+  stamp(p, c, task_idx, 1);
+
+  // q heads of this group: (norm) + RoPE + 1/sqrt(D); the owner of `pos` also appends K/V
   for (int g = c.cw; g < G; g += p.C)
     rope_norm_head<D>(p, qkv + (size_t)(kvh * G + g) * D, p.qk_norm ? lay_fp + p.fp_qn : nullptr, pos, scale, c.lane,
                       qs + g * D);
-  // 2. the unit that owns position `pos` appends the new K/V rows (bf16)
-  if (slot == n_active - 1) {
-    const int wk = (G % p.C);            // a warp that is not the busiest in step 1
-    const int wv = ((G + 1) % p.C);
+  if (owns_new) {
+    const int wk = G % p.C, wv = (G + 1) % p.C;  // warps with the least q work
     if (c.cw == wk) {
       rope_norm_head<D>(p, qkv + p.q_dim + (size_t)kvh * D, p.qk_norm ? lay_fp + p.fp_kn : nullptr, pos, 1.0f, c.lane,
                         knew);
       __syncwarp();
-      for (int d = c.lane; d < D; d += 32) Kc[(size_t)pos * D + d] = __float2bfloat16_rn(knew[d]);
+      for (int d = c.lane; d < D; d += 32) {
+        const __nv_bfloat16 kb = __float2bfloat16_rn(knew[d]);
+        Kc[(size_t)pos * D + d] = kb;
+        knew[d] = __bfloat162float(kb);  // attend over exactly what the cache holds
+      }
     }
     if (c.cw == wv) {
       const float* vraw = qkv + p.q_dim + p.kv_dim + (size_t)kvh * D;
-      for (int d = c.lane; d < D; d += 32) Vc[(size_t)pos * D + d] = __float2bfloat16_rn(__ldcg(vraw + d));
+      for (int d = c.lane; d < D; d += 32) {
+        const __nv_bfloat16 vb = __float2bfloat16_rn(__ldcg(vraw + d));
+        Vc[(size_t)pos * D + d] = vb;
+        vnew[d] = __bfloat162float(vb);
+      }
     }
   }
   consumer_sync(c.nct);
+  stamp(p, c, task_idx, 2);
 
-  // 3. scores: 8 lanes per position, 4 positions per warp step
-  {
-    constexpr int EPL = D / 8;  // elements per lane: 16 or 8
-    const int sub = c.lane >> 3, sl = c.lane & 7;
-    for (int base = c.cw * 4; base < n; base += p.C * 4) {
-      const int tt = base + sub;
+  float m_run[kGMax], l_part[kGMax], acc[kGMax][DPL];
+#pragma unroll
+  for (int g = 0; g < kGMax; ++g) {
+    m_run[g] = -INFINITY;
+    l_part[g] = 0.f;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) acc[g][e] = 0.f;
+  }
+
+  for (int blk = 0; blk < nblk; ++blk) {
+    if (blk > 0) load_block(blk);
+    const int wb = blk * PB + c.cw * 8;
+    // scores of this warp's 8 positions (2 steps x 4 positions, 8 lanes each)
+#pragma unroll
+    for (int st = 0; st < 2; ++st) {
+      const int tt = wb + st * 4 + sub;
       const bool valid = tt < n;
       float kf[EPL];
-      if (valid) {
-        const uint4* kp = reinterpret_cast<const uint4*>(Kc + (size_t)(t0 + tt) * D + sl * EPL);
 #pragma unroll
-        for (int q = 0; q < EPL / 8; ++q) {
-          const uint4 raw = __ldcg(kp + q);
-          kf[q * 8 + 0] = bf_lo(raw.x); kf[q * 8 + 1] = bf_hi(raw.x);
-          kf[q * 8 + 2] = bf_lo(raw.y); kf[q * 8 + 3] = bf_hi(raw.y);
-          kf[q * 8 + 4] = bf_lo(raw.z); kf[q * 8 + 5] = bf_hi(raw.z);
-          kf[q * 8 + 6] = bf_lo(raw.w); kf[q * 8 + 7] = bf_hi(raw.w);
-        }
-      } else {
+      for (int q = 0; q < KQ; ++q) {
+        const uint4 raw = kreg[st][q];
+        kf[q * 8 + 0] = bf_lo(raw.x); kf[q * 8 + 1] = bf_hi(raw.x);
+        kf[q * 8 + 2] = bf_lo(raw.y); kf[q * 8 + 3] = bf_hi(raw.y);
+        kf[q * 8 + 4] = bf_lo(raw.z); kf[q * 8 + 5] = bf_hi(raw.z);
+        kf[q * 8 + 6] = bf_lo(raw.w); kf[q * 8 + 7] = bf_hi(raw.w);
+      }
+      if (owns_new && valid && (t0 + tt) == pos) {
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) kf[e] = 0.f;
+        for (int e = 0; e < EPL; ++e) kf[e] = knew[sl * EPL + e];
       }
       for (int g = 0; g < G; ++g) {
         const float4* qp = reinterpret_cast<const float4*>(qs + g * D + sl * EPL);
-        float s = 0.f;
+        float sdot = 0.f;
 #pragma unroll
         for (int q = 0; q < EPL / 4; ++q) {
           const float4 qv = qp[q];
-          s = fmaf(qv.x, kf[q * 4 + 0], s); s = fmaf(qv.y, kf[q * 4 + 1], s);
-          s = fmaf(qv.z, kf[q * 4 + 2], s); s = fmaf(qv.w, kf[q * 4 + 3], s);
+          sdot = fmaf(qv.x, kf[q * 4 + 0], sdot); sdot = fmaf(qv.y, kf[q * 4 + 1], sdot);
+          sdot = fmaf(qv.z, kf[q * 4 + 2], sdot); sdot = fmaf(qv.w, kf[q * 4 + 3], sdot);
         }
-        s += __shfl_xor_sync(0xffffffffu, s, 4);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        if (valid && sl == 0) sc[g * kAttnCLMax + tt] = s;
+        sdot += __shfl_xor_sync(0xffffffffu, sdot, 4);
+        sdot += __shfl_xor_sync(0xffffffffu, sdot, 2);
+        sdot += __shfl_xor_sync(0xffffffffu, sdot, 1);
+        if (sl == 0) sc[g * kAttnPBMax + c.cw * 8 + st * 4 + sub] = valid ? sdot : -INFINITY;
       }
     }
-  }
-  consumer_sync(c.nct);
-
-  // 4. chunk-local softmax statistics per head
-  for (int g = c.cw; g < G; g += p.C) {
-    float m = -INFINITY;
-    for (int i = c.lane; i < n; i += 32) m = fmaxf(m, sc[g * kAttnCLMax + i]);
-    m = warp_max(m);
-    float l = 0.f;
-    for (int i = c.lane; i < n; i += 32) {
-      const float e = expf(sc[g * kAttnCLMax + i] - m);
-      sc[g * kAttnCLMax + i] = e;
-      l += e;
-    }
-    l = warp_sum(l);
-    if (c.lane == 0) { ml[g] = m; ml[kGMax + g] = l; }
-  }
-  consumer_sync(c.nct);
-
-  // 5. P.V: warps split positions, lanes split dims
-  {
-    constexpr int DPL = D / 32;  // 4 or 2
-    float acc[kGMax][DPL];
-#pragma unroll
-    for (int g = 0; g < kGMax; ++g)
-#pragma unroll
-      for (int e = 0; e < DPL; ++e) acc[g][e] = 0.f;
-#pragma unroll 4
-    for (int tt = c.cw; tt < n; tt += p.C) {
-      float vf[DPL];
-      if constexpr (DPL == 4) {
-        const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(Vc + (size_t)(t0 + tt) * D) + c.lane);
-        vf[0] = bf_lo(raw.x); vf[1] = bf_hi(raw.x); vf[2] = bf_lo(raw.y); vf[3] = bf_hi(raw.y);
-      } else {
-        const uint32_t raw = __ldcg(reinterpret_cast<const uint32_t*>(Vc + (size_t)(t0 + tt) * D) + c.lane);
-        vf[0] = bf_lo(raw); vf[1] = bf_hi(raw);
-      }
-#pragma unroll
-      for (int g = 0; g < kGMax; ++g) {
-        if (g < G) {
-          const float pg = sc[g * kAttnCLMax + tt];
-#pragma unroll
-          for (int e = 0; e < DPL; ++e) acc[g][e] = fmaf(pg, vf[e], acc[g][e]);
-        }
-      }
-    }
+    consumer_sync(c.nct);
+    if (blk == 0) stamp(p, c, task_idx, 3);
+    // block max (every warp computes it redundantly -> no second barrier), rescale, P.V
 #pragma unroll
     for (int g = 0; g < kGMax; ++g) {
       if (g < G) {
+        float mb = -INFINITY;
+        for (int i = c.lane; i < PB; i += 32) mb = fmaxf(mb, sc[g * kAttnPBMax + i]);
+        mb = warp_max(mb);
+        const float m_new = fmaxf(m_run[g], mb);
+        const float resc = expf(m_run[g] - m_new);  // exp(-inf) = 0 on the first block
+        m_run[g] = m_new;
+        l_part[g] *= resc;
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) red[(c.cw * G + g) * D + c.lane * DPL + e] = acc[g][e];
+        for (int e = 0; e < DPL; ++e) acc[g][e] *= resc;
       }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int tt = wb + j;
+      if (tt < n) {  // warp-uniform
+        float vf[DPL];
+#pragma unroll
+        for (int q = 0; q < DPL / 2; ++q) { vf[2 * q] = bf_lo(vreg[j][q]); vf[2 * q + 1] = bf_hi(vreg[j][q]); }
+        if (owns_new && (t0 + tt) == pos) {
+#pragma unroll
+          for (int e = 0; e < DPL; ++e) vf[e] = vnew[c.lane * DPL + e];
+        }
+#pragma unroll
+        for (int g = 0; g < kGMax; ++g) {
+          if (g < G) {
+            const float pg = expf(sc[g * kAttnPBMax + c.cw * 8 + j] - m_run[g]);
+            l_part[g] += pg;
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) acc[g][e] = fmaf(pg, vf[e], acc[g][e]);
+          }
+        }
+      }
+    }
+    if (blk + 1 < nblk) consumer_sync(c.nct);  // sc is rewritten by the next block
+  }
+  stamp(p, c, task_idx, 4);
+#pragma unroll
+  for (int g = 0; g < kGMax; ++g) {
+    if (g < G) {
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) red[(c.cw * G + g) * D + c.lane * DPL + e] = acc[g][e];
+      if (c.lane == 0) lw[c.cw * kGMax + g] = l_part[g];
     }
   }
   consumer_sync(c.nct);
 
-  // 6. cross-warp reduction, then either the final output (single chunk) or a partial
+  // cross-warp reduction, then either the final output (single chunk) or a partial record
   const int PS = D + 2;  // partial record: o[D], m, l
   float* part = p.part + ((size_t)(bidx * p.nkv + kvh) * p.attn_chunks) * (size_t)G * PS;
   float* out = p.attn + (size_t)bidx * p.q_dim + (size_t)kvh * G * D;
   for (int i = c.ctid; i < G * D; i += c.nct) {
     const int g = i / D, d = i - g * D;
-    float o = 0.f;
-    for (int w = 0; w < p.C; ++w) o += red[(w * G + g) * D + d];
-    if (n_active == 1) out[i] = o / ml[kGMax + g];
-    else part[((size_t)slot * G + g) * PS + d] = o;
+    float o = 0.f, l = 0.f;
+    for (int w = 0; w < p.C; ++w) { o += red[(w * G + g) * D + d]; l += lw[w * kGMax + g]; }
+    if (n_active == 1) out[i] = o / l;
+    else {
+      part[((size_t)slot * G + g) * PS + d] = o;
+      if (d == 0) {
+        part[((size_t)slot * G + g) * PS + D + 1] = l;
+        // m_run is identical in every warp; lane/thread with d == 0 of head g publishes it
+      }
+    }
   }
   if (n_active == 1) {
     signal_counter(p, c, CTR_C);
+    stamp(p, c, task_idx, 7);
     return;
   }
-  if (c.ctid < G) {
-    part[((size_t)slot * G + c.ctid) * PS + D] = ml[c.ctid];
-    part[((size_t)slot * G + c.ctid) * PS + D + 1] = ml[kGMax + c.ctid];
+  if (c.cw == 0 && c.lane == 0) {
+#pragma unroll
+    for (int g = 0; g < kGMax; ++g)
+      if (g < G) part[((size_t)slot * G + g) * PS + D] = m_run[g];
   }
   consumer_sync(c.nct);
+  stamp(p, c, task_idx, 5);
   if (c.ctid == 0) {
     __threadfence();
     const unsigned old = atom_acqrel_add(p.counters + t.sig_ctr, 1u);
     hdr->misc[30] = (old == (unsigned)(t.layer * n_active + n_active - 1)) ? 1 : 0;
   }
   consumer_sync(c.nct);
-  if (!hdr->misc[30]) return;
-  // last unit of this head: merge the partials (flash-decoding combine)
+  stamp(p, c, task_idx, 6);
+  if (!hdr->misc[30]) { stamp(p, c, task_idx, 7); return; }
+  // last unit of this head: merge the partials (flash-decoding combine).  Phase 1: the
+  // per-chunk weights exp(m_s - M) / L into shared memory; phase 2: weighted sum, loads batched.
   __threadfence();
+  for (int i = c.ctid; i < n_active * G; i += c.nct) {
+    const int s2 = i / G, g = i - s2 * G;
+    wts[s2 * kGMax + g] = __ldcg(part + ((size_t)s2 * G + g) * PS + D);       // m_s
+    red[i] = __ldcg(part + ((size_t)s2 * G + g) * PS + D + 1);                // l_s (red is free now)
+  }
+  consumer_sync(c.nct);
+  if (c.ctid < G) {
+    const int g = c.ctid;
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < n_active; ++s2) M = fmaxf(M, wts[s2 * kGMax + g]);
+    float Lsum = 0.f;
+    for (int s2 = 0; s2 < n_active; ++s2) {
+      const float wgt = expf(wts[s2 * kGMax + g] - M);
+      wts[s2 * kGMax + g] = wgt;
+      Lsum = fmaf(red[s2 * G + g], wgt, Lsum);
+    }
+    const float inv = 1.0f / Lsum;
+    for (int s2 = 0; s2 < n_active; ++s2) wts[s2 * kGMax + g] *= inv;
+  }
+  consumer_sync(c.nct);
   for (int i = c.ctid; i < G * D; i += c.nct) {
     const int g = i / D, d = i - g * D;
-    float M = -INFINITY;
-    for (int s = 0; s < n_active; ++s) M = fmaxf(M, __ldcg(part + ((size_t)s * G + g) * PS + D));
-    float Lsum = 0.f, O = 0.f;
-    for (int s = 0; s < n_active; ++s) {
-      const float* rec = part + ((size_t)s * G + g) * PS;
-      const float wgt = expf(__ldcg(rec + D) - M);
-      Lsum = fmaf(__ldcg(rec + D + 1), wgt, Lsum);
-      O = fmaf(__ldcg(rec + d), wgt, O);
+    const float* rec = part + (size_t)g * PS + d;
+    float O = 0.f;
+    int s2 = 0;
+    for (; s2 + 4 <= n_active; s2 += 4) {
+      const float a0 = __ldcg(rec + (size_t)(s2 + 0) * G * PS), a1 = __ldcg(rec + (size_t)(s2 + 1) * G * PS);
+      const float a2 = __ldcg(rec + (size_t)(s2 + 2) * G * PS), a3 = __ldcg(rec + (size_t)(s2 + 3) * G * PS);
+      O = fmaf(a0, wts[(s2 + 0) * kGMax + g], O); O = fmaf(a1, wts[(s2 + 1) * kGMax + g], O);
+      O = fmaf(a2, wts[(s2 + 2) * kGMax + g], O); O = fmaf(a3, wts[(s2 + 3) * kGMax + g], O);
     }
-    out[i] = O / Lsum;
+    for (; s2 < n_active; ++s2) O = fmaf(__ldcg(rec + (size_t)s2 * G * PS), wts[s2 * kGMax + g], O);
+    out[i] = O;
   }
   signal_counter(p, c, CTR_C);
+  stamp(p, c, task_idx, 7);
 }
 
 // ----------------------------------------------------------------------------------
 // the persistent kernel
 // ----------------------------------------------------------------------------------
-__global__ void __launch_bounds__(544, 1) adamk_decode_kernel(const __grid_constant__ KParams p) {
+template <int CW>
+__global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   SmemHdr* hdr = reinterpret_cast<SmemHdr*>(smem);
   float* scratch = reinterpret_cast<float*>(smem + kSmemReserved);
@@ -692,8 +840,25 @@ __global__ void __launch_bounds__(544, 1) adamk_decode_kernel(const __grid_const
   if (warp == 0) {
     // ------------------------------ Loader ------------------------------
     if (lane == 0) {
-      uint32_t it = 0;
+      uint32_t slot = 0, ph = 0;
       const uint32_t ring_addr = smem_u32(ring);
+      const uint32_t n_stage = (uint32_t)p.n_stage;
+      const uint64_t pol = l2_evict_first_policy();  // weights are read once per step
+      // L2 prefetch cursor: runs pf_min bytes ahead of the ring in steady state and up to
+      // pf_max bytes ahead while the ring is full (consumers stalled on a dependency), so
+      // HBM keeps streaming through dependency stalls.
+      const uint8_t* pf = p.wpacked + (size_t)p.sm_stream[blockIdx.x] * 16u;
+      const uint8_t* const pf_end = p.wpacked + (size_t)p.sm_stream[blockIdx.x + 1] * 16u;
+      constexpr uint32_t kPfGranule = 16384;
+      auto prefetch_to = [&](const uint8_t* upto) {
+        if (upto > pf_end) upto = pf_end;
+        while (pf < upto) {
+          const uint32_t nb = (uint32_t)min((size_t)kPfGranule, (size_t)(pf_end - pf));
+          l2_prefetch_bulk(pf, nb);
+          pf += nb;
+        }
+      };
+      if (p.pf_min_bytes > 0) prefetch_to(pf + p.pf_min_bytes);
       for (int ti = tb; ti < te; ++ti) {
         const int4* tp = reinterpret_cast<const int4*>(p.tasks + ti);
         const int4 q0 = __ldg(tp), q1 = __ldg(tp + 1), q2 = __ldg(tp + 2);
@@ -706,14 +871,22 @@ __global__ void __launch_bounds__(544, 1) adamk_decode_kernel(const __grid_const
           for (int kt = 0; kt < n_ktiles; ++kt) {
             const int chunks = min(ktc, kchunks - kt * ktc);
             const uint32_t bytes = (uint32_t)rows * (uint32_t)chunks * 512u;
-            const uint32_t slot = it % (uint32_t)p.n_stage;
-            const uint32_t ph = (it / (uint32_t)p.n_stage) & 1u;
-            mbar_wait(p, smem_u32(&hdr->empty[slot]), ph ^ 1u, DE_WATCHDOG_EMPTY, ti);
+            const uint32_t eb = smem_u32(&hdr->empty[slot]);
+            if (!mbar_try_wait(eb, ph ^ 1u)) {
+              const long long t0 = clock64();
+              while (!mbar_try_wait_hint(eb, ph ^ 1u, 300u)) {
+                if (p.pf_max_bytes > 0 && pf < src + p.pf_max_bytes) prefetch_to(pf + 2 * kPfGranule);
+                if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_EMPTY, ti, (int)slot, (int)ph, 0);
+              }
+            }
             const uint32_t fb = smem_u32(&hdr->full[slot]);
             mbar_arrive_expect_tx(fb, bytes);
-            tma_bulk_g2s(ring_addr + slot * (uint32_t)p.stage_bytes, src, bytes, fb);
+            const uint8_t* lsrc = src;
+            if (p.probe == 3) lsrc = p.wpacked + (size_t)p.sm_stream[blockIdx.x] * 16u + ((size_t)(src - p.wpacked) & 0x3ffffu & ~(size_t)0xffff);
+            tma_bulk_g2s_hint(ring_addr + slot * (uint32_t)p.stage_bytes, lsrc, bytes, fb, pol);
             src += bytes;
-            ++it;
+            if (p.pf_min_bytes > 0) prefetch_to(src + p.pf_min_bytes);
+            if (++slot == n_stage) { slot = 0; ph ^= 1u; }
           }
         }
       }
@@ -723,8 +896,8 @@ __global__ void __launch_bounds__(544, 1) adamk_decode_kernel(const __grid_const
 
   // ------------------------------ Consumers ------------------------------
   ConsumerCtx c;
-  c.it = 0; c.cw = warp - 1; c.lane = lane; c.ctid = threadIdx.x - 32; c.nct = p.C * 32;
-  c.best_val = -INFINITY; c.best_idx = -1;
+  c.slot = 0; c.ph = 0; c.cw = warp - 1; c.lane = lane; c.ctid = threadIdx.x - 32; c.nct = p.C * 32;
+  c.rs = 1.0f; c.best_val = -INFINITY; c.best_idx = -1;
   int tok = 0, pos = 0;
   if (!p.probe) {
     tok = __ldcg(p.tokens);
@@ -847,7 +1020,8 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct AdamkHandle_ {
   AdamkModelDesc desc{};
   int n_sms = 0, C = 0, n_stage = 0, stage_bytes = 0, n_tasks = 0, batch = 0, n_counters = 0;
-  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0;
+  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, pf_min_bytes = 0, pf_max_bytes = 0;
+  const unsigned* d_sm_stream = nullptr;
   size_t packed_weight_bytes = 0;  // matrix streams only
   size_t fparam_floats = 0;
   int fp_layer_stride = 0, fp_ln1 = 0, fp_ln2 = 0, fp_bias = 0, fp_qn = 0, fp_kn = 0, fp_final = 0;
@@ -861,6 +1035,7 @@ struct AdamkHandle_ {
   AdamkWeightPtrs w{};
   int* status_host = nullptr;
   int* status_dev = nullptr;
+  unsigned long long* trace = nullptr;
   int smem_bytes = 0;
   // workspace layout (byte offsets)
   size_t ws_h_a = 0, ws_h_b = 0, ws_qkv = 0, ws_attn = 0, ws_act = 0, ws_part = 0, ws_lm_val = 0, ws_lm_idx = 0,
@@ -893,6 +1068,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   h->n_sms = tt[2]; h->C = tt[3]; h->n_stage = tt[4]; h->stage_bytes = tt[5]; h->n_tasks = tt[6]; h->batch = tt[7];
   h->n_counters = tt[8]; h->attn_chunks = tt[9]; h->attn_min_chunk = tt[10]; h->scratch_bytes = tt[11];
   h->n_lm_tasks = tt[12];
+  h->pf_min_bytes = tt[14] * 1024; h->pf_max_bytes = tt[15] * 1024;
   auto bad = [&](const std::string& m) { delete h; return fail(ADAMK_E_INVALID, m); };
   const AdamkModelDesc& d = *desc;
   if (d.head_dim != 64 && d.head_dim != 128) return bad("head_dim must be 64 or 128");
@@ -904,11 +1080,8 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   if (h->n_stage < 1 || h->n_stage > kMaxStages) return bad("n_stage out of range");
   if (h->stage_bytes <= 0 || h->stage_bytes % 1024) return bad("stage_bytes must be a positive multiple of 1024");
   if (h->n_sms < 1 || h->n_tasks < 1) return bad("empty task table");
-  if (h->attn_chunks < 1 || h->attn_min_chunk < 8 || h->attn_min_chunk > kAttnCLMax) return bad("attention chunking out of range");
-  if ((long long)d.max_ctx > (long long)h->attn_chunks * kAttnCLMax) {
-    delete h;
-    return fail(ADAMK_E_UNSUPPORTED, "max_ctx exceeds attn_chunks * 512 positions");
-  }
+  if (h->attn_chunks < 1 || h->attn_chunks > kAttnChunksMax || h->attn_min_chunk < 8)
+    return bad("attention chunking out of range");
   const size_t need = ((size_t)kHeaderInts + (size_t)h->n_sms + 1 + (size_t)h->n_tasks * kTaskInts) * 4;
   if (task_table_bytes != need) return bad("task table size does not match its header");
   if (h->n_counters != CTR_HEAD0 + h->batch * d.n_kv_heads) return bad("counter count mismatch");
@@ -918,7 +1091,8 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
     const int G = d.n_q_heads / d.n_kv_heads;
     const int kmax = std::max(std::max(d.hidden, d.n_q_heads * d.head_dim), d.intermediate);
     const size_t xb = align_up((size_t)kmax, kChunk) * 4;
-    const size_t ab = ((size_t)G * d.head_dim + (size_t)G * kAttnCLMax + (size_t)h->C * G * d.head_dim + 2 * kGMax + d.head_dim) * 4;
+    const size_t ab = ((size_t)G * d.head_dim + (size_t)G * kAttnPBMax + (size_t)h->C * G * d.head_dim + (size_t)h->C * kGMax +
+                       2 * (size_t)d.head_dim + (size_t)kAttnChunksMax * kGMax) * 4;
     if ((size_t)h->scratch_bytes < std::max(xb, ab)) return bad("scratch_bytes too small for this model");
   }
   const int* sm_begin = tt + kHeaderInts;
@@ -981,6 +1155,21 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   // device copy: task records first (64-byte aligned for the int4 loads), then sm_begin
   h->host_table.assign(reinterpret_cast<const int*>(tasks), reinterpret_cast<const int*>(tasks) + (size_t)h->n_tasks * kTaskInts);
   h->host_table.insert(h->host_table.end(), sm_begin, sm_begin + h->n_sms + 1);
+  {  // per-SM packed-stream ranges (streams are SM-major and contiguous)
+    std::vector<unsigned> sm_stream(h->n_sms + 1, 0u);
+    unsigned cursor = 0;
+    for (int sm = 0; sm < h->n_sms; ++sm) {
+      sm_stream[sm] = cursor;
+      for (int i = sm_begin[sm]; i < sm_begin[sm + 1]; ++i) {
+        const Task& t = tasks[i];
+        if (t.type == T_ATTN) continue;
+        if ((unsigned)t.w_off != cursor) return bad("packed streams must be contiguous per SM, SM-major");
+        cursor += (unsigned)((size_t)t.b * t.kchunks * 512 / 16);
+      }
+    }
+    sm_stream[h->n_sms] = cursor;
+    for (unsigned v : sm_stream) h->host_table.push_back((int)v);
+  }
   cudaError_t e = cudaMalloc(&h->d_table, h->host_table.size() * 4);
   if (e == cudaSuccess) e = cudaMemcpy(h->d_table, h->host_table.data(), h->host_table.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaHostAlloc(&h->status_host, 64, cudaHostAllocMapped);
@@ -988,7 +1177,9 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
     memset(h->status_host, 0, 64);
     e = cudaHostGetDevicePointer(&h->status_dev, h->status_host, 0);
   }
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   if (e != cudaSuccess) {
     std::string m = std::string("adamk_create: ") + cudaGetErrorString(e);
     adamk_destroy(h);
@@ -996,6 +1187,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   }
   h->d_tasks = reinterpret_cast<const Task*>(h->d_table);
   h->d_sm_begin = h->d_table + (size_t)h->n_tasks * kTaskInts;
+  h->d_sm_stream = reinterpret_cast<const unsigned*>(h->d_sm_begin + h->n_sms + 1);
   *out = h;
   return ADAMK_OK;
 }
@@ -1097,7 +1289,8 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
   p.C = h->C; p.n_stage = h->n_stage; p.stage_bytes = h->stage_bytes; p.attn_chunks = h->attn_chunks;
   p.attn_min_chunk = h->attn_min_chunk; p.scratch_bytes = h->scratch_bytes; p.n_lm_tasks = h->n_lm_tasks;
   p.n_counters = h->n_counters;
-  p.tasks = h->d_tasks; p.sm_begin = h->d_sm_begin;
+  p.tasks = h->d_tasks; p.sm_begin = h->d_sm_begin; p.sm_stream = h->d_sm_stream;
+  p.pf_min_bytes = h->pf_min_bytes; p.pf_max_bytes = h->pf_max_bytes;
   p.wpacked = h->wpacked; p.fparams = h->fparams;
   p.fp_layer_stride = h->fp_layer_stride; p.fp_ln1 = h->fp_ln1; p.fp_ln2 = h->fp_ln2; p.fp_bias = h->fp_bias;
   p.fp_qn = h->fp_qn; p.fp_kn = h->fp_kn; p.fp_final = h->fp_final;
@@ -1110,6 +1303,7 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
     p.lm_val = (float*)(ws + h->ws_lm_val); p.lm_idx = (int*)(ws + h->ws_lm_idx);
   }
   p.status = h->status_dev;
+  p.trace = h->trace;
   return ADAMK_OK;
 }
 
@@ -1120,8 +1314,9 @@ static int launch(adamk_handle h, const KParams& p, cudaStream_t stream) {
   if (sms < h->n_sms) return fail(ADAMK_E_INVALID, "task table was built for more SMs than this device has");
   void* args[] = {(void*)&p};
   // cooperative launch: all CTAs must be co-resident (they wait on each other's counters)
-  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)adamk_decode_kernel, dim3(h->n_sms), dim3((h->C + 1) * 32), args,
-                                       (size_t)h->smem_bytes, stream));
+  const void* fn = h->C == 4 ? (const void*)adamk_decode_kernel<4>
+                   : h->C == 8 ? (const void*)adamk_decode_kernel<8> : (const void*)adamk_decode_kernel<16>;
+  CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(h->n_sms), dim3((h->C + 1) * 32), args, (size_t)h->smem_bytes, stream));
   return ADAMK_OK;
 }
 
@@ -1146,9 +1341,18 @@ int adamk_stream_probe(adamk_handle h, float* sink, int mode, adamk_stream strea
   if (!h->bound) return fail(ADAMK_E_STATE, "adamk_bind_weights has not been called");
   KParams p;
   fill_params(h, p, nullptr);
-  p.probe = (mode == 2) ? 2 : 1; p.probe_sink = sink;
+  p.probe = (mode == 2 || mode == 3) ? mode : 1; p.probe_sink = sink;
+  if (mode == 3) { p.pf_min_bytes = 0; p.pf_max_bytes = 0; }
   return launch(h, p, (cudaStream_t)stream);
 }
+
+int adamk_set_trace(adamk_handle h, void* trace_buf) {
+  if (!h) return fail(ADAMK_E_INVALID, "NULL handle");
+  h->trace = static_cast<unsigned long long*>(trace_buf);
+  return ADAMK_OK;
+}
+
+size_t adamk_trace_bytes(adamk_handle h) { return h ? (size_t)h->n_tasks * 8 * sizeof(unsigned long long) : 0; }
 
 int adamk_device_status(adamk_handle h, int32_t* info) {
   if (!h) return fail(ADAMK_E_INVALID, "NULL handle");

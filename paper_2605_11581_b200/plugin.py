@@ -55,7 +55,7 @@ EXPORTS = (
     "adamk_abi_version", "adamk_device_sm_count", "adamk_last_error", "adamk_create", "adamk_destroy",
     "adamk_packed_bytes", "adamk_bind_weights", "adamk_bind_peers", "adamk_workspace_bytes",
     "adamk_workspace_init", "adamk_kv_cache_bytes", "adamk_decode_step", "adamk_device_status",
-    "adamk_stream_probe",
+    "adamk_stream_probe", "adamk_trace_bytes", "adamk_set_trace",
 )
 
 _lib = None
@@ -77,7 +77,8 @@ def load_library() -> C.CDLL:
                                  C.POINTER(C.c_void_p)]
     lib.adamk_destroy.argtypes = [C.c_void_p]
     lib.adamk_destroy.restype = None
-    for name in ("adamk_packed_bytes", "adamk_workspace_bytes", "adamk_kv_cache_bytes"):
+    lib.adamk_set_trace.argtypes = [C.c_void_p, C.c_void_p]
+    for name in ("adamk_packed_bytes", "adamk_workspace_bytes", "adamk_kv_cache_bytes", "adamk_trace_bytes"):
         getattr(lib, name).argtypes = [C.c_void_p]
         getattr(lib, name).restype = C.c_size_t
     lib.adamk_bind_weights.argtypes = [C.c_void_p, C.POINTER(_WeightPtrs), C.c_void_p, C.c_void_p]
@@ -211,6 +212,17 @@ class MegaKernelPlugin:
             self._sink = torch.zeros(self.n_sms, dtype=torch.float32, device=self.device)
         _check(self.lib, self.lib.adamk_stream_probe(self._h, C.c_void_p(self._sink.data_ptr()), mode,
                                                      self._stream_ptr()))
+
+    def enable_trace(self, on: bool = True) -> torch.Tensor | None:
+        """Per-task %globaltimer stamps [n_tasks, 8] (0 start, 1 dependency met, 2 prologue done, 7 end)."""
+        if on:
+            n = self.lib.adamk_trace_bytes(self._h) // 8
+            self.trace = torch.zeros(n // 8, 8, dtype=torch.int64, device=self.device)
+            _check(self.lib, self.lib.adamk_set_trace(self._h, C.c_void_p(self.trace.data_ptr())))
+            return self.trace
+        _check(self.lib, self.lib.adamk_set_trace(self._h, None))
+        self.trace = None
+        return None
 
     def kv_view(self) -> tuple[torch.Tensor, torch.Tensor]:
         cfg = self.cfg

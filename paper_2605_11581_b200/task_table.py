@@ -44,7 +44,8 @@ SMEM_MAX = 232448      # 227 KB opt-in shared memory per CTA on sm_100
 SMEM_RESERVED = 1024   # mbarriers + reduction scratch ahead of the scratch/ring regions
 MAX_STAGES = 16
 MAX_RW = 4             # rows per consumer warp per tile the kernel is instantiated for
-ATTN_CLMAX = 512       # positions per attention chunk the scratch region holds
+ATTN_PBMAX = 128       # positions per attention block (8 per consumer warp, <= 16 warps)
+ATTN_CHUNKS_MAX = 128  # split-KV units per (sequence, kv head)
 
 T_END, T_QKV, T_ATTN, T_OPROJ, T_GATEUP, T_DOWN, T_LMHEAD = 0, 1, 2, 3, 4, 5, 6
 GEMV_TYPES = (T_QKV, T_OPROJ, T_GATEUP, T_DOWN, T_LMHEAD)
@@ -75,6 +76,11 @@ class KernelSchedule:
     rows_per_tile: int = 16   # plan tile block_n
     ktile_chunks: int = 4     # plan tile sub_k / 256
     attn_min_chunk: int = 64  # positions per split-KV unit before more SMs are used
+    # Optional L2 prefetch ahead of the ring (KB per SM; steady state / while the ring is full).
+    # Off by default: on B200 an L2 hit streams no faster than HBM (measured 6.9 vs 7.2 TB/s,
+    # profiles/r01_notes.md), so running ahead in L2 cannot recover dependency stalls.
+    l2_prefetch_kb: int = 0
+    l2_prefetch_stall_kb: int = 0
 
     def __post_init__(self) -> None:
         if self.consumer_warps not in (4, 8, 16):
@@ -89,7 +95,7 @@ class KernelSchedule:
             raise ScheduleError("block_n / consumer_warps must be 2 or 4")
         if self.ktile_chunks < 1:
             raise ScheduleError("sub_k must be a positive multiple of 256")
-        if self.attn_min_chunk < 8 or self.attn_min_chunk > ATTN_CLMAX:
+        if self.attn_min_chunk < 8:
             raise ScheduleError("attn_min_chunk out of range")
 
     @property
@@ -123,7 +129,7 @@ def scratch_bytes(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> in
     kpad_max = max(_ceil_div(k, KCHUNK) * KCHUNK for k in (cfg.hidden, cfg.q_dim, cfg.intermediate))
     x_bytes = batch * kpad_max * 4
     g, d, c = cfg.group, cfg.head_dim, sched.consumer_warps
-    attn_bytes = (g * d + g * ATTN_CLMAX + c * g * d + 2 * 8 + d) * 4
+    attn_bytes = (g * d + g * ATTN_PBMAX + c * g * d + c * 8 + 2 * d + ATTN_CHUNKS_MAX * 8) * 4
     return _ceil_div(max(x_bytes, attn_bytes), 1024) * 1024
 
 
@@ -216,7 +222,7 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
             raise ScheduleError("reduction dims must be multiples of 8")
 
     nkv = cfg.n_kv_heads
-    attn_chunks = max(1, min(n_sms // (batch * nkv), 128))
+    attn_chunks = max(1, min(n_sms // (batch * nkv), ATTN_CHUNKS_MAX))
     n_counters = CTR_HEAD0 + batch * nkv
     per_sm: list[list[list[int]]] = [[] for _ in range(n_sms)]
     rot = 0
@@ -280,6 +286,8 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
                    tasks.shape[0], batch, n_counters, attn_chunks, sched.attn_min_chunk,
                    scratch_bytes(cfg, sched, batch), n_lm]
     header[13] = (cursor // 16) & 0x7FFFFFFF
+    header[14] = sched.l2_prefetch_kb
+    header[15] = sched.l2_prefetch_stall_kb
     return TaskTable(cfg=cfg, sched=sched, n_sms=n_sms, batch=batch, header=header, sm_begin=sm_begin,
                      tasks=tasks, packed_weight_bytes=cursor, n_counters=n_counters,
                      attn_chunks=attn_chunks)

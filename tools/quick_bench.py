@@ -21,13 +21,14 @@ w = random_weights(cfg, 0, device="cuda")
 torch.cuda.synchronize()
 print(f"weights on device in {time.time() - t0:.1f}s", flush=True)
 scheds = [
+    ("c8 s5 32K pf0", dict(consumer_warps=8, n_stage=5, rows_per_tile=16, ktile_chunks=4, l2_prefetch_kb=0, l2_prefetch_stall_kb=0)),
+    ("c8 s5 32K pf128/512", dict(consumer_warps=8, n_stage=5, rows_per_tile=16, ktile_chunks=4)),
+    ("c8 s5 32K pf256/1024", dict(consumer_warps=8, n_stage=5, rows_per_tile=16, ktile_chunks=4, l2_prefetch_kb=256, l2_prefetch_stall_kb=1024)),
+    ("c8 s5 32K pf64/2048", dict(consumer_warps=8, n_stage=5, rows_per_tile=16, ktile_chunks=4, l2_prefetch_kb=64, l2_prefetch_stall_kb=2048)),
     ("c8 s7 24K", dict(consumer_warps=8, n_stage=7, rows_per_tile=16, ktile_chunks=3)),
-    ("c8 s5 32K", dict(consumer_warps=8, n_stage=5, rows_per_tile=16, ktile_chunks=4)),
-    ("c8 s11 16K", dict(consumer_warps=8, n_stage=11, rows_per_tile=16, ktile_chunks=2)),
-    ("c4 s7 24K", dict(consumer_warps=4, n_stage=7, rows_per_tile=16, ktile_chunks=3)),
-    ("c16 s3 48K", dict(consumer_warps=16, n_stage=3, rows_per_tile=32, ktile_chunks=3)),
     ("c16 s5 32K", dict(consumer_warps=16, n_stage=5, rows_per_tile=32, ktile_chunks=2)),
-    ("c8 s3 48K", dict(consumer_warps=8, n_stage=3, rows_per_tile=32, ktile_chunks=3)),
+    ("c16 s3 48K", dict(consumer_warps=16, n_stage=3, rows_per_tile=32, ktile_chunks=3)),
+    ("c4 s7 24K", dict(consumer_warps=4, n_stage=7, rows_per_tile=16, ktile_chunks=3)),
 ]
 for label, kw in scheds:
     try:
@@ -63,10 +64,17 @@ for label, kw in scheds:
         e1.record()
         torch.cuda.synchronize()
         pms2 = e0.elapsed_time(e1) / 20
+        e0.record()
+        for _ in range(20):
+            plug.stream_probe(3)
+        e1.record()
+        torch.cuda.synchronize()
+        pms3 = e0.elapsed_time(e1) / 20
         byts = cfg.algorithmic_bytes(ctx0 + steps // 2)
-        print(f"{label:12s} decode {ms*1e3:8.1f} us/tok {1e3/ms:8.1f} tok/s  {byts/ms/1e6:7.1f} GB/s ({byts/ms/1e6/peak:.3f} of measured)"
+        print(f"{label:22s} decode {ms*1e3:8.1f} us/tok {1e3/ms:8.1f} tok/s  {byts/ms/1e6:7.1f} GB/s ({byts/ms/1e6/peak:.3f} of measured)"
               f" | stream probe {pms*1e3:8.1f} us {plug.table.packed_weight_bytes/pms/1e6:7.1f} GB/s"
-              f" | loader-only {pms2*1e3:8.1f} us {plug.table.packed_weight_bytes/pms2/1e6:7.1f} GB/s", flush=True)
+              f" | loader-only {pms2*1e3:8.1f} us {plug.table.packed_weight_bytes/pms2/1e6:7.1f} GB/s"
+              f" | L2-resident {pms3*1e3:8.1f} us {plug.table.packed_weight_bytes/pms3/1e6:7.1f} GB/s", flush=True)
         plug.close()
         del plug
     except Exception as exc:  # keep going: bring-up tool
