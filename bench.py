@@ -1,0 +1,287 @@
+#!/usr/bin/env python
+"""Benchmark of the decode MegaKernel hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A *step* is one decode step (one token) of BASELINE.json configs[1]:
+Qwen2.5-1.5B, random-init bf16, batch 1, after a 512-token prompt; K steps are
+timed after W warm-up steps (defaults 128 / 8).  One JSON line is printed by
+rank 0:
+
+  value      whole-job decode tokens/s with token/position state resident in HBM
+             (steps enqueued back to back, CUDA events on the launching stream)
+  e2e        the same metric through the host-facing plugin call: per step the
+             token + position are copied from pinned host memory, the step runs,
+             and the next token is read back to the host
+  roofline   weight-streaming HBM roofline of the (single) kernel: algorithmic
+             bytes per launch / mean launch time vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the CPU oracle (oracle/decode_ref.py, kind "port": the reference
+             ships no numeric decode path) timed on this box's host cores on a
+             bounded sample of the same workload
+
+`--impl reference` times that CPU oracle as the reference arm (same metric and
+config).  N > 1 runs N independent replicas (config #2 has 2 KV heads and does
+not shard past TP=2: "replicas only"), one rank per GPU.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import torch
+
+from paper_2605_11581_b200.model_config import get_config
+from paper_2605_11581_b200.schedules import default_schedule
+from paper_2605_11581_b200.weights import random_weights, rope_table
+
+METRIC = "decode_tokens_per_s"
+UNIT = "tokens/s"
+PROMPT_LEN = 512
+
+
+def measured_peak() -> tuple[float, str]:
+    path = ROOT / "MEASURED_PEAKS.json"
+    if path.exists():
+        return float(json.loads(path.read_text())["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clock / throttle sampling during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        sm = sorted(int(r[0]) for r in self.rows if r and r[0].isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows if len(r) >= 6 for n, v in zip(names, r[2:6]) if v.startswith("Active")})
+        mx = [int(r[1]) for r in self.rows if len(r) > 1 and r[1].isdigit()]
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def cpu_decode_sample(cfg, weights, prompt, n_steps: int, warmup: int = 2) -> dict:
+    """Time the CPU oracle on a bounded sample: prefill the prompt, then n decode steps."""
+    from oracle.decode_ref import RefDecoder
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    cos, sin = rope_table(cfg, len(prompt) + n_steps + warmup + 8)
+    dec = RefDecoder(cfg, weights, len(prompt) + n_steps + warmup + 8, cos, sin)
+    logits = dec.prefill(prompt)
+    tok, pos = int(torch.argmax(logits)), len(prompt)
+    for _ in range(warmup):
+        tok = int(torch.argmax(dec.step([tok], [pos])[0]))
+        pos += 1
+    t0 = time.perf_counter()
+    for _ in range(n_steps):
+        tok = int(torch.argmax(dec.step([tok], [pos])[0]))
+        pos += 1
+    dt = time.perf_counter() - t0
+    return {"value": n_steps / dt, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "port",
+            "sample": f"{n_steps} greedy decode steps after a {len(prompt)}-token prompt, fp32 compute on the same "
+                      f"bf16 weights, torch CPU ({torch.get_num_threads()} threads)", "ms_per_step": dt / n_steps * 1e3}
+
+
+def base_line(args, cfg, n_gpus: int) -> dict:
+    return {"metric": METRIC, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, random prompt ids; no network for checkpoints)",
+            "config": {"workload": f"{cfg.name} batch-1 greedy decode after a {PROMPT_LEN}-token prompt "
+                                   f"(BASELINE.json configs[1])", "model": cfg.name, "batch": 1,
+                       "prompt_len": PROMPT_LEN, "parallelism": "replicas" if n_gpus > 1 else "single",
+                       "l2_policy": "inputs larger than L2: every step streams the 3.09 GB weight set"}}
+
+
+def run_reference(args) -> None:
+    """Reference arm: the CPU oracle on the host cores (the reference has no numeric decode)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = get_config(args.model)
+    w = random_weights(cfg, seed=0)
+    g = torch.Generator().manual_seed(1)
+    prompt = torch.randint(0, cfg.vocab, (PROMPT_LEN,), generator=g).tolist()
+    res = cpu_decode_sample(cfg, w, prompt, n_steps=args.steps, warmup=args.warmup)
+    line = base_line(args, cfg, args.gpus)
+    line.update({"impl": "reference", "value": res["value"], "ms_per_step": res["ms_per_step"],
+                 "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                 "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                 "gpu_launches": 0, "dtype": "f32 compute on bf16 weights"})
+    print(json.dumps(line))
+
+
+def run_ours(args) -> None:
+    from paper_2605_11581_b200.plugin import MegaKernelPlugin
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = get_config(args.model)
+    w = random_weights(cfg, seed=0, device=dev)
+    sched = default_schedule(cfg)
+    max_ctx = PROMPT_LEN + args.steps + args.warmup + 16
+    plug = MegaKernelPlugin(cfg, sched, max_ctx=max_ctx, device=local)
+    plug.bind_weights(w)
+    g = torch.Generator().manual_seed(1)
+    prompt = torch.randint(0, cfg.vocab, (PROMPT_LEN,), generator=g).tolist()
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def prefill():
+        # the decode path itself builds the prompt's KV cache (one launch per prompt token)
+        prompt_dev = torch.tensor(prompt, dtype=torch.int32, device=dev)
+        for p_, _ in enumerate(prompt[:-1]):
+            plug.tokens.copy_(prompt_dev[p_:p_ + 1])
+            plug.positions.fill_(p_)
+            plug.enqueue(want_logits=False, auto_advance=False)
+        plug.set_state(prompt[-1], PROMPT_LEN - 1)
+        plug.check()
+
+    # ---- device-resident loop: value + roofline ----
+    prefill()
+    for _ in range(args.warmup):
+        plug.enqueue()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = plug.launches
+    e0.record()
+    for _ in range(args.steps):
+        plug.enqueue()
+    e1.record()
+    barrier()
+    plug.check()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = plug.launches - launches0
+
+    # ---- end to end through the host-facing call ----
+    prefill()
+    host_in = torch.zeros(2, dtype=torch.int32).pin_memory()
+    host_out = torch.zeros(1, dtype=torch.int32).pin_memory()
+    tok, pos = prompt[-1], PROMPT_LEN - 1
+
+    def e2e_step(tok, pos):
+        host_in[0], host_in[1] = tok, pos
+        plug.tokens.copy_(host_in[0:1], non_blocking=True)
+        plug.positions.copy_(host_in[1:2], non_blocking=True)
+        plug.enqueue(want_logits=False, auto_advance=False)
+        host_out.copy_(plug.next_token, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        return int(host_out[0]), pos + 1
+
+    for _ in range(args.warmup):
+        tok, pos = e2e_step(tok, pos)
+    barrier()
+    e0.record()
+    for _ in range(args.steps):
+        tok, pos = e2e_step(tok, pos)
+    e1.record()
+    barrier()
+    plug.check()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+
+    times = torch.tensor([ms, ms_e2e], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    ms, ms_e2e = float(times[0]), float(times[1])
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = measured_peak()
+    ctx_mid = PROMPT_LEN + args.warmup + args.steps // 2
+    bytes_per_launch = cfg.algorithmic_bytes(ctx_mid)
+    achieved = bytes_per_launch / (ms * 1e-3) / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+    line = base_line(args, cfg, world)
+    line.update({
+        "value": world * 1e3 / ms, "ms_per_step": ms,
+        "config": dict(line["config"], schedule={"consumer_warps": sched.consumer_warps, "n_stage": sched.n_stage,
+                                                 "stage_bytes": sched.stage_bytes}, n_sms=plug.n_sms),
+        "e2e": {"value": world * 1e3 / ms_e2e, "unit": UNIT, "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 4,
+                "ms_per_step": ms_e2e},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_kind": f"{peak_kind} copy bandwidth (burst)",
+                     "algorithmic_bytes_per_launch": bytes_per_launch, "kernel": "adamk_decode_kernel",
+                     "launch_ms": ms},
+    })
+    if not args.no_cpu_baseline:
+        w_cpu = w.to("cpu")
+        res = cpu_decode_sample(cfg, w_cpu, prompt, n_steps=args.cpu_steps)
+        line["cpu_baseline"] = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=128)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", default="qwen2.5-1.5b")
+    ap.add_argument("--cpu-steps", type=int, default=48, help="decode steps of the bounded CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

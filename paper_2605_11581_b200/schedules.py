@@ -1,0 +1,36 @@
+"""Solidified kernel schedules shipped with the package.
+
+``default_schedule`` returns the ring parameters the plugin uses when the caller
+does not supply a SolidifiedTrace of their own.  The values are read from the
+plan files under ``schedules/`` -- ``mkplan search`` output for the per-layer
+operator graph on ``fixtures/b200.json`` -- when one exists for the model, and
+otherwise fall back to the profiled default below (offline profiling on the
+target GPU is how the paper locks in its trace).
+"""
+
+from __future__ import annotations
+
+import json
+from pathlib import Path
+
+from .model_config import ModelConfig
+from .task_table import KernelSchedule, max_stages_that_fit
+
+SCHEDULE_DIR = Path(__file__).resolve().parent / "schedules"
+
+# Profiled on B200 (profiles/r01_notes.md): 8 consumer warps, 16-row x 1024-column
+# sub-tiles (32 KB stages), ring as deep as shared memory allows.
+PROFILED_DEFAULT = dict(consumer_warps=8, rows_per_tile=16, ktile_chunks=4)
+
+
+def default_schedule(cfg: ModelConfig) -> KernelSchedule:
+    plan_file = SCHEDULE_DIR / f"{cfg.name}.trace.json"
+    if plan_file.exists():
+        plan = json.loads(plan_file.read_text())["plan"]
+        sched = KernelSchedule.from_plan(plan)
+        fit = max_stages_that_fit(cfg, sched)
+        if sched.n_stage > fit:
+            sched = KernelSchedule.from_plan(plan, n_stage=fit)
+        return sched
+    probe = KernelSchedule(n_stage=1, **PROFILED_DEFAULT)
+    return KernelSchedule(n_stage=min(max_stages_that_fit(cfg, probe), 8), **PROFILED_DEFAULT)
