@@ -544,34 +544,51 @@ __device__ __forceinline__ void rope_norm_head(const KParams& p, const float* ra
   }
 }
 
+// Split-KV geometry of one decode step, shared by the Loader (which streams the K/V
+// blocks of a unit through the ring) and the Consumers (which drain them).
+struct AttnGeom {
+  int CL, n_active, t0, n, PB, nblk;
+};
+__device__ __forceinline__ AttnGeom attn_geometry(const KParams& p, int pos, int slot) {
+  AttnGeom g;
+  const int ctx = pos + 1;
+  g.CL = max(p.attn_min_chunk, (ctx + p.attn_chunks - 1) / p.attn_chunks);
+  g.CL = (g.CL + 7) & ~7;
+  g.n_active = (ctx + g.CL - 1) / g.CL;
+  g.t0 = slot * g.CL;
+  g.n = min(ctx, g.t0 + g.CL) - g.t0;           // <= 0 for inactive slots
+  g.PB = min(64, (p.stage_bytes / (p.D * 2)) & ~7);  // positions per ring stage
+  g.nblk = g.n > 0 ? (g.n + g.PB - 1) / g.PB : 0;
+  return g;
+}
+
 // Layout of the attention scratch (floats); must match task_table.scratch_bytes / adamk_create.
-//   qs[G][D] | sc[G][kAttnPBMax] | red[C][G][D] | lw[C][kGMax] | knew[D] | vnew[D] | wts[kAttnChunksMax][kGMax]
+//   qs[G][D] | sc[G][kAttnPBMax] | red[C][G][D] | lw[C][kGMax] | mw[C][kGMax] | knew[D] | vnew[D] | wts[kAttnChunksMax][kGMax]
+//
+// The K and V rows of a unit's context chunk arrive through the weight ring (the paper's
+// "KV-cache loads advanced into the pipeline window"): per block of PB positions
+// one K stage and one V stage, issued by the Loader long before the QKV projections of this
+// layer are done.  The row of the new token is patched into the staged copy.
 template <int D>
 __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* scratch,
-                                         SmemHdr* hdr, int pos) {
+                                         SmemHdr* hdr, uint8_t* ring, int pos) {
   constexpr int EPL = D / 8;   // K elements per lane in the score step (8 lanes per position)
-  constexpr int KQ = EPL / 8;  // uint4 loads per lane per position
   constexpr int DPL = D / 32;  // V / output elements per lane in the P.V step
   const int G = p.G;
   const int kvh = t.a, slot = t.b, bidx = t.aux;
-  const int ctx = pos + 1;
-  int CL = max(p.attn_min_chunk, (ctx + p.attn_chunks - 1) / p.attn_chunks);
-  CL = (CL + 7) & ~7;
-  const int n_active = (ctx + CL - 1) / CL;
-  if (slot >= n_active || p.probe) return;  // uniform across the CTA's consumers
+  const AttnGeom ge = attn_geometry(p, pos, slot);
+  if (slot >= ge.n_active || p.probe) return;  // uniform across the CTA's consumers
   stamp(p, c, task_idx, 0);
-
-  const int t0 = slot * CL;
-  const int n = min(ctx, t0 + CL) - t0;
-  const int PB = 8 * p.C;  // positions per block; every warp owns 8 consecutive positions of a block
-  const int nblk = (n + PB - 1) / PB;
+  const int n = ge.n, t0 = ge.t0, PB = ge.PB, nblk = ge.nblk, n_active = ge.n_active;
+  const int PPW = PB / p.C;                    // positions per warp per block (multiple of 4)
   const bool owns_new = (slot == n_active - 1);  // this chunk contains position `pos`
 
   float* qs = scratch;
   float* sc = qs + G * D;
   float* red = sc + G * kAttnPBMax;
   float* lw = red + p.C * G * D;
-  float* knew = lw + p.C * kGMax;
+  float* mw = lw + p.C * kGMax;
+  float* knew = mw + p.C * kGMax;
   float* vnew = knew + D;
   float* wts = vnew + D;
 
@@ -582,31 +599,10 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
   __nv_bfloat16* Kc = p.kcache + head_base;
   __nv_bfloat16* Vc = p.vcache + head_base;
   const int sub = c.lane >> 3, sl = c.lane & 7;
-
-  // K/V rows of cached positions do not depend on this step: issue the first block's
-  // loads BEFORE waiting for the QKV projections (their HBM latency leaves the critical path).
-  uint4 kreg[2][KQ];
-  uint32_t vreg[8][DPL / 2];
-  auto load_block = [&](int blk) {
-    const int wb = blk * PB + c.cw * 8;  // first position (chunk-relative) owned by this warp
-#pragma unroll
-    for (int st = 0; st < 2; ++st) {
-      const int tt = wb + st * 4 + sub;
-      const bool ld = tt < n && (t0 + tt) != pos;
-      const uint4* kp = reinterpret_cast<const uint4*>(Kc + (size_t)(t0 + tt) * D + sl * EPL);
-#pragma unroll
-      for (int q = 0; q < KQ; ++q) kreg[st][q] = ld ? __ldcg(kp + q) : make_uint4(0u, 0u, 0u, 0u);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int tt = wb + j;
-      const bool ld = tt < n && (t0 + tt) != pos;
-      const uint32_t* vp = reinterpret_cast<const uint32_t*>(Vc + (size_t)(t0 + tt) * D) + c.lane * (DPL / 2);
-#pragma unroll
-      for (int q = 0; q < DPL / 2; ++q) vreg[j][q] = ld ? __ldcg(vp + q) : 0u;
-    }
-  };
-  load_block(0);
+  const uint32_t ring_addr = smem_u32(ring);
+  const uint32_t full0 = smem_u32(&hdr->full[0]);
+  const uint32_t empty0 = smem_u32(&hdr->empty[0]);
+  const uint32_t n_stage = (uint32_t)p.n_stage;
 
   wait_counter(p, c, t.wait_ctr, t.wait_val, task_idx);
   stamp(p, c, task_idx, 1);
@@ -621,18 +617,14 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
       rope_norm_head<D>(p, qkv + p.q_dim + (size_t)kvh * D, p.qk_norm ? lay_fp + p.fp_kn : nullptr, pos, 1.0f, c.lane,
                         knew);
       __syncwarp();
-      for (int d = c.lane; d < D; d += 32) {
-        const __nv_bfloat16 kb = __float2bfloat16_rn(knew[d]);
-        Kc[(size_t)pos * D + d] = kb;
-        knew[d] = __bfloat162float(kb);  // attend over exactly what the cache holds
-      }
+      for (int d = c.lane; d < D; d += 32) Kc[(size_t)pos * D + d] = __float2bfloat16_rn(knew[d]);
     }
     if (c.cw == wv) {
       const float* vraw = qkv + p.q_dim + p.kv_dim + (size_t)kvh * D;
       for (int d = c.lane; d < D; d += 32) {
-        const __nv_bfloat16 vb = __float2bfloat16_rn(__ldcg(vraw + d));
-        Vc[(size_t)pos * D + d] = vb;
-        vnew[d] = __bfloat162float(vb);
+        const float v = __ldcg(vraw + d);
+        vnew[d] = v;
+        Vc[(size_t)pos * D + d] = __float2bfloat16_rn(v);
       }
     }
   }
@@ -649,26 +641,32 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
   }
 
   for (int blk = 0; blk < nblk; ++blk) {
-    if (blk > 0) load_block(blk);
-    const int wb = blk * PB + c.cw * 8;
-    // scores of this warp's 8 positions (2 steps x 4 positions, 8 lanes each)
-#pragma unroll
-    for (int st = 0; st < 2; ++st) {
-      const int tt = wb + st * 4 + sub;
-      const bool valid = tt < n;
+    const int wb = blk * PB + c.cw * PPW;  // first chunk-relative position owned by this warp
+    const bool patch = owns_new && blk == nblk - 1;
+    const int new_row = (pos - t0) - blk * PB;  // row of the new token inside this block (if patch)
+    // ---------------- K stage: scores ----------------
+    mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);
+    const uint32_t kb = ring_addr + c.slot * (uint32_t)p.stage_bytes;
+    if (patch) {  // the staged copy predates this step's K row: overwrite it (bf16, as the cache holds it)
+      for (int d = c.ctid; d < D; d += c.nct) {
+        const unsigned short bits = __bfloat16_as_ushort(__float2bfloat16_rn(knew[d]));
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(kb + (uint32_t)(new_row * D + d) * 2u), "h"(bits) : "memory");
+      }
+      consumer_sync(c.nct);
+    }
+    for (int st = 0; st < PPW; st += 4) {
+      const int tl = c.cw * PPW + st + sub;  // block-local position
+      const bool valid = blk * PB + tl < n;
       float kf[EPL];
 #pragma unroll
-      for (int q = 0; q < KQ; ++q) {
-        const uint4 raw = kreg[st][q];
+      for (int q = 0; q < EPL / 8; ++q) {
+        const uint4 raw = lds128u(kb + (uint32_t)(tl * D + sl * EPL + q * 8) * 2u);
         kf[q * 8 + 0] = bf_lo(raw.x); kf[q * 8 + 1] = bf_hi(raw.x);
         kf[q * 8 + 2] = bf_lo(raw.y); kf[q * 8 + 3] = bf_hi(raw.y);
         kf[q * 8 + 4] = bf_lo(raw.z); kf[q * 8 + 5] = bf_hi(raw.z);
         kf[q * 8 + 6] = bf_lo(raw.w); kf[q * 8 + 7] = bf_hi(raw.w);
       }
-      if (owns_new && valid && (t0 + tt) == pos) {
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) kf[e] = knew[sl * EPL + e];
-      }
+#pragma unroll 1
       for (int g = 0; g < G; ++g) {
         const float4* qp = reinterpret_cast<const float4*>(qs + g * D + sl * EPL);
         float sdot = 0.f;
@@ -681,12 +679,15 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
         sdot += __shfl_xor_sync(0xffffffffu, sdot, 4);
         sdot += __shfl_xor_sync(0xffffffffu, sdot, 2);
         sdot += __shfl_xor_sync(0xffffffffu, sdot, 1);
-        if (sl == 0) sc[g * kAttnPBMax + c.cw * 8 + st * 4 + sub] = valid ? sdot : -INFINITY;
+        if (sl == 0) sc[g * kAttnPBMax + tl] = valid ? sdot : -INFINITY;
       }
     }
+    __syncwarp();
+    if (c.lane == 0) mbar_arrive(empty0 + c.slot * 8);
+    if (++c.slot == n_stage) { c.slot = 0; c.ph ^= 1u; }
     consumer_sync(c.nct);
     if (blk == 0) stamp(p, c, task_idx, 3);
-    // block max (every warp computes it redundantly -> no second barrier), rescale, P.V
+    // block max (every warp computes it redundantly -> no second barrier) and rescale
 #pragma unroll
     for (int g = 0; g < kGMax; ++g) {
       if (g < G) {
@@ -699,30 +700,54 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
         l_part[g] *= resc;
 #pragma unroll
         for (int e = 0; e < DPL; ++e) acc[g][e] *= resc;
+        if (c.lane == 0) mw[c.cw * kGMax + g] = m_new;
       }
     }
+    __syncwarp();
+    // probabilities of this warp's own positions, in place (entries written by this warp only)
+    for (int e = c.lane; e < G * PPW; e += 32) {
+      const int g = e / PPW, j = e - g * PPW;
+      const int idx = g * kAttnPBMax + c.cw * PPW + j;
+      sc[idx] = expf(sc[idx] - mw[c.cw * kGMax + g]);  // exp(-inf) = 0 for padded positions
+    }
+    __syncwarp();
+    // ---------------- V stage: P.V over this warp's positions ----------------
+    mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);
+    const uint32_t vb = ring_addr + c.slot * (uint32_t)p.stage_bytes;
+    if (patch) {
+      for (int d = c.ctid; d < D; d += c.nct) {
+        const unsigned short bits = __bfloat16_as_ushort(__float2bfloat16_rn(vnew[d]));
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(vb + (uint32_t)(new_row * D + d) * 2u), "h"(bits) : "memory");
+      }
+      consumer_sync(c.nct);
+    }
+#pragma unroll 1
+    for (int j = 0; j < PPW; ++j) {
+      const int tl = c.cw * PPW + j;
+      if (blk * PB + tl >= n) break;  // warp-uniform
+      float vf[DPL];
+      if constexpr (DPL == 4) {
+        uint2 raw;
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(raw.x), "=r"(raw.y) : "r"(vb + (uint32_t)(tl * D + c.lane * 4) * 2u));
+        vf[0] = bf_lo(raw.x); vf[1] = bf_hi(raw.x); vf[2] = bf_lo(raw.y); vf[3] = bf_hi(raw.y);
+      } else {
+        uint32_t raw;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(vb + (uint32_t)(tl * D + c.lane * 2) * 2u));
+        vf[0] = bf_lo(raw); vf[1] = bf_hi(raw);
+      }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int tt = wb + j;
-      if (tt < n) {  // warp-uniform
-        float vf[DPL];
+      for (int g = 0; g < kGMax; ++g) {
+        if (g < G) {
+          const float pg = sc[g * kAttnPBMax + tl];
+          l_part[g] += pg;
 #pragma unroll
-        for (int q = 0; q < DPL / 2; ++q) { vf[2 * q] = bf_lo(vreg[j][q]); vf[2 * q + 1] = bf_hi(vreg[j][q]); }
-        if (owns_new && (t0 + tt) == pos) {
-#pragma unroll
-          for (int e = 0; e < DPL; ++e) vf[e] = vnew[c.lane * DPL + e];
-        }
-#pragma unroll
-        for (int g = 0; g < kGMax; ++g) {
-          if (g < G) {
-            const float pg = expf(sc[g * kAttnPBMax + c.cw * 8 + j] - m_run[g]);
-            l_part[g] += pg;
-#pragma unroll
-            for (int e = 0; e < DPL; ++e) acc[g][e] = fmaf(pg, vf[e], acc[g][e]);
-          }
+          for (int e = 0; e < DPL; ++e) acc[g][e] = fmaf(pg, vf[e], acc[g][e]);
         }
       }
     }
+    __syncwarp();
+    if (c.lane == 0) mbar_arrive(empty0 + c.slot * 8);
+    if (++c.slot == n_stage) { c.slot = 0; c.ph ^= 1u; }
     if (blk + 1 < nblk) consumer_sync(c.nct);  // sc is rewritten by the next block
   }
   stamp(p, c, task_idx, 4);
@@ -748,8 +773,8 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
     else {
       part[((size_t)slot * G + g) * PS + d] = o;
       if (d == 0) {
+        part[((size_t)slot * G + g) * PS + D] = mw[g];  // warp 0's copy; identical in every warp
         part[((size_t)slot * G + g) * PS + D + 1] = l;
-        // m_run is identical in every warp; lane/thread with d == 0 of head g publishes it
       }
     }
   }
@@ -757,11 +782,6 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
     signal_counter(p, c, CTR_C);
     stamp(p, c, task_idx, 7);
     return;
-  }
-  if (c.cw == 0 && c.lane == 0) {
-#pragma unroll
-    for (int g = 0; g < kGMax; ++g)
-      if (g < G) part[((size_t)slot * G + g) * PS + D] = m_run[g];
   }
   consumer_sync(c.nct);
   stamp(p, c, task_idx, 5);
@@ -844,6 +864,11 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       const uint32_t ring_addr = smem_u32(ring);
       const uint32_t n_stage = (uint32_t)p.n_stage;
       const uint64_t pol = l2_evict_first_policy();  // weights are read once per step
+      int lpos = 0;
+      if (!p.probe) {
+        lpos = __ldcg(p.positions);
+        if (lpos < 0 || lpos >= p.max_ctx) return;  // the consumers report the error
+      }
       // L2 prefetch cursor: runs pf_min bytes ahead of the ring in steady state and up to
       // pf_max bytes ahead while the ring is full (consumers stalled on a dependency), so
       // HBM keeps streaming through dependency stalls.
@@ -864,7 +889,29 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
         const int4 q0 = __ldg(tp), q1 = __ldg(tp + 1), q2 = __ldg(tp + 2);
         const int type = q0.x, nrows = q0.w, kchunks = q1.y, rt = q1.z, ktc = q1.w;
         const int n_tiles = q2.x, n_ktiles = q2.y;
-        if (type == T_ATTN || type == T_END) continue;
+        if (type == T_END) continue;
+        if (type == T_ATTN) {
+          // K / V blocks of this unit's context chunk, one ring stage each (skipped in probe mode)
+          if (p.probe) continue;
+          const AttnGeom ge = attn_geometry(p, lpos, q0.w);
+          if (q0.w >= ge.n_active) continue;
+          const int4 q3 = __ldg(tp + 3);
+          const size_t head_base = ((size_t)(q0.y * p.batch + q3.w) * p.nkv + q0.z) * (size_t)p.max_ctx * p.D;
+          for (int blk = 0; blk < ge.nblk; ++blk) {
+            const int nb = min(ge.PB, ge.n - blk * ge.PB);
+            const uint32_t bytes = (uint32_t)nb * (uint32_t)p.D * 2u;
+            const size_t off = head_base + (size_t)(ge.t0 + blk * ge.PB) * p.D;
+            for (int kv = 0; kv < 2; ++kv) {
+              const uint32_t eb = smem_u32(&hdr->empty[slot]);
+              if (!mbar_try_wait(eb, ph ^ 1u)) mbar_wait_slow(p, eb, ph ^ 1u, DE_WATCHDOG_EMPTY, ti);
+              const uint32_t fb = smem_u32(&hdr->full[slot]);
+              mbar_arrive_expect_tx(fb, bytes);
+              tma_bulk_g2s(ring_addr + slot * (uint32_t)p.stage_bytes, (kv ? p.vcache : p.kcache) + off, bytes, fb);
+              if (++slot == n_stage) { slot = 0; ph ^= 1u; }
+            }
+          }
+          continue;
+        }
         const uint8_t* src = p.wpacked + (size_t)(uint32_t)q2.z * 16u;
         for (int tile = 0; tile < n_tiles; ++tile) {
           const int rows = min(rt, nrows - tile * rt);
@@ -915,8 +962,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       dst[0] = __ldg(tp); dst[1] = __ldg(tp + 1); dst[2] = __ldg(tp + 2); dst[3] = __ldg(tp + 3);
     }
     if (t.type == T_ATTN) {
-      if (p.D == 128) run_attn<128>(p, c, t, ti, scratch, hdr, pos);
-      else run_attn<64>(p, c, t, ti, scratch, hdr, pos);
+      if (p.D == 128) run_attn<128>(p, c, t, ti, scratch, hdr, ring, pos);
+      else run_attn<64>(p, c, t, ti, scratch, hdr, ring, pos);
     } else if (t.type != T_END) {
       run_gemv(p, c, t, ti, scratch, hdr, ring, tok);
     }
@@ -1082,6 +1129,10 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   if (h->n_sms < 1 || h->n_tasks < 1) return bad("empty task table");
   if (h->attn_chunks < 1 || h->attn_chunks > kAttnChunksMax || h->attn_min_chunk < 8)
     return bad("attention chunking out of range");
+  {
+    const int pb = std::min(64, (h->stage_bytes / (d.head_dim * 2)) & ~7);
+    if (pb < 8 || pb % (4 * h->C)) return bad("stage_bytes too small: a K/V block must hold 4 positions per consumer warp");
+  }
   const size_t need = ((size_t)kHeaderInts + (size_t)h->n_sms + 1 + (size_t)h->n_tasks * kTaskInts) * 4;
   if (task_table_bytes != need) return bad("task table size does not match its header");
   if (h->n_counters != CTR_HEAD0 + h->batch * d.n_kv_heads) return bad("counter count mismatch");
@@ -1091,7 +1142,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
     const int G = d.n_q_heads / d.n_kv_heads;
     const int kmax = std::max(std::max(d.hidden, d.n_q_heads * d.head_dim), d.intermediate);
     const size_t xb = align_up((size_t)kmax, kChunk) * 4;
-    const size_t ab = ((size_t)G * d.head_dim + (size_t)G * kAttnPBMax + (size_t)h->C * G * d.head_dim + (size_t)h->C * kGMax +
+    const size_t ab = ((size_t)G * d.head_dim + (size_t)G * kAttnPBMax + (size_t)h->C * G * d.head_dim + 2 * (size_t)h->C * kGMax +
                        2 * (size_t)d.head_dim + (size_t)kAttnChunksMax * kGMax) * 4;
     if ((size_t)h->scratch_bytes < std::max(xb, ab)) return bad("scratch_bytes too small for this model");
   }

@@ -129,7 +129,7 @@ def scratch_bytes(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> in
     kpad_max = max(_ceil_div(k, KCHUNK) * KCHUNK for k in (cfg.hidden, cfg.q_dim, cfg.intermediate))
     x_bytes = batch * kpad_max * 4
     g, d, c = cfg.group, cfg.head_dim, sched.consumer_warps
-    attn_bytes = (g * d + g * ATTN_PBMAX + c * g * d + c * 8 + 2 * d + ATTN_CHUNKS_MAX * 8) * 4
+    attn_bytes = (g * d + g * ATTN_PBMAX + c * g * d + 2 * c * 8 + 2 * d + ATTN_CHUNKS_MAX * 8) * 4
     return _ceil_div(max(x_bytes, attn_bytes), 1024) * 1024
 
 
