@@ -68,6 +68,7 @@ struct KParams {
   float eps;
   // schedule
   int C, n_stage, stage_bytes, attn_chunks, attn_min_chunk, scratch_bytes, n_lm_tasks, n_counters;
+  int xs_floats;  // floats reserved for the staged activation vector; the merge weights follow it
   // task table
   const Task* tasks;
   const int* sm_begin;
@@ -288,6 +289,85 @@ __device__ __forceinline__ void signal_counter(const KParams& p, const ConsumerC
   if (c.ctid == 0 && ctr >= 0 && !p.probe) red_release_add(p.counters + ctr, 1u);
 }
 
+// Split-KV geometry of one decode step, shared by the Loader (which streams the K/V
+// blocks of a unit through the ring) and the Consumers (which drain them).
+struct AttnGeom {
+  int CL, n_active, t0, n, PB, nblk;
+};
+__device__ __forceinline__ AttnGeom attn_geometry(const KParams& p, int pos, int slot) {
+  AttnGeom g;
+  const int ctx = pos + 1;
+  g.CL = max(p.attn_min_chunk, (ctx + p.attn_chunks - 1) / p.attn_chunks);
+  g.CL = (g.CL + 7) & ~7;
+  g.n_active = (ctx + g.CL - 1) / g.CL;
+  g.t0 = slot * g.CL;
+  g.n = min(ctx, g.t0 + g.CL) - g.t0;           // <= 0 for inactive slots
+  g.PB = min(64, (p.stage_bytes / (p.D * 2)) & ~7);  // positions per ring stage
+  g.nblk = g.n > 0 ? (g.n + g.PB - 1) / g.PB : 0;
+  return g;
+}
+
+// Flash-decoding merge of the split-KV partial records, done by every consumer of the
+// attention output (O-projection prologue): xs[h*D + d] = sum_s w[h][s] * o_s[h][d] with
+// w = exp(m_s - M) / sum_s l_s exp(m_s - M).  `wts` holds n_q_heads * n_active floats.
+// All global loads of a phase are independent and issued back to back (one L2 round trip).
+__device__ __forceinline__ void attn_merge_into(const KParams& p, const ConsumerCtx& c, int pos, float* xs, int kpad,
+                                                float* wts) {
+  const AttnGeom ge = attn_geometry(p, pos, 0);
+  const int na = ge.n_active, D = p.D, G = p.G, PS = D + 4;
+  const float* part = p.part;  // [nkv][attn_chunks][G][PS]   (batch 1)
+  // phase 1: (m, l) of every (head, chunk) -> shared memory
+  for (int i = c.ctid; i < p.nq * na; i += c.nct) {
+    const int h = i / na, s2 = i - h * na;
+    const int kvh = h / G, g = h - kvh * G;
+    const float2 ml = __ldcg(reinterpret_cast<const float2*>(part + (((size_t)kvh * p.attn_chunks + s2) * G + g) * PS + D));
+    wts[i] = ml.x;
+    wts[p.nq * na + i] = ml.y;
+  }
+  consumer_sync(c.nct);
+  // phase 2: normalised weights, one warp per head, lanes over chunks
+  for (int h = c.cw; h < p.nq; h += p.C) {
+    float M = -INFINITY;
+    for (int s2 = c.lane; s2 < na; s2 += 32) M = fmaxf(M, wts[h * na + s2]);
+    M = warp_max(M);
+    float L = 0.f;
+    for (int s2 = c.lane; s2 < na; s2 += 32) {
+      const float wgt = expf(wts[h * na + s2] - M);
+      L = fmaf(wts[p.nq * na + h * na + s2], wgt, L);
+      wts[h * na + s2] = wgt;
+    }
+    L = warp_sum(L);
+    const float inv = 1.0f / L;
+    for (int s2 = c.lane; s2 < na; s2 += 32) wts[h * na + s2] *= inv;
+  }
+  consumer_sync(c.nct);
+  // phase 3: weighted sum, four output dims per thread, chunks batched by four
+  const int q4 = p.q_dim >> 2;
+  for (int i = c.ctid; i < (kpad >> 2); i += c.nct) {
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < q4) {
+      const int h = (i * 4) / D, d = i * 4 - h * D;
+      const int kvh = h / G, g = h - kvh * G;
+      const float* rec = part + ((size_t)kvh * p.attn_chunks * G + g) * PS + d;
+      const size_t cs = (size_t)G * PS;
+      const float* w = wts + h * na;
+      for (int s0 = 0; s0 < na; s0 += 8) {  // eight independent 16-byte loads in flight per thread
+        float4 a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          a[u] = (s0 + u < na) ? __ldcg(reinterpret_cast<const float4*>(rec + (s0 + u) * cs)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float wu = (s0 + u < na) ? w[s0 + u] : 0.f;
+          x.x = fmaf(a[u].x, wu, x.x); x.y = fmaf(a[u].y, wu, x.y); x.z = fmaf(a[u].z, wu, x.z); x.w = fmaf(a[u].w, wu, x.w);
+        }
+      }
+    }
+    reinterpret_cast<float4*>(xs)[i] = x;
+  }
+  consumer_sync(c.nct);
+}
+
 // ----------------------------------------------------------------------------------
 // GEMV task
 // ----------------------------------------------------------------------------------
@@ -307,42 +387,65 @@ __device__ __forceinline__ float load_h1(const KParams& p, int layer, int tok, i
   return __ldcg(p.h_a + i);
 }
 
+constexpr int kPreG = 4;  // float4 gain vectors per thread preloaded before the dependency wait
+
+__device__ __forceinline__ const float* gemv_gain(const KParams& p, const Task& t) {
+  if (t.type == T_LMHEAD) return p.fparams + p.fp_final;
+  return p.fparams + (size_t)t.layer * p.fp_layer_stride + (t.type == T_GATEUP ? p.fp_ln2 : p.fp_ln1);
+}
+
 // Stage the activation vector of a GEMV in shared memory (fp32, zero padded to kpad).
 __device__ __forceinline__ void gemv_prologue(const KParams& p, ConsumerCtx& c, const Task& t, float* xs,
-                                              SmemHdr* hdr, int tok) {
+                                              SmemHdr* hdr, int tok, int pos, const float4 (&g4)[kPreG]) {
   const int kpad = t.kchunks * kChunk;
   const int type = t.type;
   c.rs = 1.0f;
-  if (type == T_OPROJ || type == T_DOWN) {
-    const float* src = (type == T_OPROJ) ? p.attn : p.act;
-    const int k4 = t.k >> 2;
-    for (int i = c.ctid; i < (kpad >> 2); i += c.nct) {
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (i < k4) v = __ldcg(reinterpret_cast<const float4*>(src) + i);
-      reinterpret_cast<float4*>(xs)[i] = v;
+  if (type == T_OPROJ) {  // input = merged split-KV attention output
+    attn_merge_into(p, c, pos, xs, kpad, xs + p.xs_floats);
+    return;
+  }
+  if (type == T_DOWN) {
+    const int k4 = t.k >> 2, kp4 = kpad >> 2;
+    for (int i0 = c.ctid; i0 < kp4; i0 += 4 * c.nct) {  // four independent loads in flight per thread
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * c.nct;
+        v[u] = (i < k4) ? __ldcg(reinterpret_cast<const float4*>(p.act) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * c.nct;
+        if (i < kp4) reinterpret_cast<float4*>(xs)[i] = v[u];
+      }
     }
     consumer_sync(c.nct);
     return;
   }
-  // RMSNorm-fused prologues: QKV (ln1 over layer input), GATEUP (ln2 over h_mid), LMHEAD (final norm)
+  // RMSNorm-fused prologues: QKV (ln1 over layer input), GATEUP (ln2 over h_mid), LMHEAD (final norm).
+  // Single pass: stage h * gain, accumulate sum(h^2); the scalar rsqrt(mean + eps) commutes with
+  // the dot products and is applied to each output row in the epilogue.
   const bool mid = (type == T_GATEUP);
   const int layer = (type == T_LMHEAD) ? p.L : t.layer;  // LM head reads h_a (layer index L > 0)
-  const float* gain = (type == T_LMHEAD) ? (p.fparams + p.fp_final)
-                                         : (p.fparams + (size_t)t.layer * p.fp_layer_stride + (mid ? p.fp_ln2 : p.fp_ln1));
-  const int h4 = p.H >> 2;
+  const float4* gain4 = reinterpret_cast<const float4*>(gemv_gain(p, t));
+  const int h4 = p.H >> 2, kp4 = kpad >> 2;
   float ss = 0.f;
-  // single pass: stage h * gain, accumulate sum(h^2); the scalar rsqrt(mean + eps) commutes
-  // with the dot products and is applied to each output row in the epilogue
-  for (int i = c.ctid; i < (kpad >> 2); i += c.nct) {
+  auto stage = [&](int i, const float4& g) {
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i < h4) {
       v = load_h4(p, layer, mid, tok, i);
-      const float4 g = __ldg(reinterpret_cast<const float4*>(gain) + i);
       ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
       v.x *= g.x; v.y *= g.y; v.z *= g.z; v.w *= g.w;
     }
     reinterpret_cast<float4*>(xs)[i] = v;
+  };
+#pragma unroll
+  for (int k = 0; k < kPreG; ++k) {
+    const int i = c.ctid + k * c.nct;
+    if (i < kp4) stage(i, g4[k]);
   }
+  for (int i = c.ctid + kPreG * c.nct; i < kp4; i += c.nct)
+    stage(i, i < h4 ? __ldg(gain4 + i) : make_float4(0.f, 0.f, 0.f, 0.f));
   ss = warp_sum(ss);
   if (c.lane == 0) hdr->red[c.cw] = ss;
   consumer_sync(c.nct);
@@ -351,16 +454,24 @@ __device__ __forceinline__ void gemv_prologue(const KParams& p, ConsumerCtx& c, 
   c.rs = rsqrtf(tot / (float)p.H + p.eps);
 }
 
-__device__ __forceinline__ void gemv_epilogue(const KParams& p, ConsumerCtx& c, const Task& t, int vrow, float v,
-                                              float v_pair, int tok) {
+// Epilogue operand of one output row that is known before the dot product finishes (bias,
+// residual input): loaded ahead of the K loop so its latency hides behind the stream.
+__device__ __forceinline__ float load_eop(const KParams& p, const Task& t, int vrow, int tok) {
   switch (t.type) {
-    case T_QKV: {
-      if (p.has_bias) v += __ldg(p.fparams + (size_t)t.layer * p.fp_layer_stride + p.fp_bias + vrow);
-      p.qkv[vrow] = v;
-    } break;
-    case T_OPROJ: p.h_b[vrow] = load_h1(p, t.layer, tok, vrow) + v; break;
+    case T_QKV: return p.has_bias ? __ldg(p.fparams + (size_t)t.layer * p.fp_layer_stride + p.fp_bias + vrow) : 0.f;
+    case T_OPROJ: return load_h1(p, t.layer, tok, vrow);
+    case T_DOWN: return __ldcg(p.h_b + vrow);
+    default: return 0.f;
+  }
+}
+
+__device__ __forceinline__ void gemv_epilogue(const KParams& p, ConsumerCtx& c, const Task& t, int vrow, float v,
+                                              float v_pair, float eop) {
+  switch (t.type) {
+    case T_QKV: p.qkv[vrow] = v + eop; break;
+    case T_OPROJ: p.h_b[vrow] = eop + v; break;
     case T_GATEUP: p.act[vrow >> 1] = silu(v) * v_pair; break;  // vrow even = gate, pair = up
-    case T_DOWN: p.h_a[vrow] = __ldcg(p.h_b + vrow) + v; break;
+    case T_DOWN: p.h_a[vrow] = eop + v; break;
     case T_LMHEAD: {
       if (p.logits) p.logits[vrow] = v;
       if (v > c.best_val) { c.best_val = v; c.best_idx = vrow; }  // rows ascend: first max wins ties
@@ -390,7 +501,8 @@ __device__ __forceinline__ void gemv_chunk(uint32_t waddr, uint32_t row_stride, 
 
 template <int RW>
 __device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx,
-                                           const float* xs, SmemHdr* hdr, uint8_t* ring, int tok) {
+                                           const float* xs, SmemHdr* hdr, uint8_t* ring, int tok,
+                                           const float (&eop0)[4]) {
   const uint32_t xs_addr = smem_u32(xs) + c.lane * 16;
   const uint32_t ring_addr = smem_u32(ring) + c.lane * 16;
   const uint32_t full0 = smem_u32(&hdr->full[0]);
@@ -401,8 +513,14 @@ __device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, con
     const int rows = min(t.rt, t.b - tile * t.rt);
     const int nrows = min(RW, rows - r0);  // rows of this tile owned by this warp (<= 0: none)
     float2 accA[RW], accB[RW];
+    float eop[RW];
 #pragma unroll
-    for (int i = 0; i < RW; ++i) { accA[i] = make_float2(0.f, 0.f); accB[i] = make_float2(0.f, 0.f); }
+    for (int i = 0; i < RW; ++i) {
+      accA[i] = make_float2(0.f, 0.f);
+      accB[i] = make_float2(0.f, 0.f);
+      eop[i] = eop0[i];
+      if (tile > 0 && c.lane == 0 && i < nrows && !p.probe) eop[i] = load_eop(p, t, t.a + tile * t.rt + r0 + i, tok);
+    }
     int kc0 = 0;
     for (int kt = 0; kt < t.n_ktiles; ++kt, kc0 += t.ktc) {
       const int chunks = min(t.ktc, t.kchunks - kc0);
@@ -440,11 +558,11 @@ __device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, con
         if (t.type == T_GATEUP) {
 #pragma unroll
           for (int i = 0; i < RW; i += 2)
-            if (i < nrows) gemv_epilogue(p, c, t, vrow0 + i, v[i], v[(i + 1) % RW], tok);
+            if (i < nrows) gemv_epilogue(p, c, t, vrow0 + i, v[i], v[(i + 1) % RW], 0.f);
         } else {
 #pragma unroll
           for (int i = 0; i < RW; ++i)
-            if (i < nrows) gemv_epilogue(p, c, t, vrow0 + i, v[i], 0.f, tok);
+            if (i < nrows) gemv_epilogue(p, c, t, vrow0 + i, v[i], 0.f, eop[i]);
         }
       }
     }
@@ -497,15 +615,43 @@ __device__ __forceinline__ void lm_finish(const KParams& p, ConsumerCtx& c, Smem
 }
 
 __device__ __forceinline__ void run_gemv(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* xs,
-                                         SmemHdr* hdr, uint8_t* ring, int tok) {
+                                         SmemHdr* hdr, uint8_t* ring, int tok, int pos) {
   stamp(p, c, task_idx, 0);
+  const int rw = t.rt / p.C;
+  // ---- before the dependency wait: everything that does not depend on the awaited data ----
+  // (per-layer vectors are always DRAM misses under the weight stream: ~1 us each if loaded late)
+  float4 g4[kPreG];
+  float eop0[4] = {0.f, 0.f, 0.f, 0.f};
+  if (!p.probe) {
+    if (t.type == T_QKV || t.type == T_GATEUP || t.type == T_LMHEAD) {
+      const float4* gain4 = reinterpret_cast<const float4*>(gemv_gain(p, t));
+#pragma unroll
+      for (int k = 0; k < kPreG; ++k) {
+        const int i = c.ctid + k * c.nct;
+        g4[k] = (i < (p.H >> 2)) ? __ldg(gain4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    if (c.lane == 0 && t.type != T_DOWN) {  // DOWN's residual (h_mid) is preloaded after its own dependency
+      const int r0 = c.cw * rw, rows0 = min(t.rt, t.b);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < rw && r0 + i < rows0) eop0[i] = load_eop(p, t, t.a + r0 + i, tok);
+    }
+  }
   wait_counter(p, c, t.wait_ctr, t.wait_val, task_idx);
   stamp(p, c, task_idx, 1);
-  if (!p.probe) gemv_prologue(p, c, t, xs, hdr, tok);
+  if (!p.probe) {
+    if (c.lane == 0 && t.type == T_DOWN) {
+      const int r0 = c.cw * rw, rows0 = min(t.rt, t.b);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < rw && r0 + i < rows0) eop0[i] = load_eop(p, t, t.a + r0 + i, tok);
+    }
+    gemv_prologue(p, c, t, xs, hdr, tok, pos, g4);
+  }
   stamp(p, c, task_idx, 2);
-  const int rw = t.rt / p.C;
-  if (rw == 2) gemv_tiles<2>(p, c, t, task_idx, xs, hdr, ring, tok);
-  else gemv_tiles<4>(p, c, t, task_idx, xs, hdr, ring, tok);
+  if (rw == 2) gemv_tiles<2>(p, c, t, task_idx, xs, hdr, ring, tok, eop0);
+  else gemv_tiles<4>(p, c, t, task_idx, xs, hdr, ring, tok, eop0);
   if (p.probe) return;
   stamp(p, c, task_idx, 3);
   if (t.type == T_LMHEAD) lm_finish(p, c, hdr);
@@ -513,84 +659,96 @@ __device__ __forceinline__ void run_gemv(const KParams& p, ConsumerCtx& c, const
   stamp(p, c, task_idx, 7);
 }
 
-// ----------------------------------------------------------------------------------
-// attention task: one (kv head, context chunk) unit of split-KV decode attention
-// ----------------------------------------------------------------------------------
+// Per-lane operands of rope_norm_head that do not depend on this step's projections:
+// loaded BEFORE the dependency wait so their DRAM latency is off the critical path
+// (small per-layer vectors never survive in L2 under the weight stream).
 template <int D>
-__device__ __forceinline__ void rope_norm_head(const KParams& p, const float* raw, const float* gain, int pos,
-                                               float scale, int lane, float* out) {
-  // one warp, one head: optional RMSNorm over D, rotate-half RoPE, scale
+struct HeadParams {
+  float gq[D / 32], gk[D / 32], cs[D / 64], sn[D / 64];
+};
+template <int D>
+__device__ __forceinline__ HeadParams<D> load_head_params(const KParams& p, const float* lay_fp, int pos, int lane) {
+  HeadParams<D> hp;
+#pragma unroll
+  for (int j = 0; j < D / 32; ++j) {
+    hp.gq[j] = p.qk_norm ? __ldg(lay_fp + p.fp_qn + lane + 32 * j) : 1.0f;
+    hp.gk[j] = p.qk_norm ? __ldg(lay_fp + p.fp_kn + lane + 32 * j) : 1.0f;
+  }
+#pragma unroll
+  for (int j = 0; j < D / 64; ++j) {
+    hp.cs[j] = __ldg(p.rope_cos + (size_t)pos * (D / 2) + lane + 32 * j);
+    hp.sn[j] = __ldg(p.rope_sin + (size_t)pos * (D / 2) + lane + 32 * j);
+  }
+  return hp;
+}
+
+// one warp, one head: optional RMSNorm over D, rotate-half RoPE, scale
+// PADL > 0: the output is laid out in segments of PADL floats separated by 4 floats of padding
+// (bank-conflict-free reads by the score step); PADL = 0: dense.
+template <int D, int PADL>
+__device__ __forceinline__ void rope_norm_head(const KParams& p, const float* raw, const float (&gain)[D / 32],
+                                               const HeadParams<D>& hp, float scale, int lane, float* out) {
+  auto at = [](int d) { return PADL > 0 ? d + (d / (PADL > 0 ? PADL : 1)) * 4 : d; };
   constexpr int PER = D / 32;  // 4 (D=128) or 2 (D=64): elements lane, lane+32, ...
   constexpr int HALF = D / 2;
   float v[PER];
   float ss = 0.f;
 #pragma unroll
   for (int j = 0; j < PER; ++j) { v[j] = __ldcg(raw + lane + 32 * j); ss += v[j] * v[j]; }
-  if (gain) {
+  if (p.qk_norm) {
     ss = warp_sum(ss);
     const float rs = rsqrtf(ss / (float)D + p.eps);
 #pragma unroll
-    for (int j = 0; j < PER; ++j) v[j] = v[j] * rs * __ldg(gain + lane + 32 * j);
+    for (int j = 0; j < PER; ++j) v[j] = v[j] * rs * gain[j];
   }
-  const float* cs = p.rope_cos + (size_t)pos * HALF;
-  const float* sn = p.rope_sin + (size_t)pos * HALF;
 #pragma unroll
   for (int j = 0; j < PER / 2; ++j) {
     const int d1 = lane + 32 * j;  // < HALF
-    const float c1 = __ldg(cs + d1), s1 = __ldg(sn + d1);
     const float x1 = v[j], x2 = v[j + PER / 2];
-    out[d1] = (x1 * c1 - x2 * s1) * scale;
-    out[d1 + HALF] = (x2 * c1 + x1 * s1) * scale;
+    out[at(d1)] = (x1 * hp.cs[j] - x2 * hp.sn[j]) * scale;
+    out[at(d1 + HALF)] = (x2 * hp.cs[j] + x1 * hp.sn[j]) * scale;
   }
 }
 
-// Split-KV geometry of one decode step, shared by the Loader (which streams the K/V
-// blocks of a unit through the ring) and the Consumers (which drain them).
-struct AttnGeom {
-  int CL, n_active, t0, n, PB, nblk;
-};
-__device__ __forceinline__ AttnGeom attn_geometry(const KParams& p, int pos, int slot) {
-  AttnGeom g;
-  const int ctx = pos + 1;
-  g.CL = max(p.attn_min_chunk, (ctx + p.attn_chunks - 1) / p.attn_chunks);
-  g.CL = (g.CL + 7) & ~7;
-  g.n_active = (ctx + g.CL - 1) / g.CL;
-  g.t0 = slot * g.CL;
-  g.n = min(ctx, g.t0 + g.CL) - g.t0;           // <= 0 for inactive slots
-  g.PB = min(64, (p.stage_bytes / (p.D * 2)) & ~7);  // positions per ring stage
-  g.nblk = g.n > 0 ? (g.n + g.PB - 1) / g.PB : 0;
-  return g;
-}
-
 // Layout of the attention scratch (floats); must match task_table.scratch_bytes / adamk_create.
-//   qs[G][D] | sc[G][kAttnPBMax] | red[C][G][D] | lw[C][kGMax] | mw[C][kGMax] | knew[D] | vnew[D] | wts[kAttnChunksMax][kGMax]
+//   qs[G][D] | sc[8][kAttnPBMax] | rsc[C][8] | prob[8][kAttnPBMax] | red[C][G][D] | lw[C][8] | mw[C][8] | knew[D] | vnew[D]
 //
 // The K and V rows of a unit's context chunk arrive through the weight ring (the paper's
 // "KV-cache loads advanced into the pipeline window"): per block of PB positions
 // one K stage and one V stage, issued by the Loader long before the QKV projections of this
-// layer are done.  The row of the new token is patched into the staged copy.
-template <int D>
+// layer are done.  The row of the new token is patched into the staged copy.  Every unit
+// publishes a partial record (o[D], m, l) per q head; the flash-decoding merge of the records
+// is done by the consumers of the attention output (the O-projection prologue), so no unit
+// waits for another.
+template <int D, int PPW>
 __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* scratch,
                                          SmemHdr* hdr, uint8_t* ring, int pos) {
-  constexpr int EPL = D / 8;   // K elements per lane in the score step (8 lanes per position)
-  constexpr int DPL = D / 32;  // V / output elements per lane in the P.V step
+  constexpr int DPL = D / 32;  // V / output elements per lane (lanes split the head dim)
   const int G = p.G;
   const int kvh = t.a, slot = t.b, bidx = t.aux;
+  if (p.probe) return;
   const AttnGeom ge = attn_geometry(p, pos, slot);
-  if (slot >= ge.n_active || p.probe) return;  // uniform across the CTA's consumers
+  if (slot >= ge.n_active) {  // no context for this slot at this length: only keep the counter target static
+    signal_counter(p, c, CTR_C);
+    return;
+  }
   stamp(p, c, task_idx, 0);
-  const int n = ge.n, t0 = ge.t0, PB = ge.PB, nblk = ge.nblk, n_active = ge.n_active;
-  const int PPW = PB / p.C;                    // positions per warp per block (multiple of 4)
-  const bool owns_new = (slot == n_active - 1);  // this chunk contains position `pos`
+  const int n = ge.n, t0 = ge.t0, PB = ge.PB, nblk = ge.nblk;
+  const bool owns_new = (slot == ge.n_active - 1);  // this chunk contains position `pos`
 
-  float* qs = scratch;
-  float* sc = qs + G * D;
-  float* red = sc + G * kAttnPBMax;
+  // compile-time lane mapping of the score step (see below) -- needed here for the padded q layout
+  constexpr int GS = PPW < 8 ? PPW : 8, LPP = 32 / GS, DL = D / LPP;
+  constexpr int QP = D + LPP * 4;           // padded q row: LPP segments of DL floats, 4 floats apart
+  constexpr int SR = kAttnPBMax + 4;        // padded score / probability row
+  float* qs = scratch;                      // [G][QP]
+  float* sc = qs + kGMax * (128 + 8 * 4);   // [kGMax][SR]   (q region sized for the largest QP)
+  float* rsc = sc + kGMax * SR;             // per-warp rescale factors [C][kGMax]
+  float* prob = rsc + p.C * kGMax;          // probabilities [kGMax][SR] (scores stay intact: other warps still read them)
+  float* red = prob + kGMax * SR;
   float* lw = red + p.C * G * D;
   float* mw = lw + p.C * kGMax;
   float* knew = mw + p.C * kGMax;
   float* vnew = knew + D;
-  float* wts = vnew + D;
 
   const float* qkv = p.qkv + (size_t)bidx * p.qkv_rows;
   const float* lay_fp = p.fparams + (size_t)t.layer * p.fp_layer_stride;
@@ -598,24 +756,22 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
   const size_t head_base = ((size_t)(t.layer * p.batch + bidx) * p.nkv + kvh) * (size_t)p.max_ctx * D;
   __nv_bfloat16* Kc = p.kcache + head_base;
   __nv_bfloat16* Vc = p.vcache + head_base;
-  const int sub = c.lane >> 3, sl = c.lane & 7;
   const uint32_t ring_addr = smem_u32(ring);
   const uint32_t full0 = smem_u32(&hdr->full[0]);
   const uint32_t empty0 = smem_u32(&hdr->empty[0]);
   const uint32_t n_stage = (uint32_t)p.n_stage;
 
+  const HeadParams<D> hp = load_head_params<D>(p, lay_fp, pos, c.lane);  // before the wait
   wait_counter(p, c, t.wait_ctr, t.wait_val, task_idx);
   stamp(p, c, task_idx, 1);
 
   // q heads of this group: (norm) + RoPE + 1/sqrt(D); the owner of `pos` also appends K/V
   for (int g = c.cw; g < G; g += p.C)
-    rope_norm_head<D>(p, qkv + (size_t)(kvh * G + g) * D, p.qk_norm ? lay_fp + p.fp_qn : nullptr, pos, scale, c.lane,
-                      qs + g * D);
+    rope_norm_head<D, DL>(p, qkv + (size_t)(kvh * G + g) * D, hp.gq, hp, scale, c.lane, qs + g * QP);
   if (owns_new) {
     const int wk = G % p.C, wv = (G + 1) % p.C;  // warps with the least q work
     if (c.cw == wk) {
-      rope_norm_head<D>(p, qkv + p.q_dim + (size_t)kvh * D, p.qk_norm ? lay_fp + p.fp_kn : nullptr, pos, 1.0f, c.lane,
-                        knew);
+      rope_norm_head<D, 0>(p, qkv + p.q_dim + (size_t)kvh * D, hp.gk, hp, 1.0f, c.lane, knew);
       __syncwarp();
       for (int d = c.lane; d < D; d += 32) Kc[(size_t)pos * D + d] = __float2bfloat16_rn(knew[d]);
     }
@@ -631,21 +787,42 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
   consumer_sync(c.nct);
   stamp(p, c, task_idx, 2);
 
-  float m_run[kGMax], l_part[kGMax], acc[kGMax][DPL];
+  // Per-warp running softmax state lives in shared memory (red = unnormalised output, mw = running
+  // max, lw = running sum) and every loop over heads is a plain runtime loop: this path runs once
+  // per layer on a few SMs, so its instruction footprint -- not its FLOPs -- is what costs time.
+  for (int g = 0; g < G; ++g) {
 #pragma unroll
-  for (int g = 0; g < kGMax; ++g) {
-    m_run[g] = -INFINITY;
-    l_part[g] = 0.f;
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) acc[g][e] = 0.f;
+    for (int e = 0; e < DPL; ++e) red[(c.cw * G + g) * D + c.lane * DPL + e] = 0.f;
+    if (c.lane == 0) { mw[c.cw * kGMax + g] = -INFINITY; lw[c.cw * kGMax + g] = 0.f; }
   }
+  __syncwarp();
+
+  auto lds_row = [&](uint32_t base, int tl, float (&out)[DPL]) {  // one bf16 row, DPL elements per lane
+    if constexpr (DPL == 4) {
+      uint2 raw;
+      asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(raw.x), "=r"(raw.y) : "r"(base + (uint32_t)(tl * D + c.lane * 4) * 2u));
+      out[0] = bf_lo(raw.x); out[1] = bf_hi(raw.x); out[2] = bf_lo(raw.y); out[3] = bf_hi(raw.y);
+    } else {
+      uint32_t raw;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(base + (uint32_t)(tl * D + c.lane * 2) * 2u));
+      out[0] = bf_lo(raw); out[1] = bf_hi(raw);
+    }
+  };
+
+  // Lane mapping of the score step: the warp's PPW positions are handled GS = min(PPW, 8) at a
+  // time by LPP = 32 / GS lanes each; a lane owns DL = D / LPP contiguous dims, so one dot product
+  // needs log2(LPP) shuffle steps and all GS positions reduce in parallel.  All compile-time.
+  const int lsub = c.lane % LPP, lpos = c.lane / LPP;
+  // Lane mapping of the softmax bookkeeping: lane -> (head hg = lane % 8, part hpart = lane / 8)
+  const int hg = c.lane & 7, hpart = c.lane >> 3;
 
   for (int blk = 0; blk < nblk; ++blk) {
-    const int wb = blk * PB + c.cw * PPW;  // first chunk-relative position owned by this warp
     const bool patch = owns_new && blk == nblk - 1;
     const int new_row = (pos - t0) - blk * PB;  // row of the new token inside this block (if patch)
-    // ---------------- K stage: scores ----------------
+    const int nvalid = min(PPW, n - blk * PB - c.cw * PPW);  // valid positions of this warp in this block (may be <= 0)
+    // ---------------- K stage: scores of this warp's PPW positions ----------------
     mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);
+    if (blk == 0) stamp(p, c, task_idx, 5);
     const uint32_t kb = ring_addr + c.slot * (uint32_t)p.stage_bytes;
     if (patch) {  // the staged copy predates this step's K row: overwrite it (bf16, as the cache holds it)
       for (int d = c.ctid; d < D; d += c.nct) {
@@ -654,32 +831,32 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
       }
       consumer_sync(c.nct);
     }
-    for (int st = 0; st < PPW; st += 4) {
-      const int tl = c.cw * PPW + st + sub;  // block-local position
-      const bool valid = blk * PB + tl < n;
-      float kf[EPL];
 #pragma unroll
-      for (int q = 0; q < EPL / 8; ++q) {
-        const uint4 raw = lds128u(kb + (uint32_t)(tl * D + sl * EPL + q * 8) * 2u);
-        kf[q * 8 + 0] = bf_lo(raw.x); kf[q * 8 + 1] = bf_hi(raw.x);
-        kf[q * 8 + 2] = bf_lo(raw.y); kf[q * 8 + 3] = bf_hi(raw.y);
-        kf[q * 8 + 4] = bf_lo(raw.z); kf[q * 8 + 5] = bf_hi(raw.z);
-        kf[q * 8 + 6] = bf_lo(raw.w); kf[q * 8 + 7] = bf_hi(raw.w);
+    for (int j0 = 0; j0 < PPW; j0 += GS) {
+      const int j = j0 + lpos;
+      const int tl = c.cw * PPW + j;
+      const uint32_t krow = kb + (uint32_t)(tl * D + lsub * DL) * 2u;
+      float kf[DL];  // this lane's slice of the K row, converted once and reused for every head
+#pragma unroll
+      for (int e = 0; e < DL; e += 8) {
+        const uint4 raw = lds128u(krow + e * 2);
+        kf[e + 0] = bf_lo(raw.x); kf[e + 1] = bf_hi(raw.x); kf[e + 2] = bf_lo(raw.y); kf[e + 3] = bf_hi(raw.y);
+        kf[e + 4] = bf_lo(raw.z); kf[e + 5] = bf_hi(raw.z); kf[e + 6] = bf_lo(raw.w); kf[e + 7] = bf_hi(raw.w);
       }
-#pragma unroll 1
+#pragma unroll 2
       for (int g = 0; g < G; ++g) {
-        const float4* qp = reinterpret_cast<const float4*>(qs + g * D + sl * EPL);
-        float sdot = 0.f;
+        const float4* qp = reinterpret_cast<const float4*>(qs + g * QP + lsub * (DL + 4));
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-        for (int q = 0; q < EPL / 4; ++q) {
-          const float4 qv = qp[q];
-          sdot = fmaf(qv.x, kf[q * 4 + 0], sdot); sdot = fmaf(qv.y, kf[q * 4 + 1], sdot);
-          sdot = fmaf(qv.z, kf[q * 4 + 2], sdot); sdot = fmaf(qv.w, kf[q * 4 + 3], sdot);
+        for (int e = 0; e < DL / 4; ++e) {
+          const float4 q4 = qp[e];
+          s0 = fmaf(q4.x, kf[e * 4 + 0], s0); s1 = fmaf(q4.y, kf[e * 4 + 1], s1);
+          s2 = fmaf(q4.z, kf[e * 4 + 2], s2); s3 = fmaf(q4.w, kf[e * 4 + 3], s3);
         }
-        sdot += __shfl_xor_sync(0xffffffffu, sdot, 4);
-        sdot += __shfl_xor_sync(0xffffffffu, sdot, 2);
-        sdot += __shfl_xor_sync(0xffffffffu, sdot, 1);
-        if (sl == 0) sc[g * kAttnPBMax + tl] = valid ? sdot : -INFINITY;
+        float sdot = (s0 + s1) + (s2 + s3);
+#pragma unroll
+        for (int o = LPP >> 1; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+        if (lsub == 0) sc[g * SR + tl] = (j < nvalid) ? sdot : -INFINITY;
       }
     }
     __syncwarp();
@@ -687,32 +864,42 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
     if (++c.slot == n_stage) { c.slot = 0; c.ph ^= 1u; }
     consumer_sync(c.nct);
     if (blk == 0) stamp(p, c, task_idx, 3);
-    // block max (every warp computes it redundantly -> no second barrier) and rescale
-#pragma unroll
-    for (int g = 0; g < kGMax; ++g) {
-      if (g < G) {
-        float mb = -INFINITY;
-        for (int i = c.lane; i < PB; i += 32) mb = fmaxf(mb, sc[g * kAttnPBMax + i]);
-        mb = warp_max(mb);
-        const float m_new = fmaxf(m_run[g], mb);
-        const float resc = expf(m_run[g] - m_new);  // exp(-inf) = 0 on the first block
-        m_run[g] = m_new;
-        l_part[g] *= resc;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) acc[g][e] *= resc;
-        if (c.lane == 0) mw[c.cw * kGMax + g] = m_new;
+    // ---------------- online softmax bookkeeping for all heads at once ----------------
+    // block max of head hg over the quarter hpart of the block, then across the 4 parts
+    float resc_l = 0.f;
+    {
+      float mb = -INFINITY;
+      if (hg < G)
+        for (int i = hpart; i < PB; i += 4) mb = fmaxf(mb, sc[hg * SR + i]);  // conflict-free: bank = 4 hg + hpart + 4k
+      mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 8));
+      mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
+      const float m_old = (hg < G) ? mw[c.cw * kGMax + hg] : 0.f;
+      const float m_new = fmaxf(m_old, mb);
+      resc_l = expf(m_old - m_new);  // exp(-inf) = 0 on the first block
+      // probabilities of this warp's own positions (entries written by this warp only): part hpart
+      // covers positions hpart, hpart + 4, ... of the warp
+      float lsum = 0.f;
+      if (hg < G) {
+        for (int j = hpart; j < PPW; j += 4) {
+          const int idx = hg * SR + c.cw * PPW + j;
+          const float pj = (j < nvalid) ? expf(sc[idx] - m_new) : 0.f;
+          prob[idx] = pj;
+          lsum += pj;
+        }
       }
+      lsum += __shfl_xor_sync(0xffffffffu, lsum, 8);
+      lsum += __shfl_xor_sync(0xffffffffu, lsum, 16);
+      __syncwarp();
+      if (hpart == 0 && hg < G) {
+        mw[c.cw * kGMax + hg] = m_new;
+        lw[c.cw * kGMax + hg] = lw[c.cw * kGMax + hg] * resc_l + lsum;
+        rsc[c.cw * kGMax + hg] = resc_l;  // per-warp rescale factors for the P.V step
+      }
+      __syncwarp();
     }
-    __syncwarp();
-    // probabilities of this warp's own positions, in place (entries written by this warp only)
-    for (int e = c.lane; e < G * PPW; e += 32) {
-      const int g = e / PPW, j = e - g * PPW;
-      const int idx = g * kAttnPBMax + c.cw * PPW + j;
-      sc[idx] = expf(sc[idx] - mw[c.cw * kGMax + g]);  // exp(-inf) = 0 for padded positions
-    }
-    __syncwarp();
-    // ---------------- V stage: P.V over this warp's positions ----------------
+    // ---------------- V stage: P.V over this warp's positions, one head at a time ----------------
     mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);
+    if (blk == 0) stamp(p, c, task_idx, 6);
     const uint32_t vb = ring_addr + c.slot * (uint32_t)p.stage_bytes;
     if (patch) {
       for (int d = c.ctid; d < D; d += c.nct) {
@@ -722,28 +909,23 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
       consumer_sync(c.nct);
     }
 #pragma unroll 1
-    for (int j = 0; j < PPW; ++j) {
-      const int tl = c.cw * PPW + j;
-      if (blk * PB + tl >= n) break;  // warp-uniform
-      float vf[DPL];
-      if constexpr (DPL == 4) {
-        uint2 raw;
-        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(raw.x), "=r"(raw.y) : "r"(vb + (uint32_t)(tl * D + c.lane * 4) * 2u));
-        vf[0] = bf_lo(raw.x); vf[1] = bf_hi(raw.x); vf[2] = bf_lo(raw.y); vf[3] = bf_hi(raw.y);
-      } else {
-        uint32_t raw;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(vb + (uint32_t)(tl * D + c.lane * 2) * 2u));
-        vf[0] = bf_lo(raw); vf[1] = bf_hi(raw);
+    for (int g = 0; g < G; ++g) {
+      const float resc = rsc[c.cw * kGMax + g];
+      float acc[DPL];
+      float* ra = red + (c.cw * G + g) * D + c.lane * DPL;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) acc[e] = ra[e] * resc;
+      const float* pr = prob + g * SR + c.cw * PPW;
+#pragma unroll 4
+      for (int j = 0; j < nvalid; ++j) {
+        float vf[DPL];
+        lds_row(vb, c.cw * PPW + j, vf);
+        const float pg = pr[j];
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) acc[e] = fmaf(pg, vf[e], acc[e]);
       }
 #pragma unroll
-      for (int g = 0; g < kGMax; ++g) {
-        if (g < G) {
-          const float pg = sc[g * kAttnPBMax + tl];
-          l_part[g] += pg;
-#pragma unroll
-          for (int e = 0; e < DPL; ++e) acc[g][e] = fmaf(pg, vf[e], acc[g][e]);
-        }
-      }
+      for (int e = 0; e < DPL; ++e) ra[e] = acc[e];
     }
     __syncwarp();
     if (c.lane == 0) mbar_arrive(empty0 + c.slot * 8);
@@ -751,84 +933,22 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
     if (blk + 1 < nblk) consumer_sync(c.nct);  // sc is rewritten by the next block
   }
   stamp(p, c, task_idx, 4);
-#pragma unroll
-  for (int g = 0; g < kGMax; ++g) {
-    if (g < G) {
-#pragma unroll
-      for (int e = 0; e < DPL; ++e) red[(c.cw * G + g) * D + c.lane * DPL + e] = acc[g][e];
-      if (c.lane == 0) lw[c.cw * kGMax + g] = l_part[g];
-    }
-  }
   consumer_sync(c.nct);
 
-  // cross-warp reduction, then either the final output (single chunk) or a partial record
-  const int PS = D + 2;  // partial record: o[D], m, l
-  float* part = p.part + ((size_t)(bidx * p.nkv + kvh) * p.attn_chunks) * (size_t)G * PS;
-  float* out = p.attn + (size_t)bidx * p.q_dim + (size_t)kvh * G * D;
+  // cross-warp reduction -> partial record (o[D], m, l) of every q head of the group
+  const int PS = D + 4;  // o[D], m, l, pad (records stay 16-byte aligned)
+  float* part = p.part + ((size_t)(bidx * p.nkv + kvh) * p.attn_chunks + slot) * (size_t)G * PS;
   for (int i = c.ctid; i < G * D; i += c.nct) {
     const int g = i / D, d = i - g * D;
-    float o = 0.f, l = 0.f;
-    for (int w = 0; w < p.C; ++w) { o += red[(w * G + g) * D + d]; l += lw[w * kGMax + g]; }
-    if (n_active == 1) out[i] = o / l;
-    else {
-      part[((size_t)slot * G + g) * PS + d] = o;
-      if (d == 0) {
-        part[((size_t)slot * G + g) * PS + D] = mw[g];  // warp 0's copy; identical in every warp
-        part[((size_t)slot * G + g) * PS + D + 1] = l;
-      }
+    float o = 0.f;
+    for (int w = 0; w < p.C; ++w) o += red[(w * G + g) * D + d];
+    part[(size_t)g * PS + d] = o;
+    if (d == 0) {
+      float l = 0.f;
+      for (int w = 0; w < p.C; ++w) l += lw[w * kGMax + g];
+      part[(size_t)g * PS + D] = mw[g];  // warp 0's copy; identical in every warp
+      part[(size_t)g * PS + D + 1] = l;
     }
-  }
-  if (n_active == 1) {
-    signal_counter(p, c, CTR_C);
-    stamp(p, c, task_idx, 7);
-    return;
-  }
-  consumer_sync(c.nct);
-  stamp(p, c, task_idx, 5);
-  if (c.ctid == 0) {
-    __threadfence();
-    const unsigned old = atom_acqrel_add(p.counters + t.sig_ctr, 1u);
-    hdr->misc[30] = (old == (unsigned)(t.layer * n_active + n_active - 1)) ? 1 : 0;
-  }
-  consumer_sync(c.nct);
-  stamp(p, c, task_idx, 6);
-  if (!hdr->misc[30]) { stamp(p, c, task_idx, 7); return; }
-  // last unit of this head: merge the partials (flash-decoding combine).  Phase 1: the
-  // per-chunk weights exp(m_s - M) / L into shared memory; phase 2: weighted sum, loads batched.
-  __threadfence();
-  for (int i = c.ctid; i < n_active * G; i += c.nct) {
-    const int s2 = i / G, g = i - s2 * G;
-    wts[s2 * kGMax + g] = __ldcg(part + ((size_t)s2 * G + g) * PS + D);       // m_s
-    red[i] = __ldcg(part + ((size_t)s2 * G + g) * PS + D + 1);                // l_s (red is free now)
-  }
-  consumer_sync(c.nct);
-  if (c.ctid < G) {
-    const int g = c.ctid;
-    float M = -INFINITY;
-    for (int s2 = 0; s2 < n_active; ++s2) M = fmaxf(M, wts[s2 * kGMax + g]);
-    float Lsum = 0.f;
-    for (int s2 = 0; s2 < n_active; ++s2) {
-      const float wgt = expf(wts[s2 * kGMax + g] - M);
-      wts[s2 * kGMax + g] = wgt;
-      Lsum = fmaf(red[s2 * G + g], wgt, Lsum);
-    }
-    const float inv = 1.0f / Lsum;
-    for (int s2 = 0; s2 < n_active; ++s2) wts[s2 * kGMax + g] *= inv;
-  }
-  consumer_sync(c.nct);
-  for (int i = c.ctid; i < G * D; i += c.nct) {
-    const int g = i / D, d = i - g * D;
-    const float* rec = part + (size_t)g * PS + d;
-    float O = 0.f;
-    int s2 = 0;
-    for (; s2 + 4 <= n_active; s2 += 4) {
-      const float a0 = __ldcg(rec + (size_t)(s2 + 0) * G * PS), a1 = __ldcg(rec + (size_t)(s2 + 1) * G * PS);
-      const float a2 = __ldcg(rec + (size_t)(s2 + 2) * G * PS), a3 = __ldcg(rec + (size_t)(s2 + 3) * G * PS);
-      O = fmaf(a0, wts[(s2 + 0) * kGMax + g], O); O = fmaf(a1, wts[(s2 + 1) * kGMax + g], O);
-      O = fmaf(a2, wts[(s2 + 2) * kGMax + g], O); O = fmaf(a3, wts[(s2 + 3) * kGMax + g], O);
-    }
-    for (; s2 < n_active; ++s2) O = fmaf(__ldcg(rec + (size_t)s2 * G * PS), wts[s2 * kGMax + g], O);
-    out[i] = O;
   }
   signal_counter(p, c, CTR_C);
   stamp(p, c, task_idx, 7);
@@ -954,18 +1074,25 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       return;
     }
   }
-  for (int ti = tb; ti < te; ++ti) {
+  auto fetch_task = [&](int ti) {
+    const int4* tp = reinterpret_cast<const int4*>(p.tasks + ti);
+    const int4 a = __ldg(tp), b = __ldg(tp + 1), cc = __ldg(tp + 2), d = __ldg(tp + 3);
     Task t;
-    {
-      const int4* tp = reinterpret_cast<const int4*>(p.tasks + ti);
-      int4* dst = reinterpret_cast<int4*>(&t);
-      dst[0] = __ldg(tp); dst[1] = __ldg(tp + 1); dst[2] = __ldg(tp + 2); dst[3] = __ldg(tp + 3);
-    }
+    t.type = a.x; t.layer = a.y; t.a = a.z; t.b = a.w;
+    t.k = b.x; t.kchunks = b.y; t.rt = b.z; t.ktc = b.w;
+    t.n_tiles = cc.x; t.n_ktiles = cc.y; t.w_off = cc.z; t.n_stages = cc.w;
+    t.wait_ctr = d.x; t.wait_val = d.y; t.sig_ctr = d.z; t.aux = d.w;
+    return t;
+  };
+  Task next = fetch_task(tb < te ? tb : 0);
+  for (int ti = tb; ti < te; ++ti) {
+    const Task t = next;
+    if (ti + 1 < te) next = fetch_task(ti + 1);  // the record is a DRAM miss: fetch one task ahead
     if (t.type == T_ATTN) {
-      if (p.D == 128) run_attn<128>(p, c, t, ti, scratch, hdr, ring, pos);
-      else run_attn<64>(p, c, t, ti, scratch, hdr, ring, pos);
+      if (p.D == 128) run_attn<128, 64 / CW>(p, c, t, ti, scratch, hdr, ring, pos);
+      else run_attn<64, 64 / CW>(p, c, t, ti, scratch, hdr, ring, pos);
     } else if (t.type != T_END) {
-      run_gemv(p, c, t, ti, scratch, hdr, ring, tok);
+      run_gemv(p, c, t, ti, scratch, hdr, ring, tok, pos);
     }
   }
 }
@@ -1068,6 +1195,7 @@ struct AdamkHandle_ {
   AdamkModelDesc desc{};
   int n_sms = 0, C = 0, n_stage = 0, stage_bytes = 0, n_tasks = 0, batch = 0, n_counters = 0;
   int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, pf_min_bytes = 0, pf_max_bytes = 0;
+  int xs_floats = 0;
   const unsigned* d_sm_stream = nullptr;
   size_t packed_weight_bytes = 0;  // matrix streams only
   size_t fparam_floats = 0;
@@ -1131,19 +1259,20 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
     return bad("attention chunking out of range");
   {
     const int pb = std::min(64, (h->stage_bytes / (d.head_dim * 2)) & ~7);
-    if (pb < 8 || pb % (4 * h->C)) return bad("stage_bytes too small: a K/V block must hold 4 positions per consumer warp");
+    if (pb != 64) return bad("stage_bytes too small: a K/V block is 64 positions (64 * head_dim * 2 bytes)");
   }
   const size_t need = ((size_t)kHeaderInts + (size_t)h->n_sms + 1 + (size_t)h->n_tasks * kTaskInts) * 4;
   if (task_table_bytes != need) return bad("task table size does not match its header");
   if (h->n_counters != CTR_HEAD0 + h->batch * d.n_kv_heads) return bad("counter count mismatch");
   h->smem_bytes = kSmemReserved + h->scratch_bytes + h->n_stage * h->stage_bytes;
   if (h->smem_bytes > kSmemMax) return bad("ring + scratch exceed 227 KB shared memory");
-  {  // the scratch region must hold the widest activation vector and the attention buffers
+  {  // the scratch region must hold the widest activation vector + merge weights, and the attention buffers
     const int G = d.n_q_heads / d.n_kv_heads;
     const int kmax = std::max(std::max(d.hidden, d.n_q_heads * d.head_dim), d.intermediate);
-    const size_t xb = align_up((size_t)kmax, kChunk) * 4;
-    const size_t ab = ((size_t)G * d.head_dim + (size_t)G * kAttnPBMax + (size_t)h->C * G * d.head_dim + 2 * (size_t)h->C * kGMax +
-                       2 * (size_t)d.head_dim + (size_t)kAttnChunksMax * kGMax) * 4;
+    h->xs_floats = (int)align_up((size_t)kmax, kChunk);
+    const size_t xb = ((size_t)h->xs_floats + 2 * (size_t)d.n_q_heads * h->attn_chunks) * 4;
+    const size_t ab = ((size_t)kGMax * (128 + 32) + 2 * (size_t)kGMax * (kAttnPBMax + 4) + (size_t)h->C * G * d.head_dim +
+                       3 * (size_t)h->C * kGMax + 2 * (size_t)d.head_dim) * 4;
     if ((size_t)h->scratch_bytes < std::max(xb, ab)) return bad("scratch_bytes too small for this model");
   }
   const int* sm_begin = tt + kHeaderInts;
@@ -1198,7 +1327,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   h->ws_qkv = take((size_t)qkv_rows * 4);
   h->ws_attn = take((size_t)d.n_q_heads * d.head_dim * 4);
   h->ws_act = take(align_up((size_t)d.intermediate, kChunk) * 4);
-  h->ws_part = take((size_t)d.n_kv_heads * h->attn_chunks * G * (d.head_dim + 2) * 4);
+  h->ws_part = take((size_t)d.n_kv_heads * h->attn_chunks * G * (d.head_dim + 4) * 4);
   h->ws_lm_val = take((size_t)h->n_sms * 4);
   h->ws_lm_idx = take((size_t)h->n_sms * 4);
   h->ws_total = o;
@@ -1340,6 +1469,7 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
   p.C = h->C; p.n_stage = h->n_stage; p.stage_bytes = h->stage_bytes; p.attn_chunks = h->attn_chunks;
   p.attn_min_chunk = h->attn_min_chunk; p.scratch_bytes = h->scratch_bytes; p.n_lm_tasks = h->n_lm_tasks;
   p.n_counters = h->n_counters;
+  p.xs_floats = h->xs_floats;
   p.tasks = h->d_tasks; p.sm_begin = h->d_sm_begin; p.sm_stream = h->d_sm_stream;
   p.pf_min_bytes = h->pf_min_bytes; p.pf_max_bytes = h->pf_max_bytes;
   p.wpacked = h->wpacked; p.fparams = h->fparams;

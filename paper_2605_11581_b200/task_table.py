@@ -127,9 +127,12 @@ def scratch_bytes(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> in
     """Shared-memory scratch: the fp32 activation vector of the widest GEMV, or
     the attention unit's q / scores / cross-warp reduction buffers."""
     kpad_max = max(_ceil_div(k, KCHUNK) * KCHUNK for k in (cfg.hidden, cfg.q_dim, cfg.intermediate))
-    x_bytes = batch * kpad_max * 4
+    nkv = cfg.n_kv_heads
+    attn_chunks = max(1, min(148 // (batch * nkv), ATTN_CHUNKS_MAX))
+    x_bytes = (batch * kpad_max + 2 * cfg.n_q_heads * ATTN_CHUNKS_MAX) * 4   # activation vector + split-KV merge (m, l)
     g, d, c = cfg.group, cfg.head_dim, sched.consumer_warps
-    attn_bytes = (g * d + g * ATTN_PBMAX + c * g * d + 2 * c * 8 + 2 * d + ATTN_CHUNKS_MAX * 8) * 4
+    attn_bytes = (8 * 160 + 2 * 8 * (ATTN_PBMAX + 4) + c * g * d + 3 * c * 8 + 2 * d) * 4
+    del attn_chunks
     return _ceil_div(max(x_bytes, attn_bytes), 1024) * 1024
 
 
@@ -258,9 +261,11 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
             for kvh in range(nkv):
                 for c in range(attn_chunks):
                     sm = ((b * nkv + kvh) * attn_chunks + c) % n_sms
+                    # every unit (active at this context length or not) signals CTR_C once
                     per_sm[sm].append([T_ATTN, layer, kvh, c, 0, 0, 0, 0, 0, 0, 0, 0,
-                                       CTR_B, done[CTR_B], CTR_HEAD0 + b * nkv + kvh, b])
-        done[CTR_D] += gemv(T_OPROJ, layer, cfg.hidden, cfg.q_dim, 1, CTR_C, (layer + 1) * batch * nkv, CTR_D)
+                                       CTR_B, done[CTR_B], CTR_C, b])
+        done[CTR_D] += gemv(T_OPROJ, layer, cfg.hidden, cfg.q_dim, 1, CTR_C,
+                            (layer + 1) * batch * nkv * attn_chunks, CTR_D)
         done[CTR_E] += gemv(T_GATEUP, layer, 2 * cfg.intermediate, cfg.hidden, 2, CTR_D, done[CTR_D], CTR_E)
         done[CTR_A] += gemv(T_DOWN, layer, cfg.hidden, cfg.intermediate, 1, CTR_E, done[CTR_E], CTR_A)
     n_lm = gemv(T_LMHEAD, cfg.n_layers, cfg.vocab, cfg.hidden, 1, CTR_A, done[CTR_A], CTR_F)

@@ -87,22 +87,14 @@ def _simulate_counters(table: tt.TaskTable, ctx: int):
                 t = table.tasks[pc[sm]]
                 ttype = int(t[tt.F_TYPE])
                 if ttype == tt.T_ATTN and int(t[tt.F_B]) >= n_active:
+                    counters[tt.CTR_C] += 1      # inactive units only keep the counter target static
                     pc[sm] += 1
                     progressed = True
                     continue
                 wc, wv = int(t[tt.F_WAITCTR]), int(t[tt.F_WAITVAL])
                 if wc >= 0 and counters[wc] < wv:
                     break
-                if ttype == tt.T_ATTN:
-                    hc = int(t[tt.F_SIGCTR])
-                    old = counters[hc]
-                    counters[hc] += 1
-                    if n_active == 1 or old == int(t[tt.F_LAYER]) * n_active + n_active - 1:
-                        counters[tt.CTR_C] += 1
-                    if n_active == 1:
-                        counters[hc] -= 1   # single-chunk units do not touch the head counter
-                else:
-                    counters[int(t[tt.F_SIGCTR])] += 1
+                counters[int(t[tt.F_SIGCTR])] += 1
                 pc[sm] += 1
                 progressed = True
         rounds += 1
@@ -116,7 +108,7 @@ def test_counter_protocol_has_no_deadlock(ctx):
     table = tt.build_task_table(TINY, SCHED_TINY, n_sms=148)
     _, counters = _simulate_counters(table, ctx)
     assert counters[tt.CTR_F] == table.header[12]
-    assert counters[tt.CTR_C] == TINY.n_layers * TINY.n_kv_heads
+    assert counters[tt.CTR_C] == TINY.n_layers * TINY.n_kv_heads * table.attn_chunks
 
 
 def test_counter_protocol_full_model_and_small_gpu():

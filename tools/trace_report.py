@@ -76,7 +76,7 @@ def report(plug, tr):
     segs = {}
     for r in rows:
         segs.setdefault(r["op"], []).append(r["seg"])
-    print("mean time of stamps 2..7 after the dependency was met (us; nan = stamp unused by some task):")
+    print("mean time of stamps 2..7 after the dependency was met (us; attn: 2 q-prep, 5 K landed, 3 scores, 6 V landed, 4 PV, 7 end):")
     for op, a in segs.items():
         a = np.array(a)
         if len(a) > 2:
