@@ -70,7 +70,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except OSError:
             self.proc = None
@@ -145,14 +145,12 @@ def run_reference(args) -> None:
 def run_ours(args) -> None:
     from paper_2605_11581_b200.plugin import MegaKernelPlugin
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    from paper_2605_11581_b200.dist_utils import RankGroup
+
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    group = RankGroup()            # nccl when WORLD_SIZE > 1; N replicas, no data-path collective
+    rank, world, dist = group.rank, group.world, group.dist
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg = get_config(args.model)
@@ -195,7 +193,6 @@ def run_ours(args) -> None:
     e1.record()
     barrier()
     plug.check()
-    clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
     launches = plug.launches - launches0
 
@@ -223,15 +220,12 @@ def run_ours(args) -> None:
     e1.record()
     barrier()
     plug.check()
+    clocks = sampler.stop()
     ms_e2e = e0.elapsed_time(e1) / args.steps
 
-    times = torch.tensor([ms, ms_e2e], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(times, op=dist.ReduceOp.MAX)
-    ms, ms_e2e = float(times[0]), float(times[1])
+    ms, ms_e2e = group.max_over_ranks([ms, ms_e2e], device=dev)
     if rank != 0:
-        if dist is not None:
-            dist.destroy_process_group()
+        group.close()
         return
 
     peak, peak_kind = measured_peak()
@@ -261,8 +255,7 @@ def run_ours(args) -> None:
         res = cpu_decode_sample(cfg, w_cpu, prompt, n_steps=args.cpu_steps)
         line["cpu_baseline"] = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line))
-    if dist is not None:
-        dist.destroy_process_group()
+    group.close()
 
 
 def main() -> None:

@@ -166,3 +166,26 @@ def test_error_paths():
     with pytest.raises(AdamkError):          # step before bind_weights
         plug.decode_step(1, 0)
     plug.close()
+
+
+def test_hybrid_engine_generate_matches_oracle():
+    """Engine hook: prefill (decode-path backend) then a device-resident decode loop."""
+    from oracle.decode_ref import RefDecoder
+    from paper_2605_11581_b200.engine import HybridEngine
+    from paper_2605_11581_b200.weights import random_weights, rope_table
+
+    cfg = D128
+    w = random_weights(cfg, seed=0)
+    cos, sin = rope_table(cfg, 128)
+    ref = RefDecoder(cfg, w, 128, cos, sin)
+    g = torch.Generator().manual_seed(7)
+    prompt = torch.randint(0, cfg.vocab, (24,), generator=g).tolist()
+    want, logits = ref.generate(prompt, 24, stepwise_prefill=True)
+    eng = HybridEngine(cfg, w, max_ctx=128, schedule=SCHEDS["c8"])
+    res = eng.generate(prompt, 24)
+    srt = torch.stack(logits).sort(dim=1).values
+    margin = (srt[:, -1] - srt[:, -2]).numpy()
+    first_tie = int(np.argmax(margin < 1e-4)) if (margin < 1e-4).any() else 24
+    assert res.tokens[:first_tie] == want[:first_tie] and first_tie >= 12
+    assert res.prefill_launches == 23 and res.decode_launches == 24
+    eng.close()
