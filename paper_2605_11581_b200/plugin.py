@@ -66,10 +66,14 @@ def load_library() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not LIB.exists():
-        raise AdamkError(-100, f"{LIB} is not built; run `python -m paper_2605_11581_b200.build` "
+    import os
+    from pathlib import Path
+
+    path = Path(os.environ.get("ADAMK_LIB", str(LIB)))   # override: A/B runs of two builds of the same ABI
+    if not path.exists():
+        raise AdamkError(-100, f"{path} is not built; run `python -m paper_2605_11581_b200.build` "
                                "(there is no CPU fallback for the decode path)")
-    lib = C.CDLL(str(LIB))
+    lib = C.CDLL(str(path))
     lib.adamk_abi_version.restype = C.c_int
     lib.adamk_last_error.restype = C.c_char_p
     lib.adamk_device_sm_count.argtypes = [C.c_int, C.POINTER(C.c_int)]

@@ -69,14 +69,44 @@ def test_packed_stream_covers_every_weight_exactly_once(cfg):
             assert (ks == 1).all(), (layer, name, row)
 
 
-def _simulate_counters(table: tt.TaskTable, ctx: int):
-    """Replay the per-SM task lists against the counter protocol the kernel uses;
-    returns the number of rounds, raises on deadlock."""
+PHASE_OF = {tt.T_QKV: 0, tt.T_ATTN: 1, tt.T_OPROJ: 2, tt.T_GATEUP: 3, tt.T_DOWN: 4}
+
+
+def _simulate_dataflow(table: tt.TaskTable, ctx: int):
+    """Replay the per-SM task lists against the kernel's data dependencies (tagged-word
+    protocol): a task needs EVERY task of the previous phase to have published its
+    outputs (attention: every unit that is active at this context length).  Returns the
+    number of rounds; raises on deadlock."""
     cfg, sched = table.cfg, table.sched
     cl = max(sched.attn_min_chunk, -(-ctx // table.attn_chunks))
     cl = (cl + 7) & ~7
     n_active = -(-ctx // cl)
-    counters = np.zeros(table.n_counters, dtype=np.int64)
+    tasks = table.tasks
+    L = cfg.n_layers
+
+    def active(t):
+        return int(t[tt.F_TYPE]) != tt.T_ATTN or int(t[tt.F_B]) < n_active
+
+    total = {}
+    for t in tasks:
+        if active(t):
+            key = (int(t[tt.F_LAYER]), int(t[tt.F_TYPE]))
+            total[key] = total.get(key, 0) + 1
+    done = {k: 0 for k in total}
+
+    def ready(t) -> bool:
+        ty, layer = int(t[tt.F_TYPE]), int(t[tt.F_LAYER])
+        if ty == tt.T_LMHEAD:
+            prev = (L - 1, tt.T_DOWN)
+        elif ty == tt.T_QKV:
+            if layer == 0:
+                return True
+            prev = (layer - 1, tt.T_DOWN)
+        else:
+            prev = (layer, {tt.T_ATTN: tt.T_QKV, tt.T_OPROJ: tt.T_ATTN, tt.T_GATEUP: tt.T_OPROJ,
+                            tt.T_DOWN: tt.T_GATEUP}[ty])
+        return done[prev] == total[prev]
+
     pc = table.sm_begin[:-1].astype(np.int64).copy()
     end = table.sm_begin[1:]
     rounds = 0
@@ -84,42 +114,48 @@ def _simulate_counters(table: tt.TaskTable, ctx: int):
         progressed = False
         for sm in range(table.n_sms):
             while pc[sm] < end[sm]:
-                t = table.tasks[pc[sm]]
-                ttype = int(t[tt.F_TYPE])
-                if ttype == tt.T_ATTN and int(t[tt.F_B]) >= n_active:
-                    counters[tt.CTR_C] += 1      # inactive units only keep the counter target static
-                    pc[sm] += 1
-                    progressed = True
-                    continue
-                wc, wv = int(t[tt.F_WAITCTR]), int(t[tt.F_WAITVAL])
-                if wc >= 0 and counters[wc] < wv:
-                    break
-                counters[int(t[tt.F_SIGCTR])] += 1
+                t = tasks[pc[sm]]
+                if active(t):
+                    if not ready(t):
+                        break
+                    done[(int(t[tt.F_LAYER]), int(t[tt.F_TYPE]))] += 1
                 pc[sm] += 1
                 progressed = True
         rounds += 1
         if not progressed:
-            raise AssertionError(f"deadlock: pcs {pc[:8]} counters {counters}")
-    return rounds, counters
+            raise AssertionError(f"deadlock: pcs {pc[:8]}")
+    return rounds, done
 
 
 @pytest.mark.parametrize("ctx", [1, 8, 9, 100, 600])
-def test_counter_protocol_has_no_deadlock(ctx):
+def test_dataflow_has_no_deadlock(ctx):
     table = tt.build_task_table(TINY, SCHED_TINY, n_sms=148)
-    _, counters = _simulate_counters(table, ctx)
-    assert counters[tt.CTR_F] == table.header[12]
-    assert counters[tt.CTR_C] == TINY.n_layers * TINY.n_kv_heads * table.attn_chunks
+    _, done = _simulate_dataflow(table, ctx)
+    assert done[(TINY.n_layers, tt.T_LMHEAD)] == table.header[12]
 
 
-def test_counter_protocol_full_model_and_small_gpu():
-    sched = tt.KernelSchedule(consumer_warps=8, n_stage=7, rows_per_tile=16, ktile_chunks=3)
+def test_every_sm_updates_the_residual_stream():
+    """The residual stream is replicated per CTA and brought up to date by the QKV, gate/up and
+    LM-head prologues: every SM must own exactly one of each per layer, even with zero rows."""
+    for n_sms in (148, 5, 300):
+        table = tt.build_task_table(TINY, SCHED_TINY, n_sms=n_sms)
+        for sm in range(n_sms):
+            ts = table.tasks_of(sm)
+            for layer in range(TINY.n_layers):
+                for ty in (tt.T_QKV, tt.T_GATEUP):
+                    assert ((ts[:, tt.F_TYPE] == ty) & (ts[:, tt.F_LAYER] == layer)).sum() == 1
+            assert (ts[:, tt.F_TYPE] == tt.T_LMHEAD).sum() == 1
+
+
+def test_dataflow_full_model_and_small_gpu():
+    sched = tt.KernelSchedule(consumer_warps=8, n_stage=5, rows_per_tile=16, ktile_chunks=3)
     table = tt.build_task_table(QWEN25_1P5B, sched, n_sms=148)
-    _simulate_counters(table, 513)
+    _simulate_dataflow(table, 513)
     s = table.summary()
     assert s["packed_weight_bytes"] * 1.0 <= QWEN25_1P5B.weight_bytes_per_token()
     assert s["stream_bytes_max"] - s["stream_bytes_min"] <= 64 * 1024
     small = tt.build_task_table(TINY, SCHED_TINY, n_sms=5)
-    _simulate_counters(small, 33)
+    _simulate_dataflow(small, 33)
 
 
 def test_schedule_validation():
