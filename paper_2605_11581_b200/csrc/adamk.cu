@@ -8,16 +8,22 @@
 //              cp.async.bulk (TMA, SASS UBLKCP) into an n_stage-deep shared-memory
 //              ring; never looks at activations, so it runs ahead across operator
 //              and layer boundaries (the paper's "asynchronous prefetching and
-//              logical decoupling") limited only by free ring slots.
-//   Consumer : warps 1..C.  Wait on the operator's dependency counter, stage the
-//              fp32 activation vector in shared memory (fusing RMSNorm), then GEMV
-//              out of the ring with LDS.128 + FFMA and warp-shuffle reductions.
-//   Storer   : the consumers' epilogue (bias / residual / SiLU*up / argmax) and the
-//              release of the operator's global counter.
+//              logical decoupling") limited by free ring slots and by
+//              a cap on the stages in flight (keeps the loaded memory latency low).
+//   Consumer : warps 1..C.  Gather the operator's input vector, stage it in shared
+//              memory (fusing RMSNorm), then GEMV out of the ring with LDS.128 +
+//              packed FFMA2.  The warps of a CTA form a WR x WK grid per operator:
+//              WR row groups of up to 8 rows, WK interleaved K groups.
+//   Storer   : the consumers' epilogue (bias / residual / SiLU*up / argmax).
 // Page states Empty -> Locked -> Ready (planner.py:84-94) = ring slot `empty`
 // mbarrier phase -> TMA in flight -> `full` mbarrier phase.
-// Inter-SM dependencies are monotonically increasing global counters whose target
-// values are fixed in the task table ("path solidification").
+//
+// Inter-SM dependencies carry no counters and no fences: every activation element is
+// published as one 64-bit word {fp32 value, 32-bit tag} with a single relaxed store, and
+// the consumers of the vector poll the words themselves until every tag equals the
+// (step, layer) tag they expect -- the data is its own flag.  Which words an operator
+// reads and the tag it expects are fixed by the task table ("path solidification",
+// PAPER.md:197); nothing is scheduled at run time.
 //
 // Numerical contract (shared with oracle/decode_ref.py): bf16 weights used exactly,
 // fp32 activations and accumulation, bf16 KV cache, fp32 RoPE tables from the host.
@@ -38,28 +44,32 @@
 // ----------------------------------------------------------------------------------
 namespace {
 
+typedef unsigned long long u64;
+
 constexpr int kMagic = 0x4B4D4441;
-constexpr int kVersion = 1;
+constexpr int kVersion = 2;
 constexpr int kHeaderInts = 16;
 constexpr int kTaskInts = 16;
 constexpr int kChunk = 256;          // K elements per chunk
 constexpr int kSmemMax = 232448;
-constexpr int kSmemReserved = 1024;  // barriers + reduction scratch
+constexpr int kSmemReserved = 4096;  // barriers + reduction scratch
 constexpr int kMaxStages = 16;
-constexpr int kAttnPBMax = 128;      // positions per attention block (8 per consumer warp)
+constexpr int kAttnBlock = 64;       // positions per K (or V) ring stage
+constexpr int kAttnWarps = 8;        // consumer warps that take part in an attention unit
 constexpr int kAttnChunksMax = 128;  // split-KV units per (sequence, kv head)
 constexpr int kGMax = 8;             // max q heads per kv head
+constexpr int kRW = 8;               // max rows per warp per tile
+constexpr int kTagStride = 256;      // tag = epoch * kTagStride + layer + 1
 
-enum TaskType { T_END = 0, T_QKV = 1, T_ATTN = 2, T_OPROJ = 3, T_GATEUP = 4, T_DOWN = 5, T_LMHEAD = 6 };
-enum Ctr { CTR_A = 0, CTR_B = 1, CTR_C = 2, CTR_D = 3, CTR_E = 4, CTR_F = 5, CTR_HEAD0 = 6 };
+enum TaskType { T_END = 0, T_QKV = 1, T_ATTN = 2, T_OPROJ = 3, T_GATEUP = 4, T_DOWN = 5, T_LMHEAD = 6, T_MERGE = 7 };
 
 struct Task {  // 64 bytes
-  int type, layer, a, b, k, kchunks, rt, ktc, n_tiles, n_ktiles, w_off, n_stages, wait_ctr, wait_val, sig_ctr, aux;
+  int type, layer, a, b, k, kchunks, rt, ktc, n_tiles, n_ktiles, w_off, geom, r12, r13, r14, aux;
 };
 static_assert(sizeof(Task) == kTaskInts * 4, "task record is 64 bytes");
 
 // device error codes written to the host-mapped status block
-enum DevErr { DE_NONE = 0, DE_WATCHDOG_CTR = 1, DE_WATCHDOG_FULL = 2, DE_WATCHDOG_EMPTY = 3, DE_BAD_POS = 4 };
+enum DevErr { DE_NONE = 0, DE_WATCHDOG_TAG = 1, DE_WATCHDOG_FULL = 2, DE_WATCHDOG_EMPTY = 3, DE_BAD_POS = 4, DE_WATCHDOG_INFLIGHT = 5 };
 
 struct KParams {
   // model
@@ -67,13 +77,13 @@ struct KParams {
   int has_bias, qk_norm;
   float eps;
   // schedule
-  int C, n_stage, stage_bytes, attn_chunks, attn_min_chunk, scratch_bytes, n_lm_tasks, n_counters;
-  int xs_floats;  // floats reserved for the staged activation vector; the merge weights follow it
+  int C, n_stage, stage_bytes, attn_chunks, attn_min_chunk, scratch_bytes, n_lm_tasks, inflight;
+  int task_cache_bytes;    // shared-memory copy of this SM's task list (32-byte packed records)
+  unsigned poll_sleep_ns;  // back-off between polls of a not-yet-complete vector (0 = none)
   // task table
   const Task* tasks;
   const int* sm_begin;
   const unsigned* sm_stream;  // [n_sms + 1] packed-stream range of every SM (16-byte units)
-  int pf_min_bytes, pf_max_bytes;  // L2 prefetch distance ahead of the ring: steady state / while stalled
   // weights
   const uint8_t* wpacked;   // tile-major bf16 weight streams
   const float* fparams;     // fp32 norm gains / biases
@@ -84,24 +94,26 @@ struct KParams {
   // per-step buffers
   __nv_bfloat16* kcache;
   __nv_bfloat16* vcache;
-  float* h_a;
-  float* h_b;
-  float* qkv;
-  float* attn;
-  float* act;
-  float* part;
+  // tagged activation vectors ({fp32, tag} words)
+  u64* ll_hx;    // [2][H]   layer input, ping-pong by layer parity
+  u64* ll_hm;    // [H]      hidden state after attention
+  u64* ll_qkv;   // [qkv_rows]
+  u64* ll_attn;  // [q_dim]  merged attention output
+  u64* ll_act;   // [I]
+  u64* ll_part;  // [nkv][attn_chunks][G][D + 2]  split-KV partial records (o[D], m, l)
   float* lm_val;
   int* lm_idx;
-  unsigned* counters;
+  unsigned* sync;  // [0] = epoch, [1] = CTAs that finished the LM head
   float* logits;
   int* tokens;
   int* positions;
   int* next_tokens;
   int* status;  // host-mapped, 8 ints
   int auto_advance;
-  int probe;    // 1 = stream probe: consumers skip dependencies and epilogues; 2 = also skip the math
+  int probe;    // 1 = stream probe: consumers skip dependencies and epilogues; 2 = also skip the math;
+                // 3 = like 1 but the Loader re-reads an L2-resident window; 4 = consumers only (no Loader, no waits)
   float* probe_sink;
-  unsigned long long* trace;  // optional [n_tasks][8] globaltimer stamps (0 start, 1 dependency met, 2 prologue done, 7 end, 3-6 op specific)
+  u64* trace;  // optional [n_tasks][8] globaltimer stamps (0 start, 1 inputs gathered, 2 body done, 7 end, 3-6 op specific)
 };
 
 // ----------------------------------------------------------------------------------
@@ -129,6 +141,17 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t bar, uint32_t parity)
       : "memory");
   return ok;
 }
+__device__ __forceinline__ uint32_t mbar_try_wait_hint(uint32_t bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(ns)
+      : "memory");
+  return ok;
+}
 // TMA bulk copy global -> shared, completion on an mbarrier (SASS: UBLKCP)
 __device__ __forceinline__ void tma_bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -146,27 +169,15 @@ __device__ __forceinline__ void tma_bulk_g2s_hint(uint32_t dst, const void* src,
       "l"(src), "r"(bytes), "r"(bar), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ void l2_prefetch_bulk(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-  unsigned long long t;
+__device__ __forceinline__ u64 globaltimer_ns() {
+  u64 t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
-}
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned atom_acqrel_add(unsigned* p, unsigned v) {
   unsigned old;
@@ -195,11 +206,24 @@ __device__ __forceinline__ float warp_sum(float v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+
+// ---- tagged words: {fp32 value (low half), tag (high half)} ----
+// A 64-bit aligned scalar store / load is single-copy atomic, so a reader that sees the
+// expected tag also sees the value written with it: no fence, no separate flag.
+__device__ __forceinline__ void ll_store(u64* p, float v, unsigned tag) {
+  const u64 w = ((u64)tag << 32) | (u64)__float_as_uint(v);
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
 }
+__device__ __forceinline__ u64 ll_load(const u64* p) {
+  u64 w;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+__device__ __forceinline__ void ll_load2(const u64* p, u64& a, u64& b) {  // 16-byte aligned pair of words
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ unsigned ll_tag(u64 w) { return (unsigned)(w >> 32); }
+__device__ __forceinline__ float ll_val(u64 w) { return __uint_as_float((unsigned)w); }
 
 constexpr long long kWatchdogCycles = 6000000000LL;  // ~3 s at 2 GHz; a step takes < 1 ms
 
@@ -214,17 +238,6 @@ __device__ __noinline__ void dev_fail(const KParams& p, int code, int task, int 
   __trap();
 }
 
-__device__ __forceinline__ uint32_t mbar_try_wait_hint(uint32_t bar, uint32_t parity, uint32_t ns) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-      "selp.b32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity), "r"(ns)
-      : "memory");
-  return ok;
-}
 __device__ __noinline__ void mbar_wait_slow(const KParams& p, uint32_t bar, uint32_t parity, int code, int task) {
   const long long t0 = clock64();
   while (!mbar_try_wait_hint(bar, parity, 2000u)) {
@@ -235,14 +248,30 @@ __device__ __forceinline__ void mbar_wait(const KParams& p, uint32_t bar, uint32
   if (!mbar_try_wait(bar, parity)) mbar_wait_slow(p, bar, parity, code, task);
 }
 
+// slow paths of the tagged-word polls (out of line: they are cold and keep the hot code small)
+__device__ __noinline__ u64 ll_spin(const KParams& p, const u64* addr, unsigned tag, int task) {
+  const long long t0 = clock64();
+  u64 w;
+  while (ll_tag(w = ll_load(addr)) != tag) {
+    if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task, (int)ll_tag(w), (int)tag, (int)((uintptr_t)addr & 0x7fffffff));
+  }
+  return w;
+}
+__device__ __forceinline__ float ll_wait(const KParams& p, const u64* addr, unsigned tag, int task) {
+  u64 w = ll_load(addr);
+  if (ll_tag(w) != tag) w = ll_spin(p, addr, tag, task);
+  return ll_val(w);
+}
+
 // ----------------------------------------------------------------------------------
 // shared-memory layout
 // ----------------------------------------------------------------------------------
 struct SmemHdr {
-  unsigned long long full[kMaxStages];
-  unsigned long long empty[kMaxStages];
+  u64 full[kMaxStages];
+  u64 empty[kMaxStages];
   float red[64];
   int misc[32];
+  float red2[2][8][32];  // cross-K-group partial sums of a tile: [tile parity][K group][row]
 };
 static_assert(sizeof(SmemHdr) <= kSmemReserved, "smem header too large");
 
@@ -253,46 +282,22 @@ struct ConsumerCtx {
   int lane;
   int ctid;           // thread index among consumers
   int nct;            // number of consumer threads
+  unsigned epoch;     // step sequence number (tag prefix)
   float rs;           // RMSNorm scale of the current GEMV's input (applied in the epilogue), else 1
-  float best_val;     // LM-head running argmax (lane 0 of each warp)
+  float best_val;     // LM-head running argmax (epilogue lanes)
   int best_idx;
 };
+
+__device__ __forceinline__ unsigned tag_of(const ConsumerCtx& c, int layer) { return c.epoch * kTagStride + (unsigned)layer + 1u; }
 
 __device__ __forceinline__ void stamp(const KParams& p, const ConsumerCtx& c, int task, int k) {
   if (p.trace && c.ctid == 0) p.trace[(size_t)task * 8 + k] = globaltimer_ns();
 }
 
-// ----------------------------------------------------------------------------------
-// dependency wait / signal
-// ----------------------------------------------------------------------------------
-__device__ __noinline__ void poll_counter_slow(const KParams& p, const unsigned* addr, int val, int ctr, int task) {
-  const long long t0 = clock64();
-  unsigned seen;
-  while ((seen = ld_relaxed_u32(addr)) < (unsigned)val) {
-    if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_CTR, task, ctr, (int)seen, val);
-  }
-}
-__device__ __forceinline__ void wait_counter(const KParams& p, const ConsumerCtx& c, int ctr, int val, int task) {
-  if (ctr >= 0 && !p.probe) {
-    if (c.ctid == 0) {
-      const unsigned* addr = p.counters + ctr;
-      if (ld_relaxed_u32(addr) < (unsigned)val) poll_counter_slow(p, addr, val, ctr, task);
-      fence_acq_rel_gpu();  // one acquire for the whole poll loop (no per-poll L1 invalidate)
-    }
-  }
-  consumer_sync(c.nct);
-}
-
-// all consumer threads have finished their global writes for this task
-__device__ __forceinline__ void signal_counter(const KParams& p, const ConsumerCtx& c, int ctr) {
-  consumer_sync(c.nct);
-  if (c.ctid == 0 && ctr >= 0 && !p.probe) red_release_add(p.counters + ctr, 1u);
-}
-
 // Split-KV geometry of one decode step, shared by the Loader (which streams the K/V
 // blocks of a unit through the ring) and the Consumers (which drain them).
 struct AttnGeom {
-  int CL, n_active, t0, n, PB, nblk;
+  int CL, n_active, t0, n, nblk;
 };
 __device__ __forceinline__ AttnGeom attn_geometry(const KParams& p, int pos, int slot) {
   AttnGeom g;
@@ -302,70 +307,83 @@ __device__ __forceinline__ AttnGeom attn_geometry(const KParams& p, int pos, int
   g.n_active = (ctx + g.CL - 1) / g.CL;
   g.t0 = slot * g.CL;
   g.n = min(ctx, g.t0 + g.CL) - g.t0;           // <= 0 for inactive slots
-  g.PB = min(64, (p.stage_bytes / (p.D * 2)) & ~7);  // positions per ring stage
-  g.nblk = g.n > 0 ? (g.n + g.PB - 1) / g.PB : 0;
+  g.nblk = g.n > 0 ? (g.n + kAttnBlock - 1) / kAttnBlock : 0;
   return g;
 }
 
-// Flash-decoding merge of the split-KV partial records, done by every consumer of the
-// attention output (O-projection prologue): xs[h*D + d] = sum_s w[h][s] * o_s[h][d] with
-// w = exp(m_s - M) / sum_s l_s exp(m_s - M).  `wts` holds n_q_heads * n_active floats.
-// All global loads of a phase are independent and issued back to back (one L2 round trip).
-__device__ __forceinline__ void attn_merge_into(const KParams& p, const ConsumerCtx& c, int pos, float* xs, int kpad,
-                                                float* wts) {
-  const AttnGeom ge = attn_geometry(p, pos, 0);
-  const int na = ge.n_active, D = p.D, G = p.G, PS = D + 4;
-  const float* part = p.part;  // [nkv][attn_chunks][G][PS]   (batch 1)
-  // phase 1: (m, l) of every (head, chunk) -> shared memory
-  for (int i = c.ctid; i < p.nq * na; i += c.nct) {
-    const int h = i / na, s2 = i - h * na;
-    const int kvh = h / G, g = h - kvh * G;
-    const float2 ml = __ldcg(reinterpret_cast<const float2*>(part + (((size_t)kvh * p.attn_chunks + s2) * G + g) * PS + D));
-    wts[i] = ml.x;
-    wts[p.nq * na + i] = ml.y;
-  }
-  consumer_sync(c.nct);
-  // phase 2: normalised weights, one warp per head, lanes over chunks
-  for (int h = c.cw; h < p.nq; h += p.C) {
-    float M = -INFINITY;
-    for (int s2 = c.lane; s2 < na; s2 += 32) M = fmaxf(M, wts[h * na + s2]);
-    M = warp_max(M);
-    float L = 0.f;
-    for (int s2 = c.lane; s2 < na; s2 += 32) {
-      const float wgt = expf(wts[h * na + s2] - M);
-      L = fmaf(wts[p.nq * na + h * na + s2], wgt, L);
-      wts[h * na + s2] = wgt;
+// ----------------------------------------------------------------------------------
+// gather of a tagged vector into shared memory
+// ----------------------------------------------------------------------------------
+// Every consumer thread owns the 16-byte word pairs i = ctid, ctid + nct, ... of the vector, issues
+// up to four loads back to back, and re-polls only the words whose tag is still old.  NORM: the
+// values are multiplied by the RMSNorm gain while staged and sum(x^2) is returned (per thread).
+__device__ __noinline__ float ll_gather(const KParams& p, int ctid, int nct, const u64* src, int n, int kpad,
+                                        unsigned tag, float* xs, const float* gain, int task) {
+  const bool NORM = gain != nullptr;
+  const int n2 = n >> 1, kp2 = kpad >> 1;
+  float ss = 0.f;
+  for (int i0 = ctid; i0 < kp2; i0 += 4 * nct) {
+    float2 g[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // static operand first: a DRAM miss under the weight stream, overlapped with the poll
+      const int i = i0 + u * nct;
+      g[u] = (NORM && i < n2) ? __ldg(reinterpret_cast<const float2*>(gain) + i) : make_float2(1.f, 1.f);
     }
-    L = warp_sum(L);
-    const float inv = 1.0f / L;
-    for (int s2 = c.lane; s2 < na; s2 += 32) wts[h * na + s2] *= inv;
-  }
-  consumer_sync(c.nct);
-  // phase 3: weighted sum, four output dims per thread, chunks batched by four
-  const int q4 = p.q_dim >> 2;
-  for (int i = c.ctid; i < (kpad >> 2); i += c.nct) {
-    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < q4) {
-      const int h = (i * 4) / D, d = i * 4 - h * D;
-      const int kvh = h / G, g = h - kvh * G;
-      const float* rec = part + ((size_t)kvh * p.attn_chunks * G + g) * PS + d;
-      const size_t cs = (size_t)G * PS;
-      const float* w = wts + h * na;
-      for (int s0 = 0; s0 < na; s0 += 8) {  // eight independent 16-byte loads in flight per thread
-        float4 a[8];
+    u64 a[4], b[4];
+    long long t0 = 0;
+    for (;;) {  // re-issue the whole batch until every tag is current (one round trip per attempt)
+      bool ok = true;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          a[u] = (s0 + u < na) ? __ldcg(reinterpret_cast<const float4*>(rec + (s0 + u) * cs)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * nct;
+        if (i < n2) ll_load2(src + 2 * i, a[u], b[u]);
+      }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const float wu = (s0 + u < na) ? w[s0 + u] : 0.f;
-          x.x = fmaf(a[u].x, wu, x.x); x.y = fmaf(a[u].y, wu, x.y); x.z = fmaf(a[u].z, wu, x.z); x.w = fmaf(a[u].w, wu, x.w);
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * nct;
+        if (i < n2) ok = ok && ll_tag(a[u]) == tag && ll_tag(b[u]) == tag;
+      }
+      if (ok) break;
+      if (p.poll_sleep_ns) __nanosleep(p.poll_sleep_ns);
+      if (t0 == 0) t0 = clock64();
+      else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task, (int)ll_tag(a[0]), (int)tag, i0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * nct;
+      if (i < kp2) {
+        float2 v = make_float2(0.f, 0.f);
+        if (i < n2) {
+          v.x = ll_val(a[u]); v.y = ll_val(b[u]);
+          ss = fmaf(v.x, v.x, fmaf(v.y, v.y, ss));
+          v.x *= g[u].x; v.y *= g[u].y;
         }
+        reinterpret_cast<float2*>(xs)[i] = v;
       }
     }
-    reinterpret_cast<float4*>(xs)[i] = x;
   }
-  consumer_sync(c.nct);
+  return ss;
+}
+
+// N words base[0], base[stride], ... gathered by one thread: all loads in flight together, re-polled as a batch.
+template <int N>
+__device__ __forceinline__ void ll_wait_strided(const KParams& p, const u64* base, int stride, unsigned tag, float (&out)[N],
+                                                int task) {
+  u64 w[N];
+  long long t0 = 0;
+  for (;;) {
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < N; ++j) w[j] = ll_load(base + (size_t)j * stride);
+#pragma unroll
+    for (int j = 0; j < N; ++j) ok = ok && ll_tag(w[j]) == tag;
+    if (ok) break;
+    if (p.poll_sleep_ns) __nanosleep(p.poll_sleep_ns);
+    if (t0 == 0) t0 = clock64();
+    else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task, (int)ll_tag(w[0]), (int)tag, -1);
+  }
+#pragma unroll
+  for (int j = 0; j < N; ++j) out[j] = ll_val(w[j]);
 }
 
 // ----------------------------------------------------------------------------------
@@ -373,94 +391,68 @@ __device__ __forceinline__ void attn_merge_into(const KParams& p, const Consumer
 // ----------------------------------------------------------------------------------
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + expf(-g)); }
 
-// fp32 hidden-state element of the layer input: layer 0 reads the embedding row
-__device__ __forceinline__ float4 load_h4(const KParams& p, int layer, bool mid, int tok, int i4) {
-  if (mid) return __ldcg(reinterpret_cast<const float4*>(p.h_b) + i4);
-  if (layer == 0) {
-    const uint2 raw = __ldg(reinterpret_cast<const uint2*>(p.embed + (size_t)tok * p.H) + i4);
-    return make_float4(bf_lo(raw.x), bf_hi(raw.x), bf_lo(raw.y), bf_hi(raw.y));
-  }
-  return __ldcg(reinterpret_cast<const float4*>(p.h_a) + i4);
-}
-__device__ __forceinline__ float load_h1(const KParams& p, int layer, int tok, int i) {
-  if (layer == 0) return __bfloat162float(p.embed[(size_t)tok * p.H + i]);
-  return __ldcg(p.h_a + i);
-}
-
-constexpr int kPreG = 4;  // float4 gain vectors per thread preloaded before the dependency wait
-
 __device__ __forceinline__ const float* gemv_gain(const KParams& p, const Task& t) {
   if (t.type == T_LMHEAD) return p.fparams + p.fp_final;
   return p.fparams + (size_t)t.layer * p.fp_layer_stride + (t.type == T_GATEUP ? p.fp_ln2 : p.fp_ln1);
 }
 
 // Stage the activation vector of a GEMV in shared memory (fp32, zero padded to kpad).
-__device__ __forceinline__ void gemv_prologue(const KParams& p, ConsumerCtx& c, const Task& t, float* xs,
-                                              SmemHdr* hdr, int tok, int pos, const float4 (&g4)[kPreG]) {
+__device__ __forceinline__ void gemv_prologue(const KParams& p, ConsumerCtx& c, const Task& t, int ti, float* xs,
+                                              SmemHdr* hdr, int tok) {
   const int kpad = t.kchunks * kChunk;
   const int type = t.type;
   c.rs = 1.0f;
-  if (type == T_OPROJ) {  // input = merged split-KV attention output
-    attn_merge_into(p, c, pos, xs, kpad, xs + p.xs_floats);
-    return;
-  }
-  if (type == T_DOWN) {
-    const int k4 = t.k >> 2, kp4 = kpad >> 2;
-    for (int i0 = c.ctid; i0 < kp4; i0 += 4 * c.nct) {  // four independent loads in flight per thread
-      float4 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * c.nct;
-        v[u] = (i < k4) ? __ldcg(reinterpret_cast<const float4*>(p.act) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * c.nct;
-        if (i < kp4) reinterpret_cast<float4*>(xs)[i] = v[u];
-      }
-    }
+  if (type == T_OPROJ) {
+    ll_gather(p, c.ctid, c.nct, p.ll_attn, p.q_dim, kpad, tag_of(c, t.layer), xs, nullptr, ti);
     consumer_sync(c.nct);
     return;
   }
-  // RMSNorm-fused prologues: QKV (ln1 over layer input), GATEUP (ln2 over h_mid), LMHEAD (final norm).
+  if (type == T_DOWN) {
+    ll_gather(p, c.ctid, c.nct, p.ll_act, p.I, kpad, tag_of(c, t.layer), xs, nullptr, ti);
+    consumer_sync(c.nct);
+    return;
+  }
+  // RMSNorm-fused prologues: QKV (ln1 over the layer input), GATEUP (ln2 over h_mid), LMHEAD (final norm).
   // Single pass: stage h * gain, accumulate sum(h^2); the scalar rsqrt(mean + eps) commutes with
   // the dot products and is applied to each output row in the epilogue.
-  const bool mid = (type == T_GATEUP);
-  const int layer = (type == T_LMHEAD) ? p.L : t.layer;  // LM head reads h_a (layer index L > 0)
-  const float4* gain4 = reinterpret_cast<const float4*>(gemv_gain(p, t));
-  const int h4 = p.H >> 2, kp4 = kpad >> 2;
+  const float* gain = gemv_gain(p, t);
   float ss = 0.f;
-  auto stage = [&](int i, const float4& g) {
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < h4) {
-      v = load_h4(p, layer, mid, tok, i);
-      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-      v.x *= g.x; v.y *= g.y; v.z *= g.z; v.w *= g.w;
+  if (type == T_QKV && t.layer == 0) {  // layer 0 reads the embedding row (bf16) directly
+    const int h2 = p.H >> 1, kp2 = kpad >> 1;
+    for (int i = c.ctid; i < kp2; i += c.nct) {
+      float2 v = make_float2(0.f, 0.f);
+      if (i < h2) {
+        const uint32_t raw = __ldg(reinterpret_cast<const uint32_t*>(p.embed + (size_t)tok * p.H) + i);
+        v.x = bf_lo(raw); v.y = bf_hi(raw);
+        ss = fmaf(v.x, v.x, fmaf(v.y, v.y, ss));
+        const float2 g = __ldg(reinterpret_cast<const float2*>(gain) + i);
+        v.x *= g.x; v.y *= g.y;
+      }
+      reinterpret_cast<float2*>(xs)[i] = v;
     }
-    reinterpret_cast<float4*>(xs)[i] = v;
-  };
-#pragma unroll
-  for (int k = 0; k < kPreG; ++k) {
-    const int i = c.ctid + k * c.nct;
-    if (i < kp4) stage(i, g4[k]);
+  } else {
+    const int layer = (type == T_LMHEAD) ? p.L : t.layer;
+    const u64* src = (type == T_GATEUP) ? p.ll_hm : p.ll_hx + (size_t)(layer & 1) * p.H;
+    ss = ll_gather(p, c.ctid, c.nct, src, p.H, kpad, tag_of(c, layer), xs, gain, ti);
   }
-  for (int i = c.ctid + kPreG * c.nct; i < kp4; i += c.nct)
-    stage(i, i < h4 ? __ldg(gain4 + i) : make_float4(0.f, 0.f, 0.f, 0.f));
   ss = warp_sum(ss);
-  if (c.lane == 0) hdr->red[c.cw] = ss;
+  float* red = hdr->red + (ti & 1) * 16;  // by task parity: a warp that runs ahead writes the other half
+  if (c.lane == 0) red[c.cw] = ss;
   consumer_sync(c.nct);
   float tot = 0.f;
-  for (int w = 0; w < p.C; ++w) tot += hdr->red[w];
+  for (int w = 0; w < p.C; ++w) tot += red[w];
   c.rs = rsqrtf(tot / (float)p.H + p.eps);
 }
 
-// Epilogue operand of one output row that is known before the dot product finishes (bias,
-// residual input): loaded ahead of the K loop so its latency hides behind the stream.
-__device__ __forceinline__ float load_eop(const KParams& p, const Task& t, int vrow, int tok) {
+// Epilogue operand of one output row (bias, residual input).  Residuals are tagged words of a
+// vector this step has already completed; the tag is still checked (cheap) rather than assumed.
+__device__ __forceinline__ float load_eop(const KParams& p, const ConsumerCtx& c, const Task& t, int ti, int vrow, int tok) {
   switch (t.type) {
     case T_QKV: return p.has_bias ? __ldg(p.fparams + (size_t)t.layer * p.fp_layer_stride + p.fp_bias + vrow) : 0.f;
-    case T_OPROJ: return load_h1(p, t.layer, tok, vrow);
-    case T_DOWN: return __ldcg(p.h_b + vrow);
+    case T_OPROJ:
+      if (t.layer == 0) return __bfloat162float(p.embed[(size_t)tok * p.H + vrow]);
+      return ll_wait(p, p.ll_hx + (size_t)(t.layer & 1) * p.H + vrow, tag_of(c, t.layer), ti);
+    case T_DOWN: return ll_wait(p, p.ll_hm + vrow, tag_of(c, t.layer), ti);
     default: return 0.f;
   }
 }
@@ -468,10 +460,10 @@ __device__ __forceinline__ float load_eop(const KParams& p, const Task& t, int v
 __device__ __forceinline__ void gemv_epilogue(const KParams& p, ConsumerCtx& c, const Task& t, int vrow, float v,
                                               float v_pair, float eop) {
   switch (t.type) {
-    case T_QKV: p.qkv[vrow] = v + eop; break;
-    case T_OPROJ: p.h_b[vrow] = eop + v; break;
-    case T_GATEUP: p.act[vrow >> 1] = silu(v) * v_pair; break;  // vrow even = gate, pair = up
-    case T_DOWN: p.h_a[vrow] = eop + v; break;
+    case T_QKV: ll_store(p.ll_qkv + vrow, v + eop, tag_of(c, t.layer)); break;
+    case T_OPROJ: ll_store(p.ll_hm + vrow, eop + v, tag_of(c, t.layer)); break;
+    case T_GATEUP: ll_store(p.ll_act + (vrow >> 1), silu(v) * v_pair, tag_of(c, t.layer)); break;  // vrow even = gate, pair = up
+    case T_DOWN: ll_store(p.ll_hx + (size_t)((t.layer + 1) & 1) * p.H + vrow, eop + v, tag_of(c, t.layer + 1)); break;
     case T_LMHEAD: {
       if (p.logits) p.logits[vrow] = v;
       if (v > c.best_val) { c.best_val = v; c.best_idx = vrow; }  // rows ascend: first max wins ties
@@ -480,89 +472,156 @@ __device__ __forceinline__ void gemv_epilogue(const KParams& p, ConsumerCtx& c, 
   }
 }
 
-// One 256-element K chunk of RW rows: acc[i] += w[i][chunk] . x[chunk].  bf16 -> fp32 is a
-// shift / mask per element; the products go through the packed FFMA2 pipe (sm_100).
-template <int RW, bool ALL>
-__device__ __forceinline__ void gemv_chunk(uint32_t waddr, uint32_t row_stride, uint32_t xaddr, int nrows,
-                                           float2 (&accA)[RW], float2 (&accB)[RW]) {
-  const float4 xa = lds128f(xaddr);
-  const float4 xb = lds128f(xaddr + 512);
+// Sum eight per-lane partials over the warp with 9 shuffles: after the call every lane holds the
+// total of row  4*bit4(lane) + 2*bit3(lane) + bit2(lane).
+__device__ __forceinline__ float reduce8(const float (&v)[kRW], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  float u[4], w[2];
 #pragma unroll
-  for (int i = 0; i < RW; ++i) {
-    if (ALL || i < nrows) {
-      const uint4 w = lds128u(waddr + i * row_stride);
-      accA[i] = __ffma2_rn(make_float2(bf_lo(w.x), bf_hi(w.x)), make_float2(xa.x, xa.y), accA[i]);
-      accB[i] = __ffma2_rn(make_float2(bf_lo(w.y), bf_hi(w.y)), make_float2(xa.z, xa.w), accB[i]);
-      accA[i] = __ffma2_rn(make_float2(bf_lo(w.z), bf_hi(w.z)), make_float2(xb.x, xb.y), accA[i]);
-      accB[i] = __ffma2_rn(make_float2(bf_lo(w.w), bf_hi(w.w)), make_float2(xb.z, xb.w), accB[i]);
+  for (int i = 0; i < 4; ++i) {
+    const float keep = b4 ? v[i + 4] : v[i], send = b4 ? v[i] : v[i + 4];
+    u[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float keep = b3 ? u[i + 2] : u[i], send = b3 ? u[i] : u[i + 2];
+    w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const float keep = b2 ? w[1] : w[0], send = b2 ? w[0] : w[1];
+  float s = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  return s;
+}
+
+// One ring stage of a warp: its K group's chunks (every WK-th) of RW rows.  No predication inside:
+// all RW weight loads of a chunk are issued back to back ahead of the convert / FFMA2 chains.
+template <int RW>
+__device__ __forceinline__ void gemv_stage(uint32_t wa, uint32_t row_stride, uint32_t xa_addr, int nch, int WK,
+                                           float2 (&acc)[kRW]) {
+  const uint32_t wstep = (uint32_t)WK * 512u, xstep = (uint32_t)WK * (kChunk * 4);
+#pragma unroll 1
+  for (int j = 0; j < nch; ++j, wa += wstep, xa_addr += xstep) {
+    const float4 xa = lds128f(xa_addr);
+    const float4 xb = lds128f(xa_addr + 512);
+    uint4 w[RW];
+#pragma unroll
+    for (int i = 0; i < RW; ++i) w[i] = lds128u(wa + i * row_stride);
+#pragma unroll
+    for (int i = 0; i < RW; ++i) {
+      acc[i] = __ffma2_rn(make_float2(bf_lo(w[i].x), bf_hi(w[i].x)), make_float2(xa.x, xa.y), acc[i]);
+      acc[i] = __ffma2_rn(make_float2(bf_lo(w[i].y), bf_hi(w[i].y)), make_float2(xa.z, xa.w), acc[i]);
+      acc[i] = __ffma2_rn(make_float2(bf_lo(w[i].z), bf_hi(w[i].z)), make_float2(xb.x, xb.y), acc[i]);
+      acc[i] = __ffma2_rn(make_float2(bf_lo(w[i].w), bf_hi(w[i].w)), make_float2(xb.z, xb.w), acc[i]);
     }
   }
 }
 
+// Per-task constants of the stage loop, computed once (nothing but the ring cursor changes per stage).
+struct StageGeom {
+  uint32_t wofs_full, wofs_last;      // byte offset of this warp's first block inside a full / the last k-tile stage
+  uint32_t rstride_full, rstride_last;
+  int nch_full, nch_last;             // chunks of this warp's K group in a full / the last k-tile stage
+};
+
+// All k-tiles of one row tile.  wait = false: consumer-only probe (no Loader, no barriers).
+// The ring cursor lives in registers here (slot, ph) and is written back by the caller.
 template <int RW>
+__device__ __forceinline__ void gemv_ktiles(const KParams& p, uint32_t& slot, uint32_t& ph, int lane, int ktc, int n_ktiles,
+                                            int task_idx, const StageGeom& sg, uint32_t ring_addr, uint32_t xs_addr,
+                                            uint32_t full0, uint32_t empty0, int WK, float2 (&acc)[kRW], bool active,
+                                            bool wait) {
+  const uint32_t n_stage = (uint32_t)p.n_stage, stage_bytes = (uint32_t)p.stage_bytes;
+  const uint32_t xtile = (uint32_t)ktc * (kChunk * 4);
+  uint32_t xa = xs_addr;
+  uint32_t sbase = ring_addr + slot * stage_bytes;
+  const int last = n_ktiles - 1;
+#pragma unroll 1
+  for (int kt = 0; kt <= last; ++kt, xa += xtile) {
+    if (wait) mbar_wait(p, full0 + slot * 8, ph, DE_WATCHDOG_FULL, task_idx);
+    if (active) {
+      const bool is_last = kt == last;
+      gemv_stage<RW>(sbase + (is_last ? sg.wofs_last : sg.wofs_full), is_last ? sg.rstride_last : sg.rstride_full, xa,
+                     is_last ? sg.nch_last : sg.nch_full, WK, acc);
+    }
+    if (wait) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + slot * 8);
+    }
+    sbase += stage_bytes;
+    if (++slot == n_stage) { slot = 0; ph ^= 1u; sbase = ring_addr; }
+  }
+}
+
 __device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx,
-                                           const float* xs, SmemHdr* hdr, uint8_t* ring, int tok,
-                                           const float (&eop0)[4]) {
-  const uint32_t xs_addr = smem_u32(xs) + c.lane * 16;
+                                           const float* xs, SmemHdr* hdr, uint8_t* ring, int tok, float eop0, int probe) {
+  const int WK = (t.geom >> 8) & 0xff, rw = (t.geom >> 16) & 0xff, lgWK = 31 - __clz(WK);
+  const int wr = c.cw >> lgWK, wk = c.cw & (WK - 1);
   const uint32_t ring_addr = smem_u32(ring) + c.lane * 16;
   const uint32_t full0 = smem_u32(&hdr->full[0]);
   const uint32_t empty0 = smem_u32(&hdr->empty[0]);
-  const int r0 = c.cw * RW;
-  const uint32_t n_stage = (uint32_t)p.n_stage;
+  const int my_r0 = wr * rw;
+  const int rsel = ((c.lane >> 4) & 1) * 4 + ((c.lane >> 3) & 1) * 2 + ((c.lane >> 2) & 1);  // row held after reduce8
+  const int chunks_last = t.kchunks - (t.n_ktiles - 1) * t.ktc;
+  StageGeom sg;
+  sg.rstride_full = (uint32_t)t.ktc * 512u; sg.rstride_last = (uint32_t)chunks_last * 512u;
+  sg.wofs_full = (uint32_t)my_r0 * sg.rstride_full + (uint32_t)wk * 512u;
+  sg.wofs_last = (uint32_t)my_r0 * sg.rstride_last + (uint32_t)wk * 512u;
+  sg.nch_full = (t.ktc - wk + WK - 1) >> lgWK; sg.nch_last = max(0, (chunks_last - wk + WK - 1) >> lgWK);
+  const uint32_t xs_addr = smem_u32(xs) + c.lane * 16 + (uint32_t)wk * (kChunk * 4);
+  const int rwc = (rw + 1) >> 1;
   for (int tile = 0; tile < t.n_tiles; ++tile) {
     const int rows = min(t.rt, t.b - tile * t.rt);
-    const int nrows = min(RW, rows - r0);  // rows of this tile owned by this warp (<= 0: none)
-    float2 accA[RW], accB[RW];
-    float eop[RW];
+    const int my_n = max(0, min(rw, rows - my_r0));  // rows of this tile owned by this warp
+    const int vrow0 = t.a + tile * t.rt;
+    // the thread that will run the epilogue of a row loads its operand ahead of the K loop
+    int erow = -1;
+    if (WK == 1) { if ((c.lane & 3) == 0 && rsel < my_n) erow = my_r0 + rsel; }
+    else if (c.ctid < rows) erow = c.ctid;
+    float eop = eop0;
+    if (tile > 0 && erow >= 0 && !probe) eop = load_eop(p, c, t, task_idx, vrow0 + erow, tok);
+    float2 acc[kRW];
 #pragma unroll
-    for (int i = 0; i < RW; ++i) {
-      accA[i] = make_float2(0.f, 0.f);
-      accB[i] = make_float2(0.f, 0.f);
-      eop[i] = eop0[i];
-      if (tile > 0 && c.lane == 0 && i < nrows && !p.probe) eop[i] = load_eop(p, t, t.a + tile * t.rt + r0 + i, tok);
-    }
-    int kc0 = 0;
-    for (int kt = 0; kt < t.n_ktiles; ++kt, kc0 += t.ktc) {
-      const int chunks = min(t.ktc, t.kchunks - kc0);
-      mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);
-      if (nrows > 0 && p.probe != 2) {
-        const uint32_t row_stride = (uint32_t)chunks * 512u;
-        uint32_t wa = ring_addr + c.slot * (uint32_t)p.stage_bytes + (uint32_t)r0 * row_stride;
-        uint32_t xa = xs_addr + (uint32_t)kc0 * (kChunk * 4);
-        if (nrows == RW) {
-#pragma unroll 2
-          for (int ch = 0; ch < chunks; ++ch, wa += 512, xa += kChunk * 4)
-            gemv_chunk<RW, true>(wa, row_stride, xa, RW, accA, accB);
-        } else {
-          for (int ch = 0; ch < chunks; ++ch, wa += 512, xa += kChunk * 4)
-            gemv_chunk<RW, false>(wa, row_stride, xa, nrows, accA, accB);
-        }
+    for (int i = 0; i < kRW; ++i) acc[i] = make_float2(0.f, 0.f);
+    // rows past my_n read stale bytes of the slot and are discarded by the epilogue (no predication in the loop)
+    const bool active = my_n > 0 && probe != 2;
+    {
+      uint32_t slot = c.slot, ph = c.ph;
+      const bool wait = probe != 4;
+      switch (probe == 4 ? 4 : rwc) {
+        case 1: gemv_ktiles<2>(p, slot, ph, c.lane, t.ktc, t.n_ktiles, task_idx, sg, ring_addr, xs_addr, full0, empty0, WK, acc, active, wait); break;
+        case 2: gemv_ktiles<4>(p, slot, ph, c.lane, t.ktc, t.n_ktiles, task_idx, sg, ring_addr, xs_addr, full0, empty0, WK, acc, active, wait); break;
+        case 3: gemv_ktiles<6>(p, slot, ph, c.lane, t.ktc, t.n_ktiles, task_idx, sg, ring_addr, xs_addr, full0, empty0, WK, acc, active, wait); break;
+        default: gemv_ktiles<8>(p, slot, ph, c.lane, t.ktc, t.n_ktiles, task_idx, sg, ring_addr, xs_addr, full0, empty0, WK, acc, active, wait); break;
       }
-      __syncwarp();
-      if (c.lane == 0) mbar_arrive(empty0 + c.slot * 8);
-      if (++c.slot == n_stage) { c.slot = 0; c.ph ^= 1u; }
+      c.slot = slot; c.ph = ph;
     }
-    if (p.probe) {
-      float s = 0.f;
+    float v[kRW];
 #pragma unroll
-      for (int i = 0; i < RW; ++i) s += accA[i].x + accA[i].y + accB[i].x + accB[i].y;
-      if (s == 1.2345678e-30f) p.probe_sink[blockIdx.x] = s;  // keep the math alive
+    for (int i = 0; i < kRW; ++i) v[i] = acc[i].x + acc[i].y;
+    float s = reduce8(v, c.lane);
+    if (probe) {
+      if (s == 1.2345678e-30f) p.probe_sink[blockIdx.x * 64] = s;  // keep the math alive
       continue;
     }
-    if (nrows > 0) {
-      float v[RW];
-#pragma unroll
-      for (int i = 0; i < RW; ++i) v[i] = c.rs * warp_sum((accA[i].x + accB[i].x) + (accA[i].y + accB[i].y));
-      if (c.lane == 0) {
-        const int vrow0 = t.a + tile * t.rt + r0;
-        if (t.type == T_GATEUP) {
-#pragma unroll
-          for (int i = 0; i < RW; i += 2)
-            if (i < nrows) gemv_epilogue(p, c, t, vrow0 + i, v[i], v[(i + 1) % RW], 0.f);
-        } else {
-#pragma unroll
-          for (int i = 0; i < RW; ++i)
-            if (i < nrows) gemv_epilogue(p, c, t, vrow0 + i, v[i], 0.f, eop[i]);
+    if (WK == 1) {
+      s *= c.rs;
+      const float partner = __shfl_xor_sync(0xffffffffu, s, 4);  // row rsel ^ 1 (the `up` row of a gate row)
+      if (erow >= 0) {
+        if (t.type != T_GATEUP) gemv_epilogue(p, c, t, vrow0 + erow, s, 0.f, eop);
+        else if (!(erow & 1)) gemv_epilogue(p, c, t, vrow0 + erow, s, partner, 0.f);
+      }
+    } else {
+      float* rb = &hdr->red2[tile & 1][0][0];
+      if ((c.lane & 3) == 0 && rsel < my_n) rb[wk * 32 + my_r0 + rsel] = s;
+      consumer_sync(c.nct);
+      if (erow >= 0) {
+        float tot = 0.f, tot2 = 0.f;
+        for (int k = 0; k < WK; ++k) tot += rb[k * 32 + erow];
+        if (t.type != T_GATEUP) gemv_epilogue(p, c, t, vrow0 + erow, tot * c.rs, 0.f, eop);
+        else if (!(erow & 1)) {
+          for (int k = 0; k < WK; ++k) tot2 += rb[k * 32 + erow + 1];
+          gemv_epilogue(p, c, t, vrow0 + erow, tot * c.rs, tot2 * c.rs, 0.f);
         }
       }
     }
@@ -570,23 +629,29 @@ __device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, con
 }
 
 __device__ __forceinline__ void lm_finish(const KParams& p, ConsumerCtx& c, SmemHdr* hdr) {
-  // per-warp best -> CTA best -> global partial -> last CTA reduces, publishes, resets counters
-  float bv = __shfl_sync(0xffffffffu, c.best_val, 0);
-  int bi = __shfl_sync(0xffffffffu, c.best_idx, 0);
-  if (c.lane == 0) { hdr->red[c.cw] = bv; hdr->misc[c.cw] = bi; }
+  // per-lane best -> per-warp best -> CTA best -> global partial -> last CTA reduces, publishes, bumps the epoch
+  float bv = c.best_val;
+  int bi = c.best_idx < 0 ? 0x7fffffff : c.best_idx;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  }
+  if (c.lane == 0) { hdr->red[32 + c.cw] = bv; hdr->misc[c.cw] = bi; }
   consumer_sync(c.nct);
   if (c.ctid == 0) {
-    float best = hdr->red[0];
+    float best = hdr->red[32];
     int idx = hdr->misc[0];
     for (int w = 1; w < p.C; ++w) {
-      const float v = hdr->red[w];
+      const float v = hdr->red[32 + w];
       const int i = hdr->misc[w];
       if (v > best || (v == best && i < idx)) { best = v; idx = i; }
     }
     p.lm_val[blockIdx.x] = best;
     p.lm_idx[blockIdx.x] = idx;
     __threadfence();
-    const unsigned old = atom_acqrel_add(p.counters + CTR_F, 1u);
+    const unsigned old = atom_acqrel_add(p.sync + 1, 1u);
     hdr->misc[31] = (old == (unsigned)(p.n_lm_tasks - 1)) ? 1 : 0;
   }
   consumer_sync(c.nct);
@@ -597,7 +662,7 @@ __device__ __forceinline__ void lm_finish(const KParams& p, ConsumerCtx& c, Smem
     for (int s = c.lane; s < (int)gridDim.x; s += 32) {
       const int i = __ldcg(p.lm_idx + s);
       const float v = __ldcg(p.lm_val + s);
-      if (i >= 0 && (v > best || (v == best && i < idx))) { best = v; idx = i; }
+      if (i >= 0 && i != 0x7fffffff && (v > best || (v == best && i < idx))) { best = v; idx = i; }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -608,152 +673,78 @@ __device__ __forceinline__ void lm_finish(const KParams& p, ConsumerCtx& c, Smem
     if (c.lane == 0) {
       p.next_tokens[0] = idx;
       if (p.auto_advance) { p.tokens[0] = idx; p.positions[0] = p.positions[0] + 1; }
+      // every CTA is past its last poll of this step: open the next epoch
+      p.sync[1] = 0u;
+      p.sync[0] = c.epoch + 1u;
     }
-    // every CTA has passed its last wait: reset the dependency counters for the next launch
-    for (int i = c.lane; i < p.n_counters; i += 32) p.counters[i] = 0u;
   }
 }
 
 __device__ __forceinline__ void run_gemv(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* xs,
-                                         SmemHdr* hdr, uint8_t* ring, int tok, int pos) {
+                                         SmemHdr* hdr, uint8_t* ring, int tok, int probe) {
   stamp(p, c, task_idx, 0);
-  const int rw = t.rt / p.C;
-  // ---- before the dependency wait: everything that does not depend on the awaited data ----
-  // (per-layer vectors are always DRAM misses under the weight stream: ~1 us each if loaded late)
-  float4 g4[kPreG];
-  float eop0[4] = {0.f, 0.f, 0.f, 0.f};
-  if (!p.probe) {
-    if (t.type == T_QKV || t.type == T_GATEUP || t.type == T_LMHEAD) {
-      const float4* gain4 = reinterpret_cast<const float4*>(gemv_gain(p, t));
-#pragma unroll
-      for (int k = 0; k < kPreG; ++k) {
-        const int i = c.ctid + k * c.nct;
-        g4[k] = (i < (p.H >> 2)) ? __ldg(gain4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-    if (c.lane == 0 && t.type != T_DOWN) {  // DOWN's residual (h_mid) is preloaded after its own dependency
-      const int r0 = c.cw * rw, rows0 = min(t.rt, t.b);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i < rw && r0 + i < rows0) eop0[i] = load_eop(p, t, t.a + r0 + i, tok);
-    }
+  // ---- before the inputs are awaited: the epilogue operand of the first tile (bias rows are DRAM
+  // misses under the weight stream; residual words were completed earlier in this step) ----
+  float eop0 = 0.f;
+  if (!probe) {
+    const int WK = (t.geom >> 8) & 0xff, rw = (t.geom >> 16) & 0xff;
+    const int rows0 = min(t.rt, t.b);
+    int erow = -1;
+    if (WK == 1) {
+      const int rsel = ((c.lane >> 4) & 1) * 4 + ((c.lane >> 3) & 1) * 2 + ((c.lane >> 2) & 1);
+      if ((c.lane & 3) == 0 && rsel < rw && c.cw * rw + rsel < rows0) erow = c.cw * rw + rsel;
+    } else if (c.ctid < rows0) erow = c.ctid;
+    if (erow >= 0) eop0 = load_eop(p, c, t, task_idx, t.a + erow, tok);
+    gemv_prologue(p, c, t, task_idx, xs, hdr, tok);
   }
-  wait_counter(p, c, t.wait_ctr, t.wait_val, task_idx);
   stamp(p, c, task_idx, 1);
-  if (!p.probe) {
-    if (c.lane == 0 && t.type == T_DOWN) {
-      const int r0 = c.cw * rw, rows0 = min(t.rt, t.b);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i < rw && r0 + i < rows0) eop0[i] = load_eop(p, t, t.a + r0 + i, tok);
-    }
-    gemv_prologue(p, c, t, xs, hdr, tok, pos, g4);
-  }
+  gemv_tiles(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe);
+  if (probe) { stamp(p, c, task_idx, 7); return; }
   stamp(p, c, task_idx, 2);
-  if (rw == 2) gemv_tiles<2>(p, c, t, task_idx, xs, hdr, ring, tok, eop0);
-  else gemv_tiles<4>(p, c, t, task_idx, xs, hdr, ring, tok, eop0);
-  if (p.probe) return;
-  stamp(p, c, task_idx, 3);
   if (t.type == T_LMHEAD) lm_finish(p, c, hdr);
-  else signal_counter(p, c, t.sig_ctr);
   stamp(p, c, task_idx, 7);
 }
 
-// Per-lane operands of rope_norm_head that do not depend on this step's projections:
-// loaded BEFORE the dependency wait so their DRAM latency is off the critical path
-// (small per-layer vectors never survive in L2 under the weight stream).
-template <int D>
-struct HeadParams {
-  float gq[D / 32], gk[D / 32], cs[D / 64], sn[D / 64];
-};
-template <int D>
-__device__ __forceinline__ HeadParams<D> load_head_params(const KParams& p, const float* lay_fp, int pos, int lane) {
-  HeadParams<D> hp;
-#pragma unroll
-  for (int j = 0; j < D / 32; ++j) {
-    hp.gq[j] = p.qk_norm ? __ldg(lay_fp + p.fp_qn + lane + 32 * j) : 1.0f;
-    hp.gk[j] = p.qk_norm ? __ldg(lay_fp + p.fp_kn + lane + 32 * j) : 1.0f;
-  }
-#pragma unroll
-  for (int j = 0; j < D / 64; ++j) {
-    hp.cs[j] = __ldg(p.rope_cos + (size_t)pos * (D / 2) + lane + 32 * j);
-    hp.sn[j] = __ldg(p.rope_sin + (size_t)pos * (D / 2) + lane + 32 * j);
-  }
-  return hp;
-}
-
-// one warp, one head: optional RMSNorm over D, rotate-half RoPE, scale
-// PADL > 0: the output is laid out in segments of PADL floats separated by 4 floats of padding
-// (bank-conflict-free reads by the score step); PADL = 0: dense.
-template <int D, int PADL>
-__device__ __forceinline__ void rope_norm_head(const KParams& p, const float* raw, const float (&gain)[D / 32],
-                                               const HeadParams<D>& hp, float scale, int lane, float* out) {
-  auto at = [](int d) { return PADL > 0 ? d + (d / (PADL > 0 ? PADL : 1)) * 4 : d; };
-  constexpr int PER = D / 32;  // 4 (D=128) or 2 (D=64): elements lane, lane+32, ...
-  constexpr int HALF = D / 2;
-  float v[PER];
-  float ss = 0.f;
-#pragma unroll
-  for (int j = 0; j < PER; ++j) { v[j] = __ldcg(raw + lane + 32 * j); ss += v[j] * v[j]; }
-  if (p.qk_norm) {
-    ss = warp_sum(ss);
-    const float rs = rsqrtf(ss / (float)D + p.eps);
-#pragma unroll
-    for (int j = 0; j < PER; ++j) v[j] = v[j] * rs * gain[j];
-  }
-#pragma unroll
-  for (int j = 0; j < PER / 2; ++j) {
-    const int d1 = lane + 32 * j;  // < HALF
-    const float x1 = v[j], x2 = v[j + PER / 2];
-    out[at(d1)] = (x1 * hp.cs[j] - x2 * hp.sn[j]) * scale;
-    out[at(d1 + HALF)] = (x2 * hp.cs[j] + x1 * hp.sn[j]) * scale;
-  }
-}
-
-// Layout of the attention scratch (floats); must match task_table.scratch_bytes / adamk_create.
-//   qs[G][D] | sc[8][kAttnPBMax] | rsc[C][8] | prob[8][kAttnPBMax] | red[C][G][D] | lw[C][8] | mw[C][8] | knew[D] | vnew[D]
+// ----------------------------------------------------------------------------------
+// attention unit = (kv head, context chunk)
+// ----------------------------------------------------------------------------------
+// Scratch layout (floats), must fit task_table.scratch_bytes:
+//   qs[kGMax][D + 16] | knew[D] | vnew[D] | pbuf[kAttnWarps][kGMax][8] | comb[kAttnWarps][kGMax][D + 2]
 //
-// The K and V rows of a unit's context chunk arrive through the weight ring (the paper's
-// "KV-cache loads advanced into the pipeline window"): per block of PB positions
-// one K stage and one V stage, issued by the Loader long before the QKV projections of this
-// layer are done.  The row of the new token is patched into the staged copy.  Every unit
-// publishes a partial record (o[D], m, l) per q head; the flash-decoding merge of the records
-// is done by the consumers of the attention output (the O-projection prologue), so no unit
-// waits for another.
-template <int D, int PPW>
+// The K and V rows of the unit's context chunk arrive through the weight ring (the paper's
+// "KV-cache loads advanced into the pipeline window"): per block of 64 positions one
+// K stage and one V stage, issued by the Loader long before the QKV projections of this layer are
+// done; the row of the new token is patched into the staged copy.  Each of the (up to 8) attention
+// warps owns 8 positions of a block and keeps its own running softmax state (m, l, o) in registers
+// for all q heads of the group; the warps are merged once at the end.  The unit publishes one
+// partial record (o[D], m, l) per q head; T_MERGE tasks combine the records of all units of a head.
+// With a single active unit the normalised output is published directly.
+template <int D>
 __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* scratch,
                                          SmemHdr* hdr, uint8_t* ring, int pos) {
-  constexpr int DPL = D / 32;  // V / output elements per lane (lanes split the head dim)
-  const int G = p.G;
-  const int kvh = t.a, slot = t.b, bidx = t.aux;
+  constexpr int DL = D / 4;      // dims per lane in the score step (4 lanes per position)
+  constexpr int QS = D + 16;     // padded q row: 4 segments of DL floats, 4 floats apart (conflict-free)
+  constexpr int DPL = D / 32;    // output dims per lane
+  constexpr int RS = D + 2;      // per-(warp, head) record: o[D], m, l
+  const int G = p.G, kvh = t.a, slot = t.b;
   if (p.probe) return;
   const AttnGeom ge = attn_geometry(p, pos, slot);
-  if (slot >= ge.n_active) {  // no context for this slot at this length: only keep the counter target static
-    signal_counter(p, c, CTR_C);
-    return;
-  }
+  if (slot >= ge.n_active) return;  // no context for this slot at this length
   stamp(p, c, task_idx, 0);
-  const int n = ge.n, t0 = ge.t0, PB = ge.PB, nblk = ge.nblk;
+  const int n = ge.n, t0 = ge.t0, nblk = ge.nblk;
   const bool owns_new = (slot == ge.n_active - 1);  // this chunk contains position `pos`
+  const unsigned tag = tag_of(c, t.layer);
+  const int AW = min(p.C, kAttnWarps);
 
-  // compile-time lane mapping of the score step (see below) -- needed here for the padded q layout
-  constexpr int GS = PPW < 8 ? PPW : 8, LPP = 32 / GS, DL = D / LPP;
-  constexpr int QP = D + LPP * 4;           // padded q row: LPP segments of DL floats, 4 floats apart
-  constexpr int SR = kAttnPBMax + 4;        // padded score / probability row
-  float* qs = scratch;                      // [G][QP]
-  float* sc = qs + kGMax * (128 + 8 * 4);   // [kGMax][SR]   (q region sized for the largest QP)
-  float* rsc = sc + kGMax * SR;             // per-warp rescale factors [C][kGMax]
-  float* prob = rsc + p.C * kGMax;          // probabilities [kGMax][SR] (scores stay intact: other warps still read them)
-  float* red = prob + kGMax * SR;
-  float* lw = red + p.C * G * D;
-  float* mw = lw + p.C * kGMax;
-  float* knew = mw + p.C * kGMax;
+  float* qs = scratch;
+  float* knew = qs + kGMax * QS;
   float* vnew = knew + D;
+  float* pbuf = vnew + D;
+  float* comb = pbuf + kAttnWarps * kGMax * 8;
 
-  const float* qkv = p.qkv + (size_t)bidx * p.qkv_rows;
   const float* lay_fp = p.fparams + (size_t)t.layer * p.fp_layer_stride;
   const float scale = rsqrtf((float)D);
-  const size_t head_base = ((size_t)(t.layer * p.batch + bidx) * p.nkv + kvh) * (size_t)p.max_ctx * D;
+  const size_t head_base = ((size_t)(t.layer * p.batch + t.aux) * p.nkv + kvh) * (size_t)p.max_ctx * D;
   __nv_bfloat16* Kc = p.kcache + head_base;
   __nv_bfloat16* Vc = p.vcache + head_base;
   const uint32_t ring_addr = smem_u32(ring);
@@ -761,69 +752,79 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
   const uint32_t empty0 = smem_u32(&hdr->empty[0]);
   const uint32_t n_stage = (uint32_t)p.n_stage;
 
-  const HeadParams<D> hp = load_head_params<D>(p, lay_fp, pos, c.lane);  // before the wait
-  wait_counter(p, c, t.wait_ctr, t.wait_val, task_idx);
-  stamp(p, c, task_idx, 1);
-
-  // q heads of this group: (norm) + RoPE + 1/sqrt(D); the owner of `pos` also appends K/V
-  for (int g = c.cw; g < G; g += p.C)
-    rope_norm_head<D, DL>(p, qkv + (size_t)(kvh * G + g) * D, hp.gq, hp, scale, c.lane, qs + g * QP);
-  if (owns_new) {
-    const int wk = G % p.C, wv = (G + 1) % p.C;  // warps with the least q work
-    if (c.cw == wk) {
-      rope_norm_head<D, 0>(p, qkv + p.q_dim + (size_t)kvh * D, hp.gk, hp, 1.0f, c.lane, knew);
-      __syncwarp();
-      for (int d = c.lane; d < D; d += 32) Kc[(size_t)pos * D + d] = __float2bfloat16_rn(knew[d]);
+  // ---- q heads of the group (+ k, v of the new token in the owner unit): gather, (norm), RoPE ----
+  // one warp per row of D elements; lane holds elements lane + 32 j so rotate-half partners share a lane
+  {
+    constexpr int PER = D / 32, HALF = D / 2;
+    float cs[PER / 2], sn[PER / 2];
+#pragma unroll
+    for (int j = 0; j < PER / 2; ++j) {  // static operands first: they are DRAM misses
+      cs[j] = __ldg(p.rope_cos + (size_t)pos * HALF + c.lane + 32 * j);
+      sn[j] = __ldg(p.rope_sin + (size_t)pos * HALF + c.lane + 32 * j);
     }
-    if (c.cw == wv) {
-      const float* vraw = qkv + p.q_dim + p.kv_dim + (size_t)kvh * D;
-      for (int d = c.lane; d < D; d += 32) {
-        const float v = __ldcg(vraw + d);
-        vnew[d] = v;
-        Vc[(size_t)pos * D + d] = __float2bfloat16_rn(v);
+    const int n_rows = G + (owns_new ? 2 : 0);
+    for (int r = c.cw; r < n_rows; r += p.C) {
+      const bool is_q = r < G, is_k = r == G;
+      const u64* src = p.ll_qkv + (is_q ? (size_t)(kvh * G + r) * D : (size_t)p.q_dim + (is_k ? 0 : p.kv_dim) + (size_t)kvh * D);
+      float v[PER];
+      ll_wait_strided<PER>(p, src + c.lane, 32, tag, v, task_idx);
+      if (!is_q && !is_k) {  // v row: cache + staged patch value
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          vnew[c.lane + 32 * j] = v[j];
+          Vc[(size_t)pos * D + c.lane + 32 * j] = __float2bfloat16_rn(v[j]);
+        }
+        continue;
+      }
+      if (p.qk_norm) {
+        float ss = 0.f;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) ss += v[j] * v[j];
+        ss = warp_sum(ss);
+        const float rs = rsqrtf(ss / (float)D + p.eps);
+        const float* gn = lay_fp + (is_q ? p.fp_qn : p.fp_kn);
+#pragma unroll
+        for (int j = 0; j < PER; ++j) v[j] = v[j] * rs * __ldg(gn + c.lane + 32 * j);
+      }
+#pragma unroll
+      for (int j = 0; j < PER / 2; ++j) {
+        const int d1 = c.lane + 32 * j;  // < HALF
+        const float x1 = v[j], x2 = v[j + PER / 2];
+        const float y1 = x1 * cs[j] - x2 * sn[j], y2 = x2 * cs[j] + x1 * sn[j];
+        if (is_q) {
+          qs[r * QS + d1 + (d1 / DL) * 4] = y1 * scale;
+          qs[r * QS + d1 + HALF + ((d1 + HALF) / DL) * 4] = y2 * scale;
+        } else {
+          knew[d1] = y1; knew[d1 + HALF] = y2;
+          Kc[(size_t)pos * D + d1] = __float2bfloat16_rn(y1);
+          Kc[(size_t)pos * D + d1 + HALF] = __float2bfloat16_rn(y2);
+        }
       }
     }
   }
   consumer_sync(c.nct);
-  stamp(p, c, task_idx, 2);
+  stamp(p, c, task_idx, 1);
 
-  // Per-warp running softmax state lives in shared memory (red = unnormalised output, mw = running
-  // max, lw = running sum) and every loop over heads is a plain runtime loop: this path runs once
-  // per layer on a few SMs, so its instruction footprint -- not its FLOPs -- is what costs time.
-  for (int g = 0; g < G; ++g) {
+  // ---- per-warp running state ----
+  float o[kGMax][DPL], m_run[kGMax], l_part[kGMax];
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) red[(c.cw * G + g) * D + c.lane * DPL + e] = 0.f;
-    if (c.lane == 0) { mw[c.cw * kGMax + g] = -INFINITY; lw[c.cw * kGMax + g] = 0.f; }
+  for (int g = 0; g < kGMax; ++g) {
+    m_run[g] = -INFINITY; l_part[g] = 0.f;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) o[g][e] = 0.f;
   }
-  __syncwarp();
-
-  auto lds_row = [&](uint32_t base, int tl, float (&out)[DPL]) {  // one bf16 row, DPL elements per lane
-    if constexpr (DPL == 4) {
-      uint2 raw;
-      asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(raw.x), "=r"(raw.y) : "r"(base + (uint32_t)(tl * D + c.lane * 4) * 2u));
-      out[0] = bf_lo(raw.x); out[1] = bf_hi(raw.x); out[2] = bf_lo(raw.y); out[3] = bf_hi(raw.y);
-    } else {
-      uint32_t raw;
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(base + (uint32_t)(tl * D + c.lane * 2) * 2u));
-      out[0] = bf_lo(raw); out[1] = bf_hi(raw);
-    }
-  };
-
-  // Lane mapping of the score step: the warp's PPW positions are handled GS = min(PPW, 8) at a
-  // time by LPP = 32 / GS lanes each; a lane owns DL = D / LPP contiguous dims, so one dot product
-  // needs log2(LPP) shuffle steps and all GS positions reduce in parallel.  All compile-time.
-  const int lsub = c.lane % LPP, lpos = c.lane / LPP;
-  // Lane mapping of the softmax bookkeeping: lane -> (head hg = lane % 8, part hpart = lane / 8)
-  const int hg = c.lane & 7, hpart = c.lane >> 3;
+  const int lsub = c.lane & 3, lpos = c.lane >> 2;
+  float* pw = pbuf + c.cw * (kGMax * 8);  // this warp's probabilities [g][8]
 
   for (int blk = 0; blk < nblk; ++blk) {
     const bool patch = owns_new && blk == nblk - 1;
-    const int new_row = (pos - t0) - blk * PB;  // row of the new token inside this block (if patch)
-    const int nvalid = min(PPW, n - blk * PB - c.cw * PPW);  // valid positions of this warp in this block (may be <= 0)
-    // ---------------- K stage: scores of this warp's PPW positions ----------------
+    const int new_row = (pos - t0) - blk * kAttnBlock;  // row of the new token inside this block (if patch)
+    const int nblkpos = min(kAttnBlock, n - blk * kAttnBlock);
+    // ---------------- K stage ----------------
     mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);
-    if (blk == 0) stamp(p, c, task_idx, 5);
     const uint32_t kb = ring_addr + c.slot * (uint32_t)p.stage_bytes;
+    const uint32_t kslot = c.slot;
+    if (++c.slot == n_stage) { c.slot = 0; c.ph ^= 1u; }
     if (patch) {  // the staged copy predates this step's K row: overwrite it (bf16, as the cache holds it)
       for (int d = c.ctid; d < D; d += c.nct) {
         const unsigned short bits = __bfloat16_as_ushort(__float2bfloat16_rn(knew[d]));
@@ -831,76 +832,11 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
       }
       consumer_sync(c.nct);
     }
-#pragma unroll
-    for (int j0 = 0; j0 < PPW; j0 += GS) {
-      const int j = j0 + lpos;
-      const int tl = c.cw * PPW + j;
-      const uint32_t krow = kb + (uint32_t)(tl * D + lsub * DL) * 2u;
-      float kf[DL];  // this lane's slice of the K row, converted once and reused for every head
-#pragma unroll
-      for (int e = 0; e < DL; e += 8) {
-        const uint4 raw = lds128u(krow + e * 2);
-        kf[e + 0] = bf_lo(raw.x); kf[e + 1] = bf_hi(raw.x); kf[e + 2] = bf_lo(raw.y); kf[e + 3] = bf_hi(raw.y);
-        kf[e + 4] = bf_lo(raw.z); kf[e + 5] = bf_hi(raw.z); kf[e + 6] = bf_lo(raw.w); kf[e + 7] = bf_hi(raw.w);
-      }
-#pragma unroll 2
-      for (int g = 0; g < G; ++g) {
-        const float4* qp = reinterpret_cast<const float4*>(qs + g * QP + lsub * (DL + 4));
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-        for (int e = 0; e < DL / 4; ++e) {
-          const float4 q4 = qp[e];
-          s0 = fmaf(q4.x, kf[e * 4 + 0], s0); s1 = fmaf(q4.y, kf[e * 4 + 1], s1);
-          s2 = fmaf(q4.z, kf[e * 4 + 2], s2); s3 = fmaf(q4.w, kf[e * 4 + 3], s3);
-        }
-        float sdot = (s0 + s1) + (s2 + s3);
-#pragma unroll
-        for (int o = LPP >> 1; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
-        if (lsub == 0) sc[g * SR + tl] = (j < nvalid) ? sdot : -INFINITY;
-      }
-    }
-    __syncwarp();
-    if (c.lane == 0) mbar_arrive(empty0 + c.slot * 8);
-    if (++c.slot == n_stage) { c.slot = 0; c.ph ^= 1u; }
-    consumer_sync(c.nct);
-    if (blk == 0) stamp(p, c, task_idx, 3);
-    // ---------------- online softmax bookkeeping for all heads at once ----------------
-    // block max of head hg over the quarter hpart of the block, then across the 4 parts
-    float resc_l = 0.f;
-    {
-      float mb = -INFINITY;
-      if (hg < G)
-        for (int i = hpart; i < PB; i += 4) mb = fmaxf(mb, sc[hg * SR + i]);  // conflict-free: bank = 4 hg + hpart + 4k
-      mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 8));
-      mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
-      const float m_old = (hg < G) ? mw[c.cw * kGMax + hg] : 0.f;
-      const float m_new = fmaxf(m_old, mb);
-      resc_l = expf(m_old - m_new);  // exp(-inf) = 0 on the first block
-      // probabilities of this warp's own positions (entries written by this warp only): part hpart
-      // covers positions hpart, hpart + 4, ... of the warp
-      float lsum = 0.f;
-      if (hg < G) {
-        for (int j = hpart; j < PPW; j += 4) {
-          const int idx = hg * SR + c.cw * PPW + j;
-          const float pj = (j < nvalid) ? expf(sc[idx] - m_new) : 0.f;
-          prob[idx] = pj;
-          lsum += pj;
-        }
-      }
-      lsum += __shfl_xor_sync(0xffffffffu, lsum, 8);
-      lsum += __shfl_xor_sync(0xffffffffu, lsum, 16);
-      __syncwarp();
-      if (hpart == 0 && hg < G) {
-        mw[c.cw * kGMax + hg] = m_new;
-        lw[c.cw * kGMax + hg] = lw[c.cw * kGMax + hg] * resc_l + lsum;
-        rsc[c.cw * kGMax + hg] = resc_l;  // per-warp rescale factors for the P.V step
-      }
-      __syncwarp();
-    }
-    // ---------------- V stage: P.V over this warp's positions, one head at a time ----------------
+    // ---------------- V stage (waited for now so both are ready; consumed below) ----------------
     mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);
-    if (blk == 0) stamp(p, c, task_idx, 6);
     const uint32_t vb = ring_addr + c.slot * (uint32_t)p.stage_bytes;
+    const uint32_t vslot = c.slot;
+    if (++c.slot == n_stage) { c.slot = 0; c.ph ^= 1u; }
     if (patch) {
       for (int d = c.ctid; d < D; d += c.nct) {
         const unsigned short bits = __bfloat16_as_ushort(__float2bfloat16_rn(vnew[d]));
@@ -908,50 +844,214 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
       }
       consumer_sync(c.nct);
     }
-#pragma unroll 1
-    for (int g = 0; g < G; ++g) {
-      const float resc = rsc[c.cw * kGMax + g];
-      float acc[DPL];
-      float* ra = red + (c.cw * G + g) * D + c.lane * DPL;
+    if (blk == 0) stamp(p, c, task_idx, 4);
+    // each attention warp takes groups of 8 positions: j0 = 8 cw, 8 (cw + AW), ...
+    if (c.cw < AW) {
+      for (int j0 = c.cw * 8; j0 < nblkpos; j0 += AW * 8) {
+        const int tl = j0 + lpos;                 // this lane's position inside the block
+        const bool valid = tl < nblkpos;
+        // scores of position tl for every head: 4 lanes share a position, each DL dims
+        float kf[DL];
+        {
+          const uint32_t krow = kb + (uint32_t)(tl * D + lsub * DL) * 2u;
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) acc[e] = ra[e] * resc;
-      const float* pr = prob + g * SR + c.cw * PPW;
-#pragma unroll 4
-      for (int j = 0; j < nvalid; ++j) {
-        float vf[DPL];
-        lds_row(vb, c.cw * PPW + j, vf);
-        const float pg = pr[j];
+          for (int e = 0; e < DL; e += 8) {
+            const uint4 raw = lds128u(krow + e * 2);
+            kf[e + 0] = bf_lo(raw.x); kf[e + 1] = bf_hi(raw.x); kf[e + 2] = bf_lo(raw.y); kf[e + 3] = bf_hi(raw.y);
+            kf[e + 4] = bf_lo(raw.z); kf[e + 5] = bf_hi(raw.z); kf[e + 6] = bf_lo(raw.w); kf[e + 7] = bf_hi(raw.w);
+          }
+        }
+        float sc[kGMax];
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) acc[e] = fmaf(pg, vf[e], acc[e]);
+        for (int g = 0; g < kGMax; ++g) {
+          sc[g] = -INFINITY;
+          if (g < G) {
+            const float4* qp = reinterpret_cast<const float4*>(qs + g * QS + lsub * (DL + 4));
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+            for (int e = 0; e < DL / 4; ++e) {
+              const float4 q4 = qp[e];
+              s0 = fmaf(q4.x, kf[e * 4 + 0], s0); s1 = fmaf(q4.y, kf[e * 4 + 1], s1);
+              s2 = fmaf(q4.z, kf[e * 4 + 2], s2); s3 = fmaf(q4.w, kf[e * 4 + 3], s3);
+            }
+            float sdot = (s0 + s1) + (s2 + s3);
+            sdot += __shfl_xor_sync(0xffffffffu, sdot, 1);
+            sdot += __shfl_xor_sync(0xffffffffu, sdot, 2);
+            sc[g] = valid ? sdot : -INFINITY;
+          }
+        }
+        // online softmax over the 8 positions of the group, all heads
+        float resc[kGMax];
+#pragma unroll
+        for (int g = 0; g < kGMax; ++g) {
+          resc[g] = 1.f;
+          if (g < G) {
+            float mb = sc[g];
+            mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 4));
+            mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 8));
+            mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
+            const float m_new = fmaxf(m_run[g], mb);   // finite: position j0 of the group is always valid
+            resc[g] = expf(m_run[g] - m_new);          // exp(-inf) = 0 on the first group
+            const float pj = valid ? expf(sc[g] - m_new) : 0.f;
+            m_run[g] = m_new;
+            l_part[g] = l_part[g] * resc[g] + (lsub == 0 ? pj : 0.f);
+            if (lsub == 0) pw[g * 8 + lpos] = pj;
+          }
+        }
+        __syncwarp();
+        // P.V: lanes split the head dim; probabilities come back as two LDS.128 per head
+#pragma unroll
+        for (int g = 0; g < kGMax; ++g) {
+          if (g < G) {
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) o[g][e] *= resc[g];
+          }
+        }
+        const int npos = min(8, nblkpos - j0);
+        for (int j = 0; j < npos; ++j) {
+          float vf[DPL];
+          if constexpr (DPL == 4) {
+            uint2 raw;
+            asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(raw.x), "=r"(raw.y) : "r"(vb + (uint32_t)((j0 + j) * D + c.lane * 4) * 2u));
+            vf[0] = bf_lo(raw.x); vf[1] = bf_hi(raw.x); vf[2] = bf_lo(raw.y); vf[3] = bf_hi(raw.y);
+          } else {
+            uint32_t raw;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(vb + (uint32_t)((j0 + j) * D + c.lane * 2) * 2u));
+            vf[0] = bf_lo(raw); vf[1] = bf_hi(raw);
+          }
+#pragma unroll
+          for (int g = 0; g < kGMax; ++g) {
+            if (g < G) {
+              const float pg = pw[g * 8 + j];
+#pragma unroll
+              for (int e = 0; e < DPL; ++e) o[g][e] = fmaf(pg, vf[e], o[g][e]);
+            }
+          }
+        }
+        __syncwarp();  // pw is rewritten by the next group
       }
-#pragma unroll
-      for (int e = 0; e < DPL; ++e) ra[e] = acc[e];
     }
     __syncwarp();
-    if (c.lane == 0) mbar_arrive(empty0 + c.slot * 8);
-    if (++c.slot == n_stage) { c.slot = 0; c.ph ^= 1u; }
-    if (blk + 1 < nblk) consumer_sync(c.nct);  // sc is rewritten by the next block
+    if (c.lane == 0) { mbar_arrive(empty0 + kslot * 8); mbar_arrive(empty0 + vslot * 8); }
   }
-  stamp(p, c, task_idx, 4);
-  consumer_sync(c.nct);
+  stamp(p, c, task_idx, 3);
 
-  // cross-warp reduction -> partial record (o[D], m, l) of every q head of the group
-  const int PS = D + 4;  // o[D], m, l, pad (records stay 16-byte aligned)
-  float* part = p.part + ((size_t)(bidx * p.nkv + kvh) * p.attn_chunks + slot) * (size_t)G * PS;
-  for (int i = c.ctid; i < G * D; i += c.nct) {
-    const int g = i / D, d = i - g * D;
-    float o = 0.f;
-    for (int w = 0; w < p.C; ++w) o += red[(w * G + g) * D + d];
-    part[(size_t)g * PS + d] = o;
-    if (d == 0) {
-      float l = 0.f;
-      for (int w = 0; w < p.C; ++w) l += lw[w * kGMax + g];
-      part[(size_t)g * PS + D] = mw[g];  // warp 0's copy; identical in every warp
-      part[(size_t)g * PS + D + 1] = l;
+  // ---- merge the attention warps: comb[w][g] = (o[D], m, l) ----
+  if (c.cw < AW) {
+#pragma unroll
+    for (int g = 0; g < kGMax; ++g) {
+      if (g < G) {
+        float l = l_part[g];
+        l += __shfl_xor_sync(0xffffffffu, l, 4);
+        l += __shfl_xor_sync(0xffffffffu, l, 8);
+        l += __shfl_xor_sync(0xffffffffu, l, 16);
+        float* rec = comb + (size_t)(c.cw * kGMax + g) * RS;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) rec[c.lane * DPL + e] = o[g][e];
+        if (c.lane == 0) { rec[D] = m_run[g]; rec[D + 1] = l; }
+      }
     }
   }
-  signal_counter(p, c, CTR_C);
+  consumer_sync(c.nct);
+  stamp(p, c, task_idx, 5);
+  const bool final_out = ge.n_active == 1;
+  u64* part = p.ll_part + ((size_t)(t.aux * p.nkv + kvh) * p.attn_chunks + slot) * (size_t)G * RS;
+  for (int i = c.ctid; i < G * D; i += c.nct) {
+    const int g = i / D, d = i - g * D;
+    float M = -INFINITY;
+    for (int w = 0; w < AW; ++w) M = fmaxf(M, comb[(size_t)(w * kGMax + g) * RS + D]);
+    float ov = 0.f, lv = 0.f;
+    for (int w = 0; w < AW; ++w) {
+      const float* rec = comb + (size_t)(w * kGMax + g) * RS;
+      const float wgt = expf(rec[D] - M);   // warps without positions: m = -inf -> weight 0
+      ov = fmaf(wgt, rec[d], ov);
+      lv = fmaf(wgt, rec[D + 1], lv);
+    }
+    if (final_out) {
+      ll_store(p.ll_attn + (size_t)(kvh * G + g) * D + d, ov / lv, tag);
+    } else {
+      ll_store(part + (size_t)g * RS + d, ov, tag);
+      if (d == 0) { ll_store(part + (size_t)g * RS + D, M, tag); ll_store(part + (size_t)g * RS + D + 1, lv, tag); }
+    }
+  }
   stamp(p, c, task_idx, 7);
+}
+
+// Flash-decoding merge of the split-KV records of one q head: out[d] = sum_s w_s o_s[d] / sum_s w_s l_s,
+// w_s = exp(m_s - M).  Thread d (< D) walks the active units with eight independent loads in flight.
+__device__ __forceinline__ void run_merge(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, int pos) {
+  if (p.probe) return;
+  const AttnGeom ge = attn_geometry(p, pos, 0);
+  if (ge.n_active <= 1) return;  // the single unit published the output itself
+  stamp(p, c, task_idx, 0);
+  const int D = p.D, G = p.G, RS = D + 2, h = t.a, kvh = h / G, g = h - kvh * G;
+  const unsigned tag = tag_of(c, t.layer);
+  const u64* base = p.ll_part + ((size_t)(t.aux * p.nkv + kvh) * p.attn_chunks) * (size_t)G * RS + (size_t)g * RS;
+  const size_t cs = (size_t)G * RS;
+  if (c.ctid < D) {
+    const int d = c.ctid;
+    float M = -INFINITY, L = 0.f, O = 0.f;
+    for (int s0 = 0; s0 < ge.n_active; s0 += 4) {
+      u64 wo[4], wm[4], wl[4];
+      long long t0 = 0;
+      for (;;) {
+        bool ok = true;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (s0 + u < ge.n_active) {
+            const u64* rec = base + (size_t)(s0 + u) * cs;
+            wo[u] = ll_load(rec + d);
+            ll_load2(rec + D, wm[u], wl[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (s0 + u < ge.n_active) ok = ok && ll_tag(wo[u]) == tag && ll_tag(wm[u]) == tag && ll_tag(wl[u]) == tag;
+        if (ok) break;
+        if (p.poll_sleep_ns) __nanosleep(p.poll_sleep_ns);
+        if (t0 == 0) t0 = clock64();
+        else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task_idx, (int)ll_tag(wo[0]), (int)tag, s0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (s0 + u < ge.n_active) {
+          const float m = ll_val(wm[u]);
+          const float Mn = fmaxf(M, m);
+          const float a = expf(M - Mn), b = expf(m - Mn);
+          O = O * a + ll_val(wo[u]) * b;
+          L = L * a + ll_val(wl[u]) * b;
+          M = Mn;
+        }
+      }
+    }
+    ll_store(p.ll_attn + (size_t)h * D + d, O / L, tag);
+  }
+  stamp(p, c, task_idx, 7);
+}
+
+struct WarpArgs {  // passed by value to the out-of-line task bodies so the consumer context stays in registers
+  int cw, lane, ctid, nct;
+  unsigned epoch;
+  uint32_t slot, ph;
+  int layer, a, b, aux, task_idx, pos;
+};
+template <int D>
+__device__ __noinline__ uint32_t run_attn_nl(const KParams& p, WarpArgs w, float* scratch, SmemHdr* hdr, uint8_t* ring) {
+  ConsumerCtx c;
+  c.cw = w.cw; c.lane = w.lane; c.ctid = w.ctid; c.nct = w.nct; c.epoch = w.epoch; c.slot = w.slot; c.ph = w.ph;
+  c.rs = 1.f; c.best_val = 0.f; c.best_idx = 0;
+  Task t{};
+  t.type = T_ATTN; t.layer = w.layer; t.a = w.a; t.b = w.b; t.aux = w.aux;
+  run_attn<D>(p, c, t, w.task_idx, scratch, hdr, ring, w.pos);
+  return c.slot | (c.ph << 8);
+}
+__device__ __noinline__ void run_merge_nl(const KParams& p, WarpArgs w) {
+  ConsumerCtx c;
+  c.cw = w.cw; c.lane = w.lane; c.ctid = w.ctid; c.nct = w.nct; c.epoch = w.epoch; c.slot = w.slot; c.ph = w.ph;
+  c.rs = 1.f; c.best_val = 0.f; c.best_idx = 0;
+  Task t{};
+  t.type = T_MERGE; t.layer = w.layer; t.a = w.a; t.aux = w.aux;
+  run_merge(p, c, t, w.task_idx, w.pos);
 }
 
 // ----------------------------------------------------------------------------------
@@ -961,10 +1061,21 @@ template <int CW>
 __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   SmemHdr* hdr = reinterpret_cast<SmemHdr*>(smem);
-  float* scratch = reinterpret_cast<float*>(smem + kSmemReserved);
-  uint8_t* ring = smem + kSmemReserved + p.scratch_bytes;
+  int4* tcache = reinterpret_cast<int4*>(smem + kSmemReserved);
+  float* scratch = reinterpret_cast<float*>(smem + kSmemReserved + p.task_cache_bytes);
+  uint8_t* ring = smem + kSmemReserved + p.task_cache_bytes + p.scratch_bytes;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tb = p.sm_begin[blockIdx.x], te = p.sm_begin[blockIdx.x + 1];
+  // This SM's task records -> shared memory, packed to 32 bytes (a record in global memory is a DRAM / L2
+  // round trip under the weight stream; short tasks would expose it every time).
+  for (int i = threadIdx.x; i < te - tb; i += blockDim.x) {
+    const int4* tp = reinterpret_cast<const int4*>(p.tasks + tb + i);
+    const int4 a = __ldg(tp), b = __ldg(tp + 1), cc = __ldg(tp + 2), d = __ldg(tp + 3);
+    // type | layer << 8 | aux << 20, a, b | rt << 16, kchunks | ktc << 16   ;   n_tiles | n_ktiles << 16, w_off, geom, k
+    tcache[2 * i] = make_int4(a.x | (a.y << 8) | (d.w << 20), a.z, a.w | (b.z << 16), b.y | (b.w << 16));
+    tcache[2 * i + 1] = make_int4(cc.x | (cc.y << 16), cc.z, cc.w, b.x);
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.n_stage; ++s) {
       mbar_init(smem_u32(&hdr->full[s]), 1);
@@ -974,13 +1085,23 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
-
-  const int tb = p.sm_begin[blockIdx.x], te = p.sm_begin[blockIdx.x + 1];
+  auto fetch_task = [&](int ti) {  // ti relative to tb
+    const int4 u = tcache[2 * ti], v = tcache[2 * ti + 1];
+    Task t;
+    t.type = u.x & 0xff; t.layer = (u.x >> 8) & 0xfff; t.aux = (int)((unsigned)u.x >> 20); t.a = u.y;
+    t.b = u.z & 0xffff; t.rt = (int)((unsigned)u.z >> 16); t.kchunks = u.w & 0xffff; t.ktc = (int)((unsigned)u.w >> 16);
+    t.n_tiles = v.x & 0xffff; t.n_ktiles = (int)((unsigned)v.x >> 16); t.w_off = v.y; t.geom = v.z; t.k = v.w;
+    t.r12 = t.r13 = t.r14 = 0;
+    return t;
+  };
 
   if (warp == 0) {
     // ------------------------------ Loader ------------------------------
-    if (lane == 0) {
-      uint32_t slot = 0, ph = 0;
+    if (lane == 0 && p.probe != 4) {
+      uint32_t slot = 0, ph = 0;          // next slot to fill
+      uint32_t wslot = 0, wph = 0;        // oldest stage that may still be in flight
+      int issued = 0;
+      const int cap = (p.inflight > 0 && p.inflight < p.n_stage) ? p.inflight : p.n_stage;
       const uint32_t ring_addr = smem_u32(ring);
       const uint32_t n_stage = (uint32_t)p.n_stage;
       const uint64_t pol = l2_evict_first_policy();  // weights are read once per step
@@ -989,71 +1110,51 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
         lpos = __ldcg(p.positions);
         if (lpos < 0 || lpos >= p.max_ctx) return;  // the consumers report the error
       }
-      // L2 prefetch cursor: runs pf_min bytes ahead of the ring in steady state and up to
-      // pf_max bytes ahead while the ring is full (consumers stalled on a dependency), so
-      // HBM keeps streaming through dependency stalls.
-      const uint8_t* pf = p.wpacked + (size_t)p.sm_stream[blockIdx.x] * 16u;
-      const uint8_t* const pf_end = p.wpacked + (size_t)p.sm_stream[blockIdx.x + 1] * 16u;
-      constexpr uint32_t kPfGranule = 16384;
-      auto prefetch_to = [&](const uint8_t* upto) {
-        if (upto > pf_end) upto = pf_end;
-        while (pf < upto) {
-          const uint32_t nb = (uint32_t)min((size_t)kPfGranule, (size_t)(pf_end - pf));
-          l2_prefetch_bulk(pf, nb);
-          pf += nb;
+      auto issue = [&](const void* src, uint32_t bytes, bool hint, int ti) {
+        if (issued >= cap) {  // at most `cap` stages in flight: wait for the oldest one to land
+          const uint32_t fbw = smem_u32(&hdr->full[wslot]);
+          if (!mbar_try_wait(fbw, wph)) mbar_wait_slow(p, fbw, wph, DE_WATCHDOG_INFLIGHT, ti);
+          if (++wslot == n_stage) { wslot = 0; wph ^= 1u; }
         }
+        const uint32_t eb = smem_u32(&hdr->empty[slot]);
+        if (!mbar_try_wait(eb, ph ^ 1u)) mbar_wait_slow(p, eb, ph ^ 1u, DE_WATCHDOG_EMPTY, ti);
+        const uint32_t fb = smem_u32(&hdr->full[slot]);
+        mbar_arrive_expect_tx(fb, bytes);
+        if (hint) tma_bulk_g2s_hint(ring_addr + slot * (uint32_t)p.stage_bytes, src, bytes, fb, pol);
+        else tma_bulk_g2s(ring_addr + slot * (uint32_t)p.stage_bytes, src, bytes, fb);
+        if (++slot == n_stage) { slot = 0; ph ^= 1u; }
+        ++issued;
       };
-      if (p.pf_min_bytes > 0) prefetch_to(pf + p.pf_min_bytes);
       for (int ti = tb; ti < te; ++ti) {
-        const int4* tp = reinterpret_cast<const int4*>(p.tasks + ti);
-        const int4 q0 = __ldg(tp), q1 = __ldg(tp + 1), q2 = __ldg(tp + 2);
-        const int type = q0.x, nrows = q0.w, kchunks = q1.y, rt = q1.z, ktc = q1.w;
-        const int n_tiles = q2.x, n_ktiles = q2.y;
-        if (type == T_END) continue;
+        const Task lt = fetch_task(ti - tb);
+        const int type = lt.type, nrows = lt.b, kchunks = lt.kchunks, rt = lt.rt, ktc = lt.ktc;
+        const int n_tiles = lt.n_tiles, n_ktiles = lt.n_ktiles;
+        if (type == T_END || type == T_MERGE) continue;
         if (type == T_ATTN) {
           // K / V blocks of this unit's context chunk, one ring stage each (skipped in probe mode)
           if (p.probe) continue;
-          const AttnGeom ge = attn_geometry(p, lpos, q0.w);
-          if (q0.w >= ge.n_active) continue;
-          const int4 q3 = __ldg(tp + 3);
-          const size_t head_base = ((size_t)(q0.y * p.batch + q3.w) * p.nkv + q0.z) * (size_t)p.max_ctx * p.D;
+          const AttnGeom ge = attn_geometry(p, lpos, lt.b);
+          if (lt.b >= ge.n_active) continue;
+          const size_t head_base = ((size_t)(lt.layer * p.batch + lt.aux) * p.nkv + lt.a) * (size_t)p.max_ctx * p.D;
           for (int blk = 0; blk < ge.nblk; ++blk) {
-            const int nb = min(ge.PB, ge.n - blk * ge.PB);
+            const int nb = min(kAttnBlock, ge.n - blk * kAttnBlock);
             const uint32_t bytes = (uint32_t)nb * (uint32_t)p.D * 2u;
-            const size_t off = head_base + (size_t)(ge.t0 + blk * ge.PB) * p.D;
-            for (int kv = 0; kv < 2; ++kv) {
-              const uint32_t eb = smem_u32(&hdr->empty[slot]);
-              if (!mbar_try_wait(eb, ph ^ 1u)) mbar_wait_slow(p, eb, ph ^ 1u, DE_WATCHDOG_EMPTY, ti);
-              const uint32_t fb = smem_u32(&hdr->full[slot]);
-              mbar_arrive_expect_tx(fb, bytes);
-              tma_bulk_g2s(ring_addr + slot * (uint32_t)p.stage_bytes, (kv ? p.vcache : p.kcache) + off, bytes, fb);
-              if (++slot == n_stage) { slot = 0; ph ^= 1u; }
-            }
+            const size_t off = head_base + (size_t)(ge.t0 + blk * kAttnBlock) * p.D;
+            issue(p.kcache + off, bytes, false, ti);
+            issue(p.vcache + off, bytes, false, ti);
           }
           continue;
         }
-        const uint8_t* src = p.wpacked + (size_t)(uint32_t)q2.z * 16u;
+        const uint8_t* src = p.wpacked + (size_t)(uint32_t)lt.w_off * 16u;
         for (int tile = 0; tile < n_tiles; ++tile) {
           const int rows = min(rt, nrows - tile * rt);
           for (int kt = 0; kt < n_ktiles; ++kt) {
             const int chunks = min(ktc, kchunks - kt * ktc);
             const uint32_t bytes = (uint32_t)rows * (uint32_t)chunks * 512u;
-            const uint32_t eb = smem_u32(&hdr->empty[slot]);
-            if (!mbar_try_wait(eb, ph ^ 1u)) {
-              const long long t0 = clock64();
-              while (!mbar_try_wait_hint(eb, ph ^ 1u, 300u)) {
-                if (p.pf_max_bytes > 0 && pf < src + p.pf_max_bytes) prefetch_to(pf + 2 * kPfGranule);
-                if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_EMPTY, ti, (int)slot, (int)ph, 0);
-              }
-            }
-            const uint32_t fb = smem_u32(&hdr->full[slot]);
-            mbar_arrive_expect_tx(fb, bytes);
             const uint8_t* lsrc = src;
             if (p.probe == 3) lsrc = p.wpacked + (size_t)p.sm_stream[blockIdx.x] * 16u + ((size_t)(src - p.wpacked) & 0x3ffffu & ~(size_t)0xffff);
-            tma_bulk_g2s_hint(ring_addr + slot * (uint32_t)p.stage_bytes, lsrc, bytes, fb, pol);
+            issue(lsrc, bytes, true, ti);
             src += bytes;
-            if (p.pf_min_bytes > 0) prefetch_to(src + p.pf_min_bytes);
-            if (++slot == n_stage) { slot = 0; ph ^= 1u; }
           }
         }
       }
@@ -1064,35 +1165,32 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
   // ------------------------------ Consumers ------------------------------
   ConsumerCtx c;
   c.slot = 0; c.ph = 0; c.cw = warp - 1; c.lane = lane; c.ctid = threadIdx.x - 32; c.nct = p.C * 32;
-  c.rs = 1.0f; c.best_val = -INFINITY; c.best_idx = -1;
+  c.rs = 1.0f; c.best_val = -INFINITY; c.best_idx = -1; c.epoch = 0;
   int tok = 0, pos = 0;
-  if (!p.probe) {
+  const int probe = p.probe;
+  if (!probe) {
     tok = __ldcg(p.tokens);
     pos = __ldcg(p.positions);
+    c.epoch = ld_relaxed_u32(p.sync);
     if (pos < 0 || pos >= p.max_ctx || tok < 0 || tok >= p.V) {
       if (c.ctid == 0) dev_fail(p, DE_BAD_POS, -1, pos, tok, p.max_ctx);
       return;
     }
   }
-  auto fetch_task = [&](int ti) {
-    const int4* tp = reinterpret_cast<const int4*>(p.tasks + ti);
-    const int4 a = __ldg(tp), b = __ldg(tp + 1), cc = __ldg(tp + 2), d = __ldg(tp + 3);
-    Task t;
-    t.type = a.x; t.layer = a.y; t.a = a.z; t.b = a.w;
-    t.k = b.x; t.kchunks = b.y; t.rt = b.z; t.ktc = b.w;
-    t.n_tiles = cc.x; t.n_ktiles = cc.y; t.w_off = cc.z; t.n_stages = cc.w;
-    t.wait_ctr = d.x; t.wait_val = d.y; t.sig_ctr = d.z; t.aux = d.w;
-    return t;
-  };
-  Task next = fetch_task(tb < te ? tb : 0);
   for (int ti = tb; ti < te; ++ti) {
-    const Task t = next;
-    if (ti + 1 < te) next = fetch_task(ti + 1);  // the record is a DRAM miss: fetch one task ahead
-    if (t.type == T_ATTN) {
-      if (p.D == 128) run_attn<128, 64 / CW>(p, c, t, ti, scratch, hdr, ring, pos);
-      else run_attn<64, 64 / CW>(p, c, t, ti, scratch, hdr, ring, pos);
+    const Task t = fetch_task(ti - tb);
+    if (t.type == T_ATTN || t.type == T_MERGE) {
+      if (probe) continue;
+      WarpArgs w;
+      w.cw = c.cw; w.lane = c.lane; w.ctid = c.ctid; w.nct = c.nct; w.epoch = c.epoch; w.slot = c.slot; w.ph = c.ph;
+      w.layer = t.layer; w.a = t.a; w.b = t.b; w.aux = t.aux; w.task_idx = ti; w.pos = pos;
+      if (t.type == T_MERGE) run_merge_nl(p, w);
+      else {
+        const uint32_t sp = (p.D == 128) ? run_attn_nl<128>(p, w, scratch, hdr, ring) : run_attn_nl<64>(p, w, scratch, hdr, ring);
+        c.slot = sp & 0xffu; c.ph = sp >> 8;
+      }
     } else if (t.type != T_END) {
-      run_gemv(p, c, t, ti, scratch, hdr, ring, tok, pos);
+      run_gemv(p, c, t, ti, scratch, hdr, ring, tok, probe);
     }
   }
 }
@@ -1108,6 +1206,8 @@ struct PackParams {
   uint8_t* wpacked;
   int H, I, q_dim, kv_dim;
 };
+
+__device__ __forceinline__ bool is_gemv(int type) { return type == T_QKV || type == T_OPROJ || type == T_GATEUP || type == T_DOWN || type == T_LMHEAD; }
 
 __device__ __forceinline__ const __nv_bfloat16* resolve_row(const PackParams& pp, const Task& t, int vrow, int* K) {
   const AdamkLayerWeights* lw = (t.type == T_LMHEAD) ? nullptr : pp.layers + t.layer;
@@ -1130,7 +1230,7 @@ __global__ void adamk_pack_kernel(const PackParams pp) {
   const int ti = blockIdx.x;
   if (ti >= pp.n_tasks) return;
   const Task t = pp.tasks[ti];
-  if (t.type == T_ATTN || t.type == T_END) return;
+  if (!is_gemv(t.type)) return;
   uint4* dst = reinterpret_cast<uint4*>(pp.wpacked + (size_t)(uint32_t)t.w_off * 16u);
   size_t done = 0;  // 16-byte elements written so far
   for (int tile = 0; tile < t.n_tiles; ++tile) {
@@ -1193,15 +1293,14 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct AdamkHandle_ {
   AdamkModelDesc desc{};
-  int n_sms = 0, C = 0, n_stage = 0, stage_bytes = 0, n_tasks = 0, batch = 0, n_counters = 0;
-  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, pf_min_bytes = 0, pf_max_bytes = 0;
-  int xs_floats = 0;
+  int n_sms = 0, C = 0, n_stage = 0, stage_bytes = 0, n_tasks = 0, batch = 0, inflight = 0;
+  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, poll_sleep_ns = 0, task_cache_bytes = 0;
   const unsigned* d_sm_stream = nullptr;
   size_t packed_weight_bytes = 0;  // matrix streams only
   size_t fparam_floats = 0;
   int fp_layer_stride = 0, fp_ln1 = 0, fp_ln2 = 0, fp_bias = 0, fp_qn = 0, fp_kn = 0, fp_final = 0;
   std::vector<int> host_table;
-  int* d_table = nullptr;  // sm_begin + tasks
+  int* d_table = nullptr;  // tasks + sm_begin + sm_stream
   const int* d_sm_begin = nullptr;
   const Task* d_tasks = nullptr;
   bool bound = false;
@@ -1213,8 +1312,8 @@ struct AdamkHandle_ {
   unsigned long long* trace = nullptr;
   int smem_bytes = 0;
   // workspace layout (byte offsets)
-  size_t ws_h_a = 0, ws_h_b = 0, ws_qkv = 0, ws_attn = 0, ws_act = 0, ws_part = 0, ws_lm_val = 0, ws_lm_idx = 0,
-         ws_counters = 0, ws_total = 0;
+  size_t ws_sync = 0, ws_hx = 0, ws_hm = 0, ws_qkv = 0, ws_attn = 0, ws_act = 0, ws_part = 0, ws_lm_val = 0,
+         ws_lm_idx = 0, ws_total = 0;
 };
 
 extern "C" {
@@ -1241,38 +1340,41 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   auto h = new AdamkHandle_();
   h->desc = *desc;
   h->n_sms = tt[2]; h->C = tt[3]; h->n_stage = tt[4]; h->stage_bytes = tt[5]; h->n_tasks = tt[6]; h->batch = tt[7];
-  h->n_counters = tt[8]; h->attn_chunks = tt[9]; h->attn_min_chunk = tt[10]; h->scratch_bytes = tt[11];
-  h->n_lm_tasks = tt[12];
-  h->pf_min_bytes = tt[14] * 1024; h->pf_max_bytes = tt[15] * 1024;
+  h->inflight = tt[8]; h->attn_chunks = tt[9]; h->attn_min_chunk = tt[10]; h->scratch_bytes = tt[11];
+  h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14];
   auto bad = [&](const std::string& m) { delete h; return fail(ADAMK_E_INVALID, m); };
   const AdamkModelDesc& d = *desc;
   if (d.head_dim != 64 && d.head_dim != 128) return bad("head_dim must be 64 or 128");
   if (d.n_kv_heads < 1 || d.n_q_heads % d.n_kv_heads) return bad("n_q_heads must be a multiple of n_kv_heads");
   if (d.n_q_heads / d.n_kv_heads > kGMax) return bad("more than 8 q heads per kv head");
   if (d.hidden % 8 || d.intermediate % 8) return bad("hidden/intermediate must be multiples of 8");
+  if (d.n_layers + 2 > kTagStride) return bad("too many layers for the tag encoding");
   if (h->batch != 1 || d.max_batch != 1) { delete h; return fail(ADAMK_E_UNSUPPORTED, "batch > 1 is not built yet"); }
   if (h->C != 4 && h->C != 8 && h->C != 16) return bad("consumer_warps must be 4, 8 or 16");
-  if (h->n_stage < 1 || h->n_stage > kMaxStages) return bad("n_stage out of range");
+  if (h->n_stage < 2 || h->n_stage > kMaxStages) return bad("n_stage out of range");
+  if (h->inflight < 0 || h->inflight > h->n_stage) return bad("inflight out of range");
   if (h->stage_bytes <= 0 || h->stage_bytes % 1024) return bad("stage_bytes must be a positive multiple of 1024");
   if (h->n_sms < 1 || h->n_tasks < 1) return bad("empty task table");
   if (h->attn_chunks < 1 || h->attn_chunks > kAttnChunksMax || h->attn_min_chunk < 8)
     return bad("attention chunking out of range");
-  {
-    const int pb = std::min(64, (h->stage_bytes / (d.head_dim * 2)) & ~7);
-    if (pb != 64) return bad("stage_bytes too small: a K/V block is 64 positions (64 * head_dim * 2 bytes)");
-  }
+  if (h->stage_bytes < kAttnBlock * d.head_dim * 2)
+    return bad("stage_bytes too small: a K/V block is 64 positions (64 * head_dim * 2 bytes)");
   const size_t need = ((size_t)kHeaderInts + (size_t)h->n_sms + 1 + (size_t)h->n_tasks * kTaskInts) * 4;
   if (task_table_bytes != need) return bad("task table size does not match its header");
-  if (h->n_counters != CTR_HEAD0 + h->batch * d.n_kv_heads) return bad("counter count mismatch");
-  h->smem_bytes = kSmemReserved + h->scratch_bytes + h->n_stage * h->stage_bytes;
-  if (h->smem_bytes > kSmemMax) return bad("ring + scratch exceed 227 KB shared memory");
-  {  // the scratch region must hold the widest activation vector + merge weights, and the attention buffers
-    const int G = d.n_q_heads / d.n_kv_heads;
+  {
+    const int* sb = tt + kHeaderInts;
+    int most = 0;
+    for (int s2 = 0; s2 < h->n_sms; ++s2) most = std::max(most, sb[s2 + 1] - sb[s2]);
+    h->task_cache_bytes = (int)align_up((size_t)most * 32, 1024);
+  }
+  h->smem_bytes = kSmemReserved + h->task_cache_bytes + h->scratch_bytes + h->n_stage * h->stage_bytes;
+  if (h->smem_bytes > kSmemMax) return bad("ring + scratch + task cache exceed 227 KB shared memory");
+  const int G = d.n_q_heads / d.n_kv_heads;
+  {  // the scratch region must hold the widest activation vector, and the attention buffers
     const int kmax = std::max(std::max(d.hidden, d.n_q_heads * d.head_dim), d.intermediate);
-    h->xs_floats = (int)align_up((size_t)kmax, kChunk);
-    const size_t xb = ((size_t)h->xs_floats + 2 * (size_t)d.n_q_heads * h->attn_chunks) * 4;
-    const size_t ab = ((size_t)kGMax * (128 + 32) + 2 * (size_t)kGMax * (kAttnPBMax + 4) + (size_t)h->C * G * d.head_dim +
-                       3 * (size_t)h->C * kGMax + 2 * (size_t)d.head_dim) * 4;
+    const size_t xb = align_up((size_t)kmax, kChunk) * 4;
+    const size_t ab = ((size_t)kGMax * (d.head_dim + 16) + 2 * (size_t)d.head_dim + (size_t)kAttnWarps * kGMax * 8 +
+                       (size_t)kAttnWarps * kGMax * (d.head_dim + 2)) * 4;
     if ((size_t)h->scratch_bytes < std::max(xb, ab)) return bad("scratch_bytes too small for this model");
   }
   const int* sm_begin = tt + kHeaderInts;
@@ -1285,11 +1387,17 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   for (int i = 0; i < h->n_tasks; ++i) {
     const Task& t = tasks[i];
     if (t.type == T_ATTN) {
-      if (t.a < 0 || t.a >= d.n_kv_heads || t.b < 0 || t.b >= h->attn_chunks || t.layer < 0 || t.layer >= d.n_layers)
+      if (t.a < 0 || t.a >= d.n_kv_heads || t.b < 0 || t.b >= h->attn_chunks || t.layer < 0 || t.layer >= d.n_layers || t.aux != 0)
         return bad("attention task out of range");
       continue;
     }
+    if (t.type == T_MERGE) {
+      if (t.a < 0 || t.a >= d.n_q_heads || t.layer < 0 || t.layer >= d.n_layers || t.aux != 0) return bad("merge task out of range");
+      continue;
+    }
     if (t.type < T_QKV || t.type > T_LMHEAD) return bad("unknown task type");
+    if (t.b > 0xffff || t.rt > 0xffff || t.kchunks > 0xffff || t.ktc > 0xffff || t.n_tiles > 0xffff || t.n_ktiles > 0xffff)
+      return bad("task field exceeds the packed 16-bit range");
     int n_rows = 0, K = 0;
     switch (t.type) {
       case T_QKV: n_rows = qkv_rows; K = d.hidden; break;
@@ -1300,13 +1408,15 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
     }
     if (t.k != K || t.kchunks != (K + kChunk - 1) / kChunk) return bad("task K mismatch");
     if (t.a < 0 || t.b < 1 || t.a + t.b > n_rows) return bad("task rows out of range");
-    if (t.rt % h->C || (t.rt / h->C != 2 && t.rt / h->C != 4)) return bad("rows_per_tile / consumer_warps must be 2 or 4");
-    if (t.type == T_GATEUP && ((t.a | t.b) & 1)) return bad("gate/up rows must come in pairs");
+    const int WR = t.geom & 0xff, WK = (t.geom >> 8) & 0xff, rw = (t.geom >> 16) & 0xff;
+    if (WR < 1 || WK < 1 || WR * WK != h->C) return bad("warp grid WR x WK must equal consumer_warps");
+    if (rw < 1 || rw > kRW || t.rt != WR * rw) return bad("rows per warp out of range / rows_per_tile != WR * rw");
+    if (WK > 1 && t.rt > 32) return bad("K-split tiles hold at most 32 rows");
+    if (t.type == T_GATEUP && ((t.a | t.b | rw) & 1)) return bad("gate/up rows must come in pairs");
     if (t.ktc < 1 || t.n_ktiles != (t.kchunks + t.ktc - 1) / t.ktc || t.n_tiles != (t.b + t.rt - 1) / t.rt)
       return bad("task tiling inconsistent");
     if ((size_t)t.rt * t.ktc * 512 > (size_t)h->stage_bytes) return bad("stage larger than stage_bytes");
     if (t.type != T_LMHEAD && (t.layer < 0 || t.layer >= d.n_layers)) return bad("task layer out of range");
-    if (t.wait_ctr >= h->n_counters || t.sig_ctr >= h->n_counters) return bad("counter index out of range");
     const size_t bytes = (size_t)t.b * t.kchunks * 512;
     const size_t off = (size_t)(uint32_t)t.w_off * 16;
     wbytes = std::max(wbytes, off + bytes);
@@ -1320,14 +1430,13 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   // workspace layout
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
-  const int G = d.n_q_heads / d.n_kv_heads;
-  h->ws_counters = take((size_t)h->n_counters * 4);
-  h->ws_h_a = take((size_t)d.hidden * 4);
-  h->ws_h_b = take((size_t)d.hidden * 4);
-  h->ws_qkv = take((size_t)qkv_rows * 4);
-  h->ws_attn = take((size_t)d.n_q_heads * d.head_dim * 4);
-  h->ws_act = take(align_up((size_t)d.intermediate, kChunk) * 4);
-  h->ws_part = take((size_t)d.n_kv_heads * h->attn_chunks * G * (d.head_dim + 4) * 4);
+  h->ws_sync = take(64);
+  h->ws_hx = take((size_t)2 * d.hidden * 8);
+  h->ws_hm = take((size_t)d.hidden * 8);
+  h->ws_qkv = take((size_t)qkv_rows * 8);
+  h->ws_attn = take((size_t)d.n_q_heads * d.head_dim * 8);
+  h->ws_act = take((size_t)d.intermediate * 8);
+  h->ws_part = take((size_t)d.n_kv_heads * h->attn_chunks * G * (d.head_dim + 2) * 8);
   h->ws_lm_val = take((size_t)h->n_sms * 4);
   h->ws_lm_idx = take((size_t)h->n_sms * 4);
   h->ws_total = o;
@@ -1342,7 +1451,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
       sm_stream[sm] = cursor;
       for (int i = sm_begin[sm]; i < sm_begin[sm + 1]; ++i) {
         const Task& t = tasks[i];
-        if (t.type == T_ATTN) continue;
+        if (t.type == T_ATTN || t.type == T_MERGE) continue;
         if ((unsigned)t.w_off != cursor) return bad("packed streams must be contiguous per SM, SM-major");
         cursor += (unsigned)((size_t)t.b * t.kchunks * 512 / 16);
       }
@@ -1392,6 +1501,11 @@ size_t adamk_kv_cache_bytes(adamk_handle h) {
 int adamk_workspace_init(adamk_handle h, void* workspace, adamk_stream stream) {
   if (!h || !workspace) return fail(ADAMK_E_INVALID, "NULL argument");
   CUDA_TRY(cudaMemsetAsync(workspace, 0, h->ws_total, (cudaStream_t)stream));
+  CUDA_TRY(cudaMemsetAsync(static_cast<uint8_t*>(workspace) + h->ws_lm_idx, 0xff, (size_t)h->n_sms * 4, (cudaStream_t)stream));
+  const unsigned first_epoch = 1u;  // tags of epoch 0 (the zeroed workspace) never match
+  CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(workspace) + h->ws_sync, &first_epoch, 4, cudaMemcpyHostToDevice,
+                           (cudaStream_t)stream));
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
   return ADAMK_OK;
 }
 
@@ -1468,19 +1582,18 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
   p.has_bias = d.qkv_bias; p.qk_norm = d.qk_norm; p.eps = d.rms_eps;
   p.C = h->C; p.n_stage = h->n_stage; p.stage_bytes = h->stage_bytes; p.attn_chunks = h->attn_chunks;
   p.attn_min_chunk = h->attn_min_chunk; p.scratch_bytes = h->scratch_bytes; p.n_lm_tasks = h->n_lm_tasks;
-  p.n_counters = h->n_counters;
-  p.xs_floats = h->xs_floats;
+  p.task_cache_bytes = h->task_cache_bytes;
+  p.inflight = h->inflight; p.poll_sleep_ns = (unsigned)h->poll_sleep_ns;
   p.tasks = h->d_tasks; p.sm_begin = h->d_sm_begin; p.sm_stream = h->d_sm_stream;
-  p.pf_min_bytes = h->pf_min_bytes; p.pf_max_bytes = h->pf_max_bytes;
   p.wpacked = h->wpacked; p.fparams = h->fparams;
   p.fp_layer_stride = h->fp_layer_stride; p.fp_ln1 = h->fp_ln1; p.fp_ln2 = h->fp_ln2; p.fp_bias = h->fp_bias;
   p.fp_qn = h->fp_qn; p.fp_kn = h->fp_kn; p.fp_final = h->fp_final;
   p.embed = (const __nv_bfloat16*)h->w.embed; p.rope_cos = h->w.rope_cos; p.rope_sin = h->w.rope_sin;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   if (ws) {
-    p.counters = (unsigned*)(ws + h->ws_counters);
-    p.h_a = (float*)(ws + h->ws_h_a); p.h_b = (float*)(ws + h->ws_h_b); p.qkv = (float*)(ws + h->ws_qkv);
-    p.attn = (float*)(ws + h->ws_attn); p.act = (float*)(ws + h->ws_act); p.part = (float*)(ws + h->ws_part);
+    p.sync = (unsigned*)(ws + h->ws_sync);
+    p.ll_hx = (u64*)(ws + h->ws_hx); p.ll_hm = (u64*)(ws + h->ws_hm); p.ll_qkv = (u64*)(ws + h->ws_qkv);
+    p.ll_attn = (u64*)(ws + h->ws_attn); p.ll_act = (u64*)(ws + h->ws_act); p.ll_part = (u64*)(ws + h->ws_part);
     p.lm_val = (float*)(ws + h->ws_lm_val); p.lm_idx = (int*)(ws + h->ws_lm_idx);
   }
   p.status = h->status_dev;
@@ -1494,7 +1607,7 @@ static int launch(adamk_handle h, const KParams& p, cudaStream_t stream) {
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (sms < h->n_sms) return fail(ADAMK_E_INVALID, "task table was built for more SMs than this device has");
   void* args[] = {(void*)&p};
-  // cooperative launch: all CTAs must be co-resident (they wait on each other's counters)
+  // cooperative launch: all CTAs must be co-resident (they poll each other's outputs)
   const void* fn = h->C == 4 ? (const void*)adamk_decode_kernel<4>
                    : h->C == 8 ? (const void*)adamk_decode_kernel<8> : (const void*)adamk_decode_kernel<16>;
   CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(h->n_sms), dim3((h->C + 1) * 32), args, (size_t)h->smem_bytes, stream));
@@ -1522,8 +1635,7 @@ int adamk_stream_probe(adamk_handle h, float* sink, int mode, adamk_stream strea
   if (!h->bound) return fail(ADAMK_E_STATE, "adamk_bind_weights has not been called");
   KParams p;
   fill_params(h, p, nullptr);
-  p.probe = (mode == 2 || mode == 3) ? mode : 1; p.probe_sink = sink;
-  if (mode == 3) { p.pf_min_bytes = 0; p.pf_max_bytes = 0; }
+  p.probe = (mode >= 2 && mode <= 4) ? mode : 1; p.probe_sink = sink;
   return launch(h, p, (cudaStream_t)stream);
 }
 

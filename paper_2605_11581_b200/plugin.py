@@ -213,7 +213,7 @@ class MegaKernelPlugin:
 
     def stream_probe(self, mode: int = 1) -> None:
         if not hasattr(self, "_sink"):
-            self._sink = torch.zeros(self.n_sms, dtype=torch.float32, device=self.device)
+            self._sink = torch.zeros(self.n_sms * 64, dtype=torch.float32, device=self.device)
         _check(self.lib, self.lib.adamk_stream_probe(self._h, C.c_void_p(self._sink.data_ptr()), mode,
                                                      self._stream_ptr()))
 

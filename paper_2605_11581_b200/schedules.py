@@ -18,9 +18,9 @@ from .task_table import KernelSchedule, max_stages_that_fit
 
 SCHEDULE_DIR = Path(__file__).resolve().parent / "schedules"
 
-# Profiled on B200 (profiles/r01_notes.md): 8 consumer warps, 16-row x 1024-column
-# sub-tiles (32 KB stages), ring as deep as shared memory allows.
-PROFILED_DEFAULT = dict(consumer_warps=8, rows_per_tile=16, ktile_chunks=4)
+# Profiled on B200 (profiles/): 8 consumer warps, 64-row x 256-column sub-tiles
+# (32 KB ring slots), ring as deep as shared memory allows.
+PROFILED_DEFAULT = dict(consumer_warps=8, rows_per_tile=64, ktile_chunks=1)
 
 
 def default_schedule(cfg: ModelConfig) -> KernelSchedule:
@@ -32,5 +32,5 @@ def default_schedule(cfg: ModelConfig) -> KernelSchedule:
         if sched.n_stage > fit:
             sched = KernelSchedule.from_plan(plan, n_stage=fit)
         return sched
-    probe = KernelSchedule(n_stage=1, **PROFILED_DEFAULT)
+    probe = KernelSchedule(n_stage=2, **PROFILED_DEFAULT)
     return KernelSchedule(n_stage=min(max_stages_that_fit(cfg, probe), 8), **PROFILED_DEFAULT)

@@ -36,27 +36,27 @@ import numpy as np
 from .model_config import ModelConfig
 
 MAGIC = 0x4B4D4441  # "ADMK"
-VERSION = 1
+VERSION = 2
 HEADER_INTS = 16
 TASK_INTS = 16
 KCHUNK = 256           # K elements per chunk: 32 lanes x 8 bf16 (one LDS.128 per lane)
 SMEM_MAX = 232448      # 227 KB opt-in shared memory per CTA on sm_100
-SMEM_RESERVED = 1024   # mbarriers + reduction scratch ahead of the scratch/ring regions
+SMEM_RESERVED = 4096   # mbarriers + reduction scratch ahead of the scratch/ring regions
 MAX_STAGES = 16
-MAX_RW = 4             # rows per consumer warp per tile the kernel is instantiated for
-ATTN_PBMAX = 128       # positions per attention block (8 per consumer warp, <= 16 warps)
+MAX_RW = 8             # rows per consumer warp per tile (eight accumulator rows per lane)
+ATTN_BLOCK = 64        # positions per K (or V) ring stage
+ATTN_WARPS = 8         # consumer warps that take part in an attention unit
 ATTN_CHUNKS_MAX = 128  # split-KV units per (sequence, kv head)
+G_MAX = 8              # q heads per kv head
 
-T_END, T_QKV, T_ATTN, T_OPROJ, T_GATEUP, T_DOWN, T_LMHEAD = 0, 1, 2, 3, 4, 5, 6
+T_END, T_QKV, T_ATTN, T_OPROJ, T_GATEUP, T_DOWN, T_LMHEAD, T_MERGE = 0, 1, 2, 3, 4, 5, 6, 7
 GEMV_TYPES = (T_QKV, T_OPROJ, T_GATEUP, T_DOWN, T_LMHEAD)
-TYPE_NAMES = {T_QKV: "qkv", T_ATTN: "attn", T_OPROJ: "oproj", T_GATEUP: "gateup",
+TYPE_NAMES = {T_QKV: "qkv", T_ATTN: "attn", T_MERGE: "merge", T_OPROJ: "oproj", T_GATEUP: "gateup",
               T_DOWN: "down", T_LMHEAD: "lmhead"}
-
-CTR_A, CTR_B, CTR_C, CTR_D, CTR_E, CTR_F, CTR_HEAD0 = 0, 1, 2, 3, 4, 5, 6
 
 # field indices inside a task record
 F_TYPE, F_LAYER, F_A, F_B, F_K, F_KCHUNKS, F_RT, F_KTC, F_NTILES, F_NKTILES, \
-    F_WOFF, F_NSTAGES, F_WAITCTR, F_WAITVAL, F_SIGCTR, F_AUX = range(16)
+    F_WOFF, F_GEOM, F_R12, F_R13, F_R14, F_AUX = range(16)
 
 
 class ScheduleError(ValueError):
@@ -72,31 +72,30 @@ class KernelSchedule:
     """Pipeline parameters of the persistent kernel, taken from the plan."""
 
     consumer_warps: int = 8
-    n_stage: int = 6
-    rows_per_tile: int = 16   # plan tile block_n
-    ktile_chunks: int = 4     # plan tile sub_k / 256
-    attn_min_chunk: int = 64  # positions per split-KV unit before more SMs are used
-    # Optional L2 prefetch ahead of the ring (KB per SM; steady state / while the ring is full).
-    # Off by default: on B200 an L2 hit streams no faster than HBM (measured 6.9 vs 7.2 TB/s,
-    # profiles/r01_notes.md), so running ahead in L2 cannot recover dependency stalls.
-    l2_prefetch_kb: int = 0
-    l2_prefetch_stall_kb: int = 0
+    n_stage: int = 5
+    rows_per_tile: int = 64   # plan tile block_n: rows of a tile of the wide operators (gate/up, LM head)
+    ktile_chunks: int = 1     # plan tile sub_k / 256; ring slot = rows_per_tile * sub_k * 2 bytes
+    attn_min_chunk: int = 128  # positions per split-KV unit before more SMs are used
+    inflight: int = 0         # ring stages the Loader keeps in flight at most (0 = all free slots)
+    poll_sleep_ns: int = 0    # back-off between polls of an incomplete activation vector
 
     def __post_init__(self) -> None:
         if self.consumer_warps not in (4, 8, 16):
             raise ScheduleError("consumer_warps must be 4, 8 or 16")
-        if not 1 <= self.n_stage <= MAX_STAGES:
-            raise ScheduleError(f"n_stage must be in 1..{MAX_STAGES}")
+        if not 2 <= self.n_stage <= MAX_STAGES:
+            raise ScheduleError(f"n_stage must be in 2..{MAX_STAGES}")
         if self.rows_per_tile % self.consumer_warps:
             raise ScheduleError("rows_per_tile (block_n) must be a multiple of consumer_warps")
         rw = self.rows_per_tile // self.consumer_warps
-        if rw not in (2, 4):
-            # rw=1 would split a gate/up row pair across warps (SwiGLU is fused in-warp)
-            raise ScheduleError("block_n / consumer_warps must be 2 or 4")
+        if rw not in (2, 4, 6, 8):
+            # an odd count would split a gate/up row pair across warps (SwiGLU is fused in-warp)
+            raise ScheduleError("block_n / consumer_warps must be 2, 4, 6 or 8")
         if self.ktile_chunks < 1:
             raise ScheduleError("sub_k must be a positive multiple of 256")
         if self.attn_min_chunk < 8:
             raise ScheduleError("attn_min_chunk out of range")
+        if not 0 <= self.inflight <= self.n_stage:
+            raise ScheduleError("inflight must be in 0..n_stage")
 
     @property
     def rows_per_warp(self) -> int:
@@ -112,7 +111,8 @@ class KernelSchedule:
 
         tile = [block_m, block_n, block_k, k_split]; sub_k = block_k / k_split.
         The ring depth is the plan's ``n_stage`` (the window of
-        ``n_stage * per_stage`` pages, reference ``planner.py:415``)."""
+        ``n_stage * per_stage`` pages, reference ``planner.py:415``); the
+        prefetch stride (``stride_eff``) bounds the stages in flight."""
         bm, bn, bk, ks = plan["tile"]
         sub_k = bk // ks
         if sub_k % KCHUNK:
@@ -125,20 +125,26 @@ class KernelSchedule:
 
 def scratch_bytes(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> int:
     """Shared-memory scratch: the fp32 activation vector of the widest GEMV, or
-    the attention unit's q / scores / cross-warp reduction buffers."""
+    the attention unit's q / probability / cross-warp merge buffers."""
     kpad_max = max(_ceil_div(k, KCHUNK) * KCHUNK for k in (cfg.hidden, cfg.q_dim, cfg.intermediate))
-    nkv = cfg.n_kv_heads
-    attn_chunks = max(1, min(148 // (batch * nkv), ATTN_CHUNKS_MAX))
-    x_bytes = (batch * kpad_max + 2 * cfg.n_q_heads * ATTN_CHUNKS_MAX) * 4   # activation vector + split-KV merge (m, l)
-    g, d, c = cfg.group, cfg.head_dim, sched.consumer_warps
-    attn_bytes = (8 * 160 + 2 * 8 * (ATTN_PBMAX + 4) + c * g * d + 3 * c * 8 + 2 * d) * 4
-    del attn_chunks
+    x_bytes = batch * kpad_max * 4
+    d = cfg.head_dim
+    attn_bytes = (G_MAX * (d + 16) + 2 * d + ATTN_WARPS * G_MAX * 8 + ATTN_WARPS * G_MAX * (d + 2)) * 4
     return _ceil_div(max(x_bytes, attn_bytes), 1024) * 1024
 
 
+def task_cache_bytes(cfg: ModelConfig, batch: int = 1, n_sms: int = 148) -> int:
+    """Shared-memory copy of one SM's task list (32 bytes per task): per layer four GEMV operators
+    plus the attention units and merge tasks placed on the busiest SM; one LM-head task."""
+    nkv = cfg.n_kv_heads
+    attn_chunks = max(1, min(n_sms // (batch * nkv), ATTN_CHUNKS_MAX))
+    per_layer = 4 + _ceil_div(batch * nkv * attn_chunks, n_sms) + _ceil_div(batch * cfg.n_q_heads, n_sms)
+    return _ceil_div((cfg.n_layers * per_layer + 1) * 32, 1024) * 1024
+
+
 def max_stages_that_fit(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> int:
-    free = SMEM_MAX - SMEM_RESERVED - scratch_bytes(cfg, sched, batch)
-    return max(0, free // sched.stage_bytes)
+    free = SMEM_MAX - SMEM_RESERVED - task_cache_bytes(cfg, batch) - scratch_bytes(cfg, sched, batch)
+    return max(0, min(MAX_STAGES, free // sched.stage_bytes))
 
 
 def split_rows(n_units: int, n_sms: int, rot: int) -> list[tuple[int, int]]:
@@ -156,6 +162,48 @@ def split_rows(n_units: int, n_sms: int, rot: int) -> list[tuple[int, int]]:
     return out
 
 
+def op_geometry(sched: KernelSchedule, max_rows: int, kchunks: int, pairs: bool) -> tuple[int, int, int, int]:
+    """Warp grid of one operator: (WR, WK, rows per warp, chunks per stage).
+
+    The C consumer warps form WR row groups x WK interleaved K groups.  Wide
+    operators (more rows per SM than a K-split tile holds) use the plan tile:
+    WR = C, WK = 1, ``rows_per_tile`` rows.  Narrow operators (10-14 rows per SM
+    for the 1.5B projections) would leave most warps idle that way, so they
+    split K across warps instead; the split with the least per-warp work
+    (row-chunk iterations + per-stage overhead) wins, ties to fewer stages."""
+    c = sched.consumer_warps
+    if max_rows > c * MAX_RW:
+        rw = sched.rows_per_warp
+        rt = c * rw
+        ktc = max(1, min(kchunks, sched.stage_bytes // (rt * KCHUNK * 2)))
+        n_kt = _ceil_div(kchunks, ktc)
+        return c, 1, rw, _ceil_div(kchunks, n_kt)
+    best = None
+    wk = 1
+    while wk <= c:
+        wr = c // wk
+        rw = _ceil_div(max_rows, wr)
+        if pairs:
+            rw += rw & 1
+        rt = wr * rw
+        if rw <= MAX_RW and (wk == 1 or rt <= 32):
+            ktc_max = min(kchunks, sched.stage_bytes // (rt * KCHUNK * 2))
+            for ktc in range(1, ktc_max + 1):
+                n_kt = _ceil_div(kchunks, ktc)
+                ktc_e = _ceil_div(kchunks, n_kt)
+                cost = 3 if wk > 1 else 0
+                for kt in range(n_kt):
+                    ch = min(ktc_e, kchunks - kt * ktc_e)
+                    cost += _ceil_div(ch, wk) * (rw + 1) + 2
+                key = (cost, n_kt, wk)
+                if best is None or key < best[0]:
+                    best = (key, (wr, wk, rw, ktc_e))
+        wk *= 2
+    if best is None:
+        raise ScheduleError(f"no warp grid fits {max_rows} rows x {kchunks} chunks in a {sched.stage_bytes}-byte stage")
+    return best[1]
+
+
 @dataclass
 class TaskTable:
     cfg: ModelConfig
@@ -166,7 +214,6 @@ class TaskTable:
     sm_begin: np.ndarray    # int32[n_sms + 1]
     tasks: np.ndarray       # int32[n_tasks, TASK_INTS]
     packed_weight_bytes: int
-    n_counters: int
     attn_chunks: int
 
     @property
@@ -189,7 +236,7 @@ class TaskTable:
             "consumer_warps": self.sched.consumer_warps, "n_stage": self.sched.n_stage,
             "stage_bytes": self.sched.stage_bytes, "packed_weight_bytes": int(self.packed_weight_bytes),
             "stream_bytes_min": int(per_sm.min()), "stream_bytes_max": int(per_sm.max()),
-            "attn_chunks": self.attn_chunks, "n_counters": self.n_counters,
+            "attn_chunks": self.attn_chunks,
         }
 
 
@@ -210,6 +257,10 @@ def task_weight_bytes(task: np.ndarray) -> int:
     return int(task[F_B]) * int(task[F_KCHUNKS]) * KCHUNK * 2
 
 
+def unpack_geom(geom: int) -> tuple[int, int, int]:
+    return geom & 0xFF, (geom >> 8) & 0xFF, (geom >> 16) & 0xFF
+
+
 def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, batch: int = 1) -> TaskTable:
     if batch != 1:
         raise ScheduleError("this build executes batch 1 only (batched path: SURVEY.md 8(f).1)")
@@ -220,55 +271,58 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
         raise ScheduleError(
             f"n_stage={sched.n_stage} x {sched.stage_bytes} B stages + "
             f"{scratch_bytes(cfg, sched, batch)} B scratch exceed {SMEM_MAX} B shared memory (max {fit})")
+    if sched.stage_bytes < ATTN_BLOCK * cfg.head_dim * 2:
+        raise ScheduleError("ring slot smaller than one 64-position K/V block")
+    if cfg.group > G_MAX:
+        raise ScheduleError(f"more than {G_MAX} q heads per kv head")
     for k in (cfg.hidden, cfg.q_dim, cfg.intermediate):
         if k % 8:
             raise ScheduleError("reduction dims must be multiples of 8")
 
     nkv = cfg.n_kv_heads
     attn_chunks = max(1, min(n_sms // (batch * nkv), ATTN_CHUNKS_MAX))
-    n_counters = CTR_HEAD0 + batch * nkv
     per_sm: list[list[list[int]]] = [[] for _ in range(n_sms)]
     rot = 0
-    done = {CTR_A: 0, CTR_B: 0, CTR_D: 0, CTR_E: 0}   # cumulative signal counts per counter
 
-    def gemv(ttype: int, layer: int, n_rows: int, k: int, unit: int, wait_ctr: int, wait_val: int,
-             sig_ctr: int) -> int:
+    def gemv(ttype: int, layer: int, n_rows: int, k: int, unit: int) -> int:
         """Emit one GEMV operator across all SMs; returns the number of tasks."""
         nonlocal rot
         assert n_rows % unit == 0
         kchunks = _ceil_div(k, KCHUNK)
-        ktc = min(sched.ktile_chunks, kchunks)
-        n_kt = _ceil_div(kchunks, ktc)
-        ktc = _ceil_div(kchunks, n_kt)          # even out the k-tiles
-        n_kt = _ceil_div(kchunks, ktc)
         split = split_rows(n_rows // unit, n_sms, rot)
         rot = (rot + (n_rows // unit) % n_sms) % n_sms
+        max_rows = max(cnt for _, cnt in split) * unit
+        wr, wk, rw, ktc = op_geometry(sched, max_rows, kchunks, pairs=(unit == 2))
+        rt = wr * rw
+        n_kt = _ceil_div(kchunks, ktc)
+        geom = wr | (wk << 8) | (rw << 16)
         emitted = 0
         for sm, (first, cnt) in enumerate(split):
             if cnt == 0:
                 continue
             nrows = cnt * unit
-            n_tiles = _ceil_div(nrows, sched.rows_per_tile)
-            per_sm[sm].append([ttype, layer, first * unit, nrows, k, kchunks, sched.rows_per_tile, ktc,
-                               n_tiles, n_kt, 0, n_tiles * n_kt, wait_ctr, wait_val, sig_ctr, 0])
+            n_tiles = _ceil_div(nrows, rt)
+            per_sm[sm].append([ttype, layer, first * unit, nrows, k, kchunks, rt, ktc,
+                               n_tiles, n_kt, 0, geom, 0, 0, 0, 0])
             emitted += 1
         return emitted
 
     for layer in range(cfg.n_layers):
-        wa = (CTR_A, done[CTR_A]) if layer > 0 else (-1, 0)
-        done[CTR_B] += gemv(T_QKV, layer, cfg.qkv_rows, cfg.hidden, 1, wa[0], wa[1], CTR_B)
+        gemv(T_QKV, layer, cfg.qkv_rows, cfg.hidden, 1)
         for b in range(batch):
             for kvh in range(nkv):
                 for c in range(attn_chunks):
                     sm = ((b * nkv + kvh) * attn_chunks + c) % n_sms
-                    # every unit (active at this context length or not) signals CTR_C once
-                    per_sm[sm].append([T_ATTN, layer, kvh, c, 0, 0, 0, 0, 0, 0, 0, 0,
-                                       CTR_B, done[CTR_B], CTR_C, b])
-        done[CTR_D] += gemv(T_OPROJ, layer, cfg.hidden, cfg.q_dim, 1, CTR_C,
-                            (layer + 1) * batch * nkv * attn_chunks, CTR_D)
-        done[CTR_E] += gemv(T_GATEUP, layer, 2 * cfg.intermediate, cfg.hidden, 2, CTR_D, done[CTR_D], CTR_E)
-        done[CTR_A] += gemv(T_DOWN, layer, cfg.hidden, cfg.intermediate, 1, CTR_E, done[CTR_E], CTR_A)
-    n_lm = gemv(T_LMHEAD, cfg.n_layers, cfg.vocab, cfg.hidden, 1, CTR_A, done[CTR_A], CTR_F)
+                    per_sm[sm].append([T_ATTN, layer, kvh, c, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, b])
+            # flash-decoding merge of the units of one q head; placed on the SMs whose attention
+            # units are the last to become active as the context grows
+            for h in range(cfg.n_q_heads):
+                sm = (n_sms - 1 - (b * cfg.n_q_heads + h)) % n_sms
+                per_sm[sm].append([T_MERGE, layer, h, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, b])
+        gemv(T_OPROJ, layer, cfg.hidden, cfg.q_dim, 1)
+        gemv(T_GATEUP, layer, 2 * cfg.intermediate, cfg.hidden, 2)
+        gemv(T_DOWN, layer, cfg.hidden, cfg.intermediate, 1)
+    n_lm = gemv(T_LMHEAD, cfg.n_layers, cfg.vocab, cfg.hidden, 1)
 
     # weight offsets: each SM's stream is one contiguous run, SM-major
     cursor = 0
@@ -288,14 +342,12 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
 
     header = np.zeros(HEADER_INTS, dtype=np.int32)
     header[:13] = [MAGIC, VERSION, n_sms, sched.consumer_warps, sched.n_stage, sched.stage_bytes,
-                   tasks.shape[0], batch, n_counters, attn_chunks, sched.attn_min_chunk,
+                   tasks.shape[0], batch, sched.inflight, attn_chunks, sched.attn_min_chunk,
                    scratch_bytes(cfg, sched, batch), n_lm]
     header[13] = (cursor // 16) & 0x7FFFFFFF
-    header[14] = sched.l2_prefetch_kb
-    header[15] = sched.l2_prefetch_stall_kb
+    header[14] = sched.poll_sleep_ns
     return TaskTable(cfg=cfg, sched=sched, n_sms=n_sms, batch=batch, header=header, sm_begin=sm_begin,
-                     tasks=tasks, packed_weight_bytes=cursor, n_counters=n_counters,
-                     attn_chunks=attn_chunks)
+                     tasks=tasks, packed_weight_bytes=cursor, attn_chunks=attn_chunks)
 
 
 # ---------------------------------------------------------------------------

@@ -1,5 +1,8 @@
 #!/usr/bin/env python
-"""Bring-up benchmark: decode-loop and stream-probe timing for several schedules."""
+"""Bring-up benchmark: decode-loop and stream-probe timing for several schedules.
+
+usage: quick_bench.py [model] [ctx] [steps] [filter]
+"""
 import json
 import sys
 import time
@@ -14,23 +17,43 @@ from paper_2605_11581_b200.weights import random_weights
 name = sys.argv[1] if len(sys.argv) > 1 else "qwen2.5-1.5b"
 ctx0 = int(sys.argv[2]) if len(sys.argv) > 2 else 512
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 64
+flt = sys.argv[4] if len(sys.argv) > 4 else ""
 cfg = PRESETS[name]
-peak = json.load(open(Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"))["hbm_gbs"] if (Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").exists() else 6447.8
+root = Path(__file__).resolve().parents[1]
+peak = json.load(open(root / "MEASURED_PEAKS.json"))["hbm_gbs"] if (root / "MEASURED_PEAKS.json").exists() else 6650.0
 t0 = time.time()
 w = random_weights(cfg, 0, device="cuda")
 torch.cuda.synchronize()
 print(f"weights on device in {time.time() - t0:.1f}s", flush=True)
+B = dict(consumer_warps=8, rows_per_tile=64, ktile_chunks=1)
 scheds = [
-    ("c8 s5 32K pf0", dict(consumer_warps=8, n_stage=5, rows_per_tile=16, ktile_chunks=4, l2_prefetch_kb=0, l2_prefetch_stall_kb=0)),
-    ("c8 s5 32K pf128/512", dict(consumer_warps=8, n_stage=5, rows_per_tile=16, ktile_chunks=4)),
-    ("c8 s5 32K pf256/1024", dict(consumer_warps=8, n_stage=5, rows_per_tile=16, ktile_chunks=4, l2_prefetch_kb=256, l2_prefetch_stall_kb=1024)),
-    ("c8 s5 32K pf64/2048", dict(consumer_warps=8, n_stage=5, rows_per_tile=16, ktile_chunks=4, l2_prefetch_kb=64, l2_prefetch_stall_kb=2048)),
-    ("c8 s7 24K", dict(consumer_warps=8, n_stage=7, rows_per_tile=16, ktile_chunks=3)),
-    ("c16 s5 32K", dict(consumer_warps=16, n_stage=5, rows_per_tile=32, ktile_chunks=2)),
-    ("c16 s3 48K", dict(consumer_warps=16, n_stage=3, rows_per_tile=32, ktile_chunks=3)),
-    ("c4 s7 24K", dict(consumer_warps=4, n_stage=7, rows_per_tile=16, ktile_chunks=3)),
+    ("c8 s5 32K", dict(B, n_stage=5)),
+    ("c8 s5 32K if2", dict(B, n_stage=5, inflight=2)),
+    ("c8 s5 32K if3", dict(B, n_stage=5, inflight=3)),
+    ("c8 s5 32K sl200", dict(B, n_stage=5, poll_sleep_ns=200)),
+    ("c8 s5 32K mc64", dict(B, n_stage=5, attn_min_chunk=64)),
+    ("c8 s5 32K mc256", dict(B, n_stage=5, attn_min_chunk=256)),
+    ("c8 s11 16K", dict(consumer_warps=8, rows_per_tile=32, ktile_chunks=1, n_stage=11)),
+    ("c8 s11 16K if4", dict(consumer_warps=8, rows_per_tile=32, ktile_chunks=1, n_stage=11, inflight=4)),
+    ("c8 s11 16K if6", dict(consumer_warps=8, rows_per_tile=32, ktile_chunks=1, n_stage=11, inflight=6)),
+    ("c16 s5 32K", dict(consumer_warps=16, rows_per_tile=64, ktile_chunks=1, n_stage=5)),
+    ("c4 s5 32K", dict(consumer_warps=4, rows_per_tile=32, ktile_chunks=2, n_stage=5)),
 ]
+
+
+def timed(fn, n):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(n):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n
+
+
 for label, kw in scheds:
+    if flt and flt not in label:
+        continue
     try:
         sched = tt.KernelSchedule(**kw)
         plug = MegaKernelPlugin(cfg, sched, max_ctx=ctx0 + steps + 64)
@@ -41,40 +64,19 @@ for label, kw in scheds:
         for _ in range(5):
             plug.enqueue()
         plug.check()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         plug.set_state(1, ctx0)
-        e0.record()
-        for _ in range(steps):
-            plug.enqueue()
-        e1.record()
+        ms = timed(plug.enqueue, steps)
         plug.check()
-        ms = e0.elapsed_time(e1) / steps
-        for _ in range(3):
-            plug.stream_probe()
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(20):
-            plug.stream_probe()
-        e1.record()
-        torch.cuda.synchronize()
-        pms = e0.elapsed_time(e1) / 20
-        e0.record()
-        for _ in range(20):
-            plug.stream_probe(2)
-        e1.record()
-        torch.cuda.synchronize()
-        pms2 = e0.elapsed_time(e1) / 20
-        e0.record()
-        for _ in range(20):
-            plug.stream_probe(3)
-        e1.record()
-        torch.cuda.synchronize()
-        pms3 = e0.elapsed_time(e1) / 20
+        probes = {}
+        for mode, nm in ((1, "stream"), (2, "loader-only"), (3, "L2-resident"), (4, "consumer-only")):
+            for _ in range(3):
+                plug.stream_probe(mode)
+            torch.cuda.synchronize()
+            probes[nm] = timed(lambda: plug.stream_probe(mode), 20)
         byts = cfg.algorithmic_bytes(ctx0 + steps // 2)
-        print(f"{label:22s} decode {ms*1e3:8.1f} us/tok {1e3/ms:8.1f} tok/s  {byts/ms/1e6:7.1f} GB/s ({byts/ms/1e6/peak:.3f} of measured)"
-              f" | stream probe {pms*1e3:8.1f} us {plug.table.packed_weight_bytes/pms/1e6:7.1f} GB/s"
-              f" | loader-only {pms2*1e3:8.1f} us {plug.table.packed_weight_bytes/pms2/1e6:7.1f} GB/s"
-              f" | L2-resident {pms3*1e3:8.1f} us {plug.table.packed_weight_bytes/pms3/1e6:7.1f} GB/s", flush=True)
+        pw = plug.table.packed_weight_bytes
+        print(f"{label:18s} decode {ms*1e3:8.1f} us/tok {1e3/ms:8.1f} tok/s  {byts/ms/1e6:7.1f} GB/s ({byts/ms/1e6/peak:.3f} of measured) | "
+              + " | ".join(f"{nm} {v*1e3:7.1f} us {pw/v/1e6:7.1f} GB/s" for nm, v in probes.items()), flush=True)
         plug.close()
         del plug
     except Exception as exc:  # keep going: bring-up tool

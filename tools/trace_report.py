@@ -1,9 +1,11 @@
 #!/usr/bin/env python
 """Per-task timeline of one decode step (in-kernel %globaltimer stamps) -> phase table.
 
-    python tools/trace_report.py qwen2.5-1.5b 512 8 5 16 4 [out.json]
+    python tools/trace_report.py qwen2.5-1.5b 512 key=value ... (KernelSchedule fields)
+
+Stamps per task: 0 start, 1 inputs gathered (attention: q prepared), 2 body done (GEMV), 3 K/V blocks
+done (attention), 7 end.
 """
-import json
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -29,6 +31,7 @@ def collect(name, ctx0, kw, steps=3):
     out = []
     for _ in range(steps):
         tr.zero_()
+        plug.set_state(1, ctx0)
         plug.enqueue()
         plug.check()
         out.append(tr.cpu().numpy().copy())
@@ -40,10 +43,11 @@ def report(plug, tr):
     types, layers = tasks[:, tt.F_TYPE], tasks[:, tt.F_LAYER]
     ran = tr[:, 7] > 0
     t0 = tr[ran][:, 0].min()
-    rel = (tr - t0) / 1e3  # us
+    rel = (tr.astype(np.float64) - float(t0)) / 1e3  # us
     L = plug.cfg.n_layers
-    order = [tt.T_QKV, tt.T_ATTN, tt.T_OPROJ, tt.T_GATEUP, tt.T_DOWN]
-    rows = []
+    order = [tt.T_QKV, tt.T_ATTN, tt.T_MERGE, tt.T_OPROJ, tt.T_GATEUP, tt.T_DOWN]
+    print(f"step total (first stamp -> last end): {rel[ran][:, 7].max():.1f} us")
+    acc = {}
     prev_end = 0.0
     for layer in range(L + 1):
         for ty in (order if layer < L else [tt.T_LMHEAD]):
@@ -51,47 +55,40 @@ def report(plug, tr):
             if not m.any():
                 continue
             r = rel[m]
-            rows.append(dict(layer=layer, op=tt.TYPE_NAMES[ty], n=int(m.sum()),
-                             first_dep=float(r[:, 1].min()), last_dep=float(r[:, 1].max()),
-                             last_pro=float(r[:, 2].max()), first_end=float(r[:, 7].min()),
-                             last_end=float(r[:, 7].max()), prev_end=prev_end,
-                             wait_mean=float((r[:, 1] - r[:, 0]).mean()), pro_mean=float((r[:, 2] - r[:, 1]).mean()),
-                             body_mean=float((r[:, 7] - r[:, 2]).mean()), body_max=float((r[:, 7] - r[:, 2]).max()),
-                             seg=[float(np.mean(r[:, k] - r[:, 1])) if (tr[m][:, k] > 0).all() else float('nan') for k in range(2, 8)]))
-            prev_end = rows[-1]["last_end"]
-    total = prev_end
-    print(f"step total (first stamp -> last end): {total:.1f} us")
-    print(f"{'op':8s} {'phase':>8s} {'sync':>7s} {'dep spread':>10s} {'prologue':>8s} {'body mean':>9s} {'body max':>8s} {'end spread':>10s}")
-    agg = {}
-    for r in rows:
-        a = agg.setdefault(r["op"], [])
-        a.append([r["last_end"] - r["prev_end"], r["first_dep"] - r["prev_end"], r["last_dep"] - r["first_dep"],
-                  r["pro_mean"], r["body_mean"], r["body_max"], r["last_end"] - r["first_end"]])
-    for op, a in agg.items():
-        a = np.array(a)
-        if len(a) > 2:
-            a = a[1:]  # drop layer 0 (cold start)
-        m = a.mean(0)
-        print(f"{op:8s} {m[0]:8.2f} {m[1]:7.2f} {m[2]:10.2f} {m[3]:8.2f} {m[4]:9.2f} {m[5]:8.2f} {m[6]:10.2f}   (x{len(a)})")
-    segs = {}
-    for r in rows:
-        segs.setdefault(r["op"], []).append(r["seg"])
-    print("mean time of stamps 2..7 after the dependency was met (us; attn: 2 q-prep, 5 K landed, 3 scores, 6 V landed, 4 PV, 7 end):")
-    for op, a in segs.items():
-        a = np.array(a)
-        if len(a) > 2:
-            a = a[1:]
-        print(f"  {op:8s}", " ".join(f"{v:6.2f}" for v in np.nanmean(a, axis=0)))
-    per_layer = sum(np.array(a)[1:].mean(0)[0] for op, a in agg.items() if op != "lmhead" and len(a) > 2)
-    print(f"mean per-layer time {per_layer:.2f} us; lm head phase {np.array(agg['lmhead'])[:, 0].mean():.1f} us")
-    return rows
+            gathered = r[:, 1] if ty != tt.T_MERGE else r[:, 0]
+            end = r[:, 7]
+            d = dict(phase=end.max() - prev_end,                 # critical-path length of the op
+                     first_in=gathered.min() - prev_end,         # first SM has its inputs after the previous op ended
+                     last_in=gathered.max() - prev_end,
+                     body_mean=(end - gathered).mean(), body_max=(end - gathered).max(),
+                     end_spread=end.max() - end.min(), early=(prev_end - r[:, 0]).mean())
+            if ty == tt.T_ATTN:
+                d.update(a_kv=(r[:, 4] - r[:, 1]).mean(), a_blocks=(r[:, 3] - r[:, 4]).mean(),
+                         a_comb=(r[:, 5] - r[:, 3]).mean(), a_out=(r[:, 7] - r[:, 5]).mean(), a_qprep=(r[:, 1] - r[:, 0]).mean())
+            prev_end = end.max()
+            if layer in (0,):
+                continue  # cold start excluded from the means
+            a = acc.setdefault(tt.TYPE_NAMES[ty], [])
+            a.append(d)
+    print(f"{'op':8s} {'phase':>7s} {'first_in':>9s} {'last_in':>8s} {'body':>7s} {'bodymax':>8s} {'endsprd':>8s} {'waiting':>8s}   (us, mean over layers >= 1)")
+    tot = 0.0
+    for op, a in acc.items():
+        mean = {k: float(np.mean([d[k] for d in a])) for k in a[0]}
+        if op != "lmhead":
+            tot += mean["phase"]
+        print(f"{op:8s} {mean['phase']:7.2f} {mean['first_in']:9.2f} {mean['last_in']:8.2f} {mean['body_mean']:7.2f} "
+              f"{mean['body_max']:8.2f} {mean['end_spread']:8.2f} {mean['early']:8.2f}   (x{len(a)})")
+        if op == "attn":
+            print("   attn unit: start->q ready %.2f | ->K/V landed %.2f | blocks %.2f | warp merge sync %.2f | records out %.2f" % tuple(
+                mean[k] for k in ("a_qprep", "a_kv", "a_blocks", "a_comb", "a_out")))
+    print(f"mean per-layer time {tot:.2f} us")
 
 
 if __name__ == "__main__":
     name, ctx0 = sys.argv[1], int(sys.argv[2])
-    kw = dict(consumer_warps=int(sys.argv[3]), n_stage=int(sys.argv[4]), rows_per_tile=int(sys.argv[5]),
-              ktile_chunks=int(sys.argv[6]))
+    kw = {}
+    for a in sys.argv[3:]:
+        k, v = a.split("=")
+        kw[k] = int(v)
     plug, traces = collect(name, ctx0, kw)
-    rows = report(plug, traces[-1])
-    if len(sys.argv) > 7:
-        Path(sys.argv[7]).write_text(json.dumps(rows))
+    report(plug, traces[-1])
