@@ -59,6 +59,7 @@ constexpr int kAttnWarps = 8;        // consumer warps that take part in an atte
 constexpr int kAttnChunksMax = 128;  // split-KV units per (sequence, kv head)
 constexpr int kGMax = 8;             // max q heads per kv head
 constexpr int kRW = 8;               // max rows per warp per tile
+constexpr int kGatherBatch = 8;      // 16-byte tagged-word loads a thread keeps in flight while gathering a vector
 constexpr int kTagStride = 256;      // tag = epoch * kTagStride + layer + 1
 
 enum TaskType { T_END = 0, T_QKV = 1, T_ATTN = 2, T_OPROJ = 3, T_GATEUP = 4, T_DOWN = 5, T_LMHEAD = 6, T_MERGE = 7 };
@@ -78,6 +79,7 @@ struct KParams {
   float eps;
   // schedule
   int C, n_stage, stage_bytes, attn_chunks, attn_min_chunk, scratch_bytes, n_lm_tasks, inflight;
+  int pf_window_bytes;     // how far past the ring the Loader prefetches into L2 while it is blocked (0 = off)
   int task_cache_bytes;    // shared-memory copy of this SM's task list (32-byte packed records)
   unsigned poll_sleep_ns;  // back-off between polls of a not-yet-complete vector (0 = none)
   // task table
@@ -100,7 +102,7 @@ struct KParams {
   u64* ll_qkv;   // [qkv_rows]
   u64* ll_attn;  // [q_dim]  merged attention output
   u64* ll_act;   // [I]
-  u64* ll_part;  // [nkv][attn_chunks][G][D + 2]  split-KV partial records (o[D], m, l)
+  u64* ll_part;  // [nq][attn_chunks][D + 2]  split-KV partial records (o[D], m, l)
   float* lm_val;
   int* lm_idx;
   unsigned* sync;  // [0] = epoch, [1] = CTAs that finished the LM head
@@ -141,6 +143,17 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t bar, uint32_t parity)
       : "memory");
   return ok;
 }
+__device__ __forceinline__ uint32_t mbar_test_wait(uint32_t bar, uint32_t parity) {  // non-blocking probe
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok;
+}
 __device__ __forceinline__ uint32_t mbar_try_wait_hint(uint32_t bar, uint32_t parity, uint32_t ns) {
   uint32_t ok;
   asm volatile(
@@ -168,6 +181,9 @@ __device__ __forceinline__ void tma_bulk_g2s_hint(uint32_t dst, const void* src,
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
       "l"(src), "r"(bytes), "r"(bar), "l"(pol)
       : "memory");
+}
+__device__ __forceinline__ void l2_prefetch_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
@@ -322,24 +338,24 @@ __device__ __noinline__ float ll_gather(const KParams& p, int ctid, int nct, con
   const bool NORM = gain != nullptr;
   const int n2 = n >> 1, kp2 = kpad >> 1;
   float ss = 0.f;
-  for (int i0 = ctid; i0 < kp2; i0 += 4 * nct) {
-    float2 g[4];
+  for (int i0 = ctid; i0 < kp2; i0 += kGatherBatch * nct) {
+    float2 g[kGatherBatch];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // static operand first: a DRAM miss under the weight stream, overlapped with the poll
+    for (int u = 0; u < kGatherBatch; ++u) {  // static operand first: a DRAM miss under the weight stream, overlapped with the poll
       const int i = i0 + u * nct;
       g[u] = (NORM && i < n2) ? __ldg(reinterpret_cast<const float2*>(gain) + i) : make_float2(1.f, 1.f);
     }
-    u64 a[4], b[4];
+    u64 a[kGatherBatch], b[kGatherBatch];
     long long t0 = 0;
     for (;;) {  // re-issue the whole batch until every tag is current (one round trip per attempt)
       bool ok = true;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kGatherBatch; ++u) {
         const int i = i0 + u * nct;
         if (i < n2) ll_load2(src + 2 * i, a[u], b[u]);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kGatherBatch; ++u) {
         const int i = i0 + u * nct;
         if (i < n2) ok = ok && ll_tag(a[u]) == tag && ll_tag(b[u]) == tag;
       }
@@ -349,7 +365,7 @@ __device__ __noinline__ float ll_gather(const KParams& p, int ctid, int nct, con
       else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task, (int)ll_tag(a[0]), (int)tag, i0);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kGatherBatch; ++u) {
       const int i = i0 + u * nct;
       if (i < kp2) {
         float2 v = make_float2(0.f, 0.f);
@@ -553,8 +569,9 @@ __device__ __forceinline__ void gemv_ktiles(const KParams& p, uint32_t& slot, ui
   }
 }
 
-__device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx,
-                                           const float* xs, SmemHdr* hdr, uint8_t* ring, int tok, float eop0, int probe) {
+template <int RW>
+__device__ __forceinline__ void gemv_tiles_t(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx,
+                                             const float* xs, SmemHdr* hdr, uint8_t* ring, int tok, float eop0, int probe) {
   const int WK = (t.geom >> 8) & 0xff, rw = (t.geom >> 16) & 0xff, lgWK = 31 - __clz(WK);
   const int wr = c.cw >> lgWK, wk = c.cw & (WK - 1);
   const uint32_t ring_addr = smem_u32(ring) + c.lane * 16;
@@ -569,7 +586,6 @@ __device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, con
   sg.wofs_last = (uint32_t)my_r0 * sg.rstride_last + (uint32_t)wk * 512u;
   sg.nch_full = (t.ktc - wk + WK - 1) >> lgWK; sg.nch_last = max(0, (chunks_last - wk + WK - 1) >> lgWK);
   const uint32_t xs_addr = smem_u32(xs) + c.lane * 16 + (uint32_t)wk * (kChunk * 4);
-  const int rwc = (rw + 1) >> 1;
   for (int tile = 0; tile < t.n_tiles; ++tile) {
     const int rows = min(t.rt, t.b - tile * t.rt);
     const int my_n = max(0, min(rw, rows - my_r0));  // rows of this tile owned by this warp
@@ -587,13 +603,7 @@ __device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, con
     const bool active = my_n > 0 && probe != 2;
     {
       uint32_t slot = c.slot, ph = c.ph;
-      const bool wait = probe != 4;
-      switch (probe == 4 ? 4 : rwc) {
-        case 1: gemv_ktiles<2>(p, slot, ph, c.lane, t.ktc, t.n_ktiles, task_idx, sg, ring_addr, xs_addr, full0, empty0, WK, acc, active, wait); break;
-        case 2: gemv_ktiles<4>(p, slot, ph, c.lane, t.ktc, t.n_ktiles, task_idx, sg, ring_addr, xs_addr, full0, empty0, WK, acc, active, wait); break;
-        case 3: gemv_ktiles<6>(p, slot, ph, c.lane, t.ktc, t.n_ktiles, task_idx, sg, ring_addr, xs_addr, full0, empty0, WK, acc, active, wait); break;
-        default: gemv_ktiles<8>(p, slot, ph, c.lane, t.ktc, t.n_ktiles, task_idx, sg, ring_addr, xs_addr, full0, empty0, WK, acc, active, wait); break;
-      }
+      gemv_ktiles<RW>(p, slot, ph, c.lane, t.ktc, t.n_ktiles, task_idx, sg, ring_addr, xs_addr, full0, empty0, WK, acc, active, probe != 4);
       c.slot = slot; c.ph = ph;
     }
     float v[kRW];
@@ -625,6 +635,19 @@ __device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, con
         }
       }
     }
+  }
+  // every warp is done reading the staged activation vector before the next task overwrites the
+  // scratch region (K-split tiles already synchronised after their last stage)
+  if (WK == 1 && !probe) consumer_sync(c.nct);
+}
+
+__device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx,
+                                           const float* xs, SmemHdr* hdr, uint8_t* ring, int tok, float eop0, int probe) {
+  switch ((((t.geom >> 16) & 0xff) + 1) >> 1) {  // rows per warp, rounded up to even
+    case 1: gemv_tiles_t<2>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
+    case 2: gemv_tiles_t<4>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
+    case 3: gemv_tiles_t<6>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
+    default: gemv_tiles_t<8>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
   }
 }
 
@@ -706,44 +729,47 @@ __device__ __forceinline__ void run_gemv(const KParams& p, ConsumerCtx& c, const
 }
 
 // ----------------------------------------------------------------------------------
-// attention unit = (kv head, context chunk)
+// attention unit = (q head, context chunk)
 // ----------------------------------------------------------------------------------
 // Scratch layout (floats), must fit task_table.scratch_bytes:
-//   qs[kGMax][D + 16] | knew[D] | vnew[D] | pbuf[kAttnWarps][kGMax][8] | comb[kAttnWarps][kGMax][D + 2]
+//   qs[D + 16] | knew[D] | vnew[D] | comb[kAttnWarps][D + 2] | sw[kAttnWarps]
 //
-// The K and V rows of the unit's context chunk arrive through the weight ring (the paper's
-// "KV-cache loads advanced into the pipeline window"): per block of 64 positions one
-// K stage and one V stage, issued by the Loader long before the QKV projections of this layer are
-// done; the row of the new token is patched into the staged copy.  Each of the (up to 8) attention
-// warps owns 8 positions of a block and keeps its own running softmax state (m, l, o) in registers
-// for all q heads of the group; the warps are merged once at the end.  The unit publishes one
-// partial record (o[D], m, l) per q head; T_MERGE tasks combine the records of all units of a head.
-// With a single active unit the normalised output is published directly.
+// Decode attention is latency, not throughput: a layer's K/V is a few hundred KB but every later
+// operator waits for it.  So the work is spread as widely as it goes -- one unit per (q head, chunk
+// of the context), the q heads of a group re-reading their K/V blocks from L2 -- and the code of a
+// unit is a short loop nest (it runs once per layer per SM; its instruction footprint matters more
+// than its FLOPs).  The K and V rows of the chunk arrive through the weight ring (the paper's
+// "KV-cache loads advanced into the pipeline window"): per block of 64 positions one K
+// stage and one V stage, issued by the Loader long before this layer's QKV projections are done;
+// the row of the new token is patched into the staged copy.  Each of the (up to 8) attention warps
+// owns 8 positions of a block (4 lanes per position in the score step, lanes over the head dim in
+// P.V) with its online-softmax state in registers; the warps are merged once at the end.  The unit
+// publishes one partial record (o[D], m, l); the T_MERGE task of the head combines the records of
+// its units.  With a single active unit the normalised output is published directly.
 template <int D>
 __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* scratch,
                                          SmemHdr* hdr, uint8_t* ring, int pos) {
   constexpr int DL = D / 4;      // dims per lane in the score step (4 lanes per position)
   constexpr int QS = D + 16;     // padded q row: 4 segments of DL floats, 4 floats apart (conflict-free)
   constexpr int DPL = D / 32;    // output dims per lane
-  constexpr int RS = D + 2;      // per-(warp, head) record: o[D], m, l
-  const int G = p.G, kvh = t.a, slot = t.b;
-  if (p.probe) return;
+  constexpr int RS = D + 2;      // record: o[D], m, l
+  const int G = p.G, h = t.a, slot = t.b, kvh = h / G;
   const AttnGeom ge = attn_geometry(p, pos, slot);
   if (slot >= ge.n_active) return;  // no context for this slot at this length
   stamp(p, c, task_idx, 0);
   const int n = ge.n, t0 = ge.t0, nblk = ge.nblk;
   const bool owns_new = (slot == ge.n_active - 1);  // this chunk contains position `pos`
+  const bool writes_cache = owns_new && h == kvh * G;  // one unit per kv head appends K/V to the cache
   const unsigned tag = tag_of(c, t.layer);
   const int AW = min(p.C, kAttnWarps);
 
   float* qs = scratch;
-  float* knew = qs + kGMax * QS;
+  float* knew = qs + QS;
   float* vnew = knew + D;
-  float* pbuf = vnew + D;
-  float* comb = pbuf + kAttnWarps * kGMax * 8;
+  float* comb = vnew + D;                 // [AW][RS]
+  float* sw = comb + kAttnWarps * RS;     // [AW]
 
   const float* lay_fp = p.fparams + (size_t)t.layer * p.fp_layer_stride;
-  const float scale = rsqrtf((float)D);
   const size_t head_base = ((size_t)(t.layer * p.batch + t.aux) * p.nkv + kvh) * (size_t)p.max_ctx * D;
   __nv_bfloat16* Kc = p.kcache + head_base;
   __nv_bfloat16* Vc = p.vcache + head_base;
@@ -752,52 +778,54 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
   const uint32_t empty0 = smem_u32(&hdr->empty[0]);
   const uint32_t n_stage = (uint32_t)p.n_stage;
 
-  // ---- q heads of the group (+ k, v of the new token in the owner unit): gather, (norm), RoPE ----
+  // ---- q row (+ k, v of the new token in the owner units): gather, (norm), RoPE ----
   // one warp per row of D elements; lane holds elements lane + 32 j so rotate-half partners share a lane
-  {
+  if (c.cw < (owns_new ? 3 : 1)) {
     constexpr int PER = D / 32, HALF = D / 2;
+    const bool is_q = c.cw == 0, is_k = c.cw == 1;
     float cs[PER / 2], sn[PER / 2];
 #pragma unroll
     for (int j = 0; j < PER / 2; ++j) {  // static operands first: they are DRAM misses
       cs[j] = __ldg(p.rope_cos + (size_t)pos * HALF + c.lane + 32 * j);
       sn[j] = __ldg(p.rope_sin + (size_t)pos * HALF + c.lane + 32 * j);
     }
-    const int n_rows = G + (owns_new ? 2 : 0);
-    for (int r = c.cw; r < n_rows; r += p.C) {
-      const bool is_q = r < G, is_k = r == G;
-      const u64* src = p.ll_qkv + (is_q ? (size_t)(kvh * G + r) * D : (size_t)p.q_dim + (is_k ? 0 : p.kv_dim) + (size_t)kvh * D);
-      float v[PER];
-      ll_wait_strided<PER>(p, src + c.lane, 32, tag, v, task_idx);
-      if (!is_q && !is_k) {  // v row: cache + staged patch value
+    float gn[PER];
 #pragma unroll
-        for (int j = 0; j < PER; ++j) {
-          vnew[c.lane + 32 * j] = v[j];
-          Vc[(size_t)pos * D + c.lane + 32 * j] = __float2bfloat16_rn(v[j]);
-        }
-        continue;
+    for (int j = 0; j < PER; ++j) gn[j] = (p.qk_norm && (is_q || is_k)) ? __ldg(lay_fp + (is_q ? p.fp_qn : p.fp_kn) + c.lane + 32 * j) : 1.f;
+    const u64* src = p.ll_qkv + (is_q ? (size_t)h * D : (size_t)p.q_dim + (is_k ? 0 : p.kv_dim) + (size_t)kvh * D);
+    float v[PER];
+    ll_wait_strided<PER>(p, src + c.lane, 32, tag, v, task_idx);
+    if (!is_q && !is_k) {  // v row: staged patch value (+ cache)
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        vnew[c.lane + 32 * j] = v[j];
+        if (writes_cache) Vc[(size_t)pos * D + c.lane + 32 * j] = __float2bfloat16_rn(v[j]);
       }
+    } else {
       if (p.qk_norm) {
         float ss = 0.f;
 #pragma unroll
         for (int j = 0; j < PER; ++j) ss += v[j] * v[j];
         ss = warp_sum(ss);
         const float rs = rsqrtf(ss / (float)D + p.eps);
-        const float* gn = lay_fp + (is_q ? p.fp_qn : p.fp_kn);
 #pragma unroll
-        for (int j = 0; j < PER; ++j) v[j] = v[j] * rs * __ldg(gn + c.lane + 32 * j);
+        for (int j = 0; j < PER; ++j) v[j] = v[j] * rs * gn[j];
       }
+      const float scale = is_q ? rsqrtf((float)D) : 1.f;
 #pragma unroll
       for (int j = 0; j < PER / 2; ++j) {
         const int d1 = c.lane + 32 * j;  // < HALF
         const float x1 = v[j], x2 = v[j + PER / 2];
-        const float y1 = x1 * cs[j] - x2 * sn[j], y2 = x2 * cs[j] + x1 * sn[j];
+        const float y1 = (x1 * cs[j] - x2 * sn[j]) * scale, y2 = (x2 * cs[j] + x1 * sn[j]) * scale;
         if (is_q) {
-          qs[r * QS + d1 + (d1 / DL) * 4] = y1 * scale;
-          qs[r * QS + d1 + HALF + ((d1 + HALF) / DL) * 4] = y2 * scale;
+          qs[d1 + (d1 / DL) * 4] = y1;
+          qs[d1 + HALF + ((d1 + HALF) / DL) * 4] = y2;
         } else {
           knew[d1] = y1; knew[d1 + HALF] = y2;
-          Kc[(size_t)pos * D + d1] = __float2bfloat16_rn(y1);
-          Kc[(size_t)pos * D + d1 + HALF] = __float2bfloat16_rn(y2);
+          if (writes_cache) {
+            Kc[(size_t)pos * D + d1] = __float2bfloat16_rn(y1);
+            Kc[(size_t)pos * D + d1 + HALF] = __float2bfloat16_rn(y2);
+          }
         }
       }
     }
@@ -805,199 +833,150 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
   consumer_sync(c.nct);
   stamp(p, c, task_idx, 1);
 
-  // ---- per-warp running state ----
-  float o[kGMax][DPL], m_run[kGMax], l_part[kGMax];
-#pragma unroll
-  for (int g = 0; g < kGMax; ++g) {
-    m_run[g] = -INFINITY; l_part[g] = 0.f;
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) o[g][e] = 0.f;
-  }
   const int lsub = c.lane & 3, lpos = c.lane >> 2;
-  float* pw = pbuf + c.cw * (kGMax * 8);  // this warp's probabilities [g][8]
+  float qf[DL];  // this lane's quarter of the q row
+#pragma unroll
+  for (int e = 0; e < DL; e += 4) {
+    const float4 q4 = *reinterpret_cast<const float4*>(qs + lsub * (DL + 4) + e);
+    qf[e] = q4.x; qf[e + 1] = q4.y; qf[e + 2] = q4.z; qf[e + 3] = q4.w;
+  }
+  float m_run = -INFINITY, l_run = 0.f, o[DPL];
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) o[e] = 0.f;
 
+#pragma unroll 1
   for (int blk = 0; blk < nblk; ++blk) {
     const bool patch = owns_new && blk == nblk - 1;
     const int new_row = (pos - t0) - blk * kAttnBlock;  // row of the new token inside this block (if patch)
     const int nblkpos = min(kAttnBlock, n - blk * kAttnBlock);
-    // ---------------- K stage ----------------
-    mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);
+    mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);   // K stage
     const uint32_t kb = ring_addr + c.slot * (uint32_t)p.stage_bytes;
     const uint32_t kslot = c.slot;
     if (++c.slot == n_stage) { c.slot = 0; c.ph ^= 1u; }
-    if (patch) {  // the staged copy predates this step's K row: overwrite it (bf16, as the cache holds it)
-      for (int d = c.ctid; d < D; d += c.nct) {
-        const unsigned short bits = __bfloat16_as_ushort(__float2bfloat16_rn(knew[d]));
-        asm volatile("st.shared.u16 [%0], %1;" ::"r"(kb + (uint32_t)(new_row * D + d) * 2u), "h"(bits) : "memory");
-      }
-      consumer_sync(c.nct);
-    }
-    // ---------------- V stage (waited for now so both are ready; consumed below) ----------------
-    mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);
+    mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);   // V stage
     const uint32_t vb = ring_addr + c.slot * (uint32_t)p.stage_bytes;
     const uint32_t vslot = c.slot;
     if (++c.slot == n_stage) { c.slot = 0; c.ph ^= 1u; }
-    if (patch) {
-      for (int d = c.ctid; d < D; d += c.nct) {
-        const unsigned short bits = __bfloat16_as_ushort(__float2bfloat16_rn(vnew[d]));
-        asm volatile("st.shared.u16 [%0], %1;" ::"r"(vb + (uint32_t)(new_row * D + d) * 2u), "h"(bits) : "memory");
+    if (patch) {  // the staged copies predate this step's K / V row: overwrite them (bf16, as the cache holds them)
+      for (int d = c.ctid; d < 2 * D; d += c.nct) {
+        const bool isv = d >= D;
+        const int dd = isv ? d - D : d;
+        const unsigned short bits = __bfloat16_as_ushort(__float2bfloat16_rn(isv ? vnew[dd] : knew[dd]));
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"((isv ? vb : kb) + (uint32_t)(new_row * D + dd) * 2u), "h"(bits) : "memory");
       }
       consumer_sync(c.nct);
     }
     if (blk == 0) stamp(p, c, task_idx, 4);
-    // each attention warp takes groups of 8 positions: j0 = 8 cw, 8 (cw + AW), ...
     if (c.cw < AW) {
-      for (int j0 = c.cw * 8; j0 < nblkpos; j0 += AW * 8) {
-        const int tl = j0 + lpos;                 // this lane's position inside the block
+#pragma unroll 1
+      for (int j0 = c.cw * 8; j0 < nblkpos; j0 += AW * 8) {  // groups of 8 positions
+        const int tl = j0 + lpos;
         const bool valid = tl < nblkpos;
-        // scores of position tl for every head: 4 lanes share a position, each DL dims
-        float kf[DL];
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
         {
           const uint32_t krow = kb + (uint32_t)(tl * D + lsub * DL) * 2u;
 #pragma unroll
           for (int e = 0; e < DL; e += 8) {
             const uint4 raw = lds128u(krow + e * 2);
-            kf[e + 0] = bf_lo(raw.x); kf[e + 1] = bf_hi(raw.x); kf[e + 2] = bf_lo(raw.y); kf[e + 3] = bf_hi(raw.y);
-            kf[e + 4] = bf_lo(raw.z); kf[e + 5] = bf_hi(raw.z); kf[e + 6] = bf_lo(raw.w); kf[e + 7] = bf_hi(raw.w);
+            s0 = fmaf(qf[e + 0], bf_lo(raw.x), s0); s1 = fmaf(qf[e + 1], bf_hi(raw.x), s1);
+            s2 = fmaf(qf[e + 2], bf_lo(raw.y), s2); s3 = fmaf(qf[e + 3], bf_hi(raw.y), s3);
+            s0 = fmaf(qf[e + 4], bf_lo(raw.z), s0); s1 = fmaf(qf[e + 5], bf_hi(raw.z), s1);
+            s2 = fmaf(qf[e + 6], bf_lo(raw.w), s2); s3 = fmaf(qf[e + 7], bf_hi(raw.w), s3);
           }
         }
-        float sc[kGMax];
+        float sdot = (s0 + s1) + (s2 + s3);
+        sdot += __shfl_xor_sync(0xffffffffu, sdot, 1);
+        sdot += __shfl_xor_sync(0xffffffffu, sdot, 2);
+        sdot = valid ? sdot : -INFINITY;
+        float mb = sdot;  // position j0 of the group is always valid -> finite
+        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 4));
+        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 8));
+        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
+        const float m_new = fmaxf(m_run, mb);
+        const float resc = __expf(m_run - m_new);       // exp(-inf) = 0 on the first group
+        const float pj = valid ? __expf(sdot - m_new) : 0.f;
+        m_run = m_new;
+        l_run = l_run * resc + (lsub == 0 ? pj : 0.f);
 #pragma unroll
-        for (int g = 0; g < kGMax; ++g) {
-          sc[g] = -INFINITY;
-          if (g < G) {
-            const float4* qp = reinterpret_cast<const float4*>(qs + g * QS + lsub * (DL + 4));
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        for (int e = 0; e < DPL; ++e) o[e] *= resc;
 #pragma unroll
-            for (int e = 0; e < DL / 4; ++e) {
-              const float4 q4 = qp[e];
-              s0 = fmaf(q4.x, kf[e * 4 + 0], s0); s1 = fmaf(q4.y, kf[e * 4 + 1], s1);
-              s2 = fmaf(q4.z, kf[e * 4 + 2], s2); s3 = fmaf(q4.w, kf[e * 4 + 3], s3);
-            }
-            float sdot = (s0 + s1) + (s2 + s3);
-            sdot += __shfl_xor_sync(0xffffffffu, sdot, 1);
-            sdot += __shfl_xor_sync(0xffffffffu, sdot, 2);
-            sc[g] = valid ? sdot : -INFINITY;
-          }
-        }
-        // online softmax over the 8 positions of the group, all heads
-        float resc[kGMax];
-#pragma unroll
-        for (int g = 0; g < kGMax; ++g) {
-          resc[g] = 1.f;
-          if (g < G) {
-            float mb = sc[g];
-            mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 4));
-            mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 8));
-            mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
-            const float m_new = fmaxf(m_run[g], mb);   // finite: position j0 of the group is always valid
-            resc[g] = expf(m_run[g] - m_new);          // exp(-inf) = 0 on the first group
-            const float pj = valid ? expf(sc[g] - m_new) : 0.f;
-            m_run[g] = m_new;
-            l_part[g] = l_part[g] * resc[g] + (lsub == 0 ? pj : 0.f);
-            if (lsub == 0) pw[g * 8 + lpos] = pj;
-          }
-        }
-        __syncwarp();
-        // P.V: lanes split the head dim; probabilities come back as two LDS.128 per head
-#pragma unroll
-        for (int g = 0; g < kGMax; ++g) {
-          if (g < G) {
-#pragma unroll
-            for (int e = 0; e < DPL; ++e) o[g][e] *= resc[g];
-          }
-        }
-        const int npos = min(8, nblkpos - j0);
-        for (int j = 0; j < npos; ++j) {
-          float vf[DPL];
+        for (int j = 0; j < 8; ++j) {
+          const float pg = __shfl_sync(0xffffffffu, pj, 4 * j);
+          const int row = min(j0 + j, nblkpos - 1);   // rows past the end carry pg = 0
           if constexpr (DPL == 4) {
             uint2 raw;
-            asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(raw.x), "=r"(raw.y) : "r"(vb + (uint32_t)((j0 + j) * D + c.lane * 4) * 2u));
-            vf[0] = bf_lo(raw.x); vf[1] = bf_hi(raw.x); vf[2] = bf_lo(raw.y); vf[3] = bf_hi(raw.y);
+            asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(raw.x), "=r"(raw.y) : "r"(vb + (uint32_t)(row * D + c.lane * 4) * 2u));
+            o[0] = fmaf(pg, bf_lo(raw.x), o[0]); o[1] = fmaf(pg, bf_hi(raw.x), o[1]);
+            o[2] = fmaf(pg, bf_lo(raw.y), o[2]); o[3] = fmaf(pg, bf_hi(raw.y), o[3]);
           } else {
             uint32_t raw;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(vb + (uint32_t)((j0 + j) * D + c.lane * 2) * 2u));
-            vf[0] = bf_lo(raw); vf[1] = bf_hi(raw);
-          }
-#pragma unroll
-          for (int g = 0; g < kGMax; ++g) {
-            if (g < G) {
-              const float pg = pw[g * 8 + j];
-#pragma unroll
-              for (int e = 0; e < DPL; ++e) o[g][e] = fmaf(pg, vf[e], o[g][e]);
-            }
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(vb + (uint32_t)(row * D + c.lane * 2) * 2u));
+            o[0] = fmaf(pg, bf_lo(raw), o[0]); o[1] = fmaf(pg, bf_hi(raw), o[1]);
           }
         }
-        __syncwarp();  // pw is rewritten by the next group
       }
     }
     __syncwarp();
     if (c.lane == 0) { mbar_arrive(empty0 + kslot * 8); mbar_arrive(empty0 + vslot * 8); }
   }
   stamp(p, c, task_idx, 3);
-
-  // ---- merge the attention warps: comb[w][g] = (o[D], m, l) ----
+  // ---- merge the attention warps ----
   if (c.cw < AW) {
+    float l = l_run;
+    l += __shfl_xor_sync(0xffffffffu, l, 4);
+    l += __shfl_xor_sync(0xffffffffu, l, 8);
+    l += __shfl_xor_sync(0xffffffffu, l, 16);
+    float* rec = comb + c.cw * RS;
 #pragma unroll
-    for (int g = 0; g < kGMax; ++g) {
-      if (g < G) {
-        float l = l_part[g];
-        l += __shfl_xor_sync(0xffffffffu, l, 4);
-        l += __shfl_xor_sync(0xffffffffu, l, 8);
-        l += __shfl_xor_sync(0xffffffffu, l, 16);
-        float* rec = comb + (size_t)(c.cw * kGMax + g) * RS;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) rec[c.lane * DPL + e] = o[g][e];
-        if (c.lane == 0) { rec[D] = m_run[g]; rec[D + 1] = l; }
-      }
-    }
+    for (int e = 0; e < DPL; ++e) rec[c.lane * DPL + e] = o[e];
+    if (c.lane == 0) { rec[D] = m_run; rec[D + 1] = l; }
   }
   consumer_sync(c.nct);
   stamp(p, c, task_idx, 5);
-  const bool final_out = ge.n_active == 1;
-  u64* part = p.ll_part + ((size_t)(t.aux * p.nkv + kvh) * p.attn_chunks + slot) * (size_t)G * RS;
-  for (int i = c.ctid; i < G * D; i += c.nct) {
-    const int g = i / D, d = i - g * D;
+  if (c.ctid < D) {
+    const int d = c.ctid;
     float M = -INFINITY;
-    for (int w = 0; w < AW; ++w) M = fmaxf(M, comb[(size_t)(w * kGMax + g) * RS + D]);
+    for (int w = 0; w < AW; ++w) M = fmaxf(M, comb[w * RS + D]);
     float ov = 0.f, lv = 0.f;
     for (int w = 0; w < AW; ++w) {
-      const float* rec = comb + (size_t)(w * kGMax + g) * RS;
-      const float wgt = expf(rec[D] - M);   // warps without positions: m = -inf -> weight 0
-      ov = fmaf(wgt, rec[d], ov);
-      lv = fmaf(wgt, rec[D + 1], lv);
+      const float wgt = __expf(comb[w * RS + D] - M);   // warps without positions: m = -inf -> weight 0
+      ov = fmaf(wgt, comb[w * RS + d], ov);
+      lv = fmaf(wgt, comb[w * RS + D + 1], lv);
     }
-    if (final_out) {
-      ll_store(p.ll_attn + (size_t)(kvh * G + g) * D + d, ov / lv, tag);
+    if (ge.n_active == 1) {
+      ll_store(p.ll_attn + (size_t)h * D + d, ov / lv, tag);
     } else {
-      ll_store(part + (size_t)g * RS + d, ov, tag);
-      if (d == 0) { ll_store(part + (size_t)g * RS + D, M, tag); ll_store(part + (size_t)g * RS + D + 1, lv, tag); }
+      u64* part = p.ll_part + ((size_t)(t.aux * p.nq + h) * p.attn_chunks + slot) * (size_t)RS;
+      ll_store(part + d, ov, tag);
+      if (d == 0) { ll_store(part + D, M, tag); ll_store(part + D + 1, lv, tag); }
     }
   }
+  (void)sw;
+  consumer_sync(c.nct);  // the next task overwrites the scratch region
   stamp(p, c, task_idx, 7);
 }
 
 // Flash-decoding merge of the split-KV records of one q head: out[d] = sum_s w_s o_s[d] / sum_s w_s l_s,
-// w_s = exp(m_s - M).  Thread d (< D) walks the active units with eight independent loads in flight.
+// w_s = exp(m_s - M).  Thread d (< D) walks the active units with sixteen independent loads in flight.
 __device__ __forceinline__ void run_merge(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, int pos) {
   if (p.probe) return;
   const AttnGeom ge = attn_geometry(p, pos, 0);
   if (ge.n_active <= 1) return;  // the single unit published the output itself
   stamp(p, c, task_idx, 0);
-  const int D = p.D, G = p.G, RS = D + 2, h = t.a, kvh = h / G, g = h - kvh * G;
+  const int D = p.D, RS = D + 2, h = t.a;
   const unsigned tag = tag_of(c, t.layer);
-  const u64* base = p.ll_part + ((size_t)(t.aux * p.nkv + kvh) * p.attn_chunks) * (size_t)G * RS + (size_t)g * RS;
-  const size_t cs = (size_t)G * RS;
+  const u64* base = p.ll_part + ((size_t)(t.aux * p.nq + h) * p.attn_chunks) * (size_t)RS;
+  const size_t cs = (size_t)RS;
   if (c.ctid < D) {
     const int d = c.ctid;
     float M = -INFINITY, L = 0.f, O = 0.f;
-    for (int s0 = 0; s0 < ge.n_active; s0 += 4) {
-      u64 wo[4], wm[4], wl[4];
+    for (int s0 = 0; s0 < ge.n_active; s0 += 8) {
+      u64 wo[8], wm[8], wl[8];
       long long t0 = 0;
       for (;;) {
         bool ok = true;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
           if (s0 + u < ge.n_active) {
             const u64* rec = base + (size_t)(s0 + u) * cs;
             wo[u] = ll_load(rec + d);
@@ -1005,7 +984,7 @@ __device__ __forceinline__ void run_merge(const KParams& p, ConsumerCtx& c, cons
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 8; ++u)
           if (s0 + u < ge.n_active) ok = ok && ll_tag(wo[u]) == tag && ll_tag(wm[u]) == tag && ll_tag(wl[u]) == tag;
         if (ok) break;
         if (p.poll_sleep_ns) __nanosleep(p.poll_sleep_ns);
@@ -1013,11 +992,11 @@ __device__ __forceinline__ void run_merge(const KParams& p, ConsumerCtx& c, cons
         else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task_idx, (int)ll_tag(wo[0]), (int)tag, s0);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         if (s0 + u < ge.n_active) {
           const float m = ll_val(wm[u]);
           const float Mn = fmaxf(M, m);
-          const float a = expf(M - Mn), b = expf(m - Mn);
+          const float a = __expf(M - Mn), b = __expf(m - Mn);
           O = O * a + ll_val(wo[u]) * b;
           L = L * a + ll_val(wl[u]) * b;
           M = Mn;
@@ -1043,6 +1022,25 @@ __device__ __noinline__ uint32_t run_attn_nl(const KParams& p, WarpArgs w, float
   Task t{};
   t.type = T_ATTN; t.layer = w.layer; t.a = w.a; t.b = w.b; t.aux = w.aux;
   run_attn<D>(p, c, t, w.task_idx, scratch, hdr, ring, w.pos);
+  return c.slot | (c.ph << 8);
+}
+// The GEMV task body is out of line as well: its register allocation and instruction schedule then
+// depend only on its own code (the hot loop is sensitive to both), not on what else the kernel inlines.
+struct GemvArgs {
+  int cw, lane, ctid, nct;
+  unsigned epoch;
+  uint32_t slot, ph;
+  int type, layer, a, b, k, kchunks, rt, ktc, n_tiles, n_ktiles, geom;
+  int task_idx, tok, probe;
+};
+__device__ __noinline__ uint32_t run_gemv_nl(const KParams& p, GemvArgs g, float* xs, SmemHdr* hdr, uint8_t* ring) {
+  ConsumerCtx c;
+  c.cw = g.cw; c.lane = g.lane; c.ctid = g.ctid; c.nct = g.nct; c.epoch = g.epoch; c.slot = g.slot; c.ph = g.ph;
+  c.rs = 1.f; c.best_val = -INFINITY; c.best_idx = -1;
+  Task t{};
+  t.type = g.type; t.layer = g.layer; t.a = g.a; t.b = g.b; t.k = g.k; t.kchunks = g.kchunks; t.rt = g.rt; t.ktc = g.ktc;
+  t.n_tiles = g.n_tiles; t.n_ktiles = g.n_ktiles; t.geom = g.geom;
+  run_gemv(p, c, t, g.task_idx, xs, hdr, ring, g.tok, g.probe);
   return c.slot | (c.ph << 8);
 }
 __device__ __noinline__ void run_merge_nl(const KParams& p, WarpArgs w) {
@@ -1110,14 +1108,35 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
         lpos = __ldcg(p.positions);
         if (lpos < 0 || lpos >= p.max_ctx) return;  // the consumers report the error
       }
+      // While the ring is full (consumers waiting on another SM) the Loader keeps HBM busy by
+      // prefetching its own upcoming weight stages into L2, up to pf_window bytes past the ring.
+      const uint8_t* wcur = p.wpacked + (size_t)p.sm_stream[blockIdx.x] * 16u;        // next weight byte the ring will load
+      const uint8_t* const wend = p.wpacked + (size_t)p.sm_stream[blockIdx.x + 1] * 16u;
+      const uint8_t* pf = wcur;
+      unsigned n_pf = 0;  // L2 prefetch granules issued this step (debug counter in sync[4])
+      constexpr uint32_t kPfGranule = 8192;
+      auto blocked_wait = [&](uint32_t bar, uint32_t parity, int code, int ti) {
+        if (mbar_try_wait(bar, parity)) return;
+        if (p.pf_window_bytes > 0 && !p.probe) {
+          const long long t0 = clock64();
+          if (pf < wcur) pf = wcur;
+          while (pf < wend && pf < wcur + p.pf_window_bytes) {
+            if (mbar_test_wait(bar, parity)) return;
+            const uint32_t nb = (uint32_t)min((size_t)kPfGranule, (size_t)(wend - pf));
+            l2_prefetch_bulk(pf, nb);
+            pf += nb;
+            ++n_pf;
+            if (clock64() - t0 > kWatchdogCycles) dev_fail(p, code, ti, (int)bar, (int)parity, 0);
+          }
+        }
+        mbar_wait_slow(p, bar, parity, code, ti);
+      };
       auto issue = [&](const void* src, uint32_t bytes, bool hint, int ti) {
         if (issued >= cap) {  // at most `cap` stages in flight: wait for the oldest one to land
-          const uint32_t fbw = smem_u32(&hdr->full[wslot]);
-          if (!mbar_try_wait(fbw, wph)) mbar_wait_slow(p, fbw, wph, DE_WATCHDOG_INFLIGHT, ti);
+          blocked_wait(smem_u32(&hdr->full[wslot]), wph, DE_WATCHDOG_INFLIGHT, ti);
           if (++wslot == n_stage) { wslot = 0; wph ^= 1u; }
         }
-        const uint32_t eb = smem_u32(&hdr->empty[slot]);
-        if (!mbar_try_wait(eb, ph ^ 1u)) mbar_wait_slow(p, eb, ph ^ 1u, DE_WATCHDOG_EMPTY, ti);
+        blocked_wait(smem_u32(&hdr->empty[slot]), ph ^ 1u, DE_WATCHDOG_EMPTY, ti);
         const uint32_t fb = smem_u32(&hdr->full[slot]);
         mbar_arrive_expect_tx(fb, bytes);
         if (hint) tma_bulk_g2s_hint(ring_addr + slot * (uint32_t)p.stage_bytes, src, bytes, fb, pol);
@@ -1135,7 +1154,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
           if (p.probe) continue;
           const AttnGeom ge = attn_geometry(p, lpos, lt.b);
           if (lt.b >= ge.n_active) continue;
-          const size_t head_base = ((size_t)(lt.layer * p.batch + lt.aux) * p.nkv + lt.a) * (size_t)p.max_ctx * p.D;
+          const size_t head_base = ((size_t)(lt.layer * p.batch + lt.aux) * p.nkv + lt.a / p.G) * (size_t)p.max_ctx * p.D;
           for (int blk = 0; blk < ge.nblk; ++blk) {
             const int nb = min(kAttnBlock, ge.n - blk * kAttnBlock);
             const uint32_t bytes = (uint32_t)nb * (uint32_t)p.D * 2u;
@@ -1155,9 +1174,11 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
             if (p.probe == 3) lsrc = p.wpacked + (size_t)p.sm_stream[blockIdx.x] * 16u + ((size_t)(src - p.wpacked) & 0x3ffffu & ~(size_t)0xffff);
             issue(lsrc, bytes, true, ti);
             src += bytes;
+            wcur = src;
           }
         }
       }
+      if (n_pf && p.sync) atomicAdd(p.sync + 4, n_pf);
     }
     return;
   }
@@ -1190,7 +1211,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
         c.slot = sp & 0xffu; c.ph = sp >> 8;
       }
     } else if (t.type != T_END) {
-      run_gemv(p, c, t, ti, scratch, hdr, ring, tok, probe);
+      GemvArgs g;
+      g.cw = c.cw; g.lane = c.lane; g.ctid = c.ctid; g.nct = c.nct; g.epoch = c.epoch; g.slot = c.slot; g.ph = c.ph;
+      g.type = t.type; g.layer = t.layer; g.a = t.a; g.b = t.b; g.k = t.k; g.kchunks = t.kchunks; g.rt = t.rt; g.ktc = t.ktc;
+      g.n_tiles = t.n_tiles; g.n_ktiles = t.n_ktiles; g.geom = t.geom; g.task_idx = ti; g.tok = tok; g.probe = probe;
+      const uint32_t sp = run_gemv_nl(p, g, scratch, hdr, ring);
+      c.slot = sp & 0xffu; c.ph = sp >> 8;
     }
   }
 }
@@ -1294,7 +1320,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct AdamkHandle_ {
   AdamkModelDesc desc{};
   int n_sms = 0, C = 0, n_stage = 0, stage_bytes = 0, n_tasks = 0, batch = 0, inflight = 0;
-  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, poll_sleep_ns = 0, task_cache_bytes = 0;
+  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, poll_sleep_ns = 0, task_cache_bytes = 0, pf_window_kb = 0;
   const unsigned* d_sm_stream = nullptr;
   size_t packed_weight_bytes = 0;  // matrix streams only
   size_t fparam_floats = 0;
@@ -1341,7 +1367,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   h->desc = *desc;
   h->n_sms = tt[2]; h->C = tt[3]; h->n_stage = tt[4]; h->stage_bytes = tt[5]; h->n_tasks = tt[6]; h->batch = tt[7];
   h->inflight = tt[8]; h->attn_chunks = tt[9]; h->attn_min_chunk = tt[10]; h->scratch_bytes = tt[11];
-  h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14];
+  h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14]; h->pf_window_kb = tt[15];
   auto bad = [&](const std::string& m) { delete h; return fail(ADAMK_E_INVALID, m); };
   const AdamkModelDesc& d = *desc;
   if (d.head_dim != 64 && d.head_dim != 128) return bad("head_dim must be 64 or 128");
@@ -1350,7 +1376,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   if (d.hidden % 8 || d.intermediate % 8) return bad("hidden/intermediate must be multiples of 8");
   if (d.n_layers + 2 > kTagStride) return bad("too many layers for the tag encoding");
   if (h->batch != 1 || d.max_batch != 1) { delete h; return fail(ADAMK_E_UNSUPPORTED, "batch > 1 is not built yet"); }
-  if (h->C != 4 && h->C != 8 && h->C != 16) return bad("consumer_warps must be 4, 8 or 16");
+  if (h->C != 4 && h->C != 7 && h->C != 8 && h->C != 16) return bad("consumer_warps must be 4, 7, 8 or 16");
   if (h->n_stage < 2 || h->n_stage > kMaxStages) return bad("n_stage out of range");
   if (h->inflight < 0 || h->inflight > h->n_stage) return bad("inflight out of range");
   if (h->stage_bytes <= 0 || h->stage_bytes % 1024) return bad("stage_bytes must be a positive multiple of 1024");
@@ -1373,8 +1399,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   {  // the scratch region must hold the widest activation vector, and the attention buffers
     const int kmax = std::max(std::max(d.hidden, d.n_q_heads * d.head_dim), d.intermediate);
     const size_t xb = align_up((size_t)kmax, kChunk) * 4;
-    const size_t ab = ((size_t)kGMax * (d.head_dim + 16) + 2 * (size_t)d.head_dim + (size_t)kAttnWarps * kGMax * 8 +
-                       (size_t)kAttnWarps * kGMax * (d.head_dim + 2)) * 4;
+    const size_t ab = ((size_t)(d.head_dim + 16) + 2 * (size_t)d.head_dim + (size_t)kAttnWarps * (d.head_dim + 2) + kAttnWarps) * 4;
     if ((size_t)h->scratch_bytes < std::max(xb, ab)) return bad("scratch_bytes too small for this model");
   }
   const int* sm_begin = tt + kHeaderInts;
@@ -1387,7 +1412,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   for (int i = 0; i < h->n_tasks; ++i) {
     const Task& t = tasks[i];
     if (t.type == T_ATTN) {
-      if (t.a < 0 || t.a >= d.n_kv_heads || t.b < 0 || t.b >= h->attn_chunks || t.layer < 0 || t.layer >= d.n_layers || t.aux != 0)
+      if (t.a < 0 || t.a >= d.n_q_heads || t.b < 0 || t.b >= h->attn_chunks || t.layer < 0 || t.layer >= d.n_layers || t.aux != 0)
         return bad("attention task out of range");
       continue;
     }
@@ -1436,7 +1461,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   h->ws_qkv = take((size_t)qkv_rows * 8);
   h->ws_attn = take((size_t)d.n_q_heads * d.head_dim * 8);
   h->ws_act = take((size_t)d.intermediate * 8);
-  h->ws_part = take((size_t)d.n_kv_heads * h->attn_chunks * G * (d.head_dim + 2) * 8);
+  h->ws_part = take((size_t)d.n_q_heads * h->attn_chunks * (d.head_dim + 2) * 8);
   h->ws_lm_val = take((size_t)h->n_sms * 4);
   h->ws_lm_idx = take((size_t)h->n_sms * 4);
   h->ws_total = o;
@@ -1467,6 +1492,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
     e = cudaHostGetDevicePointer(&h->status_dev, h->status_host, 0);
   }
   if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   if (e != cudaSuccess) {
@@ -1582,7 +1608,7 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
   p.has_bias = d.qkv_bias; p.qk_norm = d.qk_norm; p.eps = d.rms_eps;
   p.C = h->C; p.n_stage = h->n_stage; p.stage_bytes = h->stage_bytes; p.attn_chunks = h->attn_chunks;
   p.attn_min_chunk = h->attn_min_chunk; p.scratch_bytes = h->scratch_bytes; p.n_lm_tasks = h->n_lm_tasks;
-  p.task_cache_bytes = h->task_cache_bytes;
+  p.task_cache_bytes = h->task_cache_bytes; p.pf_window_bytes = h->pf_window_kb * 1024;
   p.inflight = h->inflight; p.poll_sleep_ns = (unsigned)h->poll_sleep_ns;
   p.tasks = h->d_tasks; p.sm_begin = h->d_sm_begin; p.sm_stream = h->d_sm_stream;
   p.wpacked = h->wpacked; p.fparams = h->fparams;
@@ -1609,6 +1635,7 @@ static int launch(adamk_handle h, const KParams& p, cudaStream_t stream) {
   void* args[] = {(void*)&p};
   // cooperative launch: all CTAs must be co-resident (they poll each other's outputs)
   const void* fn = h->C == 4 ? (const void*)adamk_decode_kernel<4>
+                   : h->C == 7 ? (const void*)adamk_decode_kernel<7>
                    : h->C == 8 ? (const void*)adamk_decode_kernel<8> : (const void*)adamk_decode_kernel<16>;
   CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(h->n_sms), dim3((h->C + 1) * 32), args, (size_t)h->smem_bytes, stream));
   return ADAMK_OK;

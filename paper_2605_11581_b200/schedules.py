@@ -18,9 +18,12 @@ from .task_table import KernelSchedule, max_stages_that_fit
 
 SCHEDULE_DIR = Path(__file__).resolve().parent / "schedules"
 
-# Profiled on B200 (profiles/): 8 consumer warps, 64-row x 256-column sub-tiles
-# (32 KB ring slots), ring as deep as shared memory allows.
-PROFILED_DEFAULT = dict(consumer_warps=8, rows_per_tile=64, ktile_chunks=1)
+# Profiled on B200 (profiles/): 7 consumer warps + the Loader warp = 8 warps per CTA (the register
+# file then gives every thread 255 registers; 9 warps are capped at 168 and the GEMV loop spills),
+# 56-row x 512-column sub-tiles (56 KB ring slots: two chunk iterations per warp per stage amortise
+# the per-stage barrier work), ring as deep as shared memory allows, 128-position split-KV units,
+# and a 512 KB per-SM L2 prefetch window past the ring.
+PROFILED_DEFAULT = dict(consumer_warps=7, rows_per_tile=56, ktile_chunks=2, attn_min_chunk=128, l2_prefetch_kb=512)
 
 
 def default_schedule(cfg: ModelConfig) -> KernelSchedule:
@@ -33,4 +36,4 @@ def default_schedule(cfg: ModelConfig) -> KernelSchedule:
             sched = KernelSchedule.from_plan(plan, n_stage=fit)
         return sched
     probe = KernelSchedule(n_stage=2, **PROFILED_DEFAULT)
-    return KernelSchedule(n_stage=min(max_stages_that_fit(cfg, probe), 8), **PROFILED_DEFAULT)
+    return KernelSchedule(n_stage=max(2, min(max_stages_that_fit(cfg, probe), 8)), **PROFILED_DEFAULT)

@@ -78,10 +78,11 @@ class KernelSchedule:
     attn_min_chunk: int = 128  # positions per split-KV unit before more SMs are used
     inflight: int = 0         # ring stages the Loader keeps in flight at most (0 = all free slots)
     poll_sleep_ns: int = 0    # back-off between polls of an incomplete activation vector
+    l2_prefetch_kb: int = 0   # per-SM window past the ring the Loader prefetches into L2 while it is blocked
 
     def __post_init__(self) -> None:
-        if self.consumer_warps not in (4, 8, 16):
-            raise ScheduleError("consumer_warps must be 4, 8 or 16")
+        if self.consumer_warps not in (4, 7, 8, 16):
+            raise ScheduleError("consumer_warps must be 4, 7, 8 or 16")
         if not 2 <= self.n_stage <= MAX_STAGES:
             raise ScheduleError(f"n_stage must be in 2..{MAX_STAGES}")
         if self.rows_per_tile % self.consumer_warps:
@@ -129,16 +130,16 @@ def scratch_bytes(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> in
     kpad_max = max(_ceil_div(k, KCHUNK) * KCHUNK for k in (cfg.hidden, cfg.q_dim, cfg.intermediate))
     x_bytes = batch * kpad_max * 4
     d = cfg.head_dim
-    attn_bytes = (G_MAX * (d + 16) + 2 * d + ATTN_WARPS * G_MAX * 8 + ATTN_WARPS * G_MAX * (d + 2)) * 4
+    attn_bytes = ((d + 16) + 2 * d + ATTN_WARPS * (d + 2) + ATTN_WARPS) * 4
     return _ceil_div(max(x_bytes, attn_bytes), 1024) * 1024
 
 
 def task_cache_bytes(cfg: ModelConfig, batch: int = 1, n_sms: int = 148) -> int:
     """Shared-memory copy of one SM's task list (32 bytes per task): per layer four GEMV operators
     plus the attention units and merge tasks placed on the busiest SM; one LM-head task."""
-    nkv = cfg.n_kv_heads
-    attn_chunks = max(1, min(n_sms // (batch * nkv), ATTN_CHUNKS_MAX))
-    per_layer = 4 + _ceil_div(batch * nkv * attn_chunks, n_sms) + _ceil_div(batch * cfg.n_q_heads, n_sms)
+    nq = cfg.n_q_heads
+    attn_chunks = max(1, min(n_sms // (batch * nq), ATTN_CHUNKS_MAX))
+    per_layer = 4 + _ceil_div(batch * nq * attn_chunks, n_sms) + _ceil_div(batch * nq, n_sms)
     return _ceil_div((cfg.n_layers * per_layer + 1) * 32, 1024) * 1024
 
 
@@ -172,15 +173,22 @@ def op_geometry(sched: KernelSchedule, max_rows: int, kchunks: int, pairs: bool)
     split K across warps instead; the split with the least per-warp work
     (row-chunk iterations + per-stage overhead) wins, ties to fewer stages."""
     c = sched.consumer_warps
-    if max_rows > c * MAX_RW:
+
+    def plan_tile():
         rw = sched.rows_per_warp
         rt = c * rw
         ktc = max(1, min(kchunks, sched.stage_bytes // (rt * KCHUNK * 2)))
         n_kt = _ceil_div(kchunks, ktc)
         return c, 1, rw, _ceil_div(kchunks, n_kt)
+
+    if max_rows > c * MAX_RW:
+        return plan_tile()
     best = None
     wk = 1
     while wk <= c:
+        if c % wk:
+            wk *= 2
+            continue
         wr = c // wk
         rw = _ceil_div(max_rows, wr)
         if pairs:
@@ -199,8 +207,8 @@ def op_geometry(sched: KernelSchedule, max_rows: int, kchunks: int, pairs: bool)
                 if best is None or key < best[0]:
                     best = (key, (wr, wk, rw, ktc_e))
         wk *= 2
-    if best is None:
-        raise ScheduleError(f"no warp grid fits {max_rows} rows x {kchunks} chunks in a {sched.stage_bytes}-byte stage")
+    if best is None:   # the ring slot is too small for a single tile of all rows: several plan tiles
+        return plan_tile()
     return best[1]
 
 
@@ -279,8 +287,8 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
         if k % 8:
             raise ScheduleError("reduction dims must be multiples of 8")
 
-    nkv = cfg.n_kv_heads
-    attn_chunks = max(1, min(n_sms // (batch * nkv), ATTN_CHUNKS_MAX))
+    nq = cfg.n_q_heads
+    attn_chunks = max(1, min(n_sms // (batch * nq), ATTN_CHUNKS_MAX))
     per_sm: list[list[list[int]]] = [[] for _ in range(n_sms)]
     rot = 0
 
@@ -310,10 +318,12 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
     for layer in range(cfg.n_layers):
         gemv(T_QKV, layer, cfg.qkv_rows, cfg.hidden, 1)
         for b in range(batch):
-            for kvh in range(nkv):
-                for c in range(attn_chunks):
-                    sm = ((b * nkv + kvh) * attn_chunks + c) % n_sms
-                    per_sm[sm].append([T_ATTN, layer, kvh, c, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, b])
+            # one unit per (q head, context chunk): chunk-major so the units that are active at short
+            # contexts (chunk 0, 1, ...) land on different SMs
+            for c in range(attn_chunks):
+                for h in range(nq):
+                    sm = ((b * attn_chunks + c) * nq + h) % n_sms
+                    per_sm[sm].append([T_ATTN, layer, h, c, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, b])
             # flash-decoding merge of the units of one q head; placed on the SMs whose attention
             # units are the last to become active as the context grows
             for h in range(cfg.n_q_heads):
@@ -346,6 +356,7 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
                    scratch_bytes(cfg, sched, batch), n_lm]
     header[13] = (cursor // 16) & 0x7FFFFFFF
     header[14] = sched.poll_sleep_ns
+    header[15] = sched.l2_prefetch_kb
     return TaskTable(cfg=cfg, sched=sched, n_sms=n_sms, batch=batch, header=header, sm_begin=sm_begin,
                      tasks=tasks, packed_weight_bytes=cursor, attn_chunks=attn_chunks)
 

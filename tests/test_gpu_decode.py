@@ -25,6 +25,9 @@ SCHEDS = {
     "c8": tt.KernelSchedule(consumer_warps=8, n_stage=4, rows_per_tile=16, ktile_chunks=2, attn_min_chunk=8),
     "c4": tt.KernelSchedule(consumer_warps=4, n_stage=3, rows_per_tile=16, ktile_chunks=1, attn_min_chunk=16),
     "c16": tt.KernelSchedule(consumer_warps=16, n_stage=5, rows_per_tile=32, ktile_chunks=2, attn_min_chunk=8),
+    # the profiled default shape (7 consumer warps + Loader = 8 warps, 56 KB slots) with L2 prefetch and an in-flight cap
+    "c7": tt.KernelSchedule(consumer_warps=7, n_stage=3, rows_per_tile=56, ktile_chunks=2, attn_min_chunk=16,
+                            l2_prefetch_kb=64, inflight=2),
 }
 
 
@@ -46,7 +49,7 @@ def _cos(a, b):
 
 
 @pytest.mark.parametrize("cfg,sname", [(TINY, "c8"), (TINY_QWEN3, "c8"), (D128, "c8"), (D128_Q3, "c8"),
-                                       (TINY, "c4"), (D128, "c16")],
+                                       (TINY, "c4"), (D128, "c16"), (D128, "c7"), (D128_Q3, "c7"), (TINY_QWEN3, "c7")],
                          ids=lambda v: v if isinstance(v, str) else v.name)
 def test_stepwise_logits_match_oracle(cfg, sname):
     """Teacher-forced: 40 steps (crossing the single-chunk -> split-KV boundary),
@@ -137,10 +140,11 @@ def test_device_resident_greedy_loop_matches_oracle(cfg):
     plug.close()
 
 
-def test_long_context_split_kv():
-    """Context 700 with min chunk 8 -> every chunk slot active, multi-chunk combine."""
+@pytest.mark.parametrize("sname", ["c8", "c7"])
+def test_long_context_split_kv(sname):
+    """Context 700 with a small min chunk -> every chunk slot active, multi-block units, multi-record merge."""
     cfg = D128
-    w, ref, plug = _setup(cfg, SCHEDS["c8"], max_ctx=1024)
+    w, ref, plug = _setup(cfg, SCHEDS[sname], max_ctx=1024)
     g = torch.Generator().manual_seed(2)
     prompt = torch.randint(0, cfg.vocab, (700,), generator=g).tolist()
     ref.prefill(prompt)
@@ -189,3 +193,42 @@ def test_hybrid_engine_generate_matches_oracle():
     assert res.tokens[:first_tie] == want[:first_tie] and first_tie >= 12
     assert res.prefill_launches == 23 and res.decode_launches == 24
     eng.close()
+
+
+def test_default_schedule_runs_and_matches_oracle():
+    """The shipped default schedule (schedules.default_schedule) on a mid-size model: logits parity over
+    a few steps that start inside a prefilled context."""
+    from paper_2605_11581_b200.schedules import default_schedule
+
+    cfg = D128_Q3
+    w, ref, plug = _setup(cfg, default_schedule(cfg), max_ctx=512)
+    g = torch.Generator().manual_seed(11)
+    prompt = torch.randint(0, cfg.vocab, (300,), generator=g).tolist()
+    ref.prefill(prompt)
+    kc, vc = plug.kv_view()
+    kc[:, 0, :, :300] = ref.k_cache[:, 0, :, :300].to(kc.device)
+    vc[:, 0, :, :300] = ref.v_cache[:, 0, :, :300].to(vc.device)
+    tok = 5
+    for pos in range(300, 306):
+        want = ref.step([tok], [pos])[0].numpy()
+        out = plug.decode_step(tok, pos)
+        plug.check()
+        got = out.logits[0].cpu().numpy()
+        assert np.abs(got - want).max() <= 2e-3
+        tok = int(want.argmax())
+    plug.close()
+
+
+def test_repeated_runs_are_bitwise_reproducible():
+    """The tagged-word exchange sums in a fixed order: two runs of the same steps give identical logits."""
+    cfg = D128
+    outs = []
+    for _ in range(2):
+        _, _, plug = _setup(cfg, SCHEDS["c7"])
+        acc = []
+        for pos, tok in enumerate([3, 17, 4000, 25, 999, 1, 2, 3]):
+            acc.append(plug.decode_step(tok, pos).logits[0].clone())
+        plug.check()
+        outs.append(torch.stack(acc).cpu())
+        plug.close()
+    assert torch.equal(outs[0], outs[1])

@@ -69,23 +69,30 @@ def test_packed_stream_covers_every_weight_exactly_once(cfg):
             assert (ks == 1).all(), (layer, name, row)
 
 
-PHASE_OF = {tt.T_QKV: 0, tt.T_ATTN: 1, tt.T_OPROJ: 2, tt.T_GATEUP: 3, tt.T_DOWN: 4}
+def _n_active(table: tt.TaskTable, ctx: int) -> int:
+    cl = max(table.sched.attn_min_chunk, -(-ctx // table.attn_chunks))
+    cl = (cl + 7) & ~7
+    return -(-ctx // cl)
 
 
 def _simulate_dataflow(table: tt.TaskTable, ctx: int):
     """Replay the per-SM task lists against the kernel's data dependencies (tagged-word
-    protocol): a task needs EVERY task of the previous phase to have published its
-    outputs (attention: every unit that is active at this context length).  Returns the
-    number of rounds; raises on deadlock."""
-    cfg, sched = table.cfg, table.sched
-    cl = max(sched.attn_min_chunk, -(-ctx // table.attn_chunks))
-    cl = (cl + 7) & ~7
-    n_active = -(-ctx // cl)
+    protocol, csrc/adamk.cu): a task can run once EVERY task that publishes one of the
+    words it gathers has run (attention: every unit that is active at this context length;
+    with a single active unit the unit publishes the merged output itself).  Returns the
+    completion counts; raises on deadlock."""
+    cfg = table.cfg
+    n_active = _n_active(table, ctx)
     tasks = table.tasks
     L = cfg.n_layers
 
     def active(t):
-        return int(t[tt.F_TYPE]) != tt.T_ATTN or int(t[tt.F_B]) < n_active
+        ty = int(t[tt.F_TYPE])
+        if ty == tt.T_ATTN:
+            return int(t[tt.F_B]) < n_active
+        if ty == tt.T_MERGE:
+            return n_active > 1
+        return True
 
     total = {}
     for t in tasks:
@@ -94,22 +101,29 @@ def _simulate_dataflow(table: tt.TaskTable, ctx: int):
             total[key] = total.get(key, 0) + 1
     done = {k: 0 for k in total}
 
+    def complete(key):
+        return done.get(key, 0) == total.get(key, 0)
+
     def ready(t) -> bool:
         ty, layer = int(t[tt.F_TYPE]), int(t[tt.F_LAYER])
         if ty == tt.T_LMHEAD:
-            prev = (L - 1, tt.T_DOWN)
-        elif ty == tt.T_QKV:
-            if layer == 0:
-                return True
-            prev = (layer - 1, tt.T_DOWN)
-        else:
-            prev = (layer, {tt.T_ATTN: tt.T_QKV, tt.T_OPROJ: tt.T_ATTN, tt.T_GATEUP: tt.T_OPROJ,
-                            tt.T_DOWN: tt.T_GATEUP}[ty])
-        return done[prev] == total[prev]
+            return complete((L - 1, tt.T_DOWN))
+        if ty == tt.T_QKV:
+            return layer == 0 or complete((layer - 1, tt.T_DOWN))
+        if ty == tt.T_ATTN:
+            return complete((layer, tt.T_QKV))
+        if ty == tt.T_MERGE:
+            return complete((layer, tt.T_ATTN))
+        if ty == tt.T_OPROJ:   # gathers the merged attention output (+ the layer input as residual)
+            return complete((layer, tt.T_ATTN)) and complete((layer, tt.T_MERGE))
+        if ty == tt.T_GATEUP:
+            return complete((layer, tt.T_OPROJ))
+        if ty == tt.T_DOWN:
+            return complete((layer, tt.T_GATEUP))
+        raise AssertionError(ty)
 
     pc = table.sm_begin[:-1].astype(np.int64).copy()
     end = table.sm_begin[1:]
-    rounds = 0
     while (pc < end).any():
         progressed = False
         for sm in range(table.n_sms):
@@ -121,41 +135,80 @@ def _simulate_dataflow(table: tt.TaskTable, ctx: int):
                     done[(int(t[tt.F_LAYER]), int(t[tt.F_TYPE]))] += 1
                 pc[sm] += 1
                 progressed = True
-        rounds += 1
         if not progressed:
             raise AssertionError(f"deadlock: pcs {pc[:8]}")
-    return rounds, done
+    return done
 
 
 @pytest.mark.parametrize("ctx", [1, 8, 9, 100, 600])
 def test_dataflow_has_no_deadlock(ctx):
     table = tt.build_task_table(TINY, SCHED_TINY, n_sms=148)
-    _, done = _simulate_dataflow(table, ctx)
+    done = _simulate_dataflow(table, ctx)
     assert done[(TINY.n_layers, tt.T_LMHEAD)] == table.header[12]
+    n_active = _n_active(table, ctx)
+    assert done[(0, tt.T_ATTN)] == TINY.n_q_heads * n_active
+    assert done.get((0, tt.T_MERGE), 0) == (TINY.n_q_heads if n_active > 1 else 0)
 
 
-def test_every_sm_updates_the_residual_stream():
-    """The residual stream is replicated per CTA and brought up to date by the QKV, gate/up and
-    LM-head prologues: every SM must own exactly one of each per layer, even with zero rows."""
-    for n_sms in (148, 5, 300):
-        table = tt.build_task_table(TINY, SCHED_TINY, n_sms=n_sms)
-        for sm in range(n_sms):
-            ts = table.tasks_of(sm)
-            for layer in range(TINY.n_layers):
-                for ty in (tt.T_QKV, tt.T_GATEUP):
-                    assert ((ts[:, tt.F_TYPE] == ty) & (ts[:, tt.F_LAYER] == layer)).sum() == 1
-            assert (ts[:, tt.F_TYPE] == tt.T_LMHEAD).sum() == 1
+def test_every_operator_covers_its_rows_exactly_once():
+    """Per layer, the row ranges of each GEMV operator over all SMs tile [0, n_rows) exactly;
+    attention units cover every (q head, chunk slot) once and every q head has one merge task."""
+    for cfg, n_sms in ((TINY, 148), (TINY, 5), (QWEN25_1P5B, 148)):
+        sched = SCHED_TINY if cfg is TINY else tt.KernelSchedule(consumer_warps=7, n_stage=3, rows_per_tile=56, ktile_chunks=2)
+        table = tt.build_task_table(cfg, sched, n_sms=n_sms)
+        rows = {tt.T_QKV: cfg.qkv_rows, tt.T_OPROJ: cfg.hidden, tt.T_GATEUP: 2 * cfg.intermediate, tt.T_DOWN: cfg.hidden}
+        t = table.tasks
+        for layer in (0, cfg.n_layers - 1):
+            for ty, n in rows.items():
+                m = (t[:, tt.F_TYPE] == ty) & (t[:, tt.F_LAYER] == layer)
+                spans = sorted((int(a), int(b)) for a, b in t[m][:, [tt.F_A, tt.F_B]])
+                assert spans[0][0] == 0 and sum(b for _, b in spans) == n
+                for (a0, b0), (a1, _) in zip(spans, spans[1:]):
+                    assert a0 + b0 == a1
+            m = (t[:, tt.F_TYPE] == tt.T_ATTN) & (t[:, tt.F_LAYER] == layer)
+            units = {(int(a), int(b)) for a, b in t[m][:, [tt.F_A, tt.F_B]]}
+            assert units == {(h, c) for h in range(cfg.n_q_heads) for c in range(table.attn_chunks)}
+            m = (t[:, tt.F_TYPE] == tt.T_MERGE) & (t[:, tt.F_LAYER] == layer)
+            assert sorted(int(a) for a in t[m][:, tt.F_A]) == list(range(cfg.n_q_heads))
+        m = t[:, tt.F_TYPE] == tt.T_LMHEAD
+        assert int(t[m][:, tt.F_B].sum()) == cfg.vocab
+
+
+def test_warp_grid_geometry_is_executable():
+    """Every GEMV task's warp grid satisfies the kernel's constraints (adamk_create re-checks them)."""
+    for cfg, sched in ((QWEN25_1P5B, tt.KernelSchedule(consumer_warps=7, n_stage=3, rows_per_tile=56, ktile_chunks=2)),
+                       (QWEN25_1P5B, tt.KernelSchedule(consumer_warps=8, n_stage=5, rows_per_tile=64, ktile_chunks=1)),
+                       (QWEN3_8B, tt.KernelSchedule(consumer_warps=4, n_stage=3, rows_per_tile=32, ktile_chunks=3)),
+                       (TINY, SCHED_TINY)):
+        table = tt.build_task_table(cfg, sched, n_sms=148)
+        for task in table.tasks:
+            if int(task[tt.F_TYPE]) not in tt.GEMV_TYPES:
+                continue
+            wr, wk, rw = tt.unpack_geom(int(task[tt.F_GEOM]))
+            assert wr * wk == sched.consumer_warps and 1 <= rw <= tt.MAX_RW
+            assert int(task[tt.F_RT]) == wr * rw
+            assert wk == 1 or int(task[tt.F_RT]) <= 32
+            assert wk & (wk - 1) == 0                      # K groups are a power of two (shift / mask in the kernel)
+            assert int(task[tt.F_RT]) * int(task[tt.F_KTC]) * 512 <= sched.stage_bytes
+            assert int(task[tt.F_NTILES]) == -(-int(task[tt.F_B]) // int(task[tt.F_RT]))
+            assert int(task[tt.F_NKTILES]) == -(-int(task[tt.F_KCHUNKS]) // int(task[tt.F_KTC]))
+            if int(task[tt.F_TYPE]) == tt.T_GATEUP:
+                assert rw % 2 == 0 and int(task[tt.F_A]) % 2 == 0 and int(task[tt.F_B]) % 2 == 0
+            # rows a warp group may touch past the tile end stay inside the ring slot
+            assert wr * rw * int(task[tt.F_KTC]) * 512 <= sched.stage_bytes
 
 
 def test_dataflow_full_model_and_small_gpu():
-    sched = tt.KernelSchedule(consumer_warps=8, n_stage=5, rows_per_tile=16, ktile_chunks=3)
+    sched = tt.KernelSchedule(consumer_warps=7, n_stage=3, rows_per_tile=56, ktile_chunks=2)
     table = tt.build_task_table(QWEN25_1P5B, sched, n_sms=148)
     _simulate_dataflow(table, 513)
     s = table.summary()
     assert s["packed_weight_bytes"] * 1.0 <= QWEN25_1P5B.weight_bytes_per_token()
     assert s["stream_bytes_max"] - s["stream_bytes_min"] <= 64 * 1024
+    assert int(np.diff(table.sm_begin).max()) * 32 <= tt.task_cache_bytes(QWEN25_1P5B)
     small = tt.build_task_table(TINY, SCHED_TINY, n_sms=5)
     _simulate_dataflow(small, 33)
+    assert int(np.diff(small.sm_begin).max()) * 32 <= tt.task_cache_bytes(TINY, n_sms=5)
 
 
 def test_schedule_validation():
@@ -164,7 +217,9 @@ def test_schedule_validation():
     with pytest.raises(tt.ScheduleError):
         tt.KernelSchedule(consumer_warps=6)
     with pytest.raises(tt.ScheduleError):
-        tt.build_task_table(QWEN25_1P5B, tt.KernelSchedule(n_stage=16, ktile_chunks=4))   # 16 x 32 KB > 227 KB
+        tt.build_task_table(QWEN25_1P5B, tt.KernelSchedule(n_stage=16, ktile_chunks=1))   # 16 x 32 KB > 227 KB
+    with pytest.raises(tt.ScheduleError):
+        tt.KernelSchedule(n_stage=3, inflight=4)
     s = tt.KernelSchedule.from_plan({"tile": [16, 32, 1024, 2], "n_stage": 5, "consumer_warps": 16})
     assert (s.rows_per_tile, s.ktile_chunks, s.stage_bytes) == (32, 2, 32768)
     with pytest.raises(tt.ScheduleError):
@@ -176,7 +231,7 @@ def test_blob_layout_matches_header():
     raw = np.frombuffer(table.blob, dtype="<i4")
     assert raw[0] == tt.MAGIC and raw[1] == tt.VERSION and raw[2] == 148
     assert raw.size == tt.HEADER_INTS + 149 + raw[6] * tt.TASK_INTS
-    assert tt.max_stages_that_fit(QWEN3_8B, tt.KernelSchedule(ktile_chunks=4)) >= 4
+    assert tt.max_stages_that_fit(QWEN3_8B, tt.KernelSchedule(ktile_chunks=1)) >= 4
 
 
 def test_cabi_exports_every_declared_symbol():

@@ -25,19 +25,17 @@ t0 = time.time()
 w = random_weights(cfg, 0, device="cuda")
 torch.cuda.synchronize()
 print(f"weights on device in {time.time() - t0:.1f}s", flush=True)
-B = dict(consumer_warps=8, rows_per_tile=64, ktile_chunks=1)
+B = dict(consumer_warps=8, rows_per_tile=64, ktile_chunks=1, n_stage=5, attn_min_chunk=64)
+C4 = dict(B, consumer_warps=4, rows_per_tile=32)
+C7 = dict(B, consumer_warps=7, attn_min_chunk=128)
 scheds = [
-    ("c8 s5 32K", dict(B, n_stage=5)),
-    ("c8 s5 32K if2", dict(B, n_stage=5, inflight=2)),
-    ("c8 s5 32K if3", dict(B, n_stage=5, inflight=3)),
-    ("c8 s5 32K sl200", dict(B, n_stage=5, poll_sleep_ns=200)),
-    ("c8 s5 32K mc64", dict(B, n_stage=5, attn_min_chunk=64)),
-    ("c8 s5 32K mc256", dict(B, n_stage=5, attn_min_chunk=256)),
-    ("c8 s11 16K", dict(consumer_warps=8, rows_per_tile=32, ktile_chunks=1, n_stage=11)),
-    ("c8 s11 16K if4", dict(consumer_warps=8, rows_per_tile=32, ktile_chunks=1, n_stage=11, inflight=4)),
-    ("c8 s11 16K if6", dict(consumer_warps=8, rows_per_tile=32, ktile_chunks=1, n_stage=11, inflight=6)),
-    ("c16 s5 32K", dict(consumer_warps=16, rows_per_tile=64, ktile_chunks=1, n_stage=5)),
-    ("c4 s5 32K", dict(consumer_warps=4, rows_per_tile=32, ktile_chunks=2, n_stage=5)),
+    ("c4 r32k3 s3 pf512", dict(C4, ktile_chunks=3, n_stage=3, l2_prefetch_kb=512, attn_min_chunk=128)),
+    ("c7 r56k1 s6 pf0", dict(C7, rows_per_tile=56, ktile_chunks=1, n_stage=6)),
+    ("c7 r56k2 s3 pf0", dict(C7, rows_per_tile=56, ktile_chunks=2, n_stage=3)),
+    ("c7 r56k2 s3 pf512", dict(C7, rows_per_tile=56, ktile_chunks=2, n_stage=3, l2_prefetch_kb=512)),
+    ("c7 r28k3 s4 pf512", dict(C7, rows_per_tile=28, ktile_chunks=3, n_stage=4, l2_prefetch_kb=512)),
+    ("c7 r28k2 s6 pf512", dict(C7, rows_per_tile=28, ktile_chunks=2, n_stage=6, l2_prefetch_kb=512)),
+    ("c8 r64k1 s5 pf512", dict(B, l2_prefetch_kb=512, attn_min_chunk=128)),
 ]
 
 
