@@ -110,8 +110,9 @@ int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, a
  * memory, one per rank, own rank included) for the in-kernel NVLink reduction. */
 int adamk_bind_peers(adamk_handle h, void* const* peer_workspaces, int n_peers);
 
-/* Workspace: activations, attention partials, per-SM argmax partials and the
- * dependency counters.  Must be zero-initialised once with workspace_init. */
+/* Workspace: the tagged activation vectors ({fp32 value, tag} words), split-KV
+ * partial records, per-SM argmax partials and the step epoch.  Must be
+ * initialised once with workspace_init (zeroes it and opens epoch 1). */
 size_t adamk_workspace_bytes(adamk_handle h);
 int adamk_workspace_init(adamk_handle h, void* workspace, adamk_stream stream);
 
@@ -131,7 +132,7 @@ int adamk_decode_step(adamk_handle h, int32_t* token_ids, int32_t* positions, in
                       adamk_stream stream);
 
 /* Poll the device-written status block (host-mapped); 0 = no error recorded.
- * Fills `info` (8 ints: code, sm, task, counter, seen, expected, ...) if not NULL. */
+ * Fills `info` (8 ints: code, sm, task, tag seen, tag expected, detail, thread, -) if not NULL. */
 int adamk_device_status(adamk_handle h, int32_t* info);
 
 /* Optional per-task timeline (the device analogue of the reference's
@@ -145,7 +146,9 @@ int adamk_set_trace(adamk_handle h, void* trace_buf);
 /* Standalone weight-streaming probe used by the measurement harness: runs only
  * the Loader/Consumer ring over the packed stream (no dependencies), to
  * separate HBM streaming efficiency from dependency stalls.  mode 1: Loader +
- * Consumer math; mode 2: Loader only (consumers release slots untouched). */
+ * Consumer math; mode 2: Loader only (consumers release slots untouched);
+ * mode 3: like 1 with the Loader re-reading an L2-resident window; mode 4:
+ * Consumer math only (no Loader, no barriers).  `sink` is n_sms * 64 floats. */
 int adamk_stream_probe(adamk_handle h, float* sink, int mode, adamk_stream stream);
 
 #ifdef __cplusplus
