@@ -182,8 +182,27 @@ __device__ __forceinline__ void tma_bulk_g2s_hint(uint32_t dst, const void* src,
       "l"(src), "r"(bytes), "r"(bar), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ void l2_prefetch_bulk(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+__device__ __forceinline__ void l2_prefetch_bulk(const void* src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes), "l"(pol) : "memory");
+}
+// The small per-layer fp32 vectors (norm gains, biases) sit on the critical path of every hop; the
+// weight stream flushes them out of L2 between two uses unless they are loaded evict-last.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float2 ldg_keep_f2(const float2* p) {
+  float2 v;
+  const uint64_t pol = l2_evict_last_policy();
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ldg_keep_f1(const float* p) {
+  float v;
+  const uint64_t pol = l2_evict_last_policy();
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
 }
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
@@ -343,7 +362,7 @@ __device__ __noinline__ float ll_gather(const KParams& p, int ctid, int nct, con
 #pragma unroll
     for (int u = 0; u < kGatherBatch; ++u) {  // static operand first: a DRAM miss under the weight stream, overlapped with the poll
       const int i = i0 + u * nct;
-      g[u] = (NORM && i < n2) ? __ldg(reinterpret_cast<const float2*>(gain) + i) : make_float2(1.f, 1.f);
+      g[u] = (NORM && i < n2) ? ldg_keep_f2(reinterpret_cast<const float2*>(gain) + i) : make_float2(1.f, 1.f);
     }
     u64 a[kGatherBatch], b[kGatherBatch];
     long long t0 = 0;
@@ -441,7 +460,7 @@ __device__ __forceinline__ void gemv_prologue(const KParams& p, ConsumerCtx& c, 
         const uint32_t raw = __ldg(reinterpret_cast<const uint32_t*>(p.embed + (size_t)tok * p.H) + i);
         v.x = bf_lo(raw); v.y = bf_hi(raw);
         ss = fmaf(v.x, v.x, fmaf(v.y, v.y, ss));
-        const float2 g = __ldg(reinterpret_cast<const float2*>(gain) + i);
+        const float2 g = ldg_keep_f2(reinterpret_cast<const float2*>(gain) + i);
         v.x *= g.x; v.y *= g.y;
       }
       reinterpret_cast<float2*>(xs)[i] = v;
@@ -464,7 +483,7 @@ __device__ __forceinline__ void gemv_prologue(const KParams& p, ConsumerCtx& c, 
 // vector this step has already completed; the tag is still checked (cheap) rather than assumed.
 __device__ __forceinline__ float load_eop(const KParams& p, const ConsumerCtx& c, const Task& t, int ti, int vrow, int tok) {
   switch (t.type) {
-    case T_QKV: return p.has_bias ? __ldg(p.fparams + (size_t)t.layer * p.fp_layer_stride + p.fp_bias + vrow) : 0.f;
+    case T_QKV: return p.has_bias ? ldg_keep_f1(p.fparams + (size_t)t.layer * p.fp_layer_stride + p.fp_bias + vrow) : 0.f;
     case T_OPROJ:
       if (t.layer == 0) return __bfloat162float(p.embed[(size_t)tok * p.H + vrow]);
       return ll_wait(p, p.ll_hx + (size_t)(t.layer & 1) * p.H + vrow, tag_of(c, t.layer), ti);
@@ -569,6 +588,44 @@ __device__ __forceinline__ void gemv_ktiles(const KParams& p, uint32_t& slot, ui
   }
 }
 
+// The wide operators (gate/up, LM head) in the profiled schedules: WK == 1, RW rows per warp and the
+// same KTC chunks in every stage.  Every stride is a compile-time immediate and the chunk loop is
+// unrolled, so a stage costs ~110 instructions per chunk instead of ~170 (the loop is issue-bound with
+// two warps per scheduler).
+template <int RW, int KTC>
+__device__ __forceinline__ void gemv_ktiles_wide(const KParams& p, uint32_t& slot, uint32_t& ph, int lane, int n_ktiles,
+                                                 int task_idx, uint32_t wofs, uint32_t ring_addr, uint32_t xs_addr,
+                                                 uint32_t full0, uint32_t empty0, float2 (&acc)[kRW], bool wait) {
+  const uint32_t n_stage = (uint32_t)p.n_stage, stage_bytes = (uint32_t)p.stage_bytes;
+  uint32_t xa = xs_addr;
+  uint32_t sbase = ring_addr + slot * stage_bytes + wofs;
+#pragma unroll 1
+  for (int kt = 0; kt < n_ktiles; ++kt, xa += KTC * (kChunk * 4)) {
+    if (wait) mbar_wait(p, full0 + slot * 8, ph, DE_WATCHDOG_FULL, task_idx);
+#pragma unroll
+    for (int j = 0; j < KTC; ++j) {
+      const float4 x0 = lds128f(xa + j * (kChunk * 4));
+      const float4 x1 = lds128f(xa + j * (kChunk * 4) + 512);
+      uint4 w[RW];
+#pragma unroll
+      for (int i = 0; i < RW; ++i) w[i] = lds128u(sbase + (i * KTC + j) * 512);
+#pragma unroll
+      for (int i = 0; i < RW; ++i) {
+        acc[i] = __ffma2_rn(make_float2(bf_lo(w[i].x), bf_hi(w[i].x)), make_float2(x0.x, x0.y), acc[i]);
+        acc[i] = __ffma2_rn(make_float2(bf_lo(w[i].y), bf_hi(w[i].y)), make_float2(x0.z, x0.w), acc[i]);
+        acc[i] = __ffma2_rn(make_float2(bf_lo(w[i].z), bf_hi(w[i].z)), make_float2(x1.x, x1.y), acc[i]);
+        acc[i] = __ffma2_rn(make_float2(bf_lo(w[i].w), bf_hi(w[i].w)), make_float2(x1.z, x1.w), acc[i]);
+      }
+    }
+    if (wait) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + slot * 8);
+    }
+    sbase += stage_bytes;
+    if (++slot == n_stage) { slot = 0; ph ^= 1u; sbase = ring_addr + wofs; }
+  }
+}
+
 template <int RW>
 __device__ __forceinline__ void gemv_tiles_t(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx,
                                              const float* xs, SmemHdr* hdr, uint8_t* ring, int tok, float eop0, int probe) {
@@ -603,7 +660,15 @@ __device__ __forceinline__ void gemv_tiles_t(const KParams& p, ConsumerCtx& c, c
     const bool active = my_n > 0 && probe != 2;
     {
       uint32_t slot = c.slot, ph = c.ph;
-      gemv_ktiles<RW>(p, slot, ph, c.lane, t.ktc, t.n_ktiles, task_idx, sg, ring_addr, xs_addr, full0, empty0, WK, acc, active, probe != 4);
+      const bool wide = RW >= 4 && WK == 1 && rw == RW && chunks_last == t.ktc && probe != 2;
+      if (wide && t.ktc == 2)
+        gemv_ktiles_wide<RW, 2>(p, slot, ph, c.lane, t.n_ktiles, task_idx, sg.wofs_full, ring_addr, xs_addr, full0, empty0, acc, probe != 4);
+      else if (wide && t.ktc == 1)
+        gemv_ktiles_wide<RW, 1>(p, slot, ph, c.lane, t.n_ktiles, task_idx, sg.wofs_full, ring_addr, xs_addr, full0, empty0, acc, probe != 4);
+      else if (wide && t.ktc == 3)
+        gemv_ktiles_wide<RW, 3>(p, slot, ph, c.lane, t.n_ktiles, task_idx, sg.wofs_full, ring_addr, xs_addr, full0, empty0, acc, probe != 4);
+      else
+        gemv_ktiles<RW>(p, slot, ph, c.lane, t.ktc, t.n_ktiles, task_idx, sg, ring_addr, xs_addr, full0, empty0, WK, acc, active, probe != 4);
       c.slot = slot; c.ph = ph;
     }
     float v[kRW];
@@ -791,7 +856,7 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
     }
     float gn[PER];
 #pragma unroll
-    for (int j = 0; j < PER; ++j) gn[j] = (p.qk_norm && (is_q || is_k)) ? __ldg(lay_fp + (is_q ? p.fp_qn : p.fp_kn) + c.lane + 32 * j) : 1.f;
+    for (int j = 0; j < PER; ++j) gn[j] = (p.qk_norm && (is_q || is_k)) ? ldg_keep_f1(lay_fp + (is_q ? p.fp_qn : p.fp_kn) + c.lane + 32 * j) : 1.f;
     const u64* src = p.ll_qkv + (is_q ? (size_t)h * D : (size_t)p.q_dim + (is_k ? 0 : p.kv_dim) + (size_t)kvh * D);
     float v[PER];
     ll_wait_strided<PER>(p, src + c.lane, 32, tag, v, task_idx);
@@ -1123,7 +1188,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
           while (pf < wend && pf < wcur + p.pf_window_bytes) {
             if (mbar_test_wait(bar, parity)) return;
             const uint32_t nb = (uint32_t)min((size_t)kPfGranule, (size_t)(wend - pf));
-            l2_prefetch_bulk(pf, nb);
+            l2_prefetch_bulk(pf, nb, pol);
             pf += nb;
             ++n_pf;
             if (clock64() - t0 > kWatchdogCycles) dev_fail(p, code, ti, (int)bar, (int)parity, 0);

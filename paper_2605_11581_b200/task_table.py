@@ -175,7 +175,20 @@ def op_geometry(sched: KernelSchedule, max_rows: int, kchunks: int, pairs: bool)
     c = sched.consumer_warps
 
     def plan_tile():
-        rw = sched.rows_per_warp
+        # rows per warp: at most the plan tile's, chosen so the last tile of the SM's slice is not mostly
+        # padding (122 gate/up rows on 7 warps: three 56-row tiles are 73 % full, three 42-row tiles 97 %)
+        best_rw, best_pad = sched.rows_per_warp, None
+        for rw in range(sched.rows_per_warp, 0, -1):
+            if pairs and rw & 1:
+                continue
+            rt = c * rw
+            n_t = _ceil_div(max_rows, rt)
+            # row slots computed (padding included) + ~8 rows' worth of reduce / epilogue per tile, scaled by
+            # the activation-load overhead of short row groups (2 LDS.128 of x per rw of weights)
+            cost = (n_t * rt + 8 * n_t) * (1.0 + 1.0 / rw)
+            if best_pad is None or cost < best_pad:
+                best_rw, best_pad = rw, cost
+        rw = best_rw
         rt = c * rw
         ktc = max(1, min(kchunks, sched.stage_bytes // (rt * KCHUNK * 2)))
         n_kt = _ceil_div(kchunks, ktc)

@@ -30,11 +30,9 @@ C4 = dict(B, consumer_warps=4, rows_per_tile=32)
 C7 = dict(B, consumer_warps=7, attn_min_chunk=128)
 scheds = [
     ("c7 r56k2 s3 pf512", dict(C7, rows_per_tile=56, ktile_chunks=2, n_stage=3, l2_prefetch_kb=512)),
-    ("c7 r56k2 s3 pf512 if2", dict(C7, rows_per_tile=56, ktile_chunks=2, n_stage=3, l2_prefetch_kb=512, inflight=2)),
-    ("c7 r56k2 s3 pf512 if1", dict(C7, rows_per_tile=56, ktile_chunks=2, n_stage=3, l2_prefetch_kb=512, inflight=1)),
-    ("c7 r56k1 s6 pf512 if2", dict(C7, rows_per_tile=56, ktile_chunks=1, n_stage=6, l2_prefetch_kb=512, inflight=2)),
-    ("c7 r56k1 s6 pf512 if3", dict(C7, rows_per_tile=56, ktile_chunks=1, n_stage=6, l2_prefetch_kb=512, inflight=3)),
-    ("c7 r56k2 s3 pf0 if1", dict(C7, rows_per_tile=56, ktile_chunks=2, n_stage=3, inflight=1)),
+    ("c7 r56k3 s2 pf512", dict(C7, rows_per_tile=56, ktile_chunks=3, n_stage=2, l2_prefetch_kb=512)),
+    ("c7 r56k1 s6 pf512", dict(C7, rows_per_tile=56, ktile_chunks=1, n_stage=6, l2_prefetch_kb=512)),
+    ("c4 r32k3 s3 pf512", dict(C4, ktile_chunks=3, n_stage=3, l2_prefetch_kb=512, attn_min_chunk=128)),
 ]
 
 
