@@ -21,7 +21,12 @@ rank 0:
 
 `--impl reference` times that CPU oracle as the reference arm (same metric and
 config).  N > 1 runs N independent replicas (config #2 has 2 KV heads and does
-not shard past TP=2: "replicas only"), one rank per GPU.
+not shard past TP=2: "replicas only"), one rank per GPU.  With
+`--tp` (BASELINE.json configs[3]: `--model qwen3-8b --tp --gpus N`) the N ranks
+are tensor-parallel shards of ONE sequence instead: every rank launches one
+kernel per token and the kernels exchange their partial rows through
+peer-mapped workspaces (no NCCL on the data path); `value` is then the
+sequence's tokens/s and `scaling` is "strong".
 """
 
 from __future__ import annotations
@@ -119,9 +124,11 @@ def base_line(args, cfg, n_gpus: int) -> dict:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights, random prompt ids; no network for checkpoints)",
             "config": {"workload": f"{cfg.name} batch-1 greedy decode after a {PROMPT_LEN}-token prompt "
-                                   f"(BASELINE.json configs[1])", "model": cfg.name, "batch": 1,
+                                   f"(BASELINE.json configs[{1 if cfg.name == 'qwen2.5-1.5b' else 3}])",
+                       "model": cfg.name, "batch": 1,
                        "prompt_len": PROMPT_LEN, "parallelism": "replicas" if n_gpus > 1 else "single",
-                       "l2_policy": "inputs larger than L2: every step streams the 3.09 GB weight set"}}
+                       "l2_policy": f"inputs larger than L2: every step streams the "
+                                    f"{cfg.weight_bytes_per_token() / 1e9:.2f} GB weight set"}}
 
 
 def run_reference(args) -> None:
@@ -153,14 +160,20 @@ def run_ours(args) -> None:
     rank, world, dist = group.rank, group.world, group.dist
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    cfg = get_config(args.model)
-    w = random_weights(cfg, seed=0, device=dev)
+    full_cfg = get_config(args.model)
+    tp = world if (args.tp and world > 1) else 1
+    cfg = full_cfg.shard(tp)                      # this rank's dimensions (the whole model when tp == 1)
+    w = random_weights(full_cfg, seed=0, device=dev).shard(rank, tp)   # same seed on every rank -> same model
     sched = default_schedule(cfg)
     max_ctx = PROMPT_LEN + args.steps + args.warmup + 16
-    plug = MegaKernelPlugin(cfg, sched, max_ctx=max_ctx, device=local)
+    plug = MegaKernelPlugin(cfg, sched, max_ctx=max_ctx, device=local, tp_rank=rank if tp > 1 else 0, tp_size=tp)
     plug.bind_weights(w)
+    if tp > 1:
+        from paper_2605_11581_b200.dist_utils import share_workspaces
+        plug.bind_peers(share_workspaces(group, plug.workspace))
+    cfg_bytes = full_cfg
     g = torch.Generator().manual_seed(1)
-    prompt = torch.randint(0, cfg.vocab, (PROMPT_LEN,), generator=g).tolist()
+    prompt = torch.randint(0, full_cfg.vocab, (PROMPT_LEN,), generator=g).tolist()
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -230,18 +243,22 @@ def run_ours(args) -> None:
 
     peak, peak_kind = measured_peak()
     ctx_mid = PROMPT_LEN + args.warmup + args.steps // 2
-    bytes_per_launch = cfg.algorithmic_bytes(ctx_mid)
+    bytes_per_launch = cfg_bytes.algorithmic_bytes(ctx_mid) // tp   # per rank: one kernel streams 1/tp of the model
     achieved = bytes_per_launch / (ms * 1e-3) / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
-    line = base_line(args, cfg, world)
+    line = base_line(args, full_cfg, world)
+    jobs = 1 if tp > 1 else world               # tensor parallel: one sequence; replicas: one per GPU
+    if tp > 1:
+        line["scaling"] = "strong"
+        line["config"]["parallelism"] = f"tp{tp} (in-kernel NVLink peer stores)"
     line.update({
-        "value": world * 1e3 / ms, "ms_per_step": ms,
+        "value": jobs * 1e3 / ms, "ms_per_step": ms,
         "config": dict(line["config"], schedule={"consumer_warps": sched.consumer_warps, "n_stage": sched.n_stage,
                                                  "stage_bytes": sched.stage_bytes}, n_sms=plug.n_sms),
-        "e2e": {"value": world * 1e3 / ms_e2e, "unit": UNIT, "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 4,
+        "e2e": {"value": jobs * 1e3 / ms_e2e, "unit": UNIT, "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 4,
                 "ms_per_step": ms_e2e},
         "gpu_launches": launches,
         "clocks": clocks,
@@ -251,8 +268,8 @@ def run_ours(args) -> None:
                      "launch_ms": ms},
     })
     if not args.no_cpu_baseline:
-        w_cpu = w.to("cpu")
-        res = cpu_decode_sample(cfg, w_cpu, prompt, n_steps=args.cpu_steps)
+        w_cpu = random_weights(full_cfg, seed=0, device=dev).to("cpu") if tp > 1 else w.to("cpu")
+        res = cpu_decode_sample(full_cfg, w_cpu, prompt, n_steps=args.cpu_steps)
         line["cpu_baseline"] = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line))
     group.close()
@@ -267,6 +284,7 @@ def main() -> None:
     ap.add_argument("--model", default="qwen2.5-1.5b")
     ap.add_argument("--cpu-steps", type=int, default=48, help="decode steps of the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tp", action="store_true", help="N > 1: tensor-parallel shards of one sequence instead of N replicas")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -60,6 +60,7 @@ constexpr int kAttnChunksMax = 128;  // split-KV units per (sequence, kv head)
 constexpr int kGMax = 8;             // max q heads per kv head
 constexpr int kRW = 8;               // max rows per warp per tile
 constexpr int kGatherBatch = 8;      // 16-byte tagged-word loads a thread keeps in flight while gathering a vector
+constexpr int kMaxTP = 8;
 constexpr int kTagStride = 256;      // tag = epoch * kTagStride + layer + 1
 
 enum TaskType { T_END = 0, T_QKV = 1, T_ATTN = 2, T_OPROJ = 3, T_GATEUP = 4, T_DOWN = 5, T_LMHEAD = 6, T_MERGE = 7 };
@@ -97,8 +98,9 @@ struct KParams {
   __nv_bfloat16* kcache;
   __nv_bfloat16* vcache;
   // tagged activation vectors ({fp32, tag} words)
-  u64* ll_hx;    // [2][H]   layer input, ping-pong by layer parity
-  u64* ll_hm;    // [H]      hidden state after attention
+  u64* ll_hx;    // [2][tp][H]  layer input, ping-pong by layer parity; one slot of partial rows per TP rank
+  u64* ll_hm;    // [tp][H]     hidden state after attention, likewise
+  u64* ll_lmx;   // [tp][2]     (value, index) of every rank's LM-head argmax
   u64* ll_qkv;   // [qkv_rows]
   u64* ll_attn;  // [q_dim]  merged attention output
   u64* ll_act;   // [I]
@@ -112,6 +114,12 @@ struct KParams {
   int* next_tokens;
   int* status;  // host-mapped, 8 ints
   int auto_advance;
+  // tensor parallelism: this rank publishes its partial O-proj / down-proj rows (and its LM-head argmax) into
+  // slot tp_rank of EVERY rank's workspace with the same 64-bit tagged stores (NVLink peer memory)
+  int tp_rank, tp_size, vocab_off;
+  u64* peer_hx[kMaxTP];
+  u64* peer_hm[kMaxTP];
+  u64* peer_lmx[kMaxTP];
   int probe;    // 1 = stream probe: consumers skip dependencies and epilogues; 2 = also skip the math;
                 // 3 = like 1 but the Loader re-reads an L2-resident window; 4 = consumers only (no Loader, no waits)
   float* probe_sink;
@@ -257,6 +265,19 @@ __device__ __forceinline__ u64 ll_load(const u64* p) {
 __device__ __forceinline__ void ll_load2(const u64* p, u64& a, u64& b) {  // 16-byte aligned pair of words
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
+// system-scope variants for words another GPU writes / reads (tensor-parallel slots)
+__device__ __forceinline__ void ll_store_sys(u64* p, float v, unsigned tag) {
+  const u64 w = ((u64)tag << 32) | (u64)__float_as_uint(v);
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ u64 ll_load_sys(const u64* p) {
+  u64 w;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+__device__ __forceinline__ void ll_load2_sys(const u64* p, u64& a, u64& b) {
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
 __device__ __forceinline__ unsigned ll_tag(u64 w) { return (unsigned)(w >> 32); }
 __device__ __forceinline__ float ll_val(u64 w) { return __uint_as_float((unsigned)w); }
 
@@ -400,6 +421,118 @@ __device__ __noinline__ float ll_gather(const KParams& p, int ctid, int nct, con
   return ss;
 }
 
+// Tensor-parallel gather: the vector is the sum of one slot of partial rows per rank (rank 0's partial carries
+// the residual), summed in rank order so every rank computes bit-identical activations.  8 / T words per
+// thread are in flight at a time, each with its T slot words; system-scope loads (peers write the slots).
+template <int T>
+__device__ __noinline__ float ll_gather_tp(const KParams& p, int ctid, int nct, const u64* src, int n, int kpad,
+                                           unsigned tag, float* xs, const float* gain, int task) {
+  constexpr int WB = 8 / T;  // words per batch
+  const bool NORM = gain != nullptr;
+  const int n2 = n >> 1, kp2 = kpad >> 1;
+  const size_t slot_stride = (size_t)n;  // words per slot
+  float ss = 0.f;
+  for (int i0 = ctid; i0 < kp2; i0 += WB * nct) {
+    float2 g[WB];
+#pragma unroll
+    for (int w = 0; w < WB; ++w) {
+      const int i = i0 + w * nct;
+      g[w] = (NORM && i < n2) ? ldg_keep_f2(reinterpret_cast<const float2*>(gain) + i) : make_float2(1.f, 1.f);
+    }
+    u64 a[8], b[8];
+    long long t0 = 0;
+    for (;;) {
+      bool ok = true;
+#pragma unroll
+      for (int u = 0; u < WB * T; ++u) {
+        const int i = i0 + (u / T) * nct;
+        if (i < n2) ll_load2_sys(src + (size_t)(u % T) * slot_stride + 2 * i, a[u], b[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < WB * T; ++u) {
+        const int i = i0 + (u / T) * nct;
+        if (i < n2) ok = ok && ll_tag(a[u]) == tag && ll_tag(b[u]) == tag;
+      }
+      if (ok) break;
+      if (t0 == 0) t0 = clock64();
+      else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task, (int)ll_tag(a[0]), (int)tag, i0);
+    }
+#pragma unroll
+    for (int w = 0; w < WB; ++w) {
+      const int i = i0 + w * nct;
+      if (i < kp2) {
+        float2 v = make_float2(0.f, 0.f);
+        if (i < n2) {
+#pragma unroll
+          for (int sl = 0; sl < T; ++sl) { v.x += ll_val(a[w * T + sl]); v.y += ll_val(b[w * T + sl]); }
+          ss = fmaf(v.x, v.x, fmaf(v.y, v.y, ss));
+          v.x *= g[w].x; v.y *= g[w].y;
+        }
+        reinterpret_cast<float2*>(xs)[i] = v;
+      }
+    }
+  }
+  return ss;
+}
+__device__ __forceinline__ float ll_gather_slots(const KParams& p, int ctid, int nct, const u64* src, int n, int kpad,
+                                                 unsigned tag, float* xs, const float* gain, int task) {
+  switch (p.tp_size) {
+    case 1: return ll_gather(p, ctid, nct, src, n, kpad, tag, xs, gain, task);
+    case 2: return ll_gather_tp<2>(p, ctid, nct, src, n, kpad, tag, xs, gain, task);
+    case 4: return ll_gather_tp<4>(p, ctid, nct, src, n, kpad, tag, xs, gain, task);
+    default: return ll_gather_tp<8>(p, ctid, nct, src, n, kpad, tag, xs, gain, task);
+  }
+}
+// one element of a slotted vector (residual operand of an epilogue): sum over the rank slots in rank order.
+// The tensor-parallel parts of the GEMV task body are out of line so the single-GPU body keeps its registers.
+__device__ __noinline__ float ll_wait_slots_tp(const KParams& p, const u64* src, int n, int idx, unsigned tag, int task) {
+  float v = 0.f;
+  for (int sl = 0; sl < p.tp_size; ++sl) {
+    const u64* a = src + (size_t)sl * n + idx;
+    u64 w = ll_load_sys(a);
+    const long long t0 = clock64();
+    while (ll_tag(w) != tag) {
+      w = ll_load_sys(a);
+      if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task, (int)ll_tag(w), (int)tag, idx);
+    }
+    v += ll_val(w);
+  }
+  return v;
+}
+// publish one partial row to slot tp_rank of every rank (peer-mapped memory over NVLink): which = 0 -> hm, 1 -> hx[parity]
+__device__ __noinline__ void tp_publish(const KParams& p, int which, int parity, int row, float v, unsigned tag) {
+  for (int r = 0; r < p.tp_size; ++r) {
+    u64* dst = which == 0 ? p.peer_hm[r] + (size_t)p.tp_rank * p.H + row
+                          : p.peer_hx[r] + ((size_t)parity * p.tp_size + p.tp_rank) * p.H + row;
+    ll_store_sys(dst, v, tag);
+  }
+}
+// every rank publishes (value, index) of its LM-head argmax to every rank and takes the best of all, ties to the
+// lowest index; called by one warp of the rank's last CTA
+__device__ __noinline__ void tp_argmax_exchange(const KParams& p, int lane, unsigned xtag, float& best, int& idx) {
+  if (lane < p.tp_size) {
+    ll_store_sys(p.peer_lmx[lane] + 2 * p.tp_rank, best, xtag);
+    ll_store_sys(p.peer_lmx[lane] + 2 * p.tp_rank + 1, __int_as_float(idx), xtag);
+  }
+  best = -INFINITY; idx = 0x7fffffff;
+  if (lane < p.tp_size) {
+    const u64* rec = p.ll_lmx + 2 * lane;
+    u64 wv = ll_load_sys(rec), wi = ll_load_sys(rec + 1);
+    const long long t0 = clock64();
+    while (ll_tag(wv) != xtag || ll_tag(wi) != xtag) {
+      wv = ll_load_sys(rec); wi = ll_load_sys(rec + 1);
+      if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, -2, (int)ll_tag(wv), (int)xtag, lane);
+    }
+    best = ll_val(wv); idx = __float_as_int(ll_val(wi));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > best || (ov == best && oi < idx)) { best = ov; idx = oi; }
+  }
+}
+
 // N words base[0], base[stride], ... gathered by one thread: all loads in flight together, re-polled as a batch.
 template <int N>
 __device__ __forceinline__ void ll_wait_strided(const KParams& p, const u64* base, int stride, unsigned tag, float (&out)[N],
@@ -432,6 +565,7 @@ __device__ __forceinline__ const float* gemv_gain(const KParams& p, const Task& 
 }
 
 // Stage the activation vector of a GEMV in shared memory (fp32, zero padded to kpad).
+template <bool TP>
 __device__ __forceinline__ void gemv_prologue(const KParams& p, ConsumerCtx& c, const Task& t, int ti, float* xs,
                                               SmemHdr* hdr, int tok) {
   const int kpad = t.kchunks * kChunk;
@@ -467,8 +601,13 @@ __device__ __forceinline__ void gemv_prologue(const KParams& p, ConsumerCtx& c, 
     }
   } else {
     const int layer = (type == T_LMHEAD) ? p.L : t.layer;
-    const u64* src = (type == T_GATEUP) ? p.ll_hm : p.ll_hx + (size_t)(layer & 1) * p.H;
-    ss = ll_gather(p, c.ctid, c.nct, src, p.H, kpad, tag_of(c, layer), xs, gain, ti);
+    if constexpr (TP) {
+      const u64* src = (type == T_GATEUP) ? p.ll_hm : p.ll_hx + (size_t)(layer & 1) * p.tp_size * p.H;
+      ss = ll_gather_slots(p, c.ctid, c.nct, src, p.H, kpad, tag_of(c, layer), xs, gain, ti);
+    } else {
+      const u64* src = (type == T_GATEUP) ? p.ll_hm : p.ll_hx + (size_t)(layer & 1) * p.H;
+      ss = ll_gather(p, c.ctid, c.nct, src, p.H, kpad, tag_of(c, layer), xs, gain, ti);
+    }
   }
   ss = warp_sum(ss);
   float* red = hdr->red + (ti & 1) * 16;  // by task parity: a warp that runs ahead writes the other half
@@ -481,27 +620,41 @@ __device__ __forceinline__ void gemv_prologue(const KParams& p, ConsumerCtx& c, 
 
 // Epilogue operand of one output row (bias, residual input).  Residuals are tagged words of a
 // vector this step has already completed; the tag is still checked (cheap) rather than assumed.
+template <bool TP>
 __device__ __forceinline__ float load_eop(const KParams& p, const ConsumerCtx& c, const Task& t, int ti, int vrow, int tok) {
   switch (t.type) {
     case T_QKV: return p.has_bias ? ldg_keep_f1(p.fparams + (size_t)t.layer * p.fp_layer_stride + p.fp_bias + vrow) : 0.f;
     case T_OPROJ:
+      if (TP && p.tp_rank != 0) return 0.f;  // rank 0's partial rows carry the residual
       if (t.layer == 0) return __bfloat162float(p.embed[(size_t)tok * p.H + vrow]);
-      return ll_wait(p, p.ll_hx + (size_t)(t.layer & 1) * p.H + vrow, tag_of(c, t.layer), ti);
-    case T_DOWN: return ll_wait(p, p.ll_hm + vrow, tag_of(c, t.layer), ti);
+      if constexpr (TP) return ll_wait_slots_tp(p, p.ll_hx + (size_t)(t.layer & 1) * p.tp_size * p.H, p.H, vrow, tag_of(c, t.layer), ti);
+      else return ll_wait(p, p.ll_hx + (size_t)(t.layer & 1) * p.H + vrow, tag_of(c, t.layer), ti);
+    case T_DOWN:
+      if (TP && p.tp_rank != 0) return 0.f;
+      if constexpr (TP) return ll_wait_slots_tp(p, p.ll_hm, p.H, vrow, tag_of(c, t.layer), ti);
+      else return ll_wait(p, p.ll_hm + vrow, tag_of(c, t.layer), ti);
     default: return 0.f;
   }
 }
 
+template <bool TP>
 __device__ __forceinline__ void gemv_epilogue(const KParams& p, ConsumerCtx& c, const Task& t, int vrow, float v,
                                               float v_pair, float eop) {
   switch (t.type) {
     case T_QKV: ll_store(p.ll_qkv + vrow, v + eop, tag_of(c, t.layer)); break;
-    case T_OPROJ: ll_store(p.ll_hm + vrow, eop + v, tag_of(c, t.layer)); break;
+    case T_OPROJ:
+      if constexpr (TP) tp_publish(p, 0, 0, vrow, eop + v, tag_of(c, t.layer));
+      else ll_store(p.ll_hm + vrow, eop + v, tag_of(c, t.layer));
+      break;
     case T_GATEUP: ll_store(p.ll_act + (vrow >> 1), silu(v) * v_pair, tag_of(c, t.layer)); break;  // vrow even = gate, pair = up
-    case T_DOWN: ll_store(p.ll_hx + (size_t)((t.layer + 1) & 1) * p.H + vrow, eop + v, tag_of(c, t.layer + 1)); break;
+    case T_DOWN:
+      if constexpr (TP) tp_publish(p, 1, (t.layer + 1) & 1, vrow, eop + v, tag_of(c, t.layer + 1));
+      else ll_store(p.ll_hx + (size_t)((t.layer + 1) & 1) * p.H + vrow, eop + v, tag_of(c, t.layer + 1));
+      break;
     case T_LMHEAD: {
-      if (p.logits) p.logits[vrow] = v;
-      if (v > c.best_val) { c.best_val = v; c.best_idx = vrow; }  // rows ascend: first max wins ties
+      const int gvrow = TP ? vrow + p.vocab_off : vrow;
+      if (p.logits) p.logits[gvrow] = v;
+      if (v > c.best_val) { c.best_val = v; c.best_idx = gvrow; }  // rows ascend: first max wins ties
     } break;
     default: break;
   }
@@ -626,7 +779,7 @@ __device__ __forceinline__ void gemv_ktiles_wide(const KParams& p, uint32_t& slo
   }
 }
 
-template <int RW>
+template <int RW, bool TP>
 __device__ __forceinline__ void gemv_tiles_t(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx,
                                              const float* xs, SmemHdr* hdr, uint8_t* ring, int tok, float eop0, int probe) {
   const int WK = (t.geom >> 8) & 0xff, rw = (t.geom >> 16) & 0xff, lgWK = 31 - __clz(WK);
@@ -652,7 +805,7 @@ __device__ __forceinline__ void gemv_tiles_t(const KParams& p, ConsumerCtx& c, c
     if (WK == 1) { if ((c.lane & 3) == 0 && rsel < my_n) erow = my_r0 + rsel; }
     else if (c.ctid < rows) erow = c.ctid;
     float eop = eop0;
-    if (tile > 0 && erow >= 0 && !probe) eop = load_eop(p, c, t, task_idx, vrow0 + erow, tok);
+    if (tile > 0 && erow >= 0 && !probe) eop = load_eop<TP>(p, c, t, task_idx, vrow0 + erow, tok);
     float2 acc[kRW];
 #pragma unroll
     for (int i = 0; i < kRW; ++i) acc[i] = make_float2(0.f, 0.f);
@@ -683,8 +836,8 @@ __device__ __forceinline__ void gemv_tiles_t(const KParams& p, ConsumerCtx& c, c
       s *= c.rs;
       const float partner = __shfl_xor_sync(0xffffffffu, s, 4);  // row rsel ^ 1 (the `up` row of a gate row)
       if (erow >= 0) {
-        if (t.type != T_GATEUP) gemv_epilogue(p, c, t, vrow0 + erow, s, 0.f, eop);
-        else if (!(erow & 1)) gemv_epilogue(p, c, t, vrow0 + erow, s, partner, 0.f);
+        if (t.type != T_GATEUP) gemv_epilogue<TP>(p, c, t, vrow0 + erow, s, 0.f, eop);
+        else if (!(erow & 1)) gemv_epilogue<TP>(p, c, t, vrow0 + erow, s, partner, 0.f);
       }
     } else {
       float* rb = &hdr->red2[tile & 1][0][0];
@@ -693,10 +846,10 @@ __device__ __forceinline__ void gemv_tiles_t(const KParams& p, ConsumerCtx& c, c
       if (erow >= 0) {
         float tot = 0.f, tot2 = 0.f;
         for (int k = 0; k < WK; ++k) tot += rb[k * 32 + erow];
-        if (t.type != T_GATEUP) gemv_epilogue(p, c, t, vrow0 + erow, tot * c.rs, 0.f, eop);
+        if (t.type != T_GATEUP) gemv_epilogue<TP>(p, c, t, vrow0 + erow, tot * c.rs, 0.f, eop);
         else if (!(erow & 1)) {
           for (int k = 0; k < WK; ++k) tot2 += rb[k * 32 + erow + 1];
-          gemv_epilogue(p, c, t, vrow0 + erow, tot * c.rs, tot2 * c.rs, 0.f);
+          gemv_epilogue<TP>(p, c, t, vrow0 + erow, tot * c.rs, tot2 * c.rs, 0.f);
         }
       }
     }
@@ -706,16 +859,18 @@ __device__ __forceinline__ void gemv_tiles_t(const KParams& p, ConsumerCtx& c, c
   if (WK == 1 && !probe) consumer_sync(c.nct);
 }
 
+template <bool TP>
 __device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx,
                                            const float* xs, SmemHdr* hdr, uint8_t* ring, int tok, float eop0, int probe) {
   switch ((((t.geom >> 16) & 0xff) + 1) >> 1) {  // rows per warp, rounded up to even
-    case 1: gemv_tiles_t<2>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
-    case 2: gemv_tiles_t<4>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
-    case 3: gemv_tiles_t<6>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
-    default: gemv_tiles_t<8>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
+    case 1: gemv_tiles_t<2, TP>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
+    case 2: gemv_tiles_t<4, TP>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
+    case 3: gemv_tiles_t<6, TP>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
+    default: gemv_tiles_t<8, TP>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
   }
 }
 
+template <bool TP>
 __device__ __forceinline__ void lm_finish(const KParams& p, ConsumerCtx& c, SmemHdr* hdr) {
   // per-lane best -> per-warp best -> CTA best -> global partial -> last CTA reduces, publishes, bumps the epoch
   float bv = c.best_val;
@@ -758,6 +913,7 @@ __device__ __forceinline__ void lm_finish(const KParams& p, ConsumerCtx& c, Smem
       const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
       if (ov > best || (ov == best && oi < idx)) { best = ov; idx = oi; }
     }
+    if constexpr (TP) tp_argmax_exchange(p, c.lane, tag_of(c, p.L + 1), best, idx);
     if (c.lane == 0) {
       p.next_tokens[0] = idx;
       if (p.auto_advance) { p.tokens[0] = idx; p.positions[0] = p.positions[0] + 1; }
@@ -768,6 +924,7 @@ __device__ __forceinline__ void lm_finish(const KParams& p, ConsumerCtx& c, Smem
   }
 }
 
+template <bool TP>
 __device__ __forceinline__ void run_gemv(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* xs,
                                          SmemHdr* hdr, uint8_t* ring, int tok, int probe) {
   stamp(p, c, task_idx, 0);
@@ -782,14 +939,14 @@ __device__ __forceinline__ void run_gemv(const KParams& p, ConsumerCtx& c, const
       const int rsel = ((c.lane >> 4) & 1) * 4 + ((c.lane >> 3) & 1) * 2 + ((c.lane >> 2) & 1);
       if ((c.lane & 3) == 0 && rsel < rw && c.cw * rw + rsel < rows0) erow = c.cw * rw + rsel;
     } else if (c.ctid < rows0) erow = c.ctid;
-    if (erow >= 0) eop0 = load_eop(p, c, t, task_idx, t.a + erow, tok);
-    gemv_prologue(p, c, t, task_idx, xs, hdr, tok);
+    if (erow >= 0) eop0 = load_eop<TP>(p, c, t, task_idx, t.a + erow, tok);
+    gemv_prologue<TP>(p, c, t, task_idx, xs, hdr, tok);
   }
   stamp(p, c, task_idx, 1);
-  gemv_tiles(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe);
+  gemv_tiles<TP>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe);
   if (probe) { stamp(p, c, task_idx, 7); return; }
   stamp(p, c, task_idx, 2);
-  if (t.type == T_LMHEAD) lm_finish(p, c, hdr);
+  if (t.type == T_LMHEAD) lm_finish<TP>(p, c, hdr);
   stamp(p, c, task_idx, 7);
 }
 
@@ -1098,6 +1255,7 @@ struct GemvArgs {
   int type, layer, a, b, k, kchunks, rt, ktc, n_tiles, n_ktiles, geom;
   int task_idx, tok, probe;
 };
+template <bool TP>
 __device__ __noinline__ uint32_t run_gemv_nl(const KParams& p, GemvArgs g, float* xs, SmemHdr* hdr, uint8_t* ring) {
   ConsumerCtx c;
   c.cw = g.cw; c.lane = g.lane; c.ctid = g.ctid; c.nct = g.nct; c.epoch = g.epoch; c.slot = g.slot; c.ph = g.ph;
@@ -1105,7 +1263,7 @@ __device__ __noinline__ uint32_t run_gemv_nl(const KParams& p, GemvArgs g, float
   Task t{};
   t.type = g.type; t.layer = g.layer; t.a = g.a; t.b = g.b; t.k = g.k; t.kchunks = g.kchunks; t.rt = g.rt; t.ktc = g.ktc;
   t.n_tiles = g.n_tiles; t.n_ktiles = g.n_ktiles; t.geom = g.geom;
-  run_gemv(p, c, t, g.task_idx, xs, hdr, ring, g.tok, g.probe);
+  run_gemv<TP>(p, c, t, g.task_idx, xs, hdr, ring, g.tok, g.probe);
   return c.slot | (c.ph << 8);
 }
 __device__ __noinline__ void run_merge_nl(const KParams& p, WarpArgs w) {
@@ -1120,7 +1278,7 @@ __device__ __noinline__ void run_merge_nl(const KParams& p, WarpArgs w) {
 // ----------------------------------------------------------------------------------
 // the persistent kernel
 // ----------------------------------------------------------------------------------
-template <int CW>
+template <int CW, bool TP>
 __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   SmemHdr* hdr = reinterpret_cast<SmemHdr*>(smem);
@@ -1258,7 +1416,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
     tok = __ldcg(p.tokens);
     pos = __ldcg(p.positions);
     c.epoch = ld_relaxed_u32(p.sync);
-    if (pos < 0 || pos >= p.max_ctx || tok < 0 || tok >= p.V) {
+    if (pos < 0 || pos >= p.max_ctx || tok < 0 || tok >= p.V * p.tp_size) {
       if (c.ctid == 0) dev_fail(p, DE_BAD_POS, -1, pos, tok, p.max_ctx);
       return;
     }
@@ -1280,7 +1438,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       g.cw = c.cw; g.lane = c.lane; g.ctid = c.ctid; g.nct = c.nct; g.epoch = c.epoch; g.slot = c.slot; g.ph = c.ph;
       g.type = t.type; g.layer = t.layer; g.a = t.a; g.b = t.b; g.k = t.k; g.kchunks = t.kchunks; g.rt = t.rt; g.ktc = t.ktc;
       g.n_tiles = t.n_tiles; g.n_ktiles = t.n_ktiles; g.geom = t.geom; g.task_idx = ti; g.tok = tok; g.probe = probe;
-      const uint32_t sp = run_gemv_nl(p, g, scratch, hdr, ring);
+      const uint32_t sp = run_gemv_nl<TP>(p, g, scratch, hdr, ring);
       c.slot = sp & 0xffu; c.ph = sp >> 8;
     }
   }
@@ -1398,11 +1556,15 @@ struct AdamkHandle_ {
   const uint8_t* wpacked = nullptr;
   const float* fparams = nullptr;
   AdamkWeightPtrs w{};
+  int tp_rank = 0, tp_size = 1;
+  void* peer_ws[kMaxTP] = {nullptr};
+  bool peers_bound = false;
   int* status_host = nullptr;
   int* status_dev = nullptr;
   unsigned long long* trace = nullptr;
   int smem_bytes = 0;
   // workspace layout (byte offsets)
+  size_t ws_lmx = 0;
   size_t ws_sync = 0, ws_hx = 0, ws_hm = 0, ws_qkv = 0, ws_attn = 0, ws_act = 0, ws_part = 0, ws_lm_val = 0,
          ws_lm_idx = 0, ws_total = 0;
 };
@@ -1424,12 +1586,14 @@ int adamk_device_sm_count(int device, int* out_sms) {
 int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task_table_bytes, int tp_rank, int tp_size,
                  adamk_handle* out) {
   if (!desc || !task_table || !out) return fail(ADAMK_E_INVALID, "NULL argument");
-  if (tp_size != 1 || tp_rank != 0) return fail(ADAMK_E_UNSUPPORTED, "tensor parallel shards are not built yet (tp_size must be 1)");
+  if ((tp_size != 1 && tp_size != 2 && tp_size != 4 && tp_size != 8) || tp_rank < 0 || tp_rank >= tp_size)
+    return fail(ADAMK_E_INVALID, "tp_size must be 1, 2, 4 or 8 and 0 <= tp_rank < tp_size");
   if (task_table_bytes < (size_t)kHeaderInts * 4 || task_table_bytes % 4) return fail(ADAMK_E_INVALID, "task table too small");
   const int* tt = static_cast<const int*>(task_table);
   if (tt[0] != kMagic || tt[1] != kVersion) return fail(ADAMK_E_INVALID, "task table magic/version mismatch");
   auto h = new AdamkHandle_();
   h->desc = *desc;
+  h->tp_rank = tp_rank; h->tp_size = tp_size;
   h->n_sms = tt[2]; h->C = tt[3]; h->n_stage = tt[4]; h->stage_bytes = tt[5]; h->n_tasks = tt[6]; h->batch = tt[7];
   h->inflight = tt[8]; h->attn_chunks = tt[9]; h->attn_min_chunk = tt[10]; h->scratch_bytes = tt[11];
   h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14]; h->pf_window_kb = tt[15];
@@ -1521,8 +1685,9 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
   h->ws_sync = take(64);
-  h->ws_hx = take((size_t)2 * d.hidden * 8);
-  h->ws_hm = take((size_t)d.hidden * 8);
+  h->ws_hx = take((size_t)2 * tp_size * d.hidden * 8);
+  h->ws_hm = take((size_t)tp_size * d.hidden * 8);
+  h->ws_lmx = take((size_t)kMaxTP * 2 * 8);
   h->ws_qkv = take((size_t)qkv_rows * 8);
   h->ws_attn = take((size_t)d.n_q_heads * d.head_dim * 8);
   h->ws_act = take((size_t)d.intermediate * 8);
@@ -1556,10 +1721,11 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
     memset(h->status_host, 0, 64);
     e = cudaHostGetDevicePointer(&h->status_dev, h->status_host, 0);
   }
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(adamk_decode_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  for (const void* fn : {(const void*)adamk_decode_kernel<4, false>, (const void*)adamk_decode_kernel<7, false>,
+                         (const void*)adamk_decode_kernel<8, false>, (const void*)adamk_decode_kernel<16, false>,
+                         (const void*)adamk_decode_kernel<4, true>, (const void*)adamk_decode_kernel<7, true>,
+                         (const void*)adamk_decode_kernel<8, true>, (const void*)adamk_decode_kernel<16, true>})
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   if (e != cudaSuccess) {
     std::string m = std::string("adamk_create: ") + cudaGetErrorString(e);
     adamk_destroy(h);
@@ -1658,10 +1824,16 @@ int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, a
 }
 
 int adamk_bind_peers(adamk_handle h, void* const* peer_workspaces, int n_peers) {
-  (void)peer_workspaces;
   if (!h) return fail(ADAMK_E_INVALID, "NULL handle");
-  if (n_peers == 1) return ADAMK_OK;
-  return fail(ADAMK_E_UNSUPPORTED, "tensor parallel shards are not built yet");
+  if (n_peers != h->tp_size) return fail(ADAMK_E_INVALID, "n_peers must equal tp_size");
+  if (h->tp_size == 1) return ADAMK_OK;
+  if (!peer_workspaces) return fail(ADAMK_E_INVALID, "NULL peer list");
+  for (int r = 0; r < n_peers; ++r) {
+    if (!peer_workspaces[r]) return fail(ADAMK_E_INVALID, "NULL peer workspace");
+    h->peer_ws[r] = peer_workspaces[r];
+  }
+  h->peers_bound = true;
+  return ADAMK_OK;
 }
 
 static int fill_params(adamk_handle h, KParams& p, void* workspace) {
@@ -1686,6 +1858,13 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
     p.ll_hx = (u64*)(ws + h->ws_hx); p.ll_hm = (u64*)(ws + h->ws_hm); p.ll_qkv = (u64*)(ws + h->ws_qkv);
     p.ll_attn = (u64*)(ws + h->ws_attn); p.ll_act = (u64*)(ws + h->ws_act); p.ll_part = (u64*)(ws + h->ws_part);
     p.lm_val = (float*)(ws + h->ws_lm_val); p.lm_idx = (int*)(ws + h->ws_lm_idx);
+    p.ll_lmx = (u64*)(ws + h->ws_lmx);
+  }
+  p.tp_rank = h->tp_rank; p.tp_size = h->tp_size; p.vocab_off = h->tp_rank * d.vocab;
+  for (int r = 0; r < h->tp_size; ++r) {
+    uint8_t* pw = h->tp_size == 1 ? ws : static_cast<uint8_t*>(h->peer_ws[r]);
+    if (!pw) continue;
+    p.peer_hx[r] = (u64*)(pw + h->ws_hx); p.peer_hm[r] = (u64*)(pw + h->ws_hm); p.peer_lmx[r] = (u64*)(pw + h->ws_lmx);
   }
   p.status = h->status_dev;
   p.trace = h->trace;
@@ -1699,9 +1878,11 @@ static int launch(adamk_handle h, const KParams& p, cudaStream_t stream) {
   if (sms < h->n_sms) return fail(ADAMK_E_INVALID, "task table was built for more SMs than this device has");
   void* args[] = {(void*)&p};
   // cooperative launch: all CTAs must be co-resident (they poll each other's outputs)
-  const void* fn = h->C == 4 ? (const void*)adamk_decode_kernel<4>
-                   : h->C == 7 ? (const void*)adamk_decode_kernel<7>
-                   : h->C == 8 ? (const void*)adamk_decode_kernel<8> : (const void*)adamk_decode_kernel<16>;
+  const bool tp = h->tp_size > 1;
+  const void* fn = h->C == 4 ? (tp ? (const void*)adamk_decode_kernel<4, true> : (const void*)adamk_decode_kernel<4, false>)
+                   : h->C == 7 ? (tp ? (const void*)adamk_decode_kernel<7, true> : (const void*)adamk_decode_kernel<7, false>)
+                   : h->C == 8 ? (tp ? (const void*)adamk_decode_kernel<8, true> : (const void*)adamk_decode_kernel<8, false>)
+                               : (tp ? (const void*)adamk_decode_kernel<16, true> : (const void*)adamk_decode_kernel<16, false>);
   CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(h->n_sms), dim3((h->C + 1) * 32), args, (size_t)h->smem_bytes, stream));
   return ADAMK_OK;
 }
@@ -1713,6 +1894,8 @@ int adamk_decode_step(adamk_handle h, int32_t* token_ids, int32_t* positions, in
     return fail(ADAMK_E_INVALID, "NULL argument");
   if (!h->bound) return fail(ADAMK_E_STATE, "adamk_bind_weights has not been called");
   if (batch != h->batch) return fail(ADAMK_E_INVALID, "batch does not match the task table");
+  if (h->tp_size > 1 && !h->peers_bound) return fail(ADAMK_E_STATE, "adamk_bind_peers has not been called");
+  if (h->tp_size > 1 && h->peer_ws[h->tp_rank] != workspace) return fail(ADAMK_E_INVALID, "workspace is not this rank's entry of the peer list");
   if (h->status_host[0] != 0) return fail(ADAMK_E_DEVICE, "a previous step reported a device error; see adamk_device_status");
   KParams p;
   fill_params(h, p, workspace);

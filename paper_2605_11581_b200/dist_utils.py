@@ -4,6 +4,10 @@ BASELINE.json configs[1] (Qwen2.5-1.5B, 2 KV heads) does not shard usefully:
 N GPUs run N independent replicas ("replicas only"), so the data
 path has no collective.  ``torch.distributed`` is used only to line the ranks
 up (barrier) and to take the maximum of their device-side timings.
+
+Tensor parallelism (configs[3], Qwen3-8B) keeps the step a single launch per rank: the kernel stores its
+partial rows straight into every peer's workspace over NVLink.  ``torch.distributed`` is used once, at
+start-up, to exchange the CUDA IPC handles of the workspaces (``share_workspaces``).
 """
 
 from __future__ import annotations
@@ -54,3 +58,33 @@ class RankGroup:
         if self.dist is not None:
             self.dist.destroy_process_group()
             self.dist = None
+
+
+def share_workspaces(group: RankGroup, workspace: torch.Tensor) -> list[torch.Tensor]:
+    """Map every rank's workspace into this process (same node, NVLink / NVSwitch peers).
+
+    Each rank exports its workspace allocation as a CUDA IPC handle (``UntypedStorage._share_cuda_``), the
+    handles are all-gathered as Python objects, and every rank opens its peers' handles
+    (``cudaIpcOpenMemHandle`` with lazy peer access).  Returns uint8 tensors in rank order, this rank's own
+    tensor at index ``group.rank``; keep them alive as long as the plugin runs.  NOT exercised in this
+    repository's tests (they run on one GPU, where the ranks of tools/tp_single_gpu.py share an address
+    space); the kernel side of the exchange is."""
+    if group.world == 1:
+        return [workspace]
+    assert workspace.is_cuda and workspace.dtype == torch.uint8 and workspace.is_contiguous()
+    storage = workspace.untyped_storage()
+    handle = storage._share_cuda_()
+    meta = (handle, workspace.storage_offset(), workspace.numel())
+    metas: list = [None] * group.world
+    group.dist.all_gather_object(metas, meta)
+    out = []
+    for r, (h, off, n) in enumerate(metas):
+        if r == group.rank:
+            out.append(workspace)
+            continue
+        st = torch.UntypedStorage._new_shared_cuda(*h)
+        t = torch.empty(0, dtype=torch.uint8, device=torch.device("cuda", st.device.index))
+        t.set_(st, off, (n,))
+        out.append(t)
+    group.barrier()
+    return out

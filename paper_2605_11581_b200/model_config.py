@@ -77,6 +77,22 @@ class ModelConfig:
     def algorithmic_bytes(self, ctx: int, batch: int = 1) -> int:
         return self.weight_bytes_per_token() + batch * ctx * self.kv_bytes_per_ctx_token()
 
+    def shard(self, tp: int) -> "ModelConfig":
+        """Dimensions of ONE tensor-parallel rank (Megatron-style): q/k/v heads, the MLP
+        intermediate channels and the LM-head vocabulary are split ``tp`` ways; ``hidden`` is not."""
+        if tp == 1:
+            return self
+        if tp not in (2, 4, 8):
+            raise ValueError("tp must be 1, 2, 4 or 8")
+        for f in ("n_q_heads", "n_kv_heads", "intermediate", "vocab"):
+            if getattr(self, f) % tp:
+                raise ValueError(f"{f}={getattr(self, f)} is not divisible by tp={tp}")
+        if (self.intermediate // tp) % 8:
+            raise ValueError("intermediate / tp must be a multiple of 8")
+        from dataclasses import replace
+        return replace(self, name=f"{self.name}-tp{tp}", n_q_heads=self.n_q_heads // tp, n_kv_heads=self.n_kv_heads // tp,
+                       intermediate=self.intermediate // tp, vocab=self.vocab // tp)
+
     def to_dict(self) -> dict:
         return asdict(self)
 

@@ -124,7 +124,9 @@ class MegaKernelPlugin:
     table is derived from it and the model config at construction."""
 
     def __init__(self, cfg: ModelConfig, schedule: KernelSchedule, max_ctx: int, device: int | str = 0,
-                 n_sms: int | None = None):
+                 n_sms: int | None = None, tp_rank: int = 0, tp_size: int = 1):
+        """``cfg`` holds the dimensions of THIS rank (``full_cfg.shard(tp_size)``); with ``tp_size > 1`` call
+        :meth:`bind_peers` with every rank's workspace before the first step."""
         if not torch.cuda.is_available():
             raise AdamkError(-102, "no CUDA device: the decode MegaKernel has no CPU fallback")
         self.lib = load_library()
@@ -139,7 +141,8 @@ class MegaKernelPlugin:
         blob = self.table.blob
         self._blob = C.create_string_buffer(blob, len(blob))
         h = C.c_void_p()
-        _check(self.lib, self.lib.adamk_create(C.byref(desc), self._blob, len(blob), 0, 1, C.byref(h)))
+        self.tp_rank, self.tp_size = int(tp_rank), int(tp_size)
+        _check(self.lib, self.lib.adamk_create(C.byref(desc), self._blob, len(blob), self.tp_rank, self.tp_size, C.byref(h)))
         self._h = h
         self._weights: DecoderWeights | None = None
         self.packed: torch.Tensor | None = None
@@ -152,7 +155,8 @@ class MegaKernelPlugin:
         self.tokens = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.positions = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.next_token = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.logits = torch.zeros(1, cfg.vocab, dtype=torch.float32, device=self.device)
+        # logits of the whole vocabulary; a tensor-parallel rank fills its own slice [rank * V/tp, (rank + 1) * V/tp)
+        self.logits = torch.zeros(1, cfg.vocab * self.tp_size, dtype=torch.float32, device=self.device)
         self.launches = 0
 
     # -- weights -------------------------------------------------------------
@@ -177,6 +181,15 @@ class MegaKernelPlugin:
                                                      self._stream_ptr()))
         self._embed = w.embed                      # the kernel gathers embedding rows from the source table
         self._weights = w if keep_source else None
+
+    def bind_peers(self, peer_workspaces) -> None:
+        """Tensor parallelism: device pointers (or tensors) of EVERY rank's workspace, own rank included, in rank
+        order.  On one node these are peer-mapped allocations (CUDA IPC / cuMem handles exchanged once through
+        ``torch.distributed``, see dist_utils.share_workspaces); the kernel stores its partial rows into them."""
+        ptrs = [int(w.data_ptr()) if hasattr(w, "data_ptr") else int(w) for w in peer_workspaces]
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        _check(self.lib, self.lib.adamk_bind_peers(self._h, arr, len(ptrs)))
+        self._peers = list(peer_workspaces)   # keep the mappings alive
 
     # -- decode ----------------------------------------------------------------
     def set_state(self, token: int, position: int) -> None:

@@ -66,6 +66,30 @@ class DecoderWeights:
                   for l in self.layers]
         return DecoderWeights(self.cfg, mv(self.embed), mv(self.final_norm), mv(self.lm_head), layers)
 
+    def shard(self, rank: int, tp: int) -> "DecoderWeights":
+        """The weights of tensor-parallel rank ``rank`` of ``tp`` (``cfg.shard(tp)`` dimensions): q/k/v rows by
+        head, O-proj columns by head, gate/up rows and down columns by intermediate channel, LM-head rows by
+        vocabulary slice.  ``embed`` stays whole (every rank gathers the input row); norm gains are replicated."""
+        if tp == 1:
+            return self
+        cfg, lc = self.cfg, self.cfg.shard(tp)
+        q0, q1 = rank * lc.q_dim, (rank + 1) * lc.q_dim
+        k0, k1 = rank * lc.kv_dim, (rank + 1) * lc.kv_dim
+        i0, i1 = rank * lc.intermediate, (rank + 1) * lc.intermediate
+        v0, v1 = rank * lc.vocab, (rank + 1) * lc.vocab
+
+        def rows(t, a, b):
+            return None if t is None else t[a:b].contiguous()
+
+        layers = []
+        for l in self.layers:
+            layers.append(LayerWeights(
+                ln1=l.ln1, wq=rows(l.wq, q0, q1), wk=rows(l.wk, k0, k1), wv=rows(l.wv, k0, k1),
+                wo=l.wo[:, q0:q1].contiguous(), ln2=l.ln2, wgate=rows(l.wgate, i0, i1), wup=rows(l.wup, i0, i1),
+                wdown=l.wdown[:, i0:i1].contiguous(), bq=rows(l.bq, q0, q1), bk=rows(l.bk, k0, k1), bv=rows(l.bv, k0, k1),
+                q_norm=l.q_norm, k_norm=l.k_norm))
+        return DecoderWeights(lc, self.embed, self.final_norm, self.lm_head_matrix[v0:v1].contiguous(), layers)
+
     def n_params(self) -> int:
         n = self.embed.numel() + self.final_norm.numel()
         if self.lm_head is not None:

@@ -232,3 +232,35 @@ def test_repeated_runs_are_bitwise_reproducible():
         outs.append(torch.stack(acc).cpu())
         plug.close()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+def test_tensor_parallel_ranks_on_one_gpu(tp):
+    """In-kernel tensor parallelism (adamk.cu: tp_publish / ll_gather_tp / tp_argmax_exchange): `tp` ranks with
+    148 // tp SMs each run concurrently on one GPU and store their partial O-proj / down-proj rows and LM-head
+    argmax into each other's workspaces, as ranks on different GPUs do through peer-mapped memory.  Logits and
+    tokens are checked against the unsharded oracle inside tools/tp_single_gpu.py; it runs in a subprocess so a
+    device trap (watchdog) cannot poison this process."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    res = subprocess.run([sys.executable, str(root / "tools" / "tp_single_gpu.py"), str(tp), "16"],
+                         capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+    assert f"tp={tp} on one GPU" in res.stdout and "steps ok" in res.stdout
+
+
+def test_tp_requires_peers():
+    from paper_2605_11581_b200.plugin import AdamkError, MegaKernelPlugin
+    from paper_2605_11581_b200.weights import random_weights
+
+    cfg = D128_Q3
+    plug = MegaKernelPlugin(cfg.shard(2), SCHEDS["c7"], max_ctx=64, n_sms=74, tp_rank=1, tp_size=2)
+    plug.bind_weights(random_weights(cfg, seed=0).shard(1, 2))
+    with pytest.raises(AdamkError):          # step before bind_peers
+        plug.decode_step(1, 0)
+    with pytest.raises(AdamkError):          # peer list of the wrong length
+        plug.bind_peers([plug.workspace])
+    plug.close()
