@@ -93,7 +93,8 @@ const char* adamk_last_error(void);
 /* Create a plugin instance from the model description and the device task
  * table blob (task_table.py: header, per-SM ranges, 64-byte task records).
  * The table is validated against the description and the device, then copied
- * to the GPU.  tp_rank/tp_size select the tensor-parallel shard (1 GPU: 0/1). */
+ * to the GPU.  tp_rank/tp_size select the tensor-parallel shard (1 GPU: 0/1;
+ * tp_size 2, 4 or 8 otherwise). */
 int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task_table_bytes,
                  int tp_rank, int tp_size, adamk_handle* out);
 void adamk_destroy(adamk_handle h);
@@ -106,8 +107,13 @@ size_t adamk_packed_bytes(adamk_handle h);
  * the stream has drained, except `embed`. */
 int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, adamk_stream stream);
 
-/* Tensor parallelism only: peer workspace base pointers (device-mapped peer
- * memory, one per rank, own rank included) for the in-kernel NVLink reduction. */
+/* Tensor parallelism only (tp_size > 1 at adamk_create; `desc` then holds the
+ * rank's shard: n_q_heads, n_kv_heads, intermediate and vocab divided by
+ * tp_size): base pointers of EVERY rank's workspace as seen from this GPU
+ * (peer-mapped memory; own rank included, rank order).  The kernel stores its
+ * partial O-proj / down-proj rows and its LM-head argmax into slot tp_rank of
+ * each of them and sums its own slots in rank order; no collective library is
+ * involved.  decode_step fails with ADAMK_E_STATE until this has been called. */
 int adamk_bind_peers(adamk_handle h, void* const* peer_workspaces, int n_peers);
 
 /* Workspace: the tagged activation vectors ({fp32 value, tag} words), split-KV
