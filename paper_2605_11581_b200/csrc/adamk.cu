@@ -54,7 +54,7 @@ constexpr int kChunk = 256;          // K elements per chunk
 constexpr int kSmemMax = 232448;
 constexpr int kSmemReserved = 4096;  // barriers + reduction scratch
 constexpr int kMaxStages = 16;
-constexpr int kAttnBlock = 64;       // positions per K (or V) ring stage
+constexpr int kAttnBlockMax = 64;    // positions per K (or V) ring stage: 8 per attention warp (p.attn_block)
 constexpr int kAttnWarps = 8;        // consumer warps that take part in an attention unit
 constexpr int kAttnChunksMax = 128;  // split-KV units per (sequence, kv head)
 constexpr int kGMax = 8;             // max q heads per kv head
@@ -80,6 +80,7 @@ struct KParams {
   float eps;
   // schedule
   int C, n_stage, stage_bytes, attn_chunks, attn_min_chunk, scratch_bytes, n_lm_tasks, inflight;
+  int attn_block;          // positions per K / V block = 8 x attention warps: one pass of the unit's warps per block
   int pf_window_bytes;     // how far past the ring the Loader prefetches into L2 while it is blocked (0 = off)
   int task_cache_bytes;    // shared-memory copy of this SM's task list (32-byte packed records)
   unsigned poll_sleep_ns;  // back-off between polls of a not-yet-complete vector (0 = none)
@@ -363,7 +364,7 @@ __device__ __forceinline__ AttnGeom attn_geometry(const KParams& p, int pos, int
   g.n_active = (ctx + g.CL - 1) / g.CL;
   g.t0 = slot * g.CL;
   g.n = min(ctx, g.t0 + g.CL) - g.t0;           // <= 0 for inactive slots
-  g.nblk = g.n > 0 ? (g.n + kAttnBlock - 1) / kAttnBlock : 0;
+  g.nblk = g.n > 0 ? (g.n + p.attn_block - 1) / p.attn_block : 0;
   return g;
 }
 
@@ -1069,8 +1070,8 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
 #pragma unroll 1
   for (int blk = 0; blk < nblk; ++blk) {
     const bool patch = owns_new && blk == nblk - 1;
-    const int new_row = (pos - t0) - blk * kAttnBlock;  // row of the new token inside this block (if patch)
-    const int nblkpos = min(kAttnBlock, n - blk * kAttnBlock);
+    const int new_row = (pos - t0) - blk * p.attn_block;  // row of the new token inside this block (if patch)
+    const int nblkpos = min(p.attn_block, n - blk * p.attn_block);
     mbar_wait(p, full0 + c.slot * 8, c.ph, DE_WATCHDOG_FULL, task_idx);   // K stage
     const uint32_t kb = ring_addr + c.slot * (uint32_t)p.stage_bytes;
     const uint32_t kslot = c.slot;
@@ -1379,9 +1380,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
           if (lt.b >= ge.n_active) continue;
           const size_t head_base = ((size_t)(lt.layer * p.batch + lt.aux) * p.nkv + lt.a / p.G) * (size_t)p.max_ctx * p.D;
           for (int blk = 0; blk < ge.nblk; ++blk) {
-            const int nb = min(kAttnBlock, ge.n - blk * kAttnBlock);
+            const int nb = min(p.attn_block, ge.n - blk * p.attn_block);
             const uint32_t bytes = (uint32_t)nb * (uint32_t)p.D * 2u;
-            const size_t off = head_base + (size_t)(ge.t0 + blk * kAttnBlock) * p.D;
+            const size_t off = head_base + (size_t)(ge.t0 + blk * p.attn_block) * p.D;
             issue(p.kcache + off, bytes, false, ti);
             issue(p.vcache + off, bytes, false, ti);
           }
@@ -1612,8 +1613,8 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   if (h->n_sms < 1 || h->n_tasks < 1) return bad("empty task table");
   if (h->attn_chunks < 1 || h->attn_chunks > kAttnChunksMax || h->attn_min_chunk < 8)
     return bad("attention chunking out of range");
-  if (h->stage_bytes < kAttnBlock * d.head_dim * 2)
-    return bad("stage_bytes too small: a K/V block is 64 positions (64 * head_dim * 2 bytes)");
+  if (h->stage_bytes < 8 * std::min(h->C, kAttnWarps) * d.head_dim * 2)
+    return bad("stage_bytes too small for one K/V block (8 positions per attention warp)");
   const size_t need = ((size_t)kHeaderInts + (size_t)h->n_sms + 1 + (size_t)h->n_tasks * kTaskInts) * 4;
   if (task_table_bytes != need) return bad("task table size does not match its header");
   {
@@ -1846,6 +1847,7 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
   p.C = h->C; p.n_stage = h->n_stage; p.stage_bytes = h->stage_bytes; p.attn_chunks = h->attn_chunks;
   p.attn_min_chunk = h->attn_min_chunk; p.scratch_bytes = h->scratch_bytes; p.n_lm_tasks = h->n_lm_tasks;
   p.task_cache_bytes = h->task_cache_bytes; p.pf_window_bytes = h->pf_window_kb * 1024;
+  p.attn_block = 8 * std::min(h->C, kAttnWarps);
   p.inflight = h->inflight; p.poll_sleep_ns = (unsigned)h->poll_sleep_ns;
   p.tasks = h->d_tasks; p.sm_begin = h->d_sm_begin; p.sm_stream = h->d_sm_stream;
   p.wpacked = h->wpacked; p.fparams = h->fparams;

@@ -44,7 +44,7 @@ SMEM_MAX = 232448      # 227 KB opt-in shared memory per CTA on sm_100
 SMEM_RESERVED = 4096   # mbarriers + reduction scratch ahead of the scratch/ring regions
 MAX_STAGES = 16
 MAX_RW = 8             # rows per consumer warp per tile (eight accumulator rows per lane)
-ATTN_BLOCK = 64        # positions per K (or V) ring stage
+ATTN_BLOCK = 64        # most positions per K (or V) ring stage: 8 per attention warp
 ATTN_WARPS = 8         # consumer warps that take part in an attention unit
 ATTN_CHUNKS_MAX = 128  # split-KV units per (sequence, kv head)
 G_MAX = 8              # q heads per kv head
@@ -292,7 +292,7 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
         raise ScheduleError(
             f"n_stage={sched.n_stage} x {sched.stage_bytes} B stages + "
             f"{scratch_bytes(cfg, sched, batch)} B scratch exceed {SMEM_MAX} B shared memory (max {fit})")
-    if sched.stage_bytes < ATTN_BLOCK * cfg.head_dim * 2:
+    if sched.stage_bytes < 8 * min(sched.consumer_warps, ATTN_WARPS) * cfg.head_dim * 2:
         raise ScheduleError("ring slot smaller than one 64-position K/V block")
     if cfg.group > G_MAX:
         raise ScheduleError(f"more than {G_MAX} q heads per kv head")

@@ -28,11 +28,12 @@ print(f"weights on device in {time.time() - t0:.1f}s", flush=True)
 B = dict(consumer_warps=8, rows_per_tile=64, ktile_chunks=1, n_stage=5, attn_min_chunk=64)
 C4 = dict(B, consumer_warps=4, rows_per_tile=32)
 C7 = dict(B, consumer_warps=7, attn_min_chunk=128)
+D7 = dict(C7, rows_per_tile=56, ktile_chunks=2, n_stage=3, l2_prefetch_kb=512)
 scheds = [
-    ("c7 r56k2 s3 pf512", dict(C7, rows_per_tile=56, ktile_chunks=2, n_stage=3, l2_prefetch_kb=512)),
-    ("c7 r56k3 s2 pf512", dict(C7, rows_per_tile=56, ktile_chunks=3, n_stage=2, l2_prefetch_kb=512)),
-    ("c7 r56k1 s6 pf512", dict(C7, rows_per_tile=56, ktile_chunks=1, n_stage=6, l2_prefetch_kb=512)),
-    ("c4 r32k3 s3 pf512", dict(C4, ktile_chunks=3, n_stage=3, l2_prefetch_kb=512, attn_min_chunk=128)),
+    ("c7 mc112", dict(D7, attn_min_chunk=112)),
+    ("c7 mc56", dict(D7, attn_min_chunk=56)),
+    ("c7 mc168", dict(D7, attn_min_chunk=168)),
+    ("c7 mc224", dict(D7, attn_min_chunk=224)),
 ]
 
 
