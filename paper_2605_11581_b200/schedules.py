@@ -20,10 +20,10 @@ SCHEDULE_DIR = Path(__file__).resolve().parent / "schedules"
 
 # Profiled on B200 (profiles/): 7 consumer warps + the Loader warp = 8 warps per CTA (the register
 # file then gives every thread 255 registers; 9 warps are capped at 168 and the GEMV loop spills),
-# 56-row x 512-column sub-tiles (56 KB ring slots: two chunk iterations per warp per stage amortise
-# the per-stage barrier work), ring as deep as shared memory allows, 112-position split-KV units (two 56-position K/V blocks: one pass of the seven warps each),
+# 42-row x 512-column sub-tiles (42 KB ring slots, four of them: two chunk iterations per warp per stage
+# amortise the per-stage barrier work, and 42 rows tile the 120-122 gate/up rows of an SM without padding), ring as deep as shared memory allows, 112-position split-KV units (two 56-position K/V blocks: one pass of the seven warps each),
 # and a 512 KB per-SM L2 prefetch window past the ring.
-PROFILED_DEFAULT = dict(consumer_warps=7, rows_per_tile=56, ktile_chunks=2, attn_min_chunk=112, l2_prefetch_kb=512)
+PROFILED_DEFAULT = dict(consumer_warps=7, rows_per_tile=42, ktile_chunks=2, attn_min_chunk=112, l2_prefetch_kb=512)
 
 
 def default_schedule(cfg: ModelConfig) -> KernelSchedule:
