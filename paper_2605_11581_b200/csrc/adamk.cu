@@ -92,6 +92,7 @@ struct KParams {
   const uint8_t* wpacked;   // tile-major bf16 weight streams
   const float* fparams;     // fp32 norm gains / biases
   int fp_layer_stride, fp_ln1, fp_ln2, fp_bias, fp_qn, fp_kn, fp_final;
+  unsigned fp_bytes;        // size of the fp32 parameter tail
   const __nv_bfloat16* embed;
   const float* rope_cos;
   const float* rope_sin;
@@ -1327,6 +1328,13 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       const uint32_t ring_addr = smem_u32(ring);
       const uint32_t n_stage = (uint32_t)p.n_stage;
       const uint64_t pol = l2_evict_first_policy();  // weights are read once per step
+      if (!p.probe) {
+        // The fp32 gains / biases (a few hundred KB for the whole model) are needed on the critical path of
+        // every hop: bring them into L2 now, evict-last, one 128-byte line per SM in turn.
+        const char* fpb = reinterpret_cast<const char*>(p.fparams);
+        for (unsigned off = blockIdx.x * 128u; off < p.fp_bytes; off += gridDim.x * 128u)
+          asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(fpb + off));
+      }
       int lpos = 0;
       if (!p.probe) {
         lpos = __ldcg(p.positions);
@@ -1852,7 +1860,7 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
   p.tasks = h->d_tasks; p.sm_begin = h->d_sm_begin; p.sm_stream = h->d_sm_stream;
   p.wpacked = h->wpacked; p.fparams = h->fparams;
   p.fp_layer_stride = h->fp_layer_stride; p.fp_ln1 = h->fp_ln1; p.fp_ln2 = h->fp_ln2; p.fp_bias = h->fp_bias;
-  p.fp_qn = h->fp_qn; p.fp_kn = h->fp_kn; p.fp_final = h->fp_final;
+  p.fp_qn = h->fp_qn; p.fp_kn = h->fp_kn; p.fp_final = h->fp_final; p.fp_bytes = (unsigned)(h->fparam_floats * 4);
   p.embed = (const __nv_bfloat16*)h->w.embed; p.rope_cos = h->w.rope_cos; p.rope_sin = h->w.rope_sin;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   if (ws) {
