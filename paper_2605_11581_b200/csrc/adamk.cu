@@ -59,7 +59,7 @@ constexpr int kAttnWarps = 8;        // consumer warps that take part in an atte
 constexpr int kAttnChunksMax = 128;  // split-KV units per (sequence, kv head)
 constexpr int kGMax = 8;             // max q heads per kv head
 constexpr int kRW = 8;               // max rows per warp per tile
-constexpr int kGatherBatch = 8;      // 16-byte tagged-word loads a thread keeps in flight while gathering a vector
+constexpr int kGatherBatch = 4;      // 16-byte tagged-word loads a thread keeps in flight while gathering a vector
 constexpr int kMaxTP = 8;
 constexpr int kTagStride = 256;      // tag = epoch * kTagStride + layer + 1
 

@@ -30,13 +30,14 @@ C4 = dict(B, consumer_warps=4, rows_per_tile=32)
 C7 = dict(B, consumer_warps=7, attn_min_chunk=128)
 D7 = dict(C7, rows_per_tile=56, ktile_chunks=2, n_stage=3, l2_prefetch_kb=512)
 D7 = dict(C7, l2_prefetch_kb=512, attn_min_chunk=112)
+D7 = dict(C7, l2_prefetch_kb=512, attn_min_chunk=112, rows_per_tile=42, ktile_chunks=2, n_stage=4)
 scheds = [
-    ("c7 r56k2 s3", dict(D7, rows_per_tile=56, ktile_chunks=2, n_stage=3)),
-    ("c7 r42k2 s4", dict(D7, rows_per_tile=42, ktile_chunks=2, n_stage=4)),
-    ("c7 r42k1 s8", dict(D7, rows_per_tile=42, ktile_chunks=1, n_stage=8)),
-    ("c7 r28k3 s4", dict(D7, rows_per_tile=28, ktile_chunks=3, n_stage=4)),
-    ("c7 r28k2 s6", dict(D7, rows_per_tile=28, ktile_chunks=2, n_stage=6)),
-    ("c7 r42k3 s2", dict(D7, rows_per_tile=42, ktile_chunks=3, n_stage=2)),
+    ("c7 sl0", dict(D7)),
+    ("c7 sl50", dict(D7, poll_sleep_ns=50)),
+    ("c7 sl100", dict(D7, poll_sleep_ns=100)),
+    ("c7 sl200", dict(D7, poll_sleep_ns=200)),
+    ("c7 sl400", dict(D7, poll_sleep_ns=400)),
+    ("c7 sl800", dict(D7, poll_sleep_ns=800)),
 ]
 
 
