@@ -80,6 +80,7 @@ struct KParams {
   float eps;
   // schedule
   int C, n_stage, stage_bytes, attn_chunks, attn_min_chunk, scratch_bytes, n_lm_tasks, inflight;
+  int stream_down;         // 1: the down projection streams its input vector in k-tile by k-tile (down_streamed)
   int attn_block;          // positions per K / V block = 8 x attention warps: one pass of the unit's warps per block
   int pf_window_bytes;     // how far past the ring the Loader prefetches into L2 while it is blocked (0 = off)
   int task_cache_bytes;    // shared-memory copy of this SM's task list (32-byte packed records)
@@ -1181,7 +1182,7 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
 }
 
 // Flash-decoding merge of the split-KV records of one q head: out[d] = sum_s w_s o_s[d] / sum_s w_s l_s,
-// w_s = exp(m_s - M).  Thread d (< D) walks the active units with sixteen independent loads in flight.
+// w_s = exp(m_s - M).  Thread d (< D) walks the active units with eight independent loads in flight.
 __device__ __forceinline__ void run_merge(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, int pos) {
   if (p.probe) return;
   const AttnGeom ge = attn_geometry(p, pos, 0);
@@ -1194,13 +1195,13 @@ __device__ __forceinline__ void run_merge(const KParams& p, ConsumerCtx& c, cons
   if (c.ctid < D) {
     const int d = c.ctid;
     float M = -INFINITY, L = 0.f, O = 0.f;
-    for (int s0 = 0; s0 < ge.n_active; s0 += 8) {
-      u64 wo[8], wm[8], wl[8];
+    for (int s0 = 0; s0 < ge.n_active; s0 += 4) {
+      u64 wo[4], wm[4], wl[4];
       long long t0 = 0;
       for (;;) {
         bool ok = true;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 4; ++u) {
           if (s0 + u < ge.n_active) {
             const u64* rec = base + (size_t)(s0 + u) * cs;
             wo[u] = ll_load(rec + d);
@@ -1208,7 +1209,7 @@ __device__ __forceinline__ void run_merge(const KParams& p, ConsumerCtx& c, cons
           }
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < 4; ++u)
           if (s0 + u < ge.n_active) ok = ok && ll_tag(wo[u]) == tag && ll_tag(wm[u]) == tag && ll_tag(wl[u]) == tag;
         if (ok) break;
         if (p.poll_sleep_ns) __nanosleep(p.poll_sleep_ns);
@@ -1216,7 +1217,7 @@ __device__ __forceinline__ void run_merge(const KParams& p, ConsumerCtx& c, cons
         else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task_idx, (int)ll_tag(wo[0]), (int)tag, s0);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 4; ++u) {
         if (s0 + u < ge.n_active) {
           const float m = ll_val(wm[u]);
           const float Mn = fmaxf(M, m);
@@ -1268,6 +1269,139 @@ __device__ __noinline__ uint32_t run_gemv_nl(const KParams& p, GemvArgs g, float
   run_gemv<TP>(p, c, t, g.task_idx, xs, hdr, ring, g.tok, g.probe);
   return c.slot | (c.ph << 8);
 }
+// ---- down projection with its input streamed in ------------------------------------------------------
+// The down projection reads the longest vector of the layer (I = 8960 words = 72 KB of tagged words per SM
+// for Qwen2.5-1.5B: five dependent round trips when gathered up front).  Its k-tiles are consumed in order,
+// so the words of k-tile kt+1 are copied into shared memory with cp.async (no registers held) while k-tile
+// kt is multiplied (two slices in flight), then checked, converted to fp32 and staged in the other half of a
+// double buffer.  Only the first slice's round trip is exposed.
+// Scratch layout: xbuf[2][ktc * 256] fp32 | raw[2][ktc * 256] words.
+constexpr int kStreamBatch = 4;  // 16-byte word pairs per thread per k-tile
+
+__device__ __forceinline__ bool down_is_streamable(const KParams& p, const Task& t, int nct) {
+  const int WK = (t.geom >> 8) & 0xff;
+  return t.type == T_DOWN && WK == 1 && t.n_tiles == 1 && t.n_ktiles > 1 && t.ktc * (kChunk / 2) <= kStreamBatch * nct &&
+         t.ktc * kChunk * 24 <= p.scratch_bytes;
+}
+
+template <int RW, bool TP>
+__device__ __forceinline__ void down_streamed(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* scratch,
+                                              SmemHdr* hdr, uint8_t* ring, int tok) {
+  stamp(p, c, task_idx, 0);
+  const int rw = (t.geom >> 16) & 0xff;
+  const uint32_t ring_addr = smem_u32(ring) + c.lane * 16;
+  const uint32_t full0 = smem_u32(&hdr->full[0]), empty0 = smem_u32(&hdr->empty[0]);
+  const uint32_t n_stage = (uint32_t)p.n_stage, stage_bytes = (uint32_t)p.stage_bytes;
+  const int my_r0 = c.cw * rw;
+  const int rsel = ((c.lane >> 4) & 1) * 4 + ((c.lane >> 3) & 1) * 2 + ((c.lane >> 2) & 1);
+  const int rows = t.b;
+  const int my_n = max(0, min(rw, rows - my_r0));
+  int erow = -1;
+  if ((c.lane & 3) == 0 && rsel < my_n) erow = my_r0 + rsel;
+  float eop = 0.f;
+  if (erow >= 0) eop = load_eop<TP>(p, c, t, task_idx, t.a + erow, tok);   // residual: complete since this SM's gate/up task
+
+  const unsigned tag = tag_of(c, t.layer);
+  const u64* src = p.ll_act;
+  const int n2 = p.I >> 1;                       // 16-byte word pairs of the vector
+  const int wps = t.ktc * (kChunk / 2);          // word pairs per full k-tile
+  const int w_all = t.kchunks * (kChunk / 2);    // word pairs including the zero padding of the last chunk
+  float* xbuf = scratch;                         // [2][ktc * 256]
+  u64* raw = reinterpret_cast<u64*>(scratch + 2 * t.ktc * kChunk);
+  const uint32_t raw_addr = smem_u32(raw);
+  const int last = t.n_ktiles - 1;
+
+  auto issue_raw = [&](int kt) {                 // request this thread's word pairs of k-tile kt
+    const int wb = kt * wps, we = min(wb + wps, w_all);
+#pragma unroll
+    for (int u = 0; u < kStreamBatch; ++u) {
+      const int i = wb + c.ctid + u * c.nct;
+      if (i < we && i < n2)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(raw_addr + (uint32_t)((kt & 1) * wps + i - wb) * 16u), "l"(src + 2 * (size_t)i) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto finish_raw = [&](int kt) {                // check, convert, stage k-tile kt into xbuf[kt & 1]
+    const int wb = kt * wps, we = min(wb + wps, w_all);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");   // every group but the newest (slice kt + 1) has landed
+    float2* dst = reinterpret_cast<float2*>(xbuf + (size_t)(kt & 1) * t.ktc * kChunk);
+    const u64* rawk = raw + (size_t)(kt & 1) * 2 * wps;
+#pragma unroll
+    for (int u = 0; u < kStreamBatch; ++u) {
+      const int i = wb + c.ctid + u * c.nct;
+      if (i < we) {
+        float2 v = make_float2(0.f, 0.f);
+        if (i < n2) {
+          u64 a = rawk[2 * (i - wb)], b = rawk[2 * (i - wb) + 1];
+          if (ll_tag(a) != tag) a = ll_spin(p, src + 2 * (size_t)i, tag, task_idx);       // still old: poll the word itself
+          if (ll_tag(b) != tag) b = ll_spin(p, src + 2 * (size_t)i + 1, tag, task_idx);
+          v = make_float2(ll_val(a), ll_val(b));
+        }
+        dst[i - wb] = v;
+      }
+    }
+    consumer_sync(c.nct);
+  };
+
+  // first slice: wait until its first word is current before asking for the whole slice (the copy cannot re-poll)
+  if (c.ctid < min(wps, n2)) ll_spin(p, src + 2 * (size_t)c.ctid, tag, task_idx);
+  issue_raw(0);
+  issue_raw(1);
+  finish_raw(0);
+  issue_raw(2);   // (an empty group past the last k-tile keeps the wait_group arithmetic uniform)
+  stamp(p, c, task_idx, 1);
+
+  const int chunks_last = t.kchunks - last * t.ktc;
+  const uint32_t rs_full = (uint32_t)t.ktc * 512u, rs_last = (uint32_t)chunks_last * 512u;
+  float2 acc[kRW];
+#pragma unroll
+  for (int i = 0; i < kRW; ++i) acc[i] = make_float2(0.f, 0.f);
+  uint32_t slot = c.slot, ph = c.ph;
+#pragma unroll 1
+  for (int kt = 0; kt <= last; ++kt) {
+    mbar_wait(p, full0 + slot * 8, ph, DE_WATCHDOG_FULL, task_idx);
+    if (my_n > 0) {
+      const bool is_last = kt == last;
+      const uint32_t rs = is_last ? rs_last : rs_full;
+      gemv_stage<RW>(ring_addr + slot * stage_bytes + (uint32_t)my_r0 * rs, rs,
+                     smem_u32(xbuf + (size_t)(kt & 1) * t.ktc * kChunk) + c.lane * 16, is_last ? chunks_last : t.ktc, 1, acc);
+    }
+    __syncwarp();
+    if (c.lane == 0) mbar_arrive(empty0 + slot * 8);
+    if (++slot == n_stage) { slot = 0; ph ^= 1u; }
+    if (kt < last) {
+      finish_raw(kt + 1);
+      issue_raw(kt + 3);
+    }
+  }
+  c.slot = slot; c.ph = ph;
+  float v[kRW];
+#pragma unroll
+  for (int i = 0; i < kRW; ++i) v[i] = acc[i].x + acc[i].y;
+  const float sres = reduce8(v, c.lane);
+  if (erow >= 0) gemv_epilogue<TP>(p, c, t, t.a + erow, sres, 0.f, eop);
+  stamp(p, c, task_idx, 2);
+  consumer_sync(c.nct);   // the next task overwrites the scratch region
+  stamp(p, c, task_idx, 7);
+}
+
+template <bool TP>
+__device__ __noinline__ uint32_t run_down_streamed_nl(const KParams& p, GemvArgs g, float* xs, SmemHdr* hdr, uint8_t* ring) {
+  ConsumerCtx c;
+  c.cw = g.cw; c.lane = g.lane; c.ctid = g.ctid; c.nct = g.nct; c.epoch = g.epoch; c.slot = g.slot; c.ph = g.ph;
+  c.rs = 1.f; c.best_val = -INFINITY; c.best_idx = -1;
+  Task t{};
+  t.type = g.type; t.layer = g.layer; t.a = g.a; t.b = g.b; t.k = g.k; t.kchunks = g.kchunks; t.rt = g.rt; t.ktc = g.ktc;
+  t.n_tiles = g.n_tiles; t.n_ktiles = g.n_ktiles; t.geom = g.geom;
+  switch ((((t.geom >> 16) & 0xff) + 1) >> 1) {
+    case 1: down_streamed<2, TP>(p, c, t, g.task_idx, xs, hdr, ring, g.tok); break;
+    case 2: down_streamed<4, TP>(p, c, t, g.task_idx, xs, hdr, ring, g.tok); break;
+    case 3: down_streamed<6, TP>(p, c, t, g.task_idx, xs, hdr, ring, g.tok); break;
+    default: down_streamed<8, TP>(p, c, t, g.task_idx, xs, hdr, ring, g.tok); break;
+  }
+  return c.slot | (c.ph << 8);
+}
+
 __device__ __noinline__ void run_merge_nl(const KParams& p, WarpArgs w) {
   ConsumerCtx c;
   c.cw = w.cw; c.lane = w.lane; c.ctid = w.ctid; c.nct = w.nct; c.epoch = w.epoch; c.slot = w.slot; c.ph = w.ph;
@@ -1447,7 +1581,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       g.cw = c.cw; g.lane = c.lane; g.ctid = c.ctid; g.nct = c.nct; g.epoch = c.epoch; g.slot = c.slot; g.ph = c.ph;
       g.type = t.type; g.layer = t.layer; g.a = t.a; g.b = t.b; g.k = t.k; g.kchunks = t.kchunks; g.rt = t.rt; g.ktc = t.ktc;
       g.n_tiles = t.n_tiles; g.n_ktiles = t.n_ktiles; g.geom = t.geom; g.task_idx = ti; g.tok = tok; g.probe = probe;
-      const uint32_t sp = run_gemv_nl<TP>(p, g, scratch, hdr, ring);
+      const uint32_t sp = (!probe && p.stream_down && down_is_streamable(p, t, c.nct)) ? run_down_streamed_nl<TP>(p, g, scratch, hdr, ring)
+                                                                                       : run_gemv_nl<TP>(p, g, scratch, hdr, ring);
       c.slot = sp & 0xffu; c.ph = sp >> 8;
     }
   }
@@ -1565,6 +1700,7 @@ struct AdamkHandle_ {
   const uint8_t* wpacked = nullptr;
   const float* fparams = nullptr;
   AdamkWeightPtrs w{};
+  int stream_down = 1;
   int tp_rank = 0, tp_size = 1;
   void* peer_ws[kMaxTP] = {nullptr};
   bool peers_bound = false;
@@ -1605,7 +1741,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   h->tp_rank = tp_rank; h->tp_size = tp_size;
   h->n_sms = tt[2]; h->C = tt[3]; h->n_stage = tt[4]; h->stage_bytes = tt[5]; h->n_tasks = tt[6]; h->batch = tt[7];
   h->inflight = tt[8]; h->attn_chunks = tt[9]; h->attn_min_chunk = tt[10]; h->scratch_bytes = tt[11];
-  h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14]; h->pf_window_kb = tt[15];
+  h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14] & 0xffff; h->stream_down = !((tt[14] >> 16) & 1); h->pf_window_kb = tt[15];
   auto bad = [&](const std::string& m) { delete h; return fail(ADAMK_E_INVALID, m); };
   const AdamkModelDesc& d = *desc;
   if (d.head_dim != 64 && d.head_dim != 128) return bad("head_dim must be 64 or 128");
@@ -1856,6 +1992,7 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
   p.attn_min_chunk = h->attn_min_chunk; p.scratch_bytes = h->scratch_bytes; p.n_lm_tasks = h->n_lm_tasks;
   p.task_cache_bytes = h->task_cache_bytes; p.pf_window_bytes = h->pf_window_kb * 1024;
   p.attn_block = 8 * std::min(h->C, kAttnWarps);
+  p.stream_down = h->stream_down;
   p.inflight = h->inflight; p.poll_sleep_ns = (unsigned)h->poll_sleep_ns;
   p.tasks = h->d_tasks; p.sm_begin = h->d_sm_begin; p.sm_stream = h->d_sm_stream;
   p.wpacked = h->wpacked; p.fparams = h->fparams;

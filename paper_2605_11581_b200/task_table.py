@@ -79,6 +79,7 @@ class KernelSchedule:
     inflight: int = 0         # ring stages the Loader keeps in flight at most (0 = all free slots)
     poll_sleep_ns: int = 0    # back-off between polls of an incomplete activation vector
     l2_prefetch_kb: int = 0   # per-SM window past the ring the Loader prefetches into L2 while it is blocked
+    stream_down: bool = True  # the down projection streams its input vector in k-tile by k-tile (cp.async) instead of gathering it up front
 
     def __post_init__(self) -> None:
         if self.consumer_warps not in (4, 7, 8, 16):
@@ -131,7 +132,13 @@ def scratch_bytes(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> in
     x_bytes = batch * kpad_max * 4
     d = cfg.head_dim
     attn_bytes = ((d + 16) + 2 * d + ATTN_WARPS * (d + 2) + ATTN_WARPS) * 4
-    return _ceil_div(max(x_bytes, attn_bytes), 1024) * 1024
+    # streamed down projection (csrc: down_streamed): two fp32 slices + two raw tagged-word slices of one k-tile
+    stream_bytes = 0
+    if sched.stream_down and batch == 1:
+        _, wk, _, ktc = op_geometry(sched, _ceil_div(cfg.hidden, 148), _ceil_div(cfg.intermediate, KCHUNK), False)
+        if wk == 1 and ktc * KCHUNK * 24 <= x_bytes + 8192:
+            stream_bytes = ktc * KCHUNK * 24
+    return _ceil_div(max(x_bytes, attn_bytes, stream_bytes), 1024) * 1024
 
 
 def task_cache_bytes(cfg: ModelConfig, batch: int = 1, n_sms: int = 148) -> int:
@@ -368,7 +375,7 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
                    tasks.shape[0], batch, sched.inflight, attn_chunks, sched.attn_min_chunk,
                    scratch_bytes(cfg, sched, batch), n_lm]
     header[13] = (cursor // 16) & 0x7FFFFFFF
-    header[14] = sched.poll_sleep_ns
+    header[14] = (sched.poll_sleep_ns & 0xFFFF) | ((0 if sched.stream_down else 1) << 16)
     header[15] = sched.l2_prefetch_kb
     return TaskTable(cfg=cfg, sched=sched, n_sms=n_sms, batch=batch, header=header, sm_begin=sm_begin,
                      tasks=tasks, packed_weight_bytes=cursor, attn_chunks=attn_chunks)

@@ -32,12 +32,8 @@ D7 = dict(C7, rows_per_tile=56, ktile_chunks=2, n_stage=3, l2_prefetch_kb=512)
 D7 = dict(C7, l2_prefetch_kb=512, attn_min_chunk=112)
 D7 = dict(C7, l2_prefetch_kb=512, attn_min_chunk=112, rows_per_tile=42, ktile_chunks=2, n_stage=4)
 scheds = [
-    ("c7 sl0", dict(D7)),
-    ("c7 sl50", dict(D7, poll_sleep_ns=50)),
-    ("c7 sl100", dict(D7, poll_sleep_ns=100)),
-    ("c7 sl200", dict(D7, poll_sleep_ns=200)),
-    ("c7 sl400", dict(D7, poll_sleep_ns=400)),
-    ("c7 sl800", dict(D7, poll_sleep_ns=800)),
+    ("c7 stream", dict(D7)),
+    ("c7 nostream", dict(D7, stream_down=False)),
 ]
 
 
