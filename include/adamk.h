@@ -107,6 +107,13 @@ size_t adamk_packed_bytes(adamk_handle h);
  * the stream has drained, except `embed`. */
 int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, adamk_stream stream);
 
+/* Let `h` stream the packed weights another handle already bound (no repacking, no second copy in HBM).
+ * Both handles must have been created from identical task tables.  Used by the batch lanes of
+ * plugin.BatchLanes: B instances of the kernel on disjoint SM subsets, one sequence each, reading ONE
+ * packed stream (the second reader of a stage hits L2).  `w` supplies embed / rope pointers as in
+ * adamk_bind_weights (`layers` is not read). */
+int adamk_share_weights(adamk_handle h, adamk_handle owner, const AdamkWeightPtrs* w);
+
 /* Tensor parallelism only (tp_size > 1 at adamk_create; `desc` then holds the
  * rank's shard: n_q_heads, n_kv_heads, intermediate and vocab divided by
  * tp_size): base pointers of EVERY rank's workspace as seen from this GPU

@@ -1809,7 +1809,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
     if (t.a < 0 || t.b < 1 || t.a + t.b > n_rows) return bad("task rows out of range");
     const int WR = t.geom & 0xff, WK = (t.geom >> 8) & 0xff, rw = (t.geom >> 16) & 0xff;
     if (WR < 1 || WK < 1 || WR * WK != h->C) return bad("warp grid WR x WK must equal consumer_warps");
-    if (rw < 1 || rw > kRW || t.rt != WR * rw) return bad("rows per warp out of range / rows_per_tile != WR * rw");
+    if (rw < 2 || rw > kRW || (rw & 1) || t.rt != WR * rw) return bad("rows per warp must be 2, 4, 6 or 8 and rows_per_tile == WR * rw");
     if (WK > 1 && t.rt > 32) return bad("K-split tiles hold at most 32 rows");
     if (t.type == T_GATEUP && ((t.a | t.b | rw) & 1)) return bad("gate/up rows must come in pairs");
     if (t.ktc < 1 || t.n_ktiles != (t.kchunks + t.ktc - 1) / t.ktc || t.n_tiles != (t.b + t.rt - 1) / t.rt)
@@ -1964,6 +1964,21 @@ int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, a
   h->w.layers = nullptr;
   h->wpacked = static_cast<const uint8_t*>(packed);
   h->fparams = fp;
+  h->bound = true;
+  return ADAMK_OK;
+}
+
+int adamk_share_weights(adamk_handle h, adamk_handle owner, const AdamkWeightPtrs* w) {
+  if (!h || !owner || !w) return fail(ADAMK_E_INVALID, "NULL argument");
+  if (!owner->bound) return fail(ADAMK_E_STATE, "the owner handle has no weights bound");
+  // identical task tables <=> identical packed layout
+  if (h->host_table != owner->host_table || h->packed_weight_bytes != owner->packed_weight_bytes ||
+      h->fparam_floats != owner->fparam_floats)
+    return fail(ADAMK_E_INVALID, "handles must be built from identical task tables to share packed weights");
+  h->w = *w;
+  h->w.layers = nullptr;
+  h->wpacked = owner->wpacked;
+  h->fparams = owner->fparams;
   h->bound = true;
   return ADAMK_OK;
 }

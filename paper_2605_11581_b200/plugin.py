@@ -55,7 +55,7 @@ EXPORTS = (
     "adamk_abi_version", "adamk_device_sm_count", "adamk_last_error", "adamk_create", "adamk_destroy",
     "adamk_packed_bytes", "adamk_bind_weights", "adamk_bind_peers", "adamk_workspace_bytes",
     "adamk_workspace_init", "adamk_kv_cache_bytes", "adamk_decode_step", "adamk_device_status",
-    "adamk_stream_probe", "adamk_trace_bytes", "adamk_set_trace",
+    "adamk_stream_probe", "adamk_trace_bytes", "adamk_set_trace", "adamk_share_weights",
 )
 
 _lib = None
@@ -87,6 +87,7 @@ def load_library() -> C.CDLL:
         getattr(lib, name).restype = C.c_size_t
     lib.adamk_bind_weights.argtypes = [C.c_void_p, C.POINTER(_WeightPtrs), C.c_void_p, C.c_void_p]
     lib.adamk_bind_peers.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_int]
+    lib.adamk_share_weights.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_WeightPtrs)]
     lib.adamk_workspace_init.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     lib.adamk_decode_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
@@ -182,6 +183,14 @@ class MegaKernelPlugin:
         self._embed = w.embed                      # the kernel gathers embedding rows from the source table
         self._weights = w if keep_source else None
 
+    def share_weights(self, owner: "MegaKernelPlugin") -> None:
+        """Stream the packed weights ``owner`` has bound (identical task table required) instead of repacking."""
+        assert owner.packed is not None
+        self._rope = owner._rope
+        ptrs = _WeightPtrs(owner._embed.data_ptr(), None, None, None, self._rope[0].data_ptr(), self._rope[1].data_ptr())
+        _check(self.lib, self.lib.adamk_share_weights(self._h, owner._h, C.byref(ptrs)))
+        self.packed, self._embed = owner.packed, owner._embed
+
     def bind_peers(self, peer_workspaces) -> None:
         """Tensor parallelism: device pointers (or tensors) of EVERY rank's workspace, own rank included, in rank
         order.  On one node these are peer-mapped allocations (CUDA IPC / cuMem handles exchanged once through
@@ -256,3 +265,63 @@ class MegaKernelPlugin:
             self.close()
         except Exception:
             pass
+
+
+class BatchLanes:
+    """Batched decode by SM partitioning: ``batch`` instances of the batch-1 kernel on disjoint SM subsets
+    (n_sms // batch each), one sequence per lane, all streaming ONE packed weight buffer.  The lanes start
+    together and do identical work, so the second reader of a weight stage finds it in L2 and HBM still sees
+    each weight once per step; correctness is that of the batch-1 kernel by construction.  (SURVEY.md 8(f).1's
+    tensor-core path for batch >= 8 is a separate kernel and not built yet; this is the CUDA-core path for
+    small batches.)"""
+
+    def __init__(self, cfg: ModelConfig, schedule: KernelSchedule, max_ctx: int, batch: int, device: int = 0):
+        total = device_sm_count(device)
+        self.batch = int(batch)
+        self.lanes = [MegaKernelPlugin(cfg, schedule, max_ctx, device=device, n_sms=total // self.batch)
+                      for _ in range(self.batch)]
+        self.device = self.lanes[0].device
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(self.batch)]
+        self._fork = torch.cuda.Event()
+        self._joins = [torch.cuda.Event() for _ in range(self.batch)]
+
+    def bind_weights(self, w: DecoderWeights) -> None:
+        self.lanes[0].bind_weights(w)
+        for lane in self.lanes[1:]:
+            lane.share_weights(self.lanes[0])
+
+    def set_state(self, tokens, positions) -> None:
+        for lane, t, p in zip(self.lanes, tokens, positions):
+            lane.set_state(int(t), int(p))
+
+    def enqueue(self, want_logits: bool = False, auto_advance: bool = True) -> None:
+        """One decode step of every sequence: the lanes' kernels run concurrently, forked from and joined
+        back into the current stream."""
+        cur = torch.cuda.current_stream(self.device)
+        self._fork.record(cur)
+        for lane, st, ev in zip(self.lanes, self.streams, self._joins):
+            st.wait_event(self._fork)
+            with torch.cuda.stream(st):
+                lane.enqueue(want_logits=want_logits, auto_advance=auto_advance)
+                ev.record(st)
+        for ev in self._joins:
+            cur.wait_event(ev)
+
+    def decode_step(self, tokens, positions, want_logits: bool = True) -> StepOutput:
+        self.set_state(tokens, positions)
+        self.enqueue(want_logits=want_logits, auto_advance=False)
+        nxt = torch.cat([lane.next_token for lane in self.lanes])
+        logits = torch.cat([lane.logits for lane in self.lanes]) if want_logits else None
+        return StepOutput(nxt, logits)
+
+    def check(self) -> None:
+        for lane in self.lanes:
+            lane.check()
+
+    @property
+    def launches(self) -> int:
+        return sum(lane.launches for lane in self.lanes)
+
+    def close(self) -> None:
+        for lane in self.lanes:
+            lane.close()

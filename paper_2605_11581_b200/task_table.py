@@ -186,7 +186,7 @@ def op_geometry(sched: KernelSchedule, max_rows: int, kchunks: int, pairs: bool)
         # padding (122 gate/up rows on 7 warps: three 56-row tiles are 73 % full, three 42-row tiles 97 %)
         best_rw, best_pad = sched.rows_per_warp, None
         for rw in range(sched.rows_per_warp, 0, -1):
-            if pairs and rw & 1:
+            if rw & 1:
                 continue
             rt = c * rw
             n_t = _ceil_div(max_rows, rt)
@@ -211,8 +211,8 @@ def op_geometry(sched: KernelSchedule, max_rows: int, kchunks: int, pairs: bool)
             continue
         wr = c // wk
         rw = _ceil_div(max_rows, wr)
-        if pairs:
-            rw += rw & 1
+        rw += rw & 1     # the kernel's row loops are instantiated for 2, 4, 6, 8 rows per warp: keep rt = WR * rw honest
+                         # about the rows a warp touches (and gate/up pairs inside one warp)
         rt = wr * rw
         if rw <= MAX_RW and (wk == 1 or rt <= 32):
             ktc_max = min(kchunks, sched.stage_bytes // (rt * KCHUNK * 2))

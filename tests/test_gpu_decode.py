@@ -264,3 +264,38 @@ def test_tp_requires_peers():
     with pytest.raises(AdamkError):          # peer list of the wrong length
         plug.bind_peers([plug.workspace])
     plug.close()
+
+
+@pytest.mark.parametrize("batch", [2, 4])
+def test_batch_lanes_match_oracle(batch):
+    """BASELINE.json configs[2] (batch sweep), CUDA-core path: `batch` sequences at different positions, each on
+    its own SM partition, all streaming one packed weight buffer; per-sequence logits / tokens vs the oracle."""
+    from oracle.decode_ref import RefDecoder
+    from paper_2605_11581_b200.plugin import BatchLanes
+    from paper_2605_11581_b200.weights import random_weights, rope_table
+
+    cfg = D128_Q3
+    w = random_weights(cfg, seed=0)
+    cos, sin = rope_table(cfg, 128)
+    refs = [RefDecoder(cfg, w, 128, cos, sin) for _ in range(batch)]
+    lanes = BatchLanes(cfg, SCHEDS["c7"], max_ctx=128, batch=batch)
+    lanes.bind_weights(w)
+    assert all(lane.packed.data_ptr() == lanes.lanes[0].packed.data_ptr() for lane in lanes.lanes)
+    g = torch.Generator().manual_seed(9)
+    # sequence b starts b * 3 tokens later: the lanes run at different positions in the same step
+    seqs = [torch.randint(0, cfg.vocab, (20,), generator=g).tolist() for _ in range(batch)]
+    pos = [0] * batch
+    for step in range(20 + 3 * (batch - 1)):
+        live = [b for b in range(batch) if 0 <= step - 3 * b < 20]
+        toks = [seqs[b][step - 3 * b] if b in live else 0 for b in range(batch)]
+        # idle lanes re-run position 0 with token 0 (harmless: their cache row 0 is rewritten when they go live)
+        out = lanes.decode_step(toks, [pos[b] if b in live else 0 for b in range(batch)])
+        lanes.check()
+        for b in live:
+            want = refs[b].step([toks[b]], [pos[b]])[0].numpy()
+            got = out.logits[b].cpu().numpy()
+            assert np.abs(got - want).max() <= 2e-3, (step, b)
+            if np.sort(want)[-1] - np.sort(want)[-2] > 1e-2:
+                assert int(out.next_token[b].item()) == int(want.argmax())
+            pos[b] += 1
+    lanes.close()
