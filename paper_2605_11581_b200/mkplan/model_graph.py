@@ -41,16 +41,16 @@ def build_layer_graph(cfg: ModelConfig, ctx: int, *, rows: int = 16, m: int = 1,
         return "SharedPage" if act(cols) <= wide_pages * page_bytes else "Global"
 
     buffers = [
-        ("x", "SharedPage", act(h)), ("g1", "Global", h * _ELEM), ("xn", "SharedPage", act(h)),
+        ("x", space(h), act(h)), ("g1", "Global", h * _ELEM), ("xn", space(h), act(h)),
         ("wqkv", "Global", qkv * h * _ELEM), ("qkv", space(qkv), act(qkv)),
         ("kcache", "Global", cfg.n_kv_heads * ctx * d * _ELEM),
         ("scores", space(cfg.n_q_heads * ctx), act(cfg.n_q_heads * ctx)),
         ("probs", space(cfg.n_q_heads * ctx), act(cfg.n_q_heads * ctx)),
         ("vcache", "Global", cfg.n_kv_heads * ctx * d * _ELEM),
-        ("attn", space(q_dim), act(q_dim)), ("wo", "Global", h * q_dim * _ELEM), ("o", "SharedPage", act(h)),
-        ("h1", "SharedPage", act(h)), ("g2", "Global", h * _ELEM), ("h1n", "SharedPage", act(h)),
+        ("attn", space(q_dim), act(q_dim)), ("wo", "Global", h * q_dim * _ELEM), ("o", space(h), act(h)),
+        ("h1", space(h), act(h)), ("g2", "Global", h * _ELEM), ("h1n", space(h), act(h)),
         ("wug", "Global", 2 * i * h * _ELEM), ("ug", space(2 * i), act(2 * i)), ("act", space(i), act(i)),
-        ("wd", "Global", h * i * _ELEM), ("d", "SharedPage", act(h)), ("y", "Global", act(h)),
+        ("wd", "Global", h * i * _ELEM), ("d", space(h), act(h)), ("y", "Global", act(h)),
     ]
 
     def op(op_id, kind, n, k, inputs, outputs, weight=None, quant=False):
@@ -72,7 +72,7 @@ def build_layer_graph(cfg: ModelConfig, ctx: int, *, rows: int = 16, m: int = 1,
         op("res2", "ResidualAdd", h, 0, ["d", "h1"], ["y"]),
     ]
     if lm_head:
-        buffers += [("gf", "Global", h * _ELEM), ("yn", "SharedPage", act(h)),
+        buffers += [("gf", "Global", h * _ELEM), ("yn", space(h), act(h)),
                     ("wlm", "Global", cfg.vocab * h * _ELEM), ("logits", "Global", act(cfg.vocab))]
         operators += [op("normf", "RmsNorm", h, 0, ["y"], ["yn"], "gf"),
                       op("lm_head", "LmHead", cfg.vocab, h, ["yn"], ["logits"], "wlm", quant=True)]
@@ -81,3 +81,30 @@ def build_layer_graph(cfg: ModelConfig, ctx: int, *, rows: int = 16, m: int = 1,
 
 def layer_graph_json(cfg: ModelConfig, ctx: int, **kw) -> str:
     return json.dumps(build_layer_graph(cfg, ctx, **kw), indent=1) + "\n"
+
+
+def build_sm_slice_graph(cfg: ModelConfig, ctx: int, n_sms: int = 148, **kw) -> dict:
+    """The share of one decoder layer that ONE SM executes in the decode MegaKernel: every GEMM keeps its full
+    reduction dimension and 1/n_sms of its output rows (task_table.split_rows), attention covers one
+    (q head, context chunk) unit.  The reference's planner models a single-SM pipeline ("no
+    cross-SM/block scheduling"), so this -- not the whole layer -- is the graph whose schedule the kernel
+    replays on each of its CTAs."""
+    from dataclasses import replace
+
+    def up(a: int, b: int) -> int:
+        return -(-a // b)
+
+    g = build_layer_graph(cfg, ctx, **kw)
+    rows = {"qkv": up(cfg.qkv_rows, n_sms), "oproj": up(cfg.hidden, n_sms), "upgate": 2 * up(cfg.intermediate, n_sms),
+            "down": up(cfg.hidden, n_sms)}
+    chunk = max(8, up(ctx, max(1, n_sms // cfg.n_q_heads)))
+    by_id = {o["id"]: o for o in g["operators"]}
+    for oid, n in rows.items():
+        by_id[oid]["dims"]["n"] = n
+    by_id["swiglu"]["dims"]["n"] = rows["upgate"] // 2
+    by_id["down"]["dims"]["k"] = cfg.intermediate
+    by_id["qk"]["dims"]["n"] = chunk
+    by_id["softmax"]["dims"]["n"] = chunk
+    by_id["pv"]["dims"]["k"] = chunk
+    del replace
+    return g

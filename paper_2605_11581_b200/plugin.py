@@ -160,6 +160,20 @@ class MegaKernelPlugin:
         self.logits = torch.zeros(1, cfg.vocab * self.tp_size, dtype=torch.float32, device=self.device)
         self.launches = 0
 
+    @classmethod
+    def from_trace(cls, cfg: ModelConfig, trace_text, max_ctx: int, device: int | str = 0, **schedule_overrides):
+        """Build the plugin from a SolidifiedTrace (``mkplan search --out``; reference ``search.py:79-107``): the
+        plan's tile, ring depth and consumer-warp count become the kernel schedule (KernelSchedule.from_plan);
+        run-time knobs the planner does not model (split-KV chunk, L2 prefetch window) come as overrides."""
+        from .mkplan.search import parse_trace
+
+        trace = parse_trace(trace_text if isinstance(trace_text, (bytes, bytearray)) else str(trace_text).encode())
+        sched = KernelSchedule.from_plan(trace.plan, **schedule_overrides)
+        fit = __import__("paper_2605_11581_b200.task_table", fromlist=["max_stages_that_fit"]).max_stages_that_fit(cfg, sched)
+        if sched.n_stage > fit:
+            sched = KernelSchedule.from_plan(trace.plan, **dict(schedule_overrides, n_stage=max(2, fit)))
+        return cls(cfg, sched, max_ctx, device=device)
+
     # -- weights -------------------------------------------------------------
     def bind_weights(self, w: DecoderWeights, keep_source: bool = False) -> None:
         """Repack HF-layout bf16 weights into the per-SM tile-major streams."""

@@ -119,8 +119,12 @@ class KernelSchedule:
         sub_k = bk // ks
         if sub_k % KCHUNK:
             raise ScheduleError(f"sub_k={sub_k} is not a multiple of {KCHUNK}")
-        kw = dict(consumer_warps=int(plan["consumer_warps"]), n_stage=int(plan["n_stage"]),
-                  rows_per_tile=int(bn), ktile_chunks=sub_k // KCHUNK)
+        c = int(plan["consumer_warps"])
+        # a plan tile taller than the kernel's eight rows per warp is executed as several kernel tiles
+        rows = int(bn)
+        while rows > MAX_RW * c:
+            rows //= 2
+        kw = dict(consumer_warps=c, n_stage=int(plan["n_stage"]), rows_per_tile=rows, ktile_chunks=sub_k // KCHUNK)
         kw.update(overrides)
         return cls(**kw)
 

@@ -299,3 +299,33 @@ def test_batch_lanes_match_oracle(batch):
                 assert int(out.next_token[b].item()) == int(want.argmax())
             pos[b] += 1
     lanes.close()
+
+
+def test_plugin_from_searched_trace_matches_oracle():
+    """The drop-in flow end to end: mkplan search (SM-slice graph, b200.json) -> SolidifiedTrace bytes ->
+    MegaKernelPlugin.from_trace -> decode steps that match the oracle."""
+    import json
+    from pathlib import Path
+
+    from oracle.decode_ref import RefDecoder
+    from paper_2605_11581_b200.mkplan import model_graph, search
+    from paper_2605_11581_b200.plugin import MegaKernelPlugin
+    from paper_2605_11581_b200.weights import random_weights, rope_table
+
+    cfg = TINY
+    graph = model_graph.build_sm_slice_graph(cfg, 64, n_sms=148)
+    hw = (Path(tt.__file__).parent / "mkplan" / "fixtures" / "b200.json").read_text()
+    space = {"block_m": [16], "block_n": [16, 32], "block_k": [256], "k_split": [1], "consumer_warps": [4, 8],
+             "n_stage": [2, 3], "prefetch_stride": [1], "swizzles": [31]}
+    text = search.serialize_trace(search.run_search(json.dumps(graph), hw, json.dumps(space), 100))
+    plug = MegaKernelPlugin.from_trace(cfg, text, max_ctx=64, attn_min_chunk=16)
+    w = random_weights(cfg, seed=0)
+    plug.bind_weights(w)
+    cos, sin = rope_table(cfg, 64)
+    ref = RefDecoder(cfg, w, 64, cos, sin)
+    for pos, tok in enumerate([7, 300, 12, 999, 4, 4, 250, 31]):
+        want = ref.step([tok], [pos])[0].numpy()
+        got = plug.decode_step(tok, pos).logits[0].cpu().numpy()
+        plug.check()
+        assert np.abs(got - want).max() <= 2e-3
+    plug.close()

@@ -248,3 +248,33 @@ def test_cabi_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert lib.adamk_abi_version() == plugin.ABI_VERSION
+
+
+def test_search_to_schedule_to_task_table():
+    """Offline half -> online half: the planner's search on the share of a layer one SM executes
+    (mkplan.model_graph.build_sm_slice_graph) yields a SolidifiedTrace whose plan lowers to a kernel schedule
+    and a task table (the flow of PAPER.md:195-197: search, solidify, replay)."""
+    import json
+    from pathlib import Path
+
+    from paper_2605_11581_b200.mkplan import model_graph, search
+
+    cfg = TINY
+    graph = model_graph.build_sm_slice_graph(cfg, 64, n_sms=148)
+    ops = {o["id"]: o["dims"] for o in graph["operators"]}
+    assert ops["qkv"]["n"] == -(-cfg.qkv_rows // 148) and ops["qkv"]["k"] == cfg.hidden
+    assert ops["upgate"]["n"] == 2 * -(-cfg.intermediate // 148) and ops["down"]["k"] == cfg.intermediate
+    hw = (Path(tt.__file__).parent / "mkplan" / "fixtures" / "b200.json").read_text()
+    space = {"block_m": [16], "block_n": [16, 32], "block_k": [256], "k_split": [1], "consumer_warps": [4, 8],
+             "n_stage": [2, 3], "prefetch_stride": [1], "swizzles": [31]}
+    trace = search.run_search(json.dumps(graph), hw, json.dumps(space), 100)
+    again = search.parse_trace(search.serialize_trace(trace))
+    assert again.plan == trace.plan
+    sched = tt.KernelSchedule.from_plan(trace.plan, attn_min_chunk=16)
+    assert sched.consumer_warps == trace.plan["consumer_warps"] and sched.n_stage == trace.plan["n_stage"]
+    assert sched.rows_per_tile <= tt.MAX_RW * sched.consumer_warps and sched.ktile_chunks == 1
+    table = tt.build_task_table(cfg, sched, n_sms=148)
+    _simulate_dataflow(table, 40)
+    # a plan tile taller than eight rows per warp is split into several kernel tiles
+    tall = tt.KernelSchedule.from_plan({"tile": [16, 64, 512, 2], "n_stage": 3, "consumer_warps": 4})
+    assert (tall.rows_per_tile, tall.ktile_chunks) == (32, 1)
