@@ -36,4 +36,6 @@ def default_schedule(cfg: ModelConfig) -> KernelSchedule:
             sched = KernelSchedule.from_plan(plan, n_stage=fit)
         return sched
     probe = KernelSchedule(n_stage=2, **PROFILED_DEFAULT)
-    return KernelSchedule(n_stage=max(2, min(max_stages_that_fit(cfg, probe), 8)), **PROFILED_DEFAULT)
+    n_stage = max(2, min(max_stages_that_fit(cfg, probe), 8))
+    # at most three stages in flight: a fourth only lengthens the queue every tagged-word poll waits behind
+    return KernelSchedule(n_stage=n_stage, inflight=min(3, n_stage), **PROFILED_DEFAULT)

@@ -31,9 +31,15 @@ C7 = dict(B, consumer_warps=7, attn_min_chunk=128)
 D7 = dict(C7, rows_per_tile=56, ktile_chunks=2, n_stage=3, l2_prefetch_kb=512)
 D7 = dict(C7, l2_prefetch_kb=512, attn_min_chunk=112)
 D7 = dict(C7, l2_prefetch_kb=512, attn_min_chunk=112, rows_per_tile=42, ktile_chunks=2, n_stage=4)
+D7 = dict(consumer_warps=7, rows_per_tile=42, ktile_chunks=2, n_stage=4, attn_min_chunk=112, l2_prefetch_kb=512)
 scheds = [
-    ("c7 stream", dict(D7)),
-    ("c7 nostream", dict(D7, stream_down=False)),
+    ("base", dict(D7)),
+    ("if3", dict(D7, inflight=3)),
+    ("if2", dict(D7, inflight=2)),
+    ("pf1024", dict(D7, l2_prefetch_kb=1024)),
+    ("if3 pf1024", dict(D7, inflight=3, l2_prefetch_kb=1024)),
+    ("if3 pf1024 mc168", dict(D7, inflight=3, l2_prefetch_kb=1024, attn_min_chunk=168)),
+    ("if3 pf2048", dict(D7, inflight=3, l2_prefetch_kb=2048)),
 ]
 
 
