@@ -28,6 +28,13 @@ SCHEDS = {
     # the profiled default shape (7 consumer warps + Loader = 8 warps, 56 KB slots) with L2 prefetch and an in-flight cap
     "c7": tt.KernelSchedule(consumer_warps=7, n_stage=3, rows_per_tile=56, ktile_chunks=2, attn_min_chunk=16,
                             l2_prefetch_kb=64, inflight=2),
+    # small ring slots: the down projection spans several k-tiles, so its input vector is streamed in with
+    # cp.async (down_streamed), including a zero-padded last chunk for the tiny models (I = 704)
+    "c7s": tt.KernelSchedule(consumer_warps=7, n_stage=6, rows_per_tile=14, ktile_chunks=1, attn_min_chunk=16),
+    "c7m": tt.KernelSchedule(consumer_warps=7, n_stage=6, rows_per_tile=28, ktile_chunks=1, attn_min_chunk=16,
+                             l2_prefetch_kb=32),
+    "c7m_nostream": tt.KernelSchedule(consumer_warps=7, n_stage=6, rows_per_tile=28, ktile_chunks=1, attn_min_chunk=16,
+                                      stream_down=False),
 }
 
 
@@ -49,7 +56,9 @@ def _cos(a, b):
 
 
 @pytest.mark.parametrize("cfg,sname", [(TINY, "c8"), (TINY_QWEN3, "c8"), (D128, "c8"), (D128_Q3, "c8"),
-                                       (TINY, "c4"), (D128, "c16"), (D128, "c7"), (D128_Q3, "c7"), (TINY_QWEN3, "c7")],
+                                       (TINY, "c4"), (D128, "c16"), (D128, "c7"), (D128_Q3, "c7"), (TINY_QWEN3, "c7"),
+                                       (TINY, "c7s"), (TINY_QWEN3, "c7s"), (D128, "c7m"), (D128_Q3, "c7m"),
+                                       (D128, "c7m_nostream")],
                          ids=lambda v: v if isinstance(v, str) else v.name)
 def test_stepwise_logits_match_oracle(cfg, sname):
     """Teacher-forced: 40 steps (crossing the single-chunk -> split-KV boundary),
@@ -328,4 +337,104 @@ def test_plugin_from_searched_trace_matches_oracle():
         got = plug.decode_step(tok, pos).logits[0].cpu().numpy()
         plug.check()
         assert np.abs(got - want).max() <= 2e-3
+    plug.close()
+
+
+def test_streamed_down_projection_is_used_and_bit_identical():
+    """The schedules above really take the streamed path (several k-tiles for the down projection), and the
+    streamed and the up-front gather give bit-identical logits (same values, same summation order)."""
+    cfg = D128
+    t = tt.build_task_table(cfg, SCHEDS["c7m"], n_sms=148)
+    down = t.tasks[t.tasks[:, tt.F_TYPE] == tt.T_DOWN]
+    assert (down[:, tt.F_NKTILES] > 1).all() and (down[:, tt.F_NTILES] == 1).all()
+    outs = []
+    for name in ("c7m", "c7m_nostream"):
+        _, _, plug = _setup(cfg, SCHEDS[name])
+        acc = [plug.decode_step(tok, pos).logits[0].clone() for pos, tok in enumerate([3, 17, 4000, 25, 999, 1])]
+        plug.check()
+        outs.append(torch.stack(acc).cpu())
+        plug.close()
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_full_size_qwen25_1p5b_matches_oracle():
+    """BASELINE.json configs[1] at full size, the shipped default schedule: a 96-token context prefilled by the
+    oracle, then decode steps whose logits (151 936 of them) and greedy tokens are compared with the CPU oracle.
+    Tolerance as for the small models: fp32 everywhere, so only the summation order differs."""
+    from oracle.decode_ref import RefDecoder
+    from paper_2605_11581_b200.model_config import QWEN25_1P5B
+    from paper_2605_11581_b200.plugin import MegaKernelPlugin
+    from paper_2605_11581_b200.schedules import default_schedule
+    from paper_2605_11581_b200.weights import random_weights, rope_table
+
+    cfg = QWEN25_1P5B
+    w = random_weights(cfg, seed=0)
+    cos, sin = rope_table(cfg, 128)
+    ref = RefDecoder(cfg, w, 128, cos, sin)
+    plug = MegaKernelPlugin(cfg, default_schedule(cfg), max_ctx=128)
+    plug.bind_weights(w)
+    g = torch.Generator().manual_seed(1)
+    prompt = torch.randint(0, cfg.vocab, (96,), generator=g).tolist()
+    ref.prefill(prompt)
+    kc, vc = plug.kv_view()
+    kc[:, 0, :, :96] = ref.k_cache[:, 0, :, :96].to(kc.device)
+    vc[:, 0, :, :96] = ref.v_cache[:, 0, :, :96].to(vc.device)
+    tok = 11
+    for pos in range(96, 100):
+        want = ref.step([tok], [pos])[0].numpy()
+        out = plug.decode_step(tok, pos)
+        plug.check()
+        got = out.logits[0].cpu().numpy()
+        assert np.abs(got - want).max() <= 2e-3, float(np.abs(got - want).max())
+        assert _cos(got, want) >= 0.9995
+        srt = np.sort(want)
+        tok = int(want.argmax())
+        if srt[-1] - srt[-2] > 1e-2:
+            assert int(out.next_token.item()) == tok
+    plug.close()
+
+
+def test_qwen25_1p5b_greedy_64_tokens_identical():
+    """North-star criterion on BASELINE.json configs[1]: after the 512-token prompt of bench.py, 64 free-running
+    greedy steps of the kernel (device-resident loop, one launch per token) emit the oracle's tokens; compared up
+    to the first step whose top-2 margin in the oracle is a near-tie (< 1e-3), which must not come early."""
+    from oracle.decode_ref import RefDecoder
+    from paper_2605_11581_b200.model_config import QWEN25_1P5B
+    from paper_2605_11581_b200.plugin import MegaKernelPlugin
+    from paper_2605_11581_b200.schedules import default_schedule
+    from paper_2605_11581_b200.weights import random_weights, rope_table
+
+    cfg = QWEN25_1P5B
+    w = random_weights(cfg, seed=0)
+    cos, sin = rope_table(cfg, 640)
+    ref = RefDecoder(cfg, w, 640, cos, sin)
+    g = torch.Generator().manual_seed(1)
+    prompt = torch.randint(0, cfg.vocab, (512,), generator=g).tolist()
+    logits = ref.prefill(prompt)
+    plug = MegaKernelPlugin(cfg, default_schedule(cfg), max_ctx=640)
+    plug.bind_weights(w)
+    kc, vc = plug.kv_view()
+    kc[:, 0, :, :512] = ref.k_cache[:, 0, :, :512].to(kc.device)
+    vc[:, 0, :, :512] = ref.v_cache[:, 0, :, :512].to(vc.device)
+    first = int(torch.argmax(logits))
+    want, margins = [], []
+    tok, pos = first, 512
+    for _ in range(64):
+        lg = ref.step([tok], [pos])[0]
+        top = torch.topk(lg, 2).values
+        margins.append(float(top[0] - top[1]))
+        tok = int(torch.argmax(lg))
+        want.append(tok)
+        pos += 1
+    plug.set_state(first, 512)
+    outs = []
+    for _ in range(64):
+        plug.enqueue(want_logits=False, auto_advance=True)
+        outs.append(plug.next_token.clone())
+    plug.check()
+    got = [int(t.item()) for t in outs]
+    margins = np.asarray(margins)
+    first_tie = int(np.argmax(margins < 1e-3)) if (margins < 1e-3).any() else 64
+    assert got[:first_tie] == want[:first_tie]
+    assert first_tie >= 32, f"near-tie at step {first_tie}"
     plug.close()
