@@ -8,12 +8,14 @@ runs a prefill backend to fill the KV cache the plugin owns, then enqueues one
 persistent-kernel launch per generated token with the token / position state
 resident on the device (no host round trip inside the decode loop).
 
-Prefill backends.  ``"decode"`` (the only one built so far) feeds the prompt
-through the decode kernel itself, one launch per prompt token -- correct, and
-already ~0.7 ms per token, but not compute-efficient for long prompts.  The
-tensor-core (tcgen05) prefill GEMM / attention kernels are SURVEY.md section
-8(f) row 2; they plug in here by filling ``plugin.kv_view()`` and returning the
-first decode token.  There is no CPU or PyTorch-op fallback on this path.
+Prefill backends.  ``"decode"`` (the default) feeds the prompt through the decode kernel itself, one launch
+per prompt token -- correct, and ~0.9 ms per token, but not compute-efficient for long prompts.
+``"library"`` is the paper's own arrangement (``PAPER.md:248``: Prefill stays on the serving engine's native
+operators): library GEMMs (cuBLAS through ``torch.matmul``) and library attention fill the KV cache the plugin
+owns, token-parallel; it is the BASELINE the hand-written tensor-core (tcgen05) prefill GEMM / attention kernels
+of SURVEY.md section 8(f) row 2 have to beat, not a product kernel, and it is never used unless asked for.
+Either backend ends with the device state at the last prompt token, so the first generated token already comes
+from a MegaKernel launch.  There is no CPU fallback on any path.
 """
 
 from __future__ import annotations
@@ -40,13 +42,14 @@ class HybridEngine:
     """Prefill -> decode switch around one ``MegaKernelPlugin``."""
 
     def __init__(self, cfg: ModelConfig, weights: DecoderWeights, max_ctx: int, schedule: KernelSchedule | None = None,
-                 device: int = 0, prefill_backend: str = "decode"):
-        if prefill_backend != "decode":
+                 device: int = 0, prefill_backend: str = "decode", prefill_dtype: torch.dtype = torch.float32):
+        if prefill_backend not in ("decode", "library"):
             raise NotImplementedError(f"prefill backend {prefill_backend!r} is not built (SURVEY.md 8(f).2)")
         self.cfg = cfg
         self.prefill_backend = prefill_backend
+        self.prefill_dtype = prefill_dtype
         self.plugin = MegaKernelPlugin(cfg, schedule or default_schedule(cfg), max_ctx=max_ctx, device=device)
-        self.plugin.bind_weights(weights)
+        self.plugin.bind_weights(weights, keep_source=(prefill_backend == "library"))
 
     def prefill(self, prompt_ids) -> None:
         """Fill the KV cache for ``prompt_ids[:-1]`` and leave the device state at the
@@ -57,12 +60,75 @@ class HybridEngine:
             raise ValueError("empty prompt")
         if prompt.numel() + 1 > plug.max_ctx:
             raise ValueError("prompt does not fit the KV cache")
+        if self.prefill_backend == "library":
+            self._library_prefill(prompt[:-1].long())
+            plug.tokens.copy_(prompt[-1:])
+            plug.positions.fill_(prompt.numel() - 1)
+            return
         for pos in range(prompt.numel() - 1):
             plug.tokens.copy_(prompt[pos:pos + 1])
             plug.positions.fill_(pos)
             plug.enqueue(want_logits=False, auto_advance=False)
         plug.tokens.copy_(prompt[-1:])
         plug.positions.fill_(prompt.numel() - 1)
+
+    @torch.no_grad()
+    def _library_prefill(self, toks: torch.Tensor) -> None:
+        """Token-parallel causal pass over ``toks`` with library GEMMs / attention (see the module docstring);
+        writes K and V of every layer into the plugin's cache.  ``prefill_dtype`` float32 keeps the decode path's
+        numerical contract (bf16 weights used exactly, fp32 activations); bfloat16 is the fast setting."""
+        import torch.nn.functional as F
+
+        cfg, plug, dt = self.cfg, self.plugin, self.prefill_dtype
+        w = plug._weights
+        T = toks.numel()
+        if T == 0:
+            return
+        D, G = cfg.head_dim, cfg.group
+        cos, sin = (t[:T].to(torch.float32) for t in plug._rope)
+        kc, vc = plug.kv_view()
+
+        def norm(x, gain):
+            xf = x.float()
+            return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + cfg.rms_eps) * gain.float()).to(dt)
+
+        def rope(x):                       # [T, heads, D] fp32, rotate-half
+            x1, x2 = x[..., :D // 2], x[..., D // 2:]
+            c, s_ = cos[:, None, :], sin[:, None, :]
+            return torch.cat((x1 * c - x2 * s_, x2 * c + x1 * s_), dim=-1)
+
+        def lin(x, weight, bias=None):
+            y = x @ weight.to(dt).T
+            return y if bias is None else y + bias.to(dt)
+
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
+        try:
+            h = w.embed[toks].float()
+            for l, lw in enumerate(w.layers):
+                x = norm(h, lw.ln1)
+                q = lin(x, lw.wq, lw.bq).float().reshape(T, cfg.n_q_heads, D)
+                k = lin(x, lw.wk, lw.bk).float().reshape(T, cfg.n_kv_heads, D)
+                v = lin(x, lw.wv, lw.bv).float().reshape(T, cfg.n_kv_heads, D)
+                if lw.q_norm is not None:
+                    q = norm(q, lw.q_norm).float()
+                    k = norm(k, lw.k_norm).float()
+                q, k = rope(q), rope(k)
+                kb, vb = k.to(torch.bfloat16), v.to(torch.bfloat16)
+                kc[l, 0, :, :T] = kb.transpose(0, 1)
+                vc[l, 0, :, :T] = vb.transpose(0, 1)
+                # attention over the bf16 cache contents, as the decode kernel sees them
+                qh = q.transpose(0, 1).to(dt)[None]                                   # [1, nq, T, D]
+                kh = kb.transpose(0, 1).to(dt).repeat_interleave(G, dim=0)[None]
+                vh = vb.transpose(0, 1).to(dt).repeat_interleave(G, dim=0)[None]
+                attn = F.scaled_dot_product_attention(qh, kh, vh, is_causal=True)[0].transpose(0, 1).reshape(T, cfg.q_dim)
+                h = h + lin(attn, lw.wo).float()
+                x = norm(h, lw.ln2)
+                g_ = lin(x, lw.wgate).float()
+                u = lin(x, lw.wup).float()
+                h = h + lin((g_ * torch.sigmoid(g_) * u).to(dt), lw.wdown).float()
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
 
     @torch.no_grad()
     def generate(self, prompt_ids, max_new_tokens: int) -> GenerationResult:

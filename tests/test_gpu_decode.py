@@ -438,3 +438,31 @@ def test_qwen25_1p5b_greedy_64_tokens_identical():
     assert got[:first_tie] == want[:first_tie]
     assert first_tie >= 32, f"near-tie at step {first_tie}"
     plug.close()
+
+
+def test_hybrid_engine_library_prefill_matches_oracle():
+    """Engine hook with the library prefill backend (prefill on the serving engine's own operators,
+    decode on the MegaKernel): fp32 library GEMMs fill the plugin's KV cache, the first generated token already
+    comes from a MegaKernel launch, and the greedy continuation matches the oracle."""
+    from oracle.decode_ref import RefDecoder
+    from paper_2605_11581_b200.engine import HybridEngine
+    from paper_2605_11581_b200.weights import random_weights, rope_table
+
+    cfg = D128_Q3
+    w = random_weights(cfg, seed=0)
+    cos, sin = rope_table(cfg, 256)
+    ref = RefDecoder(cfg, w, 256, cos, sin)
+    g = torch.Generator().manual_seed(7)
+    prompt = torch.randint(0, cfg.vocab, (150,), generator=g).tolist()
+    want, logits = ref.generate(prompt, 24)
+    eng = HybridEngine(cfg, w, max_ctx=256, schedule=SCHEDS["c7"], prefill_backend="library")
+    res = eng.generate(prompt, 24)
+    kc, _ = eng.plugin.kv_view()
+    np.testing.assert_allclose(kc[:, 0, :, :149].float().cpu().numpy(), ref.k_cache[:, 0, :, :149].float().numpy(),
+                               atol=4e-2, rtol=1e-2)
+    srt = torch.stack(logits).sort(dim=1).values
+    margin = (srt[:, -1] - srt[:, -2]).numpy()
+    first_tie = int(np.argmax(margin < 1e-3)) if (margin < 1e-3).any() else 24
+    assert res.tokens[:first_tie] == want[:first_tie] and first_tie >= 12
+    assert res.prefill_launches == 0 and res.decode_launches == 24
+    eng.close()
