@@ -1,0 +1,66 @@
+/*
+ * adamk_prefill.h -- C ABI of the Prefill-phase operators in libadamk.so.
+ *
+ * The paper's online half runs Prefill on the serving engine's own operators and Decode on the MegaKernel
+ * (/root/reference/PAPER.md:244-249); the reference ships neither.  These entry
+ * points are the hand-written sm_100a Prefill operators a TensorRT-LLM style engine would call in place of
+ * its library GEMMs: a tcgen05 / tensor-memory GEMM with the fused epilogues a decoder layer needs, and the
+ * element-wise kernels around it.  Same conventions as adamk.h: 0 on success, negative ADAMK_PF_E_* code
+ * otherwise, adamk_prefill_last_error() for the message, asynchronous on the given stream, no C++ or torch
+ * types in the signatures, the caller owns every buffer.
+ */
+#ifndef ADAMK_PREFILL_H_
+#define ADAMK_PREFILL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADAMK_PF_OK 0
+#define ADAMK_PF_E_INVALID (-1)
+#define ADAMK_PF_E_CUDA (-2)
+
+/* GEMM epilogues */
+#define ADAMK_PF_EPI_STORE 0  /* out fp32 [T, ldo]  = acc (+ bias)                                          */
+#define ADAMK_PF_EPI_RESID 1  /* out fp32 [T, ldo] += acc          (residual stream update)                 */
+#define ADAMK_PF_EPI_SWIGLU 2 /* out bf16 planes [parts_out][T, ldo] = split(silu(gate) * up); the weight   */
+                              /* interleaves gate and up rows in blocks of tile_n / 2 features              */
+
+typedef void* adamk_pf_stream; /* cudaStream_t */
+
+const char* adamk_prefill_last_error(void);
+
+/* D[T, N] = X[T, K] . W[N, K]^T on the tensor cores, fp32 accumulation in tensor memory.
+ *   x_planes  bf16 [parts][T, K] row-major: the activation as `parts` bf16 planes whose sum is the fp32 value
+ *             (parts 2 = hi + lo, ~2^-17 relative; parts 1 = plain bf16).
+ *   w         bf16 [N, K] row-major (Hugging Face layout).
+ *   tile_n    0 (choose), 128 or 256 output features per tile.
+ * K, N and ldo must be multiples of 8 and the pointers 16-byte aligned. */
+int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void* w, int N, const float* bias, void* out, int ldo,
+                       int epilogue, int parts_out, long long part_stride, int tile_n, adamk_pf_stream stream);
+
+/* h fp32 [T, H] = embed[tokens[t]] (bf16 table). */
+int adamk_prefill_embed(const int32_t* tokens, int T, const void* embed, int H, float* h, adamk_pf_stream stream);
+
+/* planes bf16 [parts][T, H] = split(RMSNorm(h) * gain): the GEMM's activation operand. */
+int adamk_prefill_rmsnorm_split(const float* h, const void* gain, float eps, int T, int H, void* planes, int parts,
+                                adamk_pf_stream stream);
+
+/* planes bf16 [parts][n] = split(x fp32 [n]). */
+int adamk_prefill_split(const float* x, long long n, void* planes, int parts, adamk_pf_stream stream);
+
+/* qkv fp32 [T, (n_q + 2 n_kv) D] (bias already added) -> optional per-head RMSNorm of q and k (Qwen3), rotate-half
+ * rotary embedding with the decode kernel's fp32 cos/sin tables [max_ctx, D/2], then
+ *   q_out   [n_q][T][D]  fp32 or bf16 (q_is_bf16)
+ *   k_cache / v_cache  bf16 [n_kv][max_ctx][D] of one layer, rows pos0 .. pos0 + T - 1. */
+int adamk_prefill_rope_store(const float* qkv, int T, int n_q, int n_kv, int D, const void* q_gain, const void* k_gain, float eps,
+                             const float* cos, const float* sin, int pos0, int max_ctx, void* q_out, int q_is_bf16, void* k_cache,
+                             void* v_cache, adamk_pf_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADAMK_PREFILL_H_ */

@@ -13,7 +13,7 @@ from pathlib import Path
 
 CSRC = Path(__file__).resolve().parent / "csrc"
 LIB = CSRC / "libadamk.so"
-SOURCES = [CSRC / "adamk.cu"]
+SOURCES = [CSRC / "adamk.cu", CSRC / "prefill_gemm.cu", CSRC / "prefill_ops.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -30,7 +30,7 @@ def find_nvcc() -> str:
 def is_stale() -> bool:
     if not LIB.exists():
         return True
-    deps = SOURCES + [CSRC.parents[1] / "include" / "adamk.h"]
+    deps = SOURCES + [CSRC.parents[1] / "include" / "adamk.h", CSRC.parents[1] / "include" / "adamk_prefill.h"]
     return any(d.stat().st_mtime > LIB.stat().st_mtime for d in deps)
 
 

@@ -1,0 +1,427 @@
+// prefill_gemm.cu -- token-parallel projections of the Prefill phase on the 5th-generation tensor cores.
+//
+// The paper keeps Prefill on the serving engine's own operators and switches to the MegaKernel for Decode
+// (/root/reference/PAPER.md:244-249); SURVEY.md section 8(f) row 2 asks for that Prefill half as hand-written
+// sm_100a code.  This file is its GEMM:   D[T, N] = X[T, K] . W[N, K]^T   with the decode kernel's numerical
+// contract -- bf16 weights used exactly, activations carried in fp32.  An fp32 activation is fed to the
+// tensor cores as `parts` bf16 planes (parts = 2: x = hi + lo, |x - hi - lo| <= 2^-17 |x|; parts = 1: plain
+// bf16 rounding), every plane multiplies the same weight tile and all of them accumulate into one fp32
+// accumulator in tensor memory, so the result matches the decode kernel's fp32 FMA chain to ~1e-6 relative
+// at twice the tensor work, or runs at bf16 cost when parts = 1.
+//
+// Kernel anatomy (one persistent CTA per SM, 192 threads, no cluster):
+//   warp 0      TMA producer: cp.async.bulk.tensor 2-D tiles (128 x 64 of X, BN x 64 of W, 128-byte swizzle)
+//               into an n-stage shared-memory ring, full/empty mbarriers.
+//   warp 1      allocates tensor memory; one elected lane issues tcgen05.mma.cta_group::1.kind::f16
+//               (M 128 x N BN x K 16, A and B from shared memory through matrix descriptors, D in TMEM),
+//               tcgen05.commit releases ring slots and publishes finished accumulators.
+//   warps 2-5   epilogue: tcgen05.ld 32 lanes x 32 columns at a time, fused store / residual add / SwiGLU +
+//               bf16-plane split, straight to global memory.  Two accumulators (2 x BN TMEM columns) let the
+//               tensor pipe start tile i+1 while tile i drains.
+// Tiles are walked token-block fastest, so the CTAs running at any moment share a few weight tiles out of L2
+// and every weight byte leaves HBM once.
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "../../include/adamk_prefill.h"
+
+namespace pf {
+
+constexpr int BM = 128;       // tokens per tile = TMEM lanes
+constexpr int BK = 64;        // bf16 elements per k block = one 128-byte swizzle row
+constexpr int UK = 16;        // K of one tcgen05.mma (bf16)
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Shared-memory matrix descriptor of a K-major tile stored as rows of 128 bytes with the 128-byte swizzle
+// (what the TMA box above writes): 8-row groups 1024 bytes apart (stride byte offset), descriptor version 1.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
+  uint64_t d = (addr >> 4) & 0x3fffu;
+  d |= uint64_t(1) << 16;                 // leading byte offset (unused for swizzled K-major), 16-byte units
+  d |= uint64_t(1024 >> 4) << 32;         // stride byte offset
+  d |= uint64_t(1) << 46;                 // version
+  d |= uint64_t(2) << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: fp32 accumulate, bf16 x bf16, both operands K-major, M x N.
+__host__ __device__ constexpr uint32_t instr_desc(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+struct GemmArgs {
+  int T, N, K, parts;
+  int ldo;              // row stride of `out` in elements
+  const float* bias;    // [N] or null (EPI_STORE)
+  void* out;            // fp32 [T, ldo] (STORE / RESID) or bf16 [parts_out][T, ldo] (SWIGLU)
+  int parts_out;
+  long long part_stride;  // elements between output planes (SWIGLU)
+};
+
+template <int BN>
+struct Smem {
+  static constexpr int kStageA = BM * BK * 2;
+  static constexpr int kStageB = BN * BK * 2;
+  static constexpr int kStage = kStageA + kStageB;
+  static constexpr int kStages = (BN == 256) ? 4 : 6;
+  static constexpr int kBytes = kStages * kStage + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ void split_store(__nv_bfloat16* hi_row, __nv_bfloat16* lo_row, int col, const float (&v)[8], bool two) {
+  // 8 consecutive features -> one 16-byte store per plane
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat16 h0 = __float2bfloat16_rn(v[2 * i]), h1 = __float2bfloat16_rn(v[2 * i + 1]);
+    __nv_bfloat16 l0 = __float2bfloat16_rn(v[2 * i] - __bfloat162float(h0));
+    __nv_bfloat16 l1 = __float2bfloat16_rn(v[2 * i + 1] - __bfloat162float(h1));
+    h[i] = uint32_t(__bfloat16_as_ushort(h0)) | (uint32_t(__bfloat16_as_ushort(h1)) << 16);
+    l[i] = uint32_t(__bfloat16_as_ushort(l0)) | (uint32_t(__bfloat16_as_ushort(l1)) << 16);
+  }
+  *reinterpret_cast<uint4*>(hi_row + col) = make_uint4(h[0], h[1], h[2], h[3]);
+  if (two) *reinterpret_cast<uint4*>(lo_row + col) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, const GemmArgs g) {
+  using S = Smem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kStages * S::kStage);
+  uint64_t* empty = full + S::kStages;
+  uint64_t* acc_full = empty + S::kStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m_tiles = (g.T + BM - 1) / BM;
+  const int n_tiles = (g.N + BN - 1) / BN;
+  const int tiles = m_tiles * n_tiles;
+  const int kb_per_part = (g.K + BK - 1) / BK;
+  const int n_kb = kb_per_part * g.parts;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
+    for (int s = 0; s < S::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(2 * BN) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m0 = (tile % m_tiles) * BM, n0 = (tile / m_tiles) * BN;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          const int part = kb / kb_per_part, k0 = (kb - part * kb_per_part) * BK;
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStage;
+          mbar_expect_tx(&full[stage], S::kStage);
+          tma_load_2d(&map_x, &full[stage], sa, k0, part * g.T + m0);
+          tma_load_2d(&map_w, &full[stage], sa + S::kStageA, k0, n0);
+          if (++stage == S::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = instr_desc(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+        const int as = it & 1;
+        mbar_wait(&acc_empty[as], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * S::kStage);
+          const uint64_t a_desc = smem_desc_sw128(a_addr), b_desc = smem_desc_sw128(a_addr + S::kStageA);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            umma(d_tmem, a_desc + uint64_t(k * UK * 2 >> 4), b_desc + uint64_t(k * UK * 2 >> 4), idesc, (kb | k) != 0);
+          umma_commit(&empty[stage]);
+          if (++stage == S::kStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&acc_full[as]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;   // the TMEM lanes this warp may read: 32 * (warp id % 4)
+    int it = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+      const int as = it & 1;
+      const int m0 = (tile % m_tiles) * BM, n0 = (tile / m_tiles) * BN;
+      const int row = m0 + quarter * 32 + lane;
+      const bool row_ok = row < g.T;
+      mbar_wait(&acc_full[as], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t_addr = tmem_base + as * BN + (uint32_t(quarter * 32) << 16);
+      if constexpr (EPI == ADAMK_PF_EPI_SWIGLU) {
+        // tile columns [0, BN/2) are gate rows of BN/2 features, [BN/2, BN) the up rows of the same features
+        __nv_bfloat16* hi = static_cast<__nv_bfloat16*>(g.out) + (long long)row * g.ldo;
+        __nv_bfloat16* lo = hi + g.part_stride;
+        const int f0 = (tile / m_tiles) * (BN / 2);
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 32) {
+          uint32_t ga[32], up[32];
+          tmem_ld32(t_addr + c, ga);
+          tmem_ld32(t_addr + BN / 2 + c, up);
+          tmem_ld_wait();
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              if (f0 + c + j < g.N / 2) {
+                float v[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const float a = __uint_as_float(ga[j + i]);
+                  v[i] = a / (1.0f + __expf(-a)) * __uint_as_float(up[j + i]);
+                }
+                split_store(hi, lo, f0 + c + j, v, g.parts_out == 2);
+              }
+            }
+          }
+        }
+      } else {
+        float* out = static_cast<float*>(g.out) + (long long)row * g.ldo;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t acc[32];
+          tmem_ld32(t_addr + c, acc);
+          tmem_ld_wait();
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const int col = n0 + c + j;
+              if (col < g.N) {
+                float4 v = make_float4(__uint_as_float(acc[j]), __uint_as_float(acc[j + 1]), __uint_as_float(acc[j + 2]),
+                                       __uint_as_float(acc[j + 3]));
+                if constexpr (EPI == ADAMK_PF_EPI_RESID) {
+                  const float4 o = *reinterpret_cast<const float4*>(out + col);
+                  v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                } else if (g.bias != nullptr) {
+                  const float4 b = *reinterpret_cast<const float4*>(g.bias + col);
+                  v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w;
+                }
+                *reinterpret_cast<float4*>(out + col) = v;
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[as]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(2 * BN) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------------------------------------
+// host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                  const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static thread_local char g_err[256] = "";
+char* err_buf() { return g_err; }
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor [rows, cols] row-major, box [box_rows, 64 columns], 128-byte swizzle, zero fill outside.
+static bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) {
+    snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled is not available from this driver");
+    return false;
+  }
+  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(cols) * 2};
+  cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled failed with %d (rows %lld cols %lld box %d)", int(r), rows, cols, box_rows);
+    return false;
+  }
+  return true;
+}
+
+template <int BN, int EPI>
+static int launch(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& g, int n_sms, cudaStream_t stream) {
+  static bool configured = false;
+  auto kern = gemm_kernel<BN, EPI>;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::kBytes);
+    if (e != cudaSuccess) {
+      snprintf(g_err, sizeof g_err, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+      return ADAMK_PF_E_CUDA;
+    }
+    configured = true;
+  }
+  const int tiles = ((g.T + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  const int grid = tiles < n_sms ? tiles : n_sms;
+  kern<<<grid, kThreads, Smem<BN>::kBytes, stream>>>(mx, mw, g);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof g_err, "prefill gemm launch: %s", cudaGetErrorString(e));
+    return ADAMK_PF_E_CUDA;
+  }
+  return ADAMK_PF_OK;
+}
+
+}  // namespace pf
+
+extern "C" {
+
+const char* adamk_prefill_last_error(void) { return pf::g_err; }
+
+int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void* w, int N, const float* bias, void* out, int ldo,
+                       int epilogue, int parts_out, long long part_stride, int tile_n, adamk_pf_stream stream) {
+  using namespace pf;
+  if (x_planes == nullptr || w == nullptr || out == nullptr || T <= 0 || N <= 0 || K <= 0 || (parts != 1 && parts != 2)) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: bad argument (T %d N %d K %d parts %d)", T, N, K, parts);
+    return ADAMK_PF_E_INVALID;
+  }
+  if (K % 8 != 0 || N % 8 != 0 || ldo % 8 != 0) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: K, N and ldo must be multiples of 8 (K %d N %d ldo %d)", K, N, ldo);
+    return ADAMK_PF_E_INVALID;
+  }
+  if ((reinterpret_cast<uintptr_t>(x_planes) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(out)) & 15) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: operands must be 16-byte aligned");
+    return ADAMK_PF_E_INVALID;
+  }
+  if (tile_n == 0) tile_n = (epilogue == ADAMK_PF_EPI_SWIGLU || N >= 1024) ? 256 : 128;
+  if (tile_n != 128 && tile_n != 256) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: tile_n must be 0, 128 or 256");
+    return ADAMK_PF_E_INVALID;
+  }
+  if (epilogue == ADAMK_PF_EPI_SWIGLU && (N % tile_n != 0 || (parts_out != 1 && parts_out != 2))) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: SwiGLU epilogue needs N %% tile_n == 0 and 1 or 2 output planes");
+    return ADAMK_PF_E_INVALID;
+  }
+  int dev = 0, n_sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: no CUDA device");
+    return ADAMK_PF_E_CUDA;
+  }
+  CUtensorMap mx, mw;
+  if (!make_map(&mx, x_planes, (long long)parts * T, K, BM) || !make_map(&mw, w, N, K, tile_n)) return ADAMK_PF_E_CUDA;
+  GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (epilogue * 1000 + tile_n) {
+    case ADAMK_PF_EPI_STORE * 1000 + 128: return launch<128, ADAMK_PF_EPI_STORE>(mx, mw, g, n_sms, s);
+    case ADAMK_PF_EPI_STORE * 1000 + 256: return launch<256, ADAMK_PF_EPI_STORE>(mx, mw, g, n_sms, s);
+    case ADAMK_PF_EPI_RESID * 1000 + 128: return launch<128, ADAMK_PF_EPI_RESID>(mx, mw, g, n_sms, s);
+    case ADAMK_PF_EPI_RESID * 1000 + 256: return launch<256, ADAMK_PF_EPI_RESID>(mx, mw, g, n_sms, s);
+    case ADAMK_PF_EPI_SWIGLU * 1000 + 128: return launch<128, ADAMK_PF_EPI_SWIGLU>(mx, mw, g, n_sms, s);
+    case ADAMK_PF_EPI_SWIGLU * 1000 + 256: return launch<256, ADAMK_PF_EPI_SWIGLU>(mx, mw, g, n_sms, s);
+  }
+  snprintf(g_err, sizeof g_err, "prefill gemm: unknown epilogue %d", epilogue);
+  return ADAMK_PF_E_INVALID;
+}
+
+}  // extern "C"

@@ -14,7 +14,10 @@ per prompt token -- correct, and ~0.9 ms per token, but not compute-efficient fo
 operators): library GEMMs (cuBLAS through ``torch.matmul``) and library attention fill the KV cache the plugin
 owns, token-parallel; it is the BASELINE the hand-written tensor-core (tcgen05) prefill GEMM / attention kernels
 of SURVEY.md section 8(f) row 2 have to beat, not a product kernel, and it is never used unless asked for.
-Either backend ends with the device state at the last prompt token, so the first generated token already comes
+``"tensor"`` is the hand-written replacement of that library path (``prefill.py``): a tcgen05 / tensor-memory GEMM
+with fused bias / residual / SwiGLU epilogues and the row kernels around it; ``prefill_planes`` = 2 feeds each fp32
+activation to the tensor cores as hi + lo bf16 planes (the decode kernel's numerical contract), 1 is plain bf16.
+Every backend ends with the device state at the last prompt token, so the first generated token already comes
 from a MegaKernel launch.  There is no CPU fallback on any path.
 """
 
@@ -42,14 +45,20 @@ class HybridEngine:
     """Prefill -> decode switch around one ``MegaKernelPlugin``."""
 
     def __init__(self, cfg: ModelConfig, weights: DecoderWeights, max_ctx: int, schedule: KernelSchedule | None = None,
-                 device: int = 0, prefill_backend: str = "decode", prefill_dtype: torch.dtype = torch.float32):
-        if prefill_backend not in ("decode", "library"):
-            raise NotImplementedError(f"prefill backend {prefill_backend!r} is not built (SURVEY.md 8(f).2)")
+                 device: int = 0, prefill_backend: str = "decode", prefill_dtype: torch.dtype = torch.float32,
+                 prefill_planes: int = 2):
+        if prefill_backend not in ("decode", "library", "tensor"):
+            raise NotImplementedError(f"prefill backend {prefill_backend!r} does not exist")
         self.cfg = cfg
         self.prefill_backend = prefill_backend
         self.prefill_dtype = prefill_dtype
         self.plugin = MegaKernelPlugin(cfg, schedule or default_schedule(cfg), max_ctx=max_ctx, device=device)
         self.plugin.bind_weights(weights, keep_source=(prefill_backend == "library"))
+        self._tensor_prefill = None
+        if prefill_backend == "tensor":
+            from .prefill import TensorCorePrefill
+
+            self._tensor_prefill = TensorCorePrefill(cfg, weights, self.plugin, planes=prefill_planes)
 
     def prefill(self, prompt_ids) -> None:
         """Fill the KV cache for ``prompt_ids[:-1]`` and leave the device state at the
@@ -60,8 +69,11 @@ class HybridEngine:
             raise ValueError("empty prompt")
         if prompt.numel() + 1 > plug.max_ctx:
             raise ValueError("prompt does not fit the KV cache")
-        if self.prefill_backend == "library":
-            self._library_prefill(prompt[:-1].long())
+        if self.prefill_backend in ("library", "tensor"):
+            if self.prefill_backend == "library":
+                self._library_prefill(prompt[:-1].long())
+            else:
+                self._tensor_prefill.run(prompt[:-1])
             plug.tokens.copy_(prompt[-1:])
             plug.positions.fill_(prompt.numel() - 1)
             return

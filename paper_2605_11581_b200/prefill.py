@@ -1,0 +1,179 @@
+"""Prefill phase on hand-written tensor-core operators.
+
+``PAPER.md:244-249`` runs Prefill on the serving engine's operators and Decode on the MegaKernel.  This module is
+that Prefill half built from ``include/adamk_prefill.h``: a tcgen05 / tensor-memory GEMM
+(``csrc/prefill_gemm.cu``) with fused bias, residual and SwiGLU epilogues, and the row kernels around it
+(``csrc/prefill_ops.cu``).  Layer dataflow for ``T`` prompt tokens::
+
+    h fp32 [T, H] --rmsnorm_split--> planes --GEMM(wqkv)+bias--> qkv fp32 --rope_store--> q, KV cache (bf16)
+      --attention--> a --GEMM(wo) += h--> h --rmsnorm_split--> planes --GEMM(gate|up) SwiGLU--> act planes
+      --GEMM(wdown) += h--> h
+
+``planes`` = 2 keeps the decode kernel's numerical contract (fp32 activations against exact bf16 weights: each fp32
+value enters the tensor cores as hi + lo bf16 planes); ``planes`` = 1 is plain bf16 activations at half the
+tensor work.  Causal attention over the bf16 cache is the one operator still taken from the library
+(``torch.nn.functional.scaled_dot_product_attention``): ~5 % of the Prefill FLOPs at 4K tokens; a tcgen05
+flash-attention kernel is the open item of this row.  There is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from .model_config import ModelConfig
+from .plugin import AdamkError, load_library
+from .weights import DecoderWeights
+
+EPI_STORE, EPI_RESID, EPI_SWIGLU = 0, 1, 2
+GU_BLOCK = 128   # features per gate / up block of the interleaved weight = half of the 256-wide GEMM tile
+
+PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
+                   "adamk_prefill_split", "adamk_prefill_rope_store")
+
+_declared = False
+
+
+def _lib():
+    global _declared
+    lib = load_library()
+    if not _declared:
+        vp, i, ll, f = C.c_void_p, C.c_int, C.c_longlong, C.c_float
+        lib.adamk_prefill_last_error.restype = C.c_char_p
+        lib.adamk_prefill_gemm.argtypes = [vp, i, i, i, vp, i, vp, vp, i, i, i, ll, i, vp]
+        lib.adamk_prefill_embed.argtypes = [vp, i, vp, i, vp, vp]
+        lib.adamk_prefill_rmsnorm_split.argtypes = [vp, vp, f, i, i, vp, i, vp]
+        lib.adamk_prefill_split.argtypes = [vp, ll, vp, i, vp]
+        lib.adamk_prefill_rope_store.argtypes = [vp, i, i, i, i, vp, vp, f, vp, vp, i, i, vp, i, vp, vp, vp]
+        _declared = True
+    return lib
+
+
+def _ok(code: int) -> None:
+    if code != 0:
+        raise AdamkError(code, (_lib().adamk_prefill_last_error() or b"").decode() or "prefill operator: invalid argument")
+
+
+def _stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def gemm(x_planes: torch.Tensor, w: torch.Tensor, out: torch.Tensor, bias: torch.Tensor | None = None,
+         epilogue: int = EPI_STORE, tile_n: int = 0) -> torch.Tensor:
+    """``out`` (op)= sum_p x_planes[p] @ w.T on the tensor cores.  ``x_planes`` bf16 [parts, T, K], ``w`` bf16 [N, K];
+    ``out`` fp32 [T, N] (STORE / RESID) or bf16 [parts_out, T, N / 2] (SWIGLU, gate / up interleaved in ``w``)."""
+    if not x_planes.is_cuda:
+        raise AdamkError(-102, "prefill operators have no CPU fallback")
+    assert x_planes.dtype == torch.bfloat16 and w.dtype == torch.bfloat16 and x_planes.is_contiguous() and w.is_contiguous()
+    parts, T, K = x_planes.shape
+    N = w.shape[0]
+    assert w.shape[1] == K and out.is_contiguous()
+    if epilogue == EPI_SWIGLU:
+        assert out.dtype == torch.bfloat16 and out.dim() == 3 and out.shape[1] == T and out.shape[2] == N // 2
+        parts_out, ldo, stride = out.shape[0], out.shape[2], out.shape[1] * out.shape[2]
+    else:
+        assert out.dtype == torch.float32 and out.shape == (T, N)
+        parts_out, ldo, stride = 1, N, 0
+    if bias is not None:
+        assert bias.dtype == torch.float32 and bias.numel() == N and epilogue == EPI_STORE
+    _ok(_lib().adamk_prefill_gemm(_ptr(x_planes), parts, T, K, _ptr(w), N, _ptr(bias), _ptr(out), ldo, epilogue, parts_out,
+                                  stride, tile_n, _stream()))
+    return out
+
+
+def interleave_gate_up(wgate: torch.Tensor, wup: torch.Tensor, block: int = GU_BLOCK) -> torch.Tensor:
+    """[2 * I_pad, K]: blocks of ``block`` gate rows followed by the ``block`` up rows of the same features (zero rows
+    pad I to a multiple of ``block``), so that one 2*block-wide GEMM tile holds both halves of SwiGLU."""
+    I, K = wgate.shape
+    I_pad = -(-I // block) * block
+    g = torch.zeros(I_pad, K, dtype=wgate.dtype, device=wgate.device)
+    u = torch.zeros_like(g)
+    g[:I], u[:I] = wgate, wup
+    return torch.stack((g.view(-1, block, K), u.view(-1, block, K)), dim=1).reshape(2 * I_pad, K).contiguous()
+
+
+class TensorCorePrefill:
+    """Token-parallel causal pass that fills the KV cache a ``MegaKernelPlugin`` owns."""
+
+    def __init__(self, cfg: ModelConfig, weights: DecoderWeights, plugin, planes: int = 2):
+        if planes not in (1, 2):
+            raise ValueError("planes must be 1 (bf16 activations) or 2 (hi + lo, fp32-accurate)")
+        _lib()
+        self.cfg, self.plugin, self.planes = cfg, plugin, planes
+        dev = plugin.device
+        self.embed = weights.embed.to(dev)
+        self.layers = []
+        for lw in weights.layers:
+            wqkv = torch.cat((lw.wq, lw.wk, lw.wv), dim=0).to(dev).contiguous()
+            bqkv = None
+            if lw.bq is not None:
+                bqkv = torch.cat((lw.bq, lw.bk, lw.bv)).to(dev).float().contiguous()
+            wgu = interleave_gate_up(lw.wgate.to(dev), lw.wup.to(dev))
+            i_pad = wgu.shape[0] // 2
+            wdown = lw.wdown.to(dev)
+            if i_pad != cfg.intermediate:
+                wdown = torch.nn.functional.pad(wdown, (0, i_pad - cfg.intermediate))
+            self.layers.append(dict(ln1=lw.ln1.to(dev), ln2=lw.ln2.to(dev), wqkv=wqkv, bqkv=bqkv, wo=lw.wo.to(dev).contiguous(),
+                                    wgu=wgu, wdown=wdown.contiguous(), i_pad=i_pad,
+                                    q_norm=None if lw.q_norm is None else lw.q_norm.to(dev),
+                                    k_norm=None if lw.k_norm is None else lw.k_norm.to(dev)))
+        self.launches = 0
+
+    @torch.no_grad()
+    def run(self, toks: torch.Tensor, pos0: int = 0) -> torch.Tensor:
+        """Fill cache rows ``pos0 .. pos0 + T - 1`` of every layer from ``toks`` (int32 / int64 [T] on the device) and
+        return the final hidden states fp32 [T, H].  ``pos0`` must be 0 unless the earlier rows are already cached
+        (chunked prefill attends to them)."""
+        import torch.nn.functional as F
+
+        cfg, plug, P, lib, st = self.cfg, self.plugin, self.planes, _lib(), _stream()
+        T = int(toks.numel())
+        if T == 0:
+            return torch.empty(0, cfg.hidden, device=plug.device)
+        if pos0 + T > plug.max_ctx:
+            raise ValueError("prompt does not fit the KV cache")
+        dev, H, D, nq, nkv = plug.device, cfg.hidden, cfg.head_dim, cfg.n_q_heads, cfg.n_kv_heads
+        bf = torch.bfloat16
+        toks32 = toks.to(device=dev, dtype=torch.int32).contiguous()
+        h = torch.empty(T, H, dtype=torch.float32, device=dev)
+        xp = torch.empty(P, T, H, dtype=bf, device=dev)
+        qkv = torch.empty(T, (nq + 2 * nkv) * D, dtype=torch.float32, device=dev)
+        q_dtype = bf if P == 1 else torch.float32
+        q = torch.empty(nq, T, D, dtype=q_dtype, device=dev)
+        ap = torch.empty(P, T, nq * D, dtype=bf, device=dev)
+        act = torch.empty(P, T, self.layers[0]["i_pad"], dtype=bf, device=dev)
+        cos, sin = plug._rope
+        kc, vc = plug.kv_view()
+        _ok(lib.adamk_prefill_embed(_ptr(toks32), T, _ptr(self.embed), H, _ptr(h), st))
+        n = 1
+        ctx = pos0 + T
+        for l, lw in enumerate(self.layers):
+            _ok(lib.adamk_prefill_rmsnorm_split(_ptr(h), _ptr(lw["ln1"]), cfg.rms_eps, T, H, _ptr(xp), P, st))
+            gemm(xp, lw["wqkv"], qkv, bias=lw["bqkv"])
+            _ok(lib.adamk_prefill_rope_store(_ptr(qkv), T, nq, nkv, D, _ptr(lw["q_norm"]), _ptr(lw["k_norm"]), cfg.rms_eps,
+                                             _ptr(cos), _ptr(sin), pos0, plug.max_ctx, _ptr(q), int(P == 1),
+                                             _ptr(kc[l, 0]), _ptr(vc[l, 0]), st))
+            # causal attention over the bf16 cache contents, as the decode kernel sees them (library operator)
+            kh, vh = kc[l, 0, :, :ctx].to(q_dtype)[None], vc[l, 0, :, :ctx].to(q_dtype)[None]
+            if pos0 == 0:
+                a = F.scaled_dot_product_attention(q[None], kh, vh, is_causal=True, enable_gqa=True)
+            else:
+                mask = torch.ones(T, ctx, dtype=torch.bool, device=dev).tril(diagonal=pos0)
+                a = F.scaled_dot_product_attention(q[None], kh, vh, attn_mask=mask, enable_gqa=True)
+            a = a[0].transpose(0, 1).reshape(T, nq * D)
+            if P == 1:
+                ap[0].copy_(a)
+            else:
+                _ok(lib.adamk_prefill_split(_ptr(a.contiguous()), T * nq * D, _ptr(ap), P, st))
+            gemm(ap, lw["wo"], h, epilogue=EPI_RESID)
+            _ok(lib.adamk_prefill_rmsnorm_split(_ptr(h), _ptr(lw["ln2"]), cfg.rms_eps, T, H, _ptr(xp), P, st))
+            gemm(xp, lw["wgu"], act, epilogue=EPI_SWIGLU, tile_n=2 * GU_BLOCK)
+            gemm(act, lw["wdown"], h, epilogue=EPI_RESID)
+            n += 7 + (P == 2)
+        self.launches += n
+        return h

@@ -250,6 +250,35 @@ def test_cabi_exports_every_declared_symbol():
     assert lib.adamk_abi_version() == plugin.ABI_VERSION
 
 
+def test_cabi_exports_prefill_operators():
+    """include/adamk_prefill.h: the Prefill operators live in the same library and every declared symbol is exported."""
+    from paper_2605_11581_b200 import build, plugin, prefill
+
+    build.build()
+    header = (Path(__file__).resolve().parents[1] / "include" / "adamk_prefill.h").read_text()
+    declared = set(re.findall(r"\b(adamk_prefill_[a-z_]+)\s*\(", header))
+    assert declared == set(prefill.PREFILL_EXPORTS)
+    lib = plugin.load_library()
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_prefill_gate_up_interleave():
+    """Host-side weight layout of the fused SwiGLU GEMM: blocks of gate rows followed by the up rows of the same
+    features, zero rows padding the intermediate size to a whole block."""
+    import torch
+
+    from paper_2605_11581_b200.prefill import interleave_gate_up
+
+    g = torch.arange(6 * 4, dtype=torch.float32).reshape(6, 4)
+    u = -g
+    w = interleave_gate_up(g, u, block=4)
+    assert w.shape == (16, 4)
+    assert torch.equal(w[0:4], g[0:4]) and torch.equal(w[4:8], u[0:4])
+    assert torch.equal(w[8:10], g[4:6]) and torch.equal(w[12:14], u[4:6])
+    assert w[10:12].abs().sum() == 0 and w[14:16].abs().sum() == 0
+
+
 def test_search_to_schedule_to_task_table():
     """Offline half -> online half: the planner's search on the share of a layer one SM executes
     (mkplan.model_graph.build_sm_slice_graph) yields a SolidifiedTrace whose plan lowers to a kernel schedule
