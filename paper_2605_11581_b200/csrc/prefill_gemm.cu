@@ -121,7 +121,14 @@ struct GemmArgs {
   void* out;            // fp32 [T, ldo] (STORE / RESID) or bf16 [parts_out][T, ldo] (SWIGLU)
   int parts_out;
   long long part_stride;  // elements between output planes (SWIGLU)
+  int main_items;       // work items [0, main_items) are whole BM x BN tiles ...
+  int tail_split;       // ... the remaining tiles are cut into tail_split column slices each (last-wave balance)
+  int n_items;
 };
+
+constexpr int BOXN = 64;            // weight rows per TMA box: the slice granularity of a tile
+constexpr int kStagePitch = 36;     // floats per staged row (32 + 4: conflict-free 16-byte accesses)
+constexpr int kStageFloats = 32 * kStagePitch;
 
 template <int BN>
 struct Smem {
@@ -129,22 +136,48 @@ struct Smem {
   static constexpr int kStageB = BN * BK * 2;
   static constexpr int kStage = kStageA + kStageB;
   static constexpr int kStages = (BN == 256) ? 4 : 6;
-  static constexpr int kBytes = kStages * kStage + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int kEpi = 4 * kStageFloats * 4;
+  static constexpr int kBytes = kStages * kStage + kEpi + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
-__device__ __forceinline__ void split_store(__nv_bfloat16* hi_row, __nv_bfloat16* lo_row, int col, const float (&v)[8], bool two) {
-  // 8 consecutive features -> one 16-byte store per plane
-  uint32_t h[4], l[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    __nv_bfloat16 h0 = __float2bfloat16_rn(v[2 * i]), h1 = __float2bfloat16_rn(v[2 * i + 1]);
-    __nv_bfloat16 l0 = __float2bfloat16_rn(v[2 * i] - __bfloat162float(h0));
-    __nv_bfloat16 l1 = __float2bfloat16_rn(v[2 * i + 1] - __bfloat162float(h1));
-    h[i] = uint32_t(__bfloat16_as_ushort(h0)) | (uint32_t(__bfloat16_as_ushort(h1)) << 16);
-    l[i] = uint32_t(__bfloat16_as_ushort(l0)) | (uint32_t(__bfloat16_as_ushort(l1)) << 16);
+// One unit of work: rows [m0, m0 + BM) x a slice of `w` accumulator columns of tile column n_blk.
+struct Item {
+  int m0, n_blk, sub, w;
+};
+
+template <int BN>
+__device__ __forceinline__ Item decode_item(int idx, const GemmArgs& g, int m_tiles) {
+  int tile = idx, sub = 0, w = BN;
+  if (idx >= g.main_items) {
+    const int t = idx - g.main_items;
+    tile = g.main_items + t / g.tail_split;
+    sub = t % g.tail_split;
+    w = BN / g.tail_split;
   }
-  *reinterpret_cast<uint4*>(hi_row + col) = make_uint4(h[0], h[1], h[2], h[3]);
-  if (two) *reinterpret_cast<uint4*>(lo_row + col) = make_uint4(l[0], l[1], l[2], l[3]);
+  return Item{(tile % m_tiles) * BM, tile / m_tiles, sub, w};
+}
+
+// Weight row of the j-th 64-row box of an item.  SwiGLU tiles hold BN/2 gate rows then the BN/2 up rows of the
+// same features; a slice takes w/2 of each so that gate and up of a feature stay in one accumulator.
+template <int BN, int EPI>
+__device__ __forceinline__ int box_row(const Item& it, int j) {
+  if constexpr (EPI == ADAMK_PF_EPI_SWIGLU) {
+    const int half_boxes = it.w / (2 * BOXN);
+    return j < half_boxes ? it.n_blk * BN + it.sub * (it.w / 2) + j * BOXN
+                          : it.n_blk * BN + BN / 2 + it.sub * (it.w / 2) + (j - half_boxes) * BOXN;
+  } else {
+    return it.n_blk * BN + it.sub * it.w + j * BOXN;
+  }
+}
+
+__device__ __forceinline__ uint2 split4(const float4 v, uint2* lo) {
+  const __nv_bfloat16 h0 = __float2bfloat16_rn(v.x), h1 = __float2bfloat16_rn(v.y), h2 = __float2bfloat16_rn(v.z),
+                      h3 = __float2bfloat16_rn(v.w);
+  const __nv_bfloat16 l0 = __float2bfloat16_rn(v.x - __bfloat162float(h0)), l1 = __float2bfloat16_rn(v.y - __bfloat162float(h1)),
+                      l2 = __float2bfloat16_rn(v.z - __bfloat162float(h2)), l3 = __float2bfloat16_rn(v.w - __bfloat162float(h3));
+  auto pack = [](__nv_bfloat16 a, __nv_bfloat16 b) { return uint32_t(__bfloat16_as_ushort(a)) | (uint32_t(__bfloat16_as_ushort(b)) << 16); };
+  *lo = make_uint2(pack(l0, l1), pack(l2, l3));
+  return make_uint2(pack(h0, h1), pack(h2, h3));
 }
 
 template <int BN, int EPI>
@@ -153,7 +186,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
   using S = Smem<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kStages * S::kStage);
+  float* epi_stage = reinterpret_cast<float*>(smem + S::kStages * S::kStage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kStages * S::kStage + S::kEpi);
   uint64_t* empty = full + S::kStages;
   uint64_t* acc_full = empty + S::kStages;
   uint64_t* acc_empty = acc_full + 2;
@@ -161,8 +195,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (g.T + BM - 1) / BM;
-  const int n_tiles = (g.N + BN - 1) / BN;
-  const int tiles = m_tiles * n_tiles;
   const int kb_per_part = (g.K + BK - 1) / BK;
   const int n_kb = kb_per_part * g.parts;
 
@@ -192,28 +224,32 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int m0 = (tile % m_tiles) * BM, n0 = (tile / m_tiles) * BN;
+      for (int idx = blockIdx.x; idx < g.n_items; idx += gridDim.x) {
+        const Item it = decode_item<BN>(idx, g, m_tiles);
+        const int boxes = it.w / BOXN;
+        const uint32_t bytes = S::kStageA + boxes * BOXN * BK * 2;
         for (int kb = 0; kb < n_kb; ++kb) {
           const int part = kb / kb_per_part, k0 = (kb - part * kb_per_part) * BK;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStage;
-          mbar_expect_tx(&full[stage], S::kStage);
-          tma_load_2d(&map_x, &full[stage], sa, k0, part * g.T + m0);
-          tma_load_2d(&map_w, &full[stage], sa + S::kStageA, k0, n0);
+          mbar_expect_tx(&full[stage], bytes);
+          tma_load_2d(&map_x, &full[stage], sa, k0, part * g.T + it.m0);
+          for (int j = 0; j < boxes; ++j)
+            tma_load_2d(&map_w, &full[stage], sa + S::kStageA + j * (BOXN * BK * 2), k0, box_row<BN, EPI>(it, j));
           if (++stage == S::kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = instr_desc(BM, BN);
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
-        const int as = it & 1;
-        mbar_wait(&acc_empty[as], ((it >> 1) & 1) ^ 1);
+      int n = 0;
+      for (int idx = blockIdx.x; idx < g.n_items; idx += gridDim.x, ++n) {
+        const Item it = decode_item<BN>(idx, g, m_tiles);
+        const uint32_t idesc = instr_desc(BM, it.w);
+        const int as = n & 1;
+        mbar_wait(&acc_empty[as], ((n >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
         for (int kb = 0; kb < n_kb; ++kb) {
@@ -231,67 +267,91 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
       }
     }
   } else {
+    // Epilogue.  tcgen05.ld hands each lane one accumulator row; a row-per-lane store would touch 32 lines per
+    // instruction, so every 32 x 32 block goes through a padded shared-memory patch and leaves as 4 rows x 128
+    // contiguous bytes per instruction (8 lanes per row).
     const int quarter = warp & 3;   // the TMEM lanes this warp may read: 32 * (warp id % 4)
-    int it = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
-      const int as = it & 1;
-      const int m0 = (tile % m_tiles) * BM, n0 = (tile / m_tiles) * BN;
-      const int row = m0 + quarter * 32 + lane;
-      const bool row_ok = row < g.T;
-      mbar_wait(&acc_full[as], (it >> 1) & 1);
+    float* patch = epi_stage + quarter * kStageFloats;
+    const int sub_row = lane >> 3, cg = (lane & 7) * 4;
+    int n = 0;
+    for (int idx = blockIdx.x; idx < g.n_items; idx += gridDim.x, ++n) {
+      const Item it = decode_item<BN>(idx, g, m_tiles);
+      const int as = n & 1;
+      const int row0 = it.m0 + quarter * 32;
+      mbar_wait(&acc_full[as], (n >> 1) & 1);
       tc_fence_after();
       const uint32_t t_addr = tmem_base + as * BN + (uint32_t(quarter * 32) << 16);
       if constexpr (EPI == ADAMK_PF_EPI_SWIGLU) {
-        // tile columns [0, BN/2) are gate rows of BN/2 features, [BN/2, BN) the up rows of the same features
-        __nv_bfloat16* hi = static_cast<__nv_bfloat16*>(g.out) + (long long)row * g.ldo;
-        __nv_bfloat16* lo = hi + g.part_stride;
-        const int f0 = (tile / m_tiles) * (BN / 2);
+        const int halfw = it.w / 2;
+        const int f0 = it.n_blk * (BN / 2) + it.sub * halfw;
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.out);
 #pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
+        for (int c = 0; c < halfw; c += 32) {
           uint32_t ga[32], up[32];
           tmem_ld32(t_addr + c, ga);
-          tmem_ld32(t_addr + BN / 2 + c, up);
+          tmem_ld32(t_addr + halfw + c, up);
           tmem_ld_wait();
-          if (row_ok) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              if (f0 + c + j < g.N / 2) {
-                float v[8];
+          for (int j = 0; j < 32; j += 4) {
+            float v[4];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  const float a = __uint_as_float(ga[j + i]);
-                  v[i] = a / (1.0f + __expf(-a)) * __uint_as_float(up[j + i]);
-                }
-                split_store(hi, lo, f0 + c + j, v, g.parts_out == 2);
-              }
+            for (int i = 0; i < 4; ++i) {
+              const float a = __uint_as_float(ga[j + i]);
+              v[i] = __fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(up[j + i]);   // fast divide: the IEEE slow path costs more than the tile
+            }
+            *reinterpret_cast<float4*>(patch + lane * kStagePitch + j) = make_float4(v[0], v[1], v[2], v[3]);
+          }
+          __syncwarp();
+          const int f = f0 + c + cg;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = i * 4 + sub_row, row = row0 + r;
+            const float4 v = *reinterpret_cast<const float4*>(patch + r * kStagePitch + cg);
+            if (row < g.T && f < g.N / 2) {
+              uint2 lo;
+              const uint2 hi = split4(v, &lo);
+              __nv_bfloat16* dst = out + (long long)row * g.ldo + f;
+              *reinterpret_cast<uint2*>(dst) = hi;
+              if (g.parts_out == 2) *reinterpret_cast<uint2*>(dst + g.part_stride) = lo;
             }
           }
+          __syncwarp();
         }
       } else {
-        float* out = static_cast<float*>(g.out) + (long long)row * g.ldo;
+        const int n0 = it.n_blk * BN + it.sub * it.w;
+        float* out = static_cast<float*>(g.out);
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 0; c < it.w; c += 32) {
           uint32_t acc[32];
           tmem_ld32(t_addr + c, acc);
-          tmem_ld_wait();
-          if (row_ok) {
+          const int col = n0 + c + cg;
+          const bool col_ok = col < g.N;
+          float4 o[8];
+          if constexpr (EPI == ADAMK_PF_EPI_RESID) {   // residual rows: in flight while the accumulator arrives
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const int col = n0 + c + j;
-              if (col < g.N) {
-                float4 v = make_float4(__uint_as_float(acc[j]), __uint_as_float(acc[j + 1]), __uint_as_float(acc[j + 2]),
-                                       __uint_as_float(acc[j + 3]));
-                if constexpr (EPI == ADAMK_PF_EPI_RESID) {
-                  const float4 o = *reinterpret_cast<const float4*>(out + col);
-                  v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
-                } else if (g.bias != nullptr) {
-                  const float4 b = *reinterpret_cast<const float4*>(g.bias + col);
-                  v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w;
-                }
-                *reinterpret_cast<float4*>(out + col) = v;
-              }
+            for (int i = 0; i < 8; ++i) {
+              const int row = row0 + i * 4 + sub_row;
+              o[i] = (row < g.T && col_ok) ? *reinterpret_cast<const float4*>(out + (long long)row * g.ldo + col) : make_float4(0, 0, 0, 0);
             }
+          } else {
+            const float4 b = (g.bias != nullptr && col_ok) ? *reinterpret_cast<const float4*>(g.bias + col) : make_float4(0, 0, 0, 0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = b;
           }
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(patch + lane * kStagePitch + j) =
+                make_float4(__uint_as_float(acc[j]), __uint_as_float(acc[j + 1]), __uint_as_float(acc[j + 2]), __uint_as_float(acc[j + 3]));
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = i * 4 + sub_row, row = row0 + r;
+            float4 v = *reinterpret_cast<const float4*>(patch + r * kStagePitch + cg);
+            v.x += o[i].x; v.y += o[i].y; v.z += o[i].z; v.w += o[i].w;
+            if (row < g.T && col_ok) *reinterpret_cast<float4*>(out + (long long)row * g.ldo + col) = v;
+          }
+          __syncwarp();
         }
       }
       tc_fence_before();
@@ -351,7 +411,7 @@ static bool make_map(CUtensorMap* m, const void* base, long long rows, long long
 }
 
 template <int BN, int EPI>
-static int launch(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& g, int n_sms, cudaStream_t stream) {
+static int launch(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& g_in, int n_sms, cudaStream_t stream) {
   static bool configured = false;
   auto kern = gemm_kernel<BN, EPI>;
   if (!configured) {
@@ -362,8 +422,18 @@ static int launch(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& 
     }
     configured = true;
   }
-  const int tiles = ((g.T + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  // Work items: whole tiles, except that the tiles of a last partial wave are cut into column slices so that the
+  // wave keeps every SM busy for a fraction of a tile time instead of a few SMs for a whole one.
+  const int tiles = ((g_in.T + BM - 1) / BM) * ((g_in.N + BN - 1) / BN);
   const int grid = tiles < n_sms ? tiles : n_sms;
+  const int rem = tiles % grid;
+  const int max_split = (EPI == ADAMK_PF_EPI_SWIGLU) ? BN / (2 * BOXN) : BN / BOXN;
+  int split = 1;
+  while (rem > 0 && split * 2 <= max_split && rem * split * 2 <= grid) split *= 2;
+  GemmArgs g = g_in;
+  g.main_items = tiles - rem;
+  g.tail_split = split;
+  g.n_items = g.main_items + rem * split;
   kern<<<grid, kThreads, Smem<BN>::kBytes, stream>>>(mx, mw, g);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -409,8 +479,8 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
     return ADAMK_PF_E_CUDA;
   }
   CUtensorMap mx, mw;
-  if (!make_map(&mx, x_planes, (long long)parts * T, K, BM) || !make_map(&mw, w, N, K, tile_n)) return ADAMK_PF_E_CUDA;
-  GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride};
+  if (!make_map(&mx, x_planes, (long long)parts * T, K, BM) || !make_map(&mw, w, N, K, BOXN)) return ADAMK_PF_E_CUDA;
+  GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride, 0, 1, 0};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (epilogue * 1000 + tile_n) {
     case ADAMK_PF_EPI_STORE * 1000 + 128: return launch<128, ADAMK_PF_EPI_STORE>(mx, mw, g, n_sms, s);

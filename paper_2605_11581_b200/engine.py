@@ -46,7 +46,7 @@ class HybridEngine:
 
     def __init__(self, cfg: ModelConfig, weights: DecoderWeights, max_ctx: int, schedule: KernelSchedule | None = None,
                  device: int = 0, prefill_backend: str = "decode", prefill_dtype: torch.dtype = torch.float32,
-                 prefill_planes: int = 2):
+                 prefill_planes: int = 2, prefill_attention: str | None = None):
         if prefill_backend not in ("decode", "library", "tensor"):
             raise NotImplementedError(f"prefill backend {prefill_backend!r} does not exist")
         self.cfg = cfg
@@ -58,7 +58,7 @@ class HybridEngine:
         if prefill_backend == "tensor":
             from .prefill import TensorCorePrefill
 
-            self._tensor_prefill = TensorCorePrefill(cfg, weights, self.plugin, planes=prefill_planes)
+            self._tensor_prefill = TensorCorePrefill(cfg, weights, self.plugin, planes=prefill_planes, attention=prefill_attention)
 
     def prefill(self, prompt_ids) -> None:
         """Fill the KV cache for ``prompt_ids[:-1]`` and leave the device state at the

@@ -100,11 +100,17 @@ def interleave_gate_up(wgate: torch.Tensor, wup: torch.Tensor, block: int = GU_B
 class TensorCorePrefill:
     """Token-parallel causal pass that fills the KV cache a ``MegaKernelPlugin`` owns."""
 
-    def __init__(self, cfg: ModelConfig, weights: DecoderWeights, plugin, planes: int = 2):
+    def __init__(self, cfg: ModelConfig, weights: DecoderWeights, plugin, planes: int = 2, attention: str | None = None):
+        """``attention``: dtype of the library attention operator, "fp32" (default with two planes; exact but a
+        materialised-score kernel) or "bf16" (default with one plane; flash kernel)."""
         if planes not in (1, 2):
             raise ValueError("planes must be 1 (bf16 activations) or 2 (hi + lo, fp32-accurate)")
+        attention = attention or ("bf16" if planes == 1 else "fp32")
+        if attention not in ("bf16", "fp32"):
+            raise ValueError("attention must be 'bf16' or 'fp32'")
         _lib()
         self.cfg, self.plugin, self.planes = cfg, plugin, planes
+        self.attn_bf16 = attention == "bf16"
         dev = plugin.device
         self.embed = weights.embed.to(dev)
         self.layers = []
@@ -143,7 +149,7 @@ class TensorCorePrefill:
         h = torch.empty(T, H, dtype=torch.float32, device=dev)
         xp = torch.empty(P, T, H, dtype=bf, device=dev)
         qkv = torch.empty(T, (nq + 2 * nkv) * D, dtype=torch.float32, device=dev)
-        q_dtype = bf if P == 1 else torch.float32
+        q_dtype = bf if self.attn_bf16 else torch.float32
         q = torch.empty(nq, T, D, dtype=q_dtype, device=dev)
         ap = torch.empty(P, T, nq * D, dtype=bf, device=dev)
         act = torch.empty(P, T, self.layers[0]["i_pad"], dtype=bf, device=dev)
@@ -156,7 +162,7 @@ class TensorCorePrefill:
             _ok(lib.adamk_prefill_rmsnorm_split(_ptr(h), _ptr(lw["ln1"]), cfg.rms_eps, T, H, _ptr(xp), P, st))
             gemm(xp, lw["wqkv"], qkv, bias=lw["bqkv"])
             _ok(lib.adamk_prefill_rope_store(_ptr(qkv), T, nq, nkv, D, _ptr(lw["q_norm"]), _ptr(lw["k_norm"]), cfg.rms_eps,
-                                             _ptr(cos), _ptr(sin), pos0, plug.max_ctx, _ptr(q), int(P == 1),
+                                             _ptr(cos), _ptr(sin), pos0, plug.max_ctx, _ptr(q), int(self.attn_bf16),
                                              _ptr(kc[l, 0]), _ptr(vc[l, 0]), st))
             # causal attention over the bf16 cache contents, as the decode kernel sees them (library operator)
             kh, vh = kc[l, 0, :, :ctx].to(q_dtype)[None], vc[l, 0, :, :ctx].to(q_dtype)[None]
@@ -166,14 +172,14 @@ class TensorCorePrefill:
                 mask = torch.ones(T, ctx, dtype=torch.bool, device=dev).tril(diagonal=pos0)
                 a = F.scaled_dot_product_attention(q[None], kh, vh, attn_mask=mask, enable_gqa=True)
             a = a[0].transpose(0, 1).reshape(T, nq * D)
-            if P == 1:
+            if self.attn_bf16:
                 ap[0].copy_(a)
             else:
-                _ok(lib.adamk_prefill_split(_ptr(a.contiguous()), T * nq * D, _ptr(ap), P, st))
-            gemm(ap, lw["wo"], h, epilogue=EPI_RESID)
+                _ok(lib.adamk_prefill_split(_ptr(a.float().contiguous()), T * nq * D, _ptr(ap), P, st))
+            gemm(ap[:1] if self.attn_bf16 else ap, lw["wo"], h, epilogue=EPI_RESID)
             _ok(lib.adamk_prefill_rmsnorm_split(_ptr(h), _ptr(lw["ln2"]), cfg.rms_eps, T, H, _ptr(xp), P, st))
             gemm(xp, lw["wgu"], act, epilogue=EPI_SWIGLU, tile_n=2 * GU_BLOCK)
             gemm(act, lw["wdown"], h, epilogue=EPI_RESID)
-            n += 7 + (P == 2)
+            n += 7 + (not self.attn_bf16)
         self.launches += n
         return h

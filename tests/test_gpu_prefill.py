@@ -132,7 +132,7 @@ def test_prefill_fills_the_cache_like_the_oracle(cfg, planes):
     logits = (hn @ ref.lm_head.T)[0]
     diff = (logits - want_logits).abs().max().item()
     assert diff <= (2e-3 if planes == 2 else 2e-1), diff
-    assert pre.launches == 1 + cfg.n_layers * (8 if planes == 2 else 7)
+    assert pre.launches == 1 + cfg.n_layers * (8 if planes == 2 else 7)   # own kernels; attention is the library operator
     plug.close()
 
 
