@@ -29,6 +29,12 @@ extern "C" {
 #define ADAMK_PF_EPI_SWIGLU 2 /* out bf16 planes [parts_out][T, ldo] = split(silu(gate) * up); the weight   */
                               /* interleaves gate and up rows in blocks of tile_n / 2 features              */
 
+/* GEMM tile shapes (tokens x output features) */
+#define ADAMK_PF_TILE_AUTO 0
+#define ADAMK_PF_TILE_128 128  /* 128 x 128, one CTA                                                         */
+#define ADAMK_PF_TILE_256 256  /* 128 x 256, one CTA                                                         */
+#define ADAMK_PF_TILE_PAIR 512 /* 256 x 256 on a CTA pair (cluster of 2, tcgen05.mma.cta_group::2)           */
+
 typedef void* adamk_pf_stream; /* cudaStream_t */
 
 const char* adamk_prefill_last_error(void);
@@ -37,7 +43,8 @@ const char* adamk_prefill_last_error(void);
  *   x_planes  bf16 [parts][T, K] row-major: the activation as `parts` bf16 planes whose sum is the fp32 value
  *             (parts 2 = hi + lo, ~2^-17 relative; parts 1 = plain bf16).
  *   w         bf16 [N, K] row-major (Hugging Face layout).
- *   tile_n    0 (choose), 128 or 256 output features per tile.
+ *   tile_n    one of ADAMK_PF_TILE_*; the SwiGLU weight interleaves gate / up in blocks of 128 features for the
+ *             256-wide tiles (ADAMK_PF_TILE_256 / _PAIR) and 64 for ADAMK_PF_TILE_128.
  * K, N and ldo must be multiples of 8 and the pointers 16-byte aligned. */
 int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void* w, int N, const float* bias, void* out, int ldo,
                        int epilogue, int parts_out, long long part_stride, int tile_n, adamk_pf_stream stream);

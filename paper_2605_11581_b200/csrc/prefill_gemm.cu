@@ -180,6 +180,85 @@ __device__ __forceinline__ uint2 split4(const float4 v, uint2* lo) {
   return make_uint2(pack(h0, h1), pack(h2, h3));
 }
 
+// Drain one accumulator slice (this warp's 32 rows x w columns at t_addr) with the fused epilogue.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& g, uint32_t t_addr, float* patch, int row0, int n_blk, int sub, int w,
+                                              int lane, int sub_row, int cg) {
+  if constexpr (EPI == ADAMK_PF_EPI_SWIGLU) {
+    const int halfw = w / 2;
+    const int f0 = n_blk * (BN / 2) + sub * halfw;
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.out);
+#pragma unroll 1
+    for (int c = 0; c < halfw; c += 32) {
+      uint32_t ga[32], up[32];
+      tmem_ld32(t_addr + c, ga);
+      tmem_ld32(t_addr + halfw + c, up);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float a = __uint_as_float(ga[j + i]);
+          v[i] = __fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(up[j + i]);   // fast divide: the IEEE slow path costs more than the tile
+        }
+        *reinterpret_cast<float4*>(patch + lane * kStagePitch + j) = make_float4(v[0], v[1], v[2], v[3]);
+      }
+      __syncwarp();
+      const int f = f0 + c + cg;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = i * 4 + sub_row, row = row0 + r;
+        const float4 v = *reinterpret_cast<const float4*>(patch + r * kStagePitch + cg);
+        if (row < g.T && f < g.N / 2) {
+          uint2 lo;
+          const uint2 hi = split4(v, &lo);
+          __nv_bfloat16* dst = out + (long long)row * g.ldo + f;
+          *reinterpret_cast<uint2*>(dst) = hi;
+          if (g.parts_out == 2) *reinterpret_cast<uint2*>(dst + g.part_stride) = lo;
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    const int n0 = n_blk * BN + sub * w;
+    float* out = static_cast<float*>(g.out);
+#pragma unroll 1
+    for (int c = 0; c < w; c += 32) {
+      uint32_t acc[32];
+      tmem_ld32(t_addr + c, acc);
+      const int col = n0 + c + cg;
+      const bool col_ok = col < g.N;
+      float4 o[8];
+      if constexpr (EPI == ADAMK_PF_EPI_RESID) {   // residual rows: in flight while the accumulator arrives
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = row0 + i * 4 + sub_row;
+          o[i] = (row < g.T && col_ok) ? *reinterpret_cast<const float4*>(out + (long long)row * g.ldo + col) : make_float4(0, 0, 0, 0);
+        }
+      } else {
+        const float4 b = (g.bias != nullptr && col_ok) ? *reinterpret_cast<const float4*>(g.bias + col) : make_float4(0, 0, 0, 0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = b;
+      }
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(patch + lane * kStagePitch + j) =
+            make_float4(__uint_as_float(acc[j]), __uint_as_float(acc[j + 1]), __uint_as_float(acc[j + 2]), __uint_as_float(acc[j + 3]));
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = i * 4 + sub_row, row = row0 + r;
+        float4 v = *reinterpret_cast<const float4*>(patch + r * kStagePitch + cg);
+        v.x += o[i].x; v.y += o[i].y; v.z += o[i].z; v.w += o[i].w;
+        if (row < g.T && col_ok) *reinterpret_cast<float4*>(out + (long long)row * g.ldo + col) = v;
+      }
+      __syncwarp();
+    }
+  }
+}
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, const GemmArgs g) {
@@ -281,79 +360,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
       mbar_wait(&acc_full[as], (n >> 1) & 1);
       tc_fence_after();
       const uint32_t t_addr = tmem_base + as * BN + (uint32_t(quarter * 32) << 16);
-      if constexpr (EPI == ADAMK_PF_EPI_SWIGLU) {
-        const int halfw = it.w / 2;
-        const int f0 = it.n_blk * (BN / 2) + it.sub * halfw;
-        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.out);
-#pragma unroll 1
-        for (int c = 0; c < halfw; c += 32) {
-          uint32_t ga[32], up[32];
-          tmem_ld32(t_addr + c, ga);
-          tmem_ld32(t_addr + halfw + c, up);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            float v[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float a = __uint_as_float(ga[j + i]);
-              v[i] = __fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(up[j + i]);   // fast divide: the IEEE slow path costs more than the tile
-            }
-            *reinterpret_cast<float4*>(patch + lane * kStagePitch + j) = make_float4(v[0], v[1], v[2], v[3]);
-          }
-          __syncwarp();
-          const int f = f0 + c + cg;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = i * 4 + sub_row, row = row0 + r;
-            const float4 v = *reinterpret_cast<const float4*>(patch + r * kStagePitch + cg);
-            if (row < g.T && f < g.N / 2) {
-              uint2 lo;
-              const uint2 hi = split4(v, &lo);
-              __nv_bfloat16* dst = out + (long long)row * g.ldo + f;
-              *reinterpret_cast<uint2*>(dst) = hi;
-              if (g.parts_out == 2) *reinterpret_cast<uint2*>(dst + g.part_stride) = lo;
-            }
-          }
-          __syncwarp();
-        }
-      } else {
-        const int n0 = it.n_blk * BN + it.sub * it.w;
-        float* out = static_cast<float*>(g.out);
-#pragma unroll 1
-        for (int c = 0; c < it.w; c += 32) {
-          uint32_t acc[32];
-          tmem_ld32(t_addr + c, acc);
-          const int col = n0 + c + cg;
-          const bool col_ok = col < g.N;
-          float4 o[8];
-          if constexpr (EPI == ADAMK_PF_EPI_RESID) {   // residual rows: in flight while the accumulator arrives
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int row = row0 + i * 4 + sub_row;
-              o[i] = (row < g.T && col_ok) ? *reinterpret_cast<const float4*>(out + (long long)row * g.ldo + col) : make_float4(0, 0, 0, 0);
-            }
-          } else {
-            const float4 b = (g.bias != nullptr && col_ok) ? *reinterpret_cast<const float4*>(g.bias + col) : make_float4(0, 0, 0, 0);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) o[i] = b;
-          }
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(patch + lane * kStagePitch + j) =
-                make_float4(__uint_as_float(acc[j]), __uint_as_float(acc[j + 1]), __uint_as_float(acc[j + 2]), __uint_as_float(acc[j + 3]));
-          __syncwarp();
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = i * 4 + sub_row, row = row0 + r;
-            float4 v = *reinterpret_cast<const float4*>(patch + r * kStagePitch + cg);
-            v.x += o[i].x; v.y += o[i].y; v.z += o[i].z; v.w += o[i].w;
-            if (row < g.T && col_ok) *reinterpret_cast<float4*>(out + (long long)row * g.ldo + col) = v;
-          }
-          __syncwarp();
-        }
-      }
+      epilogue_tile<BN, EPI>(g, t_addr, patch, row0, it.n_blk, it.sub, it.w, lane, sub_row, cg);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[as]);
@@ -365,6 +372,204 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(2 * BN) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------------------------------------
+// CTA-pair variant: two CTAs of one cluster (the two SMs of a TPC) share a 256 x 256 tile.  Each CTA stages its
+// own 128 token rows and HALF of the weight tile (128 rows), tcgen05.mma.cta_group::2 issued by the leader reads
+// both halves, and each CTA keeps the accumulator of its own 128 rows in its own tensor memory.  Per SM that is
+// 32 KB of operands per k block instead of 48 KB for the same tensor work, and six ring stages instead of four:
+// the single-CTA kernel is bound by the bytes it can keep in flight from L2, this one is not.
+
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;   // shared::cluster address of the same offset in the pair's leader CTA
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint64_t* leader_bar, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(leader_bar) & kPeerMask)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {   // arrive on the leader CTA's copy of `bar`
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void umma_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  const uint32_t z = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {   // arrive on `bar` in both CTAs of the pair
+  const uint16_t both = 3;
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "h"(both)
+               : "memory");
+}
+
+struct PairSmem {
+  static constexpr int BN = 256;
+  static constexpr int kStageA = BM * BK * 2;
+  static constexpr int kStageB = (BN / 2) * BK * 2;
+  static constexpr int kStage = kStageA + kStageB;
+  static constexpr int kStages = 6;
+  static constexpr int kEpi = 4 * kStageFloats * 4;
+  static constexpr int kBytes = kStages * kStage + kEpi + 1024 + 256;
+};
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+gemm_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, const GemmArgs g) {
+  using S = PairSmem;
+  constexpr int BN = S::BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* epi_stage = reinterpret_cast<float*>(smem + S::kStages * S::kStage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kStages * S::kStage + S::kEpi);
+  uint64_t* empty = full + S::kStages;
+  uint64_t* acc_full = empty + S::kStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int m_tiles = (g.T + 2 * BM - 1) / (2 * BM);
+  const int kb_per_part = (g.K + BK - 1) / BK;
+  const int n_kb = kb_per_part * g.parts;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
+    for (int s = 0; s < S::kStages; ++s) {
+      mbar_init(&full[s], 2);    // leader: arrive.expect_tx of both CTAs' bytes; peer: plain remote arrive
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 8);   // the four epilogue warps of each CTA
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(2 * BN) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // item -> (row block of 256 tokens, tile column, column slice); slices of the last wave are w = 128 wide
+  auto decode = [&](int idx, int& m0, int& n_blk, int& sub, int& w) {
+    int tile = idx;
+    sub = 0;
+    w = BN;
+    if (idx >= g.main_items) {
+      const int t = idx - g.main_items;
+      tile = g.main_items + t / g.tail_split;
+      sub = t % g.tail_split;
+      w = BN / g.tail_split;
+    }
+    m0 = (tile % m_tiles) * 2 * BM;
+    n_blk = tile / m_tiles;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int idx = pair; idx < g.n_items; idx += n_pairs) {
+        int m0, n_blk, sub, w;
+        decode(idx, m0, n_blk, sub, w);
+        const int boxes = w / (2 * BOXN);   // this CTA's half of the slice
+        const uint32_t bytes = S::kStageA + boxes * BOXN * BK * 2;
+        const int wrow0 = (EPI == ADAMK_PF_EPI_SWIGLU) ? n_blk * BN + int(rank) * (BN / 2) + sub * (w / 2)
+                                                       : n_blk * BN + sub * w + int(rank) * (w / 2);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          const int part = kb / kb_per_part, k0 = (kb - part * kb_per_part) * BK;
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStage;
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * bytes);
+          else mbar_arrive_leader(&full[stage]);
+          tma_load_2d_pair(&map_x, &full[stage], sa, k0, part * g.T + m0 + int(rank) * BM);
+          for (int j = 0; j < boxes; ++j)
+            tma_load_2d_pair(&map_w, &full[stage], sa + S::kStageA + j * (BOXN * BK * 2), k0, wrow0 + j * BOXN);
+          if (++stage == S::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int n = 0;
+      for (int idx = pair; idx < g.n_items; idx += n_pairs, ++n) {
+        int m0, n_blk, sub, w;
+        decode(idx, m0, n_blk, sub, w);
+        const uint32_t idesc = instr_desc(2 * BM, w);
+        const int as = n & 1;
+        mbar_wait(&acc_empty[as], ((n >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * S::kStage);
+          const uint64_t a_desc = smem_desc_sw128(a_addr), b_desc = smem_desc_sw128(a_addr + S::kStageA);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            umma_pair(d_tmem, a_desc + uint64_t(k * UK * 2 >> 4), b_desc + uint64_t(k * UK * 2 >> 4), idesc, (kb | k) != 0);
+          umma_commit_pair(&empty[stage]);
+          if (++stage == S::kStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_pair(&acc_full[as]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    float* patch = epi_stage + quarter * kStageFloats;
+    const int sub_row = lane >> 3, cg = (lane & 7) * 4;
+    int n = 0;
+    for (int idx = pair; idx < g.n_items; idx += n_pairs, ++n) {
+      int m0, n_blk, sub, w;
+      decode(idx, m0, n_blk, sub, w);
+      const int as = n & 1;
+      const int row0 = m0 + int(rank) * BM + quarter * 32;
+      mbar_wait(&acc_full[as], (n >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t_addr = tmem_base + as * BN + (uint32_t(quarter * 32) << 16);
+      epilogue_tile<BN, EPI>(g, t_addr, patch, row0, n_blk, sub, w, lane, sub_row, cg);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (rank == 0) mbar_arrive(&acc_empty[as]);
+        else mbar_arrive_leader(&acc_empty[as]);
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(2 * BN) : "memory");
   }
 }
 
@@ -443,6 +648,37 @@ static int launch(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& 
   return ADAMK_PF_OK;
 }
 
+template <int EPI>
+static int launch_pair(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& g_in, int n_sms, cudaStream_t stream) {
+  static bool configured = false;
+  auto kern = gemm_pair_kernel<EPI>;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairSmem::kBytes);
+    if (e != cudaSuccess) {
+      snprintf(g_err, sizeof g_err, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+      return ADAMK_PF_E_CUDA;
+    }
+    configured = true;
+  }
+  constexpr int BN = PairSmem::BN;
+  const int tiles = ((g_in.T + 2 * BM - 1) / (2 * BM)) * ((g_in.N + BN - 1) / BN);
+  const int max_pairs = n_sms / 2;
+  const int pairs = tiles < max_pairs ? tiles : max_pairs;
+  const int rem = tiles % pairs;
+  const int split = (rem > 0 && rem * 2 <= pairs) ? 2 : 1;   // a slice is at least one 64-row weight box per CTA
+  GemmArgs g = g_in;
+  g.main_items = tiles - rem;
+  g.tail_split = split;
+  g.n_items = g.main_items + rem * split;
+  kern<<<2 * pairs, kThreads, PairSmem::kBytes, stream>>>(mx, mw, g);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof g_err, "prefill gemm (CTA pair) launch: %s", cudaGetErrorString(e));
+    return ADAMK_PF_E_CUDA;
+  }
+  return ADAMK_PF_OK;
+}
+
 }  // namespace pf
 
 extern "C" {
@@ -464,24 +700,52 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
     snprintf(g_err, sizeof g_err, "prefill gemm: operands must be 16-byte aligned");
     return ADAMK_PF_E_INVALID;
   }
-  if (tile_n == 0) tile_n = (epilogue == ADAMK_PF_EPI_SWIGLU || N >= 1024) ? 256 : 128;
-  if (tile_n != 128 && tile_n != 256) {
-    snprintf(g_err, sizeof g_err, "prefill gemm: tile_n must be 0, 128 or 256");
-    return ADAMK_PF_E_INVALID;
-  }
-  if (epilogue == ADAMK_PF_EPI_SWIGLU && (N % tile_n != 0 || (parts_out != 1 && parts_out != 2))) {
-    snprintf(g_err, sizeof g_err, "prefill gemm: SwiGLU epilogue needs N %% tile_n == 0 and 1 or 2 output planes");
-    return ADAMK_PF_E_INVALID;
-  }
   int dev = 0, n_sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
     snprintf(g_err, sizeof g_err, "prefill gemm: no CUDA device");
     return ADAMK_PF_E_CUDA;
   }
+  if (tile_n == 0) {
+    // 256-wide tiles for wide outputs; between one CTA per tile and a CTA pair per 256 x 256 tile take the one whose
+    // last wave is fuller (tile times are equal: a pair does twice the work on twice the SMs), pairs on a tie.
+    if (N < 1024 && epilogue != ADAMK_PF_EPI_SWIGLU) {
+      tile_n = 128;
+    } else {
+      auto waves = [](long long tiles, int units, int max_split) {
+        const long long full = tiles / units, rem = tiles % units;
+        int split = 1;
+        while (rem > 0 && split * 2 <= max_split && rem * split * 2 <= units) split *= 2;
+        return double(full) + (rem ? 1.0 / split : 0.0);
+      };
+      const long long n_t = (N + 255) / 256;
+      const double single = waves((long long)((T + BM - 1) / BM) * n_t, n_sms, epilogue == ADAMK_PF_EPI_SWIGLU ? 2 : 4);
+      const double paired = waves((long long)((T + 2 * BM - 1) / (2 * BM)) * n_t, n_sms / 2, 2);
+      tile_n = (T > BM && paired <= single) ? ADAMK_PF_TILE_PAIR : 256;
+    }
+  }
+  if (tile_n != 128 && tile_n != 256 && tile_n != ADAMK_PF_TILE_PAIR) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: tile must be 0, 128, 256 or ADAMK_PF_TILE_PAIR");
+    return ADAMK_PF_E_INVALID;
+  }
+  const bool pair = tile_n == ADAMK_PF_TILE_PAIR;
+  if (pair) tile_n = 256;
+  if (epilogue == ADAMK_PF_EPI_SWIGLU && (N % tile_n != 0 || (parts_out != 1 && parts_out != 2))) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: SwiGLU epilogue needs N %% tile_n == 0 and 1 or 2 output planes");
+    return ADAMK_PF_E_INVALID;
+  }
   CUtensorMap mx, mw;
   if (!make_map(&mx, x_planes, (long long)parts * T, K, BM) || !make_map(&mw, w, N, K, BOXN)) return ADAMK_PF_E_CUDA;
   GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride, 0, 1, 0};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (pair) {
+    switch (epilogue) {
+      case ADAMK_PF_EPI_STORE: return launch_pair<ADAMK_PF_EPI_STORE>(mx, mw, g, n_sms, s);
+      case ADAMK_PF_EPI_RESID: return launch_pair<ADAMK_PF_EPI_RESID>(mx, mw, g, n_sms, s);
+      case ADAMK_PF_EPI_SWIGLU: return launch_pair<ADAMK_PF_EPI_SWIGLU>(mx, mw, g, n_sms, s);
+    }
+    snprintf(g_err, sizeof g_err, "prefill gemm: unknown epilogue %d", epilogue);
+    return ADAMK_PF_E_INVALID;
+  }
   switch (epilogue * 1000 + tile_n) {
     case ADAMK_PF_EPI_STORE * 1000 + 128: return launch<128, ADAMK_PF_EPI_STORE>(mx, mw, g, n_sms, s);
     case ADAMK_PF_EPI_STORE * 1000 + 256: return launch<256, ADAMK_PF_EPI_STORE>(mx, mw, g, n_sms, s);

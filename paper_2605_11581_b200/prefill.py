@@ -27,7 +27,8 @@ from .plugin import AdamkError, load_library
 from .weights import DecoderWeights
 
 EPI_STORE, EPI_RESID, EPI_SWIGLU = 0, 1, 2
-GU_BLOCK = 128   # features per gate / up block of the interleaved weight = half of the 256-wide GEMM tile
+TILE_AUTO, TILE_128, TILE_256, TILE_PAIR = 0, 128, 256, 512   # include/adamk_prefill.h ADAMK_PF_TILE_*
+GU_BLOCK = 128   # features per gate / up block of the interleaved weight = half of a 256-wide GEMM tile
 
 PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
                    "adamk_prefill_split", "adamk_prefill_rope_store")
@@ -178,7 +179,7 @@ class TensorCorePrefill:
                 _ok(lib.adamk_prefill_split(_ptr(a.float().contiguous()), T * nq * D, _ptr(ap), P, st))
             gemm(ap[:1] if self.attn_bf16 else ap, lw["wo"], h, epilogue=EPI_RESID)
             _ok(lib.adamk_prefill_rmsnorm_split(_ptr(h), _ptr(lw["ln2"]), cfg.rms_eps, T, H, _ptr(xp), P, st))
-            gemm(xp, lw["wgu"], act, epilogue=EPI_SWIGLU, tile_n=2 * GU_BLOCK)
+            gemm(xp, lw["wgu"], act, epilogue=EPI_SWIGLU)
             gemm(act, lw["wdown"], h, epilogue=EPI_RESID)
             n += 7 + (not self.attn_bf16)
         self.launches += n

@@ -30,8 +30,10 @@ def _planes(x, parts):
 
 
 @pytest.mark.parametrize("T,K,N,parts,tile_n", [
+    # tile_n: 128 / 256 = one CTA per 128 x tile_n tile, 512 = a CTA pair per 256 x 256 tile, 0 = the library's choice
     (128, 64, 128, 1, 128), (128, 256, 256, 1, 256), (1, 64, 8, 1, 128), (300, 1536, 2048, 2, 0), (300, 1536, 2048, 2, 128),
-    (77, 192, 328, 1, 128), (77, 200, 328, 2, 256), (2048, 3584, 4608, 2, 0), (4096, 1536, 2048, 1, 0)])
+    (77, 192, 328, 1, 128), (77, 200, 328, 2, 256), (2048, 3584, 4608, 2, 0), (4096, 1536, 2048, 1, 0),
+    (256, 256, 256, 1, 512), (300, 1536, 2048, 2, 512), (77, 200, 328, 1, 512), (4096, 1536, 2048, 1, 512), (1100, 512, 9728, 2, 512)])
 def test_gemm_store_bias(T, K, N, parts, tile_n):
     from paper_2605_11581_b200 import prefill as P
 
@@ -50,7 +52,8 @@ def test_gemm_store_bias(T, K, N, parts, tile_n):
         assert (out.double() - exact).abs().max().item() <= 1e-4 * max(1.0, exact.abs().max().item())
 
 
-@pytest.mark.parametrize("T,K,N,parts,tile_n", [(1000, 8960, 1536, 2, 0), (77, 192, 328, 1, 128), (640, 1536, 1536, 1, 256)])
+@pytest.mark.parametrize("T,K,N,parts,tile_n", [(1000, 8960, 1536, 2, 0), (77, 192, 328, 1, 128), (640, 1536, 1536, 1, 256),
+                                                 (640, 1536, 1536, 1, 512), (4096, 3584, 3584, 1, 512), (4096, 3584, 3584, 2, 256)])
 def test_gemm_residual(T, K, N, parts, tile_n):
     from paper_2605_11581_b200 import prefill as P
 
@@ -65,7 +68,8 @@ def test_gemm_residual(T, K, N, parts, tile_n):
     assert err <= 4e-5 * max(1.0, want.abs().max().item()), err
 
 
-@pytest.mark.parametrize("T,K,I,parts,tile_n", [(520, 1536, 1280, 2, 256), (130, 512, 512, 1, 128), (33, 64, 704, 2, 256)])
+@pytest.mark.parametrize("T,K,I,parts,tile_n", [(520, 1536, 1280, 2, 256), (130, 512, 512, 1, 128), (33, 64, 704, 2, 256),
+                                                 (520, 1536, 1280, 2, 512), (33, 64, 704, 1, 512), (2500, 256, 9600, 1, 512)])
 def test_gemm_swiglu(T, K, I, parts, tile_n):
     """Fused gate/up GEMM: silu(gate) * up, split into bf16 planes, on an interleaved (and zero-padded) weight."""
     from paper_2605_11581_b200 import prefill as P
@@ -74,7 +78,7 @@ def test_gemm_swiglu(T, K, I, parts, tile_n):
     x = torch.randn(T, K, device="cuda", generator=g)
     wg = (torch.randn(I, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
     wu = (torch.randn(I, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
-    w = P.interleave_gate_up(wg, wu, block=tile_n // 2)
+    w = P.interleave_gate_up(wg, wu, block=64 if tile_n == 128 else 128)
     i_pad = w.shape[0] // 2
     xp = _planes(x, parts)
     xs = xp.double().sum(0)

@@ -26,7 +26,7 @@ def check(T, K, N, parts, epi, tile_n=0, seed=0):
     xp = planes_of(x, parts)
     ref = xp.double().sum(0) @ w.double().T
     if epi == P.EPI_SWIGLU:
-        blk = tile_n // 2 if tile_n else 128
+        blk = 64 if tile_n == 128 else 128
         I = N // 2
         r = ref.view(T, I // blk, 2, blk)
         gate, up = r[:, :, 0].reshape(T, I), r[:, :, 1].reshape(T, I)
@@ -85,7 +85,7 @@ def bench(T, K, N, parts, epi=P.EPI_STORE, tile_n=0, iters=20, rounds=3):
         lib.append(timed(lambda: torch.matmul(x[0], w.T)))
     ms, ms_lib = sorted(ours)[rounds // 2], sorted(lib)[rounds // 2]
     tf = 2.0 * T * K * N * parts / ms / 1e9
-    print(f"bench T {T} K {K} N {N} planes {parts} epi {epi}: {ms:.3f} ms {tf:.0f} TFLOP/s | cuBLAS bf16 (1 plane, no epilogue) "
+    print(f"bench T {T} K {K} N {N} planes {parts} epi {epi} tile {tile_n}: {ms:.3f} ms {tf:.0f} TFLOP/s | cuBLAS bf16 (1 plane, no epilogue) "
           f"{ms_lib:.3f} ms {2.0 * T * K * N / ms_lib / 1e9:.0f} TFLOP/s | per-plane time ratio {ms / parts / ms_lib:.2f}", flush=True)
 
 
@@ -100,15 +100,23 @@ if __name__ == "__main__":
     ok &= check(520, 1536, 2560, 2, P.EPI_SWIGLU, 256)
     ok &= check(130, 512, 1024, 1, P.EPI_SWIGLU, 128)
     ok &= check(2048, 3584, 4608, 2, P.EPI_STORE)
+    for T in (256, 300, 77, 2048):
+        ok &= check(T, 256, 256, 1, P.EPI_STORE, 512)
+        ok &= check(T, 1536, 2048, 2, P.EPI_STORE, 512)
+        ok &= check(T, 1536, 1320, 1, P.EPI_RESID, 512)
+        ok &= check(T, 512, 2560, 2, P.EPI_SWIGLU, 512)
+    ok &= check(4096, 3584, 3584, 1, P.EPI_RESID, 512)
+    ok &= check(4096, 1536, 17920, 1, P.EPI_SWIGLU, 512)
     print("ALL OK" if ok else "FAILED", flush=True)
     if len(sys.argv) > 1 and sys.argv[1] == "quick":
         sys.exit(0 if ok else 1)
     for parts in (1, 2):
-        bench(4096, 3584, 4608, parts)
-        bench(4096, 3584, 3584, parts, P.EPI_RESID)
-        bench(4096, 3584, 37888, parts, P.EPI_SWIGLU, 256)
-        bench(4096, 18944, 3584, parts, P.EPI_RESID)
-        bench(4096, 1536, 2048, parts)
-        bench(4096, 1536, 17920, parts, P.EPI_SWIGLU, 256)
-        bench(4096, 8960, 1536, parts, P.EPI_RESID)
+        for tile in (256, 512):
+            bench(4096, 3584, 4608, parts, tile_n=tile)
+            bench(4096, 3584, 3584, parts, P.EPI_RESID, tile)
+            bench(4096, 3584, 37888, parts, P.EPI_SWIGLU, tile)
+            bench(4096, 18944, 3584, parts, P.EPI_RESID, tile)
+            bench(4096, 1536, 2048, parts, tile_n=tile)
+            bench(4096, 1536, 17920, parts, P.EPI_SWIGLU, tile)
+            bench(4096, 8960, 1536, parts, P.EPI_RESID, tile)
     sys.exit(0 if ok else 1)
