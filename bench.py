@@ -149,6 +149,46 @@ def run_reference(args) -> None:
     print(json.dumps(line))
 
 
+def prefill_sample(cfg, w, dev, local: int, tokens: int = 4096, iters: int = 5) -> dict:
+    """Extra, outside the timed decode region: the Prefill half of the hybrid engine on the
+    hand-written tcgen05 GEMM (paper_2605_11581_b200/prefill.py), 4096 prompt tokens, against the tensor roofline
+    (MEASURED_PEAKS.json sustained bf16 TFLOP/s).  GEMM FLOPs only: 2 x tokens x layer weight elements x planes."""
+    from paper_2605_11581_b200.plugin import MegaKernelPlugin
+    from paper_2605_11581_b200.prefill import TensorCorePrefill
+
+    plug = MegaKernelPlugin(cfg, default_schedule(cfg), max_ctx=tokens + 16, device=local)
+    plug.bind_weights(w)
+    toks = torch.randint(0, cfg.vocab, (tokens,), generator=torch.Generator().manual_seed(2)).to(dev)
+    peak = None
+    pfile = ROOT / "MEASURED_PEAKS.json"
+    if pfile.exists():
+        peak = json.loads(pfile.read_text()).get("bf16_tflops_sustained")
+    out = {"tokens": tokens, "attention": "library flash (bf16)", "peak_tflops": peak, "peak_kind": "measured sustained cuBLAS bf16"}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for planes in (1, 2):
+        pre = TensorCorePrefill(cfg, w, plug, planes=planes, attention="bf16")
+        for _ in range(3):
+            pre.run(toks)
+        torch.cuda.synchronize(dev)
+        n0 = pre.launches
+        e0.record()
+        for _ in range(iters):
+            pre.run(toks)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / iters
+        mats = cfg.qkv_rows * cfg.hidden + cfg.hidden * cfg.q_dim + 3 * cfg.intermediate * cfg.hidden
+        flops = 2.0 * tokens * mats * cfg.n_layers * planes
+        # the O projection always reads the single bf16 plane attention produces
+        flops -= 2.0 * tokens * cfg.q_dim * cfg.hidden * cfg.n_layers * (planes - 1)
+        out[f"planes{planes}"] = {"ms": ms, "tokens_per_s": tokens * 1e3 / ms, "gemm_tflops": flops / ms / 1e9,
+                                  "frac_of_peak": None if not peak else flops / ms / 1e9 / peak,
+                                  "own_kernel_launches": (pre.launches - n0) // iters}
+        del pre
+    plug.close()
+    return out
+
+
 def run_ours(args) -> None:
     from paper_2605_11581_b200.plugin import MegaKernelPlugin
 
@@ -267,6 +307,8 @@ def run_ours(args) -> None:
                      "algorithmic_bytes_per_launch": bytes_per_launch, "kernel": "adamk_decode_kernel",
                      "launch_ms": ms},
     })
+    if tp == 1 and not args.no_prefill:
+        line["prefill"] = prefill_sample(full_cfg, w, dev, local)
     if not args.no_cpu_baseline:
         w_cpu = random_weights(full_cfg, seed=0, device=dev).to("cpu") if tp > 1 else w.to("cpu")
         res = cpu_decode_sample(full_cfg, w_cpu, prompt, n_steps=args.cpu_steps)
@@ -284,6 +326,7 @@ def main() -> None:
     ap.add_argument("--model", default="qwen2.5-1.5b")
     ap.add_argument("--cpu-steps", type=int, default=48, help="decode steps of the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the extra tensor-core Prefill sample")
     ap.add_argument("--tp", action="store_true", help="N > 1: tensor-parallel shards of one sequence instead of N replicas")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -8,11 +8,11 @@ from paper_2605_11581_b200 import prefill as P
 parts = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 T, H, I = 4096, 3584, 18944
 x = torch.randn(parts, T, H, device="cuda").to(torch.bfloat16)
-wgu = torch.randn(2 * I, H, device="cuda").to(torch.bfloat16)
-wd = torch.randn(H, I, device="cuda").to(torch.bfloat16)
+wgu = (torch.randn(2 * I, H, device="cuda") / H ** 0.5).to(torch.bfloat16)
+wd = (torch.randn(H, I, device="cuda") / I ** 0.5).to(torch.bfloat16)
 act = torch.zeros(parts, T, I, dtype=torch.bfloat16, device="cuda")
 h = torch.zeros(T, H, device="cuda")
 for _ in range(2):
-    P.gemm(x, wgu, act, epilogue=P.EPI_SWIGLU, tile_n=256)
+    P.gemm(x, wgu, act, epilogue=P.EPI_SWIGLU)
     P.gemm(act, wd, h, epilogue=P.EPI_RESID)
 torch.cuda.synchronize()
