@@ -35,6 +35,9 @@ extern "C" {
 #define ADAMK_PF_TILE_256 256  /* 128 x 256, one CTA                                                         */
 #define ADAMK_PF_TILE_PAIR 512 /* 256 x 256 on a CTA pair (cluster of 2, tcgen05.mma.cta_group::2)           */
 
+#define ADAMK_PF_EPI_ATOMIC 3 /* out fp32 [T, ldo] += acc (+ bias once) with fp32 atomics: decode-sized T, where the  */
+                              /* library splits K across SMs to stream the weight at full width (one-CTA tiles)     */
+
 typedef void* adamk_pf_stream; /* cudaStream_t */
 
 const char* adamk_prefill_last_error(void);
@@ -66,6 +69,32 @@ int adamk_prefill_split(const float* x, long long n, void* planes, int parts, ad
 int adamk_prefill_rope_store(const float* qkv, int T, int n_q, int n_kv, int D, const void* q_gain, const void* k_gain, float eps,
                              const float* cos, const float* sin, int pos0, int max_ctx, void* q_out, int q_is_bf16, void* k_cache,
                              void* v_cache, adamk_pf_stream stream);
+
+/* ---- batched decode: one new token per sequence, B sequences per step -------------
+ * The projections are adamk_prefill_gemm with T = B and the ATOMIC / SWIGLU / STORE epilogues; these are the operators
+ * between them.  Caches: bf16 [B][n_kv][max_ctx][D] per layer (seq_stride = elements between sequences). */
+
+/* rmsnorm_split that also clears `zero_n` floats at `zero` (the fp32 targets of the ATOMIC GEMMs that follow). */
+int adamk_batch_rmsnorm_split(const float* h, const void* gain, float eps, int B, int H, void* planes, int parts, float* zero, long long zero_n,
+                              adamk_pf_stream stream);
+
+/* rope_store for a batch: token b sits at positions[b] of sequence b; q_out fp32 [n_q][B][D]. */
+int adamk_batch_rope_store(const float* qkv, int B, int n_q, int n_kv, int D, const void* q_gain, const void* k_gain, float eps,
+                           const float* cos, const float* sin, const int32_t* positions, long long seq_stride, int max_ctx, float* q_out,
+                           void* k_cache, void* v_cache, adamk_pf_stream stream);
+
+/* Attention of every sequence's new token over cache rows 0 .. positions[b] (split over 256-row chunks, merged),
+ * output as bf16 planes [parts][B][n_q * D].  workspace: adamk_batch_attention_workspace() bytes. */
+size_t adamk_batch_attention_workspace(int B, int n_q, int D, int max_ctx);
+int adamk_batch_attention(const float* q, const void* k_cache, const void* v_cache, const int32_t* positions, int B, int n_q, int n_kv, int D,
+                          int max_ctx, long long seq_stride, float* workspace, void* out_planes, int parts, adamk_pf_stream stream);
+
+/* planes bf16 [parts][B, I] = split(silu(gate) * up) from gu fp32 [B, 2 I] (gate / up interleaved in blocks of `block`
+ * features, the column order the interleaved gate/up weight produces). */
+int adamk_batch_swiglu_split(const float* gu, int B, int I, int block, void* planes, int parts, adamk_pf_stream stream);
+
+/* next[b] = argmax(logits[b]) (lowest index on ties); when non-null, tokens[b] = next[b] and positions[b] += 1. */
+int adamk_batch_argmax(const float* logits, int B, int V, int32_t* next, int32_t* tokens, int32_t* positions, adamk_pf_stream stream);
 
 #ifdef __cplusplus
 }

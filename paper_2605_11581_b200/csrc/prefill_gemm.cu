@@ -124,6 +124,10 @@ struct GemmArgs {
   int main_items;       // work items [0, main_items) are whole BM x BN tiles ...
   int tail_split;       // ... the remaining tiles are cut into tail_split column slices each (last-wave balance)
   int n_items;
+  int ksplit;           // split-K (EPI_ATOMIC only): every tile item becomes ksplit items over disjoint k-block ranges
+  int kb_per_split;
+  int stacked;          // EPI_ATOMIC with parts * T <= 128: the planes are consecutive rows of ONE token tile, K is walked
+                        // once (the weight is read once), accumulator row r adds into output row r % T
 };
 
 constexpr int BOXN = 64;            // weight rows per TMA box: the slice granularity of a tile
@@ -143,10 +147,14 @@ struct Smem {
 // One unit of work: rows [m0, m0 + BM) x a slice of `w` accumulator columns of tile column n_blk.
 struct Item {
   int m0, n_blk, sub, w;
+  int kb_lo, kb_len;    // k blocks [kb_lo, kb_lo + kb_len) of every plane
 };
 
 template <int BN>
-__device__ __forceinline__ Item decode_item(int idx, const GemmArgs& g, int m_tiles) {
+__device__ __forceinline__ Item decode_item(int idx_k, const GemmArgs& g, int m_tiles, int kb_per_part) {
+  const int idx = idx_k / g.ksplit, ks = idx_k - idx * g.ksplit;
+  const int kb_lo = ks * g.kb_per_split;
+  const int kb_len = min(g.kb_per_split, kb_per_part - kb_lo);
   int tile = idx, sub = 0, w = BN;
   if (idx >= g.main_items) {
     const int t = idx - g.main_items;
@@ -154,7 +162,7 @@ __device__ __forceinline__ Item decode_item(int idx, const GemmArgs& g, int m_ti
     sub = t % g.tail_split;
     w = BN / g.tail_split;
   }
-  return Item{(tile % m_tiles) * BM, tile / m_tiles, sub, w};
+  return Item{(tile % m_tiles) * BM, tile / m_tiles, sub, w, kb_lo, kb_len};
 }
 
 // Weight row of the j-th 64-row box of an item.  SwiGLU tiles hold BN/2 gate rows then the BN/2 up rows of the
@@ -183,7 +191,7 @@ __device__ __forceinline__ uint2 split4(const float4 v, uint2* lo) {
 // Drain one accumulator slice (this warp's 32 rows x w columns at t_addr) with the fused epilogue.
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, uint32_t t_addr, float* patch, int row0, int n_blk, int sub, int w,
-                                              int lane, int sub_row, int cg) {
+                                              int lane, int sub_row, int cg, bool first_split) {
   if constexpr (EPI == ADAMK_PF_EPI_SWIGLU) {
     const int halfw = w / 2;
     const int f0 = n_blk * (BN / 2) + sub * halfw;
@@ -237,7 +245,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, uint32_t t_addr
           o[i] = (row < g.T && col_ok) ? *reinterpret_cast<const float4*>(out + (long long)row * g.ldo + col) : make_float4(0, 0, 0, 0);
         }
       } else {
-        const float4 b = (g.bias != nullptr && col_ok) ? *reinterpret_cast<const float4*>(g.bias + col) : make_float4(0, 0, 0, 0);
+        const float4 b = (g.bias != nullptr && col_ok && first_split) ? *reinterpret_cast<const float4*>(g.bias + col) : make_float4(0, 0, 0, 0);
 #pragma unroll
         for (int i = 0; i < 8; ++i) o[i] = b;
       }
@@ -251,8 +259,16 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, uint32_t t_addr
       for (int i = 0; i < 8; ++i) {
         const int r = i * 4 + sub_row, row = row0 + r;
         float4 v = *reinterpret_cast<const float4*>(patch + r * kStagePitch + cg);
-        v.x += o[i].x; v.y += o[i].y; v.z += o[i].z; v.w += o[i].w;
-        if (row < g.T && col_ok) *reinterpret_cast<float4*>(out + (long long)row * g.ldo + col) = v;
+        if constexpr (EPI == ADAMK_PF_EPI_ATOMIC) {
+          const int rows = g.stacked ? g.parts * g.T : g.T;
+          if (row < rows && col_ok) {
+            if (row < g.T) { v.x += o[i].x; v.y += o[i].y; v.z += o[i].z; v.w += o[i].w; }   // bias: once per output row
+            atomicAdd(reinterpret_cast<float4*>(out + (long long)(g.stacked ? row % g.T : row) * g.ldo + col), v);
+          }
+        } else {
+          v.x += o[i].x; v.y += o[i].y; v.z += o[i].z; v.w += o[i].w;
+          if (row < g.T && col_ok) *reinterpret_cast<float4*>(out + (long long)row * g.ldo + col) = v;
+        }
       }
       __syncwarp();
     }
@@ -275,7 +291,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (g.T + BM - 1) / BM;
   const int kb_per_part = (g.K + BK - 1) / BK;
-  const int n_kb = kb_per_part * g.parts;
+  const int n_work = g.n_items * g.ksplit;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
@@ -303,12 +319,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int idx = blockIdx.x; idx < g.n_items; idx += gridDim.x) {
-        const Item it = decode_item<BN>(idx, g, m_tiles);
+      for (int idx = blockIdx.x; idx < n_work; idx += gridDim.x) {
+        const Item it = decode_item<BN>(idx, g, m_tiles, kb_per_part);
         const int boxes = it.w / BOXN;
         const uint32_t bytes = S::kStageA + boxes * BOXN * BK * 2;
+        const int n_kb = it.kb_len * (g.stacked ? 1 : g.parts);
         for (int kb = 0; kb < n_kb; ++kb) {
-          const int part = kb / kb_per_part, k0 = (kb - part * kb_per_part) * BK;
+          const int part = kb / it.kb_len, k0 = (it.kb_lo + kb - part * it.kb_len) * BK;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStage;
           mbar_expect_tx(&full[stage], bytes);
@@ -324,13 +341,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
       int stage = 0;
       uint32_t phase = 0;
       int n = 0;
-      for (int idx = blockIdx.x; idx < g.n_items; idx += gridDim.x, ++n) {
-        const Item it = decode_item<BN>(idx, g, m_tiles);
+      for (int idx = blockIdx.x; idx < n_work; idx += gridDim.x, ++n) {
+        const Item it = decode_item<BN>(idx, g, m_tiles, kb_per_part);
         const uint32_t idesc = instr_desc(BM, it.w);
         const int as = n & 1;
         mbar_wait(&acc_empty[as], ((n >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
+        const int n_kb = it.kb_len * (g.stacked ? 1 : g.parts);
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -353,14 +371,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
     float* patch = epi_stage + quarter * kStageFloats;
     const int sub_row = lane >> 3, cg = (lane & 7) * 4;
     int n = 0;
-    for (int idx = blockIdx.x; idx < g.n_items; idx += gridDim.x, ++n) {
-      const Item it = decode_item<BN>(idx, g, m_tiles);
+    for (int idx = blockIdx.x; idx < n_work; idx += gridDim.x, ++n) {
+      const Item it = decode_item<BN>(idx, g, m_tiles, kb_per_part);
       const int as = n & 1;
       const int row0 = it.m0 + quarter * 32;
       mbar_wait(&acc_full[as], (n >> 1) & 1);
       tc_fence_after();
       const uint32_t t_addr = tmem_base + as * BN + (uint32_t(quarter * 32) << 16);
-      epilogue_tile<BN, EPI>(g, t_addr, patch, row0, it.n_blk, it.sub, it.w, lane, sub_row, cg);
+      const int rows_live = (EPI == ADAMK_PF_EPI_ATOMIC && g.stacked) ? g.parts * g.T : g.T;
+      if (row0 < rows_live)   // decode-sized T: most warps own no live row and only hand the accumulator back
+        epilogue_tile<BN, EPI>(g, t_addr, patch, row0, it.n_blk, it.sub, it.w, lane, sub_row, cg, it.kb_lo == 0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[as]);
@@ -555,7 +575,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
       mbar_wait(&acc_full[as], (n >> 1) & 1);
       tc_fence_after();
       const uint32_t t_addr = tmem_base + as * BN + (uint32_t(quarter * 32) << 16);
-      epilogue_tile<BN, EPI>(g, t_addr, patch, row0, n_blk, sub, w, lane, sub_row, cg);
+      epilogue_tile<BN, EPI>(g, t_addr, patch, row0, n_blk, sub, w, lane, sub_row, cg, true);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -628,17 +648,41 @@ static int launch(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& 
     configured = true;
   }
   // Work items: whole tiles, except that the tiles of a last partial wave are cut into column slices so that the
-  // wave keeps every SM busy for a fraction of a tile time instead of a few SMs for a whole one.
+  // wave keeps every SM busy for a fraction of a tile time instead of a few SMs for a whole one.  With fewer tiles
+  // than SMs (decode-sized T) every tile is sliced, and the atomic epilogue also splits K.
   const int tiles = ((g_in.T + BM - 1) / BM) * ((g_in.N + BN - 1) / BN);
-  const int grid = tiles < n_sms ? tiles : n_sms;
-  const int rem = tiles % grid;
   const int max_split = (EPI == ADAMK_PF_EPI_SWIGLU) ? BN / (2 * BOXN) : BN / BOXN;
-  int split = 1;
-  while (rem > 0 && split * 2 <= max_split && rem * split * 2 <= grid) split *= 2;
   GemmArgs g = g_in;
-  g.main_items = tiles - rem;
+  int split = 1;
+  const int kb_per_part = (g.K + BK - 1) / BK;
+  g.ksplit = 1;
+  g.kb_per_split = kb_per_part;
+  g.stacked = 0;
+  if (EPI == ADAMK_PF_EPI_ATOMIC) {
+    // decode-sized: whole 32 KB weight boxes per stage and as many K ranges as there are idle SMs keep the most
+    // bytes in flight; all planes ride in one token tile when they fit
+    g.main_items = tiles;
+    g.n_items = tiles;
+    g.stacked = (g.parts * g.T <= BM) ? 1 : 0;
+    if (tiles * 2 <= n_sms) {
+      int want = n_sms / tiles;
+      if (want > kb_per_part) want = kb_per_part;
+      g.kb_per_split = (kb_per_part + want - 1) / want;
+      g.ksplit = (kb_per_part + g.kb_per_split - 1) / g.kb_per_split;
+    }
+  } else if (tiles < n_sms) {
+    while (split * 2 <= max_split && tiles * split * 2 <= n_sms) split *= 2;
+    g.main_items = 0;
+    g.n_items = tiles * split;
+  } else {
+    const int rem = tiles % n_sms;
+    while (rem > 0 && split * 2 <= max_split && rem * split * 2 <= n_sms) split *= 2;
+    g.main_items = tiles - rem;
+    g.n_items = g.main_items + rem * split;
+  }
   g.tail_split = split;
-  g.n_items = g.main_items + rem * split;
+  const long long work = (long long)g.n_items * g.ksplit;
+  const int grid = work < n_sms ? int(work) : n_sms;
   kern<<<grid, kThreads, Smem<BN>::kBytes, stream>>>(mx, mw, g);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -670,6 +714,9 @@ static int launch_pair(const CUtensorMap& mx, const CUtensorMap& mw, const GemmA
   g.main_items = tiles - rem;
   g.tail_split = split;
   g.n_items = g.main_items + rem * split;
+  g.ksplit = 1;
+  g.kb_per_split = (g.K + BK - 1) / BK;
+  g.stacked = 0;
   kern<<<2 * pairs, kThreads, PairSmem::kBytes, stream>>>(mx, mw, g);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -720,7 +767,7 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
       const long long n_t = (N + 255) / 256;
       const double single = waves((long long)((T + BM - 1) / BM) * n_t, n_sms, epilogue == ADAMK_PF_EPI_SWIGLU ? 2 : 4);
       const double paired = waves((long long)((T + 2 * BM - 1) / (2 * BM)) * n_t, n_sms / 2, 2);
-      tile_n = (T > BM && paired <= single) ? ADAMK_PF_TILE_PAIR : 256;
+      tile_n = (T > BM && paired <= single && epilogue != ADAMK_PF_EPI_ATOMIC) ? ADAMK_PF_TILE_PAIR : 256;
     }
   }
   if (tile_n != 128 && tile_n != 256 && tile_n != ADAMK_PF_TILE_PAIR) {
@@ -728,6 +775,10 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
     return ADAMK_PF_E_INVALID;
   }
   const bool pair = tile_n == ADAMK_PF_TILE_PAIR;
+  if (pair && epilogue == ADAMK_PF_EPI_ATOMIC) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: the atomic (split-K) epilogue runs on one-CTA tiles only");
+    return ADAMK_PF_E_INVALID;
+  }
   if (pair) tile_n = 256;
   if (epilogue == ADAMK_PF_EPI_SWIGLU && (N % tile_n != 0 || (parts_out != 1 && parts_out != 2))) {
     snprintf(g_err, sizeof g_err, "prefill gemm: SwiGLU epilogue needs N %% tile_n == 0 and 1 or 2 output planes");
@@ -735,7 +786,7 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
   }
   CUtensorMap mx, mw;
   if (!make_map(&mx, x_planes, (long long)parts * T, K, BM) || !make_map(&mw, w, N, K, BOXN)) return ADAMK_PF_E_CUDA;
-  GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride, 0, 1, 0};
+  GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride, 0, 1, 0, 1, 0, 0};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (pair) {
     switch (epilogue) {
@@ -751,6 +802,8 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
     case ADAMK_PF_EPI_STORE * 1000 + 256: return launch<256, ADAMK_PF_EPI_STORE>(mx, mw, g, n_sms, s);
     case ADAMK_PF_EPI_RESID * 1000 + 128: return launch<128, ADAMK_PF_EPI_RESID>(mx, mw, g, n_sms, s);
     case ADAMK_PF_EPI_RESID * 1000 + 256: return launch<256, ADAMK_PF_EPI_RESID>(mx, mw, g, n_sms, s);
+    case ADAMK_PF_EPI_ATOMIC * 1000 + 128: return launch<128, ADAMK_PF_EPI_ATOMIC>(mx, mw, g, n_sms, s);
+    case ADAMK_PF_EPI_ATOMIC * 1000 + 256: return launch<256, ADAMK_PF_EPI_ATOMIC>(mx, mw, g, n_sms, s);
     case ADAMK_PF_EPI_SWIGLU * 1000 + 128: return launch<128, ADAMK_PF_EPI_SWIGLU>(mx, mw, g, n_sms, s);
     case ADAMK_PF_EPI_SWIGLU * 1000 + 256: return launch<256, ADAMK_PF_EPI_SWIGLU>(mx, mw, g, n_sms, s);
   }

@@ -48,9 +48,11 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bflo
 
 // planes[p][t][:] = split(h[t] * rsqrt(mean(h[t]^2) + eps) * gain)
 __global__ void rmsnorm_split_kernel(const float* __restrict__ h, const __nv_bfloat16* __restrict__ gain, float eps, int H,
-                                     __nv_bfloat16* __restrict__ planes, long long plane_stride, int parts) {
+                                     __nv_bfloat16* __restrict__ planes, long long plane_stride, int parts, float4* zero, long long zero_n4) {
   __shared__ float red[32];
   const long long t = blockIdx.x;
+  // batched decode: clear the fp32 targets of the atomic GEMMs that follow (saves a memset launch per layer)
+  for (long long i = t * blockDim.x + threadIdx.x; i < zero_n4; i += (long long)gridDim.x * blockDim.x) zero[i] = make_float4(0, 0, 0, 0);
   const float* row = h + t * H;
   float ss = 0.f;
   for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
@@ -88,17 +90,21 @@ struct RopeArgs {
   __nv_bfloat16 *k_cache, *v_cache;
   int T, n_q, n_kv, D, max_ctx, pos0, q_is_bf16;
   float eps;
+  const int32_t* positions;   // batched decode: token t sits at positions[t] of sequence t (null: pos0 + t of one sequence)
+  long long seq_stride;       // cache elements between the sequences of consecutive tokens (0 for one sequence)
 };
 
 __global__ void rope_store_kernel(const RopeArgs a) {
   const int t = blockIdx.x, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int heads = a.n_q + 2 * a.n_kv, half = a.D / 2;
   const float* row = a.qkv + (long long)t * heads * a.D;
-  const int pos = a.pos0 + t;
+  const int pos = a.positions != nullptr ? a.positions[t] : a.pos0 + t;
+  __nv_bfloat16* k_cache = a.k_cache + t * a.seq_stride;
+  __nv_bfloat16* v_cache = a.v_cache + t * a.seq_stride;
   for (int hd = threadIdx.x >> 5; hd < heads; hd += nw) {
     const float* x = row + hd * a.D;
     if (hd >= a.n_q + a.n_kv) {   // value head: plain bf16 store
-      __nv_bfloat16* dst = a.v_cache + ((long long)(hd - a.n_q - a.n_kv) * a.max_ctx + pos) * a.D;
+      __nv_bfloat16* dst = v_cache + ((long long)(hd - a.n_q - a.n_kv) * a.max_ctx + pos) * a.D;
       for (int i = lane; i < a.D; i += 32) dst[i] = __float2bfloat16_rn(x[i]);
       continue;
     }
@@ -132,11 +138,242 @@ __global__ void rope_store_kernel(const RopeArgs a) {
           q[i + half] = r2;
         }
       } else {
-        __nv_bfloat16* k = a.k_cache + ((long long)(hd - a.n_q) * a.max_ctx + pos) * a.D;
+        __nv_bfloat16* k = k_cache + ((long long)(hd - a.n_q) * a.max_ctx + pos) * a.D;
         k[i] = __float2bfloat16_rn(r1);
         k[i + half] = __float2bfloat16_rn(r2);
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------------------
+// Batched decode (one new token per sequence): attention over each sequence's cache, and the greedy pick.
+
+constexpr int kAttnChunk = 64;    // cache positions per CTA: small chunks = many CTAs = many loads in flight
+constexpr int kAttnThreads = 128;
+constexpr int kMaxGroup = 8;      // q heads per kv head
+
+__device__ __forceinline__ void bf16x8_to_float(const uint4 u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    f[2 * j] = __uint_as_float(w[j] << 16);
+    f[2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
+  }
+}
+
+// grid (splits, n_kv, B).  Partial softmax of the G q heads of one kv head over positions [s * 64, s * 64 + 64) of
+// sequence b:  part[b][q head][s][0..D) = sum_p exp(score_p - m) v_p,  [D] = m,  [D + 1] = sum_p exp(score_p - m).
+// Every global load of a phase is issued before the first use (the kernel is latency-, not bandwidth-limited).
+template <int D>
+__global__ void __launch_bounds__(kAttnThreads)
+batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache, const __nv_bfloat16* __restrict__ v_cache,
+                          const int32_t* __restrict__ positions, float* __restrict__ part, int B, int n_q, int n_kv, int max_ctx,
+                          long long seq_stride, int splits, float scale) {
+  const int s = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+  const int G = n_q / n_kv;
+  const int ctx = positions[b] + 1;   // the new token's K / V are already in the cache
+  const int p0 = s * kAttnChunk;
+  if (p0 >= ctx) return;              // the merge kernel derives the live split count from positions, too
+  const int n_pos = min(kAttnChunk, ctx - p0);
+  constexpr int NW = kAttnThreads / 32;
+  __shared__ float q_s[kMaxGroup][D];
+  __shared__ float sc[kMaxGroup][kAttnChunk];
+  __shared__ float ml[kMaxGroup][2];
+  __shared__ float ored[NW][kMaxGroup][D];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const __nv_bfloat16* kb = k_cache + b * seq_stride + ((long long)kvh * max_ctx + p0) * D;
+  const __nv_bfloat16* vb = v_cache + b * seq_stride + ((long long)kvh * max_ctx + p0) * D;
+
+  // scores: two threads per position, half a K row each (D/16 16-byte loads in flight per thread)
+  constexpr int HC = D / 16;
+  const int p = tid >> 1, half = tid & 1;
+  uint4 kraw[HC];
+  if (p < n_pos) {
+    const uint4* row = reinterpret_cast<const uint4*>(kb + (long long)p * D) + half * HC;
+#pragma unroll
+    for (int c = 0; c < HC; ++c) kraw[c] = row[c];
+  } else {
+#pragma unroll
+    for (int c = 0; c < HC; ++c) kraw[c] = make_uint4(0, 0, 0, 0);
+  }
+  for (int i = tid; i < G * D; i += kAttnThreads) {
+    const int g = i / D, d = i - g * D;
+    q_s[g][d] = q[((long long)(kvh * G + g) * B + b) * D + d] * scale;
+  }
+  __syncthreads();
+  {
+    float acc[kMaxGroup];
+#pragma unroll
+    for (int g = 0; g < kMaxGroup; ++g) acc[g] = 0.f;
+#pragma unroll
+    for (int c = 0; c < HC; ++c) {
+      float kf[8];
+      bf16x8_to_float(kraw[c], kf);
+      const int d0 = (half * HC + c) * 8;
+#pragma unroll
+      for (int g = 0; g < kMaxGroup; ++g)
+        if (g < G) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[g] = fmaf(q_s[g][d0 + j], kf[j], acc[g]);
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < kMaxGroup; ++g)
+      if (g < G) {
+        const float t = acc[g] + __shfl_xor_sync(0xffffffffu, acc[g], 1);
+        if (half == 0) sc[g][p] = (p < n_pos) ? t : -INFINITY;
+      }
+  }
+  // values: warp w owns positions w, w + 4, ...; issue all of its (coalesced) V rows now, use them after the softmax
+  constexpr int E = D / 32, NV = kAttnChunk / NW;
+  float vreg[NV][E];
+#pragma unroll
+  for (int u = 0; u < NV; ++u) {
+    const int pp = warp + u * NW;
+    if (pp < n_pos) {
+      if constexpr (E == 4) {
+        const uint2 raw = *reinterpret_cast<const uint2*>(vb + (long long)pp * D + lane * 4);
+        vreg[u][0] = __uint_as_float(raw.x << 16); vreg[u][1] = __uint_as_float(raw.x & 0xffff0000u);
+        vreg[u][2] = __uint_as_float(raw.y << 16); vreg[u][3] = __uint_as_float(raw.y & 0xffff0000u);
+      } else {
+        const uint32_t raw = *reinterpret_cast<const uint32_t*>(vb + (long long)pp * D + lane * 2);
+        vreg[u][0] = __uint_as_float(raw << 16); vreg[u][1] = __uint_as_float(raw & 0xffff0000u);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) vreg[u][e] = 0.f;
+    }
+  }
+  __syncthreads();
+  // chunk softmax: warp w handles heads w, w + 4; a lane covers positions lane and lane + 32
+  for (int g = warp; g < G; g += NW) {
+    const float s0 = sc[g][lane], s1 = sc[g][lane + 32];
+    float m = fmaxf(s0, s1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float e0 = __expf(s0 - m), e1 = __expf(s1 - m);   // exp(-inf) = 0 for the positions past the end
+    sc[g][lane] = e0;
+    sc[g][lane + 32] = e1;
+    float l = e0 + e1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) { ml[g][0] = m; ml[g][1] = l; }
+  }
+  __syncthreads();
+  {
+    float o[kMaxGroup][E];
+#pragma unroll
+    for (int g = 0; g < kMaxGroup; ++g)
+#pragma unroll
+      for (int e = 0; e < E; ++e) o[g][e] = 0.f;
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      const int pp = warp + u * NW;
+#pragma unroll
+      for (int g = 0; g < kMaxGroup; ++g)
+        if (g < G) {
+          const float w = sc[g][pp];
+#pragma unroll
+          for (int e = 0; e < E; ++e) o[g][e] = fmaf(w, vreg[u][e], o[g][e]);
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < kMaxGroup; ++g)
+      if (g < G) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) ored[warp][g][lane * E + e] = o[g][e];
+      }
+  }
+  __syncthreads();
+  for (int i = tid; i < G * D; i += kAttnThreads) {
+    const int g = i / D, d = i - g * D;
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += ored[w][g][d];
+    part[(((long long)b * n_q + kvh * G + g) * splits + s) * (D + 2) + d] = t;
+  }
+  if (tid < G) {
+    float* dst = part + (((long long)b * n_q + kvh * G + tid) * splits + s) * (D + 2);
+    dst[D] = ml[tid][0];
+    dst[D + 1] = ml[tid][1];
+  }
+}
+
+// grid (n_q, B): merge the live splits and emit the attention output as bf16 planes [P][B][n_q * D].
+template <int D>
+__global__ void batch_attn_merge_kernel(const float* __restrict__ part, const int32_t* __restrict__ positions, __nv_bfloat16* __restrict__ planes,
+                                        int B, int n_q, int splits, int parts) {
+  const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
+  const int live = (positions[b] + kAttnChunk) / kAttnChunk;   // ceil((pos + 1) / chunk)
+  const float* src = part + ((long long)b * n_q + h) * splits * (D + 2);
+  // the splits' maxima through shared memory (one load each, all in flight), then the weighted sums eight splits at a time
+  extern __shared__ float m_s[];
+  for (int s = d; s < live; s += D) m_s[s] = src[s * (D + 2) + D];
+  __syncthreads();
+  float M = -INFINITY;
+  for (int s = 0; s < live; ++s) M = fmaxf(M, m_s[s]);
+  float num = 0.f, den = 0.f;
+  for (int s0 = 0; s0 < live; s0 += 8) {
+    float ov[8], lv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int s = min(s0 + u, live - 1);
+      ov[u] = src[s * (D + 2) + d];
+      lv[u] = src[s * (D + 2) + D + 1];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float w = (s0 + u < live) ? __expf(m_s[s0 + u] - M) : 0.f;
+      num = fmaf(w, ov[u], num);
+      den = fmaf(w, lv[u], den);
+    }
+  }
+  const long long o = (long long)b * n_q * D + h * D + d;
+  put_split(planes + o, parts == 2 ? planes + (long long)B * n_q * D + o : nullptr, num / den);
+}
+
+// grid B: greedy pick (lowest index on ties), written to next[b]; tokens / positions advanced in place when asked.
+__global__ void batch_argmax_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ next, int32_t* tokens, int32_t* positions) {
+  const int b = blockIdx.x;
+  const float* row = logits + (long long)b * V;
+  float best = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float v = row[i];
+    if (v > best) { best = v; idx = i; }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > best || (ov == best && oi < idx)) { best = ov; idx = oi; }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sv[warp] = best; si[warp] = idx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (blockDim.x >> 5); ++w)
+      if (sv[w] > best || (sv[w] == best && si[w] < idx)) { best = sv[w]; idx = si[w]; }
+    next[b] = idx;
+    if (tokens != nullptr) tokens[b] = idx;
+    if (positions != nullptr) positions[b] += 1;
+  }
+}
+
+// act planes [P][B][I] = split(silu(gate) * up) from gu fp32 [B][2 I] whose columns interleave gate and up in blocks of
+// `block` features (the layout of the fused-SwiGLU GEMM weight).  grid (feature blocks, tokens).
+__global__ void swiglu_split_kernel(const float* __restrict__ gu, int I, int block, __nv_bfloat16* __restrict__ planes, long long plane_stride,
+                                    int parts) {
+  const long long t = blockIdx.y;
+  const float* row = gu + t * 2 * I;
+  __nv_bfloat16* hi = planes + t * I;
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < I; f += gridDim.x * blockDim.x) {
+    const int blk = f / block, j = f - blk * block;
+    const float g = row[blk * 2 * block + j], u = row[blk * 2 * block + block + j];
+    put_split(hi + f, parts == 2 ? hi + plane_stride + f : nullptr, __fdividef(g, 1.0f + __expf(-g)) * u);
   }
 }
 
@@ -162,8 +399,19 @@ int adamk_prefill_embed(const int32_t* tokens, int T, const void* embed, int H, 
 int adamk_prefill_rmsnorm_split(const float* h, const void* gain, float eps, int T, int H, void* planes, int parts, adamk_pf_stream stream) {
   if (h == nullptr || gain == nullptr || planes == nullptr || T <= 0 || H <= 0 || H % 4 || (parts != 1 && parts != 2)) return ADAMK_PF_E_INVALID;
   pfo::rmsnorm_split_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(h, static_cast<const __nv_bfloat16*>(gain), eps, H,
-                                                                             static_cast<__nv_bfloat16*>(planes), (long long)T * H, parts);
+                                                                             static_cast<__nv_bfloat16*>(planes), (long long)T * H, parts, nullptr, 0);
   return pfo::done("prefill rmsnorm");
+}
+
+int adamk_batch_rmsnorm_split(const float* h, const void* gain, float eps, int B, int H, void* planes, int parts, float* zero, long long zero_n,
+                              adamk_pf_stream stream) {
+  if (h == nullptr || gain == nullptr || planes == nullptr || B <= 0 || H <= 0 || H % 4 || (parts != 1 && parts != 2) || zero_n % 4 ||
+      (reinterpret_cast<uintptr_t>(zero) & 15))
+    return ADAMK_PF_E_INVALID;
+  pfo::rmsnorm_split_kernel<<<B, 256, 0, static_cast<cudaStream_t>(stream)>>>(h, static_cast<const __nv_bfloat16*>(gain), eps, H,
+                                                                             static_cast<__nv_bfloat16*>(planes), (long long)B * H, parts,
+                                                                             reinterpret_cast<float4*>(zero), zero_n / 4);
+  return pfo::done("batch rmsnorm");
 }
 
 int adamk_prefill_split(const float* x, long long n, void* planes, int parts, adamk_pf_stream stream) {
@@ -180,9 +428,66 @@ int adamk_prefill_rope_store(const float* qkv, int T, int n_q, int n_kv, int D, 
       D % 2 || pos0 < 0 || pos0 + T > max_ctx || (q_gain == nullptr) != (k_gain == nullptr))
     return ADAMK_PF_E_INVALID;
   pfo::RopeArgs a{qkv, static_cast<const __nv_bfloat16*>(q_gain), static_cast<const __nv_bfloat16*>(k_gain), cos, sin, q_out,
-                  static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), T, n_q, n_kv, D, max_ctx, pos0, q_is_bf16, eps};
+                  static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), T, n_q, n_kv, D, max_ctx, pos0, q_is_bf16, eps,
+                  nullptr, 0};
   pfo::rope_store_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return pfo::done("prefill rope");
+}
+
+int adamk_batch_rope_store(const float* qkv, int B, int n_q, int n_kv, int D, const void* q_gain, const void* k_gain, float eps,
+                           const float* cos, const float* sin, const int32_t* positions, long long seq_stride, int max_ctx, float* q_out,
+                           void* k_cache, void* v_cache, adamk_pf_stream stream) {
+  if (qkv == nullptr || cos == nullptr || sin == nullptr || q_out == nullptr || k_cache == nullptr || v_cache == nullptr || positions == nullptr ||
+      B <= 0 || D % 2 || (q_gain == nullptr) != (k_gain == nullptr))
+    return ADAMK_PF_E_INVALID;
+  pfo::RopeArgs a{qkv, static_cast<const __nv_bfloat16*>(q_gain), static_cast<const __nv_bfloat16*>(k_gain), cos, sin, q_out,
+                  static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), B, n_q, n_kv, D, max_ctx, 0, 0, eps,
+                  positions, seq_stride};
+  pfo::rope_store_kernel<<<B, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return pfo::done("batch rope");
+}
+
+size_t adamk_batch_attention_workspace(int B, int n_q, int D, int max_ctx) {
+  const size_t splits = (size_t(max_ctx) + pfo::kAttnChunk - 1) / pfo::kAttnChunk;
+  return size_t(B) * n_q * splits * (D + 2) * sizeof(float);
+}
+
+int adamk_batch_attention(const float* q, const void* k_cache, const void* v_cache, const int32_t* positions, int B, int n_q, int n_kv, int D,
+                          int max_ctx, long long seq_stride, float* workspace, void* out_planes, int parts, adamk_pf_stream stream) {
+  if (q == nullptr || k_cache == nullptr || v_cache == nullptr || positions == nullptr || workspace == nullptr || out_planes == nullptr || B <= 0 ||
+      n_kv <= 0 || n_q % n_kv || n_q / n_kv > pfo::kMaxGroup || (parts != 1 && parts != 2))
+    return ADAMK_PF_E_INVALID;
+  if (D != 64 && D != 128) {
+    snprintf(pf::err_buf(), 256, "batch attention: head_dim %d is not built (64, 128)", D);
+    return ADAMK_PF_E_INVALID;
+  }
+  const int splits = (max_ctx + pfo::kAttnChunk - 1) / pfo::kAttnChunk;
+  const float scale = 1.0f / sqrtf(float(D));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const dim3 grid(splits, n_kv, B), mgrid(n_q, B);
+  const auto* kc = static_cast<const __nv_bfloat16*>(k_cache);
+  const auto* vc = static_cast<const __nv_bfloat16*>(v_cache);
+  auto* planes = static_cast<__nv_bfloat16*>(out_planes);
+  if (D == 128) {
+    pfo::batch_attn_partial_kernel<128><<<grid, pfo::kAttnThreads, 0, s>>>(q, kc, vc, positions, workspace, B, n_q, n_kv, max_ctx, seq_stride, splits, scale);
+    pfo::batch_attn_merge_kernel<128><<<mgrid, 128, splits * sizeof(float), s>>>(workspace, positions, planes, B, n_q, splits, parts);
+  } else {
+    pfo::batch_attn_partial_kernel<64><<<grid, pfo::kAttnThreads, 0, s>>>(q, kc, vc, positions, workspace, B, n_q, n_kv, max_ctx, seq_stride, splits, scale);
+    pfo::batch_attn_merge_kernel<64><<<mgrid, 64, splits * sizeof(float), s>>>(workspace, positions, planes, B, n_q, splits, parts);
+  }
+  return pfo::done("batch attention");
+}
+
+int adamk_batch_swiglu_split(const float* gu, int B, int I, int block, void* planes, int parts, adamk_pf_stream stream) {
+  if (gu == nullptr || planes == nullptr || B <= 0 || I <= 0 || block <= 0 || I % block || (parts != 1 && parts != 2)) return ADAMK_PF_E_INVALID;
+  pfo::swiglu_split_kernel<<<dim3((I + 511) / 512, B), 512, 0, static_cast<cudaStream_t>(stream)>>>(gu, I, block, static_cast<__nv_bfloat16*>(planes), (long long)B * I, parts);
+  return pfo::done("batch swiglu");
+}
+
+int adamk_batch_argmax(const float* logits, int B, int V, int32_t* next, int32_t* tokens, int32_t* positions, adamk_pf_stream stream) {
+  if (logits == nullptr || next == nullptr || B <= 0 || V <= 0) return ADAMK_PF_E_INVALID;
+  pfo::batch_argmax_kernel<<<B, 1024, 0, static_cast<cudaStream_t>(stream)>>>(logits, V, next, tokens, positions);
+  return pfo::done("batch argmax");
 }
 
 }  // extern "C"

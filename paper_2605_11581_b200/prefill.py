@@ -26,12 +26,13 @@ from .model_config import ModelConfig
 from .plugin import AdamkError, load_library
 from .weights import DecoderWeights
 
-EPI_STORE, EPI_RESID, EPI_SWIGLU = 0, 1, 2
+EPI_STORE, EPI_RESID, EPI_SWIGLU, EPI_ATOMIC = 0, 1, 2, 3
 TILE_AUTO, TILE_128, TILE_256, TILE_PAIR = 0, 128, 256, 512   # include/adamk_prefill.h ADAMK_PF_TILE_*
 GU_BLOCK = 128   # features per gate / up block of the interleaved weight = half of a 256-wide GEMM tile
 
 PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
-                   "adamk_prefill_split", "adamk_prefill_rope_store")
+                   "adamk_prefill_split", "adamk_prefill_rope_store", "adamk_batch_rope_store", "adamk_batch_attention_workspace",
+                   "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split")
 
 _declared = False
 
@@ -47,6 +48,13 @@ def _lib():
         lib.adamk_prefill_rmsnorm_split.argtypes = [vp, vp, f, i, i, vp, i, vp]
         lib.adamk_prefill_split.argtypes = [vp, ll, vp, i, vp]
         lib.adamk_prefill_rope_store.argtypes = [vp, i, i, i, i, vp, vp, f, vp, vp, i, i, vp, i, vp, vp, vp]
+        lib.adamk_batch_rope_store.argtypes = [vp, i, i, i, i, vp, vp, f, vp, vp, vp, ll, i, vp, vp, vp, vp]
+        lib.adamk_batch_attention_workspace.argtypes = [i, i, i, i]
+        lib.adamk_batch_attention_workspace.restype = C.c_size_t
+        lib.adamk_batch_attention.argtypes = [vp, vp, vp, vp, i, i, i, i, i, ll, vp, vp, i, vp]
+        lib.adamk_batch_argmax.argtypes = [vp, i, i, vp, vp, vp, vp]
+        lib.adamk_batch_swiglu_split.argtypes = [vp, i, i, i, vp, i, vp]
+        lib.adamk_batch_rmsnorm_split.argtypes = [vp, vp, f, i, i, vp, i, vp, ll, vp]
         _declared = True
     return lib
 
@@ -67,7 +75,8 @@ def _ptr(t: torch.Tensor | None) -> C.c_void_p:
 def gemm(x_planes: torch.Tensor, w: torch.Tensor, out: torch.Tensor, bias: torch.Tensor | None = None,
          epilogue: int = EPI_STORE, tile_n: int = 0) -> torch.Tensor:
     """``out`` (op)= sum_p x_planes[p] @ w.T on the tensor cores.  ``x_planes`` bf16 [parts, T, K], ``w`` bf16 [N, K];
-    ``out`` fp32 [T, N] (STORE / RESID) or bf16 [parts_out, T, N / 2] (SWIGLU, gate / up interleaved in ``w``)."""
+    ``out`` fp32 [T, N] (STORE / RESID / ATOMIC) or bf16 [parts_out, T, N / 2] (SWIGLU, gate / up interleaved in ``w``).
+    ATOMIC adds into ``out`` with fp32 atomics and lets the library split K across SMs (decode-sized T)."""
     if not x_planes.is_cuda:
         raise AdamkError(-102, "prefill operators have no CPU fallback")
     assert x_planes.dtype == torch.bfloat16 and w.dtype == torch.bfloat16 and x_planes.is_contiguous() and w.is_contiguous()
@@ -81,7 +90,7 @@ def gemm(x_planes: torch.Tensor, w: torch.Tensor, out: torch.Tensor, bias: torch
         assert out.dtype == torch.float32 and out.shape == (T, N)
         parts_out, ldo, stride = 1, N, 0
     if bias is not None:
-        assert bias.dtype == torch.float32 and bias.numel() == N and epilogue == EPI_STORE
+        assert bias.dtype == torch.float32 and bias.numel() == N and epilogue in (EPI_STORE, EPI_ATOMIC)
     _ok(_lib().adamk_prefill_gemm(_ptr(x_planes), parts, T, K, _ptr(w), N, _ptr(bias), _ptr(out), ldo, epilogue, parts_out,
                                   stride, tile_n, _stream()))
     return out
@@ -101,9 +110,11 @@ def interleave_gate_up(wgate: torch.Tensor, wup: torch.Tensor, block: int = GU_B
 class TensorCorePrefill:
     """Token-parallel causal pass that fills the KV cache a ``MegaKernelPlugin`` owns."""
 
-    def __init__(self, cfg: ModelConfig, weights: DecoderWeights, plugin, planes: int = 2, attention: str | None = None):
+    def __init__(self, cfg: ModelConfig, weights: DecoderWeights, plugin, planes: int = 2, attention: str | None = None,
+                 layers: list | None = None, embed: torch.Tensor | None = None):
         """``attention``: dtype of the library attention operator, "fp32" (default with two planes; exact but a
-        materialised-score kernel) or "bf16" (default with one plane; flash kernel)."""
+        materialised-score kernel) or "bf16" (default with one plane; flash kernel).  ``layers`` / ``embed``: already
+        prepared device weights (``batch_decode.BatchedDecoder`` shares its own)."""
         if planes not in (1, 2):
             raise ValueError("planes must be 1 (bf16 activations) or 2 (hi + lo, fp32-accurate)")
         attention = attention or ("bf16" if planes == 1 else "fp32")
@@ -113,6 +124,10 @@ class TensorCorePrefill:
         self.cfg, self.plugin, self.planes = cfg, plugin, planes
         self.attn_bf16 = attention == "bf16"
         dev = plugin.device
+        self.launches = 0
+        if layers is not None:
+            self.embed, self.layers = embed, layers
+            return
         self.embed = weights.embed.to(dev)
         self.layers = []
         for lw in weights.layers:

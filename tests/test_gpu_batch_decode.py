@@ -1,0 +1,144 @@
+"""Parity of the batched tensor-core decode path (batch_decode.BatchedDecoder, include/adamk_prefill.h adamk_batch_*)
+against the CPU oracle on a B200.
+
+Tolerance: the projections feed fp32 activations to the tensor cores as hi + lo bf16 planes (2^-17 relative) and sum
+split-K partials with fp32 atomics, and prompts are cached by the tensor-core Prefill (entries within one bf16 ulp of
+the oracle's), so logits agree to <= 5e-3 max-abs here (north-star bound 2e-2) and greedy tokens are identical
+wherever the oracle's top-2 margin exceeds 1e-3.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2605_11581_b200.model_config import TINY, TINY_QWEN3, ModelConfig
+
+pytestmark = pytest.mark.gpu
+
+D128_Q3 = ModelConfig(name="test-d128-q3", hidden=512, n_layers=3, n_q_heads=8, n_kv_heads=2, head_dim=128,
+                      intermediate=1536, vocab=3000, qkv_bias=False, qk_norm=True, tied_embed=False)
+D128 = ModelConfig(name="test-d128", hidden=512, n_layers=2, n_q_heads=4, n_kv_heads=2, head_dim=128,
+                   intermediate=1280, vocab=4096)
+
+
+def _planes(x, parts):
+    hi = x.to(torch.bfloat16)
+    if parts == 1:
+        return hi[None].contiguous()
+    return torch.stack((hi, (x - hi.float()).to(torch.bfloat16))).contiguous()
+
+
+@pytest.mark.parametrize("T,K,N,parts", [(1, 1536, 2048, 2), (8, 1536, 2048, 2), (8, 8960, 1536, 2), (64, 3584, 4608, 2),
+                                         (64, 512, 328, 1), (100, 1536, 1536, 2), (128, 1536, 17920, 2), (33, 64, 8, 1)])
+def test_gemm_atomic_split_k(T, K, N, parts):
+    """Decode-sized GEMM: K split across SMs, fp32-atomic epilogue, both planes stacked in one token tile when they fit
+    (parts * T <= 128), bias added exactly once."""
+    from paper_2605_11581_b200 import prefill as P
+
+    g = torch.Generator(device="cuda").manual_seed(T + K + N)
+    x = torch.randn(T, K, device="cuda", generator=g)
+    w = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g)
+    base = torch.randn(T, N, device="cuda", generator=g)
+    xp = _planes(x, parts)
+    want = base.double() + xp.double().sum(0) @ w.double().T + bias.double()
+    out = base.clone()
+    P.gemm(xp, w, out, bias=bias, epilogue=P.EPI_ATOMIC)
+    err = (out.double() - want).abs().max().item()
+    assert err <= 4e-5 * max(1.0, want.abs().max().item()), err
+
+
+def test_row_operators():
+    from paper_2605_11581_b200 import prefill as P
+
+    lib = P._lib()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    # swiglu_split on the interleaved column order
+    B, I, blk = 5, 384, 128
+    gate, up = torch.randn(B, I, device="cuda", generator=g) * 3, torch.randn(B, I, device="cuda", generator=g)
+    gu = torch.stack((gate.view(B, -1, blk), up.view(B, -1, blk)), dim=2).reshape(B, 2 * I).contiguous()
+    planes = torch.zeros(2, B, I, dtype=torch.bfloat16, device="cuda")
+    P._ok(lib.adamk_batch_swiglu_split(P._ptr(gu), B, I, blk, P._ptr(planes), 2, P._stream()))
+    want = torch.nn.functional.silu(gate.double()) * up.double()
+    assert (planes.double().sum(0) - want).abs().max().item() <= 2e-5 * max(1.0, want.abs().max().item())
+    # argmax: lowest index on ties, in-place advance
+    V = 3000
+    logits = torch.randn(4, V, device="cuda", generator=g)
+    logits[1, 77] = logits[1, 2500] = 50.0
+    logits[2, V - 1] = 60.0
+    nxt = torch.zeros(4, dtype=torch.int32, device="cuda")
+    toks = torch.zeros(4, dtype=torch.int32, device="cuda")
+    pos = torch.tensor([5, 6, 7, 8], dtype=torch.int32, device="cuda")
+    P._ok(lib.adamk_batch_argmax(P._ptr(logits), 4, V, P._ptr(nxt), P._ptr(toks), P._ptr(pos), P._stream()))
+    assert nxt.tolist() == logits.argmax(dim=1).tolist() and nxt[1].item() == 77 and nxt[2].item() == V - 1
+    assert toks.tolist() == nxt.tolist() and pos.tolist() == [6, 7, 8, 9]
+
+
+def _run_parity(cfg, B, steps, oracle_cache, max_ctx=320, seed=11):
+    from oracle.decode_ref import RefDecoder
+    from paper_2605_11581_b200.batch_decode import BatchedDecoder
+    from paper_2605_11581_b200.weights import random_weights, rope_table
+
+    w = random_weights(cfg, seed=0)
+    cos, sin = rope_table(cfg, max_ctx)
+    ref = RefDecoder(cfg, w, max_ctx, cos, sin, batch=B)
+    dec = BatchedDecoder(cfg, w, B, max_ctx)
+    g = torch.Generator().manual_seed(seed)
+    lens = [int(x) for x in torch.randint(1, 280, (B,), generator=g)]
+    lens[0] = 1                                    # a sequence that starts from an empty cache
+    toks, pos = [], []
+    for b in range(B):
+        prompt = torch.randint(0, cfg.vocab, (lens[b],), generator=g).tolist()
+        if lens[b] > 1:
+            ref.prefill(prompt[:-1], b=b)
+        dec.prefill(b, prompt)
+        toks.append(prompt[-1])
+        pos.append(lens[b] - 1)
+    if oracle_cache:       # isolate the decode step from the (one-ulp different) cache a tensor-core Prefill writes
+        dec.k_cache.copy_(ref.k_cache.to(dec.device))
+        dec.v_cache.copy_(ref.v_cache.to(dec.device))
+    worst = 0.0
+    for s in range(steps):
+        want = ref.step(toks, pos)
+        dec.set_state(toks, pos)
+        got_tok = dec.step(auto_advance=False).cpu().tolist()
+        worst = max(worst, float((dec.logits.cpu() - want).abs().max()))
+        toks = [int(t) for t in want.argmax(dim=1)]
+        top2 = want.topk(2, dim=1).values
+        for b in range(B):
+            if float(top2[b, 0] - top2[b, 1]) > 1e-3:
+                assert got_tok[b] == toks[b], (s, b)
+        pos = [p + 1 for p in pos]
+    return worst, dec
+
+
+@pytest.mark.parametrize("cfg,B,oracle_cache", [(TINY, 3, False), (TINY_QWEN3, 5, True), (D128, 4, False), (D128_Q3, 8, False),
+                                                 (D128_Q3, 8, True), (D128_Q3, 1, False), (D128, 70, True)])
+def test_batched_decode_matches_oracle(cfg, B, oracle_cache):
+    worst, dec = _run_parity(cfg, B, steps=5, oracle_cache=oracle_cache)
+    assert worst <= 5e-3, worst
+    assert dec.launches_per_step == 10 * cfg.n_layers + 4
+
+
+def test_cuda_graph_replay_equals_eager_steps():
+    """capture() records one auto-advancing step; replaying it generates the tokens the eager loop generates."""
+    from paper_2605_11581_b200.batch_decode import BatchedDecoder
+    from paper_2605_11581_b200.weights import random_weights
+
+    cfg, B = D128_Q3, 6
+    w = random_weights(cfg, seed=0)
+    g = torch.Generator().manual_seed(3)
+    prompts = [torch.randint(0, cfg.vocab, (int(n),), generator=g).tolist() for n in torch.randint(2, 100, (B,), generator=g)]
+    runs = []
+    for graph in (False, True):
+        dec = BatchedDecoder(cfg, w, B, 256)
+        for b, p in enumerate(prompts):
+            dec.prefill(b, p)
+        if graph:
+            dec.capture()
+        out = [dec.step().clone() for _ in range(12)]
+        torch.cuda.synchronize()
+        runs.append((torch.stack(out).cpu(), dec.positions.cpu().clone()))
+    # fp32 atomics make the two runs differ in the last bits; tokens differ only on near-ties, which these seeds avoid
+    assert torch.equal(runs[0][0], runs[1][0])
+    assert torch.equal(runs[0][1], runs[1][1]) and runs[0][1].tolist() == [len(p) - 1 + 12 for p in prompts]

@@ -256,7 +256,7 @@ def test_cabi_exports_prefill_operators():
 
     build.build()
     header = (Path(__file__).resolve().parents[1] / "include" / "adamk_prefill.h").read_text()
-    declared = set(re.findall(r"\b(adamk_prefill_[a-z_]+)\s*\(", header))
+    declared = set(re.findall(r"\b(adamk_(?:prefill|batch)_[a-z_]+)\s*\(", header))
     assert declared == set(prefill.PREFILL_EXPORTS)
     lib = plugin.load_library()
     for name in declared:
