@@ -42,6 +42,11 @@ typedef void* adamk_pf_stream; /* cudaStream_t */
 
 const char* adamk_prefill_last_error(void);
 
+/* Launch the operators below with programmatic dependent launch (stream serialization attribute): each kernel's
+ * prologue overlaps the previous kernel's tail and `griddepcontrol.wait` orders the data.  Process-wide, off by
+ * default; the batched decode step (dozens of ~10 us kernels per layer) turns it on. */
+void adamk_prefill_set_pdl(int on);
+
 /* D[T, N] = X[T, K] . W[N, K]^T on the tensor cores, fp32 accumulation in tensor memory.
  *   x_planes  bf16 [parts][T, K] row-major: the activation as `parts` bf16 planes whose sum is the fp32 value
  *             (parts 2 = hi + lo, ~2^-17 relative; parts 1 = plain bf16).

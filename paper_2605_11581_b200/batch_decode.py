@@ -4,17 +4,17 @@ The MegaKernel streams the weights once per token of ONE sequence (GEMV on the C
 flight the same weight bytes can serve all of them if the projections become ``[B, K] x [K, N]`` GEMMs.  This module
 runs one decode step of ``B`` sequences with the operators of ``include/adamk_prefill.h``:
 
-* projections: the tcgen05 GEMM of ``csrc/prefill_gemm.cu`` with ``T = B`` (TMA zero-fills the unused token rows
-  of the 128-row tile; the tensor work is free, the kernel is bound by streaming ``W``).  A decode-sized GEMM has
-  fewer tiles than SMs, so tiles are cut into 64-column slices and -- for QKV, O and down -- K is split across SMs
-  with an fp32-atomic epilogue (``EPI_ATOMIC``), which is what lets every SM pull weight bytes; both activation
-  planes ride in the one token tile, so a weight byte is read once; the LM head is a plain store.
+* projections (QKV, O, gate/up, down, LM head): the tcgen05 GEMM of ``csrc/prefill_gemm.cu`` with ``T = B`` (TMA
+  zero-fills the unused token rows of the 128-row tile; the tensor work is free, the kernel is bound by streaming
+  ``W``).  A decode-sized GEMM has fewer tiles than SMs, so K is split across SMs with an fp32-atomic epilogue
+  (``EPI_ATOMIC``), which is what lets every SM pull weight bytes, and both activation planes ride in the one token
+  tile, so a weight byte is read once.  SwiGLU is a row kernel on the gate/up result.
 * activations enter the tensor cores as two bf16 planes (hi + lo), so the step keeps the MegaKernel's numerical
   contract (fp32 activations against exact bf16 weights) at no cost in time.
 * ``adamk_batch_rope_store`` (per-sequence positions), ``adamk_batch_attention`` (split over 256-row chunks of
   each sequence's cache + merge) and ``adamk_batch_argmax`` (greedy pick, tokens / positions advanced on the device).
 
-A step is ~11 launches per layer; ``capture()`` records it once into a CUDA graph, after which a step is one graph
+A step is 10 launches per layer; ``capture()`` records it once into a CUDA graph, after which a step is one graph
 launch with no host work.  Prompts are filled by ``TensorCorePrefill`` into the same cache.  No CPU path.
 """
 
@@ -26,7 +26,7 @@ import torch
 
 from .model_config import ModelConfig
 from .plugin import AdamkError
-from .prefill import (EPI_ATOMIC, EPI_STORE, GU_BLOCK, TensorCorePrefill, _lib, _ok, _ptr, _stream, gemm,
+from .prefill import (EPI_ATOMIC, GU_BLOCK, TensorCorePrefill, _lib, _ok, _ptr, _stream, gemm,
                       interleave_gate_up)
 from .weights import DecoderWeights, rope_table
 
@@ -43,7 +43,8 @@ class _SequenceCache:
 
 
 class BatchedDecoder:
-    def __init__(self, cfg: ModelConfig, weights: DecoderWeights, batch: int, max_ctx: int, device: int = 0, planes: int = 2):
+    def __init__(self, cfg: ModelConfig, weights: DecoderWeights, batch: int, max_ctx: int, device: int = 0, planes: int = 2,
+                 pdl: bool = False):
         if not torch.cuda.is_available():
             raise AdamkError(-102, "no CUDA device: batched decode has no CPU fallback")
         if not 1 <= batch <= 128:
@@ -52,6 +53,7 @@ class BatchedDecoder:
             raise ValueError("planes must be 1 or 2")
         self.lib = _lib()
         self.cfg, self.batch, self.max_ctx, self.planes = cfg, batch, int(max_ctx), planes
+        self.pdl = bool(pdl)            # programmatic dependent launch between the step's kernels (measured: no gain)
         dev = self.device = torch.device("cuda", device)
         cos, sin = rope_table(cfg, max_ctx)
         self._rope = (cos.to(dev), sin.to(dev))
@@ -113,6 +115,13 @@ class BatchedDecoder:
     # ---- one step ----
     @torch.no_grad()
     def _enqueue(self, auto_advance: bool) -> int:
+        self.lib.adamk_prefill_set_pdl(int(self.pdl))
+        try:
+            return self._enqueue_step(auto_advance)
+        finally:
+            self.lib.adamk_prefill_set_pdl(0)
+
+    def _enqueue_step(self, auto_advance: bool) -> int:
         cfg, lib, st, B, P = self.cfg, self.lib, _stream(), self.batch, self.planes
         H, D, nq, nkv = cfg.hidden, cfg.head_dim, cfg.n_q_heads, cfg.n_kv_heads
         seq_stride = nkv * self.max_ctx * D
@@ -134,8 +143,10 @@ class BatchedDecoder:
             _ok(lib.adamk_batch_swiglu_split(_ptr(self.gu), B, lw["i_pad"], GU_BLOCK, _ptr(self.act), P, st))
             gemm(self.act, lw["wdown"], self.h, epilogue=EPI_ATOMIC)         # h += act . Wdown^T
             n += 10         # own kernels (attention is two)
-        _ok(lib.adamk_prefill_rmsnorm_split(_ptr(self.h), _ptr(self.final_norm), cfg.rms_eps, B, H, _ptr(self.xp), P, st))
-        gemm(self.xp, self.lm_head, self.logits, epilogue=EPI_STORE)
+        # LM head: also through the atomic epilogue (planes stacked, the 0.47 GB matrix is read once)
+        _ok(lib.adamk_batch_rmsnorm_split(_ptr(self.h), _ptr(self.final_norm), cfg.rms_eps, B, H, _ptr(self.xp), P,
+                                          _ptr(self.logits), self.logits.numel(), st))
+        gemm(self.xp, self.lm_head, self.logits, epilogue=EPI_ATOMIC)
         adv = auto_advance
         _ok(lib.adamk_batch_argmax(_ptr(self.logits), B, cfg.vocab, _ptr(self.next_token), _ptr(self.tokens) if adv else None,
                                    _ptr(self.positions) if adv else None, st))

@@ -97,6 +97,11 @@ __device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a_desc, uint64_t 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Programmatic dependent launch: let the next kernel of the stream start its prologue now, and wait for the previous
+// kernel's results before touching global memory (both are no-ops for a launch without the attribute).
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -288,6 +293,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
+  griddep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (g.T + BM - 1) / BM;
   const int kb_per_part = (g.K + BK - 1) / BK;
@@ -314,6 +320,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();   // everything above overlapped the previous kernel's tail
 
   if (warp == 0) {
     if (lane == 0) {
@@ -467,6 +474,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
+  griddep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
@@ -495,6 +503,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
 
   // item -> (row block of 256 tokens, tile column, column slice); slices of the last wave are w = 128 wide
   auto decode = [&](int idx, int& m0, int& n_blk, int& sub, int& w) {
@@ -603,6 +612,9 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 static thread_local char g_err[256] = "";
 char* err_buf() { return g_err; }
 
+static int g_pdl = 0;   // adamk_prefill_set_pdl(): launch with programmatic stream serialization
+int pdl_enabled() { return g_pdl; }
+
 static EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
   static std::once_flag once;
@@ -683,8 +695,18 @@ static int launch(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& 
   g.tail_split = split;
   const long long work = (long long)g.n_items * g.ksplit;
   const int grid = work < n_sms ? int(work) : n_sms;
-  kern<<<grid, kThreads, Smem<BN>::kBytes, stream>>>(mx, mw, g);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = Smem<BN>::kBytes;
+  lc.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = g_pdl ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mx, mw, g);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     snprintf(g_err, sizeof g_err, "prefill gemm launch: %s", cudaGetErrorString(e));
     return ADAMK_PF_E_CUDA;
@@ -717,8 +739,18 @@ static int launch_pair(const CUtensorMap& mx, const CUtensorMap& mw, const GemmA
   g.ksplit = 1;
   g.kb_per_split = (g.K + BK - 1) / BK;
   g.stacked = 0;
-  kern<<<2 * pairs, kThreads, PairSmem::kBytes, stream>>>(mx, mw, g);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(2 * pairs);
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = PairSmem::kBytes;
+  lc.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = g_pdl ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mx, mw, g);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     snprintf(g_err, sizeof g_err, "prefill gemm (CTA pair) launch: %s", cudaGetErrorString(e));
     return ADAMK_PF_E_CUDA;
@@ -731,6 +763,8 @@ static int launch_pair(const CUtensorMap& mx, const CUtensorMap& mw, const GemmA
 extern "C" {
 
 const char* adamk_prefill_last_error(void) { return pf::g_err; }
+
+void adamk_prefill_set_pdl(int on) { pf::g_pdl = on ? 1 : 0; }
 
 int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void* w, int N, const float* bias, void* out, int ldo,
                        int epilogue, int parts_out, long long part_stride, int tile_n, adamk_pf_stream stream) {

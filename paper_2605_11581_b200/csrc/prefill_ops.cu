@@ -14,9 +14,31 @@
 
 namespace pf {
 char* err_buf();   // prefill_gemm.cu: the thread-local message adamk_prefill_last_error() returns
+int pdl_enabled(); // prefill_gemm.cu: adamk_prefill_set_pdl()
 }
 
 namespace pfo {
+
+// Programmatic dependent launch (see prefill_gemm.cu): every kernel here starts with griddep_sync().
+__device__ __forceinline__ void griddep_sync() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+static void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = pf::pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&lc, kern, KArgs(args)...);
+}
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
 #pragma unroll
@@ -37,6 +59,7 @@ __device__ __forceinline__ void put_split(__nv_bfloat16* hi, __nv_bfloat16* lo, 
 }
 
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ embed, float* __restrict__ h, int H) {
+  griddep_sync();
   const int t = blockIdx.x;
   const __nv_bfloat16* src = embed + (long long)tokens[t] * H;
   float* dst = h + (long long)t * H;
@@ -49,6 +72,7 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bflo
 // planes[p][t][:] = split(h[t] * rsqrt(mean(h[t]^2) + eps) * gain)
 __global__ void rmsnorm_split_kernel(const float* __restrict__ h, const __nv_bfloat16* __restrict__ gain, float eps, int H,
                                      __nv_bfloat16* __restrict__ planes, long long plane_stride, int parts, float4* zero, long long zero_n4) {
+  griddep_sync();
   __shared__ float red[32];
   const long long t = blockIdx.x;
   // batched decode: clear the fp32 targets of the atomic GEMMs that follow (saves a memset launch per layer)
@@ -71,6 +95,7 @@ __global__ void rmsnorm_split_kernel(const float* __restrict__ h, const __nv_bfl
 }
 
 __global__ void split_kernel(const float* __restrict__ x, long long n, __nv_bfloat16* __restrict__ planes, long long plane_stride, int parts) {
+  griddep_sync();
   const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= n) return;
   const float4 v = *reinterpret_cast<const float4*>(x + i);
@@ -95,6 +120,7 @@ struct RopeArgs {
 };
 
 __global__ void rope_store_kernel(const RopeArgs a) {
+  griddep_sync();
   const int t = blockIdx.x, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int heads = a.n_q + 2 * a.n_kv, half = a.D / 2;
   const float* row = a.qkv + (long long)t * heads * a.D;
@@ -166,10 +192,11 @@ __device__ __forceinline__ void bf16x8_to_float(const uint4 u, float (&f)[8]) {
 // sequence b:  part[b][q head][s][0..D) = sum_p exp(score_p - m) v_p,  [D] = m,  [D + 1] = sum_p exp(score_p - m).
 // Every global load of a phase is issued before the first use (the kernel is latency-, not bandwidth-limited).
 template <int D>
-__global__ void __launch_bounds__(kAttnThreads)
+__global__ void __launch_bounds__(kAttnThreads, 5)
 batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache, const __nv_bfloat16* __restrict__ v_cache,
                           const int32_t* __restrict__ positions, float* __restrict__ part, int B, int n_q, int n_kv, int max_ctx,
                           long long seq_stride, int splits, float scale) {
+  griddep_sync();
   const int s = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
   const int G = n_q / n_kv;
   const int ctx = positions[b] + 1;   // the new token's K / V are already in the cache
@@ -227,22 +254,21 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
   }
   // values: warp w owns positions w, w + 4, ...; issue all of its (coalesced) V rows now, use them after the softmax
   constexpr int E = D / 32, NV = kAttnChunk / NW;
-  float vreg[NV][E];
+  uint32_t vraw[NV][E / 2];   // kept as bf16 pairs until used (registers decide how many CTAs share an SM)
 #pragma unroll
   for (int u = 0; u < NV; ++u) {
     const int pp = warp + u * NW;
     if (pp < n_pos) {
       if constexpr (E == 4) {
         const uint2 raw = *reinterpret_cast<const uint2*>(vb + (long long)pp * D + lane * 4);
-        vreg[u][0] = __uint_as_float(raw.x << 16); vreg[u][1] = __uint_as_float(raw.x & 0xffff0000u);
-        vreg[u][2] = __uint_as_float(raw.y << 16); vreg[u][3] = __uint_as_float(raw.y & 0xffff0000u);
+        vraw[u][0] = raw.x;
+        vraw[u][1] = raw.y;
       } else {
-        const uint32_t raw = *reinterpret_cast<const uint32_t*>(vb + (long long)pp * D + lane * 2);
-        vreg[u][0] = __uint_as_float(raw << 16); vreg[u][1] = __uint_as_float(raw & 0xffff0000u);
+        vraw[u][0] = *reinterpret_cast<const uint32_t*>(vb + (long long)pp * D + lane * 2);
       }
     } else {
 #pragma unroll
-      for (int e = 0; e < E; ++e) vreg[u][e] = 0.f;
+      for (int e = 0; e < E / 2; ++e) vraw[u][e] = 0u;
     }
   }
   __syncthreads();
@@ -271,11 +297,18 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
     for (int u = 0; u < NV; ++u) {
       const int pp = warp + u * NW;
 #pragma unroll
+      float vf[E];
+#pragma unroll
+      for (int e = 0; e < E / 2; ++e) {
+        vf[2 * e] = __uint_as_float(vraw[u][e] << 16);
+        vf[2 * e + 1] = __uint_as_float(vraw[u][e] & 0xffff0000u);
+      }
+#pragma unroll
       for (int g = 0; g < kMaxGroup; ++g)
         if (g < G) {
           const float w = sc[g][pp];
 #pragma unroll
-          for (int e = 0; e < E; ++e) o[g][e] = fmaf(w, vreg[u][e], o[g][e]);
+          for (int e = 0; e < E; ++e) o[g][e] = fmaf(w, vf[e], o[g][e]);
         }
     }
 #pragma unroll
@@ -304,6 +337,7 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
 template <int D>
 __global__ void batch_attn_merge_kernel(const float* __restrict__ part, const int32_t* __restrict__ positions, __nv_bfloat16* __restrict__ planes,
                                         int B, int n_q, int splits, int parts) {
+  griddep_sync();
   const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
   const int live = (positions[b] + kAttnChunk) / kAttnChunk;   // ceil((pos + 1) / chunk)
   const float* src = part + ((long long)b * n_q + h) * splits * (D + 2);
@@ -335,6 +369,7 @@ __global__ void batch_attn_merge_kernel(const float* __restrict__ part, const in
 
 // grid B: greedy pick (lowest index on ties), written to next[b]; tokens / positions advanced in place when asked.
 __global__ void batch_argmax_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ next, int32_t* tokens, int32_t* positions) {
+  griddep_sync();
   const int b = blockIdx.x;
   const float* row = logits + (long long)b * V;
   float best = -INFINITY;
@@ -367,6 +402,7 @@ __global__ void batch_argmax_kernel(const float* __restrict__ logits, int V, int
 // `block` features (the layout of the fused-SwiGLU GEMM weight).  grid (feature blocks, tokens).
 __global__ void swiglu_split_kernel(const float* __restrict__ gu, int I, int block, __nv_bfloat16* __restrict__ planes, long long plane_stride,
                                     int parts) {
+  griddep_sync();
   const long long t = blockIdx.y;
   const float* row = gu + t * 2 * I;
   __nv_bfloat16* hi = planes + t * I;
@@ -392,13 +428,13 @@ extern "C" {
 
 int adamk_prefill_embed(const int32_t* tokens, int T, const void* embed, int H, float* h, adamk_pf_stream stream) {
   if (tokens == nullptr || embed == nullptr || h == nullptr || T <= 0 || H <= 0 || H % 2) return ADAMK_PF_E_INVALID;
-  pfo::embed_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(tokens, static_cast<const __nv_bfloat16*>(embed), h, H);
+  pfo::launch(pfo::embed_kernel, dim3(T), dim3(256), 0, static_cast<cudaStream_t>(stream), tokens, static_cast<const __nv_bfloat16*>(embed), h, H);
   return pfo::done("prefill embed");
 }
 
 int adamk_prefill_rmsnorm_split(const float* h, const void* gain, float eps, int T, int H, void* planes, int parts, adamk_pf_stream stream) {
   if (h == nullptr || gain == nullptr || planes == nullptr || T <= 0 || H <= 0 || H % 4 || (parts != 1 && parts != 2)) return ADAMK_PF_E_INVALID;
-  pfo::rmsnorm_split_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(h, static_cast<const __nv_bfloat16*>(gain), eps, H,
+  pfo::launch(pfo::rmsnorm_split_kernel, dim3(T), dim3(256), 0, static_cast<cudaStream_t>(stream), h, static_cast<const __nv_bfloat16*>(gain), eps, H,
                                                                              static_cast<__nv_bfloat16*>(planes), (long long)T * H, parts, nullptr, 0);
   return pfo::done("prefill rmsnorm");
 }
@@ -408,7 +444,7 @@ int adamk_batch_rmsnorm_split(const float* h, const void* gain, float eps, int B
   if (h == nullptr || gain == nullptr || planes == nullptr || B <= 0 || H <= 0 || H % 4 || (parts != 1 && parts != 2) || zero_n % 4 ||
       (reinterpret_cast<uintptr_t>(zero) & 15))
     return ADAMK_PF_E_INVALID;
-  pfo::rmsnorm_split_kernel<<<B, 256, 0, static_cast<cudaStream_t>(stream)>>>(h, static_cast<const __nv_bfloat16*>(gain), eps, H,
+  pfo::launch(pfo::rmsnorm_split_kernel, dim3(B), dim3(256), 0, static_cast<cudaStream_t>(stream), h, static_cast<const __nv_bfloat16*>(gain), eps, H,
                                                                              static_cast<__nv_bfloat16*>(planes), (long long)B * H, parts,
                                                                              reinterpret_cast<float4*>(zero), zero_n / 4);
   return pfo::done("batch rmsnorm");
@@ -417,7 +453,7 @@ int adamk_batch_rmsnorm_split(const float* h, const void* gain, float eps, int B
 int adamk_prefill_split(const float* x, long long n, void* planes, int parts, adamk_pf_stream stream) {
   if (x == nullptr || planes == nullptr || n <= 0 || n % 4 || (parts != 1 && parts != 2)) return ADAMK_PF_E_INVALID;
   const long long blocks = (n / 4 + 255) / 256;
-  pfo::split_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(x, n, static_cast<__nv_bfloat16*>(planes), n, parts);
+  pfo::launch(pfo::split_kernel, dim3((unsigned)blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), x, n, static_cast<__nv_bfloat16*>(planes), n, parts);
   return pfo::done("prefill split");
 }
 
@@ -430,7 +466,7 @@ int adamk_prefill_rope_store(const float* qkv, int T, int n_q, int n_kv, int D, 
   pfo::RopeArgs a{qkv, static_cast<const __nv_bfloat16*>(q_gain), static_cast<const __nv_bfloat16*>(k_gain), cos, sin, q_out,
                   static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), T, n_q, n_kv, D, max_ctx, pos0, q_is_bf16, eps,
                   nullptr, 0};
-  pfo::rope_store_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  pfo::launch(pfo::rope_store_kernel, dim3(T), dim3(256), 0, static_cast<cudaStream_t>(stream), a);
   return pfo::done("prefill rope");
 }
 
@@ -443,7 +479,7 @@ int adamk_batch_rope_store(const float* qkv, int B, int n_q, int n_kv, int D, co
   pfo::RopeArgs a{qkv, static_cast<const __nv_bfloat16*>(q_gain), static_cast<const __nv_bfloat16*>(k_gain), cos, sin, q_out,
                   static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), B, n_q, n_kv, D, max_ctx, 0, 0, eps,
                   positions, seq_stride};
-  pfo::rope_store_kernel<<<B, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  pfo::launch(pfo::rope_store_kernel, dim3(B), dim3(256), 0, static_cast<cudaStream_t>(stream), a);
   return pfo::done("batch rope");
 }
 
@@ -469,24 +505,24 @@ int adamk_batch_attention(const float* q, const void* k_cache, const void* v_cac
   const auto* vc = static_cast<const __nv_bfloat16*>(v_cache);
   auto* planes = static_cast<__nv_bfloat16*>(out_planes);
   if (D == 128) {
-    pfo::batch_attn_partial_kernel<128><<<grid, pfo::kAttnThreads, 0, s>>>(q, kc, vc, positions, workspace, B, n_q, n_kv, max_ctx, seq_stride, splits, scale);
-    pfo::batch_attn_merge_kernel<128><<<mgrid, 128, splits * sizeof(float), s>>>(workspace, positions, planes, B, n_q, splits, parts);
+    pfo::launch(pfo::batch_attn_partial_kernel<128>, dim3(grid), dim3(pfo::kAttnThreads), 0, s, q, kc, vc, positions, workspace, B, n_q, n_kv, max_ctx, seq_stride, splits, scale);
+    pfo::launch(pfo::batch_attn_merge_kernel<128>, dim3(mgrid), dim3(128), splits * sizeof(float), s, workspace, positions, planes, B, n_q, splits, parts);
   } else {
-    pfo::batch_attn_partial_kernel<64><<<grid, pfo::kAttnThreads, 0, s>>>(q, kc, vc, positions, workspace, B, n_q, n_kv, max_ctx, seq_stride, splits, scale);
-    pfo::batch_attn_merge_kernel<64><<<mgrid, 64, splits * sizeof(float), s>>>(workspace, positions, planes, B, n_q, splits, parts);
+    pfo::launch(pfo::batch_attn_partial_kernel<64>, dim3(grid), dim3(pfo::kAttnThreads), 0, s, q, kc, vc, positions, workspace, B, n_q, n_kv, max_ctx, seq_stride, splits, scale);
+    pfo::launch(pfo::batch_attn_merge_kernel<64>, dim3(mgrid), dim3(64), splits * sizeof(float), s, workspace, positions, planes, B, n_q, splits, parts);
   }
   return pfo::done("batch attention");
 }
 
 int adamk_batch_swiglu_split(const float* gu, int B, int I, int block, void* planes, int parts, adamk_pf_stream stream) {
   if (gu == nullptr || planes == nullptr || B <= 0 || I <= 0 || block <= 0 || I % block || (parts != 1 && parts != 2)) return ADAMK_PF_E_INVALID;
-  pfo::swiglu_split_kernel<<<dim3((I + 511) / 512, B), 512, 0, static_cast<cudaStream_t>(stream)>>>(gu, I, block, static_cast<__nv_bfloat16*>(planes), (long long)B * I, parts);
+  pfo::launch(pfo::swiglu_split_kernel, dim3(dim3((I + 511) / 512, B)), dim3(512), 0, static_cast<cudaStream_t>(stream), gu, I, block, static_cast<__nv_bfloat16*>(planes), (long long)B * I, parts);
   return pfo::done("batch swiglu");
 }
 
 int adamk_batch_argmax(const float* logits, int B, int V, int32_t* next, int32_t* tokens, int32_t* positions, adamk_pf_stream stream) {
   if (logits == nullptr || next == nullptr || B <= 0 || V <= 0) return ADAMK_PF_E_INVALID;
-  pfo::batch_argmax_kernel<<<B, 1024, 0, static_cast<cudaStream_t>(stream)>>>(logits, V, next, tokens, positions);
+  pfo::launch(pfo::batch_argmax_kernel, dim3(B), dim3(1024), 0, static_cast<cudaStream_t>(stream), logits, V, next, tokens, positions);
   return pfo::done("batch argmax");
 }
 
