@@ -191,23 +191,22 @@ __device__ __forceinline__ void bf16x8_to_float(const uint4 u, float (&f)[8]) {
 // grid (splits, n_kv, B).  Partial softmax of the G q heads of one kv head over positions [s * 64, s * 64 + 64) of
 // sequence b:  part[b][q head][s][0..D) = sum_p exp(score_p - m) v_p,  [D] = m,  [D + 1] = sum_p exp(score_p - m).
 // Every global load of a phase is issued before the first use (the kernel is latency-, not bandwidth-limited).
-template <int D>
+template <int D, int G>
 __global__ void __launch_bounds__(kAttnThreads, 5)
 batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache, const __nv_bfloat16* __restrict__ v_cache,
                           const int32_t* __restrict__ positions, float* __restrict__ part, int B, int n_q, int n_kv, int max_ctx,
                           long long seq_stride, int splits, float scale) {
   griddep_sync();
   const int s = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
-  const int G = n_q / n_kv;
   const int ctx = positions[b] + 1;   // the new token's K / V are already in the cache
   const int p0 = s * kAttnChunk;
   if (p0 >= ctx) return;              // the merge kernel derives the live split count from positions, too
   const int n_pos = min(kAttnChunk, ctx - p0);
   constexpr int NW = kAttnThreads / 32;
-  __shared__ float q_s[kMaxGroup][D];
-  __shared__ float sc[kMaxGroup][kAttnChunk];
-  __shared__ float ml[kMaxGroup][2];
-  __shared__ float ored[NW][kMaxGroup][D];
+  __shared__ __align__(16) float q_s[G][D];
+  __shared__ float sc[G][kAttnChunk];
+  __shared__ float ml[G][2];
+  __shared__ __align__(16) float ored[NW][G][D];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const __nv_bfloat16* kb = k_cache + b * seq_stride + ((long long)kvh * max_ctx + p0) * D;
   const __nv_bfloat16* vb = v_cache + b * seq_stride + ((long long)kvh * max_ctx + p0) * D;
@@ -230,27 +229,30 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
   }
   __syncthreads();
   {
-    float acc[kMaxGroup];
+    float acc[G];
 #pragma unroll
-    for (int g = 0; g < kMaxGroup; ++g) acc[g] = 0.f;
+    for (int g = 0; g < G; ++g) acc[g] = 0.f;
 #pragma unroll
     for (int c = 0; c < HC; ++c) {
       float kf[8];
       bf16x8_to_float(kraw[c], kf);
       const int d0 = (half * HC + c) * 8;
 #pragma unroll
-      for (int g = 0; g < kMaxGroup; ++g)
-        if (g < G) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[g] = fmaf(q_s[g][d0 + j], kf[j], acc[g]);
+      for (int g = 0; g < G; ++g)
+        {   // q as two 16-byte broadcast reads per 8 products (the scalar form is bound by shared-memory issue)
+          const float4 qa = *reinterpret_cast<const float4*>(&q_s[g][d0]), qb = *reinterpret_cast<const float4*>(&q_s[g][d0 + 4]);
+          acc[g] = fmaf(qa.x, kf[0], acc[g]); acc[g] = fmaf(qa.y, kf[1], acc[g]);
+          acc[g] = fmaf(qa.z, kf[2], acc[g]); acc[g] = fmaf(qa.w, kf[3], acc[g]);
+          acc[g] = fmaf(qb.x, kf[4], acc[g]); acc[g] = fmaf(qb.y, kf[5], acc[g]);
+          acc[g] = fmaf(qb.z, kf[6], acc[g]); acc[g] = fmaf(qb.w, kf[7], acc[g]);
         }
     }
 #pragma unroll
-    for (int g = 0; g < kMaxGroup; ++g)
-      if (g < G) {
-        const float t = acc[g] + __shfl_xor_sync(0xffffffffu, acc[g], 1);
-        if (half == 0) sc[g][p] = (p < n_pos) ? t : -INFINITY;
-      }
+    for (int g = 0; g < G; ++g)
+    {
+      const float t = acc[g] + __shfl_xor_sync(0xffffffffu, acc[g], 1);
+      if (half == 0) sc[g][p] = (p < n_pos) ? t : -INFINITY;
+    }
   }
   // values: warp w owns positions w, w + 4, ...; issue all of its (coalesced) V rows now, use them after the softmax
   constexpr int E = D / 32, NV = kAttnChunk / NW;
@@ -288,9 +290,9 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
   }
   __syncthreads();
   {
-    float o[kMaxGroup][E];
+    float o[G][E];
 #pragma unroll
-    for (int g = 0; g < kMaxGroup; ++g)
+    for (int g = 0; g < G; ++g)
 #pragma unroll
       for (int e = 0; e < E; ++e) o[g][e] = 0.f;
 #pragma unroll
@@ -304,19 +306,17 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
         vf[2 * e + 1] = __uint_as_float(vraw[u][e] & 0xffff0000u);
       }
 #pragma unroll
-      for (int g = 0; g < kMaxGroup; ++g)
-        if (g < G) {
+      for (int g = 0; g < G; ++g) {
           const float w = sc[g][pp];
 #pragma unroll
           for (int e = 0; e < E; ++e) o[g][e] = fmaf(w, vf[e], o[g][e]);
         }
     }
 #pragma unroll
-    for (int g = 0; g < kMaxGroup; ++g)
-      if (g < G) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) ored[warp][g][lane * E + e] = o[g][e];
-      }
+    for (int g = 0; g < G; ++g) {
+      if constexpr (E == 4) *reinterpret_cast<float4*>(&ored[warp][g][lane * 4]) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+      else *reinterpret_cast<float2*>(&ored[warp][g][lane * 2]) = make_float2(o[g][0], o[g][1]);
+    }
   }
   __syncthreads();
   for (int i = tid; i < G * D; i += kAttnThreads) {
@@ -504,12 +504,36 @@ int adamk_batch_attention(const float* q, const void* k_cache, const void* v_cac
   const auto* kc = static_cast<const __nv_bfloat16*>(k_cache);
   const auto* vc = static_cast<const __nv_bfloat16*>(v_cache);
   auto* planes = static_cast<__nv_bfloat16*>(out_planes);
+  const int G = n_q / n_kv;
+  bool ok = true;
+#define ADAMK_ATTN_CASE(DD, GG)                                                                                                          \
+  pfo::launch(pfo::batch_attn_partial_kernel<DD, GG>, dim3(grid), dim3(pfo::kAttnThreads), 0, s, q, kc, vc, positions, workspace, B, n_q, \
+              n_kv, max_ctx, seq_stride, splits, scale)
   if (D == 128) {
-    pfo::launch(pfo::batch_attn_partial_kernel<128>, dim3(grid), dim3(pfo::kAttnThreads), 0, s, q, kc, vc, positions, workspace, B, n_q, n_kv, max_ctx, seq_stride, splits, scale);
-    pfo::launch(pfo::batch_attn_merge_kernel<128>, dim3(mgrid), dim3(128), splits * sizeof(float), s, workspace, positions, planes, B, n_q, splits, parts);
+    switch (G) {
+      case 1: ADAMK_ATTN_CASE(128, 1); break;
+      case 2: ADAMK_ATTN_CASE(128, 2); break;
+      case 4: ADAMK_ATTN_CASE(128, 4); break;
+      case 6: ADAMK_ATTN_CASE(128, 6); break;
+      case 7: ADAMK_ATTN_CASE(128, 7); break;
+      case 8: ADAMK_ATTN_CASE(128, 8); break;
+      default: ok = false;
+    }
+    if (ok) pfo::launch(pfo::batch_attn_merge_kernel<128>, dim3(mgrid), dim3(128), splits * sizeof(float), s, workspace, positions, planes, B, n_q, splits, parts);
   } else {
-    pfo::launch(pfo::batch_attn_partial_kernel<64>, dim3(grid), dim3(pfo::kAttnThreads), 0, s, q, kc, vc, positions, workspace, B, n_q, n_kv, max_ctx, seq_stride, splits, scale);
-    pfo::launch(pfo::batch_attn_merge_kernel<64>, dim3(mgrid), dim3(64), splits * sizeof(float), s, workspace, positions, planes, B, n_q, splits, parts);
+    switch (G) {
+      case 1: ADAMK_ATTN_CASE(64, 1); break;
+      case 2: ADAMK_ATTN_CASE(64, 2); break;
+      case 4: ADAMK_ATTN_CASE(64, 4); break;
+      case 8: ADAMK_ATTN_CASE(64, 8); break;
+      default: ok = false;
+    }
+    if (ok) pfo::launch(pfo::batch_attn_merge_kernel<64>, dim3(mgrid), dim3(64), splits * sizeof(float), s, workspace, positions, planes, B, n_q, splits, parts);
+  }
+#undef ADAMK_ATTN_CASE
+  if (!ok) {
+    snprintf(pf::err_buf(), 256, "batch attention: %d q heads per kv head at head_dim %d is not built", G, D);
+    return ADAMK_PF_E_INVALID;
   }
   return pfo::done("batch attention");
 }
