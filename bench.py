@@ -189,6 +189,35 @@ def prefill_sample(cfg, w, dev, local: int, tokens: int = 4096, iters: int = 5) 
     return out
 
 
+def batch_decode_sample(cfg, w, dev, local: int, ctx: int = 2048, steps: int = 32) -> dict:
+    """Extra, outside the timed batch-1 region: BASELINE.json configs[2], batched decode on the tensor cores
+    (paper_2605_11581_b200/batch_decode.py): one CUDA-graph launch per step of B sequences, every sequence at context
+    ``ctx``.  `weights_gbs` = the model's weight bytes / step time (the weights are streamed once per step)."""
+    from paper_2605_11581_b200.batch_decode import BatchedDecoder
+
+    out = {"context": ctx, "steps": steps, "launch": "one CUDA graph of 10 kernels per layer"}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for B in (8, 64):
+        dec = BatchedDecoder(cfg, w, B, ctx + steps + 32, device=local)
+        g = torch.Generator().manual_seed(3)
+        dec.set_state(torch.randint(0, cfg.vocab, (B,), generator=g).tolist(), [ctx] * B)
+        dec.capture()
+        for _ in range(8):
+            dec.step()
+        torch.cuda.synchronize(dev)
+        e0.record()
+        for _ in range(steps):
+            dec.step()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / steps
+        out[f"batch{B}"] = {"ms_per_step": ms, "tokens_per_s": B * 1e3 / ms, "own_kernel_launches_per_step": dec.launches_per_step,
+                            "weights_gbs": cfg.weight_bytes_per_token() / ms / 1e6}
+        del dec
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args) -> None:
     from paper_2605_11581_b200.plugin import MegaKernelPlugin
 
@@ -309,6 +338,7 @@ def run_ours(args) -> None:
     })
     if tp == 1 and not args.no_prefill:
         line["prefill"] = prefill_sample(full_cfg, w, dev, local)
+        line["batch_decode"] = batch_decode_sample(full_cfg, w, dev, local)
     if not args.no_cpu_baseline:
         w_cpu = random_weights(full_cfg, seed=0, device=dev).to("cpu") if tp > 1 else w.to("cpu")
         res = cpu_decode_sample(full_cfg, w_cpu, prompt, n_steps=args.cpu_steps)
@@ -326,7 +356,7 @@ def main() -> None:
     ap.add_argument("--model", default="qwen2.5-1.5b")
     ap.add_argument("--cpu-steps", type=int, default=48, help="decode steps of the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-prefill", action="store_true", help="skip the extra tensor-core Prefill sample")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the extra tensor-core Prefill and batched-decode samples")
     ap.add_argument("--tp", action="store_true", help="N > 1: tensor-parallel shards of one sequence instead of N replicas")
     args = ap.parse_args()
     if args.warmup < 3:
