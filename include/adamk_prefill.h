@@ -47,6 +47,11 @@ const char* adamk_prefill_last_error(void);
  * default; the batched decode step (dozens of ~10 us kernels per layer) turns it on. */
 void adamk_prefill_set_pdl(int on);
 
+/* Debug: when non-null, CTA 0 of every one-CTA-tile GEMM launch writes six %globaltimer stamps (ns) to `stamps`
+ * (device memory, 8 x uint64): start, prologue done, first operands landed, last MMA issued, epilogue done, exit,
+ * accumulator visible to the epilogue. */
+void adamk_prefill_set_trace(void* stamps);
+
 /* D[T, N] = X[T, K] . W[N, K]^T on the tensor cores, fp32 accumulation in tensor memory.
  *   x_planes  bf16 [parts][T, K] row-major: the activation as `parts` bf16 planes whose sum is the fp32 value
  *             (parts 2 = hi + lo, ~2^-17 relative; parts 1 = plain bf16).

@@ -27,6 +27,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/adamk_prefill.h"
@@ -102,6 +103,15 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// stamps (CTA 0 only): 0 start, 1 prologue done, 2 first operands landed, 3 accumulator complete (MMA lane),
+// 4 epilogue warp 0 done, 5 before exit, 6 accumulator seen by epilogue warp 0
+#define PF_STAMP(i) do { if (g.trace != nullptr && blockIdx.x == 0) g.trace[i] = gtime(); } while (0)
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -131,6 +141,7 @@ struct GemmArgs {
   int n_items;
   int ksplit;           // split-K (EPI_ATOMIC only): every tile item becomes ksplit items over disjoint k-block ranges
   int kb_per_split;
+  unsigned long long* trace;   // debug: %globaltimer stamps of CTA 0 (adamk_prefill_set_trace), or null
   int stacked;          // EPI_ATOMIC with parts * T <= 128: the planes are consecutive rows of ONE token tile, K is walked
                         // once (the weight is read once), accumulator row r adds into output row r % T
 };
@@ -233,6 +244,58 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, uint32_t t_addr
       }
       __syncwarp();
     }
+  } else if constexpr (EPI == ADAMK_PF_EPI_ATOMIC) {
+    // Decode-sized tiles: a handful of live rows drained by the one warp that owns their TMEM lanes, so that warp's
+    // instruction latency is the cost (tools/gemm_trace.py: 4.9 us per tile for the general path, 3.3 us for this one;
+    // a register-resident variant without the patch measured 4.1 us).  Row bookkeeping is done once per tile, only
+    // live rows are staged and sent, and when both stacked planes of a row sit in this 32-row patch (2 T <= 32) they
+    // are summed here so that T rows go out.
+    const int n0 = n_blk * BN + sub * w;
+    float* out = static_cast<float*>(g.out);
+    const bool fold = g.stacked && g.parts == 2 && 2 * g.T <= 32;
+    const int staged = min(32, (g.stacked ? g.parts * g.T : g.T) - row0);   // rows of this patch that hold data
+    const int live = fold ? g.T : staged;                                    // rows that go out
+    const int n_it = (live + 3) >> 2;
+    long long roff[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = row0 + i * 4 + sub_row;
+      roff[i] = (i * 4 + sub_row < live) ? (long long)(g.stacked ? row % g.T : row) * g.ldo : -1;
+    }
+#pragma unroll 1
+    for (int c = 0; c < w; c += 64) {   // two tensor-memory loads in flight per wait (w is a multiple of 64)
+      uint32_t acc[2][32];
+      tmem_ld32(t_addr + c, acc[0]);
+      tmem_ld32(t_addr + c + 32, acc[1]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int hc = 0; hc < 2; ++hc) {
+        const int col = n0 + c + hc * 32 + cg;
+        const bool col_ok = col < g.N;
+        const float4 b = (g.bias != nullptr && col_ok && first_split) ? *reinterpret_cast<const float4*>(g.bias + col) : make_float4(0, 0, 0, 0);
+        if (lane < staged) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(patch + lane * kStagePitch + j) = make_float4(
+                __uint_as_float(acc[hc][j]), __uint_as_float(acc[hc][j + 1]), __uint_as_float(acc[hc][j + 2]), __uint_as_float(acc[hc][j + 3]));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i < n_it && roff[i] >= 0 && col_ok) {
+            const int r = i * 4 + sub_row;
+            float4 v = *reinterpret_cast<const float4*>(patch + r * kStagePitch + cg);
+            if (fold) {
+              const float4 lo = *reinterpret_cast<const float4*>(patch + (r + g.T) * kStagePitch + cg);
+              v.x += lo.x; v.y += lo.y; v.z += lo.z; v.w += lo.w;
+            }
+            if (row0 + r < g.T) { v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w; }   // bias: once per output row
+            atomicAdd(reinterpret_cast<float4*>(out + roff[i] + col), v);
+          }
+        }
+        __syncwarp();
+      }
+    }
   } else {
     const int n0 = n_blk * BN + sub * w;
     float* out = static_cast<float*>(g.out);
@@ -250,7 +313,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, uint32_t t_addr
           o[i] = (row < g.T && col_ok) ? *reinterpret_cast<const float4*>(out + (long long)row * g.ldo + col) : make_float4(0, 0, 0, 0);
         }
       } else {
-        const float4 b = (g.bias != nullptr && col_ok && first_split) ? *reinterpret_cast<const float4*>(g.bias + col) : make_float4(0, 0, 0, 0);
+        const float4 b = (g.bias != nullptr && col_ok) ? *reinterpret_cast<const float4*>(g.bias + col) : make_float4(0, 0, 0, 0);
 #pragma unroll
         for (int i = 0; i < 8; ++i) o[i] = b;
       }
@@ -264,16 +327,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, uint32_t t_addr
       for (int i = 0; i < 8; ++i) {
         const int r = i * 4 + sub_row, row = row0 + r;
         float4 v = *reinterpret_cast<const float4*>(patch + r * kStagePitch + cg);
-        if constexpr (EPI == ADAMK_PF_EPI_ATOMIC) {
-          const int rows = g.stacked ? g.parts * g.T : g.T;
-          if (row < rows && col_ok) {
-            if (row < g.T) { v.x += o[i].x; v.y += o[i].y; v.z += o[i].z; v.w += o[i].w; }   // bias: once per output row
-            atomicAdd(reinterpret_cast<float4*>(out + (long long)(g.stacked ? row % g.T : row) * g.ldo + col), v);
-          }
-        } else {
-          v.x += o[i].x; v.y += o[i].y; v.z += o[i].z; v.w += o[i].w;
-          if (row < g.T && col_ok) *reinterpret_cast<float4*>(out + (long long)row * g.ldo + col) = v;
-        }
+        v.x += o[i].x; v.y += o[i].y; v.z += o[i].z; v.w += o[i].w;
+        if (row < g.T && col_ok) *reinterpret_cast<float4*>(out + (long long)row * g.ldo + col) = v;
       }
       __syncwarp();
     }
@@ -294,6 +349,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   griddep_launch();
+  if (threadIdx.x == 0) PF_STAMP(0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (g.T + BM - 1) / BM;
   const int kb_per_part = (g.K + BK - 1) / BK;
@@ -321,6 +377,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_wait();   // everything above overlapped the previous kernel's tail
+  if (threadIdx.x == 0) PF_STAMP(1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -359,6 +416,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (n == 0 && kb == 0) PF_STAMP(2);
           const uint32_t a_addr = smem_u32(smem + stage * S::kStage);
           const uint64_t a_desc = smem_desc_sw128(a_addr), b_desc = smem_desc_sw128(a_addr + S::kStageA);
 #pragma unroll
@@ -368,6 +426,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
           if (++stage == S::kStages) { stage = 0; phase ^= 1; }
         }
         umma_commit(&acc_full[as]);
+        if (n == 0) PF_STAMP(3);
       }
     }
   } else {
@@ -384,6 +443,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
       const int row0 = it.m0 + quarter * 32;
       mbar_wait(&acc_full[as], (n >> 1) & 1);
       tc_fence_after();
+      if (n == 0 && quarter == 0 && lane == 0) PF_STAMP(6);
       const uint32_t t_addr = tmem_base + as * BN + (uint32_t(quarter * 32) << 16);
       const int rows_live = (EPI == ADAMK_PF_EPI_ATOMIC && g.stacked) ? g.parts * g.T : g.T;
       if (row0 < rows_live)   // decode-sized T: most warps own no live row and only hand the accumulator back
@@ -391,11 +451,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[as]);
+      if (n == 0 && quarter == 0 && lane == 0) PF_STAMP(4);
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) PF_STAMP(5);
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(2 * BN) : "memory");
@@ -612,6 +674,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 static thread_local char g_err[256] = "";
 char* err_buf() { return g_err; }
 
+static unsigned long long* g_trace = nullptr;   // adamk_prefill_set_trace()
 static int g_pdl = 0;   // adamk_prefill_set_pdl(): launch with programmatic stream serialization
 int pdl_enabled() { return g_pdl; }
 
@@ -678,6 +741,8 @@ static int launch(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& 
     g.stacked = (g.parts * g.T <= BM) ? 1 : 0;
     if (tiles * 2 <= n_sms) {
       int want = n_sms / tiles;
+      static const int cap = [] { const char* e = getenv("ADAMK_PF_KSPLIT_MAX"); return e ? atoi(e) : 1 << 30; }();   // experiments
+      if (want > cap) want = cap;
       if (want > kb_per_part) want = kb_per_part;
       g.kb_per_split = (kb_per_part + want - 1) / want;
       g.ksplit = (kb_per_part + g.kb_per_split - 1) / g.kb_per_split;
@@ -766,6 +831,8 @@ const char* adamk_prefill_last_error(void) { return pf::g_err; }
 
 void adamk_prefill_set_pdl(int on) { pf::g_pdl = on ? 1 : 0; }
 
+void adamk_prefill_set_trace(void* stamps) { pf::g_trace = static_cast<unsigned long long*>(stamps); }
+
 int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void* w, int N, const float* bias, void* out, int ldo,
                        int epilogue, int parts_out, long long part_stride, int tile_n, adamk_pf_stream stream) {
   using namespace pf;
@@ -820,7 +887,7 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
   }
   CUtensorMap mx, mw;
   if (!make_map(&mx, x_planes, (long long)parts * T, K, BM) || !make_map(&mw, w, N, K, BOXN)) return ADAMK_PF_E_CUDA;
-  GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride, 0, 1, 0, 1, 0, 0};
+  GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride, 0, 1, 0, 1, 0, g_trace, 0};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (pair) {
     switch (epilogue) {

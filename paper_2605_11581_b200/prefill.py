@@ -30,7 +30,7 @@ EPI_STORE, EPI_RESID, EPI_SWIGLU, EPI_ATOMIC = 0, 1, 2, 3
 TILE_AUTO, TILE_128, TILE_256, TILE_PAIR = 0, 128, 256, 512   # include/adamk_prefill.h ADAMK_PF_TILE_*
 GU_BLOCK = 128   # features per gate / up block of the interleaved weight = half of a 256-wide GEMM tile
 
-PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
+PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_prefill_set_trace", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
                    "adamk_prefill_split", "adamk_prefill_rope_store", "adamk_batch_rope_store", "adamk_batch_attention_workspace",
                    "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split")
 
@@ -45,6 +45,8 @@ def _lib():
         lib.adamk_prefill_last_error.restype = C.c_char_p
         lib.adamk_prefill_set_pdl.argtypes = [i]
         lib.adamk_prefill_set_pdl.restype = None
+        lib.adamk_prefill_set_trace.argtypes = [vp]
+        lib.adamk_prefill_set_trace.restype = None
         lib.adamk_prefill_gemm.argtypes = [vp, i, i, i, vp, i, vp, vp, i, i, i, ll, i, vp]
         lib.adamk_prefill_embed.argtypes = [vp, i, vp, i, vp, vp]
         lib.adamk_prefill_rmsnorm_split.argtypes = [vp, vp, f, i, i, vp, i, vp]
