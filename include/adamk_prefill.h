@@ -47,6 +47,11 @@ const char* adamk_prefill_last_error(void);
  * default; the batched decode step (dozens of ~10 us kernels per layer) turns it on. */
 void adamk_prefill_set_pdl(int on);
 
+/* One-shot hint for the NEXT adamk_prefill_gemm call on this thread (one-CTA tiles): while that GEMM waits for its own
+ * operands, its idle warps pull `bytes` at `ptr` -- the weight the kernel AFTER it will stream -- into L2
+ * (cp.async.bulk.prefetch.L2).  The batched decode step chains its GEMMs this way; 16-byte aligned, < L2 size. */
+void adamk_prefill_prefetch_next(const void* ptr, long long bytes);
+
 /* Debug: when non-null, CTA 0 of every one-CTA-tile GEMM launch writes six %globaltimer stamps (ns) to `stamps`
  * (device memory, 8 x uint64): start, prologue done, first operands landed, last MMA issued, epilogue done, exit,
  * accumulator visible to the epilogue. */

@@ -141,6 +141,8 @@ struct GemmArgs {
   int n_items;
   int ksplit;           // split-K (EPI_ATOMIC only): every tile item becomes ksplit items over disjoint k-block ranges
   int kb_per_split;
+  const uint8_t* pf_ptr;       // adamk_prefill_prefetch_next(): bytes the NEXT kernel will stream, pulled into L2 by this
+  long long pf_bytes;          // launch's otherwise idle epilogue warps while its own operands are in flight
   unsigned long long* trace;   // debug: %globaltimer stamps of CTA 0 (adamk_prefill_set_trace), or null
   int stacked;          // EPI_ATOMIC with parts * T <= 128: the planes are consecutive rows of ONE token tile, K is walked
                         // once (the weight is read once), accumulator row r adds into output row r % T
@@ -430,6 +432,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
       }
     }
   } else {
+    if (g.pf_bytes > 0 && warp == 2) {
+      // L2 prefetch of the next kernel's weights: this CTA's 1/gridDim share, 4 KB per request, one lane per request
+      const long long per = ((g.pf_bytes / gridDim.x) + 4095) & ~4095ll;
+      const long long lo = per * blockIdx.x, hi = min(lo + per, g.pf_bytes & ~15ll);
+      for (long long off = lo + lane * 4096ll; off < hi; off += 32 * 4096ll) {
+        const uint32_t sz = uint32_t(min(4096ll, hi - off));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g.pf_ptr + off), "r"(sz) : "memory");
+      }
+    }
     // Epilogue.  tcgen05.ld hands each lane one accumulator row; a row-per-lane store would touch 32 lines per
     // instruction, so every 32 x 32 block goes through a padded shared-memory patch and leaves as 4 rows x 128
     // contiguous bytes per instruction (8 lanes per row).
@@ -675,6 +686,8 @@ static thread_local char g_err[256] = "";
 char* err_buf() { return g_err; }
 
 static unsigned long long* g_trace = nullptr;   // adamk_prefill_set_trace()
+static const uint8_t* g_pf_ptr = nullptr;        // adamk_prefill_prefetch_next(): consumed by the next GEMM launch
+static long long g_pf_bytes = 0;
 static int g_pdl = 0;   // adamk_prefill_set_pdl(): launch with programmatic stream serialization
 int pdl_enabled() { return g_pdl; }
 
@@ -831,6 +844,11 @@ const char* adamk_prefill_last_error(void) { return pf::g_err; }
 
 void adamk_prefill_set_pdl(int on) { pf::g_pdl = on ? 1 : 0; }
 
+void adamk_prefill_prefetch_next(const void* ptr, long long bytes) {
+  pf::g_pf_ptr = static_cast<const uint8_t*>(ptr);
+  pf::g_pf_bytes = (ptr != nullptr && bytes > 0) ? bytes : 0;
+}
+
 void adamk_prefill_set_trace(void* stamps) { pf::g_trace = static_cast<unsigned long long*>(stamps); }
 
 int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void* w, int N, const float* bias, void* out, int ldo,
@@ -887,7 +905,9 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
   }
   CUtensorMap mx, mw;
   if (!make_map(&mx, x_planes, (long long)parts * T, K, BM) || !make_map(&mw, w, N, K, BOXN)) return ADAMK_PF_E_CUDA;
-  GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride, 0, 1, 0, 1, 0, g_trace, 0};
+  GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride, 0, 1, 0, 1, 0, g_pf_ptr, g_pf_bytes, g_trace, 0};
+  g_pf_ptr = nullptr;
+  g_pf_bytes = 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (pair) {
     switch (epilogue) {

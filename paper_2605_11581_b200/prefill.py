@@ -28,9 +28,10 @@ from .weights import DecoderWeights
 
 EPI_STORE, EPI_RESID, EPI_SWIGLU, EPI_ATOMIC = 0, 1, 2, 3
 TILE_AUTO, TILE_128, TILE_256, TILE_PAIR = 0, 128, 256, 512   # include/adamk_prefill.h ADAMK_PF_TILE_*
+PREFETCH_MAX_BYTES = 64 << 20   # L2 prefetch hint cap (half of the 126 MB L2)
 GU_BLOCK = 128   # features per gate / up block of the interleaved weight = half of a 256-wide GEMM tile
 
-PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_prefill_set_trace", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
+PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_prefill_set_trace", "adamk_prefill_prefetch_next", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
                    "adamk_prefill_split", "adamk_prefill_rope_store", "adamk_batch_rope_store", "adamk_batch_attention_workspace",
                    "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split")
 
@@ -46,6 +47,8 @@ def _lib():
         lib.adamk_prefill_set_pdl.argtypes = [i]
         lib.adamk_prefill_set_pdl.restype = None
         lib.adamk_prefill_set_trace.argtypes = [vp]
+        lib.adamk_prefill_prefetch_next.argtypes = [vp, ll]
+        lib.adamk_prefill_prefetch_next.restype = None
         lib.adamk_prefill_set_trace.restype = None
         lib.adamk_prefill_gemm.argtypes = [vp, i, i, i, vp, i, vp, vp, i, i, i, ll, i, vp]
         lib.adamk_prefill_embed.argtypes = [vp, i, vp, i, vp, vp]
@@ -77,7 +80,7 @@ def _ptr(t: torch.Tensor | None) -> C.c_void_p:
 
 
 def gemm(x_planes: torch.Tensor, w: torch.Tensor, out: torch.Tensor, bias: torch.Tensor | None = None,
-         epilogue: int = EPI_STORE, tile_n: int = 0) -> torch.Tensor:
+         epilogue: int = EPI_STORE, tile_n: int = 0, prefetch: torch.Tensor | None = None) -> torch.Tensor:
     """``out`` (op)= sum_p x_planes[p] @ w.T on the tensor cores.  ``x_planes`` bf16 [parts, T, K], ``w`` bf16 [N, K];
     ``out`` fp32 [T, N] (STORE / RESID / ATOMIC) or bf16 [parts_out, T, N / 2] (SWIGLU, gate / up interleaved in ``w``).
     ATOMIC adds into ``out`` with fp32 atomics and lets the library split K across SMs (decode-sized T)."""
@@ -95,6 +98,8 @@ def gemm(x_planes: torch.Tensor, w: torch.Tensor, out: torch.Tensor, bias: torch
         parts_out, ldo, stride = 1, N, 0
     if bias is not None:
         assert bias.dtype == torch.float32 and bias.numel() == N and epilogue in (EPI_STORE, EPI_ATOMIC)
+    if prefetch is not None:       # the weight of the GEMM that follows this one: pulled into L2 by this launch's idle warps
+        _lib().adamk_prefill_prefetch_next(_ptr(prefetch), min(prefetch.numel() * prefetch.element_size(), PREFETCH_MAX_BYTES))
     _ok(_lib().adamk_prefill_gemm(_ptr(x_planes), parts, T, K, _ptr(w), N, _ptr(bias), _ptr(out), ldo, epilogue, parts_out,
                                   stride, tile_n, _stream()))
     return out

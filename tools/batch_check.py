@@ -48,10 +48,10 @@ def parity(cfg, B, steps=6, max_ctx=320, oracle_cache=False):
     return worst
 
 
-def bench(name, B, ctx, steps=64, pdl=False):
+def bench(name, B, ctx, steps=64, pdl=False, l2_prefetch=False):
     cfg = PRESETS[name]
     w = random_weights(cfg, 0, device="cuda")
-    dec = BatchedDecoder(cfg, w, B, ctx + steps * 3 + 16, pdl=pdl)
+    dec = BatchedDecoder(cfg, w, B, ctx + steps * 3 + 16, pdl=pdl, l2_prefetch=l2_prefetch)
     dec.set_state(torch.randint(0, cfg.vocab, (B,)).tolist(), [ctx] * B)
     dec.capture()
     for _ in range(8):
@@ -65,7 +65,7 @@ def bench(name, B, ctx, steps=64, pdl=False):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     gb = cfg.algorithmic_bytes(ctx, 1) / 1e9
-    print(f"{name} batch {B} ctx {ctx} pdl {pdl}: {ms:.3f} ms/step, {B * 1e3 / ms:.0f} tokens/s, weights once per step -> "
+    print(f"{name} batch {B} ctx {ctx} pdl {pdl} l2_prefetch {l2_prefetch}: {ms:.3f} ms/step, {B * 1e3 / ms:.0f} tokens/s, weights once per step -> "
           f"{gb / ms * 1e3:.0f} GB/s of weight streaming ({dec.launches_per_step} own launches/step, CUDA graph)", flush=True)
     del dec
 
@@ -79,6 +79,7 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "quick":
         sys.exit(0)
     bench("qwen2.5-1.5b", 8, 2048, pdl=True)
+    bench("qwen2.5-1.5b", 8, 2048, l2_prefetch=True)
     for B in (8, 16, 32, 64, 128):
         bench("qwen2.5-1.5b", B, 2048)
     bench("qwen2.5-7b", 8, 2048)
