@@ -142,3 +142,33 @@ def test_cuda_graph_replay_equals_eager_steps():
     # fp32 atomics make the two runs differ in the last bits; tokens differ only on near-ties, which these seeds avoid
     assert torch.equal(runs[0][0], runs[1][0])
     assert torch.equal(runs[0][1], runs[1][1]) and runs[0][1].tolist() == [len(p) - 1 + 12 for p in prompts]
+
+
+def test_gemm_hints_do_not_change_results():
+    """adamk_prefill_prefetch_next (L2 prefetch of the next weight by the idle warps), adamk_prefill_set_pdl and
+    adamk_prefill_set_trace are performance / debug hooks: same numbers with and without them, and the trace holds
+    ordered %globaltimer stamps."""
+    from paper_2605_11581_b200 import prefill as P
+
+    lib = P._lib()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = _planes(torch.randn(8, 1536, device="cuda", generator=g), 2)
+    w = (torch.randn(2048, 1536, device="cuda", generator=g) / 39.0).to(torch.bfloat16)
+    nxt = torch.randn(3 << 20, device="cuda", generator=g).to(torch.bfloat16)
+    want = x.double().sum(0) @ w.double().T
+    stamps = torch.zeros(16, dtype=torch.int64, device="cuda")
+    outs = []
+    for hints in (False, True):
+        out = torch.zeros(8, 2048, device="cuda")
+        if hints:
+            lib.adamk_prefill_set_pdl(1)
+            lib.adamk_prefill_set_trace(P._ptr(stamps))
+        P.gemm(x, w, out, epilogue=P.EPI_ATOMIC, prefetch=nxt if hints else None)
+        lib.adamk_prefill_set_pdl(0)
+        lib.adamk_prefill_set_trace(None)
+        torch.cuda.synchronize()
+        outs.append(out)
+        assert (out.double() - want).abs().max().item() <= 4e-5 * want.abs().max().item()
+    t = stamps.tolist()
+    assert 0 < t[0] <= t[1] <= t[2] <= t[3] <= t[6] <= t[4] <= t[5]
+    assert (outs[0] - outs[1]).abs().max().item() <= 1e-5      # fp32 atomics: order-dependent last bits only
