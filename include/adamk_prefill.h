@@ -67,6 +67,11 @@ void adamk_prefill_set_trace(void* stamps);
 int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void* w, int N, const float* bias, void* out, int ldo,
                        int epilogue, int parts_out, long long part_stride, int tile_n, adamk_pf_stream stream);
 
+/* How adamk_prefill_gemm would cut this problem on a GPU with n_sms SMs -- host arithmetic only, no device needed:
+ * plan_out = {tile (ADAMK_PF_TILE_*), tiles, whole-tile items, column slices per last-wave tile, work items, K splits,
+ * k blocks (of 64) per split, planes stacked in one token tile (0/1), grid size}. */
+int adamk_prefill_gemm_plan(int parts, int T, int K, int N, int epilogue, int tile_n, int n_sms, int32_t plan_out[9]);
+
 /* h fp32 [T, H] = embed[tokens[t]] (bf16 table). */
 int adamk_prefill_embed(const int32_t* tokens, int T, const void* embed, int H, float* h, adamk_pf_stream stream);
 

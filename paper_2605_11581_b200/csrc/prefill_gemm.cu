@@ -27,7 +27,6 @@
 #include <stdint.h>
 
 #include <cstdio>
-#include <cstdlib>
 #include <mutex>
 
 #include "../../include/adamk_prefill.h"
@@ -723,8 +722,95 @@ static bool make_map(CUtensorMap* m, const void* base, long long rows, long long
   return true;
 }
 
+// How one GEMM call is cut into work: tile shape, work items (whole tiles + column slices of the last wave), split-K.
+// Pure host arithmetic (adamk_prefill_gemm_plan exposes it; tests/test_prefill_plan.py checks it without a GPU).
+struct Plan {
+  int tile;   // ADAMK_PF_TILE_128 / _256 / _PAIR
+  int tiles, main_items, tail_split, n_items, ksplit, kb_per_split, stacked, grid;
+};
+
+static double waves_of(long long tiles, int units, int max_split) {
+  const long long full = tiles / units, rem = tiles % units;
+  int split = 1;
+  while (rem > 0 && split * 2 <= max_split && rem * split * 2 <= units) split *= 2;
+  return double(full) + (rem ? 1.0 / split : 0.0);
+}
+
+static Plan plan_gemm(int T, int N, int K, int parts, int epilogue, int tile, int n_sms) {
+  Plan p = {};
+  if (tile == ADAMK_PF_TILE_AUTO) {
+    // 256-wide tiles for wide outputs; between one CTA per tile and a CTA pair per 256 x 256 tile take the one whose
+    // last wave is fuller (tile times are equal: a pair does twice the work on twice the SMs), pairs on a tie.
+    if (N < 1024 && epilogue != ADAMK_PF_EPI_SWIGLU) {
+      tile = ADAMK_PF_TILE_128;
+    } else {
+      const long long n_t = (N + 255) / 256;
+      const double single = waves_of((long long)((T + BM - 1) / BM) * n_t, n_sms, epilogue == ADAMK_PF_EPI_SWIGLU ? 2 : 4);
+      const double paired = waves_of((long long)((T + 2 * BM - 1) / (2 * BM)) * n_t, n_sms / 2, 2);
+      tile = (T > BM && paired <= single && epilogue != ADAMK_PF_EPI_ATOMIC && n_sms >= 2) ? ADAMK_PF_TILE_PAIR : ADAMK_PF_TILE_256;
+    }
+  }
+  p.tile = tile;
+  const int kb_per_part = (K + BK - 1) / BK;
+  p.ksplit = 1;
+  p.kb_per_split = kb_per_part;
+  p.tail_split = 1;
+  if (tile == ADAMK_PF_TILE_PAIR) {
+    p.tiles = ((T + 2 * BM - 1) / (2 * BM)) * ((N + 255) / 256);
+    const int max_pairs = n_sms / 2;
+    const int pairs = p.tiles < max_pairs ? p.tiles : max_pairs;
+    const int rem = p.tiles % pairs;
+    p.tail_split = (rem > 0 && rem * 2 <= pairs) ? 2 : 1;   // a slice is at least one 64-row weight box per CTA
+    p.main_items = p.tiles - rem;
+    p.n_items = p.main_items + rem * p.tail_split;
+    p.grid = 2 * pairs;
+    return p;
+  }
+  // One CTA per tile.  Whole tiles, except that the tiles of a last partial wave are cut into column slices so that
+  // the wave keeps every SM busy for a fraction of a tile time; with fewer tiles than SMs every tile is sliced.
+  const int BN = tile;
+  p.tiles = ((T + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int max_split = (epilogue == ADAMK_PF_EPI_SWIGLU) ? BN / (2 * BOXN) : BN / BOXN;
+  int split = 1;
+  if (epilogue == ADAMK_PF_EPI_ATOMIC) {
+    // decode-sized: whole weight boxes per stage and as many K ranges as there are idle SMs keep the most bytes in
+    // flight; all planes ride in one token tile when they fit
+    p.main_items = p.tiles;
+    p.n_items = p.tiles;
+    p.stacked = (parts * T <= BM) ? 1 : 0;
+    if (p.tiles * 2 <= n_sms) {
+      int want = n_sms / p.tiles;
+      if (want > kb_per_part) want = kb_per_part;
+      p.kb_per_split = (kb_per_part + want - 1) / want;
+      p.ksplit = (kb_per_part + p.kb_per_split - 1) / p.kb_per_split;
+    }
+  } else if (p.tiles < n_sms) {
+    while (split * 2 <= max_split && p.tiles * split * 2 <= n_sms) split *= 2;
+    p.main_items = 0;
+    p.n_items = p.tiles * split;
+  } else {
+    const int rem = p.tiles % n_sms;
+    while (rem > 0 && split * 2 <= max_split && rem * split * 2 <= n_sms) split *= 2;
+    p.main_items = p.tiles - rem;
+    p.n_items = p.main_items + rem * split;
+  }
+  p.tail_split = split;
+  const long long work = (long long)p.n_items * p.ksplit;
+  p.grid = work < n_sms ? int(work) : n_sms;
+  return p;
+}
+
+static void apply_plan(GemmArgs& g, const Plan& p) {
+  g.main_items = p.main_items;
+  g.tail_split = p.tail_split;
+  g.n_items = p.n_items;
+  g.ksplit = p.ksplit;
+  g.kb_per_split = p.kb_per_split;
+  g.stacked = p.stacked;
+}
+
 template <int BN, int EPI>
-static int launch(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& g_in, int n_sms, cudaStream_t stream) {
+static int launch(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& g_in, const Plan& plan, cudaStream_t stream) {
   static bool configured = false;
   auto kern = gemm_kernel<BN, EPI>;
   if (!configured) {
@@ -735,44 +821,9 @@ static int launch(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& 
     }
     configured = true;
   }
-  // Work items: whole tiles, except that the tiles of a last partial wave are cut into column slices so that the
-  // wave keeps every SM busy for a fraction of a tile time instead of a few SMs for a whole one.  With fewer tiles
-  // than SMs (decode-sized T) every tile is sliced, and the atomic epilogue also splits K.
-  const int tiles = ((g_in.T + BM - 1) / BM) * ((g_in.N + BN - 1) / BN);
-  const int max_split = (EPI == ADAMK_PF_EPI_SWIGLU) ? BN / (2 * BOXN) : BN / BOXN;
   GemmArgs g = g_in;
-  int split = 1;
-  const int kb_per_part = (g.K + BK - 1) / BK;
-  g.ksplit = 1;
-  g.kb_per_split = kb_per_part;
-  g.stacked = 0;
-  if (EPI == ADAMK_PF_EPI_ATOMIC) {
-    // decode-sized: whole 32 KB weight boxes per stage and as many K ranges as there are idle SMs keep the most
-    // bytes in flight; all planes ride in one token tile when they fit
-    g.main_items = tiles;
-    g.n_items = tiles;
-    g.stacked = (g.parts * g.T <= BM) ? 1 : 0;
-    if (tiles * 2 <= n_sms) {
-      int want = n_sms / tiles;
-      static const int cap = [] { const char* e = getenv("ADAMK_PF_KSPLIT_MAX"); return e ? atoi(e) : 1 << 30; }();   // experiments
-      if (want > cap) want = cap;
-      if (want > kb_per_part) want = kb_per_part;
-      g.kb_per_split = (kb_per_part + want - 1) / want;
-      g.ksplit = (kb_per_part + g.kb_per_split - 1) / g.kb_per_split;
-    }
-  } else if (tiles < n_sms) {
-    while (split * 2 <= max_split && tiles * split * 2 <= n_sms) split *= 2;
-    g.main_items = 0;
-    g.n_items = tiles * split;
-  } else {
-    const int rem = tiles % n_sms;
-    while (rem > 0 && split * 2 <= max_split && rem * split * 2 <= n_sms) split *= 2;
-    g.main_items = tiles - rem;
-    g.n_items = g.main_items + rem * split;
-  }
-  g.tail_split = split;
-  const long long work = (long long)g.n_items * g.ksplit;
-  const int grid = work < n_sms ? int(work) : n_sms;
+  apply_plan(g, plan);
+  const int grid = plan.grid;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(grid);
   lc.blockDim = dim3(kThreads);
@@ -793,7 +844,7 @@ static int launch(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& 
 }
 
 template <int EPI>
-static int launch_pair(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& g_in, int n_sms, cudaStream_t stream) {
+static int launch_pair(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& g_in, const Plan& plan, cudaStream_t stream) {
   static bool configured = false;
   auto kern = gemm_pair_kernel<EPI>;
   if (!configured) {
@@ -804,21 +855,10 @@ static int launch_pair(const CUtensorMap& mx, const CUtensorMap& mw, const GemmA
     }
     configured = true;
   }
-  constexpr int BN = PairSmem::BN;
-  const int tiles = ((g_in.T + 2 * BM - 1) / (2 * BM)) * ((g_in.N + BN - 1) / BN);
-  const int max_pairs = n_sms / 2;
-  const int pairs = tiles < max_pairs ? tiles : max_pairs;
-  const int rem = tiles % pairs;
-  const int split = (rem > 0 && rem * 2 <= pairs) ? 2 : 1;   // a slice is at least one 64-row weight box per CTA
   GemmArgs g = g_in;
-  g.main_items = tiles - rem;
-  g.tail_split = split;
-  g.n_items = g.main_items + rem * split;
-  g.ksplit = 1;
-  g.kb_per_split = (g.K + BK - 1) / BK;
-  g.stacked = 0;
+  apply_plan(g, plan);
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(2 * pairs);
+  lc.gridDim = dim3(plan.grid);
   lc.blockDim = dim3(kThreads);
   lc.dynamicSmemBytes = PairSmem::kBytes;
   lc.stream = stream;
@@ -851,10 +891,10 @@ void adamk_prefill_prefetch_next(const void* ptr, long long bytes) {
 
 void adamk_prefill_set_trace(void* stamps) { pf::g_trace = static_cast<unsigned long long*>(stamps); }
 
-int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void* w, int N, const float* bias, void* out, int ldo,
-                       int epilogue, int parts_out, long long part_stride, int tile_n, adamk_pf_stream stream) {
+// Argument checks shared by the planner and the launcher (no device access).
+static int check_shape(int parts, int T, int K, int N, int ldo, int epilogue, int parts_out, int tile_n) {
   using namespace pf;
-  if (x_planes == nullptr || w == nullptr || out == nullptr || T <= 0 || N <= 0 || K <= 0 || (parts != 1 && parts != 2)) {
+  if (T <= 0 || N <= 0 || K <= 0 || (parts != 1 && parts != 2)) {
     snprintf(g_err, sizeof g_err, "prefill gemm: bad argument (T %d N %d K %d parts %d)", T, N, K, parts);
     return ADAMK_PF_E_INVALID;
   }
@@ -862,6 +902,47 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
     snprintf(g_err, sizeof g_err, "prefill gemm: K, N and ldo must be multiples of 8 (K %d N %d ldo %d)", K, N, ldo);
     return ADAMK_PF_E_INVALID;
   }
+  if (epilogue < ADAMK_PF_EPI_STORE || epilogue > ADAMK_PF_EPI_ATOMIC) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: unknown epilogue %d", epilogue);
+    return ADAMK_PF_E_INVALID;
+  }
+  if (tile_n != ADAMK_PF_TILE_AUTO && tile_n != ADAMK_PF_TILE_128 && tile_n != ADAMK_PF_TILE_256 && tile_n != ADAMK_PF_TILE_PAIR) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: tile must be 0, 128, 256 or ADAMK_PF_TILE_PAIR");
+    return ADAMK_PF_E_INVALID;
+  }
+  if (tile_n == ADAMK_PF_TILE_PAIR && epilogue == ADAMK_PF_EPI_ATOMIC) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: the atomic (split-K) epilogue runs on one-CTA tiles only");
+    return ADAMK_PF_E_INVALID;
+  }
+  if (epilogue == ADAMK_PF_EPI_SWIGLU) {
+    const int width = tile_n == ADAMK_PF_TILE_128 ? 128 : 256;
+    if (N % width != 0 || (parts_out != 1 && parts_out != 2)) {
+      snprintf(g_err, sizeof g_err, "prefill gemm: SwiGLU epilogue needs N %% tile width == 0 and 1 or 2 output planes");
+      return ADAMK_PF_E_INVALID;
+    }
+  }
+  return ADAMK_PF_OK;
+}
+
+int adamk_prefill_gemm_plan(int parts, int T, int K, int N, int epilogue, int tile_n, int n_sms, int32_t plan_out[9]) {
+  if (plan_out == nullptr || n_sms <= 0) return ADAMK_PF_E_INVALID;
+  const int rc = check_shape(parts, T, K, N, 8, epilogue, 2, tile_n);
+  if (rc != ADAMK_PF_OK) return rc;
+  const pf::Plan p = pf::plan_gemm(T, N, K, parts, epilogue, tile_n, n_sms);
+  const int32_t v[9] = {p.tile, p.tiles, p.main_items, p.tail_split, p.n_items, p.ksplit, p.kb_per_split, p.stacked, p.grid};
+  for (int i = 0; i < 9; ++i) plan_out[i] = v[i];
+  return ADAMK_PF_OK;
+}
+
+int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void* w, int N, const float* bias, void* out, int ldo,
+                       int epilogue, int parts_out, long long part_stride, int tile_n, adamk_pf_stream stream) {
+  using namespace pf;
+  if (x_planes == nullptr || w == nullptr || out == nullptr) {
+    snprintf(g_err, sizeof g_err, "prefill gemm: null operand");
+    return ADAMK_PF_E_INVALID;
+  }
+  const int rc = check_shape(parts, T, K, N, ldo, epilogue, parts_out, tile_n);
+  if (rc != ADAMK_PF_OK) return rc;
   if ((reinterpret_cast<uintptr_t>(x_planes) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(out)) & 15) {
     snprintf(g_err, sizeof g_err, "prefill gemm: operands must be 16-byte aligned");
     return ADAMK_PF_E_INVALID;
@@ -871,65 +952,30 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
     snprintf(g_err, sizeof g_err, "prefill gemm: no CUDA device");
     return ADAMK_PF_E_CUDA;
   }
-  if (tile_n == 0) {
-    // 256-wide tiles for wide outputs; between one CTA per tile and a CTA pair per 256 x 256 tile take the one whose
-    // last wave is fuller (tile times are equal: a pair does twice the work on twice the SMs), pairs on a tie.
-    if (N < 1024 && epilogue != ADAMK_PF_EPI_SWIGLU) {
-      tile_n = 128;
-    } else {
-      auto waves = [](long long tiles, int units, int max_split) {
-        const long long full = tiles / units, rem = tiles % units;
-        int split = 1;
-        while (rem > 0 && split * 2 <= max_split && rem * split * 2 <= units) split *= 2;
-        return double(full) + (rem ? 1.0 / split : 0.0);
-      };
-      const long long n_t = (N + 255) / 256;
-      const double single = waves((long long)((T + BM - 1) / BM) * n_t, n_sms, epilogue == ADAMK_PF_EPI_SWIGLU ? 2 : 4);
-      const double paired = waves((long long)((T + 2 * BM - 1) / (2 * BM)) * n_t, n_sms / 2, 2);
-      tile_n = (T > BM && paired <= single && epilogue != ADAMK_PF_EPI_ATOMIC) ? ADAMK_PF_TILE_PAIR : 256;
-    }
-  }
-  if (tile_n != 128 && tile_n != 256 && tile_n != ADAMK_PF_TILE_PAIR) {
-    snprintf(g_err, sizeof g_err, "prefill gemm: tile must be 0, 128, 256 or ADAMK_PF_TILE_PAIR");
-    return ADAMK_PF_E_INVALID;
-  }
-  const bool pair = tile_n == ADAMK_PF_TILE_PAIR;
-  if (pair && epilogue == ADAMK_PF_EPI_ATOMIC) {
-    snprintf(g_err, sizeof g_err, "prefill gemm: the atomic (split-K) epilogue runs on one-CTA tiles only");
-    return ADAMK_PF_E_INVALID;
-  }
-  if (pair) tile_n = 256;
-  if (epilogue == ADAMK_PF_EPI_SWIGLU && (N % tile_n != 0 || (parts_out != 1 && parts_out != 2))) {
-    snprintf(g_err, sizeof g_err, "prefill gemm: SwiGLU epilogue needs N %% tile_n == 0 and 1 or 2 output planes");
-    return ADAMK_PF_E_INVALID;
-  }
+  const Plan plan = plan_gemm(T, N, K, parts, epilogue, tile_n, n_sms);
   CUtensorMap mx, mw;
   if (!make_map(&mx, x_planes, (long long)parts * T, K, BM) || !make_map(&mw, w, N, K, BOXN)) return ADAMK_PF_E_CUDA;
   GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride, 0, 1, 0, 1, 0, g_pf_ptr, g_pf_bytes, g_trace, 0};
   g_pf_ptr = nullptr;
   g_pf_bytes = 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (pair) {
+  if (plan.tile == ADAMK_PF_TILE_PAIR) {
     switch (epilogue) {
-      case ADAMK_PF_EPI_STORE: return launch_pair<ADAMK_PF_EPI_STORE>(mx, mw, g, n_sms, s);
-      case ADAMK_PF_EPI_RESID: return launch_pair<ADAMK_PF_EPI_RESID>(mx, mw, g, n_sms, s);
-      case ADAMK_PF_EPI_SWIGLU: return launch_pair<ADAMK_PF_EPI_SWIGLU>(mx, mw, g, n_sms, s);
+      case ADAMK_PF_EPI_STORE: return launch_pair<ADAMK_PF_EPI_STORE>(mx, mw, g, plan, s);
+      case ADAMK_PF_EPI_RESID: return launch_pair<ADAMK_PF_EPI_RESID>(mx, mw, g, plan, s);
+      default: return launch_pair<ADAMK_PF_EPI_SWIGLU>(mx, mw, g, plan, s);
     }
-    snprintf(g_err, sizeof g_err, "prefill gemm: unknown epilogue %d", epilogue);
-    return ADAMK_PF_E_INVALID;
   }
-  switch (epilogue * 1000 + tile_n) {
-    case ADAMK_PF_EPI_STORE * 1000 + 128: return launch<128, ADAMK_PF_EPI_STORE>(mx, mw, g, n_sms, s);
-    case ADAMK_PF_EPI_STORE * 1000 + 256: return launch<256, ADAMK_PF_EPI_STORE>(mx, mw, g, n_sms, s);
-    case ADAMK_PF_EPI_RESID * 1000 + 128: return launch<128, ADAMK_PF_EPI_RESID>(mx, mw, g, n_sms, s);
-    case ADAMK_PF_EPI_RESID * 1000 + 256: return launch<256, ADAMK_PF_EPI_RESID>(mx, mw, g, n_sms, s);
-    case ADAMK_PF_EPI_ATOMIC * 1000 + 128: return launch<128, ADAMK_PF_EPI_ATOMIC>(mx, mw, g, n_sms, s);
-    case ADAMK_PF_EPI_ATOMIC * 1000 + 256: return launch<256, ADAMK_PF_EPI_ATOMIC>(mx, mw, g, n_sms, s);
-    case ADAMK_PF_EPI_SWIGLU * 1000 + 128: return launch<128, ADAMK_PF_EPI_SWIGLU>(mx, mw, g, n_sms, s);
-    case ADAMK_PF_EPI_SWIGLU * 1000 + 256: return launch<256, ADAMK_PF_EPI_SWIGLU>(mx, mw, g, n_sms, s);
+  switch (epilogue * 1000 + plan.tile) {
+    case ADAMK_PF_EPI_STORE * 1000 + 128: return launch<128, ADAMK_PF_EPI_STORE>(mx, mw, g, plan, s);
+    case ADAMK_PF_EPI_STORE * 1000 + 256: return launch<256, ADAMK_PF_EPI_STORE>(mx, mw, g, plan, s);
+    case ADAMK_PF_EPI_RESID * 1000 + 128: return launch<128, ADAMK_PF_EPI_RESID>(mx, mw, g, plan, s);
+    case ADAMK_PF_EPI_RESID * 1000 + 256: return launch<256, ADAMK_PF_EPI_RESID>(mx, mw, g, plan, s);
+    case ADAMK_PF_EPI_ATOMIC * 1000 + 128: return launch<128, ADAMK_PF_EPI_ATOMIC>(mx, mw, g, plan, s);
+    case ADAMK_PF_EPI_ATOMIC * 1000 + 256: return launch<256, ADAMK_PF_EPI_ATOMIC>(mx, mw, g, plan, s);
+    case ADAMK_PF_EPI_SWIGLU * 1000 + 128: return launch<128, ADAMK_PF_EPI_SWIGLU>(mx, mw, g, plan, s);
+    default: return launch<256, ADAMK_PF_EPI_SWIGLU>(mx, mw, g, plan, s);
   }
-  snprintf(g_err, sizeof g_err, "prefill gemm: unknown epilogue %d", epilogue);
-  return ADAMK_PF_E_INVALID;
 }
 
 }  // extern "C"

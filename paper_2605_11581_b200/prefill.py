@@ -31,7 +31,8 @@ TILE_AUTO, TILE_128, TILE_256, TILE_PAIR = 0, 128, 256, 512   # include/adamk_pr
 PREFETCH_MAX_BYTES = 64 << 20   # L2 prefetch hint cap (half of the 126 MB L2)
 GU_BLOCK = 128   # features per gate / up block of the interleaved weight = half of a 256-wide GEMM tile
 
-PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_prefill_set_trace", "adamk_prefill_prefetch_next", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
+PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_prefill_set_trace", "adamk_prefill_prefetch_next",
+                   "adamk_prefill_gemm_plan", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
                    "adamk_prefill_split", "adamk_prefill_rope_store", "adamk_batch_rope_store", "adamk_batch_attention_workspace",
                    "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split")
 
@@ -51,6 +52,7 @@ def _lib():
         lib.adamk_prefill_prefetch_next.restype = None
         lib.adamk_prefill_set_trace.restype = None
         lib.adamk_prefill_gemm.argtypes = [vp, i, i, i, vp, i, vp, vp, i, i, i, ll, i, vp]
+        lib.adamk_prefill_gemm_plan.argtypes = [i, i, i, i, i, i, i, C.POINTER(C.c_int32)]
         lib.adamk_prefill_embed.argtypes = [vp, i, vp, i, vp, vp]
         lib.adamk_prefill_rmsnorm_split.argtypes = [vp, vp, f, i, i, vp, i, vp]
         lib.adamk_prefill_split.argtypes = [vp, ll, vp, i, vp]
@@ -103,6 +105,16 @@ def gemm(x_planes: torch.Tensor, w: torch.Tensor, out: torch.Tensor, bias: torch
     _ok(_lib().adamk_prefill_gemm(_ptr(x_planes), parts, T, K, _ptr(w), N, _ptr(bias), _ptr(out), ldo, epilogue, parts_out,
                                   stride, tile_n, _stream()))
     return out
+
+
+PLAN_FIELDS = ("tile", "tiles", "main_items", "tail_split", "n_items", "ksplit", "kb_per_split", "stacked", "grid")
+
+
+def gemm_plan(parts: int, T: int, K: int, N: int, epilogue: int = EPI_STORE, tile_n: int = 0, n_sms: int = 148) -> dict:
+    """How ``gemm`` would cut this problem into work items on ``n_sms`` SMs (host arithmetic in the library; no GPU)."""
+    out = (C.c_int32 * 9)()
+    _ok(_lib().adamk_prefill_gemm_plan(parts, T, K, N, epilogue, tile_n, n_sms, out))
+    return dict(zip(PLAN_FIELDS, out))
 
 
 def interleave_gate_up(wgate: torch.Tensor, wup: torch.Tensor, block: int = GU_BLOCK) -> torch.Tensor:
