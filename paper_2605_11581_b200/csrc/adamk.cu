@@ -54,7 +54,6 @@ constexpr int kChunk = 256;          // K elements per chunk
 constexpr int kSmemMax = 232448;
 constexpr int kSmemReserved = 4096;  // barriers + reduction scratch
 constexpr int kMaxStages = 16;
-constexpr int kAttnBlockMax = 64;    // positions per K (or V) ring stage: 8 per attention warp (p.attn_block)
 constexpr int kAttnWarps = 8;        // consumer warps that take part in an attention unit
 constexpr int kAttnChunksMax = 128;  // split-KV units per (sequence, kv head)
 constexpr int kGMax = 8;             // max q heads per kv head
@@ -1769,7 +1768,6 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   }
   h->smem_bytes = kSmemReserved + h->task_cache_bytes + h->scratch_bytes + h->n_stage * h->stage_bytes;
   if (h->smem_bytes > kSmemMax) return bad("ring + scratch + task cache exceed 227 KB shared memory");
-  const int G = d.n_q_heads / d.n_kv_heads;
   {  // the scratch region must hold the widest activation vector, and the attention buffers
     const int kmax = std::max(std::max(d.hidden, d.n_q_heads * d.head_dim), d.intermediate);
     const size_t xb = align_up((size_t)kmax, kChunk) * 4;

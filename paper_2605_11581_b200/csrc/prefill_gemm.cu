@@ -743,6 +743,11 @@ static Plan plan_gemm(int T, int N, int K, int parts, int epilogue, int tile, in
     // last wave is fuller (tile times are equal: a pair does twice the work on twice the SMs), pairs on a tie.
     if (N < 1024 && epilogue != ADAMK_PF_EPI_SWIGLU) {
       tile = ADAMK_PF_TILE_128;
+    } else if (epilogue == ADAMK_PF_EPI_ATOMIC && T <= BM && (long long)N * K * 2 <= (32ll << 20)) {
+      // decode-sized and short: the one-warp epilogue (1.8 us per 128 columns) outweighs the k loop, which a
+      // 128-wide tile lengthens (tools/gemm_trace.py: 12.1 vs 13.3 us for QKV, 16.3 vs 17.4 for down, but 24.8 vs
+      // 24.3 for the 55 MB gate/up matrix, which therefore stays on 256)
+      tile = ADAMK_PF_TILE_128;
     } else {
       const long long n_t = (N + 255) / 256;
       const double single = waves_of((long long)((T + BM - 1) / BM) * n_t, n_sms, epilogue == ADAMK_PF_EPI_SWIGLU ? 2 : 4);

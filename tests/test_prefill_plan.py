@@ -23,14 +23,17 @@ def test_prefill_shapes_pick_the_fuller_last_wave():
 
 
 def test_decode_shapes_split_k_and_stack_planes():
-    # batch 8, two planes: 16 rows of one token tile, 8 tiles x 12 K ranges of 2 k blocks = 96 CTAs
+    # batch 8, two planes: 16 rows of one token tile; short weights take 128-wide tiles (half the one-warp epilogue):
+    # 16 tiles x 8 K ranges of 3 k blocks = 128 CTAs
     p = P.gemm_plan(2, 8, 1536, 2048, P.EPI_ATOMIC)
-    assert (p["tile"], p["tiles"], p["ksplit"], p["kb_per_split"], p["stacked"], p["grid"]) == (P.TILE_256, 8, 12, 2, 1, 96)
-    assert p["ksplit"] * p["kb_per_split"] >= 1536 // 64 > (p["ksplit"] - 1) * p["kb_per_split"]      # ranges cover K, none empty
-    # down projection: 6 tiles x 24 ranges; gate/up has 70 tiles -> 2 ranges
-    assert P.gemm_plan(2, 8, 8960, 1536, P.EPI_ATOMIC)["ksplit"] == 24
+    assert (p["tile"], p["tiles"], p["ksplit"], p["kb_per_split"], p["stacked"], p["grid"]) == (P.TILE_128, 16, 8, 3, 1, 128)
+    p = P.gemm_plan(2, 8, 1536, 2048, P.EPI_ATOMIC, tile_n=P.TILE_256)
+    assert (p["tiles"], p["ksplit"], p["kb_per_split"], p["grid"]) == (8, 12, 2, 96)
+    # down projection: 12 tiles x 12 ranges; the 55 MB gate/up matrix stays on 256-wide tiles: 70 tiles x 2 ranges
+    p = P.gemm_plan(2, 8, 8960, 1536, P.EPI_ATOMIC)
+    assert (p["tile"], p["tiles"], p["ksplit"], p["grid"]) == (P.TILE_128, 12, 12, 144)
     p = P.gemm_plan(2, 8, 1536, 17920, P.EPI_ATOMIC)
-    assert p["tiles"] == 70 and p["ksplit"] == 2 and p["grid"] == 140
+    assert p["tile"] == P.TILE_256 and p["tiles"] == 70 and p["ksplit"] == 2 and p["grid"] == 140
     # LM head: more tiles than SMs -> no K split; batch 128 x 2 planes does not fit one tile -> two passes over K
     assert P.gemm_plan(2, 8, 1536, 151936, P.EPI_ATOMIC)["ksplit"] == 1
     assert P.gemm_plan(2, 128, 1536, 2048, P.EPI_ATOMIC)["stacked"] == 0 and P.gemm_plan(2, 64, 1536, 2048, P.EPI_ATOMIC)["stacked"] == 1
