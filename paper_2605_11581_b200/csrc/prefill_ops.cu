@@ -522,6 +522,8 @@ int adamk_batch_attention(const float* q, const void* k_cache, const void* v_cac
       case 1: ADAMK_ATTN_CASE(64, 1); break;
       case 2: ADAMK_ATTN_CASE(64, 2); break;
       case 4: ADAMK_ATTN_CASE(64, 4); break;
+      case 6: ADAMK_ATTN_CASE(64, 6); break;
+      case 7: ADAMK_ATTN_CASE(64, 7); break;
       case 8: ADAMK_ATTN_CASE(64, 8); break;
       default: ok = false;
     }

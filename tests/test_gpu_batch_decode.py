@@ -17,6 +17,10 @@ pytestmark = pytest.mark.gpu
 
 D128_Q3 = ModelConfig(name="test-d128-q3", hidden=512, n_layers=3, n_q_heads=8, n_kv_heads=2, head_dim=128,
                       intermediate=1536, vocab=3000, qkv_bias=False, qk_norm=True, tied_embed=False)
+# the GQA group sizes of the real presets: Qwen2.5-1.5B 12/2 = 6, Qwen2.5-7B 28/4 = 7 (Qwen3-8B's 4 is D128_Q3)
+G6 = ModelConfig(name="test-g6", hidden=512, n_layers=2, n_q_heads=12, n_kv_heads=2, head_dim=128, intermediate=1024, vocab=2048)
+G7 = ModelConfig(name="test-g7", hidden=896, n_layers=2, n_q_heads=7, n_kv_heads=1, head_dim=128, intermediate=1152, vocab=2048,
+                 tied_embed=False)
 D128 = ModelConfig(name="test-d128", hidden=512, n_layers=2, n_q_heads=4, n_kv_heads=2, head_dim=128,
                    intermediate=1280, vocab=4096)
 
@@ -113,7 +117,8 @@ def _run_parity(cfg, B, steps, oracle_cache, max_ctx=320, seed=11):
 
 
 @pytest.mark.parametrize("cfg,B,oracle_cache", [(TINY, 3, False), (TINY_QWEN3, 5, True), (D128, 4, False), (D128_Q3, 8, False),
-                                                 (D128_Q3, 8, True), (D128_Q3, 1, False), (D128, 70, True)])
+                                                 (D128_Q3, 8, True), (D128_Q3, 1, False), (D128, 70, True), (G6, 5, False),
+                                                 (G7, 9, False)])
 def test_batched_decode_matches_oracle(cfg, B, oracle_cache):
     worst, dec = _run_parity(cfg, B, steps=5, oracle_cache=oracle_cache)
     assert worst <= 5e-3, worst
