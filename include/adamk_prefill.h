@@ -59,7 +59,8 @@ void adamk_prefill_set_trace(void* stamps);
 
 /* D[T, N] = X[T, K] . W[N, K]^T on the tensor cores, fp32 accumulation in tensor memory.
  *   x_planes  bf16 [parts][T, K] row-major: the activation as `parts` bf16 planes whose sum is the fp32 value
- *             (parts 2 = hi + lo, ~2^-17 relative; parts 1 = plain bf16).
+ *             (parts 1 = plain bf16; 2 = hi + lo, ~2^-17 relative; 3 = hi + mid + lo, below fp32 resolution --
+ *             free for decode-sized T, where all planes ride in one token tile).
  *   w         bf16 [N, K] row-major (Hugging Face layout).
  *   tile_n    one of ADAMK_PF_TILE_*; the SwiGLU weight interleaves gate / up in blocks of 128 features for the
  *             256-wide tiles (ADAMK_PF_TILE_256 / _PAIR) and 64 for ADAMK_PF_TILE_128.

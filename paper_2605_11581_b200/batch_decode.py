@@ -9,8 +9,9 @@ runs one decode step of ``B`` sequences with the operators of ``include/adamk_pr
   ``W``).  A decode-sized GEMM has fewer tiles than SMs, so K is split across SMs with an fp32-atomic epilogue
   (``EPI_ATOMIC``), which is what lets every SM pull weight bytes, and both activation planes ride in the one token
   tile, so a weight byte is read once.  SwiGLU is a row kernel on the gate/up result.
-* activations enter the tensor cores as two bf16 planes (hi + lo), so the step keeps the MegaKernel's numerical
-  contract (fp32 activations against exact bf16 weights) at no cost in time.
+* activations enter the tensor cores as bf16 planes whose sum is the fp32 value -- three (hi + mid + lo, exact to
+  fp32) while 3 B <= 128 rows still fit the one token tile, two (2^-17) beyond -- so the step keeps the MegaKernel's
+  numerical contract (fp32 activations against exact bf16 weights) at no cost in time.
 * ``adamk_batch_rope_store`` (per-sequence positions), ``adamk_batch_attention`` (split over 256-row chunks of
   each sequence's cache + merge) and ``adamk_batch_argmax`` (greedy pick, tokens / positions advanced on the device).
 
@@ -43,14 +44,16 @@ class _SequenceCache:
 
 
 class BatchedDecoder:
-    def __init__(self, cfg: ModelConfig, weights: DecoderWeights, batch: int, max_ctx: int, device: int = 0, planes: int = 2,
+    def __init__(self, cfg: ModelConfig, weights: DecoderWeights, batch: int, max_ctx: int, device: int = 0, planes: int | None = None,
                  pdl: bool = False, l2_prefetch: bool = False):
         if not torch.cuda.is_available():
             raise AdamkError(-102, "no CUDA device: batched decode has no CPU fallback")
         if not 1 <= batch <= 128:
             raise ValueError("batch must be 1..128 (one 128-row GEMM tile)")
-        if planes not in (1, 2):
-            raise ValueError("planes must be 1 or 2")
+        if planes is None:      # three planes (activations exact to fp32) while they still share one 128-row token tile
+            planes = 3 if 3 * batch <= 128 else 2
+        if planes not in (1, 2, 3):
+            raise ValueError("planes must be 1, 2 or 3")
         self.lib = _lib()
         self.cfg, self.batch, self.max_ctx, self.planes = cfg, batch, int(max_ctx), planes
         # every GEMM pulls the next GEMM's weight into L2 while it waits for its own (measured: -3.6 % step time on
@@ -106,7 +109,7 @@ class BatchedDecoder:
         if prompt.numel() < 1 or prompt.numel() + 1 > self.max_ctx:
             raise ValueError("prompt is empty or does not fit the KV cache")
         if prompt.numel() > 1:
-            TensorCorePrefill(self.cfg, self._weights, _SequenceCache(self, b), planes=self.planes,
+            TensorCorePrefill(self.cfg, self._weights, _SequenceCache(self, b), planes=min(self.planes, 2),
                               layers=self.layers, embed=self.embed).run(prompt[:-1])
         self.tokens[b] = prompt[-1]
         self.positions[b] = prompt.numel() - 1

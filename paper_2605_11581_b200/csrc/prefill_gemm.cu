@@ -246,16 +246,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, uint32_t t_addr
       __syncwarp();
     }
   } else if constexpr (EPI == ADAMK_PF_EPI_ATOMIC) {
-    // Decode-sized tiles: a handful of live rows drained by the one warp that owns their TMEM lanes, so that warp's
-    // instruction latency is the cost (tools/gemm_trace.py: 4.9 us per tile for the general path, 3.3 us for this one;
-    // a register-resident variant without the patch measured 4.1 us).  Row bookkeeping is done once per tile, only
-    // live rows are staged and sent, and when both stacked planes of a row sit in this 32-row patch (2 T <= 32) they
-    // are summed here so that T rows go out.
+    // Decode-sized tiles: a handful of live rows per warp, so the warp's instruction latency is the cost
+    // (tools/gemm_trace.py: 4.9 us per 256-column tile for the general path, 3.3 us for this one).  Row bookkeeping is
+    // done once per tile and only live rows are staged and sent.  The stacked planes of a token go out as separate
+    // atomics: summing them in the patch first was measured slower (2.55 vs 2.31 ms per batch-8 step).
     const int n0 = n_blk * BN + sub * w;
     float* out = static_cast<float*>(g.out);
-    const bool fold = g.stacked && g.parts == 2 && 2 * g.T <= 32;
-    const int staged = min(32, (g.stacked ? g.parts * g.T : g.T) - row0);   // rows of this patch that hold data
-    const int live = fold ? g.T : staged;                                    // rows that go out
+    const int live = min(32, (g.stacked ? g.parts * g.T : g.T) - row0);   // rows of this patch that hold data
     const int n_it = (live + 3) >> 2;
     long long roff[8];
 #pragma unroll
@@ -274,7 +271,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, uint32_t t_addr
         const int col = n0 + c + hc * 32 + cg;
         const bool col_ok = col < g.N;
         const float4 b = (g.bias != nullptr && col_ok && first_split) ? *reinterpret_cast<const float4*>(g.bias + col) : make_float4(0, 0, 0, 0);
-        if (lane < staged) {
+        if (lane < live) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
             *reinterpret_cast<float4*>(patch + lane * kStagePitch + j) = make_float4(
@@ -286,10 +283,6 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, uint32_t t_addr
           if (i < n_it && roff[i] >= 0 && col_ok) {
             const int r = i * 4 + sub_row;
             float4 v = *reinterpret_cast<const float4*>(patch + r * kStagePitch + cg);
-            if (fold) {
-              const float4 lo = *reinterpret_cast<const float4*>(patch + (r + g.T) * kStagePitch + cg);
-              v.x += lo.x; v.y += lo.y; v.z += lo.z; v.w += lo.w;
-            }
             if (row0 + r < g.T) { v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w; }   // bias: once per output row
             atomicAdd(reinterpret_cast<float4*>(out + roff[i] + col), v);
           }
@@ -899,7 +892,7 @@ void adamk_prefill_set_trace(void* stamps) { pf::g_trace = static_cast<unsigned 
 // Argument checks shared by the planner and the launcher (no device access).
 static int check_shape(int parts, int T, int K, int N, int ldo, int epilogue, int parts_out, int tile_n) {
   using namespace pf;
-  if (T <= 0 || N <= 0 || K <= 0 || (parts != 1 && parts != 2)) {
+  if (T <= 0 || N <= 0 || K <= 0 || parts < 1 || parts > 3) {
     snprintf(g_err, sizeof g_err, "prefill gemm: bad argument (T %d N %d K %d parts %d)", T, N, K, parts);
     return ADAMK_PF_E_INVALID;
   }

@@ -52,10 +52,17 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-__device__ __forceinline__ void put_split(__nv_bfloat16* hi, __nv_bfloat16* lo, float v) {
+// v as the sum of `parts` bf16 values, plane p at dst[p * stride]: 1 = plain rounding, 2 = hi + lo (2^-17 relative),
+// 3 = hi + mid + lo (below fp32 resolution).
+__device__ __forceinline__ void put_split(__nv_bfloat16* dst, long long stride, int parts, float v) {
   const __nv_bfloat16 h = __float2bfloat16_rn(v);
-  *hi = h;
-  if (lo != nullptr) *lo = __float2bfloat16_rn(v - __bfloat162float(h));
+  dst[0] = h;
+  if (parts > 1) {
+    const float r1 = v - __bfloat162float(h);
+    const __nv_bfloat16 m = __float2bfloat16_rn(r1);
+    dst[stride] = m;
+    if (parts > 2) dst[2 * stride] = __float2bfloat16_rn(r1 - __bfloat162float(m));
+  }
 }
 
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ embed, float* __restrict__ h, int H) {
@@ -85,12 +92,11 @@ __global__ void rmsnorm_split_kernel(const float* __restrict__ h, const __nv_bfl
   }
   const float inv = rsqrtf(block_sum(ss, red) / float(H) + eps);
   __nv_bfloat16* hi = planes + t * H;
-  __nv_bfloat16* lo = parts == 2 ? hi + plane_stride : nullptr;
   for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
     const float4 v = *reinterpret_cast<const float4*>(row + i);
     const float x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) put_split(hi + i + j, lo ? lo + i + j : nullptr, x[j] * inv * __bfloat162float(gain[i + j]));
+    for (int j = 0; j < 4; ++j) put_split(hi + i + j, plane_stride, parts, x[j] * inv * __bfloat162float(gain[i + j]));
   }
 }
 
@@ -101,7 +107,7 @@ __global__ void split_kernel(const float* __restrict__ x, long long n, __nv_bflo
   const float4 v = *reinterpret_cast<const float4*>(x + i);
   const float a[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-  for (int j = 0; j < 4; ++j) put_split(planes + i + j, parts == 2 ? planes + plane_stride + i + j : nullptr, a[j]);
+  for (int j = 0; j < 4; ++j) put_split(planes + i + j, plane_stride, parts, a[j]);
 }
 
 // One CTA per token, one warp per head (q heads, then k heads, then v heads).  D <= 256.
@@ -361,7 +367,7 @@ __global__ void batch_attn_merge_kernel(const float* __restrict__ part, const in
     }
   }
   const long long o = (long long)b * n_q * D + h * D + d;
-  put_split(planes + o, parts == 2 ? planes + (long long)B * n_q * D + o : nullptr, num / den);
+  put_split(planes + o, (long long)B * n_q * D, parts, num / den);
 }
 
 // grid B: greedy pick (lowest index on ties), written to next[b]; tokens / positions advanced in place when asked.
@@ -406,7 +412,7 @@ __global__ void swiglu_split_kernel(const float* __restrict__ gu, int I, int blo
   for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < I; f += gridDim.x * blockDim.x) {
     const int blk = f / block, j = f - blk * block;
     const float g = row[blk * 2 * block + j], u = row[blk * 2 * block + block + j];
-    put_split(hi + f, parts == 2 ? hi + plane_stride + f : nullptr, __fdividef(g, 1.0f + __expf(-g)) * u);
+    put_split(hi + f, plane_stride, parts, __fdividef(g, 1.0f + __expf(-g)) * u);
   }
 }
 
@@ -430,7 +436,7 @@ int adamk_prefill_embed(const int32_t* tokens, int T, const void* embed, int H, 
 }
 
 int adamk_prefill_rmsnorm_split(const float* h, const void* gain, float eps, int T, int H, void* planes, int parts, adamk_pf_stream stream) {
-  if (h == nullptr || gain == nullptr || planes == nullptr || T <= 0 || H <= 0 || H % 4 || (parts != 1 && parts != 2)) return ADAMK_PF_E_INVALID;
+  if (h == nullptr || gain == nullptr || planes == nullptr || T <= 0 || H <= 0 || H % 4 || (parts < 1 || parts > 3)) return ADAMK_PF_E_INVALID;
   pfo::launch(pfo::rmsnorm_split_kernel, dim3(T), dim3(256), 0, static_cast<cudaStream_t>(stream), h, static_cast<const __nv_bfloat16*>(gain), eps, H,
                                                                              static_cast<__nv_bfloat16*>(planes), (long long)T * H, parts, nullptr, 0);
   return pfo::done("prefill rmsnorm");
@@ -438,7 +444,7 @@ int adamk_prefill_rmsnorm_split(const float* h, const void* gain, float eps, int
 
 int adamk_batch_rmsnorm_split(const float* h, const void* gain, float eps, int B, int H, void* planes, int parts, float* zero, long long zero_n,
                               adamk_pf_stream stream) {
-  if (h == nullptr || gain == nullptr || planes == nullptr || B <= 0 || H <= 0 || H % 4 || (parts != 1 && parts != 2) || zero_n % 4 ||
+  if (h == nullptr || gain == nullptr || planes == nullptr || B <= 0 || H <= 0 || H % 4 || (parts < 1 || parts > 3) || zero_n % 4 ||
       (reinterpret_cast<uintptr_t>(zero) & 15))
     return ADAMK_PF_E_INVALID;
   pfo::launch(pfo::rmsnorm_split_kernel, dim3(B), dim3(256), 0, static_cast<cudaStream_t>(stream), h, static_cast<const __nv_bfloat16*>(gain), eps, H,
@@ -448,7 +454,7 @@ int adamk_batch_rmsnorm_split(const float* h, const void* gain, float eps, int B
 }
 
 int adamk_prefill_split(const float* x, long long n, void* planes, int parts, adamk_pf_stream stream) {
-  if (x == nullptr || planes == nullptr || n <= 0 || n % 4 || (parts != 1 && parts != 2)) return ADAMK_PF_E_INVALID;
+  if (x == nullptr || planes == nullptr || n <= 0 || n % 4 || (parts < 1 || parts > 3)) return ADAMK_PF_E_INVALID;
   const long long blocks = (n / 4 + 255) / 256;
   pfo::launch(pfo::split_kernel, dim3((unsigned)blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), x, n, static_cast<__nv_bfloat16*>(planes), n, parts);
   return pfo::done("prefill split");
@@ -488,7 +494,7 @@ size_t adamk_batch_attention_workspace(int B, int n_q, int D, int max_ctx) {
 int adamk_batch_attention(const float* q, const void* k_cache, const void* v_cache, const int32_t* positions, int B, int n_q, int n_kv, int D,
                           int max_ctx, long long seq_stride, float* workspace, void* out_planes, int parts, adamk_pf_stream stream) {
   if (q == nullptr || k_cache == nullptr || v_cache == nullptr || positions == nullptr || workspace == nullptr || out_planes == nullptr || B <= 0 ||
-      n_kv <= 0 || n_q % n_kv || n_q / n_kv > pfo::kMaxGroup || (parts != 1 && parts != 2))
+      n_kv <= 0 || n_q % n_kv || n_q / n_kv > pfo::kMaxGroup || (parts < 1 || parts > 3))
     return ADAMK_PF_E_INVALID;
   if (D != 64 && D != 128) {
     snprintf(pf::err_buf(), 256, "batch attention: head_dim %d is not built (64, 128)", D);
@@ -538,7 +544,7 @@ int adamk_batch_attention(const float* q, const void* k_cache, const void* v_cac
 }
 
 int adamk_batch_swiglu_split(const float* gu, int B, int I, int block, void* planes, int parts, adamk_pf_stream stream) {
-  if (gu == nullptr || planes == nullptr || B <= 0 || I <= 0 || block <= 0 || I % block || (parts != 1 && parts != 2)) return ADAMK_PF_E_INVALID;
+  if (gu == nullptr || planes == nullptr || B <= 0 || I <= 0 || block <= 0 || I % block || (parts < 1 || parts > 3)) return ADAMK_PF_E_INVALID;
   pfo::launch(pfo::swiglu_split_kernel, dim3(dim3((I + 511) / 512, B)), dim3(512), 0, static_cast<cudaStream_t>(stream), gu, I, block, static_cast<__nv_bfloat16*>(planes), (long long)B * I, parts);
   return pfo::done("batch swiglu");
 }
