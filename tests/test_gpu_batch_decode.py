@@ -26,14 +26,16 @@ D128 = ModelConfig(name="test-d128", hidden=512, n_layers=2, n_q_heads=4, n_kv_h
 
 
 def _planes(x, parts):
-    hi = x.to(torch.bfloat16)
-    if parts == 1:
-        return hi[None].contiguous()
-    return torch.stack((hi, (x - hi.float()).to(torch.bfloat16))).contiguous()
+    out, rest = [], x
+    for _ in range(parts):
+        out.append(rest.to(torch.bfloat16))
+        rest = rest - out[-1].float()
+    return torch.stack(out).contiguous()
 
 
 @pytest.mark.parametrize("T,K,N,parts", [(1, 1536, 2048, 2), (8, 1536, 2048, 2), (8, 8960, 1536, 2), (64, 3584, 4608, 2),
-                                         (64, 512, 328, 1), (100, 1536, 1536, 2), (128, 1536, 17920, 2), (33, 64, 8, 1)])
+                                         (64, 512, 328, 1), (100, 1536, 1536, 2), (128, 1536, 17920, 2), (33, 64, 8, 1),
+                                         (8, 1536, 2048, 3), (42, 8960, 1536, 3), (50, 512, 1024, 3)])
 def test_gemm_atomic_split_k(T, K, N, parts):
     """Decode-sized GEMM: K split across SMs, fp32-atomic epilogue, both planes stacked in one token tile when they fit
     (parts * T <= 128), bias added exactly once."""
@@ -50,6 +52,9 @@ def test_gemm_atomic_split_k(T, K, N, parts):
     P.gemm(xp, w, out, bias=bias, epilogue=P.EPI_ATOMIC)
     err = (out.double() - want).abs().max().item()
     assert err <= 4e-5 * max(1.0, want.abs().max().item()), err
+    if parts == 3:    # three planes carry the fp32 activation exactly: as close to the exact product as an fp32 GEMM
+        exact = base.double() + x.double() @ w.double().T + bias.double()
+        assert (out.double() - exact).abs().max().item() <= 8e-6 * max(1.0, exact.abs().max().item())
 
 
 def test_row_operators():

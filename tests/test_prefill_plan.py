@@ -37,6 +37,7 @@ def test_decode_shapes_split_k_and_stack_planes():
     # LM head: more tiles than SMs -> no K split; batch 128 x 2 planes does not fit one tile -> two passes over K
     assert P.gemm_plan(2, 8, 1536, 151936, P.EPI_ATOMIC)["ksplit"] == 1
     assert P.gemm_plan(2, 128, 1536, 2048, P.EPI_ATOMIC)["stacked"] == 0 and P.gemm_plan(2, 64, 1536, 2048, P.EPI_ATOMIC)["stacked"] == 1
+    assert P.gemm_plan(3, 42, 1536, 2048, P.EPI_ATOMIC)["stacked"] == 1 and P.gemm_plan(3, 43, 1536, 2048, P.EPI_ATOMIC)["stacked"] == 0
     # every split count the planner can produce covers K exactly
     for K in (64, 192, 1536, 3584, 8960, 18944):
         for N in (256, 1536, 4608):
@@ -47,7 +48,7 @@ def test_decode_shapes_split_k_and_stack_planes():
 
 
 def test_plan_rejects_what_the_launcher_rejects():
-    for args in ((1, 16, 60, 64, P.EPI_STORE, 0), (3, 16, 64, 64, P.EPI_STORE, 0), (1, 16, 64, 64, 7, 0), (1, 16, 64, 64, P.EPI_STORE, 192),
+    for args in ((1, 16, 60, 64, P.EPI_STORE, 0), (4, 16, 64, 64, P.EPI_STORE, 0), (1, 16, 64, 64, 7, 0), (1, 16, 64, 64, P.EPI_STORE, 192),
                  (1, 16, 64, 2048, P.EPI_ATOMIC, P.TILE_PAIR), (1, 16, 64, 200, P.EPI_SWIGLU, P.TILE_256)):
         with pytest.raises(AdamkError):
             P.gemm_plan(*args)
