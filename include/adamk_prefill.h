@@ -104,7 +104,7 @@ int adamk_batch_rope_store(const float* qkv, int B, int n_q, int n_kv, int D, co
                            const float* cos, const float* sin, const int32_t* positions, long long seq_stride, int max_ctx, float* q_out,
                            void* k_cache, void* v_cache, adamk_pf_stream stream);
 
-/* Attention of every sequence's new token over cache rows 0 .. positions[b] (split over 256-row chunks, merged),
+/* Attention of every sequence's new token over cache rows 0 .. positions[b] (split over 64-row chunks, merged),
  * output as bf16 planes [parts][B][n_q * D].  workspace: adamk_batch_attention_workspace() bytes. */
 size_t adamk_batch_attention_workspace(int B, int n_q, int D, int max_ctx);
 int adamk_batch_attention(const float* q, const void* k_cache, const void* v_cache, const int32_t* positions, int B, int n_q, int n_kv, int D,

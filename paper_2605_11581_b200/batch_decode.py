@@ -12,7 +12,7 @@ runs one decode step of ``B`` sequences with the operators of ``include/adamk_pr
 * activations enter the tensor cores as bf16 planes whose sum is the fp32 value -- three (hi + mid + lo, exact to
   fp32) while 3 B <= 128 rows still fit the one token tile, two (2^-17) beyond -- so the step keeps the MegaKernel's
   numerical contract (fp32 activations against exact bf16 weights) at no cost in time.
-* ``adamk_batch_rope_store`` (per-sequence positions), ``adamk_batch_attention`` (split over 256-row chunks of
+* ``adamk_batch_rope_store`` (per-sequence positions), ``adamk_batch_attention`` (split over 64-row chunks of
   each sequence's cache + merge) and ``adamk_batch_argmax`` (greedy pick, tokens / positions advanced on the device).
 
 A step is 10 launches per layer; ``capture()`` records it once into a CUDA graph, after which a step is one graph
