@@ -9,17 +9,23 @@
 // accumulator in tensor memory, so the result matches the decode kernel's fp32 FMA chain to ~1e-6 relative
 // at twice the tensor work, or runs at bf16 cost when parts = 1.
 //
-// Kernel anatomy (one persistent CTA per SM, 192 threads, no cluster):
-//   warp 0      TMA producer: cp.async.bulk.tensor 2-D tiles (128 x 64 of X, BN x 64 of W, 128-byte swizzle)
+// Kernel anatomy (persistent, 192 threads per CTA):
+//   warp 0      TMA producer: cp.async.bulk.tensor 2-D tiles (128 x 64 of X, 64-row boxes of W, 128-byte swizzle)
 //               into an n-stage shared-memory ring, full/empty mbarriers.
-//   warp 1      allocates tensor memory; one elected lane issues tcgen05.mma.cta_group::1.kind::f16
-//               (M 128 x N BN x K 16, A and B from shared memory through matrix descriptors, D in TMEM),
-//               tcgen05.commit releases ring slots and publishes finished accumulators.
-//   warps 2-5   epilogue: tcgen05.ld 32 lanes x 32 columns at a time, fused store / residual add / SwiGLU +
-//               bf16-plane split, straight to global memory.  Two accumulators (2 x BN TMEM columns) let the
-//               tensor pipe start tile i+1 while tile i drains.
-// Tiles are walked token-block fastest, so the CTAs running at any moment share a few weight tiles out of L2
-// and every weight byte leaves HBM once.
+//   warp 1      allocates tensor memory; one elected lane issues tcgen05.mma.kind::f16 (A and B from shared memory
+//               through matrix descriptors, D in TMEM), tcgen05.commit releases ring slots and publishes finished
+//               accumulators.
+//   warps 2-5   epilogue: tcgen05.ld 32 lanes x 32 columns at a time through a padded shared-memory patch (4 rows x 128
+//               contiguous bytes per global instruction), fused store+bias / residual add / SwiGLU + bf16-plane split /
+//               fp32 atomics.  Two accumulators (2 x 256 TMEM columns) let the tensor pipe start tile i+1 while tile i
+//               drains.
+// Two kernels share these roles: gemm_kernel<BN, EPI> -- one CTA per 128 x BN tile (4 stages x 48 KB at BN 256) -- and
+// gemm_pair_kernel<EPI> -- a cluster of two CTAs per 256 x 256 tile with tcgen05.mma.cta_group::2, each SM staging its
+// own 128 token rows and half of the weight tile (6 stages x 32 KB).  plan_gemm() (host, exported as
+// adamk_prefill_gemm_plan) picks the shape and cuts the problem into work items: whole tiles walked token-block fastest
+// (the CTAs running at any moment share a few weight tiles out of L2 and every weight byte leaves HBM once), the tiles
+// of a last partial wave as 64/128-column slices, and -- for decode-sized T with the atomic epilogue -- K ranges
+// spread over the idle SMs with all activation planes stacked in the one token tile.
 
 #include <cuda.h>
 #include <cuda_bf16.h>
