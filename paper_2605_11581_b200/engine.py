@@ -8,13 +8,13 @@ runs a prefill backend to fill the KV cache the plugin owns, then enqueues one
 persistent-kernel launch per generated token with the token / position state
 resident on the device (no host round trip inside the decode loop).
 
-Prefill backends.  ``"decode"`` (the default) feeds the prompt through the decode kernel itself, one launch
-per prompt token -- correct, and ~0.9 ms per token, but not compute-efficient for long prompts.
+Prefill backends.  ``"decode"`` feeds the prompt through the decode kernel itself, one launch per prompt token --
+bit-for-bit the decode path's cache, ~0.9 ms per token, not compute-efficient for long prompts.
 ``"library"`` is the paper's own arrangement (``PAPER.md:248``: Prefill stays on the serving engine's native
 operators): library GEMMs (cuBLAS through ``torch.matmul``) and library attention fill the KV cache the plugin
 owns, token-parallel; it is the BASELINE the hand-written tensor-core (tcgen05) prefill GEMM / attention kernels
 of SURVEY.md section 8(f) row 2 have to beat, not a product kernel, and it is never used unless asked for.
-``"tensor"`` is the hand-written replacement of that library path (``prefill.py``): a tcgen05 / tensor-memory GEMM
+``"tensor"`` (the default) is the hand-written replacement of that library path (``prefill.py``): a tcgen05 / tensor-memory GEMM
 with fused bias / residual / SwiGLU epilogues and the row kernels around it; ``prefill_planes`` = 2 feeds each fp32
 activation to the tensor cores as hi + lo bf16 planes (the decode kernel's numerical contract), 1 is plain bf16.
 Every backend ends with the device state at the last prompt token, so the first generated token already comes
@@ -45,7 +45,7 @@ class HybridEngine:
     """Prefill -> decode switch around one ``MegaKernelPlugin``."""
 
     def __init__(self, cfg: ModelConfig, weights: DecoderWeights, max_ctx: int, schedule: KernelSchedule | None = None,
-                 device: int = 0, prefill_backend: str = "decode", prefill_dtype: torch.dtype = torch.float32,
+                 device: int = 0, prefill_backend: str = "tensor", prefill_dtype: torch.dtype = torch.float32,
                  prefill_planes: int = 2, prefill_attention: str | None = None):
         if prefill_backend not in ("decode", "library", "tensor"):
             raise NotImplementedError(f"prefill backend {prefill_backend!r} does not exist")

@@ -194,7 +194,7 @@ def test_hybrid_engine_generate_matches_oracle():
     g = torch.Generator().manual_seed(7)
     prompt = torch.randint(0, cfg.vocab, (24,), generator=g).tolist()
     want, logits = ref.generate(prompt, 24, stepwise_prefill=True)
-    eng = HybridEngine(cfg, w, max_ctx=128, schedule=SCHEDS["c8"])
+    eng = HybridEngine(cfg, w, max_ctx=128, schedule=SCHEDS["c8"], prefill_backend="decode")
     res = eng.generate(prompt, 24)
     srt = torch.stack(logits).sort(dim=1).values
     margin = (srt[:, -1] - srt[:, -2]).numpy()
