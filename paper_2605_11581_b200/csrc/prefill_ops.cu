@@ -65,6 +65,22 @@ __device__ __forceinline__ void put_split(__nv_bfloat16* dst, long long stride, 
   }
 }
 
+// Four consecutive values at once: one 8-byte store per plane.
+__device__ __forceinline__ void put_split4(__nv_bfloat16* dst, long long stride, int parts, const float (&v)[4]) {
+  float r[4] = {v[0], v[1], v[2], v[3]};
+  for (int p = 0; p < parts; ++p) {
+    __nv_bfloat16 b[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      b[j] = __float2bfloat16_rn(r[j]);
+      r[j] -= __bfloat162float(b[j]);
+    }
+    const uint32_t lo = uint32_t(__bfloat16_as_ushort(b[0])) | (uint32_t(__bfloat16_as_ushort(b[1])) << 16);
+    const uint32_t hi = uint32_t(__bfloat16_as_ushort(b[2])) | (uint32_t(__bfloat16_as_ushort(b[3])) << 16);
+    *reinterpret_cast<uint2*>(dst + p * stride) = make_uint2(lo, hi);
+  }
+}
+
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ embed, float* __restrict__ h, int H) {
   griddep_sync();
   const int t = blockIdx.x;
@@ -94,9 +110,10 @@ __global__ void rmsnorm_split_kernel(const float* __restrict__ h, const __nv_bfl
   __nv_bfloat16* hi = planes + t * H;
   for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
     const float4 v = *reinterpret_cast<const float4*>(row + i);
-    const float x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) put_split(hi + i + j, plane_stride, parts, x[j] * inv * __bfloat162float(gain[i + j]));
+    const uint2 graw = *reinterpret_cast<const uint2*>(gain + i);
+    const float x[4] = {v.x * inv * __uint_as_float(graw.x << 16), v.y * inv * __uint_as_float(graw.x & 0xffff0000u),
+                        v.z * inv * __uint_as_float(graw.y << 16), v.w * inv * __uint_as_float(graw.y & 0xffff0000u)};
+    put_split4(hi + i, plane_stride, parts, x);
   }
 }
 
@@ -106,8 +123,7 @@ __global__ void split_kernel(const float* __restrict__ x, long long n, __nv_bflo
   if (i >= n) return;
   const float4 v = *reinterpret_cast<const float4*>(x + i);
   const float a[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) put_split(planes + i + j, plane_stride, parts, a[j]);
+  put_split4(planes + i, plane_stride, parts, a);
 }
 
 // One CTA per token, one warp per head (q heads, then k heads, then v heads).  D <= 256.
