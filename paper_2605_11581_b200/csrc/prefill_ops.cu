@@ -225,7 +225,8 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
   if (p0 >= ctx) return;              // the merge kernel derives the live split count from positions, too
   const int n_pos = min(kAttnChunk, ctx - p0);
   constexpr int NW = kAttnThreads / 32;
-  __shared__ __align__(16) float q_s[G][D];
+  __shared__ __align__(16) float q_s[G][D + 4];   // second half of a row shifted by 16 bytes: the two threads of a position
+                                                  // read different banks (ncu: a third of all shared wavefronts were conflicts)
   __shared__ float sc[G][kAttnChunk];
   __shared__ float ml[G][2];
   __shared__ __align__(16) float ored[NW][G][D];
@@ -235,7 +236,7 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
 
   // scores: TPP threads per position, 1/TPP of a K row each (all of its 16-byte loads in flight)
   constexpr int TPP = kAttnThreads / kAttnChunk, HC = D / 8 / TPP;
-  static_assert(TPP == 2 || TPP == 4, "threads per position");
+  static_assert(TPP == 2, "threads per position (the q layout in shared memory assumes two)");
   const int p = tid / TPP, half = tid % TPP;
   uint4 kraw[HC];
   if (p < n_pos) {
@@ -248,7 +249,7 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
   }
   for (int i = tid; i < G * D; i += kAttnThreads) {
     const int g = i / D, d = i - g * D;
-    q_s[g][d] = q[((long long)(kvh * G + g) * B + b) * D + d] * scale;
+    q_s[g][d + (d >= D / 2 ? 4 : 0)] = q[((long long)(kvh * G + g) * B + b) * D + d] * scale;
   }
   __syncthreads();
   {
@@ -259,7 +260,7 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
     for (int c = 0; c < HC; ++c) {
       float kf[8];
       bf16x8_to_float(kraw[c], kf);
-      const int d0 = (half * HC + c) * 8;
+      const int d0 = (half * HC + c) * 8 + half * 4;   // + the bank shift of the second half
 #pragma unroll
       for (int g = 0; g < G; ++g) {   // q as two 16-byte broadcast reads per 8 products
         const float4 qa = *reinterpret_cast<const float4*>(&q_s[g][d0]), qb = *reinterpret_cast<const float4*>(&q_s[g][d0 + 4]);
@@ -273,7 +274,6 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
     for (int g = 0; g < G; ++g) {
       float t = acc[g].x + acc[g].y;
       t += __shfl_xor_sync(0xffffffffu, t, 1);
-      if constexpr (TPP == 4) t += __shfl_xor_sync(0xffffffffu, t, 2);
       if (half == 0) sc[g][p] = (p < n_pos) ? t : -INFINITY;
     }
   }
