@@ -225,8 +225,9 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
   if (p0 >= ctx) return;              // the merge kernel derives the live split count from positions, too
   const int n_pos = min(kAttnChunk, ctx - p0);
   constexpr int NW = kAttnThreads / 32;
-  __shared__ __align__(16) float q_s[G][D + 4];   // second half of a row shifted by 16 bytes: the two threads of a position
-                                                  // read different banks (ncu: a third of all shared wavefronts were conflicts)
+  __shared__ __align__(16) float q_s[G][D + 12];   // each quarter of a row shifted by 16 more bytes: the four threads of a
+                                                   // position pair read different banks (ncu: a third of all shared wavefronts
+                                                   // were conflicts without the shift)
   __shared__ float sc[G][kAttnChunk];
   __shared__ float ml[G][2];
   __shared__ __align__(16) float ored[NW][G][D];
@@ -234,48 +235,63 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
   const __nv_bfloat16* kb = k_cache + b * seq_stride + ((long long)kvh * max_ctx + p0) * D;
   const __nv_bfloat16* vb = v_cache + b * seq_stride + ((long long)kvh * max_ctx + p0) * D;
 
-  // scores: TPP threads per position, 1/TPP of a K row each (all of its 16-byte loads in flight)
-  constexpr int TPP = kAttnThreads / kAttnChunk, HC = D / 8 / TPP;
-  static_assert(TPP == 2, "threads per position (the q layout in shared memory assumes two)");
-  const int p = tid / TPP, half = tid % TPP;
-  uint4 kraw[HC];
-  if (p < n_pos) {
-    const uint4* row = reinterpret_cast<const uint4*>(kb + (long long)p * D) + half * HC;
+  // scores: four threads share two positions -- a quarter of each K row per thread, so that every 16-byte q read from
+  // shared memory feeds the products of two positions (all global loads in flight before the first use)
+  constexpr int QC = D / 32;                 // 16-byte pieces of a quarter row
+  const int pi = tid >> 2, qd = tid & 3;     // position pair, quarter
+  uint4 kraw[2][QC];
 #pragma unroll
-    for (int c = 0; c < HC; ++c) kraw[c] = row[c];
-  } else {
+  for (int r = 0; r < 2; ++r) {
+    const int pp = 2 * pi + r;
+    if (pp < n_pos) {
+      const uint4* row = reinterpret_cast<const uint4*>(kb + (long long)pp * D) + qd * QC;
 #pragma unroll
-    for (int c = 0; c < HC; ++c) kraw[c] = make_uint4(0, 0, 0, 0);
+      for (int c = 0; c < QC; ++c) kraw[r][c] = row[c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < QC; ++c) kraw[r][c] = make_uint4(0, 0, 0, 0);
+    }
   }
   for (int i = tid; i < G * D; i += kAttnThreads) {
     const int g = i / D, d = i - g * D;
-    q_s[g][d + (d >= D / 2 ? 4 : 0)] = q[((long long)(kvh * G + g) * B + b) * D + d] * scale;
+    q_s[g][d + (d / (D / 4)) * 4] = q[((long long)(kvh * G + g) * B + b) * D + d] * scale;   // quarter q at a 16-byte bank shift
   }
   __syncthreads();
   {
-    float2 acc[G];   // even / odd feature sums, packed fp32 FMAs (FFMA2): half the issue slots of scalar FMAs
+    float2 acc[2][G];   // even / odd feature sums, packed fp32 FMAs (FFMA2): half the issue slots of scalar FMAs
 #pragma unroll
-    for (int g = 0; g < G; ++g) acc[g] = make_float2(0.f, 0.f);
+    for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int c = 0; c < HC; ++c) {
-      float kf[8];
-      bf16x8_to_float(kraw[c], kf);
-      const int d0 = (half * HC + c) * 8 + half * 4;   // + the bank shift of the second half
+      for (int g = 0; g < G; ++g) acc[r][g] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int g = 0; g < G; ++g) {   // q as two 16-byte broadcast reads per 8 products
+    for (int c = 0; c < QC; ++c) {
+      float k0[8], k1[8];
+      bf16x8_to_float(kraw[0][c], k0);
+      bf16x8_to_float(kraw[1][c], k1);
+      const int d0 = qd * (D / 4) + c * 8 + qd * 4;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
         const float4 qa = *reinterpret_cast<const float4*>(&q_s[g][d0]), qb = *reinterpret_cast<const float4*>(&q_s[g][d0 + 4]);
-        acc[g] = __ffma2_rn(make_float2(qa.x, qa.y), make_float2(kf[0], kf[1]), acc[g]);
-        acc[g] = __ffma2_rn(make_float2(qa.z, qa.w), make_float2(kf[2], kf[3]), acc[g]);
-        acc[g] = __ffma2_rn(make_float2(qb.x, qb.y), make_float2(kf[4], kf[5]), acc[g]);
-        acc[g] = __ffma2_rn(make_float2(qb.z, qb.w), make_float2(kf[6], kf[7]), acc[g]);
+        const float2 q01 = make_float2(qa.x, qa.y), q23 = make_float2(qa.z, qa.w), q45 = make_float2(qb.x, qb.y), q67 = make_float2(qb.z, qb.w);
+        acc[0][g] = __ffma2_rn(q01, make_float2(k0[0], k0[1]), acc[0][g]);
+        acc[0][g] = __ffma2_rn(q23, make_float2(k0[2], k0[3]), acc[0][g]);
+        acc[0][g] = __ffma2_rn(q45, make_float2(k0[4], k0[5]), acc[0][g]);
+        acc[0][g] = __ffma2_rn(q67, make_float2(k0[6], k0[7]), acc[0][g]);
+        acc[1][g] = __ffma2_rn(q01, make_float2(k1[0], k1[1]), acc[1][g]);
+        acc[1][g] = __ffma2_rn(q23, make_float2(k1[2], k1[3]), acc[1][g]);
+        acc[1][g] = __ffma2_rn(q45, make_float2(k1[4], k1[5]), acc[1][g]);
+        acc[1][g] = __ffma2_rn(q67, make_float2(k1[6], k1[7]), acc[1][g]);
       }
     }
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float t = acc[g].x + acc[g].y;
-      t += __shfl_xor_sync(0xffffffffu, t, 1);
-      if (half == 0) sc[g][p] = (p < n_pos) ? t : -INFINITY;
-    }
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float t = acc[r][g].x + acc[r][g].y;
+        t += __shfl_xor_sync(0xffffffffu, t, 1);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);
+        if (qd == 0) sc[g][2 * pi + r] = (2 * pi + r < n_pos) ? t : -INFINITY;
+      }
   }
   // values: warp w owns positions w, w + 4, ...; issue all of its (coalesced) V rows now, use them after the softmax
   constexpr int E = D / 32, NV = kAttnChunk / NW;
