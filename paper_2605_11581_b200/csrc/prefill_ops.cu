@@ -210,6 +210,10 @@ __device__ __forceinline__ void bf16x8_to_float(const uint4 u, float (&f)[8]) {
   }
 }
 
+// Scores in shared memory are stored per consuming warp: position p belongs to warp p % 4 in the value phase, which
+// reads its 16 positions as four 16-byte words.
+__device__ __forceinline__ int sc_slot(int p) { return (p & 3) * (kAttnChunk / 4) + (p >> 2); }
+
 // grid (splits, n_kv, B).  Partial softmax of the G q heads of one kv head over positions [s * 64, s * 64 + 64) of
 // sequence b:  part[b][q head][s][0..D) = sum_p exp(score_p - m) v_p,  [D] = m,  [D + 1] = sum_p exp(score_p - m).
 // Every global load of a phase is issued before the first use (the kernel is latency-, not bandwidth-limited).
@@ -228,7 +232,7 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
   __shared__ __align__(16) float q_s[G][D + 12];   // each quarter of a row shifted by 16 more bytes: the four threads of a
                                                    // position pair read different banks (ncu: a third of all shared wavefronts
                                                    // were conflicts without the shift)
-  __shared__ float sc[G][kAttnChunk];
+  __shared__ __align__(16) float sc[G][kAttnChunk];   // position p at sc_slot(p): a warp's positions are contiguous
   __shared__ float ml[G][2];
   __shared__ __align__(16) float ored[NW][G][D];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -290,7 +294,7 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
         float t = acc[r][g].x + acc[r][g].y;
         t += __shfl_xor_sync(0xffffffffu, t, 1);
         t += __shfl_xor_sync(0xffffffffu, t, 2);
-        if (qd == 0) sc[g][2 * pi + r] = (2 * pi + r < n_pos) ? t : -INFINITY;
+        if (qd == 0) sc[g][sc_slot(2 * pi + r)] = (2 * pi + r < n_pos) ? t : -INFINITY;
       }
   }
   // values: warp w owns positions w, w + 4, ...; issue all of its (coalesced) V rows now, use them after the softmax
@@ -315,13 +319,13 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
   __syncthreads();
   // chunk softmax: warp w handles heads w, w + 4; a lane covers positions lane and lane + 32
   for (int g = warp; g < G; g += NW) {
-    const float s0 = sc[g][lane], s1 = sc[g][lane + 32];
+    const float s0 = sc[g][sc_slot(lane)], s1 = sc[g][sc_slot(lane + 32)];
     float m = fmaxf(s0, s1);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     const float e0 = __expf(s0 - m), e1 = __expf(s1 - m);   // exp(-inf) = 0 for the positions past the end
-    sc[g][lane] = e0;
-    sc[g][lane + 32] = e1;
+    sc[g][sc_slot(lane)] = e0;
+    sc[g][sc_slot(lane + 32)] = e1;
     float l = e0 + e1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
@@ -335,16 +339,21 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
 #pragma unroll
       for (int e = 0; e < E / 2; ++e) o[g][e] = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int u = 0; u < NV; ++u) {
-      const int pp = warp + u * NW;
-      float2 vf[E / 2];
+    for (int u4 = 0; u4 < NV; u4 += 4) {
+      float2 vf[4][E / 2];
 #pragma unroll
-      for (int e = 0; e < E / 2; ++e) vf[e] = make_float2(__uint_as_float(vraw[u][e] << 16), __uint_as_float(vraw[u][e] & 0xffff0000u));
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int e = 0; e < E / 2; ++e)
+          vf[k][e] = make_float2(__uint_as_float(vraw[u4 + k][e] << 16), __uint_as_float(vraw[u4 + k][e] & 0xffff0000u));
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const float w = sc[g][pp];
+        const float4 w4 = *reinterpret_cast<const float4*>(&sc[g][warp * NV + u4]);   // this warp's four next positions
+        const float w[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-        for (int e = 0; e < E / 2; ++e) o[g][e] = __ffma2_rn(make_float2(w, w), vf[e], o[g][e]);
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int e = 0; e < E / 2; ++e) o[g][e] = __ffma2_rn(make_float2(w[k], w[k]), vf[k][e], o[g][e]);
       }
     }
 #pragma unroll
