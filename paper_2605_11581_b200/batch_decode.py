@@ -54,6 +54,8 @@ class BatchedDecoder:
             planes = 3 if 3 * batch <= 128 else 2
         if planes not in (1, 2, 3):
             raise ValueError("planes must be 1, 2 or 3")
+        if cfg.vocab % 8 or cfg.hidden % 8 or cfg.intermediate % 8 or cfg.head_dim not in (64, 128):
+            raise ValueError("batched decode needs vocab / hidden / intermediate sizes that are multiples of 8 and head_dim 64 or 128")
         self.lib = _lib()
         self.cfg, self.batch, self.max_ctx, self.planes = cfg, batch, int(max_ctx), planes
         # every GEMM pulls the next GEMM's weight into L2 while it waits for its own (measured: -3.6 % step time on
