@@ -60,6 +60,7 @@ constexpr int kGMax = 8;             // max q heads per kv head
 constexpr int kRW = 8;               // max rows per warp per tile
 constexpr int kGatherBatch = 4;      // 16-byte tagged-word loads a thread keeps in flight while gathering a vector
 constexpr int kMaxTP = 8;
+constexpr int kRep = 4;              // copies of the vectors every SM gathers whole (single-GPU kernel)
 constexpr int kTagStride = 256;      // tag = epoch * kTagStride + layer + 1
 
 enum TaskType { T_END = 0, T_QKV = 1, T_ATTN = 2, T_OPROJ = 3, T_GATEUP = 4, T_DOWN = 5, T_LMHEAD = 6, T_MERGE = 7 };
@@ -82,6 +83,8 @@ struct KParams {
   int stream_down;         // 1: the down projection streams its input vector in k-tile by k-tile (down_streamed)
   int attn_block;          // positions per K / V block = 8 x attention warps: one pass of the unit's warps per block
   int pf_window_bytes;     // how far past the ring the Loader prefetches into L2 while it is blocked (0 = off)
+  int poll_inflight;       // ring stages the Loader keeps in flight (and no L2 prefetch) while its consumers poll for inputs (0 = no change)
+  int pace_clk_per_64k;    // Loader pacing: SM clocks per 64 KB of NEW bytes this SM asks HBM for (0 = unpaced)
   int task_cache_bytes;    // shared-memory copy of this SM's task list (32-byte packed records)
   unsigned poll_sleep_ns;  // back-off between polls of a not-yet-complete vector (0 = none)
   // task table
@@ -100,11 +103,15 @@ struct KParams {
   __nv_bfloat16* kcache;
   __nv_bfloat16* vcache;
   // tagged activation vectors ({fp32, tag} words)
-  u64* ll_hx;    // [2][tp][H]  layer input, ping-pong by layer parity; one slot of partial rows per TP rank
-  u64* ll_hm;    // [tp][H]     hidden state after attention, likewise
+  // The vectors every SM gathers whole (hx, hm, attn) are published in `rep` copies; SM s reads copy s % rep.  A
+  // 12 KB vector sits in ~48 of the ~184 L2 slices (256-byte hash granules): with one copy, 148 SMs polling it
+  // queue 100 K requests on those slices and every hop pays that queue twice (the producers' stores wait in it too).
+  int rep;
+  u64* ll_hx;    // [rep][2][tp][H]  layer input, ping-pong by layer parity; one slot of partial rows per TP rank
+  u64* ll_hm;    // [rep][tp][H]     hidden state after attention, likewise
   u64* ll_lmx;   // [tp][2]     (value, index) of every rank's LM-head argmax
   u64* ll_qkv;   // [qkv_rows]
-  u64* ll_attn;  // [q_dim]  merged attention output
+  u64* ll_attn;  // [rep][q_dim]  merged attention output
   u64* ll_act;   // [I]
   u64* ll_part;  // [nq][attn_chunks][D + 2]  split-KV partial records (o[D], m, l)
   float* lm_val;
@@ -208,6 +215,12 @@ __device__ __forceinline__ float2 ldg_keep_f2(const float2* p) {
   asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
   return v;
 }
+__device__ __forceinline__ float4 ldg_keep_f4(const float4* p) {
+  float4 v;
+  const uint64_t pol = l2_evict_last_policy();
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ float ldg_keep_f1(const float* p) {
   float v;
   const uint64_t pol = l2_evict_last_policy();
@@ -266,6 +279,10 @@ __device__ __forceinline__ u64 ll_load(const u64* p) {
 }
 __device__ __forceinline__ void ll_load2(const u64* p, u64& a, u64& b) {  // 16-byte aligned pair of words
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+// four words = one full 32-byte L2 sector per request (LDG.E.256.STRONG.GPU; every word carries its own tag)
+__device__ __forceinline__ void ll_load4(const u64* p, u64 (&w)[4]) {
+  asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(p) : "memory");
 }
 // system-scope variants for words another GPU writes / reads (tensor-parallel slots)
 __device__ __forceinline__ void ll_store_sys(u64* p, float v, unsigned tag) {
@@ -330,6 +347,7 @@ struct SmemHdr {
   float red[64];
   int misc[32];
   float red2[2][8][32];  // cross-K-group partial sums of a tile: [tile parity][K group][row]
+  u64 xbar[8];           // slice barriers of a streamed activation vector (down_streamed)
 };
 static_assert(sizeof(SmemHdr) <= kSmemReserved, "smem header too large");
 
@@ -346,6 +364,12 @@ struct ConsumerCtx {
   int best_idx;
 };
 
+// "the consumers of this SM are polling for their inputs": the Loader holds its bulk traffic back meanwhile
+// (a poll's round trip queues behind every bulk byte in flight to the same SM and to the same L2 slices)
+constexpr int kMiscPolling = 24;
+__device__ __forceinline__ void set_polling(SmemHdr* hdr, int ctid, int v) {
+  if (ctid == 0) *reinterpret_cast<volatile int*>(&hdr->misc[kMiscPolling]) = v;
+}
 __device__ __forceinline__ unsigned tag_of(const ConsumerCtx& c, int layer) { return c.epoch * kTagStride + (unsigned)layer + 1u; }
 
 __device__ __forceinline__ void stamp(const KParams& p, const ConsumerCtx& c, int task, int k) {
@@ -372,51 +396,51 @@ __device__ __forceinline__ AttnGeom attn_geometry(const KParams& p, int pos, int
 // ----------------------------------------------------------------------------------
 // gather of a tagged vector into shared memory
 // ----------------------------------------------------------------------------------
-// Every consumer thread owns the 16-byte word pairs i = ctid, ctid + nct, ... of the vector, issues
-// up to four loads back to back, and re-polls only the words whose tag is still old.  NORM: the
+// Every consumer thread owns the 32-byte word quads i = ctid, ctid + nct, ... of the vector, issues up to
+// kGatherBatch sector loads back to back, and re-polls the batch until every tag is current.  NORM: the
 // values are multiplied by the RMSNorm gain while staged and sum(x^2) is returned (per thread).
 __device__ __noinline__ float ll_gather(const KParams& p, int ctid, int nct, const u64* src, int n, int kpad,
-                                        unsigned tag, float* xs, const float* gain, int task) {
+                                        unsigned tag, float* xs, const float* gain, int task, int first = 0) {
   const bool NORM = gain != nullptr;
-  const int n2 = n >> 1, kp2 = kpad >> 1;
+  const int n4 = n >> 2, kp4 = kpad >> 2;
   float ss = 0.f;
-  for (int i0 = ctid; i0 < kp2; i0 += kGatherBatch * nct) {
-    float2 g[kGatherBatch];
+  for (int i0 = first + ctid; i0 < kp4; i0 += kGatherBatch * nct) {
+    float4 g[kGatherBatch];
 #pragma unroll
     for (int u = 0; u < kGatherBatch; ++u) {  // static operand first: a DRAM miss under the weight stream, overlapped with the poll
       const int i = i0 + u * nct;
-      g[u] = (NORM && i < n2) ? ldg_keep_f2(reinterpret_cast<const float2*>(gain) + i) : make_float2(1.f, 1.f);
+      g[u] = (NORM && i < n4) ? ldg_keep_f4(reinterpret_cast<const float4*>(gain) + i) : make_float4(1.f, 1.f, 1.f, 1.f);
     }
-    u64 a[kGatherBatch], b[kGatherBatch];
+    u64 w[kGatherBatch][4];
     long long t0 = 0;
     for (;;) {  // re-issue the whole batch until every tag is current (one round trip per attempt)
       bool ok = true;
 #pragma unroll
       for (int u = 0; u < kGatherBatch; ++u) {
         const int i = i0 + u * nct;
-        if (i < n2) ll_load2(src + 2 * i, a[u], b[u]);
+        if (i < n4) ll_load4(src + 4 * i, w[u]);
       }
 #pragma unroll
       for (int u = 0; u < kGatherBatch; ++u) {
         const int i = i0 + u * nct;
-        if (i < n2) ok = ok && ll_tag(a[u]) == tag && ll_tag(b[u]) == tag;
+        if (i < n4) ok = ok && ll_tag(w[u][0]) == tag && ll_tag(w[u][1]) == tag && ll_tag(w[u][2]) == tag && ll_tag(w[u][3]) == tag;
       }
       if (ok) break;
       if (p.poll_sleep_ns) __nanosleep(p.poll_sleep_ns);
       if (t0 == 0) t0 = clock64();
-      else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task, (int)ll_tag(a[0]), (int)tag, i0);
+      else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task, (int)ll_tag(w[0][0]), (int)tag, i0);
     }
 #pragma unroll
     for (int u = 0; u < kGatherBatch; ++u) {
       const int i = i0 + u * nct;
-      if (i < kp2) {
-        float2 v = make_float2(0.f, 0.f);
-        if (i < n2) {
-          v.x = ll_val(a[u]); v.y = ll_val(b[u]);
-          ss = fmaf(v.x, v.x, fmaf(v.y, v.y, ss));
-          v.x *= g[u].x; v.y *= g[u].y;
+      if (i < kp4) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < n4) {
+          v = make_float4(ll_val(w[u][0]), ll_val(w[u][1]), ll_val(w[u][2]), ll_val(w[u][3]));
+          ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+          v.x *= g[u].x; v.y *= g[u].y; v.z *= g[u].z; v.w *= g[u].w;
         }
-        reinterpret_cast<float2*>(xs)[i] = v;
+        reinterpret_cast<float4*>(xs)[i] = v;
       }
     }
   }
@@ -566,29 +590,45 @@ __device__ __forceinline__ const float* gemv_gain(const KParams& p, const Task& 
   return p.fparams + (size_t)t.layer * p.fp_layer_stride + (t.type == T_GATEUP ? p.fp_ln2 : p.fp_ln1);
 }
 
-// Stage the activation vector of a GEMV in shared memory (fp32, zero padded to kpad).
+// The input vector of a GEMV: where its tagged words are, its length, the tag that marks it current and, for the
+// RMSNorm-fused operators (QKV: ln1 over the layer input, GATEUP: ln2 over h_mid, LMHEAD: final norm), the gain.
+struct VecSrc {
+  const u64* src;
+  const float* gain;
+  int n;
+  unsigned tag;
+};
+template <bool TP>
+__device__ __forceinline__ bool gemv_input(const KParams& p, const ConsumerCtx& c, const Task& t, VecSrc& v) {
+  const int type = t.type;
+  const size_t cp = blockIdx.x % p.rep;
+  v.gain = nullptr;
+  if (type == T_OPROJ) { v.src = p.ll_attn + cp * p.q_dim; v.n = p.q_dim; v.tag = tag_of(c, t.layer); return true; }
+  if (type == T_DOWN) { v.src = p.ll_act; v.n = p.I; v.tag = tag_of(c, t.layer); return true; }
+  if (type == T_QKV && t.layer == 0) return false;   // layer 0 reads the embedding row directly
+  const int layer = (type == T_LMHEAD) ? p.L : t.layer;
+  v.gain = gemv_gain(p, t); v.n = p.H; v.tag = tag_of(c, layer);
+  if constexpr (TP) v.src = (type == T_GATEUP) ? p.ll_hm : p.ll_hx + (size_t)(layer & 1) * p.tp_size * p.H;
+  else v.src = (type == T_GATEUP) ? p.ll_hm + cp * p.H : p.ll_hx + (cp * 2 + (size_t)(layer & 1)) * p.H;
+  return true;
+}
+__device__ __forceinline__ bool ll_quad_ok(const u64 (&w)[4], unsigned tag) {
+  return ll_tag(w[0]) == tag && ll_tag(w[1]) == tag && ll_tag(w[2]) == tag && ll_tag(w[3]) == tag;
+}
+
+// Stage the activation vector of a GEMV in shared memory (fp32, zero padded to kpad).  The first two sectors of
+// every thread (w0, w1: quads ctid and ctid + nct) were requested at the very top of the task (`early`), before
+// any other work of the task: ~2000 clocks of task preamble used to sit between the task start and its first poll.
 template <bool TP>
 __device__ __forceinline__ void gemv_prologue(const KParams& p, ConsumerCtx& c, const Task& t, int ti, float* xs,
-                                              SmemHdr* hdr, int tok) {
+                                              SmemHdr* hdr, int tok, const VecSrc& vs, bool have, bool early,
+                                              u64 (&w0)[4], u64 (&w1)[4]) {
   const int kpad = t.kchunks * kChunk;
   const int type = t.type;
   c.rs = 1.0f;
-  if (type == T_OPROJ) {
-    ll_gather(p, c.ctid, c.nct, p.ll_attn, p.q_dim, kpad, tag_of(c, t.layer), xs, nullptr, ti);
-    consumer_sync(c.nct);
-    return;
-  }
-  if (type == T_DOWN) {
-    ll_gather(p, c.ctid, c.nct, p.ll_act, p.I, kpad, tag_of(c, t.layer), xs, nullptr, ti);
-    consumer_sync(c.nct);
-    return;
-  }
-  // RMSNorm-fused prologues: QKV (ln1 over the layer input), GATEUP (ln2 over h_mid), LMHEAD (final norm).
-  // Single pass: stage h * gain, accumulate sum(h^2); the scalar rsqrt(mean + eps) commutes with
-  // the dot products and is applied to each output row in the epilogue.
-  const float* gain = gemv_gain(p, t);
   float ss = 0.f;
-  if (type == T_QKV && t.layer == 0) {  // layer 0 reads the embedding row (bf16) directly
+  if (!have) {  // QKV of layer 0: the embedding row (bf16), RMSNorm-fused
+    const float* gain = gemv_gain(p, t);
     const int h2 = p.H >> 1, kp2 = kpad >> 1;
     for (int i = c.ctid; i < kp2; i += c.nct) {
       float2 v = make_float2(0.f, 0.f);
@@ -601,20 +641,55 @@ __device__ __forceinline__ void gemv_prologue(const KParams& p, ConsumerCtx& c, 
       }
       reinterpret_cast<float2*>(xs)[i] = v;
     }
+  } else if (!early) {
+    if (TP && vs.gain) ss = ll_gather_slots(p, c.ctid, c.nct, vs.src, vs.n, kpad, vs.tag, xs, vs.gain, ti);
+    else ss = ll_gather(p, c.ctid, c.nct, vs.src, vs.n, kpad, vs.tag, xs, vs.gain, ti);
   } else {
-    const int layer = (type == T_LMHEAD) ? p.L : t.layer;
-    if constexpr (TP) {
-      const u64* src = (type == T_GATEUP) ? p.ll_hm : p.ll_hx + (size_t)(layer & 1) * p.tp_size * p.H;
-      ss = ll_gather_slots(p, c.ctid, c.nct, src, p.H, kpad, tag_of(c, layer), xs, gain, ti);
-    } else {
-      const u64* src = (type == T_GATEUP) ? p.ll_hm : p.ll_hx + (size_t)(layer & 1) * p.H;
-      ss = ll_gather(p, c.ctid, c.nct, src, p.H, kpad, tag_of(c, layer), xs, gain, ti);
+    const int n4 = vs.n >> 2, kp4 = kpad >> 2, ia = c.ctid, ib = c.ctid + c.nct;
+    float4 ga = make_float4(1.f, 1.f, 1.f, 1.f), gb = ga;
+    if (vs.gain) {
+      if (ia < n4) ga = ldg_keep_f4(reinterpret_cast<const float4*>(vs.gain) + ia);
+      if (ib < n4) gb = ldg_keep_f4(reinterpret_cast<const float4*>(vs.gain) + ib);
     }
+    long long t0 = 0;
+    while (!((ia >= n4 || ll_quad_ok(w0, vs.tag)) && (ib >= n4 || ll_quad_ok(w1, vs.tag)))) {
+      if (ia < n4) ll_load4(vs.src + 4 * ia, w0);
+      if (ib < n4) ll_load4(vs.src + 4 * ib, w1);
+      if (t0 == 0) t0 = clock64();
+      else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, ti, (int)ll_tag(w0[0]), (int)vs.tag, ia);
+    }
+    if (ia < kp4) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ia < n4) {
+        v = make_float4(ll_val(w0[0]), ll_val(w0[1]), ll_val(w0[2]), ll_val(w0[3]));
+        ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+        v.x *= ga.x; v.y *= ga.y; v.z *= ga.z; v.w *= ga.w;
+      }
+      reinterpret_cast<float4*>(xs)[ia] = v;
+    }
+    if (ib < kp4) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ib < n4) {
+        v = make_float4(ll_val(w1[0]), ll_val(w1[1]), ll_val(w1[2]), ll_val(w1[3]));
+        ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+        v.x *= gb.x; v.y *= gb.y; v.z *= gb.z; v.w *= gb.w;
+      }
+      reinterpret_cast<float4*>(xs)[ib] = v;
+    }
+    if (kp4 > 2 * c.nct) ss += ll_gather(p, c.ctid, c.nct, vs.src, vs.n, kpad, vs.tag, xs, vs.gain, ti, 2 * c.nct);
   }
+  if (type == T_OPROJ || type == T_DOWN) {
+    consumer_sync(c.nct);
+    set_polling(hdr, c.ctid, 0);
+    return;
+  }
+  // RMSNorm: h * gain was staged and sum(h^2) accumulated in one pass; the scalar rsqrt(mean + eps) commutes
+  // with the dot products and is applied to each output row in the epilogue.
   ss = warp_sum(ss);
   float* red = hdr->red + (ti & 1) * 16;  // by task parity: a warp that runs ahead writes the other half
   if (c.lane == 0) red[c.cw] = ss;
   consumer_sync(c.nct);
+  set_polling(hdr, c.ctid, 0);
   float tot = 0.f;
   for (int w = 0; w < p.C; ++w) tot += red[w];
   c.rs = rsqrtf(tot / (float)p.H + p.eps);
@@ -630,11 +705,11 @@ __device__ __forceinline__ float load_eop(const KParams& p, const ConsumerCtx& c
       if (TP && p.tp_rank != 0) return 0.f;  // rank 0's partial rows carry the residual
       if (t.layer == 0) return __bfloat162float(p.embed[(size_t)tok * p.H + vrow]);
       if constexpr (TP) return ll_wait_slots_tp(p, p.ll_hx + (size_t)(t.layer & 1) * p.tp_size * p.H, p.H, vrow, tag_of(c, t.layer), ti);
-      else return ll_wait(p, p.ll_hx + (size_t)(t.layer & 1) * p.H + vrow, tag_of(c, t.layer), ti);
+      else return ll_wait(p, p.ll_hx + ((size_t)(blockIdx.x % p.rep) * 2 + (size_t)(t.layer & 1)) * p.H + vrow, tag_of(c, t.layer), ti);
     case T_DOWN:
       if (TP && p.tp_rank != 0) return 0.f;
       if constexpr (TP) return ll_wait_slots_tp(p, p.ll_hm, p.H, vrow, tag_of(c, t.layer), ti);
-      else return ll_wait(p, p.ll_hm + vrow, tag_of(c, t.layer), ti);
+      else return ll_wait(p, p.ll_hm + (size_t)(blockIdx.x % p.rep) * p.H + vrow, tag_of(c, t.layer), ti);
     default: return 0.f;
   }
 }
@@ -646,12 +721,12 @@ __device__ __forceinline__ void gemv_epilogue(const KParams& p, ConsumerCtx& c, 
     case T_QKV: ll_store(p.ll_qkv + vrow, v + eop, tag_of(c, t.layer)); break;
     case T_OPROJ:
       if constexpr (TP) tp_publish(p, 0, 0, vrow, eop + v, tag_of(c, t.layer));
-      else ll_store(p.ll_hm + vrow, eop + v, tag_of(c, t.layer));
+      else for (int r = 0; r < p.rep; ++r) ll_store(p.ll_hm + (size_t)r * p.H + vrow, eop + v, tag_of(c, t.layer));
       break;
     case T_GATEUP: ll_store(p.ll_act + (vrow >> 1), silu(v) * v_pair, tag_of(c, t.layer)); break;  // vrow even = gate, pair = up
     case T_DOWN:
       if constexpr (TP) tp_publish(p, 1, (t.layer + 1) & 1, vrow, eop + v, tag_of(c, t.layer + 1));
-      else ll_store(p.ll_hx + (size_t)((t.layer + 1) & 1) * p.H + vrow, eop + v, tag_of(c, t.layer + 1));
+      else for (int r = 0; r < p.rep; ++r) ll_store(p.ll_hx + ((size_t)r * 2 + (size_t)((t.layer + 1) & 1)) * p.H + vrow, eop + v, tag_of(c, t.layer + 1));
       break;
     case T_LMHEAD: {
       const int gvrow = TP ? vrow + p.vocab_off : vrow;
@@ -926,10 +1001,39 @@ __device__ __forceinline__ void lm_finish(const KParams& p, ConsumerCtx& c, Smem
   }
 }
 
+// The fp32 gains / biases an operator multiplies while it gathers are loaded on the critical path of its hop,
+// and under the weight stream they do not stay in L2 from one step to the next: an operator that runs well
+// before them asks for their lines (evict-last), one line per SM in turn.
+__device__ __forceinline__ void prefetch_fparams(const KParams& p, const ConsumerCtx& c, const float* ptr, int nfloats) {
+  const char* base = reinterpret_cast<const char*>(ptr);
+  const int nlines = (nfloats * 4 + 127) >> 7;
+  for (int i = blockIdx.x + c.ctid * gridDim.x; i < nlines; i += c.nct * gridDim.x)
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(base + (size_t)i * 128));
+}
+
 template <bool TP>
 __device__ __forceinline__ void run_gemv(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* xs,
                                          SmemHdr* hdr, uint8_t* ring, int tok, int probe) {
+  // ---- first of all: ask for the first words of the input vector (the round trip overlaps the rest of the preamble) ----
+  VecSrc vs;
+  vs.src = nullptr; vs.gain = nullptr; vs.n = 0; vs.tag = 0;
+  const bool have = !probe && gemv_input<TP>(p, c, t, vs);
+  const bool early = have && !TP;
+  u64 w0[4] = {0, 0, 0, 0}, w1[4] = {0, 0, 0, 0};
+  if (early) {
+    const int n4 = vs.n >> 2;
+    if (c.ctid < n4) ll_load4(vs.src + 4 * c.ctid, w0);
+    if (c.ctid + c.nct < n4) ll_load4(vs.src + 4 * (c.ctid + c.nct), w1);
+  }
   stamp(p, c, task_idx, 0);
+  if (!probe) {
+    if (t.type == T_QKV) {          // this layer's second norm (gate/up runs three operators later)
+      prefetch_fparams(p, c, p.fparams + (size_t)t.layer * p.fp_layer_stride + p.fp_ln2, p.H);
+    } else if (t.type == T_GATEUP) {  // the next layer's first norm, biases and q/k-norm gains (or the final norm)
+      if (t.layer + 1 < p.L) prefetch_fparams(p, c, p.fparams + (size_t)(t.layer + 1) * p.fp_layer_stride, p.fp_layer_stride);
+      else prefetch_fparams(p, c, p.fparams + p.fp_final, p.H);
+    }
+  }
   // ---- before the inputs are awaited: the epilogue operand of the first tile (bias rows are DRAM
   // misses under the weight stream; residual words were completed earlier in this step) ----
   float eop0 = 0.f;
@@ -941,8 +1045,9 @@ __device__ __forceinline__ void run_gemv(const KParams& p, ConsumerCtx& c, const
       const int rsel = ((c.lane >> 4) & 1) * 4 + ((c.lane >> 3) & 1) * 2 + ((c.lane >> 2) & 1);
       if ((c.lane & 3) == 0 && rsel < rw && c.cw * rw + rsel < rows0) erow = c.cw * rw + rsel;
     } else if (c.ctid < rows0) erow = c.ctid;
+    set_polling(hdr, c.ctid, 1);
     if (erow >= 0) eop0 = load_eop<TP>(p, c, t, task_idx, t.a + erow, tok);
-    gemv_prologue<TP>(p, c, t, task_idx, xs, hdr, tok);
+    gemv_prologue<TP>(p, c, t, task_idx, xs, hdr, tok, vs, have, early, w0, w1);
   }
   stamp(p, c, task_idx, 1);
   gemv_tiles<TP>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe);
@@ -1004,6 +1109,7 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
 
   // ---- q row (+ k, v of the new token in the owner units): gather, (norm), RoPE ----
   // one warp per row of D elements; lane holds elements lane + 32 j so rotate-half partners share a lane
+  set_polling(hdr, c.ctid, 1);
   if (c.cw < (owns_new ? 3 : 1)) {
     constexpr int PER = D / 32, HALF = D / 2;
     const bool is_q = c.cw == 0, is_k = c.cw == 1;
@@ -1055,6 +1161,7 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
     }
   }
   consumer_sync(c.nct);
+  set_polling(hdr, c.ctid, 0);
   stamp(p, c, task_idx, 1);
 
   const int lsub = c.lane & 3, lpos = c.lane >> 2;
@@ -1168,7 +1275,7 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
       lv = fmaf(wgt, comb[w * RS + D + 1], lv);
     }
     if (ge.n_active == 1) {
-      ll_store(p.ll_attn + (size_t)h * D + d, ov / lv, tag);
+      for (int r = 0; r < p.rep; ++r) ll_store(p.ll_attn + (size_t)r * p.q_dim + (size_t)h * D + d, ov / lv, tag);
     } else {
       u64* part = p.ll_part + ((size_t)(t.aux * p.nq + h) * p.attn_chunks + slot) * (size_t)RS;
       ll_store(part + d, ov, tag);
@@ -1227,7 +1334,7 @@ __device__ __forceinline__ void run_merge(const KParams& p, ConsumerCtx& c, cons
         }
       }
     }
-    ll_store(p.ll_attn + (size_t)h * D + d, O / L, tag);
+    for (int r = 0; r < p.rep; ++r) ll_store(p.ll_attn + (size_t)r * p.q_dim + (size_t)h * D + d, O / L, tag);
   }
   stamp(p, c, task_idx, 7);
 }
@@ -1270,17 +1377,18 @@ __device__ __noinline__ uint32_t run_gemv_nl(const KParams& p, GemvArgs g, float
 }
 // ---- down projection with its input streamed in ------------------------------------------------------
 // The down projection reads the longest vector of the layer (I = 8960 words = 72 KB of tagged words per SM
-// for Qwen2.5-1.5B: five dependent round trips when gathered up front).  Its k-tiles are consumed in order,
-// so the words of k-tile kt+1 are copied into shared memory with cp.async (no registers held) while k-tile
-// kt is multiplied (two slices in flight), then checked, converted to fp32 and staged in the other half of a
-// double buffer.  Only the first slice's round trip is exposed.
-// Scratch layout: xbuf[2][ktc * 256] fp32 | raw[2][ktc * 256] words.
-constexpr int kStreamBatch = 4;  // 16-byte word pairs per thread per k-tile
+// for Qwen2.5-1.5B).  Its k-tiles are consumed in order, so the words of k-tiles kt+1 .. kt+kXSlots are in
+// flight as bulk copies (cp.async.bulk: one request instruction per 4 KB slice, full sectors, no registers
+// held) into a small ring of raw slices while k-tile kt is multiplied; a landed slice is checked, converted
+// to fp32 and staged in the other half of a double buffer.  A word that was still old when its slice was
+// copied is polled directly.  Only the first slice's round trip is exposed.
+// Scratch layout: xbuf[2][ktc * 256] fp32 | raw[kXSlots][ktc * 256] words.
+constexpr int kXSlots = 4;
 
 __device__ __forceinline__ bool down_is_streamable(const KParams& p, const Task& t, int nct) {
   const int WK = (t.geom >> 8) & 0xff;
-  return t.type == T_DOWN && WK == 1 && t.n_tiles == 1 && t.n_ktiles > 1 && t.ktc * (kChunk / 2) <= kStreamBatch * nct &&
-         t.ktc * kChunk * 24 <= p.scratch_bytes;
+  return t.type == T_DOWN && WK == 1 && t.n_tiles == 1 && t.n_ktiles > 1 && t.ktc * (kChunk / 4) <= nct &&
+         t.ktc * kChunk * (8 + 8 * kXSlots) <= p.scratch_bytes;
 }
 
 template <int RW, bool TP>
@@ -1302,52 +1410,69 @@ __device__ __forceinline__ void down_streamed(const KParams& p, ConsumerCtx& c, 
 
   const unsigned tag = tag_of(c, t.layer);
   const u64* src = p.ll_act;
-  const int n2 = p.I >> 1;                       // 16-byte word pairs of the vector
-  const int wps = t.ktc * (kChunk / 2);          // word pairs per full k-tile
-  const int w_all = t.kchunks * (kChunk / 2);    // word pairs including the zero padding of the last chunk
+  const int n4 = p.I >> 2;                       // 32-byte word quads of the vector
+  const int qps = t.ktc * (kChunk / 4);          // quads per full k-tile
+  const int q_all = t.kchunks * (kChunk / 4);    // quads including the zero padding of the last chunk
   float* xbuf = scratch;                         // [2][ktc * 256]
-  u64* raw = reinterpret_cast<u64*>(scratch + 2 * t.ktc * kChunk);
+  u64* raw = reinterpret_cast<u64*>(scratch + 2 * t.ktc * kChunk);   // [kXSlots][ktc * 256]
   const uint32_t raw_addr = smem_u32(raw);
+  const uint32_t xbar0 = smem_u32(&hdr->xbar[0]);
   const int last = t.n_ktiles - 1;
 
-  auto issue_raw = [&](int kt) {                 // request this thread's word pairs of k-tile kt
-    const int wb = kt * wps, we = min(wb + wps, w_all);
-#pragma unroll
-    for (int u = 0; u < kStreamBatch; ++u) {
-      const int i = wb + c.ctid + u * c.nct;
-      if (i < we && i < n2)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(raw_addr + (uint32_t)((kt & 1) * wps + i - wb) * 16u), "l"(src + 2 * (size_t)i) : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  auto finish_raw = [&](int kt) {                // check, convert, stage k-tile kt into xbuf[kt & 1]
-    const int wb = kt * wps, we = min(wb + wps, w_all);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");   // every group but the newest (slice kt + 1) has landed
-    float2* dst = reinterpret_cast<float2*>(xbuf + (size_t)(kt & 1) * t.ktc * kChunk);
-    const u64* rawk = raw + (size_t)(kt & 1) * 2 * wps;
-#pragma unroll
-    for (int u = 0; u < kStreamBatch; ++u) {
-      const int i = wb + c.ctid + u * c.nct;
-      if (i < we) {
-        float2 v = make_float2(0.f, 0.f);
-        if (i < n2) {
-          u64 a = rawk[2 * (i - wb)], b = rawk[2 * (i - wb) + 1];
-          if (ll_tag(a) != tag) a = ll_spin(p, src + 2 * (size_t)i, tag, task_idx);       // still old: poll the word itself
-          if (ll_tag(b) != tag) b = ll_spin(p, src + 2 * (size_t)i + 1, tag, task_idx);
-          v = make_float2(ll_val(a), ll_val(b));
-        }
-        dst[i - wb] = v;
+  auto issue_raw = [&](int kt) {                 // one thread: bulk copy of slice kt into raw slot kt % kXSlots
+    if (c.ctid == 0 && kt <= last) {
+      const int qb = kt * qps, qe = min(min(qb + qps, q_all), n4);
+      if (qe > qb) {
+        const uint32_t bytes = (uint32_t)(qe - qb) * 32u, bar = xbar0 + (uint32_t)(kt % kXSlots) * 8u;
+        mbar_arrive_expect_tx(bar, bytes);
+        tma_bulk_g2s(raw_addr + (uint32_t)(kt % kXSlots) * (uint32_t)qps * 32u, src + 4 * (size_t)qb, bytes, bar);
       }
+    }
+  };
+  auto finish_raw = [&](int kt) {                // check, convert, stage slice kt into xbuf[kt & 1]
+    const int qb = kt * qps, qe = min(qb + qps, q_all);
+    if (min(qe, n4) > qb) mbar_wait(p, xbar0 + (uint32_t)(kt % kXSlots) * 8u, (uint32_t)(kt / kXSlots) & 1u, DE_WATCHDOG_FULL, task_idx);
+    float4* dst = reinterpret_cast<float4*>(xbuf + (size_t)(kt & 1) * t.ktc * kChunk);
+    const u64* rawk = raw + (size_t)(kt % kXSlots) * 4 * qps;
+    const int i = qb + c.ctid;
+    if (i < qe) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < n4) {
+        u64 w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = rawk[4 * (i - qb) + j];
+        if (ll_tag(w[0]) != tag || ll_tag(w[1]) != tag || ll_tag(w[2]) != tag || ll_tag(w[3]) != tag) {
+          long long t0 = 0;                       // copied before its producer stored it: poll the sector itself
+          for (;;) {
+            ll_load4(src + 4 * (size_t)i, w);
+            if (ll_tag(w[0]) == tag && ll_tag(w[1]) == tag && ll_tag(w[2]) == tag && ll_tag(w[3]) == tag) break;
+            if (t0 == 0) t0 = clock64();
+            else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task_idx, (int)ll_tag(w[0]), (int)tag, i);
+          }
+        }
+        v = make_float4(ll_val(w[0]), ll_val(w[1]), ll_val(w[2]), ll_val(w[3]));
+      }
+      dst[i - qb] = v;
     }
     consumer_sync(c.nct);
   };
 
-  // first slice: wait until its first word is current before asking for the whole slice (the copy cannot re-poll)
-  if (c.ctid < min(wps, n2)) ll_spin(p, src + 2 * (size_t)c.ctid, tag, task_idx);
-  issue_raw(0);
-  issue_raw(1);
+  // the slice barriers start every task in phase 0 (no copy is pending between tasks)
+  if (c.ctid == 0) {
+#pragma unroll
+    for (int s2 = 0; s2 < kXSlots; ++s2) mbar_init(xbar0 + s2 * 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  // first slice: wait until its words are current before asking for copies (a copy cannot re-poll)
+  set_polling(hdr, c.ctid, 1);
+  if (c.ctid < min(qps, n4)) ll_spin(p, src + 4 * (size_t)c.ctid, tag, task_idx);
+  consumer_sync(c.nct);
+  set_polling(hdr, c.ctid, 0);
+#pragma unroll
+  for (int s2 = 0; s2 < kXSlots; ++s2) issue_raw(s2);
   finish_raw(0);
-  issue_raw(2);   // (an empty group past the last k-tile keeps the wait_group arithmetic uniform)
+  issue_raw(kXSlots);
   stamp(p, c, task_idx, 1);
 
   const int chunks_last = t.kchunks - last * t.ktc;
@@ -1370,7 +1495,7 @@ __device__ __forceinline__ void down_streamed(const KParams& p, ConsumerCtx& c, 
     if (++slot == n_stage) { slot = 0; ph ^= 1u; }
     if (kt < last) {
       finish_raw(kt + 1);
-      issue_raw(kt + 3);
+      issue_raw(kt + 1 + kXSlots);
     }
   }
   c.slot = slot; c.ph = ph;
@@ -1439,6 +1564,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    hdr->misc[kMiscPolling] = 0;
   }
   __syncthreads();
   auto fetch_task = [&](int ti) {  // ti relative to tb
@@ -1456,7 +1582,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
     if (lane == 0 && p.probe != 4) {
       uint32_t slot = 0, ph = 0;          // next slot to fill
       uint32_t wslot = 0, wph = 0;        // oldest stage that may still be in flight
-      int issued = 0;
+      int issued = 0, retired = 0;
+      volatile int* polling = reinterpret_cast<volatile int*>(&hdr->misc[kMiscPolling]);
       const int cap = (p.inflight > 0 && p.inflight < p.n_stage) ? p.inflight : p.n_stage;
       const uint32_t ring_addr = smem_u32(ring);
       const uint32_t n_stage = (uint32_t)p.n_stage;
@@ -1480,6 +1607,19 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       const uint8_t* pf = wcur;
       unsigned n_pf = 0;  // L2 prefetch granules issued this step (debug counter in sync[4])
       constexpr uint32_t kPfGranule = 8192;
+      // Pacing.  Every request that reaches DRAM queues behind the ones already there, and so does every tagged-word
+      // poll that shares the L2 slice queues with them: an unpaced Loader (148 SMs x ring + prefetch window, all
+      // issued at once) keeps megabytes queued and the loaded L2 round trip of a hop grows from ~0.15 us to > 1 us.
+      // So the NEW bytes this SM asks HBM for (the frontier `pf`: L2 prefetch granules, or ring stages the prefetch
+      // has not covered) are metered at pace_clk_per_64k clocks per 64 KB -- the SM's share of the HBM rate --
+      // with a small burst allowance; ring stages behind the frontier are L2 hits and are not metered.
+      const long long pace = p.pace_clk_per_64k;
+      constexpr long long kPaceBurstClk = 512;
+      long long next_ok = clock64();
+      auto pace_charge = [&](uint32_t nb) {
+        const long long now = clock64();
+        next_ok = max(next_ok, now - kPaceBurstClk) + (((long long)nb * pace) >> 16);
+      };
       auto blocked_wait = [&](uint32_t bar, uint32_t parity, int code, int ti) {
         if (mbar_try_wait(bar, parity)) return;
         if (p.pf_window_bytes > 0 && !p.probe) {
@@ -1487,21 +1627,44 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
           if (pf < wcur) pf = wcur;
           while (pf < wend && pf < wcur + p.pf_window_bytes) {
             if (mbar_test_wait(bar, parity)) return;
+            if (p.poll_inflight && *polling) {
+              if (clock64() - t0 > kWatchdogCycles) dev_fail(p, code, ti, (int)bar, (int)parity, 0);
+              continue;   // the consumers are polling: no new HBM requests from this SM
+            }
+            if (pace) {
+              const long long now = clock64();
+              if (now < next_ok) {
+                if (now - t0 > kWatchdogCycles) dev_fail(p, code, ti, (int)bar, (int)parity, 0);
+                continue;   // budget not open yet: keep watching the barrier
+              }
+            }
             const uint32_t nb = (uint32_t)min((size_t)kPfGranule, (size_t)(wend - pf));
             l2_prefetch_bulk(pf, nb, pol);
             pf += nb;
             ++n_pf;
+            if (pace) pace_charge(nb);
             if (clock64() - t0 > kWatchdogCycles) dev_fail(p, code, ti, (int)bar, (int)parity, 0);
           }
         }
         mbar_wait_slow(p, bar, parity, code, ti);
       };
       auto issue = [&](const void* src, uint32_t bytes, bool hint, int ti) {
-        if (issued >= cap) {  // at most `cap` stages in flight: wait for the oldest one to land
+        // at most `cap` stages in flight (`poll_inflight` while the consumers poll): wait for the oldest one to land
+        while (issued - retired >= ((p.poll_inflight && *polling) ? p.poll_inflight : cap)) {
           blocked_wait(smem_u32(&hdr->full[wslot]), wph, DE_WATCHDOG_INFLIGHT, ti);
           if (++wslot == n_stage) { wslot = 0; wph ^= 1u; }
+          ++retired;
         }
         blocked_wait(smem_u32(&hdr->empty[slot]), ph ^ 1u, DE_WATCHDOG_EMPTY, ti);
+        if (pace && hint && p.probe != 3) {   // weight stage: meter the part the prefetch frontier has not covered
+          const uint8_t* e = static_cast<const uint8_t*>(src) + bytes;
+          if (e > pf) {
+            while (clock64() < next_ok) {}
+            const uint8_t* b0 = static_cast<const uint8_t*>(src);
+            pace_charge((uint32_t)(e - (pf > b0 ? pf : b0)));
+            pf = e;
+          }
+        }
         const uint32_t fb = smem_u32(&hdr->full[slot]);
         mbar_arrive_expect_tx(fb, bytes);
         if (hint) tma_bulk_g2s_hint(ring_addr + slot * (uint32_t)p.stage_bytes, src, bytes, fb, pol);
@@ -1686,7 +1849,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct AdamkHandle_ {
   AdamkModelDesc desc{};
   int n_sms = 0, C = 0, n_stage = 0, stage_bytes = 0, n_tasks = 0, batch = 0, inflight = 0;
-  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, poll_sleep_ns = 0, task_cache_bytes = 0, pf_window_kb = 0;
+  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, poll_sleep_ns = 0, task_cache_bytes = 0, pf_window_kb = 0, pace = 0, poll_inflight = 0;
   const unsigned* d_sm_stream = nullptr;
   size_t packed_weight_bytes = 0;  // matrix streams only
   size_t fparam_floats = 0;
@@ -1700,7 +1863,7 @@ struct AdamkHandle_ {
   const float* fparams = nullptr;
   AdamkWeightPtrs w{};
   int stream_down = 1;
-  int tp_rank = 0, tp_size = 1;
+  int tp_rank = 0, tp_size = 1, rep = 1;
   void* peer_ws[kMaxTP] = {nullptr};
   bool peers_bound = false;
   int* status_host = nullptr;
@@ -1740,7 +1903,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   h->tp_rank = tp_rank; h->tp_size = tp_size;
   h->n_sms = tt[2]; h->C = tt[3]; h->n_stage = tt[4]; h->stage_bytes = tt[5]; h->n_tasks = tt[6]; h->batch = tt[7];
   h->inflight = tt[8]; h->attn_chunks = tt[9]; h->attn_min_chunk = tt[10]; h->scratch_bytes = tt[11];
-  h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14] & 0xffff; h->stream_down = !((tt[14] >> 16) & 1); h->pf_window_kb = tt[15];
+  h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14] & 0xffff; h->stream_down = !((tt[14] >> 16) & 1); h->pf_window_kb = tt[15] & 0xffff; h->pace = (tt[15] >> 16) & 0x7fff; h->poll_inflight = (tt[14] >> 20) & 0xf;
   auto bad = [&](const std::string& m) { delete h; return fail(ADAMK_E_INVALID, m); };
   const AdamkModelDesc& d = *desc;
   if (d.head_dim != 64 && d.head_dim != 128) return bad("head_dim must be 64 or 128");
@@ -1828,11 +1991,12 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
   h->ws_sync = take(64);
-  h->ws_hx = take((size_t)2 * tp_size * d.hidden * 8);
-  h->ws_hm = take((size_t)tp_size * d.hidden * 8);
+  h->rep = tp_size == 1 ? kRep : 1;
+  h->ws_hx = take((size_t)h->rep * 2 * tp_size * d.hidden * 8);
+  h->ws_hm = take((size_t)h->rep * tp_size * d.hidden * 8);
   h->ws_lmx = take((size_t)kMaxTP * 2 * 8);
   h->ws_qkv = take((size_t)qkv_rows * 8);
-  h->ws_attn = take((size_t)d.n_q_heads * d.head_dim * 8);
+  h->ws_attn = take((size_t)h->rep * d.n_q_heads * d.head_dim * 8);
   h->ws_act = take((size_t)d.intermediate * 8);
   h->ws_part = take((size_t)d.n_q_heads * h->attn_chunks * (d.head_dim + 2) * 8);
   h->ws_lm_val = take((size_t)h->n_sms * 4);
@@ -2003,7 +2167,7 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
   p.has_bias = d.qkv_bias; p.qk_norm = d.qk_norm; p.eps = d.rms_eps;
   p.C = h->C; p.n_stage = h->n_stage; p.stage_bytes = h->stage_bytes; p.attn_chunks = h->attn_chunks;
   p.attn_min_chunk = h->attn_min_chunk; p.scratch_bytes = h->scratch_bytes; p.n_lm_tasks = h->n_lm_tasks;
-  p.task_cache_bytes = h->task_cache_bytes; p.pf_window_bytes = h->pf_window_kb * 1024;
+  p.task_cache_bytes = h->task_cache_bytes; p.pf_window_bytes = h->pf_window_kb * 1024; p.pace_clk_per_64k = h->pace; p.poll_inflight = h->poll_inflight;
   p.attn_block = 8 * std::min(h->C, kAttnWarps);
   p.stream_down = h->stream_down;
   p.inflight = h->inflight; p.poll_sleep_ns = (unsigned)h->poll_sleep_ns;
@@ -2020,6 +2184,7 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
     p.lm_val = (float*)(ws + h->ws_lm_val); p.lm_idx = (int*)(ws + h->ws_lm_idx);
     p.ll_lmx = (u64*)(ws + h->ws_lmx);
   }
+  p.rep = h->rep;
   p.tp_rank = h->tp_rank; p.tp_size = h->tp_size; p.vocab_off = h->tp_rank * d.vocab;
   for (int r = 0; r < h->tp_size; ++r) {
     uint8_t* pw = h->tp_size == 1 ? ws : static_cast<uint8_t*>(h->peer_ws[r]);

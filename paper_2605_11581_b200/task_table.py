@@ -79,6 +79,8 @@ class KernelSchedule:
     inflight: int = 0         # ring stages the Loader keeps in flight at most (0 = all free slots)
     poll_sleep_ns: int = 0    # back-off between polls of an incomplete activation vector
     l2_prefetch_kb: int = 0   # per-SM window past the ring the Loader prefetches into L2 while it is blocked
+    poll_inflight: int = 0    # ring stages in flight (and no L2 prefetch) while this SM's consumers poll for inputs (0 = unchanged)
+    pace_clk_per_64k: int = 0  # Loader pacing: SM clocks per 64 KB of new HBM requests per SM (0 = unpaced); see pace_for()
     stream_down: bool = True  # the down projection streams its input vector in k-tile by k-tile (cp.async) instead of gathering it up front
 
     def __post_init__(self) -> None:
@@ -98,6 +100,8 @@ class KernelSchedule:
             raise ScheduleError("attn_min_chunk out of range")
         if not 0 <= self.inflight <= self.n_stage:
             raise ScheduleError("inflight must be in 0..n_stage")
+        if not 0 <= self.l2_prefetch_kb <= 0xFFFF or not 0 <= self.pace_clk_per_64k <= 0x7FFF:
+            raise ScheduleError("l2_prefetch_kb / pace_clk_per_64k out of range")
 
     @property
     def rows_per_warp(self) -> int:
@@ -129,6 +133,14 @@ class KernelSchedule:
         return cls(**kw)
 
 
+def pace_for(hbm_gbs: float, n_sms: int = 148, sm_mhz: float = 1965.0) -> int:
+    """``pace_clk_per_64k`` that meters the Loaders of ``n_sms`` SMs to ``hbm_gbs`` GB/s in aggregate."""
+    if hbm_gbs <= 0:
+        return 0
+    bytes_per_clk = hbm_gbs * 1e9 / n_sms / (sm_mhz * 1e6)
+    return max(1, min(0x7FFF, round(65536 / bytes_per_clk)))
+
+
 def scratch_bytes(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> int:
     """Shared-memory scratch: the fp32 activation vector of the widest GEMV, or
     the attention unit's q / probability / cross-warp merge buffers."""
@@ -136,12 +148,12 @@ def scratch_bytes(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> in
     x_bytes = batch * kpad_max * 4
     d = cfg.head_dim
     attn_bytes = ((d + 16) + 2 * d + ATTN_WARPS * (d + 2) + ATTN_WARPS) * 4
-    # streamed down projection (csrc: down_streamed): two fp32 slices + two raw tagged-word slices of one k-tile
+    # streamed down projection (csrc: down_streamed): two fp32 slices + four raw tagged-word slices of one k-tile
     stream_bytes = 0
     if sched.stream_down and batch == 1:
         _, wk, _, ktc = op_geometry(sched, _ceil_div(cfg.hidden, 148), _ceil_div(cfg.intermediate, KCHUNK), False)
-        if wk == 1 and ktc * KCHUNK * 24 <= x_bytes + 8192:
-            stream_bytes = ktc * KCHUNK * 24
+        if wk == 1 and ktc * KCHUNK * 40 <= x_bytes + 8192:
+            stream_bytes = ktc * KCHUNK * 40
     return _ceil_div(max(x_bytes, attn_bytes, stream_bytes), 1024) * 1024
 
 
@@ -379,8 +391,8 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
                    tasks.shape[0], batch, sched.inflight, attn_chunks, sched.attn_min_chunk,
                    scratch_bytes(cfg, sched, batch), n_lm]
     header[13] = (cursor // 16) & 0x7FFFFFFF
-    header[14] = (sched.poll_sleep_ns & 0xFFFF) | ((0 if sched.stream_down else 1) << 16)
-    header[15] = sched.l2_prefetch_kb
+    header[14] = (sched.poll_sleep_ns & 0xFFFF) | ((0 if sched.stream_down else 1) << 16) | ((sched.poll_inflight & 0xF) << 20)
+    header[15] = (sched.l2_prefetch_kb & 0xFFFF) | ((sched.pace_clk_per_64k & 0x7FFF) << 16)
     return TaskTable(cfg=cfg, sched=sched, n_sms=n_sms, batch=batch, header=header, sm_begin=sm_begin,
                      tasks=tasks, packed_weight_bytes=cursor, attn_chunks=attn_chunks)
 
