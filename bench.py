@@ -233,7 +233,7 @@ def run_ours(args) -> None:
     tp = world if (args.tp and world > 1) else 1
     cfg = full_cfg.shard(tp)                      # this rank's dimensions (the whole model when tp == 1)
     w = random_weights(full_cfg, seed=0, device=dev).shard(rank, tp)   # same seed on every rank -> same model
-    sched = default_schedule(cfg)
+    sched = default_schedule(cfg, tp_size=tp)
     max_ctx = PROMPT_LEN + args.steps + args.warmup + 16
     plug = MegaKernelPlugin(cfg, sched, max_ctx=max_ctx, device=local, tp_rank=rank if tp > 1 else 0, tp_size=tp)
     plug.bind_weights(w)

@@ -52,7 +52,7 @@ constexpr int kHeaderInts = 16;
 constexpr int kTaskInts = 16;
 constexpr int kChunk = 256;          // K elements per chunk
 constexpr int kSmemMax = 232448;
-constexpr int kSmemReserved = 4096;  // barriers + reduction scratch
+constexpr int kSmemReserved = 3584;  // barriers + reduction scratch + the shared-memory copy of the kernel parameters
 constexpr int kMaxStages = 16;
 constexpr int kAttnWarps = 8;        // consumer warps that take part in an attention unit
 constexpr int kAttnChunksMax = 128;  // split-KV units per (sequence, kv head)
@@ -63,7 +63,7 @@ constexpr int kMaxTP = 8;
 constexpr int kRep = 4;              // copies of the vectors every SM gathers whole (single-GPU kernel)
 constexpr int kTagStride = 256;      // tag = epoch * kTagStride + layer + 1
 
-enum TaskType { T_END = 0, T_QKV = 1, T_ATTN = 2, T_OPROJ = 3, T_GATEUP = 4, T_DOWN = 5, T_LMHEAD = 6, T_MERGE = 7 };
+enum TaskType { T_END = 0, T_QKV = 1, T_ATTN = 2, T_OPROJ = 3, T_GATEUP = 4, T_DOWN = 5, T_LMHEAD = 6, T_MERGE = 7, T_DOWNK = 8, T_HRED = 9 };
 
 struct Task {  // 64 bytes
   int type, layer, a, b, k, kchunks, rt, ktc, n_tiles, n_ktiles, w_off, geom, r12, r13, r14, aux;
@@ -114,6 +114,7 @@ struct KParams {
   u64* ll_attn;  // [rep][q_dim]  merged attention output
   u64* ll_act;   // [I]
   u64* ll_part;  // [nq][attn_chunks][D + 2]  split-KV partial records (o[D], m, l)
+  u64* ll_part2; // [H / 4][n_sms][4]  fused down projection: every SM's partial rows (T_DOWNK -> T_HRED), row-quad major
   float* lm_val;
   int* lm_idx;
   unsigned* sync;  // [0] = epoch, [1] = CTAs that finished the LM head
@@ -315,8 +316,10 @@ __device__ __noinline__ void dev_fail(const KParams& p, int code, int task, int 
 
 __device__ __noinline__ void mbar_wait_slow(const KParams& p, uint32_t bar, uint32_t parity, int code, int task) {
   const long long t0 = clock64();
+  // the Loader's waits (EMPTY / INFLIGHT) time out later than the consumers': the first report names the root cause
+  const long long limit = (code == DE_WATCHDOG_EMPTY || code == DE_WATCHDOG_INFLIGHT) ? 2 * kWatchdogCycles : kWatchdogCycles;
   while (!mbar_try_wait_hint(bar, parity, 2000u)) {
-    if (clock64() - t0 > kWatchdogCycles) dev_fail(p, code, task, (int)bar, (int)parity, 0);
+    if (clock64() - t0 > limit) dev_fail(p, code, task, (int)bar, (int)parity, 0);
   }
 }
 __device__ __forceinline__ void mbar_wait(const KParams& p, uint32_t bar, uint32_t parity, int code, int task) {
@@ -348,6 +351,11 @@ struct SmemHdr {
   int misc[32];
   float red2[2][8][32];  // cross-K-group partial sums of a tile: [tile parity][K group][row]
   u64 xbar[8];           // slice barriers of a streamed activation vector (down_streamed)
+  // A copy of the kernel parameters.  The out-of-line task bodies take `const KParams&`; a reference to the
+  // __grid_constant__ parameter makes every p.field a generic load that misses L1 (the shared-memory carve-out
+  // leaves no L1) and pays an L2 round trip under the weight stream -- dozens of them, dependent, at the top of
+  // every task.  The copy in shared memory is one LDS away.
+  KParams kp;
 };
 static_assert(sizeof(SmemHdr) <= kSmemReserved, "smem header too large");
 
@@ -360,6 +368,7 @@ struct ConsumerCtx {
   int nct;            // number of consumer threads
   unsigned epoch;     // step sequence number (tag prefix)
   float rs;           // RMSNorm scale of the current GEMV's input (applied in the epilogue), else 1
+  float* act_loc;     // fused down projection: this SM's SwiGLU outputs (shared memory, behind the staged gate/up input)
   float best_val;     // LM-head running argmax (epilogue lanes)
   int best_idx;
 };
@@ -723,7 +732,10 @@ __device__ __forceinline__ void gemv_epilogue(const KParams& p, ConsumerCtx& c, 
       if constexpr (TP) tp_publish(p, 0, 0, vrow, eop + v, tag_of(c, t.layer));
       else for (int r = 0; r < p.rep; ++r) ll_store(p.ll_hm + (size_t)r * p.H + vrow, eop + v, tag_of(c, t.layer));
       break;
-    case T_GATEUP: ll_store(p.ll_act + (vrow >> 1), silu(v) * v_pair, tag_of(c, t.layer)); break;  // vrow even = gate, pair = up
+    case T_GATEUP:   // vrow even = gate, pair = up
+      if (t.aux) c.act_loc[(vrow - t.a) >> 1] = silu(v) * v_pair;   // fused down projection: the value stays on this SM
+      else ll_store(p.ll_act + (vrow >> 1), silu(v) * v_pair, tag_of(c, t.layer));
+      break;
     case T_DOWN:
       if constexpr (TP) tp_publish(p, 1, (t.layer + 1) & 1, vrow, eop + v, tag_of(c, t.layer + 1));
       else for (int r = 0; r < p.rep; ++r) ll_store(p.ll_hx + ((size_t)r * 2 + (size_t)((t.layer + 1) & 1)) * p.H + vrow, eop + v, tag_of(c, t.layer + 1));
@@ -1113,18 +1125,36 @@ __device__ __forceinline__ void run_attn(const KParams& p, ConsumerCtx& c, const
   if (c.cw < (owns_new ? 3 : 1)) {
     constexpr int PER = D / 32, HALF = D / 2;
     const bool is_q = c.cw == 0, is_k = c.cw == 1;
+    // first of all: ask for the row's words (the round trip overlaps the loads of the static operands)
+    const u64* src = p.ll_qkv + (is_q ? (size_t)h * D : (size_t)p.q_dim + (is_k ? 0 : p.kv_dim) + (size_t)kvh * D) + c.lane;
+    u64 wr[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) wr[j] = ll_load(src + 32 * j);
     float cs[PER / 2], sn[PER / 2];
 #pragma unroll
-    for (int j = 0; j < PER / 2; ++j) {  // static operands first: they are DRAM misses
+    for (int j = 0; j < PER / 2; ++j) {  // static operands: DRAM misses the first time a position is used
       cs[j] = __ldg(p.rope_cos + (size_t)pos * HALF + c.lane + 32 * j);
       sn[j] = __ldg(p.rope_sin + (size_t)pos * HALF + c.lane + 32 * j);
     }
     float gn[PER];
 #pragma unroll
     for (int j = 0; j < PER; ++j) gn[j] = (p.qk_norm && (is_q || is_k)) ? ldg_keep_f1(lay_fp + (is_q ? p.fp_qn : p.fp_kn) + c.lane + 32 * j) : 1.f;
-    const u64* src = p.ll_qkv + (is_q ? (size_t)h * D : (size_t)p.q_dim + (is_k ? 0 : p.kv_dim) + (size_t)kvh * D);
     float v[PER];
-    ll_wait_strided<PER>(p, src + c.lane, 32, tag, v, task_idx);
+    {
+      long long t0 = 0;
+      for (;;) {
+        bool ok = true;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) ok = ok && ll_tag(wr[j]) == tag;
+        if (ok) break;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) wr[j] = ll_load(src + 32 * j);
+        if (t0 == 0) t0 = clock64();
+        else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, task_idx, (int)ll_tag(wr[0]), (int)tag, -1);
+      }
+#pragma unroll
+      for (int j = 0; j < PER; ++j) v[j] = ll_val(wr[j]);
+    }
     if (!is_q && !is_k) {  // v row: staged patch value (+ cache)
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
@@ -1345,6 +1375,202 @@ struct WarpArgs {  // passed by value to the out-of-line task bodies so the cons
   uint32_t slot, ph;
   int layer, a, b, aux, task_idx, pos;
 };
+// ---- fused down projection ---------------------------------------------------------------------------
+// T_DOWNK: the SwiGLU outputs of this SM's gate/up rows (act_loc, nk = 60-61 values for Qwen2.5-1.5B) never leave
+// the SM: they multiply the SM's own K-slice of the down projection -- columns k0 .. k0 + nk, stored column-major,
+// all H rows each -- and the SM publishes H partial rows.  A lane owns eight consecutive rows of a 256-row block
+// (one LDS.128 per column), a warp owns the blocks cw, cw + C, ...: no shuffles, no gather, nothing to wait for.
+constexpr int kDownkBlocks = 3;   // 256-row blocks per warp at most (H <= 768 C)
+
+__device__ __forceinline__ void st_quad(u64* dst, const float (&v)[4], unsigned tag) {   // one 32-byte sector, two 16-byte stores
+  const u64 t = (u64)tag << 32;
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(t | (u64)__float_as_uint(v[0])), "l"(t | (u64)__float_as_uint(v[1])) : "memory");
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst + 2), "l"(t | (u64)__float_as_uint(v[2])), "l"(t | (u64)__float_as_uint(v[3])) : "memory");
+}
+
+// `cols` columns of one stage for the NB row blocks of this warp: four columns per iteration, every LDS.128 of
+// an iteration issued before the first FFMA2 (the loop is latency-bound otherwise: one warp or two per scheduler).
+template <int NB>
+__device__ __forceinline__ void downk_stage(uint32_t cb, uint32_t col_bytes, uint32_t blk_step, const float* act, int cols,
+                                            bool probe, float2 (&acc)[kDownkBlocks][4]) {
+  int j = 0;
+#pragma unroll 1
+  for (; j + 4 <= cols; j += 4, cb += 4 * col_bytes) {
+    uint4 q[4][NB];
+    float a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = probe ? 1.f : act[j + u];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) q[u][i] = lds128u(cb + u * col_bytes + i * blk_step);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float2 a2 = make_float2(a[u], a[u]);
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        acc[i][0] = __ffma2_rn(make_float2(bf_lo(q[u][i].x), bf_hi(q[u][i].x)), a2, acc[i][0]);
+        acc[i][1] = __ffma2_rn(make_float2(bf_lo(q[u][i].y), bf_hi(q[u][i].y)), a2, acc[i][1]);
+        acc[i][2] = __ffma2_rn(make_float2(bf_lo(q[u][i].z), bf_hi(q[u][i].z)), a2, acc[i][2]);
+        acc[i][3] = __ffma2_rn(make_float2(bf_lo(q[u][i].w), bf_hi(q[u][i].w)), a2, acc[i][3]);
+      }
+    }
+  }
+#pragma unroll 1
+  for (; j < cols; ++j, cb += col_bytes) {
+    const float av = probe ? 1.f : act[j];
+    const float2 a2 = make_float2(av, av);
+    uint4 q[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) q[i] = lds128u(cb + i * blk_step);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      acc[i][0] = __ffma2_rn(make_float2(bf_lo(q[i].x), bf_hi(q[i].x)), a2, acc[i][0]);
+      acc[i][1] = __ffma2_rn(make_float2(bf_lo(q[i].y), bf_hi(q[i].y)), a2, acc[i][1]);
+      acc[i][2] = __ffma2_rn(make_float2(bf_lo(q[i].z), bf_hi(q[i].z)), a2, acc[i][2]);
+      acc[i][3] = __ffma2_rn(make_float2(bf_lo(q[i].w), bf_hi(q[i].w)), a2, acc[i][3]);
+    }
+  }
+}
+
+__device__ __noinline__ uint32_t run_downk_nl(const KParams& p, WarpArgs w, int nk, int cps, int n_st, float* scratch,
+                                              SmemHdr* hdr, uint8_t* ring) {
+  const int H = p.H, nblk = H >> 8;
+  if (p.trace && w.ctid == 0) p.trace[(size_t)w.task_idx * 8 + 0] = globaltimer_ns();
+  const float* act = scratch + ((H + kChunk - 1) / kChunk) * kChunk;
+  if (!p.probe) consumer_sync(w.nct);   // every warp's SwiGLU outputs are in act_loc (K-split gate/up tiles end without a barrier)
+  const uint32_t full0 = smem_u32(&hdr->full[0]), empty0 = smem_u32(&hdr->empty[0]);
+  const uint32_t ring_addr = smem_u32(ring), n_stage = (uint32_t)p.n_stage, stage_bytes = (uint32_t)p.stage_bytes;
+  uint32_t slot = w.slot, ph = w.ph;
+  float2 acc[kDownkBlocks][4];
+#pragma unroll
+  for (int i = 0; i < kDownkBlocks; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  const int probe_mode = p.probe, C = p.C;
+  const uint32_t lane_off = (uint32_t)(w.cw * 256 + w.lane * 8) * 2u, blk_step = (uint32_t)C * 512u, col_bytes = (uint32_t)H * 2u;
+  const bool probe = probe_mode != 0;
+  const int nmine = w.cw < nblk ? (nblk - w.cw + C - 1) / C : 0;   // row blocks cw, cw + C, ... of this warp
+  int col = 0;
+#pragma unroll 1
+  for (int st = 0; st < n_st; ++st) {
+    if (probe_mode != 4) mbar_wait(p, full0 + slot * 8, ph, DE_WATCHDOG_FULL, w.task_idx);
+    const int cols = min(cps, nk - col);
+    if (probe_mode != 2) {
+      const uint32_t cb = ring_addr + slot * stage_bytes + lane_off;
+      if (nmine == 1) downk_stage<1>(cb, col_bytes, blk_step, act + col, cols, probe, acc);
+      else if (nmine == 2) downk_stage<2>(cb, col_bytes, blk_step, act + col, cols, probe, acc);
+      else if (nmine == 3) downk_stage<3>(cb, col_bytes, blk_step, act + col, cols, probe, acc);
+    }
+    col += cols;
+    if (probe_mode != 4) {
+      __syncwarp();
+      if (w.lane == 0) mbar_arrive(empty0 + slot * 8);
+    }
+    if (++slot == n_stage) { slot = 0; ph ^= 1u; }
+  }
+  if (probe) {
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < kDownkBlocks; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s += acc[i][j].x + acc[i][j].y;
+    if (s == 1.2345678e-30f) p.probe_sink[blockIdx.x * 64] = s;
+    return slot | (ph << 8);
+  }
+  // publish: row quad q of SM s lives at part2[(q * n_sms + s) * 4]: a T_HRED task reads its quads of all SMs contiguously
+  const unsigned tag = w.epoch * kTagStride + (unsigned)w.layer + 1u;
+#pragma unroll
+  for (int i = 0; i < kDownkBlocks; ++i) {
+    if (i < nmine) {
+      const size_t q0 = (size_t)(w.cw + i * C) * 64 + (size_t)w.lane * 2;
+      const float lo4[4] = {acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y};
+      const float hi4[4] = {acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y};
+      st_quad(p.ll_part2 + (q0 * gridDim.x + blockIdx.x) * 4, lo4, tag);
+      st_quad(p.ll_part2 + ((q0 + 1) * gridDim.x + blockIdx.x) * 4, hi4, tag);
+    }
+  }
+  if (p.trace && w.ctid == 0) p.trace[(size_t)w.task_idx * 8 + 2] = globaltimer_ns();
+  consumer_sync(w.nct);   // act_loc / the staged gate/up input may be overwritten by the next task
+  if (p.trace && w.ctid == 0) p.trace[(size_t)w.task_idx * 8 + 7] = globaltimer_ns();
+  return slot | (ph << 8);
+}
+
+// T_HRED: rows 4 q0 .. 4 (q0 + nq) of the next layer's input = residual (h_mid) + the sum of every SM's partial
+// row, in a fixed order (SMs 32 apart per lane, then the xor tree) -- the result does not depend on timing.
+constexpr int kHredQuadsMax = 16;
+__device__ __noinline__ void run_hred_nl(const KParams& p, WarpArgs w, int q0, int nq, float* stage) {
+  const int S = (int)gridDim.x, SP = S + 1, items = nq * S;
+  const unsigned tag = w.epoch * kTagStride + (unsigned)w.layer + 1u;
+  const u64* base = p.ll_part2 + (size_t)q0 * S * 4;   // [nq][S][4] contiguous
+  // first of all: ask for the first two sectors of this thread and for its residual word
+  u64 wa[4] = {0, 0, 0, 0}, wb[4] = {0, 0, 0, 0};
+  const int ia = w.ctid, ib = w.ctid + w.nct;
+  if (ia < items) ll_load4(base + 4 * (size_t)ia, wa);
+  if (ib < items) ll_load4(base + 4 * (size_t)ib, wb);
+  const int nrows = nq * 4, C = p.C;
+  const u64* res = p.ll_hm + (size_t)(blockIdx.x % p.rep) * p.H + (size_t)q0 * 4;
+  // lane k of warp cw finishes row cw + k C (k < 4): its residual word is requested now as well
+  const int my_row = w.cw + w.lane * C;
+  const bool has_res = w.lane < 4 && my_row < nrows;
+  u64 rw0 = 0;
+  if (has_res) rw0 = ll_load(res + my_row);
+  if (p.trace && w.ctid == 0) p.trace[(size_t)w.task_idx * 8 + 0] = globaltimer_ns();
+  for (int i0 = w.ctid; i0 < items; i0 += 2 * w.nct) {
+    const int i1 = i0 + w.nct;
+    if (i0 != w.ctid) {
+      ll_load4(base + 4 * (size_t)i0, wa);
+      if (i1 < items) ll_load4(base + 4 * (size_t)i1, wb);
+    }
+    long long t0 = 0;
+    while (!(ll_quad_ok(wa, tag) && (i1 >= items || ll_quad_ok(wb, tag)))) {
+      ll_load4(base + 4 * (size_t)i0, wa);
+      if (i1 < items) ll_load4(base + 4 * (size_t)i1, wb);
+      if (t0 == 0) t0 = clock64();
+      else if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, w.task_idx, (int)ll_tag(wa[0]), (int)tag, i0);
+    }
+    {
+      const int q = i0 / S, s = i0 - q * S;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) stage[(q * 4 + j) * SP + s] = ll_val(wa[j]);
+    }
+    if (i1 < items) {
+      const int q = i1 / S, s = i1 - q * S;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) stage[(q * 4 + j) * SP + s] = ll_val(wb[j]);
+    }
+  }
+  consumer_sync(w.nct);
+  if (p.trace && w.ctid == 0) p.trace[(size_t)w.task_idx * 8 + 1] = globaltimer_ns();
+  const unsigned tag_out = w.epoch * kTagStride + (unsigned)(w.layer + 1) + 1u;
+  float mine = 0.f;
+  for (int k = 0; w.cw + k * C < nrows; ++k) {   // rows cw, cw + C, ...: the total of row cw + k C ends up in lane k
+    const int r = w.cw + k * C;
+    float s = 0.f;
+    for (int j = w.lane; j < S; j += 32) s += stage[r * SP + j];
+    s = warp_sum(s);
+    if (w.lane == (k & 3)) mine = s;
+    if ((k & 3) == 3 || r + C >= nrows) {        // lanes 0..3 publish up to four finished rows
+      const int kr = (k & ~3) + w.lane, row_l = w.cw + kr * C;
+      if (w.lane < 4 && row_l < nrows) {
+        u64 rw = (kr == w.lane) ? rw0 : ll_load(res + row_l);
+        const long long t0 = clock64();
+        while (ll_tag(rw) != tag) {
+          rw = ll_load(res + row_l);
+          if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_TAG, w.task_idx, (int)ll_tag(rw), (int)tag, row_l);
+        }
+        const float v = ll_val(rw) + mine;
+        const int row = q0 * 4 + row_l;
+        for (int c2 = 0; c2 < p.rep; ++c2)
+          ll_store(p.ll_hx + ((size_t)c2 * 2 + (size_t)((w.layer + 1) & 1)) * p.H + row, v, tag_out);
+      }
+    }
+  }
+  if (p.trace && w.ctid == 0) p.trace[(size_t)w.task_idx * 8 + 2] = globaltimer_ns();
+  consumer_sync(w.nct);   // the next task overwrites the staging array
+  if (p.trace && w.ctid == 0) p.trace[(size_t)w.task_idx * 8 + 7] = globaltimer_ns();
+}
+
 template <int D>
 __device__ __noinline__ uint32_t run_attn_nl(const KParams& p, WarpArgs w, float* scratch, SmemHdr* hdr, uint8_t* ring) {
   ConsumerCtx c;
@@ -1361,7 +1587,7 @@ struct GemvArgs {
   int cw, lane, ctid, nct;
   unsigned epoch;
   uint32_t slot, ph;
-  int type, layer, a, b, k, kchunks, rt, ktc, n_tiles, n_ktiles, geom;
+  int type, layer, a, b, k, kchunks, rt, ktc, n_tiles, n_ktiles, geom, aux;
   int task_idx, tok, probe;
 };
 template <bool TP>
@@ -1371,7 +1597,8 @@ __device__ __noinline__ uint32_t run_gemv_nl(const KParams& p, GemvArgs g, float
   c.rs = 1.f; c.best_val = -INFINITY; c.best_idx = -1;
   Task t{};
   t.type = g.type; t.layer = g.layer; t.a = g.a; t.b = g.b; t.k = g.k; t.kchunks = g.kchunks; t.rt = g.rt; t.ktc = g.ktc;
-  t.n_tiles = g.n_tiles; t.n_ktiles = g.n_ktiles; t.geom = g.geom;
+  t.n_tiles = g.n_tiles; t.n_ktiles = g.n_ktiles; t.geom = g.geom; t.aux = g.aux;
+  c.act_loc = xs + ((p.H + kChunk - 1) / kChunk) * kChunk;
   run_gemv<TP>(p, c, t, g.task_idx, xs, hdr, ring, g.tok, g.probe);
   return c.slot | (c.ph << 8);
 }
@@ -1557,6 +1784,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
     tcache[2 * i] = make_int4(a.x | (a.y << 8) | (d.w << 20), a.z, a.w | (b.z << 16), b.y | (b.w << 16));
     tcache[2 * i + 1] = make_int4(cc.x | (cc.y << 16), cc.z, cc.w, b.x);
   }
+  {
+    const uint32_t* ksrc = reinterpret_cast<const uint32_t*>(&p);
+    uint32_t* kdst = reinterpret_cast<uint32_t*>(&hdr->kp);
+    for (int i = threadIdx.x; i < (int)(sizeof(KParams) / 4); i += blockDim.x) kdst[i] = ksrc[i];
+  }
+  const KParams& kp = hdr->kp;   // what the out-of-line task bodies read
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.n_stage; ++s) {
       mbar_init(smem_u32(&hdr->full[s]), 1);
@@ -1676,7 +1909,17 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
         const Task lt = fetch_task(ti - tb);
         const int type = lt.type, nrows = lt.b, kchunks = lt.kchunks, rt = lt.rt, ktc = lt.ktc;
         const int n_tiles = lt.n_tiles, n_ktiles = lt.n_ktiles;
-        if (type == T_END || type == T_MERGE) continue;
+        if (type == T_END || type == T_MERGE || type == T_HRED) continue;
+        if (type == T_DOWNK) {   // nrows = columns of the SM's K-slice, kchunks = columns per stage, lt.k = H rows per column
+          const uint8_t* src = p.wpacked + (size_t)(uint32_t)lt.w_off * 16u;
+          for (int col = 0; col < nrows; col += kchunks) {
+            const uint32_t bytes = (uint32_t)min(kchunks, nrows - col) * (uint32_t)lt.k * 2u;
+            issue(src, bytes, true, ti);
+            src += bytes;
+            wcur = src;
+          }
+          continue;
+        }
         if (type == T_ATTN) {
           // K / V blocks of this unit's context chunk, one ring stage each (skipped in probe mode)
           if (p.probe) continue;
@@ -1728,23 +1971,33 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
   }
   for (int ti = tb; ti < te; ++ti) {
     const Task t = fetch_task(ti - tb);
-    if (t.type == T_ATTN || t.type == T_MERGE) {
+    if (t.type == T_DOWNK || t.type == T_HRED) {
+      if (probe && t.type == T_HRED) continue;
+      WarpArgs w;
+      w.cw = c.cw; w.lane = c.lane; w.ctid = c.ctid; w.nct = c.nct; w.epoch = c.epoch; w.slot = c.slot; w.ph = c.ph;
+      w.layer = t.layer; w.a = t.a; w.b = t.b; w.aux = t.aux; w.task_idx = ti; w.pos = pos;
+      if (t.type == T_HRED) run_hred_nl(kp, w, t.a, t.b, scratch);
+      else {
+        const uint32_t sp = run_downk_nl(kp, w, t.b, t.kchunks, t.n_ktiles, scratch, hdr, ring);
+        c.slot = sp & 0xffu; c.ph = sp >> 8;
+      }
+    } else if (t.type == T_ATTN || t.type == T_MERGE) {
       if (probe) continue;
       WarpArgs w;
       w.cw = c.cw; w.lane = c.lane; w.ctid = c.ctid; w.nct = c.nct; w.epoch = c.epoch; w.slot = c.slot; w.ph = c.ph;
       w.layer = t.layer; w.a = t.a; w.b = t.b; w.aux = t.aux; w.task_idx = ti; w.pos = pos;
-      if (t.type == T_MERGE) run_merge_nl(p, w);
+      if (t.type == T_MERGE) run_merge_nl(kp, w);
       else {
-        const uint32_t sp = (p.D == 128) ? run_attn_nl<128>(p, w, scratch, hdr, ring) : run_attn_nl<64>(p, w, scratch, hdr, ring);
+        const uint32_t sp = (p.D == 128) ? run_attn_nl<128>(kp, w, scratch, hdr, ring) : run_attn_nl<64>(kp, w, scratch, hdr, ring);
         c.slot = sp & 0xffu; c.ph = sp >> 8;
       }
     } else if (t.type != T_END) {
       GemvArgs g;
       g.cw = c.cw; g.lane = c.lane; g.ctid = c.ctid; g.nct = c.nct; g.epoch = c.epoch; g.slot = c.slot; g.ph = c.ph;
       g.type = t.type; g.layer = t.layer; g.a = t.a; g.b = t.b; g.k = t.k; g.kchunks = t.kchunks; g.rt = t.rt; g.ktc = t.ktc;
-      g.n_tiles = t.n_tiles; g.n_ktiles = t.n_ktiles; g.geom = t.geom; g.task_idx = ti; g.tok = tok; g.probe = probe;
-      const uint32_t sp = (!probe && p.stream_down && down_is_streamable(p, t, c.nct)) ? run_down_streamed_nl<TP>(p, g, scratch, hdr, ring)
-                                                                                       : run_gemv_nl<TP>(p, g, scratch, hdr, ring);
+      g.n_tiles = t.n_tiles; g.n_ktiles = t.n_ktiles; g.geom = t.geom; g.aux = t.aux; g.task_idx = ti; g.tok = tok; g.probe = probe;
+      const uint32_t sp = (!probe && p.stream_down && down_is_streamable(p, t, c.nct)) ? run_down_streamed_nl<TP>(kp, g, scratch, hdr, ring)
+                                                                                       : run_gemv_nl<TP>(kp, g, scratch, hdr, ring);
       c.slot = sp & 0xffu; c.ph = sp >> 8;
     }
   }
@@ -1785,6 +2038,16 @@ __global__ void adamk_pack_kernel(const PackParams pp) {
   const int ti = blockIdx.x;
   if (ti >= pp.n_tasks) return;
   const Task t = pp.tasks[ti];
+  if (t.type == T_DOWNK) {   // columns t.a .. t.a + t.b of the down projection [H][I], each as H consecutive rows
+    __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(pp.wpacked + (size_t)(uint32_t)t.w_off * 16u);
+    const __nv_bfloat16* wd = (const __nv_bfloat16*)pp.layers[t.layer].wdown;
+    const int n = t.b * pp.H;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+      const int j = e / pp.H, r = e - j * pp.H;
+      d[e] = wd[(size_t)r * pp.I + t.a + j];
+    }
+    return;
+  }
   if (!is_gemv(t.type)) return;
   uint4* dst = reinterpret_cast<uint4*>(pp.wpacked + (size_t)(uint32_t)t.w_off * 16u);
   size_t done = 0;  // 16-byte elements written so far
@@ -1849,7 +2112,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct AdamkHandle_ {
   AdamkModelDesc desc{};
   int n_sms = 0, C = 0, n_stage = 0, stage_bytes = 0, n_tasks = 0, batch = 0, inflight = 0;
-  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, poll_sleep_ns = 0, task_cache_bytes = 0, pf_window_kb = 0, pace = 0, poll_inflight = 0;
+  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, poll_sleep_ns = 0, task_cache_bytes = 0, pf_window_kb = 0, pace = 0, poll_inflight = 0, fuse_down = 0;
   const unsigned* d_sm_stream = nullptr;
   size_t packed_weight_bytes = 0;  // matrix streams only
   size_t fparam_floats = 0;
@@ -1872,6 +2135,7 @@ struct AdamkHandle_ {
   int smem_bytes = 0;
   // workspace layout (byte offsets)
   size_t ws_lmx = 0;
+  size_t ws_part2 = 0;
   size_t ws_sync = 0, ws_hx = 0, ws_hm = 0, ws_qkv = 0, ws_attn = 0, ws_act = 0, ws_part = 0, ws_lm_val = 0,
          ws_lm_idx = 0, ws_total = 0;
 };
@@ -1903,7 +2167,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   h->tp_rank = tp_rank; h->tp_size = tp_size;
   h->n_sms = tt[2]; h->C = tt[3]; h->n_stage = tt[4]; h->stage_bytes = tt[5]; h->n_tasks = tt[6]; h->batch = tt[7];
   h->inflight = tt[8]; h->attn_chunks = tt[9]; h->attn_min_chunk = tt[10]; h->scratch_bytes = tt[11];
-  h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14] & 0xffff; h->stream_down = !((tt[14] >> 16) & 1); h->pf_window_kb = tt[15] & 0xffff; h->pace = (tt[15] >> 16) & 0x7fff; h->poll_inflight = (tt[14] >> 20) & 0xf;
+  h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14] & 0xffff; h->stream_down = !((tt[14] >> 16) & 1); h->pf_window_kb = tt[15] & 0xffff; h->pace = (tt[15] >> 16) & 0x7fff; h->poll_inflight = (tt[14] >> 20) & 0xf; h->fuse_down = (tt[14] >> 24) & 1;
   auto bad = [&](const std::string& m) { delete h; return fail(ADAMK_E_INVALID, m); };
   const AdamkModelDesc& d = *desc;
   if (d.head_dim != 64 && d.head_dim != 128) return bad("head_dim must be 64 or 128");
@@ -1927,13 +2191,20 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
     const int* sb = tt + kHeaderInts;
     int most = 0;
     for (int s2 = 0; s2 < h->n_sms; ++s2) most = std::max(most, sb[s2 + 1] - sb[s2]);
-    h->task_cache_bytes = (int)align_up((size_t)most * 32, 1024);
+    h->task_cache_bytes = (int)align_up((size_t)most * 32, 512);
   }
   h->smem_bytes = kSmemReserved + h->task_cache_bytes + h->scratch_bytes + h->n_stage * h->stage_bytes;
   if (h->smem_bytes > kSmemMax) return bad("ring + scratch + task cache exceed 227 KB shared memory");
   {  // the scratch region must hold the widest activation vector, and the attention buffers
-    const int kmax = std::max(std::max(d.hidden, d.n_q_heads * d.head_dim), d.intermediate);
-    const size_t xb = align_up((size_t)kmax, kChunk) * 4;
+    const int kmax = std::max(std::max(d.hidden, d.n_q_heads * d.head_dim), h->fuse_down ? 0 : d.intermediate);
+    size_t xb = align_up((size_t)kmax, kChunk) * 4;
+    if (h->fuse_down) {   // staged gate/up input + this SM's SwiGLU outputs; the [rows][n_sms + 1] staging array of T_HRED
+      if (tp_size != 1) return bad("fuse_down is a single-GPU schedule");
+      if (d.hidden % 256 || (d.hidden / 256 + h->C - 1) / h->C > kDownkBlocks) return bad("fuse_down: hidden must be a multiple of 256, at most 3 row blocks per warp");
+      const size_t act_loc = (size_t)(d.intermediate + h->n_sms - 1) / h->n_sms + 1;
+      const size_t quads = (size_t)(d.hidden / 4 + h->n_sms - 1) / h->n_sms;
+      xb = std::max(align_up((size_t)d.hidden, kChunk) * 4 + act_loc * 4, std::max(xb, quads * 4 * (size_t)(h->n_sms + 1) * 4));
+    }
     const size_t ab = ((size_t)(d.head_dim + 16) + 2 * (size_t)d.head_dim + (size_t)kAttnWarps * (d.head_dim + 2) + kAttnWarps) * 4;
     if ((size_t)h->scratch_bytes < std::max(xb, ab)) return bad("scratch_bytes too small for this model");
   }
@@ -1955,6 +2226,25 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
       if (t.a < 0 || t.a >= d.n_q_heads || t.layer < 0 || t.layer >= d.n_layers || t.aux != 0) return bad("merge task out of range");
       continue;
     }
+    if (t.type == T_DOWNK || t.type == T_HRED) {
+      if (!h->fuse_down) return bad("fused down-projection task in a table without the fuse_down flag");
+      if (t.layer < 0 || t.layer >= d.n_layers || t.k != d.hidden) return bad("fused down-projection task out of range");
+      if (t.type == T_HRED) {
+        if (t.a < 0 || t.b < 1 || t.b > kHredQuadsMax || (t.a + t.b) * 4 > d.hidden) return bad("T_HRED rows out of range");
+        continue;
+      }
+      // T_DOWNK must follow the gate/up task of the same SM whose SwiGLU outputs it multiplies
+      if (i == 0 || tasks[i - 1].type != T_GATEUP || tasks[i - 1].aux != 1 || tasks[i - 1].layer != t.layer ||
+          tasks[i - 1].a != 2 * t.a || tasks[i - 1].b != 2 * t.b)
+        return bad("T_DOWNK does not match the preceding gate/up task");
+      if (t.a < 0 || t.b < 1 || t.a + t.b > d.intermediate || t.b > 0xffff) return bad("T_DOWNK columns out of range");
+      if (t.kchunks < 1 || (size_t)t.kchunks * d.hidden * 2 > (size_t)h->stage_bytes || t.n_ktiles != (t.b + t.kchunks - 1) / t.kchunks)
+        return bad("T_DOWNK staging inconsistent");
+      const size_t bytes = (size_t)t.b * d.hidden * 2;
+      const size_t off = (size_t)(uint32_t)t.w_off * 16;
+      wbytes = std::max(wbytes, off + bytes);
+      continue;
+    }
     if (t.type < T_QKV || t.type > T_LMHEAD) return bad("unknown task type");
     if (t.b > 0xffff || t.rt > 0xffff || t.kchunks > 0xffff || t.ktc > 0xffff || t.n_tiles > 0xffff || t.n_ktiles > 0xffff)
       return bad("task field exceeds the packed 16-bit range");
@@ -1973,6 +2263,8 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
     if (rw < 2 || rw > kRW || (rw & 1) || t.rt != WR * rw) return bad("rows per warp must be 2, 4, 6 or 8 and rows_per_tile == WR * rw");
     if (WK > 1 && t.rt > 32) return bad("K-split tiles hold at most 32 rows");
     if (t.type == T_GATEUP && ((t.a | t.b | rw) & 1)) return bad("gate/up rows must come in pairs");
+    if (t.aux != 0 && !(t.type == T_GATEUP && t.aux == 1 && h->fuse_down)) return bad("task aux field out of range");
+    if (t.type == T_DOWN && h->fuse_down) return bad("T_DOWN in a fuse_down table");
     if (t.ktc < 1 || t.n_ktiles != (t.kchunks + t.ktc - 1) / t.ktc || t.n_tiles != (t.b + t.rt - 1) / t.rt)
       return bad("task tiling inconsistent");
     if ((size_t)t.rt * t.ktc * 512 > (size_t)h->stage_bytes) return bad("stage larger than stage_bytes");
@@ -1999,6 +2291,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   h->ws_attn = take((size_t)h->rep * d.n_q_heads * d.head_dim * 8);
   h->ws_act = take((size_t)d.intermediate * 8);
   h->ws_part = take((size_t)d.n_q_heads * h->attn_chunks * (d.head_dim + 2) * 8);
+  h->ws_part2 = take(h->fuse_down ? (size_t)d.hidden * h->n_sms * 8 : 0);
   h->ws_lm_val = take((size_t)h->n_sms * 4);
   h->ws_lm_idx = take((size_t)h->n_sms * 4);
   h->ws_total = o;
@@ -2013,9 +2306,10 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
       sm_stream[sm] = cursor;
       for (int i = sm_begin[sm]; i < sm_begin[sm + 1]; ++i) {
         const Task& t = tasks[i];
-        if (t.type == T_ATTN || t.type == T_MERGE) continue;
+        if (t.type == T_ATTN || t.type == T_MERGE || t.type == T_HRED) continue;
         if ((unsigned)t.w_off != cursor) return bad("packed streams must be contiguous per SM, SM-major");
-        cursor += (unsigned)((size_t)t.b * t.kchunks * 512 / 16);
+        if (t.type == T_DOWNK) cursor += (unsigned)((size_t)t.b * t.k * 2 / 16);
+        else cursor += (unsigned)((size_t)t.b * t.kchunks * 512 / 16);
       }
     }
     sm_stream[h->n_sms] = cursor;
@@ -2183,6 +2477,7 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
     p.ll_attn = (u64*)(ws + h->ws_attn); p.ll_act = (u64*)(ws + h->ws_act); p.ll_part = (u64*)(ws + h->ws_part);
     p.lm_val = (float*)(ws + h->ws_lm_val); p.lm_idx = (int*)(ws + h->ws_lm_idx);
     p.ll_lmx = (u64*)(ws + h->ws_lmx);
+    p.ll_part2 = (u64*)(ws + h->ws_part2);
   }
   p.rep = h->rep;
   p.tp_rank = h->tp_rank; p.tp_size = h->tp_size; p.vocab_off = h->tp_rank * d.vocab;

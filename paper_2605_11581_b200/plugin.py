@@ -169,7 +169,9 @@ class MegaKernelPlugin:
 
         trace = parse_trace(trace_text if isinstance(trace_text, (bytes, bytearray)) else str(trace_text).encode())
         sched = KernelSchedule.from_plan(trace.plan, **schedule_overrides)
-        fit = __import__("paper_2605_11581_b200.task_table", fromlist=["max_stages_that_fit"]).max_stages_that_fit(cfg, sched)
+        from .task_table import max_stages_that_fit
+
+        fit = max_stages_that_fit(cfg, sched)
         if sched.n_stage > fit:
             sched = KernelSchedule.from_plan(trace.plan, **dict(schedule_overrides, n_stage=max(2, fit)))
         return cls(cfg, sched, max_ctx, device=device)
@@ -290,8 +292,11 @@ class BatchLanes:
     small batches.)"""
 
     def __init__(self, cfg: ModelConfig, schedule: KernelSchedule, max_ctx: int, batch: int, device: int = 0):
+        from .schedules import fit_schedule
+
         total = device_sm_count(device)
         self.batch = int(batch)
+        schedule = fit_schedule(cfg, schedule, n_sms=total // self.batch)   # ring depth / fused down projection for the lane's SM count
         self.lanes = [MegaKernelPlugin(cfg, schedule, max_ctx, device=device, n_sms=total // self.batch)
                       for _ in range(self.batch)]
         self.device = self.lanes[0].device

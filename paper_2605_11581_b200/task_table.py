@@ -41,7 +41,7 @@ HEADER_INTS = 16
 TASK_INTS = 16
 KCHUNK = 256           # K elements per chunk: 32 lanes x 8 bf16 (one LDS.128 per lane)
 SMEM_MAX = 232448      # 227 KB opt-in shared memory per CTA on sm_100
-SMEM_RESERVED = 4096   # mbarriers + reduction scratch ahead of the scratch/ring regions
+SMEM_RESERVED = 3584   # mbarriers + reduction scratch + parameter copy ahead of the scratch/ring regions
 MAX_STAGES = 16
 MAX_RW = 8             # rows per consumer warp per tile (eight accumulator rows per lane)
 ATTN_BLOCK = 64        # most positions per K (or V) ring stage: 8 per attention warp
@@ -49,10 +49,11 @@ ATTN_WARPS = 8         # consumer warps that take part in an attention unit
 ATTN_CHUNKS_MAX = 128  # split-KV units per (sequence, kv head)
 G_MAX = 8              # q heads per kv head
 
-T_END, T_QKV, T_ATTN, T_OPROJ, T_GATEUP, T_DOWN, T_LMHEAD, T_MERGE = 0, 1, 2, 3, 4, 5, 6, 7
+T_END, T_QKV, T_ATTN, T_OPROJ, T_GATEUP, T_DOWN, T_LMHEAD, T_MERGE, T_DOWNK, T_HRED = 0, 1, 2, 3, 4, 5, 6, 7, 8, 9
 GEMV_TYPES = (T_QKV, T_OPROJ, T_GATEUP, T_DOWN, T_LMHEAD)
+STREAM_TYPES = GEMV_TYPES + (T_DOWNK,)   # tasks that own a run of the packed weight stream
 TYPE_NAMES = {T_QKV: "qkv", T_ATTN: "attn", T_MERGE: "merge", T_OPROJ: "oproj", T_GATEUP: "gateup",
-              T_DOWN: "down", T_LMHEAD: "lmhead"}
+              T_DOWN: "down", T_LMHEAD: "lmhead", T_DOWNK: "downk", T_HRED: "hred"}
 
 # field indices inside a task record
 F_TYPE, F_LAYER, F_A, F_B, F_K, F_KCHUNKS, F_RT, F_KTC, F_NTILES, F_NKTILES, \
@@ -81,6 +82,8 @@ class KernelSchedule:
     l2_prefetch_kb: int = 0   # per-SM window past the ring the Loader prefetches into L2 while it is blocked
     poll_inflight: int = 0    # ring stages in flight (and no L2 prefetch) while this SM's consumers poll for inputs (0 = unchanged)
     pace_clk_per_64k: int = 0  # Loader pacing: SM clocks per 64 KB of new HBM requests per SM (0 = unpaced); see pace_for()
+    fuse_down: bool = False   # gate/up keeps its SwiGLU outputs on the SM and multiplies them by its own K-slice of the down projection (T_DOWNK);
+                              # the 1/n_sms partial rows are summed by T_HRED tasks (no gather of the I-long activation vector)
     stream_down: bool = True  # the down projection streams its input vector in k-tile by k-tile (cp.async) instead of gathering it up front
 
     def __post_init__(self) -> None:
@@ -141,34 +144,69 @@ def pace_for(hbm_gbs: float, n_sms: int = 148, sm_mhz: float = 1965.0) -> int:
     return max(1, min(0x7FFF, round(65536 / bytes_per_clk)))
 
 
-def scratch_bytes(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> int:
+def scratch_bytes(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1, n_sms: int = 148) -> int:
     """Shared-memory scratch: the fp32 activation vector of the widest GEMV, or
     the attention unit's q / probability / cross-warp merge buffers."""
-    kpad_max = max(_ceil_div(k, KCHUNK) * KCHUNK for k in (cfg.hidden, cfg.q_dim, cfg.intermediate))
+    fused = sched.fuse_down and batch == 1
+    ks = (cfg.hidden, cfg.q_dim) if fused else (cfg.hidden, cfg.q_dim, cfg.intermediate)   # fused: nobody gathers the I-long vector
+    kpad_max = max(_ceil_div(k, KCHUNK) * KCHUNK for k in ks)
     x_bytes = batch * kpad_max * 4
     d = cfg.head_dim
     attn_bytes = ((d + 16) + 2 * d + ATTN_WARPS * (d + 2) + ATTN_WARPS) * 4
     # streamed down projection (csrc: down_streamed): two fp32 slices + four raw tagged-word slices of one k-tile
     stream_bytes = 0
-    if sched.stream_down and batch == 1:
-        _, wk, _, ktc = op_geometry(sched, _ceil_div(cfg.hidden, 148), _ceil_div(cfg.intermediate, KCHUNK), False)
+    if sched.stream_down and batch == 1 and not fused:
+        _, wk, _, ktc = op_geometry(sched, _ceil_div(cfg.hidden, n_sms), _ceil_div(cfg.intermediate, KCHUNK), False)
         if wk == 1 and ktc * KCHUNK * 40 <= x_bytes + 8192:
             stream_bytes = ktc * KCHUNK * 40
-    return _ceil_div(max(x_bytes, attn_bytes, stream_bytes), 1024) * 1024
+    fused_bytes = fused_scratch_bytes(cfg, n_sms) if fused else 0
+    return _ceil_div(max(x_bytes, attn_bytes, stream_bytes, fused_bytes), 1024) * 1024
 
 
-def task_cache_bytes(cfg: ModelConfig, batch: int = 1, n_sms: int = 148) -> int:
-    """Shared-memory copy of one SM's task list (32 bytes per task): per layer four GEMV operators
-    plus the attention units and merge tasks placed on the busiest SM; one LM-head task."""
+def fused_scratch_bytes(cfg: ModelConfig, n_sms: int) -> int:
+    """Scratch the fused down projection needs: the staged gate/up input (H fp32) followed by this SM's SwiGLU
+    outputs (T_DOWNK), or the [rows][n_sms + 1] partial sums a T_HRED task adds up."""
+    kpad_h = _ceil_div(cfg.hidden, KCHUNK) * KCHUNK
+    act_loc = _ceil_div(cfg.intermediate, n_sms) + 1
+    quads = _ceil_div(cfg.hidden // 4, n_sms)
+    return max(kpad_h * 4 + act_loc * 4, quads * 4 * hred_stride(n_sms) * 4)
+
+
+def hred_stride(n_sms: int) -> int:
+    """Row stride (floats) of the T_HRED staging array."""
+    return n_sms + 1
+
+
+def task_cache_bytes(cfg: ModelConfig, batch: int = 1, n_sms: int = 148, fused: bool = False) -> int:
+    """Shared-memory copy of one SM's task list (32 bytes per task): per layer four GEMV operators (five tasks
+    with the fused down projection) plus the attention units and merge tasks placed on the busiest SM; one LM-head task."""
     nq = cfg.n_q_heads
     attn_chunks = max(1, min(n_sms // (batch * nq), ATTN_CHUNKS_MAX))
-    per_layer = 4 + _ceil_div(batch * nq * attn_chunks, n_sms) + _ceil_div(batch * nq, n_sms)
-    return _ceil_div((cfg.n_layers * per_layer + 1) * 32, 1024) * 1024
+    per_layer = (5 if fused else 4) + _ceil_div(batch * nq * attn_chunks, n_sms) + _ceil_div(batch * nq, n_sms)
+    return _ceil_div((cfg.n_layers * per_layer + 1) * 32, 512) * 512
 
 
-def max_stages_that_fit(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1) -> int:
-    free = SMEM_MAX - SMEM_RESERVED - task_cache_bytes(cfg, batch) - scratch_bytes(cfg, sched, batch)
+def max_stages_that_fit(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1, n_sms: int = 148) -> int:
+    free = (SMEM_MAX - SMEM_RESERVED - task_cache_bytes(cfg, batch, n_sms, sched.fuse_down)
+            - scratch_bytes(cfg, sched, batch, n_sms))
     return max(0, min(MAX_STAGES, free // sched.stage_bytes))
+
+
+def fuse_down_error(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, tp_size: int = 1) -> str | None:
+    """Why the fused down projection (T_DOWNK / T_HRED) cannot run for this model / SM count, or None."""
+    if tp_size != 1:
+        return "fuse_down is a single-GPU schedule (tensor-parallel ranks publish partial rows to their peers instead)"
+    if cfg.hidden % 256:
+        return "fuse_down needs hidden to be a multiple of 256 (eight rows per lane, 32 lanes)"
+    if _ceil_div(cfg.hidden // 256, sched.consumer_warps) > 3:
+        return "fuse_down: more than three 256-row blocks per consumer warp"
+    if sched.stage_bytes < cfg.hidden * 2:
+        return "fuse_down: a ring slot must hold one column of the down projection"
+    if _ceil_div(cfg.hidden // 4, n_sms) > 16:
+        return "fuse_down: more than 16 row quads per T_HRED task"
+    if cfg.intermediate < n_sms:
+        return "fuse_down: every SM must own at least one gate/up pair (its partial rows are awaited by every T_HRED task)"
+    return None
 
 
 def split_rows(n_units: int, n_sms: int, rot: int) -> list[tuple[int, int]]:
@@ -295,6 +333,8 @@ def stage_shapes(task: np.ndarray):
 
 
 def task_weight_bytes(task: np.ndarray) -> int:
+    if int(task[F_TYPE]) == T_DOWNK:      # b columns of the down projection, k = H rows each
+        return int(task[F_B]) * int(task[F_K]) * 2
     if int(task[F_TYPE]) not in GEMV_TYPES:
         return 0
     # rows * kchunks * 512, independent of tiling
@@ -310,11 +350,11 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
         raise ScheduleError("this build executes batch 1 only (batched path: SURVEY.md 8(f).1)")
     if n_sms < 1:
         raise ScheduleError("n_sms must be >= 1")
-    fit = max_stages_that_fit(cfg, sched, batch)
+    fit = max_stages_that_fit(cfg, sched, batch, n_sms)
     if sched.n_stage > fit:
         raise ScheduleError(
             f"n_stage={sched.n_stage} x {sched.stage_bytes} B stages + "
-            f"{scratch_bytes(cfg, sched, batch)} B scratch exceed {SMEM_MAX} B shared memory (max {fit})")
+            f"{scratch_bytes(cfg, sched, batch, n_sms)} B scratch exceed {SMEM_MAX} B shared memory (max {fit})")
     if sched.stage_bytes < 8 * min(sched.consumer_warps, ATTN_WARPS) * cfg.head_dim * 2:
         raise ScheduleError("ring slot smaller than one 64-position K/V block")
     if cfg.group > G_MAX:
@@ -328,7 +368,13 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
     per_sm: list[list[list[int]]] = [[] for _ in range(n_sms)]
     rot = 0
 
-    def gemv(ttype: int, layer: int, n_rows: int, k: int, unit: int) -> int:
+    fuse = sched.fuse_down
+    if fuse:
+        why = fuse_down_error(cfg, sched, n_sms)
+        if why:
+            raise ScheduleError(why)
+
+    def gemv(ttype: int, layer: int, n_rows: int, k: int, unit: int, aux: int = 0) -> int:
         """Emit one GEMV operator across all SMs; returns the number of tasks."""
         nonlocal rot
         assert n_rows % unit == 0
@@ -347,9 +393,25 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
             nrows = cnt * unit
             n_tiles = _ceil_div(nrows, rt)
             per_sm[sm].append([ttype, layer, first * unit, nrows, k, kchunks, rt, ktc,
-                               n_tiles, n_kt, 0, geom, 0, 0, 0, 0])
+                               n_tiles, n_kt, 0, geom, 0, 0, 0, aux])
             emitted += 1
+            if ttype == T_GATEUP and aux:
+                # this SM's K-slice of the down projection: columns first .. first + cnt, all H rows each, column-major;
+                # a ring stage holds `cps` whole columns
+                cps = max(1, sched.stage_bytes // (cfg.hidden * 2))
+                per_sm[sm].append([T_DOWNK, layer, first, cnt, cfg.hidden, cps, 0, 0, 1, _ceil_div(cnt, cps),
+                                   0, 0, 0, 0, 0, 0])
         return emitted
+
+    def hred(layer: int) -> None:
+        """Sum the n_sms partial rows of the fused down projection (+ residual): row quads split over the SMs."""
+        nonlocal rot
+        nquads = cfg.hidden // 4
+        split = split_rows(nquads, n_sms, rot)
+        rot = (rot + nquads % n_sms) % n_sms
+        for sm, (first, cnt) in enumerate(split):
+            if cnt:
+                per_sm[sm].append([T_HRED, layer, first, cnt, cfg.hidden, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0])
 
     for layer in range(cfg.n_layers):
         gemv(T_QKV, layer, cfg.qkv_rows, cfg.hidden, 1)
@@ -366,8 +428,12 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
                 sm = (n_sms - 1 - (b * cfg.n_q_heads + h)) % n_sms
                 per_sm[sm].append([T_MERGE, layer, h, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, b])
         gemv(T_OPROJ, layer, cfg.hidden, cfg.q_dim, 1)
-        gemv(T_GATEUP, layer, 2 * cfg.intermediate, cfg.hidden, 2)
-        gemv(T_DOWN, layer, cfg.hidden, cfg.intermediate, 1)
+        if fuse:
+            gemv(T_GATEUP, layer, 2 * cfg.intermediate, cfg.hidden, 2, aux=1)
+            hred(layer)
+        else:
+            gemv(T_GATEUP, layer, 2 * cfg.intermediate, cfg.hidden, 2)
+            gemv(T_DOWN, layer, cfg.hidden, cfg.intermediate, 1)
     n_lm = gemv(T_LMHEAD, cfg.n_layers, cfg.vocab, cfg.hidden, 1)
 
     # weight offsets: each SM's stream is one contiguous run, SM-major
@@ -380,6 +446,9 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
             if t[F_TYPE] in GEMV_TYPES:
                 t[F_WOFF] = cursor // 16
                 cursor += t[F_B] * t[F_KCHUNKS] * KCHUNK * 2
+            elif t[F_TYPE] == T_DOWNK:
+                t[F_WOFF] = cursor // 16
+                cursor += t[F_B] * t[F_K] * 2
             flat.append(t)
     sm_begin[n_sms] = len(flat)
     if cursor // 16 >= 2 ** 31:
@@ -389,9 +458,10 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
     header = np.zeros(HEADER_INTS, dtype=np.int32)
     header[:13] = [MAGIC, VERSION, n_sms, sched.consumer_warps, sched.n_stage, sched.stage_bytes,
                    tasks.shape[0], batch, sched.inflight, attn_chunks, sched.attn_min_chunk,
-                   scratch_bytes(cfg, sched, batch), n_lm]
+                   scratch_bytes(cfg, sched, batch, n_sms), n_lm]
     header[13] = (cursor // 16) & 0x7FFFFFFF
-    header[14] = (sched.poll_sleep_ns & 0xFFFF) | ((0 if sched.stream_down else 1) << 16) | ((sched.poll_inflight & 0xF) << 20)
+    header[14] = ((sched.poll_sleep_ns & 0xFFFF) | ((0 if sched.stream_down else 1) << 16) | ((sched.poll_inflight & 0xF) << 20)
+                  | ((1 if fuse else 0) << 24))
     header[15] = (sched.l2_prefetch_kb & 0xFFFF) | ((sched.pace_clk_per_64k & 0x7FFF) << 16)
     return TaskTable(cfg=cfg, sched=sched, n_sms=n_sms, batch=batch, header=header, sm_begin=sm_begin,
                      tasks=tasks, packed_weight_bytes=cursor, attn_chunks=attn_chunks)
@@ -456,6 +526,13 @@ def pack_weights_reference(table: TaskTable, weights) -> np.ndarray:
 
     for task in table.tasks:
         ttype = int(task[F_TYPE])
+        if ttype == T_DOWNK:   # columns k0 .. k0 + nk of the down projection, each as H consecutive rows
+            k0, nk = int(task[F_A]), int(task[F_B])
+            pos = int(task[F_WOFF]) * 8
+            src = mat(int(task[F_LAYER]), "wdown")           # [H, I]
+            blk = np.ascontiguousarray(src[:, k0:k0 + nk].T).reshape(-1)
+            out[pos:pos + blk.size] = blk
+            continue
         if ttype not in GEMV_TYPES:
             continue
         layer, vrow0, k = int(task[F_LAYER]), int(task[F_A]), int(task[F_K])

@@ -35,6 +35,12 @@ SCHEDS = {
                              l2_prefetch_kb=32),
     "c7m_nostream": tt.KernelSchedule(consumer_warps=7, n_stage=6, rows_per_tile=28, ktile_chunks=1, attn_min_chunk=16,
                                       stream_down=False),
+    # fused down projection: gate/up keeps its SwiGLU outputs on the SM, multiplies its own K-slice of the down
+    # projection (T_DOWNK) and the partial rows are summed by T_HRED tasks
+    "c7f": tt.KernelSchedule(consumer_warps=7, n_stage=3, rows_per_tile=56, ktile_chunks=2, attn_min_chunk=16,
+                             l2_prefetch_kb=64, inflight=2, fuse_down=True),
+    "c8f": tt.KernelSchedule(consumer_warps=8, n_stage=4, rows_per_tile=16, ktile_chunks=2, attn_min_chunk=8, fuse_down=True),
+    "c4f": tt.KernelSchedule(consumer_warps=4, n_stage=3, rows_per_tile=16, ktile_chunks=1, attn_min_chunk=16, fuse_down=True),
 }
 
 
@@ -58,7 +64,8 @@ def _cos(a, b):
 @pytest.mark.parametrize("cfg,sname", [(TINY, "c8"), (TINY_QWEN3, "c8"), (D128, "c8"), (D128_Q3, "c8"),
                                        (TINY, "c4"), (D128, "c16"), (D128, "c7"), (D128_Q3, "c7"), (TINY_QWEN3, "c7"),
                                        (TINY, "c7s"), (TINY_QWEN3, "c7s"), (D128, "c7m"), (D128_Q3, "c7m"),
-                                       (D128, "c7m_nostream")],
+                                       (D128, "c7m_nostream"), (TINY, "c7f"), (TINY_QWEN3, "c8f"), (D128, "c7f"),
+                                       (D128_Q3, "c7f"), (D128_Q3, "c4f")],
                          ids=lambda v: v if isinstance(v, str) else v.name)
 def test_stepwise_logits_match_oracle(cfg, sname):
     """Teacher-forced: 40 steps (crossing the single-chunk -> split-KV boundary),
@@ -87,9 +94,9 @@ def test_stepwise_logits_match_oracle(cfg, sname):
     plug.close()
 
 
-@pytest.mark.parametrize("cfg", [TINY, D128_Q3], ids=lambda c: c.name)
-def test_device_packer_is_bit_exact(cfg):
-    w, _, plug = _setup(cfg, SCHEDS["c8"])
+@pytest.mark.parametrize("cfg,sname", [(TINY, "c8"), (D128_Q3, "c8"), (D128_Q3, "c7f")], ids=lambda v: v if isinstance(v, str) else v.name)
+def test_device_packer_is_bit_exact(cfg, sname):
+    w, _, plug = _setup(cfg, SCHEDS[sname])
     want = tt.pack_weights_reference(plug.table, w)
     got = plug.packed[:plug.table.packed_weight_bytes].cpu().numpy().view(np.uint16)
     assert (got == want).all()

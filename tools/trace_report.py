@@ -45,7 +45,7 @@ def report(plug, tr):
     t0 = tr[ran][:, 0].min()
     rel = (tr.astype(np.float64) - float(t0)) / 1e3  # us
     L = plug.cfg.n_layers
-    order = [tt.T_QKV, tt.T_ATTN, tt.T_MERGE, tt.T_OPROJ, tt.T_GATEUP, tt.T_DOWN]
+    order = [tt.T_QKV, tt.T_ATTN, tt.T_MERGE, tt.T_OPROJ, tt.T_GATEUP, tt.T_DOWN, tt.T_DOWNK, tt.T_HRED]
     print(f"step total (first stamp -> last end): {rel[ran][:, 7].max():.1f} us")
     acc = {}
     prev_end = 0.0
@@ -55,7 +55,7 @@ def report(plug, tr):
             if not m.any():
                 continue
             r = rel[m]
-            gathered = r[:, 1] if ty != tt.T_MERGE else r[:, 0]
+            gathered = r[:, 1] if ty not in (tt.T_MERGE, tt.T_DOWNK) else r[:, 0]
             end = r[:, 7]
             d = dict(phase=end.max() - prev_end,                 # critical-path length of the op
                      first_in=gathered.min() - prev_end,         # first SM has its inputs after the previous op ended
