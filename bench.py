@@ -46,7 +46,7 @@ sys.path.insert(0, str(ROOT))
 import torch
 
 from paper_2605_11581_b200.model_config import get_config
-from paper_2605_11581_b200.schedules import default_schedule
+from paper_2605_11581_b200.schedules import default_schedule, schedule_id
 from paper_2605_11581_b200.weights import random_weights, rope_table
 
 METRIC = "decode_tokens_per_s"
@@ -128,7 +128,10 @@ def base_line(args, cfg, n_gpus: int) -> dict:
                        "model": cfg.name, "batch": 1,
                        "prompt_len": PROMPT_LEN, "parallelism": "replicas" if n_gpus > 1 else "single",
                        "l2_policy": f"inputs larger than L2: every step streams the "
-                                    f"{cfg.weight_bytes_per_token() / 1e9:.2f} GB weight set"}}
+                                    f"{cfg.weight_bytes_per_token() / 1e9:.2f} GB weight set",
+                       # the solidified schedule the workload is decoded with (mkplan search output; both arms name it so
+                       # that their config objects are identical -- the CPU arm itself has no schedule)
+                       "schedule": schedule_id(cfg)}}
 
 
 def run_reference(args) -> None:
@@ -314,10 +317,11 @@ def run_ours(args) -> None:
     ctx_mid = PROMPT_LEN + args.warmup + args.steps // 2
     bytes_per_launch = cfg_bytes.algorithmic_bytes(ctx_mid) // tp   # per rank: one kernel streams 1/tp of the model
     achieved = bytes_per_launch / (ms * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     tfile = ROOT / "profiles" / "traffic.json"
-    if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+    if tfile.exists():   # dram__bytes_read + write of one launch from an `ncu --set full` capture (not measurable inside this run)
+        tj = json.loads(tfile.read_text())
+        traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
     line = base_line(args, full_cfg, world)
     jobs = 1 if tp > 1 else world               # tensor parallel: one sequence; replicas: one per GPU
     if tp > 1:
@@ -325,14 +329,14 @@ def run_ours(args) -> None:
         line["config"]["parallelism"] = f"tp{tp} (in-kernel NVLink peer stores)"
     line.update({
         "value": jobs * 1e3 / ms, "ms_per_step": ms,
-        "config": dict(line["config"], schedule={"consumer_warps": sched.consumer_warps, "n_stage": sched.n_stage,
-                                                 "stage_bytes": sched.stage_bytes}, n_sms=plug.n_sms),
+        "kernel": {"consumer_warps": sched.consumer_warps, "n_stage": sched.n_stage, "stage_bytes": sched.stage_bytes,
+                   "inflight": sched.inflight, "fuse_down": sched.fuse_down, "n_sms": plug.n_sms},
         "e2e": {"value": jobs * 1e3 / ms_e2e, "unit": UNIT, "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 4,
                 "ms_per_step": ms_e2e},
         "gpu_launches": launches,
         "clocks": clocks,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_kind": f"{peak_kind} copy bandwidth (burst)",
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_kind": f"{peak_kind} copy bandwidth (burst)",
                      "algorithmic_bytes_per_launch": bytes_per_launch, "kernel": "adamk_decode_kernel",
                      "launch_ms": ms},
     })
@@ -361,6 +365,17 @@ def main() -> None:
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        # `python bench.py --gpus N` outside torchrun: spawn the N ranks ourselves, one per GPU, NCCL rendezvous on
+        # 127.0.0.1 (the driver's own launch line, reproduced)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+        raise SystemExit(subprocess.run(cmd).returncode)
     if args.impl == "reference":
         run_reference(args)
     else:

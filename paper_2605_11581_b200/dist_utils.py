@@ -66,9 +66,9 @@ def share_workspaces(group: RankGroup, workspace: torch.Tensor) -> list[torch.Te
     Each rank exports its workspace allocation as a CUDA IPC handle (``UntypedStorage._share_cuda_``), the
     handles are all-gathered as Python objects, and every rank opens its peers' handles
     (``cudaIpcOpenMemHandle`` with lazy peer access).  Returns uint8 tensors in rank order, this rank's own
-    tensor at index ``group.rank``; keep them alive as long as the plugin runs.  NOT exercised in this
-    repository's tests (they run on one GPU, where the ranks of tools/tp_single_gpu.py share an address
-    space); the kernel side of the exchange is."""
+    tensor at index ``group.rank``; keep them alive as long as the plugin runs.  Exercised on hardware by
+    tools/tp_two_process.py (tests/test_gpu_decode.py::test_tensor_parallel_across_processes_with_ipc_workspaces):
+    two processes, IPC handles over gloo, in-kernel exchange across the two address spaces."""
     if group.world == 1:
         return [workspace]
     assert workspace.is_cuda and workspace.dtype == torch.uint8 and workspace.is_contiguous()

@@ -10,7 +10,6 @@ target GPU is how the paper locks in its trace).
 
 from __future__ import annotations
 
-import json
 from pathlib import Path
 
 from .model_config import ModelConfig
@@ -29,15 +28,28 @@ PROFILED_DEFAULT = dict(consumer_warps=7, rows_per_tile=42, ktile_chunks=2, attn
 
 
 def default_schedule(cfg: ModelConfig, n_sms: int = 148, tp_size: int = 1) -> KernelSchedule:
-    plan_file = SCHEDULE_DIR / f"{cfg.name}.trace.json"
-    if plan_file.exists():
-        plan = json.loads(plan_file.read_text())["plan"]
-        sched = KernelSchedule.from_plan(plan)
-        fit = max_stages_that_fit(cfg, sched, n_sms=n_sms)
-        if sched.n_stage > fit:
-            sched = KernelSchedule.from_plan(plan, n_stage=fit)
-        return sched
+    """The model's shipped SolidifiedTrace (``schedules/<model>.trace.json``, written by ``mkplan search`` through
+    ``tools/make_schedules.py``) lowered to the kernel; models without one fall back to the profiled default."""
+    from .solidify import schedule_from_trace, shipped_trace
+
+    shipped = shipped_trace(cfg)
+    if shipped is not None:
+        trace, knobs, _ = shipped
+        return schedule_from_trace(cfg, trace, knobs, n_sms, tp_size)
     return fit_schedule(cfg, KernelSchedule(n_stage=2, **PROFILED_DEFAULT), n_sms, tp_size)
+
+
+def schedule_id(cfg: ModelConfig) -> dict:
+    """What the bench line reports about the schedule in use."""
+    from .solidify import shipped_trace
+
+    shipped = shipped_trace(cfg)
+    if shipped is None:
+        return {"source": "profiled default (no solidified trace shipped for this model)"}
+    trace, knobs, order = shipped
+    return {"source": f"mkplan search -> schedules/{cfg.name}.trace.json", "content_hash": trace.content_hash,
+            "tile": trace.plan["tile"], "plan_n_stage": trace.plan["n_stage"], "stride_eff": trace.plan["stride_eff"],
+            "kernel_knobs": knobs, "program_order_checked": order is not None}
 
 
 def fit_schedule(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, tp_size: int = 1) -> KernelSchedule:

@@ -115,25 +115,66 @@ class KernelSchedule:
         return self.rows_per_tile * self.ktile_chunks * KCHUNK * 2
 
     @classmethod
-    def from_plan(cls, plan: dict, **overrides) -> "KernelSchedule":
-        """Read the ring parameters out of ``SolidifiedTrace.plan``.
+    def from_plan(cls, plan: dict, cfg: "ModelConfig | None" = None, n_sms: int = 148, **overrides) -> "KernelSchedule":
+        """Lower ``SolidifiedTrace.plan`` (reference ``search.py:138-171``) to the kernel's pipeline parameters.
 
-        tile = [block_m, block_n, block_k, k_split]; sub_k = block_k / k_split.
-        The ring depth is the plan's ``n_stage`` (the window of
-        ``n_stage * per_stage`` pages, reference ``planner.py:415``); the
-        prefetch stride (``stride_eff``) bounds the stages in flight."""
+        * ``tile`` = [block_m, block_n, block_k, k_split]: a ring stage holds ``rows x sub_k`` weights with
+          ``sub_k = block_k / k_split`` and ``rows`` the rows a grid of ``consumer_warps`` warps covers inside the plan
+          tile with an even number of rows per warp (gate/up pairs stay in one warp): ``block_n`` rounded down to a
+          multiple of ``2 * consumer_warps``, halved while a warp would hold more than eight rows.
+        * ``stride_eff``: the planner lets fill ``j`` issue once iteration ``j - stride_eff`` has started (reference
+          ``planner.py:583-613``), i.e. ``stride_eff + 1`` stages are in flight at most -> the Loader's ``inflight`` cap.
+        * ``n_stage`` / ``per_stage`` / ``window`` / ``pages_required``: the plan is valid on any ring that holds its
+          window of ``n_stage`` stages.  The ring's real depth comes from Eq.1 / Eq.2 (reference ``hwmodel.py:207-237``)
+          evaluated on the kernel's own shared-memory accounting (``ring_depth``) when ``cfg`` is given; a plan whose
+          window does not fit is rejected.
+        Run-time knobs the planner does not model (split-KV chunk, L2 prefetch window, fused down projection) come as
+        ``overrides``."""
         bm, bn, bk, ks = plan["tile"]
         sub_k = bk // ks
         if sub_k % KCHUNK:
             raise ScheduleError(f"sub_k={sub_k} is not a multiple of {KCHUNK}")
         c = int(plan["consumer_warps"])
-        # a plan tile taller than the kernel's eight rows per warp is executed as several kernel tiles
-        rows = int(bn)
-        while rows > MAX_RW * c:
+        rows = (int(bn) // (2 * c)) * 2 * c
+        if rows < 2 * c:
+            raise ScheduleError(f"block_n={bn} holds fewer than two rows per consumer warp")
+        while rows > MAX_RW * c:     # a plan tile taller than eight rows per warp is executed as several kernel tiles
             rows //= 2
-        kw = dict(consumer_warps=c, n_stage=int(plan["n_stage"]), rows_per_tile=rows, ktile_chunks=sub_k // KCHUNK)
+            rows -= rows % (2 * c)
+        n_plan = int(plan["n_stage"])
+        window, per_stage = int(plan.get("window", 0)), int(plan.get("per_stage", 0))
+        if window and per_stage and window != n_plan * per_stage:
+            raise ScheduleError("plan window is not n_stage * per_stage pages")
+        if "pages_required" in plan and window and int(plan["pages_required"]) < window:
+            raise ScheduleError("plan pages_required is smaller than its stream window")
+        kw = dict(consumer_warps=c, n_stage=n_plan, rows_per_tile=rows, ktile_chunks=sub_k // KCHUNK,
+                  inflight=min(n_plan, int(plan.get("stride_eff", n_plan - 1)) + 1))
         kw.update(overrides)
-        return cls(**kw)
+        sched = cls(**kw)
+        if cfg is not None and "n_stage" not in overrides:
+            depth = ring_depth(cfg, sched, n_sms=n_sms)
+            if depth < n_plan:
+                raise ScheduleError(f"the plan's window of {n_plan} stages does not fit the kernel's ring (Eq.2 gives {depth})")
+            depth = min(depth, 8)
+            sched = cls(**dict(kw, n_stage=depth, inflight=min(kw["inflight"], depth)))
+        return sched
+
+
+RING_PAGE = 1024   # the kernel carves its ring out of shared memory in 1 KB pages (stage_bytes % 1024 == 0)
+
+
+def ring_depth(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1, n_sms: int = 148) -> int:
+    """Ring depth by the paper's constraint model on the kernel's own numbers: Eq.1 gives the pages left after the
+    per-CTA overhead (instruction buffer = task cache, semaphores = barrier header, scratch), Eq.2 divides them by
+    the pages one stage occupies (reference ``hwmodel.py:207-237``, ``PAPER.md:99-109``)."""
+    from .mkplan.hwmodel import HardwareSpec, compute_page_budget, compute_stage_count
+
+    spec = HardwareSpec(smem_max=SMEM_MAX, page_size=RING_PAGE,
+                        instr_buf=task_cache_bytes(cfg, batch, n_sms, sched.fuse_down), semaphores=SMEM_RESERVED,
+                        scratch=scratch_bytes(cfg, sched, batch, n_sms))
+    total = compute_page_budget(spec, 1)                 # the overhead is per CTA, not per stage: N_stage = 1 in Eq.1
+    per_stage = _ceil_div(sched.stage_bytes, RING_PAGE)
+    return min(MAX_STAGES, compute_stage_count(total, 0, 0, 0, per_stage))
 
 
 def pace_for(hbm_gbs: float, n_sms: int = 148, sm_mhz: float = 1965.0) -> int:
@@ -187,9 +228,7 @@ def task_cache_bytes(cfg: ModelConfig, batch: int = 1, n_sms: int = 148, fused: 
 
 
 def max_stages_that_fit(cfg: ModelConfig, sched: KernelSchedule, batch: int = 1, n_sms: int = 148) -> int:
-    free = (SMEM_MAX - SMEM_RESERVED - task_cache_bytes(cfg, batch, n_sms, sched.fuse_down)
-            - scratch_bytes(cfg, sched, batch, n_sms))
-    return max(0, min(MAX_STAGES, free // sched.stage_bytes))
+    return ring_depth(cfg, sched, batch, n_sms)
 
 
 def fuse_down_error(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, tp_size: int = 1) -> str | None:

@@ -250,6 +250,23 @@ def test_repeated_runs_are_bitwise_reproducible():
     assert torch.equal(outs[0], outs[1])
 
 
+def test_tensor_parallel_across_processes_with_ipc_workspaces():
+    """The start-up path of a multi-GPU tensor-parallel run, on hardware: two PROCESSES exchange the CUDA IPC handles
+    of their workspaces through torch.distributed (dist_utils.share_workspaces), map each other's buffers and then
+    publish partial rows into them from inside the kernel (system-scope tagged words across address spaces).  With one
+    GPU in the box the ranks share it (74 SMs each; the two contexts are time-sliced).  Logits are checked against the
+    unsharded oracle and the ranks must agree on every token (tools/tp_two_process.py)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    res = subprocess.run([sys.executable, str(root / "tools" / "tp_two_process.py"), "2", "4"],
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+    assert "tp_two_process ok: tp=2 ranks in 2 processes" in res.stdout
+
+
 @pytest.mark.parametrize("tp", [2, 4])
 def test_tensor_parallel_ranks_on_one_gpu(tp):
     """In-kernel tensor parallelism (adamk.cu: tp_publish / ll_gather_tp / tp_argmax_exchange): `tp` ranks with
