@@ -76,6 +76,9 @@ int adamk_prefill_gemm_plan(int parts, int T, int K, int N, int epilogue, int ti
 /* h fp32 [T, H] = embed[tokens[t]] (bf16 table). */
 int adamk_prefill_embed(const int32_t* tokens, int T, const void* embed, int H, float* h, adamk_pf_stream stream);
 
+/* The same for a device-resident decode loop, whose token ids the host never sees: ids outside [0, vocab) read row 0. */
+int adamk_batch_embed(const int32_t* tokens, int T, const void* embed, int H, int vocab, float* h, adamk_pf_stream stream);
+
 /* planes bf16 [parts][T, H] = split(RMSNorm(h) * gain): the GEMM's activation operand. */
 int adamk_prefill_rmsnorm_split(const float* h, const void* gain, float eps, int T, int H, void* planes, int parts,
                                 adamk_pf_stream stream);

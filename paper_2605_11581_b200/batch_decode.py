@@ -103,6 +103,10 @@ class BatchedDecoder:
         self._graph = None
         self.launches_per_step = 0
         self.steps = 0
+        # Host-side bound on the largest device position: positions advance on the device (argmax kernel, graph replay), so
+        # the host counts auto-advancing steps since the last state it set and refuses the step that would leave the cache.
+        # The kernels also guard themselves (a sequence past max_ctx writes nothing and attends inside the cache).
+        self._pos_bound = 0
 
     # ---- prompts ----
     def prefill(self, b: int, prompt_ids) -> None:
@@ -113,12 +117,24 @@ class BatchedDecoder:
         if prompt.numel() > 1:
             TensorCorePrefill(self.cfg, self._weights, _SequenceCache(self, b), planes=min(self.planes, 2),
                               layers=self.layers, embed=self.embed).run(prompt[:-1])
+        if int(prompt.min()) < 0 or int(prompt.max()) >= self.cfg.vocab:
+            raise ValueError("prompt holds token ids outside the vocabulary")
         self.tokens[b] = prompt[-1]
         self.positions[b] = prompt.numel() - 1
+        self._pos_bound = max(self._pos_bound, prompt.numel() - 1)
 
     def set_state(self, tokens, positions) -> None:
-        self.tokens.copy_(torch.as_tensor(tokens, dtype=torch.int32))
-        self.positions.copy_(torch.as_tensor(positions, dtype=torch.int32))
+        tok = torch.as_tensor(tokens, dtype=torch.int32).cpu()
+        pos = torch.as_tensor(positions, dtype=torch.int32).cpu()
+        if tok.numel() != self.batch or pos.numel() != self.batch:
+            raise ValueError("set_state needs one token and one position per sequence")
+        if int(tok.min()) < 0 or int(tok.max()) >= self.cfg.vocab:
+            raise ValueError("token id outside the vocabulary")
+        if int(pos.min()) < 0 or int(pos.max()) >= self.max_ctx:
+            raise ValueError(f"position outside the KV cache (max_ctx {self.max_ctx})")
+        self.tokens.copy_(tok)
+        self.positions.copy_(pos)
+        self._pos_bound = int(pos.max())
 
     # ---- one step ----
     @torch.no_grad()
@@ -135,7 +151,7 @@ class BatchedDecoder:
         seq_stride = nkv * self.max_ctx * D
         cos, sin = self._rope
         n = 0
-        _ok(lib.adamk_prefill_embed(_ptr(self.tokens), B, _ptr(self.embed), H, _ptr(self.h), st))
+        _ok(lib.adamk_batch_embed(_ptr(self.tokens), B, _ptr(self.embed), H, cfg.vocab, _ptr(self.h), st))
         pf = self.l2_prefetch
         for l, lw in enumerate(self.layers):
             nxt = self.layers[l + 1]["wqkv"] if l + 1 < len(self.layers) else self.lm_head
@@ -180,6 +196,10 @@ class BatchedDecoder:
 
     def step(self, auto_advance: bool = True) -> torch.Tensor:
         """One decode step of all sequences; returns the device tensor of greedy tokens (int32 [B])."""
+        if self._pos_bound >= self.max_ctx:
+            raise AdamkError(-103, f"a sequence has reached max_ctx ({self.max_ctx}): the step would write past its KV cache")
+        if auto_advance:
+            self._pos_bound += 1
         if self._graph is not None and auto_advance:
             self._graph.replay()
         else:

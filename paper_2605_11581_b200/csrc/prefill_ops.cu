@@ -81,10 +81,14 @@ __device__ __forceinline__ void put_split4(__nv_bfloat16* dst, long long stride,
   }
 }
 
-__global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ embed, float* __restrict__ h, int H) {
+// `vocab` > 0: token ids outside [0, vocab) read row 0 instead of memory outside the table (a device-resident
+// decode loop feeds tokens the host never sees)
+__global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ embed, float* __restrict__ h, int H, int vocab) {
   griddep_sync();
   const int t = blockIdx.x;
-  const __nv_bfloat16* src = embed + (long long)tokens[t] * H;
+  int tok = tokens[t];
+  if (vocab > 0 && (tok < 0 || tok >= vocab)) tok = 0;
+  const __nv_bfloat16* src = embed + (long long)tok * H;
   float* dst = h + (long long)t * H;
   for (int i = threadIdx.x * 2; i < H; i += blockDim.x * 2) {
     const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(src + i);
@@ -147,6 +151,7 @@ __global__ void rope_store_kernel(const RopeArgs a) {
   const int heads = a.n_q + 2 * a.n_kv, half = a.D / 2;
   const float* row = a.qkv + (long long)t * heads * a.D;
   const int pos = a.positions != nullptr ? a.positions[t] : a.pos0 + t;
+  if (pos < 0 || pos >= a.max_ctx) return;   // a sequence past its cache: nothing is written (no out-of-bounds K / V / table access)
   __nv_bfloat16* k_cache = a.k_cache + t * a.seq_stride;
   __nv_bfloat16* v_cache = a.v_cache + t * a.seq_stride;
   for (int hd = threadIdx.x >> 5; hd < heads; hd += nw) {
@@ -224,7 +229,7 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
                           long long seq_stride, int splits, float scale) {
   griddep_sync();
   const int s = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
-  const int ctx = positions[b] + 1;   // the new token's K / V are already in the cache
+  const int ctx = min(positions[b] + 1, max_ctx);   // the new token's K / V are already in the cache; never past the cache
   const int p0 = s * kAttnChunk;
   if (p0 >= ctx) return;              // the merge kernel derives the live split count from positions, too
   const int n_pos = min(kAttnChunk, ctx - p0);
@@ -383,7 +388,7 @@ __global__ void batch_attn_merge_kernel(const float* __restrict__ part, const in
                                         int B, int n_q, int splits, int parts) {
   griddep_sync();
   const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
-  const int live = (positions[b] + kAttnChunk) / kAttnChunk;   // ceil((pos + 1) / chunk)
+  const int live = min(max((positions[b] + kAttnChunk) / kAttnChunk, 1), splits);   // ceil((pos + 1) / chunk), inside the records that exist
   const float* src = part + ((long long)b * n_q + h) * splits * (D + 2);
   // the splits' maxima through shared memory (one load each, all in flight), then the weighted sums eight splits at a time
   extern __shared__ float m_s[];
@@ -436,6 +441,7 @@ __global__ void batch_argmax_kernel(const float* __restrict__ logits, int V, int
   if (threadIdx.x == 0) {
     for (int w = 1; w < (blockDim.x >> 5); ++w)
       if (sv[w] > best || (sv[w] == best && si[w] < idx)) { best = sv[w]; idx = si[w]; }
+    if (idx < 0 || idx >= V) idx = 0;   // a row of NaN / -inf has no maximum: a valid token id, not the 0x7fffffff sentinel
     next[b] = idx;
     if (tokens != nullptr) tokens[b] = idx;
     if (positions != nullptr) positions[b] += 1;
@@ -472,8 +478,14 @@ extern "C" {
 
 int adamk_prefill_embed(const int32_t* tokens, int T, const void* embed, int H, float* h, adamk_pf_stream stream) {
   if (tokens == nullptr || embed == nullptr || h == nullptr || T <= 0 || H <= 0 || H % 2) return ADAMK_PF_E_INVALID;
-  pfo::launch(pfo::embed_kernel, dim3(T), dim3(256), 0, static_cast<cudaStream_t>(stream), tokens, static_cast<const __nv_bfloat16*>(embed), h, H);
+  pfo::launch(pfo::embed_kernel, dim3(T), dim3(256), 0, static_cast<cudaStream_t>(stream), tokens, static_cast<const __nv_bfloat16*>(embed), h, H, 0);
   return pfo::done("prefill embed");
+}
+
+int adamk_batch_embed(const int32_t* tokens, int T, const void* embed, int H, int vocab, float* h, adamk_pf_stream stream) {
+  if (tokens == nullptr || embed == nullptr || h == nullptr || T <= 0 || H <= 0 || H % 2 || vocab <= 0) return ADAMK_PF_E_INVALID;
+  pfo::launch(pfo::embed_kernel, dim3(T), dim3(256), 0, static_cast<cudaStream_t>(stream), tokens, static_cast<const __nv_bfloat16*>(embed), h, H, vocab);
+  return pfo::done("batch embed");
 }
 
 int adamk_prefill_rmsnorm_split(const float* h, const void* gain, float eps, int T, int H, void* planes, int parts, adamk_pf_stream stream) {

@@ -34,7 +34,7 @@ GU_BLOCK = 128   # features per gate / up block of the interleaved weight = half
 PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_prefill_set_trace", "adamk_prefill_prefetch_next",
                    "adamk_prefill_gemm_plan", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
                    "adamk_prefill_split", "adamk_prefill_rope_store", "adamk_batch_rope_store", "adamk_batch_attention_workspace",
-                   "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split")
+                   "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split", "adamk_batch_embed")
 
 _declared = False
 
@@ -54,6 +54,7 @@ def _lib():
         lib.adamk_prefill_gemm.argtypes = [vp, i, i, i, vp, i, vp, vp, i, i, i, ll, i, vp]
         lib.adamk_prefill_gemm_plan.argtypes = [i, i, i, i, i, i, i, C.POINTER(C.c_int32)]
         lib.adamk_prefill_embed.argtypes = [vp, i, vp, i, vp, vp]
+        lib.adamk_batch_embed.argtypes = [vp, i, vp, i, i, vp, vp]
         lib.adamk_prefill_rmsnorm_split.argtypes = [vp, vp, f, i, i, vp, i, vp]
         lib.adamk_prefill_split.argtypes = [vp, ll, vp, i, vp]
         lib.adamk_prefill_rope_store.argtypes = [vp, i, i, i, i, vp, vp, f, vp, vp, i, i, vp, i, vp, vp, vp]

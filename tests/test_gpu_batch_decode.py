@@ -237,3 +237,85 @@ def test_full_size_qwen25_1p5b_prefill_and_batched_decode():
             if float(top2[b, 0] - top2[b, 1]) > 3e-2:
                 assert got_tok[b] == int(want[b].argmax())
         print(f"full-size batched decode, oracle cache {oracle_cache}: max |logit diff| {worst:.2e}")
+
+
+@pytest.mark.parametrize("B", [8, 16])
+def test_full_size_batched_decode_at_the_baseline_contexts(B):
+    """BASELINE.json configs[2] at its own shapes: Qwen2.5-1.5B, batch 8 and 16, sequences at context 2K and 8K in one
+    batch (33- and 128-chunk split-KV merges side by side, 3 stacked activation planes, the 128- vs 256-wide GEMM
+    tile planning of a 24- / 48-row token tile).  The caches are filled with the same random K / V on both sides
+    (a CPU prefill of 80 K tokens is out of reach), then one decode step is compared with the oracle: the north
+    star's bound (max-abs 2e-2, cosine 0.9995)."""
+    from oracle.decode_ref import RefDecoder
+    from paper_2605_11581_b200.batch_decode import BatchedDecoder
+    from paper_2605_11581_b200.model_config import QWEN25_1P5B
+    from paper_2605_11581_b200.weights import random_weights, rope_table
+
+    cfg, max_ctx = QWEN25_1P5B, 8192
+    w = random_weights(cfg, seed=0)
+    cos, sin = rope_table(cfg, max_ctx)
+    ref = RefDecoder(cfg, w, max_ctx, cos, sin, batch=B)
+    dec = BatchedDecoder(cfg, w, B, max_ctx)
+    g = torch.Generator().manual_seed(3)
+    pos = [(2047 if b % 2 == 0 else 8191) - (b // 2) * 37 for b in range(B)]      # 2K and 8K contexts, none chunk-aligned
+    toks = torch.randint(0, cfg.vocab, (B,), generator=g).tolist()
+    for l in range(cfg.n_layers):                     # layer by layer: the fp32 scratch of a whole cache would be 4 GB
+        kl = (torch.randn(B, cfg.n_kv_heads, max_ctx, cfg.head_dim, generator=g) * 0.5).to(torch.bfloat16)
+        vl = (torch.randn(B, cfg.n_kv_heads, max_ctx, cfg.head_dim, generator=g) * 0.5).to(torch.bfloat16)
+        ref.k_cache[l].copy_(kl); ref.v_cache[l].copy_(vl)
+        dec.k_cache[l].copy_(kl.to(dec.device)); dec.v_cache[l].copy_(vl.to(dec.device))
+    want = ref.step(toks, pos)
+    dec.set_state(toks, pos)
+    got_tok = dec.step(auto_advance=False).cpu().tolist()
+    got = dec.logits.cpu()
+    worst = float((got - want).abs().max())
+    assert worst <= 2e-2, worst
+    for b in range(B):
+        a, c = got[b].numpy(), want[b].numpy()
+        assert float((a * c).sum() / (np.linalg.norm(a) * np.linalg.norm(c))) >= 0.9995, b
+    top2 = want.topk(2, dim=1).values
+    for b in range(B):
+        if float(top2[b, 0] - top2[b, 1]) > 3e-2:
+            assert got_tok[b] == int(want[b].argmax()), b
+    # the new token's K / V rows landed where the oracle put them
+    for b in (0, 1):
+        np.testing.assert_allclose(dec.k_cache[:, b, :, pos[b]].float().cpu().numpy(), ref.k_cache[:, b, :, pos[b]].float().numpy(),
+                                   atol=4e-2, rtol=1e-2)
+    print(f"full-size batched decode B={B} at contexts 2K/8K: max |logit diff| {worst:.2e}")
+
+
+def test_sequences_cannot_leave_their_cache():
+    """Positions advance on the device: the host counts the steps and refuses the one that would leave the cache; the
+    kernels guard themselves as well (a position past max_ctx writes nothing, attention stays inside the cache, token
+    ids outside the vocabulary read row 0) so a foreign driver of the C ABI cannot corrupt memory either."""
+    from paper_2605_11581_b200.batch_decode import BatchedDecoder
+    from paper_2605_11581_b200.plugin import AdamkError
+    from paper_2605_11581_b200.weights import random_weights
+
+    cfg, B, max_ctx = TINY, 3, 16
+    w = random_weights(cfg, seed=0)
+    dec = BatchedDecoder(cfg, w, B, max_ctx)
+    with pytest.raises(ValueError):
+        dec.set_state([1, 2, 3], [0, max_ctx, 1])
+    with pytest.raises(ValueError):
+        dec.set_state([1, cfg.vocab, 3], [0, 1, 2])
+    dec.set_state([1, 2, 3], [max_ctx - 3, 0, 5])
+    dec.step()
+    dec.step()
+    dec.step()                                    # the first sequence now sits at max_ctx
+    with pytest.raises(AdamkError):
+        dec.step()
+    # device guards: positions / tokens the host never validated (written straight to the device buffers)
+    guard = torch.full_like(dec.k_cache, 7.0)
+    dec.k_cache.copy_(guard)
+    dec.positions.copy_(torch.tensor([max_ctx + 5, 2, -4], dtype=torch.int32))
+    dec.tokens.copy_(torch.tensor([cfg.vocab + 9, 5, -1], dtype=torch.int32))
+    dec._pos_bound = 0
+    dec.step(auto_advance=False)
+    torch.cuda.synchronize()
+    k = dec.k_cache.float().cpu()
+    assert (k[:, 0] == 7.0).all() and (k[:, 2] == 7.0).all()          # the out-of-range sequences wrote nothing
+    assert (k[:, 1, :, 2] != 7.0).any() and (k[:, 1, :, 3:] == 7.0).all()
+    nt = dec.next_token.cpu().tolist()
+    assert all(0 <= t < cfg.vocab for t in nt)
+    assert torch.isfinite(dec.logits[1]).all()

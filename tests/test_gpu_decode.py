@@ -420,8 +420,9 @@ def test_full_size_qwen25_1p5b_matches_oracle():
 
 def test_qwen25_1p5b_greedy_64_tokens_identical():
     """North-star criterion on BASELINE.json configs[1]: after the 512-token prompt of bench.py, 64 free-running
-    greedy steps of the kernel (device-resident loop, one launch per token) emit the oracle's tokens; compared up
-    to the first step whose top-2 margin in the oracle is a near-tie (< 1e-3), which must not come early."""
+    greedy steps of the kernel (device-resident loop, one launch per token) emit the oracle's tokens -- all 64, no
+    near-tie escape: the prompt seed is chosen so that the oracle's own top-1 / top-2 margin never comes near the logit
+    tolerance (the minimum margin is printed)."""
     from oracle.decode_ref import RefDecoder
     from paper_2605_11581_b200.model_config import QWEN25_1P5B
     from paper_2605_11581_b200.plugin import MegaKernelPlugin
@@ -432,7 +433,9 @@ def test_qwen25_1p5b_greedy_64_tokens_identical():
     w = random_weights(cfg, seed=0)
     cos, sin = rope_table(cfg, 640)
     ref = RefDecoder(cfg, w, 640, cos, sin)
-    g = torch.Generator().manual_seed(1)
+    # prompt seed 3: the oracle's own top-1 / top-2 margin stays >= 1.0e-2 over all 64 steps (seeds 1..8 scanned on the
+    # CPU oracle; 1, 2 and 4 dip below 5e-3) -- five times the 2e-3 logit tolerance
+    g = torch.Generator().manual_seed(3)
     prompt = torch.randint(0, cfg.vocab, (512,), generator=g).tolist()
     logits = ref.prefill(prompt)
     plug = MegaKernelPlugin(cfg, default_schedule(cfg), max_ctx=640)
@@ -458,9 +461,9 @@ def test_qwen25_1p5b_greedy_64_tokens_identical():
     plug.check()
     got = [int(t.item()) for t in outs]
     margins = np.asarray(margins)
-    first_tie = int(np.argmax(margins < 1e-3)) if (margins < 1e-3).any() else 64
-    assert got[:first_tie] == want[:first_tie]
-    assert first_tie >= 32, f"near-tie at step {first_tie}"
+    print(f"greedy 64: minimum top-1/top-2 margin of the oracle {margins.min():.2e} at step {int(margins.argmin())}")
+    assert margins.min() >= 5e-3, "the documented prompt seed no longer keeps the margins clear of the tolerance"
+    assert got == want
     plug.close()
 
 
@@ -490,3 +493,78 @@ def test_hybrid_engine_library_prefill_matches_oracle():
     assert res.tokens[:first_tie] == want[:first_tie] and first_tie >= 12
     assert res.prefill_launches == 0 and res.decode_launches == 24
     eng.close()
+
+
+def test_full_size_qwen3_8b_matches_oracle_tp1_and_tp2():
+    """BASELINE.json configs[3] at full size (Qwen3-8B: H 4096, 32/8 heads, I 12288, QK-norm, untied 151 936-row LM
+    head, 36 layers, 15 GB of weights): per-step logits of the MegaKernel against the CPU oracle, first as one rank
+    with all 148 SMs (the fused down projection: three 256-row blocks per warp), then as two tensor-parallel ranks of
+    74 SMs each on the one GPU (heads / intermediate / vocabulary split, in-kernel partial-row exchange).
+
+    Tolerance: the north star's (max-abs 2e-2, cosine 0.9995).  Both sides keep fp32 activations, but the KV cache is
+    bf16 on both: with 1024 V elements per layer a few land within one fp32 ulp of a bf16 rounding boundary, the two
+    summation orders round them to neighbouring bf16 values (measured: one 7.8e-3 flip in layer 0), and 36 layers
+    carry that to ~1e-2 in the logits -- fused and unfused schedules give the same numbers (tools/dbg_8b.py)."""
+    from oracle.decode_ref import RefDecoder
+    from paper_2605_11581_b200.model_config import QWEN3_8B
+    from paper_2605_11581_b200.plugin import MegaKernelPlugin, device_sm_count
+    from paper_2605_11581_b200.schedules import default_schedule
+    from paper_2605_11581_b200.weights import random_weights, rope_table
+
+    cfg, max_ctx, steps = QWEN3_8B, 32, 4
+    w = random_weights(cfg, seed=0)
+    cos, sin = rope_table(cfg, max_ctx)
+    ref = RefDecoder(cfg, w, max_ctx, cos, sin)
+    g = torch.Generator().manual_seed(1)
+    toks = torch.randint(0, cfg.vocab, (steps,), generator=g).tolist()
+    wants = [ref.step([tok], [pos])[0].numpy() for pos, tok in enumerate(toks)]
+    del ref
+
+    sched = default_schedule(cfg)
+    assert sched.fuse_down
+    plug = MegaKernelPlugin(cfg, sched, max_ctx=max_ctx)
+    plug.bind_weights(w)
+    for pos, tok in enumerate(toks):
+        out = plug.decode_step(tok, pos, want_logits=True)
+        plug.check()
+        got = out.logits[0].cpu().numpy()
+        err = float(np.abs(got - wants[pos]).max())
+        assert err <= 2e-2, (pos, err)
+        assert _cos(got, wants[pos]) >= 0.9995
+        srt = np.sort(wants[pos])
+        if srt[-1] - srt[-2] > 5e-2:
+            assert int(out.next_token.item()) == int(wants[pos].argmax())
+        print(f"qwen3-8b tp=1 step {pos}: max |logit diff| {err:.2e}")
+    plug.close()
+    del plug
+    torch.cuda.empty_cache()
+
+    tp = 2
+    lcfg = cfg.shard(tp)
+    n_sms = device_sm_count(0) // tp
+    sched2 = default_schedule(lcfg, n_sms=n_sms, tp_size=tp)
+    plugs, streams = [], []
+    for r in range(tp):
+        pl = MegaKernelPlugin(lcfg, sched2, max_ctx=max_ctx, n_sms=n_sms, tp_rank=r, tp_size=tp)
+        pl.bind_weights(w.shard(r, tp))
+        plugs.append(pl)
+        streams.append(torch.cuda.Stream())
+    for pl in plugs:
+        pl.bind_peers([q.workspace for q in plugs])
+    torch.cuda.synchronize()
+    vl = lcfg.vocab
+    for pos, tok in enumerate(toks):
+        outs = []
+        for r, pl in enumerate(plugs):
+            with torch.cuda.stream(streams[r]):
+                outs.append(pl.decode_step(tok, pos, want_logits=True))
+        for pl in plugs:
+            pl.check()
+        got = np.concatenate([plugs[r].logits[0, r * vl:(r + 1) * vl].cpu().numpy() for r in range(tp)])
+        err = float(np.abs(got - wants[pos]).max())
+        assert err <= 2e-2, (pos, err)
+        assert _cos(got, wants[pos]) >= 0.9995
+        assert int(outs[0].next_token.item()) == int(outs[1].next_token.item())
+        print(f"qwen3-8b tp=2 step {pos}: max |logit diff| {err:.2e}")
+    for pl in plugs:
+        pl.close()
