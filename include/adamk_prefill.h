@@ -73,6 +73,19 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
  * k blocks (of 64) per split, planes stacked in one token tile (0/1), grid size}. */
 int adamk_prefill_gemm_plan(int parts, int T, int K, int N, int epilogue, int tile_n, int n_sms, int32_t plan_out[9]);
 
+/* Causal flash attention of a Prefill pass on the tensor cores (csrc/prefill_attn.cu; replaces the serving engine's
+ * attention operator of PAPER.md:248).  q bf16 [n_q][T][D] (rotary applied, unscaled); k_cache bf16 [n_kv][max_ctx][D]
+ * (one layer of the decode kernel's cache, rows pos0 .. pos0 + T - 1 already written); vt bf16 [n_kv][D][ctx_pad] =
+ * adamk_prefill_vt of the same layer's V cache.  Row t attends to positions 0 .. pos0 + t.  out: bf16 planes
+ * [parts][T][n_q * D] (parts 1: the bf16 value; 2: value + residual), the activation operand of the O projection. */
+int adamk_prefill_attention(const void* q, const void* k_cache, const void* vt, int T, int pos0, int n_q, int n_kv, int D, int max_ctx,
+                            int ctx_pad, void* out_planes, int parts, adamk_pf_stream stream);
+
+/* vt bf16 [n_kv][D][ctx_pad] = transpose of v_cache bf16 [n_kv][max_ctx][D] rows 0 .. ctx - 1, zero padded to ctx_pad (a multiple of 64). */
+int adamk_prefill_vt(const void* v_cache, int n_kv, int D, int max_ctx, int ctx, int ctx_pad, void* vt, adamk_pf_stream stream);
+
+const char* adamk_prefill_attention_last_error(void);
+
 /* h fp32 [T, H] = embed[tokens[t]] (bf16 table). */
 int adamk_prefill_embed(const int32_t* tokens, int T, const void* embed, int H, float* h, adamk_pf_stream stream);
 

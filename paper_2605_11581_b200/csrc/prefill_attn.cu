@@ -1,0 +1,449 @@
+// prefill_attn.cu -- causal flash attention for Prefill on the sm_100a tensor cores (tcgen05 / TMEM / TMA).
+//
+// The paper runs Prefill on the serving engine's fused operators; this is the attention operator of
+// this repository's own Prefill (prefill.TensorCorePrefill), replacing the library call the first round used.
+// One CTA = one (q head, 128-row q tile); it walks the K / V blocks of 128 positions up to the causal diagonal:
+//
+//   warp 0     TMA producer: the Q tile once, then K_j and V^T_j blocks into a two-stage ring
+//              (cp.async.bulk.tensor.2d, 128-byte swizzle, K-major boxes of 64 elements)
+//   warp 1     one lane issues tcgen05.mma: S_j = Q K_j^T into one of two S accumulators in tensor memory,
+//              O_j = P_j V_j into a third; tcgen05.commit publishes them and frees the ring stage
+//   warps 2-5  softmax: thread r owns q row r (= TMEM lane r): tcgen05.ld of its S row, causal mask, running
+//              maximum / sum (exp2 with the scale folded in), P_j written as bf16 into shared memory in the swizzled
+//              K-major layout the PV MMA reads, the O row (fp32, registers) rescaled and accumulated from tensor memory
+//
+// S_{j+1} is issued before P_j is awaited (two S buffers), so QK^T of the next block overlaps the softmax of this one.
+// K comes straight from the KV cache the decode kernel uses ([kv head][max_ctx][D] bf16: rows are K-major); V is
+// needed K-major over positions, i.e. transposed: adamk_prefill_vt writes V^T [kv head][D][ctx_pad] (zero padded)
+// once per layer -- 2 x ctx x kv_dim bytes, noise next to the GEMMs.  GQA: the q heads of a group are separate CTAs
+// that re-read the same K / V^T blocks from L2.
+//
+// Numerics: bf16 Q, K, V and P, fp32 scores / softmax state / output -- the usual flash-attention contract.
+// Output: the bf16 plane(s) [parts][T][n_q * D] the O-projection GEMM takes as its activation operand.
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+
+#include "../../include/adamk_prefill.h"
+
+namespace fa {
+
+constexpr int BQ = 128;    // q rows per tile = TMEM lanes
+constexpr int BKV = 128;   // positions per K / V block
+constexpr int KB = 64;     // bf16 elements per 128-byte swizzle row
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+               : "memory");
+}
+// K-major operand tile stored as rows of 128 bytes with the 128-byte swizzle; 8-row groups 1024 bytes apart
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
+  uint64_t d = (addr >> 4) & 0x3fffu;
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(1024 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
+}
+// fp32 accumulate, bf16 x bf16, both operands K-major, M x N
+__host__ __device__ constexpr uint32_t instr_desc(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+__device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct Args {
+  int T, pos0, n_q, n_kv, max_ctx, parts;
+  float sl2e;                 // softmax scale * log2(e)
+  __nv_bfloat16* out;         // [parts][T][n_q * D]
+  long long plane_stride;
+};
+
+// shared memory: Q | 2 x (K | V^T) | P | barriers
+template <int D>
+struct Smem {
+  static constexpr int kQ = BQ * D * 2;
+  static constexpr int kK = BKV * D * 2;
+  static constexpr int kV = D * BKV * 2;
+  static constexpr int kStage = kK + kV;
+  static constexpr int kP = BQ * BKV * 2;
+  static constexpr int kBars = 256;
+  static constexpr int kTotal = kQ + 2 * kStage + kP + kBars + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+             const __grid_constant__ CUtensorMap map_vt, const Args a) {
+  using S = Smem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* q_s = smem;
+  uint8_t* kv_s = smem + S::kQ;
+  uint8_t* p_s = kv_s + 2 * S::kStage;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p_s + S::kP);
+  uint64_t* q_full = bars;            // 1
+  uint64_t* kv_full = bars + 1;       // 2
+  uint64_t* kv_empty = bars + 3;      // 2
+  uint64_t* s_full = bars + 5;        // 2
+  uint64_t* p_full = bars + 7;        // 1 (128 arrivals)
+  uint64_t* o_full = bars + 8;        // 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.y, kvh = h / (a.n_q / a.n_kv);
+  const int qt = (int)gridDim.x - 1 - (int)blockIdx.x;   // the long tiles (late q rows) are scheduled first
+  const int q0 = qt * BQ;
+  const int ctx = a.pos0 + a.T;
+  const int kv_end = min(ctx, a.pos0 + q0 + BQ);          // causal: nothing past the tile's last row
+  const int n_blk = (kv_end + BKV - 1) / BKV;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_k)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_vt)) : "memory");
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+    }
+    mbar_init(p_full, 128);
+    mbar_init(o_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tm_s0 = tmem_base, tm_o = tmem_base + 2 * BKV;   // S buffers at columns 0 and 128, O_j at 256
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, S::kQ);
+      for (int kb = 0; kb < D / KB; ++kb) tma_load_2d(&map_q, q_full, q_s + kb * (BQ * 128), kb * KB, h * a.T + q0);
+      for (int j = 0; j < n_blk; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        uint8_t* ks = kv_s + st * S::kStage;
+        uint8_t* vs = ks + S::kK;
+        mbar_expect_tx(&kv_full[st], S::kStage);
+        for (int kb = 0; kb < D / KB; ++kb) tma_load_2d(&map_k, &kv_full[st], ks + kb * (BKV * 128), kb * KB, kvh * a.max_ctx + j * BKV);
+        for (int kb = 0; kb < BKV / KB; ++kb) tma_load_2d(&map_vt, &kv_full[st], vs + kb * (D * 128), j * BKV + kb * KB, kvh * D);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = instr_desc(BQ, BKV), idesc_o = instr_desc(BQ, D);
+      auto issue_s = [&](int j) {   // S_j = Q K_j^T into S buffer j & 1
+        const int st = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(q_s), ka = smem_u32(kv_s + st * S::kStage);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off_q = (k / 4) * (BQ * 128) + (k % 4) * 32, off_k = (k / 4) * (BKV * 128) + (k % 4) * 32;
+          umma(tm_s0 + st * BKV, smem_desc_sw128(qa + off_q), smem_desc_sw128(ka + off_k), idesc_s, k != 0);
+        }
+        umma_commit(&s_full[st]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int j = 0; j < n_blk; ++j) {
+        const int st = j & 1;
+        if (j + 1 < n_blk) issue_s(j + 1);      // the next block's scores while this block's softmax runs
+        mbar_wait(p_full, j & 1);               // P_j is in shared memory; S_j and O_{j-1} have been read
+        tc_fence_after();
+        const uint32_t pa = smem_u32(p_s), va = smem_u32(kv_s + st * S::kStage + S::kK);
+#pragma unroll
+        for (int k = 0; k < BKV / 16; ++k) {
+          const uint32_t off_p = (k / 4) * (BQ * 128) + (k % 4) * 32, off_v = (k / 4) * (D * 128) + (k % 4) * 32;
+          umma(tm_o, smem_desc_sw128(pa + off_p), smem_desc_sw128(va + off_v), idesc_o, k != 0);
+        }
+        umma_commit(&kv_empty[st]);             // K_j / V^T_j may be overwritten
+        umma_commit(o_full);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;               // the TMEM lanes this warp may read
+    const int row = quarter * 32 + lane;        // q row of the tile = TMEM lane
+    const int q_pos = a.pos0 + q0 + row;
+    const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+    float o[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) o[i] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;
+    const uint32_t p_row = smem_u32(p_s) + row * 128;
+    const int sw = row & 7;
+    for (int j = 0; j < n_blk; ++j) {
+      const int st = j & 1, kv0 = j * BKV;
+      const bool diag = kv0 + BKV - 1 > a.pos0 + q0;   // some row of the tile masks part of this block
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t ts = tm_s0 + st * BKV + lane_addr;
+      // pass 1: the row maximum
+      float m_blk = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(ts + c * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float s = __uint_as_float(r[i]);
+          m_blk = fmaxf(m_blk, (!diag || kv0 + c * 32 + i <= q_pos) ? s : -INFINITY);
+        }
+      }
+      const float m_new = fmaxf(m_run, m_blk);
+      const float mb = m_new * a.sl2e;
+      const float alpha = ex2(m_run * a.sl2e - mb);       // 0 on the first block (m_run = -inf)
+      // O_{j-1} out of tensor memory (which also means the PV product of block j-1 is done reading P), rescaled
+      if (j > 0) {
+        mbar_wait(o_full, (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tm_o + lane_addr + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[c * 32 + i] = (o[c * 32 + i] + __uint_as_float(r[i])) * alpha;
+        }
+      }
+      // pass 2: P = exp2(s * scale * log2e - m), written as bf16 in the swizzled K-major layout of the PV operand
+      float l_blk = 0.f;
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(ts + c * 32, r);
+        tmem_ld_wait();
+        uint32_t packed[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float p0 = ex2(fmaf(__uint_as_float(r[i]), a.sl2e, -mb)), p1 = ex2(fmaf(__uint_as_float(r[i + 1]), a.sl2e, -mb));
+          if (diag) {
+            if (kv0 + c * 32 + i > q_pos) p0 = 0.f;
+            if (kv0 + c * 32 + i + 1 > q_pos) p1 = 0.f;
+          }
+          const __nv_bfloat162 b = __floats2bfloat162_rn(p0, p1);
+          l_blk += __low2float(b) + __high2float(b);      // the sum of what the tensor cores will multiply
+          packed[i >> 1] = *reinterpret_cast<const uint32_t*>(&b);
+        }
+        // 32 columns = four 16-byte chunks of k block c / 2: chunk index (c % 2) * 4 + q, swizzled by the row
+        const uint32_t base = p_row + (c >> 1) * (BQ * 128);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint32_t chunk = uint32_t(((c & 1) * 4 + q4) ^ sw);
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(base + chunk * 16), "r"(packed[4 * q4]), "r"(packed[4 * q4 + 1]),
+                       "r"(packed[4 * q4 + 2]), "r"(packed[4 * q4 + 3])
+                       : "memory");
+        }
+      }
+      l_run = l_run * alpha + l_blk;
+      m_run = m_new;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P: generic-proxy stores -> tensor-core reads
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    mbar_wait(o_full, (n_blk - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l_run;
+    const int t = q0 + row;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(tm_o + lane_addr + c * 32, r);
+      tmem_ld_wait();
+      if (t < a.T) {
+        __nv_bfloat16* dst = a.out + (long long)t * a.n_q * D + h * D + c * 32;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            const float v0 = (o[c * 32 + i + e] + __uint_as_float(r[i + e])) * inv;
+            const float v1 = (o[c * 32 + i + e + 1] + __uint_as_float(r[i + e + 1])) * inv;
+            const __nv_bfloat162 b = __floats2bfloat162_rn(v0, v1);
+            hi[e >> 1] = *reinterpret_cast<const uint32_t*>(&b);
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(v0 - __low2float(b), v1 - __high2float(b));
+            lo[e >> 1] = *reinterpret_cast<const uint32_t*>(&b2);
+          }
+          *reinterpret_cast<uint4*>(dst + i) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          if (a.parts > 1) *reinterpret_cast<uint4*>(dst + a.plane_stride + i) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(512) : "memory");
+  }
+}
+
+// V^T [n_kv][D][ctx_pad] bf16 from the cache layout [n_kv][max_ctx][D]; columns >= ctx are zero.  grid (ctx_pad / 64, n_kv)
+template <int D>
+__global__ void vt_kernel(const __nv_bfloat16* __restrict__ v, __nv_bfloat16* __restrict__ vt, int max_ctx, int ctx, int ctx_pad) {
+  __shared__ __nv_bfloat16 tile[64][D + 2];
+  const int p0 = blockIdx.x * 64, kvh = blockIdx.y;
+  for (int i = threadIdx.x; i < 64 * D; i += blockDim.x) {
+    const int p = i / D, d = i - p * D;
+    tile[p][d] = (p0 + p < ctx) ? v[((long long)kvh * max_ctx + p0 + p) * D + d] : __float2bfloat16(0.f);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 64 * D; i += blockDim.x) {
+    const int d = i / 64, p = i - d * 64;
+    vt[((long long)kvh * D + d) * ctx_pad + p0 + p] = tile[p][d];
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                  const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+static thread_local char g_err[256] = "";
+
+// 2-D bf16 tensor [rows, cols] row-major, box [box_rows, 64 columns], 128-byte swizzle
+static bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) {
+    snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled is not available from this driver");
+    return false;
+  }
+  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(cols) * 2};
+  cuuint32_t box[2] = {cuuint32_t(KB), cuuint32_t(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled failed with %d (rows %lld cols %lld box %d)", int(r), rows, cols, box_rows);
+    return false;
+  }
+  return true;
+}
+
+template <int D>
+static int run(const void* q, const void* k_cache, const void* vt, const Args& a, int ctx_pad, cudaStream_t stream) {
+  CUtensorMap mq, mk, mv;
+  if (!make_map(&mq, q, (long long)a.n_q * a.T, D, BQ)) return ADAMK_PF_E_CUDA;
+  if (!make_map(&mk, k_cache, (long long)a.n_kv * a.max_ctx, D, BKV)) return ADAMK_PF_E_CUDA;
+  if (!make_map(&mv, vt, (long long)a.n_kv * D, ctx_pad, D)) return ADAMK_PF_E_CUDA;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(flash_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<D>::kTotal) != cudaSuccess) return ADAMK_PF_E_CUDA;
+    configured = true;
+  }
+  flash_kernel<D><<<dim3((a.T + BQ - 1) / BQ, a.n_q), kThreads, Smem<D>::kTotal, stream>>>(mq, mk, mv, a);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof g_err, "prefill attention launch: %s", cudaGetErrorString(e));
+    return ADAMK_PF_E_CUDA;
+  }
+  return ADAMK_PF_OK;
+}
+
+}  // namespace fa
+
+extern "C" {
+
+const char* adamk_prefill_attention_last_error(void) { return fa::g_err; }
+
+int adamk_prefill_vt(const void* v_cache, int n_kv, int D, int max_ctx, int ctx, int ctx_pad, void* vt, adamk_pf_stream stream) {
+  if (v_cache == nullptr || vt == nullptr || n_kv < 1 || (D != 64 && D != 128) || ctx < 1 || ctx > max_ctx || ctx_pad < ctx || ctx_pad % 64)
+    return ADAMK_PF_E_INVALID;
+  const dim3 grid(ctx_pad / 64, n_kv);
+  if (D == 128) fa::vt_kernel<128><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const __nv_bfloat16*>(v_cache), static_cast<__nv_bfloat16*>(vt), max_ctx, ctx, ctx_pad);
+  else fa::vt_kernel<64><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const __nv_bfloat16*>(v_cache), static_cast<__nv_bfloat16*>(vt), max_ctx, ctx, ctx_pad);
+  return cudaGetLastError() == cudaSuccess ? ADAMK_PF_OK : ADAMK_PF_E_CUDA;
+}
+
+int adamk_prefill_attention(const void* q, const void* k_cache, const void* vt, int T, int pos0, int n_q, int n_kv, int D, int max_ctx,
+                            int ctx_pad, void* out_planes, int parts, adamk_pf_stream stream) {
+  if (q == nullptr || k_cache == nullptr || vt == nullptr || out_planes == nullptr) return ADAMK_PF_E_INVALID;
+  if (T < 1 || pos0 < 0 || pos0 + T > max_ctx || n_kv < 1 || n_q % n_kv || (D != 64 && D != 128) || (parts != 1 && parts != 2) ||
+      ctx_pad < pos0 + T || ctx_pad % 64)
+    return ADAMK_PF_E_INVALID;
+  fa::Args a{};
+  a.T = T; a.pos0 = pos0; a.n_q = n_q; a.n_kv = n_kv; a.max_ctx = max_ctx; a.parts = parts;
+  a.sl2e = 1.4426950408889634f / sqrtf(float(D));
+  a.out = static_cast<__nv_bfloat16*>(out_planes);
+  a.plane_stride = (long long)T * n_q * D;
+  return D == 128 ? fa::run<128>(q, k_cache, vt, a, ctx_pad, static_cast<cudaStream_t>(stream))
+                  : fa::run<64>(q, k_cache, vt, a, ctx_pad, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

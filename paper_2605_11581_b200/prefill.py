@@ -34,7 +34,8 @@ GU_BLOCK = 128   # features per gate / up block of the interleaved weight = half
 PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_prefill_set_trace", "adamk_prefill_prefetch_next",
                    "adamk_prefill_gemm_plan", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
                    "adamk_prefill_split", "adamk_prefill_rope_store", "adamk_batch_rope_store", "adamk_batch_attention_workspace",
-                   "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split", "adamk_batch_embed")
+                   "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split", "adamk_batch_embed",
+                   "adamk_prefill_attention", "adamk_prefill_vt", "adamk_prefill_attention_last_error")
 
 _declared = False
 
@@ -55,6 +56,9 @@ def _lib():
         lib.adamk_prefill_gemm_plan.argtypes = [i, i, i, i, i, i, i, C.POINTER(C.c_int32)]
         lib.adamk_prefill_embed.argtypes = [vp, i, vp, i, vp, vp]
         lib.adamk_batch_embed.argtypes = [vp, i, vp, i, i, vp, vp]
+        lib.adamk_prefill_attention.argtypes = [vp, vp, vp, i, i, i, i, i, i, i, vp, i, vp]
+        lib.adamk_prefill_vt.argtypes = [vp, i, i, i, i, i, vp, vp]
+        lib.adamk_prefill_attention_last_error.restype = C.c_char_p
         lib.adamk_prefill_rmsnorm_split.argtypes = [vp, vp, f, i, i, vp, i, vp]
         lib.adamk_prefill_split.argtypes = [vp, ll, vp, i, vp]
         lib.adamk_prefill_rope_store.argtypes = [vp, i, i, i, i, vp, vp, f, vp, vp, i, i, vp, i, vp, vp, vp]
@@ -72,6 +76,11 @@ def _lib():
 def _ok(code: int) -> None:
     if code != 0:
         raise AdamkError(code, (_lib().adamk_prefill_last_error() or b"").decode() or "prefill operator: invalid argument")
+
+
+def _attn_ok(code: int) -> None:
+    if code != 0:
+        raise AdamkError(code, (_lib().adamk_prefill_attention_last_error() or b"").decode() or "prefill attention: invalid argument")
 
 
 def _stream() -> C.c_void_p:
@@ -134,17 +143,17 @@ class TensorCorePrefill:
 
     def __init__(self, cfg: ModelConfig, weights: DecoderWeights, plugin, planes: int = 2, attention: str | None = None,
                  layers: list | None = None, embed: torch.Tensor | None = None):
-        """``attention``: dtype of the library attention operator, "fp32" (default with two planes; exact but a
-        materialised-score kernel) or "bf16" (default with one plane; flash kernel).  ``layers`` / ``embed``: already
-        prepared device weights (``batch_decode.BatchedDecoder`` shares its own)."""
+        """``planes``: bf16 planes per fp32 activation fed to the GEMMs (1: plain bf16; 2: hi + lo, fp32-accurate).
+        Attention is this library's tcgen05 flash kernel (``csrc/prefill_attn.cu``: bf16 Q / K / V / P, fp32 scores and
+        output -- the flash-attention contract) for either setting; ``attention`` is accepted for compatibility with
+        the first round's "bf16" / "fp32" library-operator switch and ignored.  ``layers`` / ``embed``: already prepared
+        device weights (``batch_decode.BatchedDecoder`` shares its own)."""
         if planes not in (1, 2):
             raise ValueError("planes must be 1 (bf16 activations) or 2 (hi + lo, fp32-accurate)")
-        attention = attention or ("bf16" if planes == 1 else "fp32")
-        if attention not in ("bf16", "fp32"):
-            raise ValueError("attention must be 'bf16' or 'fp32'")
+        if attention not in (None, "bf16", "fp32", "flash"):
+            raise ValueError("attention must be 'flash' (or the legacy 'bf16' / 'fp32')")
         _lib()
         self.cfg, self.plugin, self.planes = cfg, plugin, planes
-        self.attn_bf16 = attention == "bf16"
         dev = plugin.device
         self.launches = 0
         if layers is not None:
@@ -173,8 +182,6 @@ class TensorCorePrefill:
         """Fill cache rows ``pos0 .. pos0 + T - 1`` of every layer from ``toks`` (int32 / int64 [T] on the device) and
         return the final hidden states fp32 [T, H].  ``pos0`` must be 0 unless the earlier rows are already cached
         (chunked prefill attends to them)."""
-        import torch.nn.functional as F
-
         cfg, plug, P, lib, st = self.cfg, self.plugin, self.planes, _lib(), _stream()
         T = int(toks.numel())
         if T == 0:
@@ -187,37 +194,30 @@ class TensorCorePrefill:
         h = torch.empty(T, H, dtype=torch.float32, device=dev)
         xp = torch.empty(P, T, H, dtype=bf, device=dev)
         qkv = torch.empty(T, (nq + 2 * nkv) * D, dtype=torch.float32, device=dev)
-        q_dtype = bf if self.attn_bf16 else torch.float32
-        q = torch.empty(nq, T, D, dtype=q_dtype, device=dev)
+        q = torch.empty(nq, T, D, dtype=bf, device=dev)
         ap = torch.empty(P, T, nq * D, dtype=bf, device=dev)
         act = torch.empty(P, T, self.layers[0]["i_pad"], dtype=bf, device=dev)
+        ctx = pos0 + T
+        ctx_pad = -(-ctx // 64) * 64
+        vt = torch.empty(nkv, D, ctx_pad, dtype=bf, device=dev)     # V^T of the current layer (K-major operand of P.V)
         cos, sin = plug._rope
         kc, vc = plug.kv_view()
         _ok(lib.adamk_prefill_embed(_ptr(toks32), T, _ptr(self.embed), H, _ptr(h), st))
         n = 1
-        ctx = pos0 + T
         for l, lw in enumerate(self.layers):
             _ok(lib.adamk_prefill_rmsnorm_split(_ptr(h), _ptr(lw["ln1"]), cfg.rms_eps, T, H, _ptr(xp), P, st))
             gemm(xp, lw["wqkv"], qkv, bias=lw["bqkv"])
             _ok(lib.adamk_prefill_rope_store(_ptr(qkv), T, nq, nkv, D, _ptr(lw["q_norm"]), _ptr(lw["k_norm"]), cfg.rms_eps,
-                                             _ptr(cos), _ptr(sin), pos0, plug.max_ctx, _ptr(q), int(self.attn_bf16),
+                                             _ptr(cos), _ptr(sin), pos0, plug.max_ctx, _ptr(q), 1,
                                              _ptr(kc[l, 0]), _ptr(vc[l, 0]), st))
-            # causal attention over the bf16 cache contents, as the decode kernel sees them (library operator)
-            kh, vh = kc[l, 0, :, :ctx].to(q_dtype)[None], vc[l, 0, :, :ctx].to(q_dtype)[None]
-            if pos0 == 0:
-                a = F.scaled_dot_product_attention(q[None], kh, vh, is_causal=True, enable_gqa=True)
-            else:
-                mask = torch.ones(T, ctx, dtype=torch.bool, device=dev).tril(diagonal=pos0)
-                a = F.scaled_dot_product_attention(q[None], kh, vh, attn_mask=mask, enable_gqa=True)
-            a = a[0].transpose(0, 1).reshape(T, nq * D)
-            if self.attn_bf16:
-                ap[0].copy_(a)
-            else:
-                _ok(lib.adamk_prefill_split(_ptr(a.float().contiguous()), T * nq * D, _ptr(ap), P, st))
-            gemm(ap[:1] if self.attn_bf16 else ap, lw["wo"], h, epilogue=EPI_RESID)
+            # causal attention over the bf16 cache contents, as the decode kernel sees them: tcgen05 flash kernel
+            _attn_ok(lib.adamk_prefill_vt(_ptr(vc[l, 0]), nkv, D, plug.max_ctx, ctx, ctx_pad, _ptr(vt), st))
+            _attn_ok(lib.adamk_prefill_attention(_ptr(q), _ptr(kc[l, 0]), _ptr(vt), T, pos0, nq, nkv, D, plug.max_ctx, ctx_pad,
+                                                 _ptr(ap), P, st))
+            gemm(ap, lw["wo"], h, epilogue=EPI_RESID)
             _ok(lib.adamk_prefill_rmsnorm_split(_ptr(h), _ptr(lw["ln2"]), cfg.rms_eps, T, H, _ptr(xp), P, st))
             gemm(xp, lw["wgu"], act, epilogue=EPI_SWIGLU)
             gemm(act, lw["wdown"], h, epilogue=EPI_RESID)
-            n += 7 + (not self.attn_bf16)
+            n += 9
         self.launches += n
         return h

@@ -128,15 +128,19 @@ def test_prefill_fills_the_cache_like_the_oracle(cfg, planes):
         a = got[:, 0, :, :T].float().cpu().numpy()
         b = want[:, 0, :, :T].float().numpy()
         if planes == 2:
-            np.testing.assert_allclose(a, b, atol=5e-3, rtol=8e-3)        # one bf16 ulp; atol: entries that cancel in RoPE
-            assert (a[0] == b[0]).mean() > 0.99 and (a == b).mean() > 0.8, ((a[0] == b[0]).mean(), (a == b).mean())
+            # layer 0 does not depend on attention: one bf16 ulp, almost all bit-identical.  Deeper layers see the flash
+            # kernel's bf16 P (2^-9 relative): up to two bf16 ulps on a per-cent of the entries
+            np.testing.assert_allclose(a[0], b[0], atol=5e-3, rtol=8e-3)
+            np.testing.assert_allclose(a, b, atol=2e-2, rtol=1.6e-2)
+            assert (a[0] == b[0]).mean() > 0.99 and (a == b).mean() > 0.6, ((a[0] == b[0]).mean(), (a == b).mean())
         else:
             np.testing.assert_allclose(a, b, atol=6e-2, rtol=5e-2)
     hn = _rmsnorm(h[-1:].cpu(), ref.final_norm, cfg.rms_eps)
     logits = (hn @ ref.lm_head.T)[0]
     diff = (logits - want_logits).abs().max().item()
-    assert diff <= (2e-3 if planes == 2 else 2e-1), diff
-    assert pre.launches == 1 + cfg.n_layers * (8 if planes == 2 else 7)   # own kernels; attention is the library operator
+    print(f"prefill {cfg.name} planes {planes}: max |logit diff| of the last position {diff:.2e}")
+    assert diff <= (2e-2 if planes == 2 else 2e-1), diff      # north-star bound with fp32-accurate GEMMs and bf16 flash attention
+    assert pre.launches == 1 + cfg.n_layers * 9   # own kernels only: embed + per layer 2 norms, 4 GEMMs, rope/cache, V^T, flash attention
     plug.close()
 
 
@@ -192,3 +196,41 @@ def test_hybrid_engine_tensor_prefill_matches_oracle(cfg):
     assert res.tokens[:first_tie] == want[:first_tie] and first_tie >= 12
     assert res.prefill_launches == 0 and res.decode_launches == 24
     eng.close()
+
+
+@pytest.mark.parametrize("D,nq,nkv,T,pos0", [(128, 4, 2, 300, 0), (128, 12, 2, 1000, 0), (64, 4, 2, 130, 0), (64, 2, 1, 1, 0), (128, 8, 8, 128, 0),
+                                               (128, 6, 1, 200, 96), (64, 4, 4, 257, 300), (128, 28, 4, 4096, 0)])
+def test_flash_attention_matches_fp32_reference(D, nq, nkv, T, pos0):
+    """csrc/prefill_attn.cu (tcgen05 QK^T and PV, softmax out of tensor memory) against a plain fp32 causal attention on
+    the same bf16 q / k / v: GQA group sizes 1-7, ragged last tiles, a single row, chunked prefill (pos0 > 0), the
+    Qwen2.5-7B shape at 4096 tokens.  Tolerance: P and the output planes are bf16 (2^-9 relative)."""
+    from paper_2605_11581_b200.prefill import _attn_ok, _lib, _ptr, _stream
+
+    lib = _lib()
+    g = torch.Generator(device="cuda").manual_seed(D + T + pos0)
+    ctx, max_ctx = pos0 + T, pos0 + T + 37
+    ctx_pad = -(-ctx // 64) * 64
+    q = torch.randn(nq, T, D, device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn(nkv, max_ctx, D, device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn(nkv, max_ctx, D, device="cuda", generator=g).to(torch.bfloat16)
+    k[:, ctx:] = float("nan")                       # rows past the context must never reach the output
+    v[:, ctx:] = float("nan")
+    vt = torch.full((nkv, D, ctx_pad), float("nan"), device="cuda", dtype=torch.bfloat16)
+    out = torch.zeros(2, T, nq * D, device="cuda", dtype=torch.bfloat16)
+    _attn_ok(lib.adamk_prefill_vt(_ptr(v), nkv, D, max_ctx, ctx, ctx_pad, _ptr(vt), _stream()))
+    _attn_ok(lib.adamk_prefill_attention(_ptr(q), _ptr(k), _ptr(vt), T, pos0, nq, nkv, D, max_ctx, ctx_pad, _ptr(out), 2, _stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(vt[:, :, :ctx], v[:, :ctx].transpose(1, 2)) and (vt[:, :, ctx:] == 0).all()
+    G = nq // nkv
+    qf, kf, vf = q.float(), k[:, :ctx].float().repeat_interleave(G, 0), v[:, :ctx].float().repeat_interleave(G, 0)
+    s = torch.einsum("htd,hcd->htc", qf, kf) / D ** 0.5
+    mask = torch.arange(ctx, device="cuda")[None, :] > (pos0 + torch.arange(T, device="cuda"))[:, None]
+    s.masked_fill_(mask[None], float("-inf"))
+    want = torch.einsum("htc,hcd->htd", torch.softmax(s, dim=-1), vf).transpose(0, 1).reshape(T, nq * D)
+    got = out[0].float() + out[1].float()
+    assert torch.isfinite(got).all()
+    err = (got - want).abs().max().item()
+    assert err <= 2e-2, err
+    assert (got - want).abs().mean().item() <= 1.5e-3
+    # one plane = the bf16 rounding of the two-plane value
+    assert (out[0].float() - got).abs().max().item() <= 2 ** -8 * got.abs().max().item()
