@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define ADAMK_ABI_VERSION 1
+#define ADAMK_ABI_VERSION 2
 
 #define ADAMK_OK 0
 #define ADAMK_E_INVALID (-1)     /* bad argument / malformed task table        */
@@ -106,6 +106,19 @@ size_t adamk_packed_bytes(adamk_handle h);
  * `stream` and remember the pointers.  The source matrices may be freed after
  * the stream has drained, except `embed`. */
 int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, adamk_stream stream);
+
+/* W4A16 (GPTQ-format) weights of one layer: for every projection matrix W [N, K] the 4-bit codes q uint8 [N, K / 2]
+ * (element k of a row in byte k / 2, even k in the low nibble) and the fp16 scales s [N, ceil(K / 128)];
+ * W[n][k] = (q[n][k] - 8) * s[n][k / 128]  (reference byte model: pkg/src/mkplan/graph_ir.py:296-318, group 128,
+ * two bytes per scale).  K must be a multiple of 8. */
+typedef struct AdamkW4A16Layer {
+  const void *q_wq, *s_wq, *q_wk, *s_wk, *q_wv, *s_wv, *q_wo, *s_wo, *q_wgate, *s_wgate, *q_wup, *s_wup, *q_wdown, *s_wdown;
+} AdamkW4A16Layer;
+
+/* adamk_bind_weights for a task table built with the W4A16 schedule flag: the layer matrices come from `qlayers` (HOST
+ * array of n_layers entries, device pointers inside); `w->layers` still supplies norms / biases (its matrix pointers
+ * are ignored); embedding and LM head stay bf16. */
+int adamk_bind_weights_w4a16(adamk_handle h, const AdamkWeightPtrs* w, const AdamkW4A16Layer* qlayers, void* packed, adamk_stream stream);
 
 /* Let `h` stream the packed weights another handle already bound (no repacking, no second copy in HBM).
  * Both handles must have been created from identical task tables.  Used by the batch lanes of

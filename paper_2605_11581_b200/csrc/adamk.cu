@@ -30,6 +30,7 @@
 
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
@@ -733,7 +734,7 @@ __device__ __forceinline__ void gemv_epilogue(const KParams& p, ConsumerCtx& c, 
       else for (int r = 0; r < p.rep; ++r) ll_store(p.ll_hm + (size_t)r * p.H + vrow, eop + v, tag_of(c, t.layer));
       break;
     case T_GATEUP:   // vrow even = gate, pair = up
-      if (t.aux) c.act_loc[(vrow - t.a) >> 1] = silu(v) * v_pair;   // fused down projection: the value stays on this SM
+      if (t.aux & 1) c.act_loc[(vrow - t.a) >> 1] = silu(v) * v_pair;   // fused down projection: the value stays on this SM
       else ll_store(p.ll_act + (vrow >> 1), silu(v) * v_pair, tag_of(c, t.layer));
       break;
     case T_DOWN:
@@ -868,7 +869,84 @@ __device__ __forceinline__ void gemv_ktiles_wide(const KParams& p, uint32_t& slo
   }
 }
 
-template <int RW, bool TP>
+// ---- W4A16 (GPTQ-format int4 weights, fp16 group scales; reference byte model graph_ir.py:296-318) ----------------
+// A task whose aux field has bit 1 set streams its weights as 4-bit codes: value = (code - 8) * scale[row][k / 128].
+// Ring stage of `rows x chunks`: rows * chunks blocks of 128 bytes (a 256-element chunk of one row: lane l owns 4 bytes =
+// the codes of elements 4l..4l+3 and 128+4l..128+4l+3, the elements its two activation LDS.128 hold), then rows * chunks
+// pairs of fp16 scales (the chunk's two groups of 128).  Dequantisation without integer conversions: the fp32 word
+// 0x41800000 | code << 19 IS 16 + code, so a code costs one shift, one LOP3 and half a packed add (minus 24, exact).
+constexpr int kI4ChunkBytes = 128, kI4ScaleBytes = 4, kI4Group = 128;
+// groups of 128 reduction elements touched by columns k0 .. k0 + nk of the down projection
+__host__ __device__ __forceinline__ int downk_i4_groups(int k0, int nk) { return (k0 + nk - 1) / kI4Group - k0 / kI4Group + 1; }
+constexpr int kDownkGroupsMax = 3;
+__host__ __device__ __forceinline__ uint32_t i4_stage_bytes(int rows, int chunks) {
+  return ((uint32_t)rows * (uint32_t)chunks * (kI4ChunkBytes + kI4ScaleBytes) + 15u) & ~15u;
+}
+__device__ __forceinline__ void i4_unpack(uint32_t w, float (&lo)[4], float (&hi)[4]) {   // codes 0-3 / 4-7 as code - 8, exactly
+  // 0x41800000 | code << 19 is the fp32 number 16 + code; minus 24 (exact) leaves code - 8
+  const float2 m24 = make_float2(-24.f, -24.f);
+  const float2 a = __fadd2_rn(make_float2(__uint_as_float(((w << 19) & 0x00780000u) | 0x41800000u),
+                                          __uint_as_float(((w << 15) & 0x00780000u) | 0x41800000u)), m24);
+  const float2 b = __fadd2_rn(make_float2(__uint_as_float(((w << 11) & 0x00780000u) | 0x41800000u),
+                                          __uint_as_float(((w << 7) & 0x00780000u) | 0x41800000u)), m24);
+  const float2 c = __fadd2_rn(make_float2(__uint_as_float(((w << 3) & 0x00780000u) | 0x41800000u),
+                                          __uint_as_float(((w >> 1) & 0x00780000u) | 0x41800000u)), m24);
+  const float2 d = __fadd2_rn(make_float2(__uint_as_float(((w >> 5) & 0x00780000u) | 0x41800000u),
+                                          __uint_as_float(((w >> 9) & 0x00780000u) | 0x41800000u)), m24);
+  lo[0] = a.x; lo[1] = a.y; lo[2] = b.x; lo[3] = b.y;
+  hi[0] = c.x; hi[1] = c.y; hi[2] = d.x; hi[3] = d.y;
+}
+__device__ __forceinline__ float2 h2_to_f2(uint32_t h2) {
+  const __half2 h = *reinterpret_cast<const __half2*>(&h2);
+  return __half22float2(h);
+}
+
+// All k-tiles of one row tile of an int4 task.  acc[i].x / .y accumulate the two groups of every chunk.
+template <int RW>
+__device__ __forceinline__ void gemv_ktiles_i4(const KParams& p, uint32_t& slot, uint32_t& ph, int lane, int ktc, int chunks_last,
+                                               int n_ktiles, int rows, int my_r0, int wk, int WK, int task_idx, uint32_t ring0,
+                                               uint32_t xs_addr, uint32_t full0, uint32_t empty0, float2 (&acc)[kRW], bool active, bool wait) {
+  const uint32_t n_stage = (uint32_t)p.n_stage, stage_bytes = (uint32_t)p.stage_bytes;
+  uint32_t xa0 = xs_addr;   // lane's 16 bytes of the k-tile's first chunk (already offset by wk chunks)
+#pragma unroll 1
+  for (int kt = 0; kt < n_ktiles; ++kt, xa0 += (uint32_t)ktc * (kChunk * 4)) {
+    if (wait) mbar_wait(p, full0 + slot * 8, ph, DE_WATCHDOG_FULL, task_idx);
+    const int chunks = kt == n_ktiles - 1 ? chunks_last : ktc;
+    if (active) {
+      const uint32_t sbase = ring0 + slot * stage_bytes;
+      const uint32_t sc_base = sbase + (uint32_t)rows * (uint32_t)chunks * kI4ChunkBytes;
+      uint32_t xa = xa0;
+#pragma unroll 1
+      for (int j = wk; j < chunks; j += WK, xa += (uint32_t)WK * (kChunk * 4)) {
+        const float4 x0 = lds128f(xa), x1 = lds128f(xa + 512);
+        uint32_t w[RW], sc[RW];
+#pragma unroll
+        for (int i = 0; i < RW; ++i) {
+          const uint32_t blk = (uint32_t)((my_r0 + i) * chunks + j);
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[i]) : "r"(sbase + blk * kI4ChunkBytes + lane * 4));
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sc[i]) : "r"(sc_base + blk * kI4ScaleBytes));
+        }
+#pragma unroll
+        for (int i = 0; i < RW; ++i) {
+          float lo[4], hi[4];
+          i4_unpack(w[i], lo, hi);
+          float2 a = __ffma2_rn(make_float2(lo[0], hi[0]), make_float2(x0.x, x1.x), make_float2(0.f, 0.f));
+          a = __ffma2_rn(make_float2(lo[1], hi[1]), make_float2(x0.y, x1.y), a);
+          a = __ffma2_rn(make_float2(lo[2], hi[2]), make_float2(x0.z, x1.z), a);
+          a = __ffma2_rn(make_float2(lo[3], hi[3]), make_float2(x0.w, x1.w), a);
+          acc[i] = __ffma2_rn(h2_to_f2(sc[i]), a, acc[i]);
+        }
+      }
+    }
+    if (wait) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + slot * 8);
+    }
+    if (++slot == n_stage) { slot = 0; ph ^= 1u; }
+  }
+}
+
+template <int RW, bool TP, bool I4>
 __device__ __forceinline__ void gemv_tiles_t(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx,
                                              const float* xs, SmemHdr* hdr, uint8_t* ring, int tok, float eop0, int probe) {
   const int WK = (t.geom >> 8) & 0xff, rw = (t.geom >> 16) & 0xff, lgWK = 31 - __clz(WK);
@@ -903,7 +981,10 @@ __device__ __forceinline__ void gemv_tiles_t(const KParams& p, ConsumerCtx& c, c
     {
       uint32_t slot = c.slot, ph = c.ph;
       const bool wide = RW >= 4 && WK == 1 && rw == RW && chunks_last == t.ktc && probe != 2;
-      if (wide && t.ktc == 2)
+      if constexpr (I4)
+        gemv_ktiles_i4<RW>(p, slot, ph, c.lane, t.ktc, chunks_last, t.n_ktiles, rows, my_r0, wk, WK, task_idx, smem_u32(ring), xs_addr,
+                           full0, empty0, acc, active, probe != 4);
+      else if (wide && t.ktc == 2)
         gemv_ktiles_wide<RW, 2>(p, slot, ph, c.lane, t.n_ktiles, task_idx, sg.wofs_full, ring_addr, xs_addr, full0, empty0, acc, probe != 4);
       else if (wide && t.ktc == 1)
         gemv_ktiles_wide<RW, 1>(p, slot, ph, c.lane, t.n_ktiles, task_idx, sg.wofs_full, ring_addr, xs_addr, full0, empty0, acc, probe != 4);
@@ -948,14 +1029,14 @@ __device__ __forceinline__ void gemv_tiles_t(const KParams& p, ConsumerCtx& c, c
   if (WK == 1 && !probe) consumer_sync(c.nct);
 }
 
-template <bool TP>
+template <bool TP, bool I4>
 __device__ __forceinline__ void gemv_tiles(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx,
                                            const float* xs, SmemHdr* hdr, uint8_t* ring, int tok, float eop0, int probe) {
   switch ((((t.geom >> 16) & 0xff) + 1) >> 1) {  // rows per warp, rounded up to even
-    case 1: gemv_tiles_t<2, TP>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
-    case 2: gemv_tiles_t<4, TP>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
-    case 3: gemv_tiles_t<6, TP>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
-    default: gemv_tiles_t<8, TP>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
+    case 1: gemv_tiles_t<2, TP, I4>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
+    case 2: gemv_tiles_t<4, TP, I4>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
+    case 3: gemv_tiles_t<6, TP, I4>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
+    default: gemv_tiles_t<8, TP, I4>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe); break;
   }
 }
 
@@ -1023,7 +1104,7 @@ __device__ __forceinline__ void prefetch_fparams(const KParams& p, const Consume
     asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(base + (size_t)i * 128));
 }
 
-template <bool TP>
+template <bool TP, bool I4>
 __device__ __forceinline__ void run_gemv(const KParams& p, ConsumerCtx& c, const Task& t, int task_idx, float* xs,
                                          SmemHdr* hdr, uint8_t* ring, int tok, int probe) {
   // ---- first of all: ask for the first words of the input vector (the round trip overlaps the rest of the preamble) ----
@@ -1062,7 +1143,7 @@ __device__ __forceinline__ void run_gemv(const KParams& p, ConsumerCtx& c, const
     gemv_prologue<TP>(p, c, t, task_idx, xs, hdr, tok, vs, have, early, w0, w1);
   }
   stamp(p, c, task_idx, 1);
-  gemv_tiles<TP>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe);
+  gemv_tiles<TP, I4>(p, c, t, task_idx, xs, hdr, ring, tok, eop0, probe);
   if (probe) { stamp(p, c, task_idx, 7); return; }
   stamp(p, c, task_idx, 2);
   if (t.type == T_LMHEAD) lm_finish<TP>(p, c, hdr);
@@ -1433,6 +1514,55 @@ __device__ __forceinline__ void downk_stage(uint32_t cb, uint32_t col_bytes, uin
   }
 }
 
+// int4 columns (W4A16): a lane's eight rows of a column are one 32-bit word of codes; the caller folds scale * acc into
+// its output rows at the end of every group of 128 columns.
+template <int NB>
+__device__ __forceinline__ void downk_stage_i4(uint32_t cb, uint32_t col_bytes, uint32_t blk_step, const float* act, int cols,
+                                               bool probe, float2 (&acc)[kDownkBlocks][4]) {
+  int j = 0;
+#pragma unroll 1
+  for (; j + 4 <= cols; j += 4, cb += 4 * col_bytes) {
+    uint32_t q[4][NB];
+    float a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = probe ? 1.f : act[j + u];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(q[u][i]) : "r"(cb + u * col_bytes + i * blk_step));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float2 a2 = make_float2(a[u], a[u]);
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        float lo[4], hi[4];
+        i4_unpack(q[u][i], lo, hi);
+        acc[i][0] = __ffma2_rn(make_float2(lo[0], lo[1]), a2, acc[i][0]);
+        acc[i][1] = __ffma2_rn(make_float2(lo[2], lo[3]), a2, acc[i][1]);
+        acc[i][2] = __ffma2_rn(make_float2(hi[0], hi[1]), a2, acc[i][2]);
+        acc[i][3] = __ffma2_rn(make_float2(hi[2], hi[3]), a2, acc[i][3]);
+      }
+    }
+  }
+#pragma unroll 1
+  for (; j < cols; ++j, cb += col_bytes) {
+    const float av = probe ? 1.f : act[j];
+    const float2 a2 = make_float2(av, av);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      uint32_t q;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(q) : "r"(cb + i * blk_step));
+      float lo[4], hi[4];
+      i4_unpack(q, lo, hi);
+      acc[i][0] = __ffma2_rn(make_float2(lo[0], lo[1]), a2, acc[i][0]);
+      acc[i][1] = __ffma2_rn(make_float2(lo[2], lo[3]), a2, acc[i][1]);
+      acc[i][2] = __ffma2_rn(make_float2(hi[0], hi[1]), a2, acc[i][2]);
+      acc[i][3] = __ffma2_rn(make_float2(hi[2], hi[3]), a2, acc[i][3]);
+    }
+  }
+}
+
+template <bool I4>
 __device__ __noinline__ uint32_t run_downk_nl(const KParams& p, WarpArgs w, int nk, int cps, int n_st, float* scratch,
                                               SmemHdr* hdr, uint8_t* ring) {
   const int H = p.H, nblk = H >> 8;
@@ -1448,19 +1578,76 @@ __device__ __noinline__ uint32_t run_downk_nl(const KParams& p, WarpArgs w, int 
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
   const int probe_mode = p.probe, C = p.C;
-  const uint32_t lane_off = (uint32_t)(w.cw * 256 + w.lane * 8) * 2u, blk_step = (uint32_t)C * 512u, col_bytes = (uint32_t)H * 2u;
+  constexpr bool i4 = I4;
+  constexpr uint32_t ebits = I4 ? 4u : 16u;   // bits per weight
+  const uint32_t lane_off = (uint32_t)(w.cw * 256 + w.lane * 8) * ebits / 8u, blk_step = (uint32_t)C * 32u * ebits, col_bytes = (uint32_t)H * ebits / 8u;
   const bool probe = probe_mode != 0;
   const int nmine = w.cw < nblk ? (nblk - w.cw + C - 1) / C : 0;   // row blocks cw, cw + C, ... of this warp
   int col = 0;
+  // W4A16: the slice's fp16 scales [group][H] arrive as a stage of their own and stay in registers (packed pairs);
+  // out[] collects scale * acc at the end of every group, acc restarts
+  uint4 sc[kDownkBlocks][kDownkGroupsMax];
+  float2 out[kDownkBlocks][4];
+  int grp = 0;
+  if (i4) {
+#pragma unroll
+    for (int i = 0; i < kDownkBlocks; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) out[i][j] = make_float2(0.f, 0.f);
+    const int ng = downk_i4_groups(w.a, nk);
+    if (probe_mode != 4) mbar_wait(p, full0 + slot * 8, ph, DE_WATCHDOG_FULL, w.task_idx);
+#pragma unroll
+    for (int i = 0; i < kDownkBlocks; ++i)
+#pragma unroll
+      for (int g = 0; g < kDownkGroupsMax; ++g) {
+        sc[i][g] = make_uint4(0, 0, 0, 0);
+        if (i < nmine && g < ng && probe_mode != 2)
+          sc[i][g] = lds128u(ring_addr + slot * stage_bytes + (uint32_t)((g * H + (w.cw + i * C) * 256 + w.lane * 8) * 2));
+      }
+    if (probe_mode != 4) {
+      __syncwarp();
+      if (w.lane == 0) mbar_arrive(empty0 + slot * 8);
+    }
+    if (++slot == n_stage) { slot = 0; ph ^= 1u; }
+  }
+  auto fold = [&]() {   // end of a group of 128 columns (or of the slice)
+#pragma unroll
+    for (int i = 0; i < kDownkBlocks; ++i) {
+      uint4 s4 = sc[i][0];
+#pragma unroll
+      for (int g = 1; g < kDownkGroupsMax; ++g) if (grp == g) s4 = sc[i][g];
+      const uint32_t sw[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        out[i][j] = __ffma2_rn(h2_to_f2(sw[j]), acc[i][j], out[i][j]);
+        acc[i][j] = make_float2(0.f, 0.f);
+      }
+    }
+    ++grp;
+  };
 #pragma unroll 1
   for (int st = 0; st < n_st; ++st) {
     if (probe_mode != 4) mbar_wait(p, full0 + slot * 8, ph, DE_WATCHDOG_FULL, w.task_idx);
     const int cols = min(cps, nk - col);
     if (probe_mode != 2) {
       const uint32_t cb = ring_addr + slot * stage_bytes + lane_off;
-      if (nmine == 1) downk_stage<1>(cb, col_bytes, blk_step, act + col, cols, probe, acc);
-      else if (nmine == 2) downk_stage<2>(cb, col_bytes, blk_step, act + col, cols, probe, acc);
-      else if (nmine == 3) downk_stage<3>(cb, col_bytes, blk_step, act + col, cols, probe, acc);
+      if (!i4) {
+        if (nmine == 1) downk_stage<1>(cb, col_bytes, blk_step, act + col, cols, probe, acc);
+        else if (nmine == 2) downk_stage<2>(cb, col_bytes, blk_step, act + col, cols, probe, acc);
+        else if (nmine == 3) downk_stage<3>(cb, col_bytes, blk_step, act + col, cols, probe, acc);
+      } else {
+        int c0 = 0;
+        while (c0 < cols) {   // runs of columns inside one group of 128
+          const int k_abs = w.a + col + c0;
+          const int run = min(cols - c0, kI4Group - (k_abs & (kI4Group - 1)));
+          const uint32_t cbr = cb + (uint32_t)c0 * col_bytes;
+          if (nmine == 1) downk_stage_i4<1>(cbr, col_bytes, blk_step, act + col + c0, run, probe, acc);
+          else if (nmine == 2) downk_stage_i4<2>(cbr, col_bytes, blk_step, act + col + c0, run, probe, acc);
+          else if (nmine == 3) downk_stage_i4<3>(cbr, col_bytes, blk_step, act + col + c0, run, probe, acc);
+          c0 += run;
+          if (((k_abs + run) & (kI4Group - 1)) == 0 || col + c0 == nk) fold();
+        }
+      }
     }
     col += cols;
     if (probe_mode != 4) {
@@ -1468,6 +1655,12 @@ __device__ __noinline__ uint32_t run_downk_nl(const KParams& p, WarpArgs w, int 
       if (w.lane == 0) mbar_arrive(empty0 + slot * 8);
     }
     if (++slot == n_stage) { slot = 0; ph ^= 1u; }
+  }
+  if (i4) {
+#pragma unroll
+    for (int i = 0; i < kDownkBlocks; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = out[i][j];
   }
   if (probe) {
     float s = 0.f;
@@ -1590,7 +1783,7 @@ struct GemvArgs {
   int type, layer, a, b, k, kchunks, rt, ktc, n_tiles, n_ktiles, geom, aux;
   int task_idx, tok, probe;
 };
-template <bool TP>
+template <bool TP, bool I4>
 __device__ __noinline__ uint32_t run_gemv_nl(const KParams& p, GemvArgs g, float* xs, SmemHdr* hdr, uint8_t* ring) {
   ConsumerCtx c;
   c.cw = g.cw; c.lane = g.lane; c.ctid = g.ctid; c.nct = g.nct; c.epoch = g.epoch; c.slot = g.slot; c.ph = g.ph;
@@ -1599,7 +1792,7 @@ __device__ __noinline__ uint32_t run_gemv_nl(const KParams& p, GemvArgs g, float
   t.type = g.type; t.layer = g.layer; t.a = g.a; t.b = g.b; t.k = g.k; t.kchunks = g.kchunks; t.rt = g.rt; t.ktc = g.ktc;
   t.n_tiles = g.n_tiles; t.n_ktiles = g.n_ktiles; t.geom = g.geom; t.aux = g.aux;
   c.act_loc = xs + ((p.H + kChunk - 1) / kChunk) * kChunk;
-  run_gemv<TP>(p, c, t, g.task_idx, xs, hdr, ring, g.tok, g.probe);
+  run_gemv<TP, I4>(p, c, t, g.task_idx, xs, hdr, ring, g.tok, g.probe);
   return c.slot | (c.ph << 8);
 }
 // ---- down projection with its input streamed in ------------------------------------------------------
@@ -1912,8 +2105,15 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
         if (type == T_END || type == T_MERGE || type == T_HRED) continue;
         if (type == T_DOWNK) {   // nrows = columns of the SM's K-slice, kchunks = columns per stage, lt.k = H rows per column
           const uint8_t* src = p.wpacked + (size_t)(uint32_t)lt.w_off * 16u;
+          const bool i4 = (lt.aux & 2) != 0;
+          if (i4) {              // first the fp16 scales of the groups the slice touches: [group][H]
+            const uint32_t bytes = (uint32_t)downk_i4_groups(lt.a, nrows) * (uint32_t)lt.k * 2u;
+            issue(src, bytes, true, ti);
+            src += bytes;
+            wcur = src;
+          }
           for (int col = 0; col < nrows; col += kchunks) {
-            const uint32_t bytes = (uint32_t)min(kchunks, nrows - col) * (uint32_t)lt.k * 2u;
+            const uint32_t bytes = (uint32_t)min(kchunks, nrows - col) * (uint32_t)lt.k * (i4 ? 1u : 4u) / 2u;
             issue(src, bytes, true, ti);
             src += bytes;
             wcur = src;
@@ -1940,7 +2140,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
           const int rows = min(rt, nrows - tile * rt);
           for (int kt = 0; kt < n_ktiles; ++kt) {
             const int chunks = min(ktc, kchunks - kt * ktc);
-            const uint32_t bytes = (uint32_t)rows * (uint32_t)chunks * 512u;
+            const uint32_t bytes = (lt.aux & 2) ? i4_stage_bytes(rows, chunks) : (uint32_t)rows * (uint32_t)chunks * 512u;
             const uint8_t* lsrc = src;
             if (p.probe == 3) lsrc = p.wpacked + (size_t)p.sm_stream[blockIdx.x] * 16u + ((size_t)(src - p.wpacked) & 0x3ffffu & ~(size_t)0xffff);
             issue(lsrc, bytes, true, ti);
@@ -1978,7 +2178,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       w.layer = t.layer; w.a = t.a; w.b = t.b; w.aux = t.aux; w.task_idx = ti; w.pos = pos;
       if (t.type == T_HRED) run_hred_nl(kp, w, t.a, t.b, scratch);
       else {
-        const uint32_t sp = run_downk_nl(kp, w, t.b, t.kchunks, t.n_ktiles, scratch, hdr, ring);
+        const uint32_t sp = (t.aux & 2) ? run_downk_nl<true>(kp, w, t.b, t.kchunks, t.n_ktiles, scratch, hdr, ring)
+                                        : run_downk_nl<false>(kp, w, t.b, t.kchunks, t.n_ktiles, scratch, hdr, ring);
         c.slot = sp & 0xffu; c.ph = sp >> 8;
       }
     } else if (t.type == T_ATTN || t.type == T_MERGE) {
@@ -1997,7 +2198,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       g.type = t.type; g.layer = t.layer; g.a = t.a; g.b = t.b; g.k = t.k; g.kchunks = t.kchunks; g.rt = t.rt; g.ktc = t.ktc;
       g.n_tiles = t.n_tiles; g.n_ktiles = t.n_ktiles; g.geom = t.geom; g.aux = t.aux; g.task_idx = ti; g.tok = tok; g.probe = probe;
       const uint32_t sp = (!probe && p.stream_down && down_is_streamable(p, t, c.nct)) ? run_down_streamed_nl<TP>(kp, g, scratch, hdr, ring)
-                                                                                       : run_gemv_nl<TP>(kp, g, scratch, hdr, ring);
+                          : (!TP && (t.aux & 2))                                        ? run_gemv_nl<false, true>(kp, g, scratch, hdr, ring)
+                                                                                       : run_gemv_nl<TP, false>(kp, g, scratch, hdr, ring);
       c.slot = sp & 0xffu; c.ph = sp >> 8;
     }
   }
@@ -2013,6 +2215,7 @@ struct PackParams {
   const void* lm_head;
   uint8_t* wpacked;
   int H, I, q_dim, kv_dim;
+  const AdamkW4A16Layer* qlayers;   // device copy (W4A16 tables) or nullptr
 };
 
 __device__ __forceinline__ bool is_gemv(int type) { return type == T_QKV || type == T_OPROJ || type == T_GATEUP || type == T_DOWN || type == T_LMHEAD; }
@@ -2034,10 +2237,91 @@ __device__ __forceinline__ const __nv_bfloat16* resolve_row(const PackParams& pp
   }
 }
 
+// W4A16 source of a virtual row: codes, scales, K
+__device__ __forceinline__ void resolve_row_i4(const PackParams& pp, const Task& t, int vrow, const uint8_t** q, const __half** sc, int* K) {
+  const AdamkW4A16Layer& L = pp.qlayers[t.layer];
+  const void* qm; const void* sm; int row, k;
+  switch (t.type) {
+    case T_QKV:
+      k = pp.H;
+      if (vrow < pp.q_dim) { qm = L.q_wq; sm = L.s_wq; row = vrow; }
+      else if (vrow < pp.q_dim + pp.kv_dim) { qm = L.q_wk; sm = L.s_wk; row = vrow - pp.q_dim; }
+      else { qm = L.q_wv; sm = L.s_wv; row = vrow - pp.q_dim - pp.kv_dim; }
+      break;
+    case T_OPROJ: k = pp.q_dim; qm = L.q_wo; sm = L.s_wo; row = vrow; break;
+    default:      // T_GATEUP
+      k = pp.H; row = vrow >> 1;
+      if (vrow & 1) { qm = L.q_wup; sm = L.s_wup; } else { qm = L.q_wgate; sm = L.s_wgate; }
+      break;
+  }
+  *K = k;
+  *q = static_cast<const uint8_t*>(qm) + (size_t)row * (k / 2);
+  *sc = static_cast<const __half*>(sm) + (size_t)row * ((k + kI4Group - 1) / kI4Group);
+}
+__device__ __forceinline__ unsigned code_at(const uint8_t* q, int k, int K) {   // 8 (= zero) past the end of the row
+  if (k >= K) return 8u;
+  const unsigned b = q[k >> 1];
+  return (k & 1) ? (b >> 4) : (b & 15u);
+}
+__device__ void pack_task_i4(const PackParams& pp, const Task& t) {
+  uint8_t* dst = pp.wpacked + (size_t)(uint32_t)t.w_off * 16u;
+  if (t.type == T_DOWNK) {
+    const AdamkW4A16Layer& L = pp.qlayers[t.layer];
+    const uint8_t* qd = static_cast<const uint8_t*>(L.q_wdown);
+    const __half* sd = static_cast<const __half*>(L.s_wdown);
+    const int H = pp.H, ng_row = (pp.I + kI4Group - 1) / kI4Group, g0 = t.a / kI4Group, ng = downk_i4_groups(t.a, t.b);
+    __half* sdst = reinterpret_cast<__half*>(dst);
+    for (int e = threadIdx.x; e < ng * H; e += blockDim.x) {   // [group][row]
+      const int g = e / H, r = e - g * H;
+      sdst[e] = sd[(size_t)r * ng_row + g0 + g];
+    }
+    uint8_t* cdst = dst + (size_t)ng * H * 2;
+    for (int e = threadIdx.x; e < t.b * (H / 2); e += blockDim.x) {   // column j: byte b holds rows 2b (low) and 2b + 1
+      const int j = e / (H / 2), b = e - j * (H / 2), k = t.a + j;
+      const unsigned lo = code_at(qd + (size_t)(2 * b) * (pp.I / 2), k, pp.I), hi = code_at(qd + (size_t)(2 * b + 1) * (pp.I / 2), k, pp.I);
+      cdst[e] = (uint8_t)(lo | (hi << 4));
+    }
+    return;
+  }
+  for (int tile = 0; tile < t.n_tiles; ++tile) {
+    const int rows = min(t.rt, t.b - tile * t.rt);
+    for (int kt = 0; kt < t.n_ktiles; ++kt) {
+      const int chunks = min(t.ktc, t.kchunks - kt * t.ktc);
+      const int nblk = rows * chunks;
+      for (int e = threadIdx.x; e < nblk * kI4ChunkBytes; e += blockDim.x) {
+        const int blk = e / kI4ChunkBytes, b = e - blk * kI4ChunkBytes, r = blk / chunks, ch = blk - r * chunks;
+        const int lane = b >> 2, pair = b & 3;          // byte `pair` of lane's word: elements 2 pair, 2 pair + 1 of its eight
+        const uint8_t* q; const __half* sc; int K;
+        resolve_row_i4(pp, t, t.a + tile * t.rt + r, &q, &sc, &K);
+        const int kbase = (kt * t.ktc + ch) * kChunk;
+        unsigned v = 0;
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int el = 2 * pair + h2;                 // 0-3: offsets 4 lane + el; 4-7: 128 + 4 lane + el - 4
+          const int k = kbase + (el < 4 ? 4 * lane + el : 128 + 4 * lane + (el - 4));
+          v |= code_at(q, k, K) << (4 * h2);
+        }
+        dst[e] = (uint8_t)v;
+      }
+      __half* sdst = reinterpret_cast<__half*>(dst + (size_t)nblk * kI4ChunkBytes);
+      for (int e = threadIdx.x; e < nblk * 2; e += blockDim.x) {
+        const int blk = e >> 1, r = blk / chunks, ch = blk - r * chunks;
+        const uint8_t* q; const __half* sc; int K;
+        resolve_row_i4(pp, t, t.a + tile * t.rt + r, &q, &sc, &K);
+        const int g = ((kt * t.ktc + ch) * kChunk) / kI4Group + (e & 1);
+        sdst[e] = g < (K + kI4Group - 1) / kI4Group ? sc[g] : __float2half(0.f);
+      }
+      for (uint32_t e = (uint32_t)nblk * (kI4ChunkBytes + kI4ScaleBytes) + threadIdx.x; e < i4_stage_bytes(rows, chunks); e += blockDim.x)
+        dst[e] = 0;      // alignment padding of the stage
+      dst += i4_stage_bytes(rows, chunks);
+    }
+  }
+}
+
 __global__ void adamk_pack_kernel(const PackParams pp) {
   const int ti = blockIdx.x;
   if (ti >= pp.n_tasks) return;
   const Task t = pp.tasks[ti];
+  if ((t.aux & 2) && pp.qlayers != nullptr) { pack_task_i4(pp, t); return; }
   if (t.type == T_DOWNK) {   // columns t.a .. t.a + t.b of the down projection [H][I], each as H consecutive rows
     __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(pp.wpacked + (size_t)(uint32_t)t.w_off * 16u);
     const __nv_bfloat16* wd = (const __nv_bfloat16*)pp.layers[t.layer].wdown;
@@ -2109,10 +2393,24 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 }  // namespace
 
+// bytes of the packed weight stream a task owns (keep in sync with task_table.task_weight_bytes)
+static size_t task_stream_bytes(const Task& t) {
+  const bool i4 = (t.aux & 2) != 0;
+  if (t.type == T_DOWNK) return i4 ? (size_t)downk_i4_groups(t.a, t.b) * t.k * 2 + (size_t)t.b * t.k / 2 : (size_t)t.b * t.k * 2;
+  if (t.type == T_ATTN || t.type == T_MERGE || t.type == T_HRED) return 0;
+  if (!i4) return (size_t)t.b * t.kchunks * 512;
+  size_t total = 0;
+  for (int tile = 0; tile < t.n_tiles; ++tile) {
+    const int rows = std::min(t.rt, t.b - tile * t.rt);
+    for (int kt = 0; kt < t.n_ktiles; ++kt) total += i4_stage_bytes(rows, std::min(t.ktc, t.kchunks - kt * t.ktc));
+  }
+  return total;
+}
+
 struct AdamkHandle_ {
   AdamkModelDesc desc{};
   int n_sms = 0, C = 0, n_stage = 0, stage_bytes = 0, n_tasks = 0, batch = 0, inflight = 0;
-  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, poll_sleep_ns = 0, task_cache_bytes = 0, pf_window_kb = 0, pace = 0, poll_inflight = 0, fuse_down = 0;
+  int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, poll_sleep_ns = 0, task_cache_bytes = 0, pf_window_kb = 0, pace = 0, poll_inflight = 0, fuse_down = 0, w4a16 = 0;
   const unsigned* d_sm_stream = nullptr;
   size_t packed_weight_bytes = 0;  // matrix streams only
   size_t fparam_floats = 0;
@@ -2167,7 +2465,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   h->tp_rank = tp_rank; h->tp_size = tp_size;
   h->n_sms = tt[2]; h->C = tt[3]; h->n_stage = tt[4]; h->stage_bytes = tt[5]; h->n_tasks = tt[6]; h->batch = tt[7];
   h->inflight = tt[8]; h->attn_chunks = tt[9]; h->attn_min_chunk = tt[10]; h->scratch_bytes = tt[11];
-  h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14] & 0xffff; h->stream_down = !((tt[14] >> 16) & 1); h->pf_window_kb = tt[15] & 0xffff; h->pace = (tt[15] >> 16) & 0x7fff; h->poll_inflight = (tt[14] >> 20) & 0xf; h->fuse_down = (tt[14] >> 24) & 1;
+  h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14] & 0xffff; h->stream_down = !((tt[14] >> 16) & 1); h->pf_window_kb = tt[15] & 0xffff; h->pace = (tt[15] >> 16) & 0x7fff; h->poll_inflight = (tt[14] >> 20) & 0xf; h->fuse_down = (tt[14] >> 24) & 1; h->w4a16 = (tt[14] >> 26) & 1;
   auto bad = [&](const std::string& m) { delete h; return fail(ADAMK_E_INVALID, m); };
   const AdamkModelDesc& d = *desc;
   if (d.head_dim != 64 && d.head_dim != 128) return bad("head_dim must be 64 or 128");
@@ -2234,15 +2532,20 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
         continue;
       }
       // T_DOWNK must follow the gate/up task of the same SM whose SwiGLU outputs it multiplies
-      if (i == 0 || tasks[i - 1].type != T_GATEUP || tasks[i - 1].aux != 1 || tasks[i - 1].layer != t.layer ||
+      if (i == 0 || tasks[i - 1].type != T_GATEUP || !(tasks[i - 1].aux & 1) || tasks[i - 1].layer != t.layer ||
           tasks[i - 1].a != 2 * t.a || tasks[i - 1].b != 2 * t.b)
         return bad("T_DOWNK does not match the preceding gate/up task");
       if (t.a < 0 || t.b < 1 || t.a + t.b > d.intermediate || t.b > 0xffff) return bad("T_DOWNK columns out of range");
-      if (t.kchunks < 1 || (size_t)t.kchunks * d.hidden * 2 > (size_t)h->stage_bytes || t.n_ktiles != (t.b + t.kchunks - 1) / t.kchunks)
+      if (t.kchunks < 1 || (size_t)t.kchunks * d.hidden * ((t.aux & 2) ? 1 : 4) / 2 > (size_t)h->stage_bytes || t.n_ktiles != (t.b + t.kchunks - 1) / t.kchunks)
         return bad("T_DOWNK staging inconsistent");
-      const size_t bytes = (size_t)t.b * d.hidden * 2;
+      if (t.aux & ~2) return bad("T_DOWNK aux field out of range");
+      if (t.aux & 2) {
+        if (!h->w4a16) return bad("int4 task in a table without the W4A16 flag");
+        const int ng = downk_i4_groups(t.a, t.b);
+        if (ng > kDownkGroupsMax || (size_t)ng * d.hidden * 2 > (size_t)h->stage_bytes) return bad("T_DOWNK: too many scale groups for one stage");
+      }
       const size_t off = (size_t)(uint32_t)t.w_off * 16;
-      wbytes = std::max(wbytes, off + bytes);
+      wbytes = std::max(wbytes, off + task_stream_bytes(t));
       continue;
     }
     if (t.type < T_QKV || t.type > T_LMHEAD) return bad("unknown task type");
@@ -2263,15 +2566,20 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
     if (rw < 2 || rw > kRW || (rw & 1) || t.rt != WR * rw) return bad("rows per warp must be 2, 4, 6 or 8 and rows_per_tile == WR * rw");
     if (WK > 1 && t.rt > 32) return bad("K-split tiles hold at most 32 rows");
     if (t.type == T_GATEUP && ((t.a | t.b | rw) & 1)) return bad("gate/up rows must come in pairs");
-    if (t.aux != 0 && !(t.type == T_GATEUP && t.aux == 1 && h->fuse_down)) return bad("task aux field out of range");
+    if ((t.aux & 1) && !(t.type == T_GATEUP && h->fuse_down)) return bad("task aux field out of range");
+    if (t.aux & 2) {
+      if (!h->w4a16) return bad("int4 task in a table without the W4A16 flag");
+      if (t.type != T_QKV && t.type != T_OPROJ && t.type != T_GATEUP) return bad("W4A16 covers the QKV / O / gate-up / fused down projections only");
+      if (i4_stage_bytes(t.rt, t.ktc) > (uint32_t)h->stage_bytes) return bad("int4 stage larger than stage_bytes");
+    }
+    if (t.aux & ~3) return bad("task aux field out of range");
     if (t.type == T_DOWN && h->fuse_down) return bad("T_DOWN in a fuse_down table");
     if (t.ktc < 1 || t.n_ktiles != (t.kchunks + t.ktc - 1) / t.ktc || t.n_tiles != (t.b + t.rt - 1) / t.rt)
       return bad("task tiling inconsistent");
-    if ((size_t)t.rt * t.ktc * 512 > (size_t)h->stage_bytes) return bad("stage larger than stage_bytes");
+    if (!(t.aux & 2) && (size_t)t.rt * t.ktc * 512 > (size_t)h->stage_bytes) return bad("stage larger than stage_bytes");
     if (t.type != T_LMHEAD && (t.layer < 0 || t.layer >= d.n_layers)) return bad("task layer out of range");
-    const size_t bytes = (size_t)t.b * t.kchunks * 512;
     const size_t off = (size_t)(uint32_t)t.w_off * 16;
-    wbytes = std::max(wbytes, off + bytes);
+    wbytes = std::max(wbytes, off + task_stream_bytes(t));
   }
   h->packed_weight_bytes = align_up(wbytes, 256);
   // fp32 parameter tail
@@ -2308,8 +2616,8 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
         const Task& t = tasks[i];
         if (t.type == T_ATTN || t.type == T_MERGE || t.type == T_HRED) continue;
         if ((unsigned)t.w_off != cursor) return bad("packed streams must be contiguous per SM, SM-major");
-        if (t.type == T_DOWNK) cursor += (unsigned)((size_t)t.b * t.k * 2 / 16);
-        else cursor += (unsigned)((size_t)t.b * t.kchunks * 512 / 16);
+        if (task_stream_bytes(t) % 16) return bad("a task's weight stream is not a multiple of 16 bytes");
+        cursor += (unsigned)(task_stream_bytes(t) / 16);
       }
     }
     sm_stream[h->n_sms] = cursor;
@@ -2367,16 +2675,24 @@ int adamk_workspace_init(adamk_handle h, void* workspace, adamk_stream stream) {
   return ADAMK_OK;
 }
 
-int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, adamk_stream stream_) {
+static int bind_weights_impl(adamk_handle h, const AdamkWeightPtrs* w, const AdamkW4A16Layer* qlayers, void* packed, adamk_stream stream_) {
   if (!h || !w || !packed) return fail(ADAMK_E_INVALID, "NULL argument");
+  if ((qlayers != nullptr) != (h->w4a16 != 0)) return fail(ADAMK_E_INVALID, "W4A16 task tables bind through adamk_bind_weights_w4a16, bf16 ones through adamk_bind_weights");
   if (!w->embed || !w->final_norm || !w->layers || !w->rope_cos || !w->rope_sin) return fail(ADAMK_E_INVALID, "missing weight pointer");
   if ((uintptr_t)packed % 256) return fail(ADAMK_E_INVALID, "packed buffer must be 256-byte aligned");
   const AdamkModelDesc& d = h->desc;
   cudaStream_t stream = (cudaStream_t)stream_;
   for (int l = 0; l < d.n_layers; ++l) {
     const AdamkLayerWeights& lw = w->layers[l];
-    if (!lw.ln1 || !lw.wq || !lw.wk || !lw.wv || !lw.wo || !lw.ln2 || !lw.wgate || !lw.wup || !lw.wdown)
+    if (!lw.ln1 || !lw.ln2) return fail(ADAMK_E_INVALID, "layer " + std::to_string(l) + ": missing norm pointer");
+    if (!qlayers && (!lw.wq || !lw.wk || !lw.wv || !lw.wo || !lw.wgate || !lw.wup || !lw.wdown))
       return fail(ADAMK_E_INVALID, "layer " + std::to_string(l) + ": missing matrix pointer");
+    if (qlayers) {
+      const AdamkW4A16Layer& q = qlayers[l];
+      if (!q.q_wq || !q.s_wq || !q.q_wk || !q.s_wk || !q.q_wv || !q.s_wv || !q.q_wo || !q.s_wo || !q.q_wgate || !q.s_wgate || !q.q_wup ||
+          !q.s_wup || !q.q_wdown || !q.s_wdown)
+        return fail(ADAMK_E_INVALID, "layer " + std::to_string(l) + ": missing W4A16 code / scale pointer");
+    }
     if (d.qkv_bias && (!lw.bq || !lw.bk || !lw.bv)) return fail(ADAMK_E_INVALID, "qkv_bias set but bias pointer missing");
     if (d.qk_norm && (!lw.q_norm || !lw.k_norm)) return fail(ADAMK_E_INVALID, "qk_norm set but norm pointer missing");
   }
@@ -2384,7 +2700,14 @@ int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, a
   CUDA_TRY(cudaMalloc(&d_layers, sizeof(AdamkLayerWeights) * d.n_layers));
   cudaError_t e = cudaMemcpyAsync(d_layers, w->layers, sizeof(AdamkLayerWeights) * d.n_layers, cudaMemcpyHostToDevice, stream);
   if (e != cudaSuccess) { cudaFree(d_layers); return fail(ADAMK_E_CUDA, cudaGetErrorString(e)); }
+  AdamkW4A16Layer* d_qlayers = nullptr;
+  if (qlayers) {
+    e = cudaMalloc(&d_qlayers, sizeof(AdamkW4A16Layer) * d.n_layers);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_qlayers, qlayers, sizeof(AdamkW4A16Layer) * d.n_layers, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) { cudaFree(d_layers); if (d_qlayers) cudaFree(d_qlayers); return fail(ADAMK_E_CUDA, cudaGetErrorString(e)); }
+  }
   PackParams pp{};
+  pp.qlayers = d_qlayers;
   pp.tasks = h->d_tasks; pp.n_tasks = h->n_tasks; pp.layers = d_layers;
   pp.lm_head = w->lm_head ? w->lm_head : w->embed;
   pp.wpacked = static_cast<uint8_t*>(packed);
@@ -2415,6 +2738,7 @@ int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, a
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   cudaFree(d_layers);
+  if (d_qlayers) cudaFree(d_qlayers);
   if (e != cudaSuccess) return fail(ADAMK_E_CUDA, std::string("adamk_bind_weights: ") + cudaGetErrorString(e));
   h->w = *w;
   h->w.layers = nullptr;
@@ -2422,6 +2746,15 @@ int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, a
   h->fparams = fp;
   h->bound = true;
   return ADAMK_OK;
+}
+
+int adamk_bind_weights(adamk_handle h, const AdamkWeightPtrs* w, void* packed, adamk_stream stream) {
+  return bind_weights_impl(h, w, nullptr, packed, stream);
+}
+
+int adamk_bind_weights_w4a16(adamk_handle h, const AdamkWeightPtrs* w, const AdamkW4A16Layer* qlayers, void* packed, adamk_stream stream) {
+  if (!qlayers) return fail(ADAMK_E_INVALID, "NULL W4A16 layer array");
+  return bind_weights_impl(h, w, qlayers, packed, stream);
 }
 
 int adamk_share_weights(adamk_handle h, adamk_handle owner, const AdamkWeightPtrs* w) {

@@ -22,7 +22,7 @@ from .model_config import ModelConfig
 from .task_table import KernelSchedule, TaskTable, build_task_table
 from .weights import DecoderWeights, rope_table
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class AdamkError(RuntimeError):
@@ -46,6 +46,13 @@ class _LayerWeights(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in _LAYER_FIELDS]
 
 
+_QUANT_FIELDS = tuple(f"{kind}_{name}" for name in ("wq", "wk", "wv", "wo", "wgate", "wup", "wdown") for kind in ("q", "s"))
+
+
+class _W4A16Layer(C.Structure):   # include/adamk.h: AdamkW4A16Layer
+    _fields_ = [(n, C.c_void_p) for n in _QUANT_FIELDS]
+
+
 class _WeightPtrs(C.Structure):
     _fields_ = [("embed", C.c_void_p), ("final_norm", C.c_void_p), ("lm_head", C.c_void_p),
                 ("layers", C.POINTER(_LayerWeights)), ("rope_cos", C.c_void_p), ("rope_sin", C.c_void_p)]
@@ -55,7 +62,7 @@ EXPORTS = (
     "adamk_abi_version", "adamk_device_sm_count", "adamk_last_error", "adamk_create", "adamk_destroy",
     "adamk_packed_bytes", "adamk_bind_weights", "adamk_bind_peers", "adamk_workspace_bytes",
     "adamk_workspace_init", "adamk_kv_cache_bytes", "adamk_decode_step", "adamk_device_status",
-    "adamk_stream_probe", "adamk_trace_bytes", "adamk_set_trace", "adamk_share_weights",
+    "adamk_stream_probe", "adamk_trace_bytes", "adamk_set_trace", "adamk_share_weights", "adamk_bind_weights_w4a16",
 )
 
 _lib = None
@@ -86,6 +93,7 @@ def load_library() -> C.CDLL:
         getattr(lib, name).argtypes = [C.c_void_p]
         getattr(lib, name).restype = C.c_size_t
     lib.adamk_bind_weights.argtypes = [C.c_void_p, C.POINTER(_WeightPtrs), C.c_void_p, C.c_void_p]
+    lib.adamk_bind_weights_w4a16.argtypes = [C.c_void_p, C.POINTER(_WeightPtrs), C.POINTER(_W4A16Layer), C.c_void_p, C.c_void_p]
     lib.adamk_bind_peers.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_int]
     lib.adamk_share_weights.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_WeightPtrs)]
     lib.adamk_workspace_init.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -177,10 +185,16 @@ class MegaKernelPlugin:
         return cls(cfg, sched, max_ctx, device=device)
 
     # -- weights -------------------------------------------------------------
-    def bind_weights(self, w: DecoderWeights, keep_source: bool = False) -> None:
-        """Repack HF-layout bf16 weights into the per-SM tile-major streams."""
+    def bind_weights(self, w, keep_source: bool = False) -> None:
+        """Repack the weights into the per-SM tile-major streams: HF-layout bf16 ``DecoderWeights``, or -- for a
+        schedule with ``w4a16`` -- ``quant.QuantizedWeights`` (4-bit codes + fp16 group scales of the layer projections;
+        embedding, norms, biases and LM head come from its bf16 ``base``)."""
         cfg = self.cfg
-        w = w.to(self.device)
+        quantized = hasattr(w, "base")
+        if quantized != bool(self.schedule.w4a16):
+            raise AdamkError(-101, "a w4a16 schedule takes quant.QuantizedWeights, a bf16 schedule DecoderWeights")
+        qw = w.to(self.device) if quantized else None
+        w = qw.base if quantized else w.to(self.device)
         cos, sin = rope_table(cfg, self.max_ctx)
         self._rope = (cos.to(self.device), sin.to(self.device))
         layers = (_LayerWeights * cfg.n_layers)()
@@ -194,10 +208,20 @@ class MegaKernelPlugin:
                            None if w.lm_head is None else w.lm_head.data_ptr(),
                            layers, self._rope[0].data_ptr(), self._rope[1].data_ptr())
         self.packed = torch.empty(self.lib.adamk_packed_bytes(self._h), dtype=torch.uint8, device=self.device)
-        _check(self.lib, self.lib.adamk_bind_weights(self._h, C.byref(ptrs), C.c_void_p(self.packed.data_ptr()),
-                                                     self._stream_ptr()))
+        if quantized:
+            qlayers = (_W4A16Layer * cfg.n_layers)()
+            for i, ql in enumerate(qw.layers):
+                for name, m in ql.items():
+                    assert m.q.dtype == torch.uint8 and m.s.dtype == torch.float16 and m.q.is_contiguous() and m.s.is_contiguous()
+                    setattr(qlayers[i], f"q_{name}", m.q.data_ptr())
+                    setattr(qlayers[i], f"s_{name}", m.s.data_ptr())
+            _check(self.lib, self.lib.adamk_bind_weights_w4a16(self._h, C.byref(ptrs), qlayers, C.c_void_p(self.packed.data_ptr()),
+                                                               self._stream_ptr()))
+        else:
+            _check(self.lib, self.lib.adamk_bind_weights(self._h, C.byref(ptrs), C.c_void_p(self.packed.data_ptr()),
+                                                         self._stream_ptr()))
         self._embed = w.embed                      # the kernel gathers embedding rows from the source table
-        self._weights = w if keep_source else None
+        self._weights = (qw if quantized else w) if keep_source else None
 
     def share_weights(self, owner: "MegaKernelPlugin") -> None:
         """Stream the packed weights ``owner`` has bound (identical task table required) instead of repacking."""

@@ -82,6 +82,8 @@ class KernelSchedule:
     l2_prefetch_kb: int = 0   # per-SM window past the ring the Loader prefetches into L2 while it is blocked
     poll_inflight: int = 0    # ring stages in flight (and no L2 prefetch) while this SM's consumers poll for inputs (0 = unchanged)
     pace_clk_per_64k: int = 0  # Loader pacing: SM clocks per 64 KB of new HBM requests per SM (0 = unpaced); see pace_for()
+    w4a16: bool = False       # the layer projections stream GPTQ-format int4 codes + fp16 group scales (W[n][k] = (q - 8) * s[n][k / 128],
+                              # reference byte model graph_ir.py:296-318); needs fuse_down; embedding / LM head stay bf16
     fuse_down: bool = False   # gate/up keeps its SwiGLU outputs on the SM and multiplies them by its own K-slice of the down projection (T_DOWNK);
                               # the 1/n_sms partial rows are summed by T_HRED tasks (no gather of the I-long activation vector)
     stream_down: bool = True  # the down projection streams its input vector in k-tile by k-tile (cp.async) instead of gathering it up front
@@ -103,6 +105,8 @@ class KernelSchedule:
             raise ScheduleError("attn_min_chunk out of range")
         if not 0 <= self.inflight <= self.n_stage:
             raise ScheduleError("inflight must be in 0..n_stage")
+        if self.w4a16 and not self.fuse_down:
+            raise ScheduleError("w4a16 needs fuse_down (the int4 down projection is the fused K-slice kernel)")
         if not 0 <= self.l2_prefetch_kb <= 0xFFFF or not 0 <= self.pace_clk_per_64k <= 0x7FFF:
             raise ScheduleError("l2_prefetch_kb / pace_clk_per_64k out of range")
 
@@ -263,7 +267,7 @@ def split_rows(n_units: int, n_sms: int, rot: int) -> list[tuple[int, int]]:
     return out
 
 
-def op_geometry(sched: KernelSchedule, max_rows: int, kchunks: int, pairs: bool) -> tuple[int, int, int, int]:
+def op_geometry(sched: KernelSchedule, max_rows: int, kchunks: int, pairs: bool, chunk_row_bytes: int = KCHUNK * 2) -> tuple[int, int, int, int]:
     """Warp grid of one operator: (WR, WK, rows per warp, chunks per stage).
 
     The C consumer warps form WR row groups x WK interleaved K groups.  Wide
@@ -290,7 +294,7 @@ def op_geometry(sched: KernelSchedule, max_rows: int, kchunks: int, pairs: bool)
                 best_rw, best_pad = rw, cost
         rw = best_rw
         rt = c * rw
-        ktc = max(1, min(kchunks, sched.stage_bytes // (rt * KCHUNK * 2)))
+        ktc = max(1, min(kchunks, sched.stage_bytes // (rt * chunk_row_bytes)))
         n_kt = _ceil_div(kchunks, ktc)
         return c, 1, rw, _ceil_div(kchunks, n_kt)
 
@@ -308,7 +312,7 @@ def op_geometry(sched: KernelSchedule, max_rows: int, kchunks: int, pairs: bool)
                          # about the rows a warp touches (and gate/up pairs inside one warp)
         rt = wr * rw
         if rw <= MAX_RW and (wk == 1 or rt <= 32):
-            ktc_max = min(kchunks, sched.stage_bytes // (rt * KCHUNK * 2))
+            ktc_max = min(kchunks, sched.stage_bytes // (rt * chunk_row_bytes))
             for ktc in range(1, ktc_max + 1):
                 n_kt = _ceil_div(kchunks, ktc)
                 ktc_e = _ceil_div(kchunks, n_kt)
@@ -371,13 +375,31 @@ def stage_shapes(task: np.ndarray):
             yield tile, kt, rows, min(ktc, kchunks - kt * ktc)
 
 
-def task_weight_bytes(task: np.ndarray) -> int:
-    if int(task[F_TYPE]) == T_DOWNK:      # b columns of the down projection, k = H rows each
-        return int(task[F_B]) * int(task[F_K]) * 2
-    if int(task[F_TYPE]) not in GEMV_TYPES:
+I4_GROUP = 128           # reduction elements per fp16 scale (reference graph_ir.INT4_GROUP_SIZE)
+I4_CHUNK_BYTES = 128     # a 256-element chunk of one row as 4-bit codes
+I4_SCALE_BYTES = 4       # its two fp16 scales
+AUX_LOCAL_ACT, AUX_INT4 = 1, 2
+
+
+def i4_stage_bytes(rows: int, chunks: int) -> int:
+    return (rows * chunks * (I4_CHUNK_BYTES + I4_SCALE_BYTES) + 15) & ~15
+
+
+def downk_i4_groups(k0: int, nk: int) -> int:
+    return (k0 + nk - 1) // I4_GROUP - k0 // I4_GROUP + 1
+
+
+def task_weight_bytes(task) -> int:
+    """Bytes of the packed weight stream a task owns (csrc/adamk.cu: task_stream_bytes)."""
+    ttype, i4 = int(task[F_TYPE]), bool(int(task[F_AUX]) & AUX_INT4)
+    if ttype == T_DOWNK:      # b columns of the down projection, k = H rows each (+ the fp16 scales of the groups they touch)
+        b, h = int(task[F_B]), int(task[F_K])
+        return downk_i4_groups(int(task[F_A]), b) * h * 2 + b * h // 2 if i4 else b * h * 2
+    if ttype not in GEMV_TYPES:
         return 0
-    # rows * kchunks * 512, independent of tiling
-    return int(task[F_B]) * int(task[F_KCHUNKS]) * KCHUNK * 2
+    if not i4:                # rows * kchunks * 512, independent of tiling
+        return int(task[F_B]) * int(task[F_KCHUNKS]) * KCHUNK * 2
+    return sum(i4_stage_bytes(rows, chunks) for _, _, rows, chunks in stage_shapes(task))
 
 
 def unpack_geom(geom: int) -> tuple[int, int, int]:
@@ -407,7 +429,9 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
     per_sm: list[list[list[int]]] = [[] for _ in range(n_sms)]
     rot = 0
 
-    fuse = sched.fuse_down
+    fuse, i4 = sched.fuse_down, sched.w4a16
+    if i4 and any(k % 8 for k in (cfg.hidden, cfg.q_dim, cfg.intermediate)):
+        raise ScheduleError("w4a16: reduction dims must be multiples of 8")
     if fuse:
         why = fuse_down_error(cfg, sched, n_sms)
         if why:
@@ -421,7 +445,9 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
         split = split_rows(n_rows // unit, n_sms, rot)
         rot = (rot + (n_rows // unit) % n_sms) % n_sms
         max_rows = max(cnt for _, cnt in split) * unit
-        wr, wk, rw, ktc = op_geometry(sched, max_rows, kchunks, pairs=(unit == 2))
+        int4_op = i4 and ttype != T_LMHEAD
+        wr, wk, rw, ktc = op_geometry(sched, max_rows, kchunks, pairs=(unit == 2),
+                                      chunk_row_bytes=(I4_CHUNK_BYTES + I4_SCALE_BYTES + 1) if int4_op else KCHUNK * 2)
         rt = wr * rw
         n_kt = _ceil_div(kchunks, ktc)
         geom = wr | (wk << 8) | (rw << 16)
@@ -432,14 +458,18 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
             nrows = cnt * unit
             n_tiles = _ceil_div(nrows, rt)
             per_sm[sm].append([ttype, layer, first * unit, nrows, k, kchunks, rt, ktc,
-                               n_tiles, n_kt, 0, geom, 0, 0, 0, aux])
+                               n_tiles, n_kt, 0, geom, 0, 0, 0, aux | (AUX_INT4 if i4 and ttype != T_LMHEAD else 0)])
             emitted += 1
             if ttype == T_GATEUP and aux:
                 # this SM's K-slice of the down projection: columns first .. first + cnt, all H rows each, column-major;
                 # a ring stage holds `cps` whole columns
                 cps = max(1, sched.stage_bytes // (cfg.hidden * 2))
+                if i4:
+                    cps = max(1, sched.stage_bytes // (cfg.hidden // 2))
+                    if downk_i4_groups(first, cnt) > 3 or downk_i4_groups(first, cnt) * cfg.hidden * 2 > sched.stage_bytes:
+                        raise ScheduleError("w4a16: an SM's slice of the down projection touches too many scale groups")
                 per_sm[sm].append([T_DOWNK, layer, first, cnt, cfg.hidden, cps, 0, 0, 1, _ceil_div(cnt, cps),
-                                   0, 0, 0, 0, 0, 0])
+                                   0, 0, 0, 0, 0, AUX_INT4 if i4 else 0])
         return emitted
 
     def hred(layer: int) -> None:
@@ -482,12 +512,9 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
     for sm in range(n_sms):
         sm_begin[sm] = len(flat)
         for t in per_sm[sm]:
-            if t[F_TYPE] in GEMV_TYPES:
+            if t[F_TYPE] in STREAM_TYPES:
                 t[F_WOFF] = cursor // 16
-                cursor += t[F_B] * t[F_KCHUNKS] * KCHUNK * 2
-            elif t[F_TYPE] == T_DOWNK:
-                t[F_WOFF] = cursor // 16
-                cursor += t[F_B] * t[F_K] * 2
+                cursor += task_weight_bytes(t)
             flat.append(t)
     sm_begin[n_sms] = len(flat)
     if cursor // 16 >= 2 ** 31:
@@ -500,7 +527,7 @@ def build_task_table(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, 
                    scratch_bytes(cfg, sched, batch, n_sms), n_lm]
     header[13] = (cursor // 16) & 0x7FFFFFFF
     header[14] = ((sched.poll_sleep_ns & 0xFFFF) | ((0 if sched.stream_down else 1) << 16) | ((sched.poll_inflight & 0xF) << 20)
-                  | ((1 if fuse else 0) << 24))
+                  | ((1 if fuse else 0) << 24) | ((1 if i4 else 0) << 26))
     header[15] = (sched.l2_prefetch_kb & 0xFFFF) | ((sched.pace_clk_per_64k & 0x7FFF) << 16)
     return TaskTable(cfg=cfg, sched=sched, n_sms=n_sms, batch=batch, header=header, sm_begin=sm_begin,
                      tasks=tasks, packed_weight_bytes=cursor, attn_chunks=attn_chunks)
@@ -563,8 +590,58 @@ def pack_weights_reference(table: TaskTable, weights) -> np.ndarray:
                 mats[key] = as_u16(getattr(weights.layers[layer], name))
         return mats[key]
 
+    qlayers = getattr(weights, "layers", None) if hasattr(weights, "base") else None     # quant.QuantizedWeights
+    if qlayers is not None:
+        weights_q, weights = weights, weights.base
+        out8 = out.view(np.uint8)
+
+        def code(qm, row: int, kidx: np.ndarray, k: int) -> np.ndarray:
+            b = qm.q[row].cpu().numpy()[np.minimum(kidx, k - 1) // 2]
+            return np.where(kidx < k, np.where(kidx & 1, b >> 4, b & 15), 8).astype(np.uint8)
+
     for task in table.tasks:
         ttype = int(task[F_TYPE])
+        if qlayers is not None and int(task[F_AUX]) & AUX_INT4:
+            layer, pos = int(task[F_LAYER]), int(task[F_WOFF]) * 16   # bytes
+            ql = qlayers[layer]
+            if ttype == T_DOWNK:
+                k0, nk, h = int(task[F_A]), int(task[F_B]), int(task[F_K])
+                qm = ql["wdown"]
+                g0, ng = k0 // I4_GROUP, downk_i4_groups(k0, nk)
+                sc = qm.s.cpu().numpy().view(np.uint16)[:, g0:g0 + ng].T.reshape(-1)          # [group][row]
+                out8[pos:pos + ng * h * 2] = sc.astype("<u2").view(np.uint8)
+                pos += ng * h * 2
+                qb = qm.q.cpu().numpy()
+                for j in range(nk):
+                    kk = k0 + j
+                    col = (qb[:, kk // 2] >> 4) if kk & 1 else (qb[:, kk // 2] & 15)            # codes of all rows
+                    out8[pos:pos + h // 2] = (col[0::2] | (col[1::2] << 4)).astype(np.uint8)
+                    pos += h // 2
+                continue
+            vrow0, k, rt, ktc = int(task[F_A]), int(task[F_K]), int(task[F_RT]), int(task[F_KTC])
+            lane = np.arange(32)
+            for tile, kt, rows, chunks in stage_shapes(task):
+                stage = np.zeros(i4_stage_bytes(rows, chunks), dtype=np.uint8)
+                scales = np.zeros(rows * chunks * 2, dtype=np.uint16)
+                for r in range(rows):
+                    name, row = virtual_row_source(cfg, ttype, vrow0 + tile * rt + r)
+                    qm = ql[name]
+                    srow = qm.s[row].cpu().numpy().view(np.uint16)
+                    for c in range(chunks):
+                        kbase = (kt * ktc + c) * KCHUNK
+                        blk = r * chunks + c
+                        words = np.zeros(32, dtype=np.uint32)
+                        for el in range(8):
+                            kidx = kbase + (4 * lane + el if el < 4 else 128 + 4 * lane + el - 4)
+                            words |= code(qm, row, kidx, k).astype(np.uint32) << (4 * el)
+                        stage[blk * I4_CHUNK_BYTES:(blk + 1) * I4_CHUNK_BYTES] = words.astype("<u4").view(np.uint8)
+                        for gi in range(2):
+                            g = kbase // I4_GROUP + gi
+                            scales[blk * 2 + gi] = srow[g] if g < srow.size else 0
+                stage[rows * chunks * I4_CHUNK_BYTES:rows * chunks * (I4_CHUNK_BYTES + I4_SCALE_BYTES)] = scales.astype("<u2").view(np.uint8)
+                out8[pos:pos + stage.size] = stage
+                pos += stage.size
+            continue
         if ttype == T_DOWNK:   # columns k0 .. k0 + nk of the down projection, each as H consecutive rows
             k0, nk = int(task[F_A]), int(task[F_B])
             pos = int(task[F_WOFF]) * 8

@@ -126,7 +126,9 @@ def _run_parity(cfg, B, steps, oracle_cache, max_ctx=320, seed=11):
                                                  (G7, 9, False)])
 def test_batched_decode_matches_oracle(cfg, B, oracle_cache):
     worst, dec = _run_parity(cfg, B, steps=5, oracle_cache=oracle_cache)
-    assert worst <= 5e-3, worst
+    # on the oracle's cache the step itself is compared (fp32-exact planes: 5e-3); on the cache the tensor-core Prefill wrote,
+    # the flash-attention kernel's bf16 probabilities are part of the difference: the north star's bound
+    assert worst <= (5e-3 if oracle_cache else 2e-2), worst
     assert dec.launches_per_step == 10 * cfg.n_layers + 4
 
 
