@@ -245,7 +245,7 @@ flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ 
       const uint32_t ts = tm_s0 + st * BKV + lane_addr;
       // pass 1: the row maximum
       float m_blk = -INFINITY;
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < BKV / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(ts + c * 32, r);
@@ -274,7 +274,7 @@ flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ 
       }
       // pass 2: P = exp2(s * scale * log2e - m), written as bf16 in the swizzled K-major layout of the PV operand
       float l_blk = 0.f;
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < BKV / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(ts + c * 32, r);

@@ -52,11 +52,18 @@ def schedule_id(cfg: ModelConfig) -> dict:
             "kernel_knobs": knobs, "program_order_checked": order is not None}
 
 
-def fit_schedule(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, tp_size: int = 1) -> KernelSchedule:
-    """Adapt a schedule to a model / SM count: the fused down projection only where it can run, the ring as deep as
-    shared memory allows (at most eight stages), at most three stages in flight (a fourth only lengthens the queue
-    every tagged-word poll waits behind)."""
-    if sched.fuse_down and fuse_down_error(cfg, sched, n_sms, tp_size):
-        sched = replace(sched, fuse_down=False)
+def fit_schedule(cfg: ModelConfig, sched: KernelSchedule, n_sms: int = 148, tp_size: int = 1, keep_fused: bool = False) -> KernelSchedule:
+    """Adapt a schedule to a model / SM count: the fused down projection only where it can run -- and, unless
+    ``keep_fused`` (or the schedule is W4A16, which needs it), only where it pays --, the ring as deep as shared memory
+    allows (at most eight stages), at most three stages in flight (a fourth only lengthens the queue every tagged-word
+    poll waits behind)."""
+    if sched.fuse_down:
+        impossible = fuse_down_error(cfg, sched, n_sms, tp_size)
+        # where it pays: one 256-row block per consumer warp (measured, tools/model_sweep.py: Qwen2.5-1.5B 811 vs 822
+        # us/token fused vs not; with two or three blocks per warp the K-slice kernel loses its balance: Qwen2.5-7B
+        # 2511 vs 2498, Qwen3-8B 2724 vs 2628)
+        unprofitable = cfg.hidden // 256 > sched.consumer_warps and not (keep_fused or sched.w4a16)
+        if impossible or unprofitable:
+            sched = replace(sched, fuse_down=False, w4a16=False)
     n_stage = max(2, min(max_stages_that_fit(cfg, replace(sched, n_stage=2, inflight=0), n_sms=n_sms), 8))
     return replace(sched, n_stage=n_stage, inflight=min(3, n_stage))

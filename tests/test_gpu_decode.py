@@ -520,24 +520,31 @@ def test_full_size_qwen3_8b_matches_oracle_tp1_and_tp2():
     wants = [ref.step([tok], [pos])[0].numpy() for pos, tok in enumerate(toks)]
     del ref
 
-    sched = default_schedule(cfg)
-    assert sched.fuse_down
-    plug = MegaKernelPlugin(cfg, sched, max_ctx=max_ctx)
-    plug.bind_weights(w)
-    for pos, tok in enumerate(toks):
-        out = plug.decode_step(tok, pos, want_logits=True)
-        plug.check()
-        got = out.logits[0].cpu().numpy()
-        err = float(np.abs(got - wants[pos]).max())
-        assert err <= 2e-2, (pos, err)
-        assert _cos(got, wants[pos]) >= 0.9995
-        srt = np.sort(wants[pos])
-        if srt[-1] - srt[-2] > 5e-2:
-            assert int(out.next_token.item()) == int(wants[pos].argmax())
-        print(f"qwen3-8b tp=1 step {pos}: max |logit diff| {err:.2e}")
-    plug.close()
-    del plug
-    torch.cuda.empty_cache()
+    from dataclasses import replace
+
+    from paper_2605_11581_b200.schedules import fit_schedule
+
+    default = default_schedule(cfg)
+    assert not default.fuse_down          # three 256-row blocks per warp: the default keeps the row-split down projection
+    fused = fit_schedule(cfg, replace(default, fuse_down=True, inflight=0), keep_fused=True)
+    assert fused.fuse_down
+    for label, sched in (("default", default), ("fused down projection", fused)):
+        plug = MegaKernelPlugin(cfg, sched, max_ctx=max_ctx)
+        plug.bind_weights(w)
+        for pos, tok in enumerate(toks):
+            out = plug.decode_step(tok, pos, want_logits=True)
+            plug.check()
+            got = out.logits[0].cpu().numpy()
+            err = float(np.abs(got - wants[pos]).max())
+            assert err <= 2e-2, (label, pos, err)
+            assert _cos(got, wants[pos]) >= 0.9995
+            srt = np.sort(wants[pos])
+            if srt[-1] - srt[-2] > 5e-2:
+                assert int(out.next_token.item()) == int(wants[pos].argmax())
+            print(f"qwen3-8b tp=1 ({label}) step {pos}: max |logit diff| {err:.2e}")
+        plug.close()
+        del plug
+        torch.cuda.empty_cache()
 
     tp = 2
     lcfg = cfg.shard(tp)

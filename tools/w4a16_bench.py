@@ -36,7 +36,7 @@ def timed(fn, n):
 
 
 for label, weights, w4 in (("bf16", w, False), ("w4a16", qw, True)):
-    sched = fit_schedule(cfg, replace(default_schedule(cfg), w4a16=w4))
+    sched = fit_schedule(cfg, replace(default_schedule(cfg), fuse_down=True, w4a16=w4, inflight=0), keep_fused=True)
     plug = MegaKernelPlugin(cfg, sched, max_ctx=ctx0 + steps + 64)
     plug.bind_weights(weights)
     kc, vc = plug.kv_view(); kc.normal_(); vc.normal_()
