@@ -166,7 +166,7 @@ def prefill_sample(cfg, w, dev, local: int, tokens: int = 4096, iters: int = 5) 
     pfile = ROOT / "MEASURED_PEAKS.json"
     if pfile.exists():
         peak = json.loads(pfile.read_text()).get("bf16_tflops_sustained")
-    out = {"tokens": tokens, "attention": "library flash (bf16)", "peak_tflops": peak, "peak_kind": "measured sustained cuBLAS bf16"}
+    out = {"tokens": tokens, "attention": "own tcgen05 flash kernel (csrc/prefill_attn.cu, bf16 Q/K/V/P, fp32 scores and output)", "peak_tflops": peak, "peak_kind": "measured sustained cuBLAS bf16"}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for planes in (1, 2):
         pre = TensorCorePrefill(cfg, w, plug, planes=planes, attention="bf16")
@@ -182,9 +182,9 @@ def prefill_sample(cfg, w, dev, local: int, tokens: int = 4096, iters: int = 5) 
         ms = e0.elapsed_time(e1) / iters
         mats = cfg.qkv_rows * cfg.hidden + cfg.hidden * cfg.q_dim + 3 * cfg.intermediate * cfg.hidden
         flops = 2.0 * tokens * mats * cfg.n_layers * planes
-        # the O projection always reads the single bf16 plane attention produces
-        flops -= 2.0 * tokens * cfg.q_dim * cfg.hidden * cfg.n_layers * (planes - 1)
-        out[f"planes{planes}"] = {"ms": ms, "tokens_per_s": tokens * 1e3 / ms, "gemm_tflops": flops / ms / 1e9,
+        # + causal attention (QK^T and PV, half of the square), one plane
+        flops += 4.0 * cfg.n_q_heads * cfg.head_dim * tokens * tokens / 2 * cfg.n_layers
+        out[f"planes{planes}"] = {"ms": ms, "tokens_per_s": tokens * 1e3 / ms, "tflops": flops / ms / 1e9,
                                   "frac_of_peak": None if not peak else flops / ms / 1e9 / peak,
                                   "own_kernel_launches": (pre.launches - n0) // iters}
         del pre

@@ -18,11 +18,10 @@ Qwen2/Qwen3 decoder definition (Hugging Face ``transformers`` 5.5.0,
       -> W_o -> +x -> RMSNorm -> W_down(SiLU(W_gate x) * W_up x) -> +
     final RMSNorm -> LM head -> argmax.
 
-Parity pin: ``tests/test_oracle_vs_hf.py`` checks this restatement against
-``transformers.Qwen2ForCausalLM`` / ``Qwen3ForCausalLM`` run in this container
-(fp32 compute on the same bf16-rounded weights), and ``tests/golden/`` holds
-logits/token fixtures produced by ``tools/make_decode_golden.py`` from that HF
-run.  Parity of the numeric half is pinned to Hugging Face, not to the
+Parity pin: ``tools/make_decode_golden.py`` runs ``transformers.Qwen2ForCausalLM`` /
+``Qwen3ForCausalLM`` in the build container (fp32 compute on the same bf16-rounded
+weights) and stores logits / tokens under ``tests/golden/decode_*.npz``;
+``tests/test_oracle_decode.py`` checks this restatement against those fixtures.  Parity of the numeric half is pinned to Hugging Face, not to the
 reference repo (which has nothing to pin against).
 
 Numerical contract shared with the CUDA kernel: weights are bf16 in memory and

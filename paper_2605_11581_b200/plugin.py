@@ -169,20 +169,22 @@ class MegaKernelPlugin:
         self.launches = 0
 
     @classmethod
-    def from_trace(cls, cfg: ModelConfig, trace_text, max_ctx: int, device: int | str = 0, **schedule_overrides):
-        """Build the plugin from a SolidifiedTrace (``mkplan search --out``; reference ``search.py:79-107``): the
-        plan's tile, ring depth and consumer-warp count become the kernel schedule (KernelSchedule.from_plan);
-        run-time knobs the planner does not model (split-KV chunk, L2 prefetch window) come as overrides."""
+    def from_trace(cls, cfg: ModelConfig, trace_text, max_ctx: int, device: int | str = 0, graph_text: str | None = None,
+                   hw_text: str | None = None, **kernel_knobs):
+        """Build the plugin from a SolidifiedTrace (``mkplan search --out``; reference ``search.py:79-171``).
+        ``KernelSchedule.from_plan`` lowers the plan: tile -> ring stage geometry, consumer warps, ``stride_eff`` -> the
+        Loader's stages in flight, ``n_stage`` / ``window`` checked against the ring depth Eq.1 / Eq.2 give on this
+        kernel's shared-memory accounting.  With the trace's ``graph_text`` / ``hw_text`` the plan's Loader / Consumer
+        programs are checked against the order the kernel replays (``solidify.check_program_order``).  Run-time knobs
+        the planner does not model (split-KV chunk, L2 prefetch window, fused down projection) come as ``kernel_knobs``."""
         from .mkplan.search import parse_trace
+        from .solidify import check_program_order, schedule_from_trace
 
         trace = parse_trace(trace_text if isinstance(trace_text, (bytes, bytearray)) else str(trace_text).encode())
-        sched = KernelSchedule.from_plan(trace.plan, **schedule_overrides)
-        from .task_table import max_stages_that_fit
-
-        fit = max_stages_that_fit(cfg, sched)
-        if sched.n_stage > fit:
-            sched = KernelSchedule.from_plan(trace.plan, **dict(schedule_overrides, n_stage=max(2, fit)))
-        return cls(cfg, sched, max_ctx, device=device)
+        if graph_text is not None and hw_text is not None:
+            check_program_order(trace, graph_text, hw_text)
+        n_sms = device_sm_count(device if isinstance(device, int) else torch.device(device).index or 0)
+        return cls(cfg, schedule_from_trace(cfg, trace, kernel_knobs, n_sms=n_sms), max_ctx, device=device)
 
     # -- weights -------------------------------------------------------------
     def bind_weights(self, w, keep_source: bool = False) -> None:

@@ -2,18 +2,18 @@
 
 ``PAPER.md:244-249`` runs Prefill on the serving engine's operators and Decode on the MegaKernel.  This module is
 that Prefill half built from ``include/adamk_prefill.h``: a tcgen05 / tensor-memory GEMM
-(``csrc/prefill_gemm.cu``) with fused bias, residual and SwiGLU epilogues, and the row kernels around it
-(``csrc/prefill_ops.cu``).  Layer dataflow for ``T`` prompt tokens::
+(``csrc/prefill_gemm.cu``) with fused bias, residual and SwiGLU epilogues, a tcgen05 causal flash-attention kernel
+(``csrc/prefill_attn.cu``) and the row kernels around them (``csrc/prefill_ops.cu``).  Layer dataflow for ``T`` prompt tokens::
 
     h fp32 [T, H] --rmsnorm_split--> planes --GEMM(wqkv)+bias--> qkv fp32 --rope_store--> q, KV cache (bf16)
-      --attention--> a --GEMM(wo) += h--> h --rmsnorm_split--> planes --GEMM(gate|up) SwiGLU--> act planes
+      --V^T, flash attention--> a planes --GEMM(wo) += h--> h --rmsnorm_split--> planes --GEMM(gate|up) SwiGLU--> act planes
       --GEMM(wdown) += h--> h
 
 ``planes`` = 2 keeps the decode kernel's numerical contract (fp32 activations against exact bf16 weights: each fp32
 value enters the tensor cores as hi + lo bf16 planes); ``planes`` = 1 is plain bf16 activations at half the
-tensor work.  Causal attention over the bf16 cache is the one operator still taken from the library
-(``torch.nn.functional.scaled_dot_product_attention``): ~5 % of the Prefill FLOPs at 4K tokens; a tcgen05
-flash-attention kernel is the open item of this row.  There is no CPU path.
+tensor work.  Causal attention over the bf16 cache (as the decode kernel will see it) is the flash kernel in either
+mode: bf16 Q / K / V / P, fp32 scores, softmax state and output -- no library operator is left on this path.  There
+is no CPU path.
 """
 
 from __future__ import annotations

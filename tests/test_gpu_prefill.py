@@ -188,7 +188,7 @@ def test_hybrid_engine_tensor_prefill_matches_oracle(cfg):
     g = torch.Generator().manual_seed(7)
     prompt = torch.randint(0, cfg.vocab, (150,), generator=g).tolist()
     want, logits = ref.generate(prompt, 24)
-    eng = HybridEngine(cfg, w, max_ctx=256, schedule=default_schedule(cfg), prefill_backend="tensor")
+    eng = HybridEngine(cfg, w, max_ctx=256, schedule=default_schedule(cfg), prefill_backend="tensor", prefill_planes=2)
     res = eng.generate(prompt, 24)
     srt = torch.stack(logits).sort(dim=1).values
     margin = (srt[:, -1] - srt[:, -2]).numpy()
