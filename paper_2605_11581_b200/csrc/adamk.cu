@@ -2047,7 +2047,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
         next_ok = max(next_ok, now - kPaceBurstClk) + (((long long)nb * pace) >> 16);
       };
       auto blocked_wait = [&](uint32_t bar, uint32_t parity, int code, int ti) {
-        if (mbar_try_wait(bar, parity)) return;
+        if (mbar_test_wait(bar, parity)) return;   // test, not try: try_wait may suspend the lane for its whole time limit, and that time is the prefetcher's
         if (p.pf_window_bytes > 0 && !p.probe) {
           const long long t0 = clock64();
           if (pf < wcur) pf = wcur;

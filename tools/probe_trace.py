@@ -30,10 +30,12 @@ tasks = plug.table.tasks
 ran = t[:, 7] > 0
 t0 = t[ran][:, 0].min()
 print(f"mode {mode}: total {(t[ran][:, 7].max() - t0) / 1e3:.1f} us")
-for ty in tt.GEMV_TYPES:
+for ty in tuple(tt.GEMV_TYPES) + (tt.T_DOWNK,):
     m = ran & (tasks[:, tt.F_TYPE] == ty)
+    if not m.any():
+        continue
     d = (t[m][:, 7] - t[m][:, 0]) / 1e3
-    byts = tasks[m][:, tt.F_B].astype(np.float64) * tasks[m][:, tt.F_KCHUNKS] * 512
+    byts = np.array([tt.task_weight_bytes(row) for row in tasks[m]], dtype=np.float64) if hasattr(tt, 'task_weight_bytes') else tasks[m][:, tt.F_B].astype(np.float64) * tasks[m][:, tt.F_KCHUNKS] * 512
     print(f"  {tt.TYPE_NAMES[ty]:7s} n={m.sum():6d} body mean {d.mean():7.3f} us  KB/task {byts.mean() / 1e3:8.1f}  -> {byts.sum() / d.sum() / 1e3:7.1f} KB/us per SM")
 gaps = []
 for sm in range(plug.n_sms):

@@ -31,7 +31,7 @@ C7 = dict(B, consumer_warps=7, attn_min_chunk=128)
 D7 = dict(C7, rows_per_tile=56, ktile_chunks=2, n_stage=3, l2_prefetch_kb=512)
 D7 = dict(C7, l2_prefetch_kb=512, attn_min_chunk=112)
 D7 = dict(C7, l2_prefetch_kb=512, attn_min_chunk=112, rows_per_tile=42, ktile_chunks=2, n_stage=4)
-D7 = dict(consumer_warps=7, rows_per_tile=42, ktile_chunks=2, n_stage=4, attn_min_chunk=112, l2_prefetch_kb=512)
+D7 = dict(consumer_warps=7, rows_per_tile=42, ktile_chunks=2, n_stage=5, attn_min_chunk=112, l2_prefetch_kb=512)
 scheds = [
     ("fused", dict(D7, inflight=3, fuse_down=True)),
     ("base", dict(D7)),
