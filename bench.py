@@ -283,18 +283,12 @@ def run_ours(args) -> None:
 
     # ---- end to end through the host-facing call ----
     prefill()
-    host_in = torch.zeros(2, dtype=torch.int32).pin_memory()
-    host_out = torch.zeros(1, dtype=torch.int32).pin_memory()
     tok, pos = prompt[-1], PROMPT_LEN - 1
 
     def e2e_step(tok, pos):
-        host_in[0], host_in[1] = tok, pos
-        plug.tokens.copy_(host_in[0:1], non_blocking=True)
-        plug.positions.copy_(host_in[1:2], non_blocking=True)
-        plug.enqueue(want_logits=False, auto_advance=False)
-        host_out.copy_(plug.next_token, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
-        return int(host_out[0]), pos + 1
+        # adamk_decode_step_host: H2D copy of (token, position) from pinned host memory, one launch, D2H copy of the
+        # greedy token, stream synchronise -- one C-ABI call per token
+        return plug.decode_step_host(tok, pos), pos + 1
 
     for _ in range(args.warmup):
         tok, pos = e2e_step(tok, pos)

@@ -157,6 +157,17 @@ int adamk_decode_step(adamk_handle h, int32_t* token_ids, int32_t* positions, in
                       float* logits_out, int32_t* next_token_out, int auto_advance,
                       adamk_stream stream);
 
+/* The same step with HOST buffers, for a caller that feeds one token at a time (the serving engine's
+ * decode hook): copies token_ids / positions (HOST int32[batch], pinned memory for the copies
+ * to be asynchronous) into the device state, launches the step (auto_advance = 0), copies the greedy next token
+ * into next_token_host (HOST int32[batch]) and waits for the stream.  One library call per token instead of
+ * three copies, a launch and a synchronise issued from the host language. */
+int adamk_decode_step_host(adamk_handle h, const int32_t* token_ids_host, const int32_t* positions_host, int batch,
+                           int32_t* token_ids, int32_t* positions,
+                           void* k_cache, void* v_cache, void* workspace,
+                           float* logits_out, int32_t* next_token_out, int32_t* next_token_host,
+                           adamk_stream stream);
+
 /* Poll the device-written status block (host-mapped); 0 = no error recorded.
  * Fills `info` (8 ints: code, sm, task, tag seen, tag expected, detail, thread, -) if not NULL. */
 int adamk_device_status(adamk_handle h, int32_t* info);

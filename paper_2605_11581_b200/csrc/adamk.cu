@@ -2858,6 +2858,28 @@ int adamk_decode_step(adamk_handle h, int32_t* token_ids, int32_t* positions, in
   return launch(h, p, (cudaStream_t)stream);
 }
 
+int adamk_decode_step_host(adamk_handle h, const int32_t* token_ids_host, const int32_t* positions_host, int batch,
+                           int32_t* token_ids, int32_t* positions, void* k_cache, void* v_cache, void* workspace,
+                           float* logits_out, int32_t* next_token_out, int32_t* next_token_host, adamk_stream stream) {
+  if (!token_ids_host || !positions_host || !next_token_host || !token_ids || !positions || !next_token_out)
+    return fail(ADAMK_E_INVALID, "NULL argument");
+  if (!h || batch != h->batch) return fail(ADAMK_E_INVALID, "batch does not match the task table");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t nb = (size_t)batch * sizeof(int32_t);
+  if (positions == token_ids + batch && positions_host == token_ids_host + batch) {   // adjacent state: one copy
+    CUDA_TRY(cudaMemcpyAsync(token_ids, token_ids_host, 2 * nb, cudaMemcpyHostToDevice, st));
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(token_ids, token_ids_host, nb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(positions, positions_host, nb, cudaMemcpyHostToDevice, st));
+  }
+  const int rc = adamk_decode_step(h, token_ids, positions, batch, k_cache, v_cache, workspace, logits_out, next_token_out, 0, stream);
+  if (rc != ADAMK_OK) return rc;
+  CUDA_TRY(cudaMemcpyAsync(next_token_host, next_token_out, nb, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (h->status_host[0] != 0) return fail(ADAMK_E_DEVICE, "the step reported a device error; see adamk_device_status");
+  return ADAMK_OK;
+}
+
 int adamk_stream_probe(adamk_handle h, float* sink, int mode, adamk_stream stream) {
   if (!h || !sink) return fail(ADAMK_E_INVALID, "NULL argument");
   if (!h->bound) return fail(ADAMK_E_STATE, "adamk_bind_weights has not been called");

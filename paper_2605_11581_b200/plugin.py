@@ -63,6 +63,7 @@ EXPORTS = (
     "adamk_packed_bytes", "adamk_bind_weights", "adamk_bind_peers", "adamk_workspace_bytes",
     "adamk_workspace_init", "adamk_kv_cache_bytes", "adamk_decode_step", "adamk_device_status",
     "adamk_stream_probe", "adamk_trace_bytes", "adamk_set_trace", "adamk_share_weights", "adamk_bind_weights_w4a16",
+    "adamk_decode_step_host",
 )
 
 _lib = None
@@ -99,6 +100,7 @@ def load_library() -> C.CDLL:
     lib.adamk_workspace_init.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     lib.adamk_decode_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+    lib.adamk_decode_step_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int] + [C.c_void_p] * 9
     lib.adamk_device_status.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
     lib.adamk_stream_probe.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     if lib.adamk_abi_version() != ABI_VERSION:
@@ -161,8 +163,10 @@ class MegaKernelPlugin:
         kv_elems = self.lib.adamk_kv_cache_bytes(h) // 2
         self.k_cache = torch.zeros(kv_elems, dtype=torch.bfloat16, device=self.device)
         self.v_cache = torch.zeros(kv_elems, dtype=torch.bfloat16, device=self.device)
-        self.tokens = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.positions = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._state = torch.zeros(2, dtype=torch.int32, device=self.device)   # token | position, adjacent: one H2D copy
+        self.tokens = self._state[0:1]
+        self.positions = self._state[1:2]
+        self._host_io = None                      # pinned int32[3]: token, position | next token (decode_step_host)
         self.next_token = torch.zeros(1, dtype=torch.int32, device=self.device)
         # logits of the whole vocabulary; a tensor-parallel rank fills its own slice [rank * V/tp, (rank + 1) * V/tp)
         self.logits = torch.zeros(1, cfg.vocab * self.tp_size, dtype=torch.float32, device=self.device)
@@ -263,6 +267,25 @@ class MegaKernelPlugin:
         self.set_state(token, position)
         self.enqueue(want_logits=want_logits, auto_advance=False)
         return StepOutput(self.next_token, self.logits if want_logits else None)
+
+    def decode_step_host(self, token: int, position: int, want_logits: bool = False) -> int:
+        """The serving engine's per-token hook with HOST buffers (``adamk_decode_step_host``): token and position go
+        from pinned host memory to the device, one launch, the greedy next token comes back; returns it."""
+        if self._host_io is None:
+            self._host_io = torch.zeros(3, dtype=torch.int32).pin_memory()
+            self._host_np = self._host_io.numpy()
+        io = self._host_np
+        io[0], io[1] = token, position
+        base = self._host_io.data_ptr()
+        _check(self.lib, self.lib.adamk_decode_step_host(
+            self._h, C.c_void_p(base), C.c_void_p(base + 4), 1,
+            C.c_void_p(self.tokens.data_ptr()), C.c_void_p(self.positions.data_ptr()),
+            C.c_void_p(self.k_cache.data_ptr()), C.c_void_p(self.v_cache.data_ptr()),
+            C.c_void_p(self.workspace.data_ptr()),
+            C.c_void_p(self.logits.data_ptr()) if want_logits else None,
+            C.c_void_p(self.next_token.data_ptr()), C.c_void_p(base + 8), self._stream_ptr()))
+        self.launches += 1
+        return int(io[2])
 
     def check(self) -> None:
         """Synchronise and raise if the kernel reported an error."""

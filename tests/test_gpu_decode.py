@@ -156,6 +156,37 @@ def test_device_resident_greedy_loop_matches_oracle(cfg):
     plug.close()
 
 
+def test_host_buffer_step_equals_the_device_resident_loop():
+    """`adamk_decode_step_host` (host token / position in, host next token out, one C call per token) produces the
+    token sequence of the device-resident loop, and reports bad arguments."""
+    cfg = TINY
+    _, ref, plug = _setup(cfg, SCHEDS["c7"])
+    g = torch.Generator().manual_seed(5)
+    prompt = torch.randint(0, cfg.vocab, (16,), generator=g).tolist()
+    for pos, tok in enumerate(prompt[:-1]):
+        plug.decode_step(tok, pos, want_logits=False)
+    plug.set_state(prompt[-1], len(prompt) - 1)
+    dev = []
+    for _ in range(24):
+        plug.enqueue(want_logits=False, auto_advance=True)
+        dev.append(plug.next_token.clone())
+    plug.check()
+    dev = [int(t.item()) for t in dev]
+    tok, pos, host = prompt[-1], len(prompt) - 1, []
+    for _ in range(24):
+        tok = plug.decode_step_host(tok, pos)
+        pos += 1
+        host.append(tok)
+    assert host == dev
+    assert int(plug.next_token.item()) == host[-1] and int(plug.positions.item()) == pos - 1
+    plug.close()
+    from paper_2605_11581_b200.plugin import AdamkError, MegaKernelPlugin
+    unbound = MegaKernelPlugin(TINY, SCHEDS["c7"], max_ctx=64)
+    with pytest.raises(AdamkError):          # step before bind_weights
+        unbound.decode_step_host(1, 0)
+    unbound.close()
+
+
 @pytest.mark.parametrize("sname", ["c8", "c7"])
 def test_long_context_split_kv(sname):
     """Context 700 with a small min chunk -> every chunk slot active, multi-block units, multi-record merge."""
