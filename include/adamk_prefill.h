@@ -107,6 +107,46 @@ int adamk_prefill_rope_store(const float* qkv, int T, int n_q, int n_kv, int D, 
                              const float* cos, const float* sin, int pos0, int max_ctx, void* q_out, int q_is_bf16, void* k_cache,
                              void* v_cache, adamk_pf_stream stream);
 
+/* ---- the whole Prefill pass behind one call (csrc/prefill_pass.cu) ------------------------
+ * What the serving engine's Prefill phase hands to this library: T prompt tokens in, rows
+ * pos0 .. pos0 + T - 1 of every layer of the decode kernel's KV cache filled, final hidden states out.  Host-side
+ * orchestration of the operators above on one stream (embedding, then per layer: RMSNorm + plane split, QKV GEMM + bias,
+ * rotary embedding + cache write, V transpose, causal flash attention, O GEMM += residual, RMSNorm + split, gate/up GEMM
+ * with SwiGLU, down GEMM += residual): 1 + 9 launches per layer, asynchronous, no allocation. */
+typedef struct {
+  int n_layers, hidden, n_q_heads, n_kv_heads, head_dim;
+  int intermediate_padded;      /* I rounded up to a multiple of 128: rows / 2 of wgu, columns of wdown (zero padded) */
+  int max_ctx;                  /* rows per head of the KV cache and of the rope tables */
+  float rms_eps;
+  long long kv_layer_stride;    /* BYTES between consecutive layers of k_cache / v_cache (the plugin's cache:
+                                   max_batch * n_kv_heads * max_ctx * head_dim * 2) */
+} AdamkPrefillModel;
+
+typedef struct {
+  const void* ln1;      /* bf16 [hidden] */
+  const void* ln2;      /* bf16 [hidden] */
+  const void* wqkv;     /* bf16 [(n_q + 2 n_kv) * head_dim, hidden]: q, k, v rows concatenated */
+  const float* bqkv;    /* fp32 [(n_q + 2 n_kv) * head_dim] or NULL */
+  const void* wo;       /* bf16 [hidden, n_q * head_dim] */
+  const void* wgu;      /* bf16 [2 * intermediate_padded, hidden]: gate / up interleaved in blocks of 128 features */
+  const void* wdown;    /* bf16 [hidden, intermediate_padded] */
+  const void* q_norm;   /* bf16 [head_dim] or NULL (Qwen3) */
+  const void* k_norm;   /* bf16 [head_dim] or NULL */
+} AdamkPrefillLayer;
+
+/* Scratch the pass needs for T tokens at offset pos0 with `planes` (1 | 2) bf16 planes per activation; 0 = bad arguments. */
+size_t adamk_prefill_workspace_bytes(const AdamkPrefillModel* model, int T, int pos0, int planes);
+
+/* tokens: DEVICE int32 [T]; embed bf16 [vocab, hidden]; rope_cos / rope_sin fp32 [max_ctx, head_dim / 2] (the decode
+ * kernel's tables); k_cache / v_cache: sequence 0 of layer 0 of the decode kernel's cache; workspace: DEVICE,
+ * adamk_prefill_workspace_bytes, 256-byte aligned; hidden: DEVICE fp32 [T, hidden], the final hidden states (before
+ * the final norm).  pos0 > 0 = chunked Prefill: rows 0 .. pos0 - 1 must already be cached. */
+int adamk_prefill(const AdamkPrefillModel* model, const AdamkPrefillLayer* layers, const void* embed, const float* rope_cos,
+                  const float* rope_sin, const int32_t* tokens, int T, int pos0, int planes, void* k_cache, void* v_cache,
+                  void* workspace, float* hidden, adamk_pf_stream stream);
+
+const char* adamk_prefill_pass_last_error(void);
+
 /* ---- batched decode: one new token per sequence, B sequences per step -------------
  * The projections are adamk_prefill_gemm with T = B and the ATOMIC / SWIGLU / STORE epilogues; these are the operators
  * between them.  Caches: bf16 [B][n_kv][max_ctx][D] per layer (seq_stride = elements between sequences). */

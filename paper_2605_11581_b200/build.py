@@ -13,7 +13,7 @@ from pathlib import Path
 
 CSRC = Path(__file__).resolve().parent / "csrc"
 LIB = CSRC / "libadamk.so"
-SOURCES = [CSRC / "adamk.cu", CSRC / "prefill_gemm.cu", CSRC / "prefill_ops.cu", CSRC / "prefill_attn.cu"]
+SOURCES = [CSRC / "adamk.cu", CSRC / "prefill_gemm.cu", CSRC / "prefill_ops.cu", CSRC / "prefill_attn.cu", CSRC / "prefill_pass.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

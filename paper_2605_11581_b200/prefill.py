@@ -35,7 +35,20 @@ PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_p
                    "adamk_prefill_gemm_plan", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
                    "adamk_prefill_split", "adamk_prefill_rope_store", "adamk_batch_rope_store", "adamk_batch_attention_workspace",
                    "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split", "adamk_batch_embed",
-                   "adamk_prefill_attention", "adamk_prefill_vt", "adamk_prefill_attention_last_error")
+                   "adamk_prefill_attention", "adamk_prefill_vt", "adamk_prefill_attention_last_error",
+                   "adamk_prefill", "adamk_prefill_workspace_bytes", "adamk_prefill_pass_last_error")
+
+
+class _PassModel(C.Structure):          # include/adamk_prefill.h: AdamkPrefillModel
+    _fields_ = [("n_layers", C.c_int), ("hidden", C.c_int), ("n_q_heads", C.c_int), ("n_kv_heads", C.c_int), ("head_dim", C.c_int),
+                ("intermediate_padded", C.c_int), ("max_ctx", C.c_int), ("rms_eps", C.c_float), ("kv_layer_stride", C.c_longlong)]
+
+
+_PASS_LAYER_FIELDS = ("ln1", "ln2", "wqkv", "bqkv", "wo", "wgu", "wdown", "q_norm", "k_norm")
+
+
+class _PassLayer(C.Structure):          # include/adamk_prefill.h: AdamkPrefillLayer
+    _fields_ = [(n, C.c_void_p) for n in _PASS_LAYER_FIELDS]
 
 _declared = False
 
@@ -59,6 +72,10 @@ def _lib():
         lib.adamk_prefill_attention.argtypes = [vp, vp, vp, i, i, i, i, i, i, i, vp, i, vp]
         lib.adamk_prefill_vt.argtypes = [vp, i, i, i, i, i, vp, vp]
         lib.adamk_prefill_attention_last_error.restype = C.c_char_p
+        lib.adamk_prefill_pass_last_error.restype = C.c_char_p
+        lib.adamk_prefill_workspace_bytes.argtypes = [C.POINTER(_PassModel), i, i, i]
+        lib.adamk_prefill_workspace_bytes.restype = C.c_size_t
+        lib.adamk_prefill.argtypes = [C.POINTER(_PassModel), C.POINTER(_PassLayer), vp, vp, vp, vp, i, i, i, vp, vp, vp, vp, vp]
         lib.adamk_prefill_rmsnorm_split.argtypes = [vp, vp, f, i, i, vp, i, vp]
         lib.adamk_prefill_split.argtypes = [vp, ll, vp, i, vp]
         lib.adamk_prefill_rope_store.argtypes = [vp, i, i, i, i, vp, vp, f, vp, vp, i, i, vp, i, vp, vp, vp]
@@ -156,6 +173,7 @@ class TensorCorePrefill:
         self.cfg, self.plugin, self.planes = cfg, plugin, planes
         dev = plugin.device
         self.launches = 0
+        self._ws, self._pass = None, None
         if layers is not None:
             self.embed, self.layers = embed, layers
             return
@@ -182,42 +200,41 @@ class TensorCorePrefill:
         """Fill cache rows ``pos0 .. pos0 + T - 1`` of every layer from ``toks`` (int32 / int64 [T] on the device) and
         return the final hidden states fp32 [T, H].  ``pos0`` must be 0 unless the earlier rows are already cached
         (chunked prefill attends to them)."""
-        cfg, plug, P, lib, st = self.cfg, self.plugin, self.planes, _lib(), _stream()
+        cfg, plug, P, lib = self.cfg, self.plugin, self.planes, _lib()
         T = int(toks.numel())
         if T == 0:
             return torch.empty(0, cfg.hidden, device=plug.device)
         if pos0 + T > plug.max_ctx:
             raise ValueError("prompt does not fit the KV cache")
-        dev, H, D, nq, nkv = plug.device, cfg.hidden, cfg.head_dim, cfg.n_q_heads, cfg.n_kv_heads
-        bf = torch.bfloat16
+        dev = plug.device
         toks32 = toks.to(device=dev, dtype=torch.int32).contiguous()
-        h = torch.empty(T, H, dtype=torch.float32, device=dev)
-        xp = torch.empty(P, T, H, dtype=bf, device=dev)
-        qkv = torch.empty(T, (nq + 2 * nkv) * D, dtype=torch.float32, device=dev)
-        q = torch.empty(nq, T, D, dtype=bf, device=dev)
-        ap = torch.empty(P, T, nq * D, dtype=bf, device=dev)
-        act = torch.empty(P, T, self.layers[0]["i_pad"], dtype=bf, device=dev)
-        ctx = pos0 + T
-        ctx_pad = -(-ctx // 64) * 64
-        vt = torch.empty(nkv, D, ctx_pad, dtype=bf, device=dev)     # V^T of the current layer (K-major operand of P.V)
+        model, layers = self._pass_args()
+        need = lib.adamk_prefill_workspace_bytes(C.byref(model), T, pos0, P)
+        if need == 0:
+            raise AdamkError(-1, "adamk_prefill_workspace_bytes rejected the model / shape")
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        h = torch.empty(T, cfg.hidden, dtype=torch.float32, device=dev)
         cos, sin = plug._rope
         kc, vc = plug.kv_view()
-        _ok(lib.adamk_prefill_embed(_ptr(toks32), T, _ptr(self.embed), H, _ptr(h), st))
-        n = 1
-        for l, lw in enumerate(self.layers):
-            _ok(lib.adamk_prefill_rmsnorm_split(_ptr(h), _ptr(lw["ln1"]), cfg.rms_eps, T, H, _ptr(xp), P, st))
-            gemm(xp, lw["wqkv"], qkv, bias=lw["bqkv"])
-            _ok(lib.adamk_prefill_rope_store(_ptr(qkv), T, nq, nkv, D, _ptr(lw["q_norm"]), _ptr(lw["k_norm"]), cfg.rms_eps,
-                                             _ptr(cos), _ptr(sin), pos0, plug.max_ctx, _ptr(q), 1,
-                                             _ptr(kc[l, 0]), _ptr(vc[l, 0]), st))
-            # causal attention over the bf16 cache contents, as the decode kernel sees them: tcgen05 flash kernel
-            _attn_ok(lib.adamk_prefill_vt(_ptr(vc[l, 0]), nkv, D, plug.max_ctx, ctx, ctx_pad, _ptr(vt), st))
-            _attn_ok(lib.adamk_prefill_attention(_ptr(q), _ptr(kc[l, 0]), _ptr(vt), T, pos0, nq, nkv, D, plug.max_ctx, ctx_pad,
-                                                 _ptr(ap), P, st))
-            gemm(ap, lw["wo"], h, epilogue=EPI_RESID)
-            _ok(lib.adamk_prefill_rmsnorm_split(_ptr(h), _ptr(lw["ln2"]), cfg.rms_eps, T, H, _ptr(xp), P, st))
-            gemm(xp, lw["wgu"], act, epilogue=EPI_SWIGLU)
-            gemm(act, lw["wdown"], h, epilogue=EPI_RESID)
-            n += 9
-        self.launches += n
+        # ONE library call enqueues the whole pass (csrc/prefill_pass.cu): 1 + 9 launches per layer
+        if lib.adamk_prefill(C.byref(model), layers, _ptr(self.embed), _ptr(cos), _ptr(sin), _ptr(toks32), T, pos0, P,
+                             _ptr(kc[0, 0]), _ptr(vc[0, 0]), _ptr(self._ws), _ptr(h), _stream()) != 0:
+            raise AdamkError(-1, (lib.adamk_prefill_pass_last_error() or b"").decode())
+        self.launches += 1 + 9 * len(self.layers)
         return h
+
+    def _pass_args(self):
+        """The C description of the model and its prepared weights (cached; tensors stay owned by ``self.layers``)."""
+        if self._pass is None:
+            cfg, plug = self.cfg, self.plugin
+            kc, _ = plug.kv_view()
+            model = _PassModel(len(self.layers), cfg.hidden, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, self.layers[0]["i_pad"],
+                               plug.max_ctx, cfg.rms_eps, kc.stride(0) * kc.element_size())
+            arr = (_PassLayer * len(self.layers))()
+            for i, lw in enumerate(self.layers):
+                for name in _PASS_LAYER_FIELDS:
+                    t = lw[name]
+                    setattr(arr[i], name, None if t is None else t.data_ptr())
+            self._pass = (model, arr)
+        return self._pass

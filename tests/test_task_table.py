@@ -256,7 +256,7 @@ def test_cabi_exports_prefill_operators():
 
     build.build()
     header = (Path(__file__).resolve().parents[1] / "include" / "adamk_prefill.h").read_text()
-    declared = set(re.findall(r"\b(adamk_(?:prefill|batch)_[a-z_]+)\s*\(", header))
+    declared = set(re.findall(r"\b(adamk_(?:prefill|batch)(?:_[a-z_]+)?)\s*\(", header))
     assert declared == set(prefill.PREFILL_EXPORTS)
     lib = plugin.load_library()
     for name in declared:
@@ -307,3 +307,32 @@ def test_search_to_schedule_to_task_table():
     # a plan tile taller than eight rows per warp is split into several kernel tiles
     tall = tt.KernelSchedule.from_plan({"tile": [16, 64, 512, 2], "n_stage": 3, "consumer_warps": 4})
     assert (tall.rows_per_tile, tall.ktile_chunks) == (32, 1)
+
+
+def test_prefill_pass_entry_validates_on_the_host():
+    """`adamk_prefill` (the whole Prefill pass behind one C call): workspace sizing and argument checks are host
+    arithmetic and need no GPU."""
+    import ctypes as C
+
+    from paper_2605_11581_b200 import prefill
+
+    lib = prefill._lib()
+    cfg = QWEN25_1P5B
+    i_pad = -(-cfg.intermediate // 128) * 128
+    model = prefill._PassModel(cfg.n_layers, cfg.hidden, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, i_pad, 4096, cfg.rms_eps,
+                               cfg.n_kv_heads * 4096 * cfg.head_dim * 2)
+    T, P = 512, 1
+    need = lib.adamk_prefill_workspace_bytes(C.byref(model), T, 0, P)
+    lower = 2 * T * (cfg.hidden + cfg.q_dim + cfg.q_dim + i_pad) + 4 * T * cfg.qkv_rows + 2 * cfg.kv_dim * 512
+    assert lower <= need <= lower + 6 * 256
+    assert lib.adamk_prefill_workspace_bytes(C.byref(model), T, 0, 2) > need
+    assert lib.adamk_prefill_workspace_bytes(C.byref(model), 0, 0, 1) == 0          # no tokens
+    assert lib.adamk_prefill_workspace_bytes(C.byref(model), T, 0, 3) == 0          # planes must be 1 or 2
+    bad = prefill._PassModel(cfg.n_layers, cfg.hidden, cfg.n_q_heads, cfg.n_kv_heads, 96, i_pad, 4096, cfg.rms_eps, 1)
+    assert lib.adamk_prefill_workspace_bytes(C.byref(bad), T, 0, 1) == 0            # head_dim 64 / 128 only
+    layers = (prefill._PassLayer * cfg.n_layers)()
+    rc = lib.adamk_prefill(C.byref(model), layers, None, None, None, None, T, 0, P, None, None, None, None, None)
+    assert rc != 0 and b"NULL argument" in lib.adamk_prefill_pass_last_error()
+    one = C.c_void_p(256)
+    rc = lib.adamk_prefill(C.byref(model), layers, one, one, one, one, 4096, 1, P, one, one, one, one, None)
+    assert rc != 0 and b"does not fit the KV cache" in lib.adamk_prefill_pass_last_error()
