@@ -26,8 +26,11 @@ NAME = "qwen2.5-1.5b"
 CFG = PRESETS[NAME]
 
 
-def _files():
-    return {k: (SCHEDULE_DIR / f"{NAME}.{k}.json") for k in ("trace", "graph", "hw", "space", "kernel")}
+SHIPPED = ("qwen2.5-1.5b", "qwen2.5-7b", "qwen3-8b")
+
+
+def _files(name=NAME):
+    return {k: (SCHEDULE_DIR / f"{name}.{k}.json") for k in ("trace", "graph", "hw", "space", "kernel")}
 
 
 def test_shipped_trace_is_well_formed_and_hash_checked():
@@ -44,17 +47,19 @@ def test_shipped_trace_is_well_formed_and_hash_checked():
         search.parse_trace(bad)
 
 
-def test_mirror_planner_reproduces_the_shipped_trace_bytes():
-    f = _files()
+@pytest.mark.parametrize("name", SHIPPED)
+def test_mirror_planner_reproduces_the_shipped_trace_bytes(name):
+    f = _files(name)
     trace = search.run_search(f["graph"].read_text(), f["hw"].read_text(), f["space"].read_text(), 10000)
     assert search.serialize_trace(trace) == f["trace"].read_bytes()
 
 
 @pytest.mark.skipif(not REF.exists(), reason="the reference planner is only mounted in the build container")
-def test_reference_planner_reproduces_the_shipped_trace_bytes():
+@pytest.mark.parametrize("name", SHIPPED)
+def test_reference_planner_reproduces_the_shipped_trace_bytes(name):
     import importlib
 
-    f = _files()
+    f = _files(name)
     saved = {k: v for k, v in sys.modules.items() if k == "mkplan" or k.startswith("mkplan.")}
     for k in saved:
         del sys.modules[k]
@@ -136,10 +141,25 @@ def test_program_order_check_rejects_hoists_across_stages():
 
 
 def test_models_without_a_trace_fall_back_to_the_profiled_default():
-    cfg = PRESETS["qwen3-8b"]
-    assert shipped_trace(cfg) is None
-    sched = default_schedule(cfg)
+    from paper_2605_11581_b200.model_config import TINY
+
+    assert shipped_trace(TINY) is None
+    sched = default_schedule(TINY)
     assert sched.consumer_warps == 7 and sched.n_stage >= 3
-    assert "profiled default" in schedule_id(cfg)["source"]
-    # a tensor-parallel rank cannot run the fused down projection
+    assert "profiled default" in schedule_id(TINY)["source"]
+
+
+@pytest.mark.parametrize("name", SHIPPED[1:])
+def test_larger_models_ship_traces_that_lower_to_the_profiled_schedule(name):
+    """Qwen2.5-7B / Qwen3-8B: the searched plan lowers to the schedule profiling chose (42 x 512 tiles on seven warps,
+    unfused down projection, ring depth from Eq.2), and a tensor-parallel rank never gets the fused down projection."""
+    from paper_2605_11581_b200.schedules import PROFILED_DEFAULT, fit_schedule
+
+    cfg = PRESETS[name]
+    trace, knobs, order = shipped_trace(cfg)
+    assert order is not None and order["fills"] > 0 and knobs["fuse_down"] is False
+    sched = default_schedule(cfg)
+    assert sched == fit_schedule(cfg, tt.KernelSchedule(n_stage=2, **PROFILED_DEFAULT))
+    assert sched.inflight == trace.plan["stride_eff"] + 1
+    assert schedule_id(cfg)["content_hash"] == trace.content_hash
     assert not default_schedule(cfg.shard(2), tp_size=2).fuse_down

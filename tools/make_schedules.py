@@ -37,6 +37,8 @@ NARROW = {"block_m": [16], "block_n": [48], "block_k": [512], "k_split": [1], "c
           "n_stage": [2, 3, 4], "prefetch_stride": [1, 2], "swizzles": [31], "flags": {"gap_fill": [False, True]}}
 # run-time knobs the planner does not model
 KERNEL = {"attn_min_chunk": 112, "l2_prefetch_kb": 512, "fuse_down": True}
+# the fused K-slice down projection pays only with one 256-row block per consumer warp (tools/model_sweep.py)
+KERNEL_BY_MODEL = {"qwen2.5-7b": dict(KERNEL, fuse_down=False), "qwen3-8b": dict(KERNEL, fuse_down=False)}
 
 
 def main() -> None:
@@ -68,7 +70,7 @@ def main() -> None:
         (OUT / f"{name}.graph.json").write_text(graph_text)
         (OUT / f"{name}.space.json").write_text(space_text)
         (OUT / f"{name}.hw.json").write_text(HW)
-        (OUT / f"{name}.kernel.json").write_text(json.dumps(KERNEL, indent=1) + "\n")
+        (OUT / f"{name}.kernel.json").write_text(json.dumps(KERNEL_BY_MODEL.get(name, KERNEL), indent=1) + "\n")
         order = check_program_order(search.parse_trace(text), graph_text, HW)
         p = trace.plan
         print(f"{name}: {time.time() - t0:.1f}s  tile {p['tile']} n_stage {p['n_stage']} consumer_warps {p['consumer_warps']} "
