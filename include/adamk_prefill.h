@@ -47,6 +47,11 @@ const char* adamk_prefill_last_error(void);
  * default; the batched decode step (dozens of ~10 us kernels per layer) turns it on. */
 void adamk_prefill_set_pdl(int on);
 
+/* Tile walk order of adamk_prefill_gemm, process-wide: -1 (default) = chosen per call -- tile column fastest when the
+ * activation operand is larger than the weight and the weight fits L2 (the down projection of a long prompt), token
+ * block fastest otherwise; 0 / 1 force one of them (A/B measurements, tools/ncu_prefill.py). */
+void adamk_prefill_set_walk(int mode);
+
 /* One-shot hint for the NEXT adamk_prefill_gemm call on this thread (one-CTA tiles): while that GEMM waits for its own
  * operands, its idle warps pull `bytes` at `ptr` -- the weight the kernel AFTER it will stream -- into L2
  * (cp.async.bulk.prefetch.L2).  The batched decode step chains its GEMMs this way; 16-byte aligned, < L2 size. */

@@ -149,6 +149,11 @@ struct GemmArgs {
   const uint8_t* pf_ptr;       // adamk_prefill_prefetch_next(): bytes the NEXT kernel will stream, pulled into L2 by this
   long long pf_bytes;          // launch's otherwise idle epilogue warps while its own operands are in flight
   unsigned long long* trace;   // debug: %globaltimer stamps of CTA 0 (adamk_prefill_set_trace), or null
+  int col_fast;         // walk order of the tiles: 0 = token block fastest (CTAs of a wave share a weight tile: the weight
+                        // leaves HBM once, right when it is the large operand), 1 = tile column fastest (CTAs of a wave
+                        // share a token block and the whole weight sits in L2: right when the ACTIVATION is the large
+                        // operand, e.g. the down projection of a 4096-token pass: 73 MB of activations against 27 MB)
+  int n_tiles_n;        // tile columns
   int stacked;          // EPI_ATOMIC with parts * T <= 128: the planes are consecutive rows of ONE token tile, K is walked
                         // once (the weight is read once), accumulator row r adds into output row r % T
 };
@@ -185,6 +190,7 @@ __device__ __forceinline__ Item decode_item(int idx_k, const GemmArgs& g, int m_
     sub = t % g.tail_split;
     w = BN / g.tail_split;
   }
+  if (g.col_fast) return Item{(tile / g.n_tiles_n) * BM, tile % g.n_tiles_n, sub, w, kb_lo, kb_len};
   return Item{(tile % m_tiles) * BM, tile / m_tiles, sub, w, kb_lo, kb_len};
 }
 
@@ -587,8 +593,13 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
       sub = t % g.tail_split;
       w = BN / g.tail_split;
     }
-    m0 = (tile % m_tiles) * 2 * BM;
-    n_blk = tile / m_tiles;
+    if (g.col_fast) {
+      m0 = (tile / g.n_tiles_n) * 2 * BM;
+      n_blk = tile % g.n_tiles_n;
+    } else {
+      m0 = (tile % m_tiles) * 2 * BM;
+      n_blk = tile / m_tiles;
+    }
   };
 
   if (warp == 0) {
@@ -687,6 +698,7 @@ static unsigned long long* g_trace = nullptr;   // adamk_prefill_set_trace()
 static const uint8_t* g_pf_ptr = nullptr;        // adamk_prefill_prefetch_next(): consumed by the next GEMM launch
 static long long g_pf_bytes = 0;
 static int g_pdl = 0;   // adamk_prefill_set_pdl(): launch with programmatic stream serialization
+static int g_walk = -1;  // adamk_prefill_set_walk(): -1 = choose per call, 0 = token block fastest, 1 = tile column fastest
 int pdl_enabled() { return g_pdl; }
 
 static EncodeTiledFn encode_fn() {
@@ -886,6 +898,7 @@ extern "C" {
 
 const char* adamk_prefill_last_error(void) { return pf::g_err; }
 
+void adamk_prefill_set_walk(int mode) { pf::g_walk = mode < 0 ? -1 : (mode ? 1 : 0); }
 void adamk_prefill_set_pdl(int on) { pf::g_pdl = on ? 1 : 0; }
 
 void adamk_prefill_prefetch_next(const void* ptr, long long bytes) {
@@ -962,6 +975,13 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
   GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride, 0, 1, 0, 1, 0, g_pf_ptr, g_pf_bytes, g_trace, 0};
   g_pf_ptr = nullptr;
   g_pf_bytes = 0;
+  {
+    // walk order: tile column fastest when the activation is the larger operand and the weight fits L2 with room to spare
+    const long long xb = (long long)parts * T * K * 2, wb = (long long)N * K * 2;
+    const int bn = plan.tile == ADAMK_PF_TILE_PAIR ? 256 : plan.tile;
+    g.n_tiles_n = (N + bn - 1) / bn;
+    g.col_fast = g_walk >= 0 ? g_walk : (epilogue != ADAMK_PF_EPI_ATOMIC && xb > wb && wb <= (48ll << 20));
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (plan.tile == ADAMK_PF_TILE_PAIR) {
     switch (epilogue) {

@@ -52,6 +52,38 @@ def test_gemm_store_bias(T, K, N, parts, tile_n):
         assert (out.double() - exact).abs().max().item() <= 1e-4 * max(1.0, exact.abs().max().item())
 
 
+@pytest.mark.parametrize("T,K,N,tile_n,epi", [(1100, 512, 1536, 0, "store"), (1100, 512, 1536, 128, "store"), (4096, 2048, 1536, 512, "resid"),
+                                              (700, 256, 1024, 256, "swiglu"), (2100, 1024, 768, 0, "resid")])
+def test_gemm_walk_orders_agree_bit_for_bit(T, K, N, tile_n, epi):
+    """`adamk_prefill_set_walk`: token-block-fastest and tile-column-fastest walks assign the same tiles to different
+    CTAs; every output element is computed by the same instructions, so the results are identical (whole tiles and the
+    column slices of the last wave, one-CTA and CTA-pair kernels, every epilogue)."""
+    from paper_2605_11581_b200 import prefill as P
+
+    lib = P._lib()
+    g = torch.Generator(device="cuda").manual_seed(T + N)
+    xp = _planes(torch.randn(T, K, device="cuda", generator=g), 1)
+    w = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    base = torch.randn(T, N, device="cuda", generator=g)
+    outs = []
+    try:
+        for mode in (0, 1, -1):
+            lib.adamk_prefill_set_walk(mode)
+            if epi == "swiglu":
+                out = torch.zeros(1, T, N // 2, dtype=torch.bfloat16, device="cuda")
+                P.gemm(xp, w, out, epilogue=P.EPI_SWIGLU, tile_n=tile_n)
+            else:
+                out = base.clone()
+                P.gemm(xp, w, out, epilogue=P.EPI_RESID if epi == "resid" else P.EPI_STORE, tile_n=tile_n)
+            outs.append(out)
+    finally:
+        lib.adamk_prefill_set_walk(-1)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    if epi != "swiglu":
+        want = xp[0].double() @ w.double().T + (base.double() if epi == "resid" else 0)
+        assert (outs[1].double() - want).abs().max().item() <= 4e-5 * max(1.0, want.abs().max().item())
+
+
 @pytest.mark.parametrize("T,K,N,parts,tile_n", [(1000, 8960, 1536, 2, 0), (77, 192, 328, 1, 128), (640, 1536, 1536, 1, 256),
                                                  (640, 1536, 1536, 1, 512), (4096, 3584, 3584, 1, 512), (4096, 3584, 3584, 2, 256)])
 def test_gemm_residual(T, K, N, parts, tile_n):
