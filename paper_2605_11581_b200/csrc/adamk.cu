@@ -61,7 +61,7 @@ constexpr int kGMax = 8;             // max q heads per kv head
 constexpr int kRW = 8;               // max rows per warp per tile
 constexpr int kGatherBatch = 4;      // 16-byte tagged-word loads a thread keeps in flight while gathering a vector
 constexpr int kMaxTP = 8;
-constexpr int kRep = 4;              // copies of the vectors every SM gathers whole (single-GPU kernel)
+constexpr int kRep = 2;              // copies of the vectors every SM gathers whole (single-GPU kernel; measured 1 / 2 / 4 / 8 copies: 804 / 796 / 800 / 805 us per token)
 constexpr int kTagStride = 256;      // tag = epoch * kTagStride + layer + 1
 
 enum TaskType { T_END = 0, T_QKV = 1, T_ATTN = 2, T_OPROJ = 3, T_GATEUP = 4, T_DOWN = 5, T_LMHEAD = 6, T_MERGE = 7, T_DOWNK = 8, T_HRED = 9 };
