@@ -2053,7 +2053,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
           if (pf < wcur) pf = wcur;
           while (pf < wend && pf < wcur + p.pf_window_bytes) {
             if (mbar_test_wait(bar, parity)) return;
-            if (p.poll_inflight && *polling) {
+            if (p.poll_inflight && p.poll_inflight != 9 && *polling) {
               if (clock64() - t0 > kWatchdogCycles) dev_fail(p, code, ti, (int)bar, (int)parity, 0);
               continue;   // the consumers are polling: no new HBM requests from this SM
             }
@@ -2076,7 +2076,22 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       };
       auto issue = [&](const void* src, uint32_t bytes, bool hint, int ti) {
         // at most `cap` stages in flight (`poll_inflight` while the consumers poll): wait for the oldest one to land
-        while (issued - retired >= ((p.poll_inflight && *polling) ? p.poll_inflight : cap)) {
+        if (p.poll_inflight == 9 && !p.probe) {   // ring fills return data to THIS SM ahead of its poll replies: hold them, keep the L2 prefetch going
+          const long long t0 = clock64();
+          while (*polling) {
+            if (p.pf_window_bytes > 0) {
+              if (pf < wcur) pf = wcur;
+              if (pf < wend && pf < wcur + p.pf_window_bytes) {
+                const uint32_t nb = (uint32_t)min((size_t)kPfGranule, (size_t)(wend - pf));
+                l2_prefetch_bulk(pf, nb, pol);
+                pf += nb;
+                ++n_pf;
+              }
+            }
+            if (clock64() - t0 > kWatchdogCycles) dev_fail(p, DE_WATCHDOG_INFLIGHT, ti, 9, 0, 0);
+          }
+        }
+        while (issued - retired >= ((p.poll_inflight && p.poll_inflight != 9 && *polling) ? p.poll_inflight : cap)) {
           blocked_wait(smem_u32(&hdr->full[wslot]), wph, DE_WATCHDOG_INFLIGHT, ti);
           if (++wslot == n_stage) { wslot = 0; wph ^= 1u; }
           ++retired;
@@ -2176,7 +2191,11 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       WarpArgs w;
       w.cw = c.cw; w.lane = c.lane; w.ctid = c.ctid; w.nct = c.nct; w.epoch = c.epoch; w.slot = c.slot; w.ph = c.ph;
       w.layer = t.layer; w.a = t.a; w.b = t.b; w.aux = t.aux; w.task_idx = ti; w.pos = pos;
-      if (t.type == T_HRED) run_hred_nl(kp, w, t.a, t.b, scratch);
+      if (t.type == T_HRED) {
+        set_polling(hdr, c.ctid, 1);
+        run_hred_nl(kp, w, t.a, t.b, scratch);
+        set_polling(hdr, c.ctid, 0);
+      }
       else {
         const uint32_t sp = (t.aux & 2) ? run_downk_nl<true>(kp, w, t.b, t.kchunks, t.n_ktiles, scratch, hdr, ring)
                                         : run_downk_nl<false>(kp, w, t.b, t.kchunks, t.n_ktiles, scratch, hdr, ring);

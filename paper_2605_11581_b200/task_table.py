@@ -80,7 +80,9 @@ class KernelSchedule:
     inflight: int = 0         # ring stages the Loader keeps in flight at most (0 = all free slots)
     poll_sleep_ns: int = 0    # back-off between polls of an incomplete activation vector
     l2_prefetch_kb: int = 0   # per-SM window past the ring the Loader prefetches into L2 while it is blocked
-    poll_inflight: int = 0    # ring stages in flight (and no L2 prefetch) while this SM's consumers poll for inputs (0 = unchanged)
+    poll_inflight: int = 0    # while this SM's consumers poll for inputs: 1-8 = ring stages in flight and no L2 prefetch;
+                              # 9 = no new ring fills (their data would return to this SM ahead of the poll replies), L2
+                              # prefetch continues; 0 = the Loader ignores the consumers' state
     pace_clk_per_64k: int = 0  # Loader pacing: SM clocks per 64 KB of new HBM requests per SM (0 = unpaced); see pace_for()
     w4a16: bool = False       # the layer projections stream GPTQ-format int4 codes + fp16 group scales (W[n][k] = (q - 8) * s[n][k / 128],
                               # reference byte model graph_ir.py:296-318); needs fuse_down; embedding / LM head stay bf16

@@ -50,6 +50,7 @@ __device__ __forceinline__ void tma_g2s(uint32_t dst, const void* src, uint32_t 
 struct Params {
   u64* vec;          // [rep][2][n]
   int n, rep, iters, variant, late_ns, bg, depth, stage_bytes;
+  int qs;            // words between consecutive quads of the vector (4 = dense; 32 = one 32-byte sector per 256-byte L2 granule)
   const uint8_t* stream;   // background stream source
   size_t stream_bytes_per_sm;
   u64* t_pub;        // [iters][grid]
@@ -113,15 +114,17 @@ __global__ void __launch_bounds__(256, 1) hop_kernel(const Params p) {
   long long spins = 0;
   for (int it = 0; it < p.iters; ++it) {
     const unsigned tag = (unsigned)it + 1u;
-    u64* dst = p.vec + (size_t)(it & 1) * p.n;
-    const size_t cstride = (size_t)2 * p.n;
+    const size_t vlen = (size_t)(p.n >> 2) * p.qs;   // words one copy of the vector spans
+    u64* dst = p.vec + (size_t)(it & 1) * vlen;
+    const size_t cstride = (size_t)2 * vlen;
     // ---- publish ----
     const bool late = (it % grid) == b;
     if (late && p.late_ns > 0) { const u64 t0 = gtime(); while (gtime() - t0 < (u64)p.late_ns) {} }
     asm volatile("bar.sync 1, 224;" ::: "memory");
     if (ctid == 0) p.t_pub[(size_t)it * grid + b] = gtime();
     if (w0 + ctid < w1) {
-      for (int r = 0; r < p.rep; ++r) ll_store(dst + r * cstride + w0 + ctid, (float)(it + ctid), tag);
+      const int wi = w0 + ctid;
+      for (int r = 0; r < p.rep; ++r) ll_store(dst + r * cstride + (size_t)(wi >> 2) * p.qs + (wi & 3), (float)(it + ctid), tag);
     }
     if (p.variant >= 3) {
       asm volatile("bar.sync 1, 224;" ::: "memory");
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(256, 1) hop_kernel(const Params p) {
         for (;;) {
           bool ok = true;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) { const int i = i0 + u * nct; if (i < n4) ll_load4(src + 4 * i, w[u]); }
+          for (int u = 0; u < 4; ++u) { const int i = i0 + u * nct; if (i < n4) ll_load4(src + (size_t)p.qs * i, w[u]); }
 #pragma unroll
           for (int u = 0; u < 4; ++u) { const int i = i0 + u * nct; if (i < n4) ok = ok && tagof(w[u][0]) == tag && tagof(w[u][1]) == tag && tagof(w[u][2]) == tag && tagof(w[u][3]) == tag; }
           if (ok) break;
@@ -202,7 +205,8 @@ int main(int argc, char** argv) {
   const int grid = sms;
   const size_t stream_per_sm = (size_t)20 << 20;
   uint8_t* stream; CK(cudaMalloc(&stream, stream_per_sm * grid)); CK(cudaMemset(stream, 1, stream_per_sm * grid));
-  u64* vec; CK(cudaMalloc(&vec, (size_t)16 * 2 * n * 8));
+  const size_t vec_bytes = (size_t)16 * 2 * n * 8 * 16;
+  u64* vec; CK(cudaMalloc(&vec, vec_bytes));
   u64 *t_pub, *t_done; CK(cudaMalloc(&t_pub, (size_t)iters * grid * 8)); CK(cudaMalloc(&t_done, (size_t)iters * grid * 8));
   unsigned* counter; CK(cudaMalloc(&counter, (size_t)(iters + 2) * 4));
   float* sink; CK(cudaMalloc(&sink, grid * 4));
@@ -211,20 +215,26 @@ int main(int argc, char** argv) {
   std::vector<u64> hp((size_t)iters * grid), hd((size_t)iters * grid);
   setvbuf(stdout, nullptr, _IONBF, 0);
   printf("n=%d words, grid=%d, 224 consumer threads; us from the late CTA's publish: first / median / p90 / last CTA done (mean over iterations)\n", n, grid);
-  struct Cfg { int variant, rep, bg, depth; };
+  struct Cfg { int variant, rep, bg, depth, qs; };
   std::vector<Cfg> cfgs;
-  for (int bg : {0, 1, 2})
-    for (int depth : {3})
-      for (int variant : {0, 1, 2, 3, 4})
-        for (int rep : {1, 4}) cfgs.push_back({variant, rep, bg, depth});
-  cfgs.push_back({0, 1, 1, 1}); cfgs.push_back({0, 1, 1, 2}); cfgs.push_back({0, 1, 1, 4});
-  cfgs.push_back({1, 4, 1, 1}); cfgs.push_back({1, 4, 1, 2}); cfgs.push_back({1, 4, 1, 4});
+  if (argc > 2) {   // quad-stride sweep (32-byte loads): does spreading the vector over more L2 slices shorten the hop?
+    for (int bg : {0, 1})
+      for (int rep : {1, 2})
+        for (int qs : {4, 8, 16, 32, 64}) cfgs.push_back({1, rep, bg, 3, qs});
+  } else {
+    for (int bg : {0, 1, 2})
+      for (int depth : {3})
+        for (int variant : {0, 1, 2, 3, 4})
+          for (int rep : {1, 4}) cfgs.push_back({variant, rep, bg, depth, 4});
+    cfgs.push_back({0, 1, 1, 1, 4}); cfgs.push_back({0, 1, 1, 2, 4}); cfgs.push_back({0, 1, 1, 4, 4});
+    cfgs.push_back({1, 4, 1, 1, 4}); cfgs.push_back({1, 4, 1, 2, 4}); cfgs.push_back({1, 4, 1, 4, 4});
+  }
   for (const Cfg& c : cfgs) {
     Params p{};
-    p.vec = vec; p.n = n; p.rep = c.rep; p.iters = iters; p.variant = c.variant; p.late_ns = 3000; p.bg = c.bg; p.depth = c.depth;
+    p.vec = vec; p.n = n; p.rep = c.rep; p.iters = iters; p.variant = c.variant; p.late_ns = 3000; p.bg = c.bg; p.depth = c.depth; p.qs = c.qs;
     p.stage_bytes = 43008; p.stream = stream; p.stream_bytes_per_sm = stream_per_sm; p.t_pub = t_pub; p.t_done = t_done;
     p.counter = counter; p.sink = sink;
-    CK(cudaMemset(vec, 0, (size_t)16 * 2 * n * 8));
+    CK(cudaMemset(vec, 0, vec_bytes));
     CK(cudaMemset(counter, 0, (size_t)(iters + 2) * 4));
     void* args[] = {&p};
     cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
@@ -246,8 +256,8 @@ int main(int argc, char** argv) {
       s_first += d[0]; s_med += d[grid / 2]; s_p90 += d[grid * 9 / 10]; s_last += d[grid - 1];
       ++cnt;
     }
-    printf("bg %d depth %d variant %d rep %d: first %.2f  median %.2f  p90 %.2f  last %.2f   (%.2f us per iteration)\n", c.bg, c.depth,
-           c.variant, c.rep, s_first / cnt, s_med / cnt, s_p90 / cnt, s_last / cnt, ms * 1e3 / iters);
+    printf("bg %d depth %d variant %d rep %d qs %d: first %.2f  median %.2f  p90 %.2f  last %.2f   (%.2f us per iteration)\n", c.bg, c.depth,
+           c.variant, c.rep, c.qs, s_first / cnt, s_med / cnt, s_p90 / cnt, s_last / cnt, ms * 1e3 / iters);
     fflush(stdout);
   }
   return 0;

@@ -36,9 +36,11 @@ WIDE = {"block_m": [16], "block_n": [32, 48, 56, 64], "block_k": [256, 512], "k_
 NARROW = {"block_m": [16], "block_n": [48], "block_k": [512], "k_split": [1], "consumer_warps": [7],
           "n_stage": [2, 3, 4], "prefetch_stride": [1, 2], "swizzles": [31], "flags": {"gap_fill": [False, True]}}
 # run-time knobs the planner does not model
-KERNEL = {"attn_min_chunk": 112, "l2_prefetch_kb": 512, "fuse_down": True}
+KERNEL = {"attn_min_chunk": 112, "l2_prefetch_kb": 512, "fuse_down": True, "poll_inflight": 9}
 # the fused K-slice down projection pays only with one 256-row block per consumer warp (tools/model_sweep.py)
-KERNEL_BY_MODEL = {"qwen2.5-7b": dict(KERNEL, fuse_down=False), "qwen3-8b": dict(KERNEL, fuse_down=False)}
+# (and holding ring fills while the consumers poll measures 0.6 % slower on them, 1.2 % faster on the 1.5B)
+BIG = {"attn_min_chunk": 112, "l2_prefetch_kb": 512, "fuse_down": False}
+KERNEL_BY_MODEL = {"qwen2.5-7b": BIG, "qwen3-8b": BIG}
 
 
 def main() -> None:
