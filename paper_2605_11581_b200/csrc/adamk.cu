@@ -2894,7 +2894,11 @@ int adamk_decode_step_host(adamk_handle h, const int32_t* token_ids_host, const 
   const int rc = adamk_decode_step(h, token_ids, positions, batch, k_cache, v_cache, workspace, logits_out, next_token_out, 0, stream);
   if (rc != ADAMK_OK) return rc;
   CUDA_TRY(cudaMemcpyAsync(next_token_host, next_token_out, nb, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  // the caller needs the token to form the next step's input: spin on the stream rather than block (a blocking wait
+  // adds the scheduler's wake-up latency to every token)
+  cudaError_t q;
+  while ((q = cudaStreamQuery(st)) == cudaErrorNotReady) {}
+  if (q != cudaSuccess) return fail(ADAMK_E_CUDA, cudaGetErrorString(q));
   if (h->status_host[0] != 0) return fail(ADAMK_E_DEVICE, "the step reported a device error; see adamk_device_status");
   return ADAMK_OK;
 }
