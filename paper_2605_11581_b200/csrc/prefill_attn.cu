@@ -8,7 +8,8 @@
 //              (cp.async.bulk.tensor.2d, 128-byte swizzle, K-major boxes of 64 elements)
 //   warp 1     one lane issues tcgen05.mma: S_j = Q K_j^T into one of two S accumulators in tensor memory,
 //              O_j = P_j V_j into a third; tcgen05.commit publishes them and frees the ring stage
-//   warps 2-5  softmax: thread r owns q row r (= TMEM lane r): tcgen05.ld of its S row, causal mask, running
+//   warps 2-9  two softmax warpgroups: threads r of both own q row r (= TMEM lane r), one half of its columns each:
+//              tcgen05.ld of its half of the S row, causal mask, running
 //              maximum / sum (exp2 with the scale folded in), P_j written as bf16 into shared memory in the swizzled
 //              K-major layout the PV MMA reads, the O row (fp32, registers) rescaled and accumulated from tensor memory
 //
@@ -36,7 +37,7 @@ namespace fa {
 constexpr int BQ = 128;    // q rows per tile = TMEM lanes
 constexpr int BKV = 128;   // positions per K / V block
 constexpr int KB = 64;     // bf16 elements per 128-byte swizzle row
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;   // TMA warp, MMA warp, two softmax warpgroups
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -86,6 +87,15 @@ __device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a_desc, uint64_t 
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// the same with the A operand in tensor memory (K-major: lane = row, two bf16 per 32-bit column along K)
+__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -103,6 +113,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr)
       : "memory");
 }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]),
+      "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]),
+      "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]),
+      "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -117,16 +139,15 @@ struct Args {
   long long plane_stride;
 };
 
-// shared memory: Q | 2 x (K | V^T) | P | barriers
+// shared memory: Q | 2 x (K | V^T) | barriers, exchange buffers   (P lives in tensor memory)
 template <int D>
 struct Smem {
   static constexpr int kQ = BQ * D * 2;
   static constexpr int kK = BKV * D * 2;
   static constexpr int kV = D * BKV * 2;
   static constexpr int kStage = kK + kV;
-  static constexpr int kP = BQ * BKV * 2;
-  static constexpr int kBars = 256;
-  static constexpr int kTotal = kQ + 2 * kStage + kP + kBars + 1024;
+  static constexpr int kBars = 256 + 3 * 1024;   // mbarriers + tensor-memory slot | row-maximum exchange [2][2][128] | row-sum exchange [2][128]
+  static constexpr int kTotal = kQ + 2 * kStage + kBars + 1024;
 };
 
 template <int D>
@@ -138,15 +159,18 @@ flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* q_s = smem;
   uint8_t* kv_s = smem + S::kQ;
-  uint8_t* p_s = kv_s + 2 * S::kStage;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(p_s + S::kP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(kv_s + 2 * S::kStage);
   uint64_t* q_full = bars;            // 1
-  uint64_t* kv_full = bars + 1;       // 2
-  uint64_t* kv_empty = bars + 3;      // 2
+  uint64_t* k_full = bars + 1;        // 2   K and V^T blocks travel in separate two-stage rings: a K stage is free as soon
+  uint64_t* k_empty = bars + 3;       // 2   as its QK^T product is done, long before the PV product of the same block
   uint64_t* s_full = bars + 5;        // 2
-  uint64_t* p_full = bars + 7;        // 1 (128 arrivals)
+  uint64_t* p_full = bars + 7;        // 1 (256 arrivals)
   uint64_t* o_full = bars + 8;        // 1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  uint64_t* v_full = bars + 9;        // 2
+  uint64_t* v_empty = bars + 11;      // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  float* mx = reinterpret_cast<float*>(bars) + 64;     // [block parity][warpgroup][row]
+  float* lx = mx + 512;                                // [warpgroup][row]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.y, kvh = h / (a.n_q / a.n_kv);
@@ -162,11 +186,13 @@ flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ 
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_vt)) : "memory");
     mbar_init(q_full, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
     }
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 256);
     mbar_init(o_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -186,12 +212,14 @@ flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ 
       for (int kb = 0; kb < D / KB; ++kb) tma_load_2d(&map_q, q_full, q_s + kb * (BQ * 128), kb * KB, h * a.T + q0);
       for (int j = 0; j < n_blk; ++j) {
         const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
         uint8_t* ks = kv_s + st * S::kStage;
         uint8_t* vs = ks + S::kK;
-        mbar_expect_tx(&kv_full[st], S::kStage);
-        for (int kb = 0; kb < D / KB; ++kb) tma_load_2d(&map_k, &kv_full[st], ks + kb * (BKV * 128), kb * KB, kvh * a.max_ctx + j * BKV);
-        for (int kb = 0; kb < BKV / KB; ++kb) tma_load_2d(&map_vt, &kv_full[st], vs + kb * (D * 128), j * BKV + kb * KB, kvh * D);
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], S::kK);
+        for (int kb = 0; kb < D / KB; ++kb) tma_load_2d(&map_k, &k_full[st], ks + kb * (BKV * 128), kb * KB, kvh * a.max_ctx + j * BKV);
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], S::kV);
+        for (int kb = 0; kb < BKV / KB; ++kb) tma_load_2d(&map_vt, &v_full[st], vs + kb * (D * 128), j * BKV + kb * KB, kvh * D);
       }
     }
   } else if (warp == 1) {
@@ -199,7 +227,7 @@ flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ 
       constexpr uint32_t idesc_s = instr_desc(BQ, BKV), idesc_o = instr_desc(BQ, D);
       auto issue_s = [&](int j) {   // S_j = Q K_j^T into S buffer j & 1
         const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        mbar_wait(&k_full[st], (j >> 1) & 1);
         tc_fence_after();
         const uint32_t qa = smem_u32(q_s), ka = smem_u32(kv_s + st * S::kStage);
 #pragma unroll
@@ -208,123 +236,145 @@ flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ 
           umma(tm_s0 + st * BKV, smem_desc_sw128(qa + off_q), smem_desc_sw128(ka + off_k), idesc_s, k != 0);
         }
         umma_commit(&s_full[st]);
+        umma_commit(&k_empty[st]);              // K_j may be overwritten
       };
       mbar_wait(q_full, 0);
       issue_s(0);
       for (int j = 0; j < n_blk; ++j) {
         const int st = j & 1;
         if (j + 1 < n_blk) issue_s(j + 1);      // the next block's scores while this block's softmax runs
-        mbar_wait(p_full, j & 1);               // P_j is in shared memory; S_j and O_{j-1} have been read
+        mbar_wait(p_full, j & 1);               // P_j is in tensor memory (over the first half of S_j), O is rescaled if it had to be
+        mbar_wait(&v_full[st], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t pa = smem_u32(p_s), va = smem_u32(kv_s + st * S::kStage + S::kK);
+        const uint32_t va = smem_u32(kv_s + st * S::kStage + S::kK);
 #pragma unroll
-        for (int k = 0; k < BKV / 16; ++k) {
-          const uint32_t off_p = (k / 4) * (BQ * 128) + (k % 4) * 32, off_v = (k / 4) * (D * 128) + (k % 4) * 32;
-          umma(tm_o, smem_desc_sw128(pa + off_p), smem_desc_sw128(va + off_v), idesc_o, k != 0);
+        for (int k = 0; k < BKV / 16; ++k) {    // O += P_j V_j: A from tensor memory (8 columns per 16 positions), accumulating across blocks
+          const uint32_t off_v = (k / 4) * (D * 128) + (k % 4) * 32;
+          umma_ts(tm_o, tm_s0 + st * BKV + k * 8, smem_desc_sw128(va + off_v), idesc_o, (j | k) != 0);
         }
-        umma_commit(&kv_empty[st]);             // K_j / V^T_j may be overwritten
+        umma_commit(&v_empty[st]);              // V^T_j may be overwritten
         umma_commit(o_full);
       }
     }
   } else {
-    const int quarter = warp & 3;               // the TMEM lanes this warp may read
+    // Two softmax warpgroups share every q row: warpgroup g owns columns 64 g .. 64 g + 63 of each S block (its half of
+    // the maximum, of the exponentials and of P) and columns g D/2 .. of the output row.  The two threads of a row
+    // exchange their half maxima through shared memory once per block and their half sums once at the end; everything
+    // else (reference maximum, rescale decisions) they compute identically.
+    //
+    // O accumulates in tensor memory across blocks (the PV MMAs add into it), so the softmax of block j + 1 does not wait
+    // for the PV product of block j.  The exponentials are taken against a REFERENCE maximum that is only raised -- and O
+    // and the running sum rescaled, in tensor memory -- when the row maximum has grown by more than 2^8 since (P stays
+    // below 256, far inside bf16 / fp32 range; the final division by the sum taken against the same reference makes the
+    // result independent of it).  P_j goes to tensor memory as well, over the first 64 columns of the S_j it was
+    // computed from: it is the A operand of the PV MMA, and no shared-memory round trip is left in the loop.
+    const int wg = (warp - 2) >> 2;
+    const int quarter = warp & 3;               // the TMEM lanes this warp may access
     const int row = quarter * 32 + lane;        // q row of the tile = TMEM lane
     const int q_pos = a.pos0 + q0 + row;
     const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
-    float o[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) o[i] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;
-    const uint32_t p_row = smem_u32(p_s) + row * 128;
-    const int sw = row & 7;
+    constexpr int DH = D / 2;
+    constexpr int NC = BKV / 64;                // 32-column groups of S per thread
+    constexpr float kRaise = 8.f;               // log2 of the largest P tolerated before the reference is raised
+    float m_ref = -INFINITY, l_run = 0.f;       // reference maximum (raw score units), this thread's half of the sum
+    const int c0 = wg * NC;
+    const uint32_t to = tm_o + lane_addr + wg * DH;
     for (int j = 0; j < n_blk; ++j) {
       const int st = j & 1, kv0 = j * BKV;
       const bool diag = kv0 + BKV - 1 > a.pos0 + q0;   // some row of the tile masks part of this block
       mbar_wait(&s_full[st], (j >> 1) & 1);
       tc_fence_after();
       const uint32_t ts = tm_s0 + st * BKV + lane_addr;
-      // pass 1: the row maximum
+      // this thread's half of the S row: one trip to tensor memory, kept in registers for the maximum and the exponentials
+      uint32_t sr[NC][32];
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) tmem_ld32(ts + (c0 + cc) * 32, sr[cc]);
+      tmem_ld_wait();
       float m_blk = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < BKV / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(ts + c * 32, r);
-        tmem_ld_wait();
+      if (!diag) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float s = __uint_as_float(r[i]);
-          m_blk = fmaxf(m_blk, (!diag || kv0 + c * 32 + i <= q_pos) ? s : -INFINITY);
+        for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) m_blk = fmaxf(m_blk, __uint_as_float(sr[cc][i]));
+      } else {
+        const int lim = q_pos - kv0 - c0 * 32;            // columns 0 .. lim of this half are visible to the row
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (cc * 32 + i > lim) sr[cc][i] = 0xff800000u;   // -inf: exp2 gives exactly 0 below
+            m_blk = fmaxf(m_blk, __uint_as_float(sr[cc][i]));
+          }
+      }
+      mx[(st * 2 + wg) * BQ + row] = m_blk;
+      tc_fence_before();                                  // the S loads of this thread are done before its partner may write P over them
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      tc_fence_after();
+      m_blk = fmaxf(m_blk, mx[(st * 2 + (wg ^ 1)) * BQ + row]);
+      if (j == 0) {
+        m_ref = m_blk;                                    // column 0 of block 0 is visible to every row: finite
+      } else {
+        const bool raise = (m_blk - m_ref) * a.sl2e > kRaise;
+        if (__any_sync(0xffffffffu, raise)) {             // rare: rescale this warp's rows of O in tensor memory
+          mbar_wait(o_full, (j - 1) & 1);                 // every PV product issued so far has been added
+          tc_fence_after();
+          const float alpha = raise ? ex2((m_ref - m_blk) * a.sl2e) : 1.f;
+#pragma unroll
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(to + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            tmem_st32(to + c * 32, r);
+          }
+          tmem_st_wait();
+          if (raise) { l_run *= alpha; m_ref = m_blk; }
         }
       }
-      const float m_new = fmaxf(m_run, m_blk);
-      const float mb = m_new * a.sl2e;
-      const float alpha = ex2(m_run * a.sl2e - mb);       // 0 on the first block (m_run = -inf)
-      // O_{j-1} out of tensor memory (which also means the PV product of block j-1 is done reading P), rescaled
-      if (j > 0) {
-        mbar_wait(o_full, (j - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tm_o + lane_addr + c * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[c * 32 + i] = (o[c * 32 + i] + __uint_as_float(r[i])) * alpha;
-        }
-      }
-      // pass 2: P = exp2(s * scale * log2e - m), written as bf16 in the swizzled K-major layout of the PV operand
+      // P = exp2((s - m_ref) * scale * log2e) as bf16 pairs, straight into tensor memory: the K-major A operand of the PV MMA
+      const float mb = m_ref * a.sl2e;
       float l_blk = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < BKV / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(ts + c * 32, r);
-        tmem_ld_wait();
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
         uint32_t packed[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          float p0 = ex2(fmaf(__uint_as_float(r[i]), a.sl2e, -mb)), p1 = ex2(fmaf(__uint_as_float(r[i + 1]), a.sl2e, -mb));
-          if (diag) {
-            if (kv0 + c * 32 + i > q_pos) p0 = 0.f;
-            if (kv0 + c * 32 + i + 1 > q_pos) p1 = 0.f;
-          }
+          const float p0 = ex2(fmaf(__uint_as_float(sr[cc][i]), a.sl2e, -mb)), p1 = ex2(fmaf(__uint_as_float(sr[cc][i + 1]), a.sl2e, -mb));
           const __nv_bfloat162 b = __floats2bfloat162_rn(p0, p1);
           l_blk += __low2float(b) + __high2float(b);      // the sum of what the tensor cores will multiply
           packed[i >> 1] = *reinterpret_cast<const uint32_t*>(&b);
         }
-        // 32 columns = four 16-byte chunks of k block c / 2: chunk index (c % 2) * 4 + q, swizzled by the row
-        const uint32_t base = p_row + (c >> 1) * (BQ * 128);
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const uint32_t chunk = uint32_t(((c & 1) * 4 + q4) ^ sw);
-          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(base + chunk * 16), "r"(packed[4 * q4]), "r"(packed[4 * q4 + 1]),
-                       "r"(packed[4 * q4 + 2]), "r"(packed[4 * q4 + 3])
-                       : "memory");
-        }
+        for (int i = 0; i < 16; ++i) sr[cc >> 1][(cc & 1) * 16 + i] = packed[i];   // gather the pairs of both groups into one 32-column store
       }
-      l_run = l_run * alpha + l_blk;
-      m_run = m_new;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P: generic-proxy stores -> tensor-core reads
+      l_run += l_blk;
+      static_assert(NC == 2, "one 32-column tcgen05.st per thread carries its 64 probabilities");
+      tmem_st32(tm_s0 + st * BKV + lane_addr + wg * 32, sr[0]);
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(p_full);
     }
     mbar_wait(o_full, (n_blk - 1) & 1);
     tc_fence_after();
-    const float inv = 1.f / l_run;
+    lx[wg * BQ + row] = l_run;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const float inv = 1.f / (l_run + lx[(wg ^ 1) * BQ + row]);
     const int t = q0 + row;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < DH / 32; ++c) {
       uint32_t r[32];
-      tmem_ld32(tm_o + lane_addr + c * 32, r);
+      tmem_ld32(to + c * 32, r);
       tmem_ld_wait();
       if (t < a.T) {
-        __nv_bfloat16* dst = a.out + (long long)t * a.n_q * D + h * D + c * 32;
+        __nv_bfloat16* dst = a.out + (long long)t * a.n_q * D + h * D + wg * DH + c * 32;
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
           uint32_t hi[4], lo[4];
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {
-            const float v0 = (o[c * 32 + i + e] + __uint_as_float(r[i + e])) * inv;
-            const float v1 = (o[c * 32 + i + e + 1] + __uint_as_float(r[i + e + 1])) * inv;
+            const float v0 = __uint_as_float(r[i + e]) * inv;
+            const float v1 = __uint_as_float(r[i + e + 1]) * inv;
             const __nv_bfloat162 b = __floats2bfloat162_rn(v0, v1);
             hi[e >> 1] = *reinterpret_cast<const uint32_t*>(&b);
             const __nv_bfloat162 b2 = __floats2bfloat162_rn(v0 - __low2float(b), v1 - __high2float(b));

@@ -230,19 +230,23 @@ def test_hybrid_engine_tensor_prefill_matches_oracle(cfg):
     eng.close()
 
 
-@pytest.mark.parametrize("D,nq,nkv,T,pos0", [(128, 4, 2, 300, 0), (128, 12, 2, 1000, 0), (64, 4, 2, 130, 0), (64, 2, 1, 1, 0), (128, 8, 8, 128, 0),
-                                               (128, 6, 1, 200, 96), (64, 4, 4, 257, 300), (128, 28, 4, 4096, 0)])
-def test_flash_attention_matches_fp32_reference(D, nq, nkv, T, pos0):
+@pytest.mark.parametrize("D,nq,nkv,T,pos0,qscale", [(128, 4, 2, 300, 0, 1), (128, 12, 2, 1000, 0, 1), (64, 4, 2, 130, 0, 1), (64, 2, 1, 1, 0, 1),
+                                                      (128, 8, 8, 128, 0, 1), (128, 6, 1, 200, 96, 1), (64, 4, 4, 257, 300, 1),
+                                                      (128, 28, 4, 4096, 0, 1), (128, 4, 2, 1500, 0, 12), (64, 4, 2, 900, 70, 12),
+                                                      (128, 2, 1, 2048, 0, 40)])
+def test_flash_attention_matches_fp32_reference(D, nq, nkv, T, pos0, qscale):
     """csrc/prefill_attn.cu (tcgen05 QK^T and PV, softmax out of tensor memory) against a plain fp32 causal attention on
     the same bf16 q / k / v: GQA group sizes 1-7, ragged last tiles, a single row, chunked prefill (pos0 > 0), the
-    Qwen2.5-7B shape at 4096 tokens.  Tolerance: P and the output planes are bf16 (2^-9 relative)."""
+    Qwen2.5-7B shape at 4096 tokens.  ``qscale`` > 1 sharpens the scores (maxima that keep growing by many powers of two
+    from block to block), which is what drives the kernel's lazy rescale of the output in tensor memory.  Tolerance: P
+    and the output planes are bf16 (2^-9 relative)."""
     from paper_2605_11581_b200.prefill import _attn_ok, _lib, _ptr, _stream
 
     lib = _lib()
     g = torch.Generator(device="cuda").manual_seed(D + T + pos0)
     ctx, max_ctx = pos0 + T, pos0 + T + 37
     ctx_pad = -(-ctx // 64) * 64
-    q = torch.randn(nq, T, D, device="cuda", generator=g).to(torch.bfloat16)
+    q = (qscale * torch.randn(nq, T, D, device="cuda", generator=g)).to(torch.bfloat16)
     k = torch.randn(nkv, max_ctx, D, device="cuda", generator=g).to(torch.bfloat16)
     v = torch.randn(nkv, max_ctx, D, device="cuda", generator=g).to(torch.bfloat16)
     k[:, ctx:] = float("nan")                       # rows past the context must never reach the output
