@@ -91,6 +91,11 @@ int adamk_prefill_vt(const void* v_cache, int n_kv, int D, int max_ctx, int ctx,
 
 const char* adamk_prefill_attention_last_error(void);
 
+/* Which flash kernel adamk_prefill_attention launches, process-wide: 0 (default) = a pair of 128-row q tiles per CTA
+ * (one tile when the pass has at most 128 rows), 1 = always one tile per CTA with its rows split between two softmax
+ * warpgroups.  Same results up to summation order; for A/B measurements and tests. */
+void adamk_prefill_attention_set_kernel(int one_tile);
+
 /* h fp32 [T, H] = embed[tokens[t]] (bf16 table). */
 int adamk_prefill_embed(const int32_t* tokens, int T, const void* embed, int H, float* h, adamk_pf_stream stream);
 

@@ -290,22 +290,20 @@ flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ 
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) tmem_ld32(ts + (c0 + cc) * 32, sr[cc]);
       tmem_ld_wait();
-      float m_blk = -INFINITY;
-      if (!diag) {
-#pragma unroll
-        for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) m_blk = fmaxf(m_blk, __uint_as_float(sr[cc][i]));
-      } else {
+      if (diag) {
         const int lim = q_pos - kv0 - c0 * 32;            // columns 0 .. lim of this half are visible to the row
 #pragma unroll
         for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < 32; ++i)
             if (cc * 32 + i > lim) sr[cc][i] = 0xff800000u;   // -inf: exp2 gives exactly 0 below
-            m_blk = fmaxf(m_blk, __uint_as_float(sr[cc][i]));
-          }
       }
+      float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // four independent chains: a single one is 64 dependent FMNMX
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sr[cc][i]));
+      float m_blk = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
       mx[(st * 2 + wg) * BQ + row] = m_blk;
       tc_fence_before();                                  // the S loads of this thread are done before its partner may write P over them
       asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -334,7 +332,7 @@ flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ 
       }
       // P = exp2((s - m_ref) * scale * log2e) as bf16 pairs, straight into tensor memory: the K-major A operand of the PV MMA
       const float mb = m_ref * a.sl2e;
-      float l_blk = 0.f;
+      float lq[4] = {0.f, 0.f, 0.f, 0.f};                 // independent partial sums, for the same reason
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         uint32_t packed[16];
@@ -342,13 +340,13 @@ flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ 
         for (int i = 0; i < 32; i += 2) {
           const float p0 = ex2(fmaf(__uint_as_float(sr[cc][i]), a.sl2e, -mb)), p1 = ex2(fmaf(__uint_as_float(sr[cc][i + 1]), a.sl2e, -mb));
           const __nv_bfloat162 b = __floats2bfloat162_rn(p0, p1);
-          l_blk += __low2float(b) + __high2float(b);      // the sum of what the tensor cores will multiply
+          lq[(i >> 1) & 3] += __low2float(b) + __high2float(b);      // the sum of what the tensor cores will multiply
           packed[i >> 1] = *reinterpret_cast<const uint32_t*>(&b);
         }
 #pragma unroll
         for (int i = 0; i < 16; ++i) sr[cc >> 1][(cc & 1) * 16 + i] = packed[i];   // gather the pairs of both groups into one 32-column store
       }
-      l_run += l_blk;
+      l_run += (lq[0] + lq[1]) + (lq[2] + lq[3]);
       static_assert(NC == 2, "one 32-column tcgen05.st per thread carries its 64 probabilities");
       tmem_st32(tm_s0 + st * BKV + lane_addr + wg * 32, sr[0]);
       tmem_st_wait();
@@ -394,6 +392,259 @@ flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ 
   }
 }
 
+// ---- two q tiles per CTA ----------------------------------------------------------------------------------------------
+// The kernel above keeps one 128-row q tile per CTA and splits every row between two softmax warpgroups, which then hit
+// their exponentials (the MUFU pipe: 16 ex2 per clock per SM = 1024 clocks per 128 x 128 block) at the same time and
+// leave it idle the rest of the block.  Here a CTA owns TWO adjacent q tiles of one head; warpgroup t is the softmax of
+// tile t (a thread = a whole row: no exchange, no CTA barrier in the loop) and the single MMA lane interleaves the two
+// tiles -- PV_A(j), QK_A(j + 1), PV_B(j), QK_B(j + 1) -- so that one tile's softmax runs under the other's MMAs and
+// the two warpgroups drift out of phase.  Both tiles multiply the same K / V^T blocks (half the shared-memory traffic
+// per q row).  Tensor memory: S_A | S_B | O_A | O_B, 128 columns each; P_t overwrites the first 64 columns of S_t.
+template <int D>
+struct Smem2 {
+  static constexpr int kQt = BQ * D * 2;          // one q tile
+  static constexpr int kK = BKV * D * 2;
+  static constexpr int kV = D * BKV * 2;
+  static constexpr int kBars = 256;
+  static constexpr int kTotal = 2 * kQt + 2 * kK + 2 * kV + kBars + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+flash2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+              const __grid_constant__ CUtensorMap map_vt, const Args a) {
+  using S = Smem2<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* q_s = smem;                          // tile t at q_s + t * kQt
+  uint8_t* k_s = smem + 2 * S::kQt;             // two stages
+  uint8_t* v_s = k_s + 2 * S::kK;               // two stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(v_s + 2 * S::kV);
+  uint64_t* q_full = bars;            // 1
+  uint64_t* k_full = bars + 1;        // 2 stages
+  uint64_t* k_empty = bars + 3;
+  uint64_t* v_full = bars + 5;
+  uint64_t* v_empty = bars + 7;
+  uint64_t* s_full = bars + 9;        // per tile
+  uint64_t* p_full = bars + 11;       // per tile, 128 arrivals
+  uint64_t* o_full = bars + 13;       // per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.y, kvh = h / (a.n_q / a.n_kv);
+  const int qp = (int)gridDim.x - 1 - (int)blockIdx.x;   // the long tile pairs (late q rows) are scheduled first
+  const int q0 = qp * 2 * BQ;
+  const int ctx = a.pos0 + a.T;
+  int nb[2];                                             // K / V blocks each tile attends to (0: the tile lies past T)
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int q0t = q0 + t * BQ;
+    nb[t] = q0t < a.T ? (min(ctx, a.pos0 + q0t + BQ) + BKV - 1) / BKV : 0;
+  }
+  const int n_blk = max(nb[0], nb[1]);
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_q)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_k)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_vt)) : "memory");
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 128);
+      mbar_init(&o_full[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, (nb[1] > 0 ? 2 : 1) * S::kQt);
+      for (int t = 0; t < 2; ++t)
+        if (nb[t] > 0)
+          for (int kb = 0; kb < D / KB; ++kb) tma_load_2d(&map_q, q_full, q_s + t * S::kQt + kb * (BQ * 128), kb * KB, h * a.T + q0 + t * BQ);
+      for (int j = 0; j < n_blk; ++j) {
+        const int st = j & 1;
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], S::kK);
+        for (int kb = 0; kb < D / KB; ++kb)
+          tma_load_2d(&map_k, &k_full[st], k_s + st * S::kK + kb * (BKV * 128), kb * KB, kvh * a.max_ctx + j * BKV);
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], S::kV);
+        for (int kb = 0; kb < BKV / KB; ++kb)
+          tma_load_2d(&map_vt, &v_full[st], v_s + st * S::kV + kb * (D * 128), j * BKV + kb * KB, kvh * D);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = instr_desc(BQ, BKV), idesc_o = instr_desc(BQ, D);
+      auto qk = [&](int t, int j) {   // S_t = Q_t K_j^T
+        const uint32_t qa = smem_u32(q_s + t * S::kQt), ka = smem_u32(k_s + (j & 1) * S::kK);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off_q = (k / 4) * (BQ * 128) + (k % 4) * 32, off_k = (k / 4) * (BKV * 128) + (k % 4) * 32;
+          umma(tmem_base + t * BKV, smem_desc_sw128(qa + off_q), smem_desc_sw128(ka + off_k), idesc_s, k != 0);
+        }
+        umma_commit(&s_full[t]);
+      };
+      auto pv = [&](int t, int j) {   // O_t += P_t V_j, P_t from tensor memory (over the first half of S_t)
+        mbar_wait(&p_full[t], j & 1);
+        tc_fence_after();
+        const uint32_t va = smem_u32(v_s + (j & 1) * S::kV);
+#pragma unroll
+        for (int k = 0; k < BKV / 16; ++k) {
+          const uint32_t off_v = (k / 4) * (D * 128) + (k % 4) * 32;
+          umma_ts(tmem_base + (2 + t) * BKV, tmem_base + t * BKV + k * 8, smem_desc_sw128(va + off_v), idesc_o, (j | k) != 0);
+        }
+        umma_commit(&o_full[t]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      for (int t = 0; t < 2; ++t)
+        if (nb[t] > 0) qk(t, 0);
+      umma_commit(&k_empty[0]);
+      for (int j = 0; j < n_blk; ++j) {
+        const int st = j & 1;
+        const bool next = j + 1 < n_blk;
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        if (next) mbar_wait(&k_full[st ^ 1], ((j + 1) >> 1) & 1);
+        tc_fence_after();
+        for (int t = 0; t < 2; ++t) {
+          if (j < nb[t]) pv(t, j);
+          if (j + 1 < nb[t]) qk(t, j + 1);
+        }
+        umma_commit(&v_empty[st]);               // V^T_j may be overwritten
+        if (next) umma_commit(&k_empty[st ^ 1]); // and K_{j+1}
+      }
+    }
+  } else {
+    const int t = (warp - 2) >> 2;              // the q tile of this warpgroup
+    if (nb[t] > 0) {
+      const int quarter = warp & 3;             // the TMEM lanes this warp may access
+      const int row = quarter * 32 + lane;      // q row of the tile = TMEM lane
+      const int q0t = q0 + t * BQ;
+      const int q_pos = a.pos0 + q0t + row;
+      const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+      const uint32_t ts = tmem_base + t * BKV + lane_addr, to = tmem_base + (2 + t) * BKV + lane_addr;
+      constexpr float kRaise = 8.f;             // log2 of the largest P tolerated before the reference maximum is raised
+      float m_ref = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < nb[t]; ++j) {
+        const int kv0 = j * BKV;
+        const bool diag = kv0 + BKV - 1 > a.pos0 + q0t;
+        mbar_wait(&s_full[t], j & 1);
+        tc_fence_after();
+        uint32_t sr[4][32];                     // the whole S row: one trip to tensor memory
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(ts + c * 32, sr[c]);
+        tmem_ld_wait();
+        if (diag) {
+          const int lim = q_pos - kv0;          // columns 0 .. lim are visible to the row
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i > lim) sr[c][i] = 0xff800000u;   // -inf: exp2 gives exactly 0 below
+        }
+        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sr[c][i]));
+        const float m_blk = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+        if (j == 0) {
+          m_ref = m_blk;                        // column 0 of block 0 is visible to every row: finite
+        } else {
+          const bool raise = (m_blk - m_ref) * a.sl2e > kRaise;
+          if (__any_sync(0xffffffffu, raise)) { // rare: rescale this warp's rows of O in tensor memory
+            mbar_wait(&o_full[t], (j - 1) & 1); // every PV product issued so far has been added
+            tc_fence_after();
+            const float alpha = raise ? ex2((m_ref - m_blk) * a.sl2e) : 1.f;
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t r[32];
+              tmem_ld32(to + c * 32, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+              tmem_st32(to + c * 32, r);
+            }
+            tmem_st_wait();
+            if (raise) { l_run *= alpha; m_ref = m_blk; }
+          }
+        }
+        // P = exp2((s - m_ref) * scale * log2e) as bf16 pairs, gathered into the first two register groups
+        const float mb = m_ref * a.sl2e;
+        float lq[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float p0 = ex2(fmaf(__uint_as_float(sr[c][i]), a.sl2e, -mb)), p1 = ex2(fmaf(__uint_as_float(sr[c][i + 1]), a.sl2e, -mb));
+            const __nv_bfloat162 b = __floats2bfloat162_rn(p0, p1);
+            lq[(i >> 1) & 3] += __low2float(b) + __high2float(b);   // the sum of what the tensor cores will multiply
+            packed[i >> 1] = *reinterpret_cast<const uint32_t*>(&b);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) sr[c >> 1][(c & 1) * 16 + i] = packed[i];
+        }
+        l_run += (lq[0] + lq[1]) + (lq[2] + lq[3]);
+        tmem_st32(ts, sr[0]);
+        tmem_st32(ts + 32, sr[1]);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[t]);
+      }
+      mbar_wait(&o_full[t], (nb[t] - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l_run;
+      const int tok = q0t + row;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(to + c * 32, r);
+        tmem_ld_wait();
+        if (tok < a.T) {
+          __nv_bfloat16* dst = a.out + (long long)tok * a.n_q * D + h * D + c * 32;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const float v0 = __uint_as_float(r[i + e]) * inv;
+              const float v1 = __uint_as_float(r[i + e + 1]) * inv;
+              const __nv_bfloat162 b = __floats2bfloat162_rn(v0, v1);
+              hi[e >> 1] = *reinterpret_cast<const uint32_t*>(&b);
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(v0 - __low2float(b), v1 - __high2float(b));
+              lo[e >> 1] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
+            *reinterpret_cast<uint4*>(dst + i) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            if (a.parts > 1) *reinterpret_cast<uint4*>(dst + a.plane_stride + i) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          }
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(512) : "memory");
+  }
+}
+
 // V^T [n_kv][D][ctx_pad] bf16 from the cache layout [n_kv][max_ctx][D]; columns >= ctx are zero.  grid (ctx_pad / 64, n_kv)
 template <int D>
 __global__ void vt_kernel(const __nv_bfloat16* __restrict__ v, __nv_bfloat16* __restrict__ vt, int max_ctx, int ctx, int ctx_pad) {
@@ -425,6 +676,7 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 static thread_local char g_err[256] = "";
+static int g_one_tile = 0;   // adamk_prefill_attention_set_kernel(): 1 = always the one-tile kernel (A/B measurements, tests)
 
 // 2-D bf16 tensor [rows, cols] row-major, box [box_rows, 64 columns], 128-byte swizzle
 static bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols, int box_rows) {
@@ -455,9 +707,14 @@ static int run(const void* q, const void* k_cache, const void* vt, const Args& a
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(flash_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<D>::kTotal) != cudaSuccess) return ADAMK_PF_E_CUDA;
+    if (cudaFuncSetAttribute(flash2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem2<D>::kTotal) != cudaSuccess) return ADAMK_PF_E_CUDA;
     configured = true;
   }
-  flash_kernel<D><<<dim3((a.T + BQ - 1) / BQ, a.n_q), kThreads, Smem<D>::kTotal, stream>>>(mq, mk, mv, a);
+  // one q tile per CTA for a pass of at most one tile (a second tile would idle half the CTA), tile pairs otherwise
+  if (a.T <= BQ || g_one_tile)
+    flash_kernel<D><<<dim3((a.T + BQ - 1) / BQ, a.n_q), kThreads, Smem<D>::kTotal, stream>>>(mq, mk, mv, a);
+  else
+    flash2_kernel<D><<<dim3((a.T + 2 * BQ - 1) / (2 * BQ), a.n_q), kThreads, Smem2<D>::kTotal, stream>>>(mq, mk, mv, a);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     snprintf(g_err, sizeof g_err, "prefill attention launch: %s", cudaGetErrorString(e));
@@ -471,6 +728,8 @@ static int run(const void* q, const void* k_cache, const void* vt, const Args& a
 extern "C" {
 
 const char* adamk_prefill_attention_last_error(void) { return fa::g_err; }
+
+void adamk_prefill_attention_set_kernel(int one_tile) { fa::g_one_tile = one_tile ? 1 : 0; }
 
 int adamk_prefill_vt(const void* v_cache, int n_kv, int D, int max_ctx, int ctx, int ctx_pad, void* vt, adamk_pf_stream stream) {
   if (v_cache == nullptr || vt == nullptr || n_kv < 1 || (D != 64 && D != 128) || ctx < 1 || ctx > max_ctx || ctx_pad < ctx || ctx_pad % 64)

@@ -35,7 +35,7 @@ PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_p
                    "adamk_prefill_gemm_plan", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
                    "adamk_prefill_split", "adamk_prefill_rope_store", "adamk_batch_rope_store", "adamk_batch_attention_workspace",
                    "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split", "adamk_batch_embed",
-                   "adamk_prefill_attention", "adamk_prefill_vt", "adamk_prefill_attention_last_error",
+                   "adamk_prefill_attention", "adamk_prefill_vt", "adamk_prefill_attention_last_error", "adamk_prefill_attention_set_kernel",
                    "adamk_prefill", "adamk_prefill_workspace_bytes", "adamk_prefill_pass_last_error")
 
 
@@ -74,6 +74,8 @@ def _lib():
         lib.adamk_prefill_attention.argtypes = [vp, vp, vp, i, i, i, i, i, i, i, vp, i, vp]
         lib.adamk_prefill_vt.argtypes = [vp, i, i, i, i, i, vp, vp]
         lib.adamk_prefill_attention_last_error.restype = C.c_char_p
+        lib.adamk_prefill_attention_set_kernel.argtypes = [i]
+        lib.adamk_prefill_attention_set_kernel.restype = None
         lib.adamk_prefill_pass_last_error.restype = C.c_char_p
         lib.adamk_prefill_workspace_bytes.argtypes = [C.POINTER(_PassModel), i, i, i]
         lib.adamk_prefill_workspace_bytes.restype = C.c_size_t
