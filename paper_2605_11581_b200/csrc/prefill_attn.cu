@@ -332,21 +332,26 @@ flash_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ 
       }
       // P = exp2((s - m_ref) * scale * log2e) as bf16 pairs, straight into tensor memory: the K-major A operand of the PV MMA
       const float mb = m_ref * a.sl2e;
-      float lq[4] = {0.f, 0.f, 0.f, 0.f};                 // independent partial sums, for the same reason
+      const float2 sc2 = make_float2(a.sl2e, a.sl2e), mb2 = make_float2(-mb, -mb);   // packed FFMA2 / FADD2 around the MUFU.EX2
+      float2 lq[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         uint32_t packed[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(sr[cc][i]), a.sl2e, -mb)), p1 = ex2(fmaf(__uint_as_float(sr[cc][i + 1]), a.sl2e, -mb));
-          const __nv_bfloat162 b = __floats2bfloat162_rn(p0, p1);
-          lq[(i >> 1) & 3] += __low2float(b) + __high2float(b);      // the sum of what the tensor cores will multiply
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[cc][i]), __uint_as_float(sr[cc][i + 1])), sc2, mb2);
+          const float2 pp = make_float2(ex2(x.x), ex2(x.y));
+          lq[(i >> 1) & 3] = __fadd2_rn(lq[(i >> 1) & 3], pp);       // row sum over the fp32 exponentials
+          const __nv_bfloat162 b = __floats2bfloat162_rn(pp.x, pp.y);
           packed[i >> 1] = *reinterpret_cast<const uint32_t*>(&b);
         }
 #pragma unroll
         for (int i = 0; i < 16; ++i) sr[cc >> 1][(cc & 1) * 16 + i] = packed[i];   // gather the pairs of both groups into one 32-column store
       }
-      l_run += (lq[0] + lq[1]) + (lq[2] + lq[3]);
+      {
+        const float2 s01 = __fadd2_rn(lq[0], lq[1]), s23 = __fadd2_rn(lq[2], lq[3]);
+        l_run += (s01.x + s01.y) + (s23.x + s23.y);
+      }
       static_assert(NC == 2, "one 32-column tcgen05.st per thread carries its 64 probabilities");
       tmem_st32(tm_s0 + st * BKV + lane_addr + wg * 32, sr[0]);
       tmem_st_wait();
@@ -586,21 +591,29 @@ flash2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         }
         // P = exp2((s - m_ref) * scale * log2e) as bf16 pairs, gathered into the first two register groups
         const float mb = m_ref * a.sl2e;
-        float lq[4] = {0.f, 0.f, 0.f, 0.f};
+        // packed arithmetic (FFMA2 / FADD2) around the 128 MUFU.EX2 of the row: the exponentials alone keep this warp's
+        // SFU busy for 1024 clocks per block, everything else in the loop is issue slots the warp loses on top of that.
+        // The row sum is taken over the fp32 exponentials (the usual flash-attention choice), not their bf16 roundings.
+        const float2 sc2 = make_float2(a.sl2e, a.sl2e), mb2 = make_float2(-mb, -mb);
+        float2 lq[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
-            const float p0 = ex2(fmaf(__uint_as_float(sr[c][i]), a.sl2e, -mb)), p1 = ex2(fmaf(__uint_as_float(sr[c][i + 1]), a.sl2e, -mb));
-            const __nv_bfloat162 b = __floats2bfloat162_rn(p0, p1);
-            lq[(i >> 1) & 3] += __low2float(b) + __high2float(b);   // the sum of what the tensor cores will multiply
+            const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[c][i]), __uint_as_float(sr[c][i + 1])), sc2, mb2);
+            const float2 pp = make_float2(ex2(x.x), ex2(x.y));
+            lq[(i >> 1) & 3] = __fadd2_rn(lq[(i >> 1) & 3], pp);
+            const __nv_bfloat162 b = __floats2bfloat162_rn(pp.x, pp.y);
             packed[i >> 1] = *reinterpret_cast<const uint32_t*>(&b);
           }
 #pragma unroll
           for (int i = 0; i < 16; ++i) sr[c >> 1][(c & 1) * 16 + i] = packed[i];
         }
-        l_run += (lq[0] + lq[1]) + (lq[2] + lq[3]);
+        {
+          const float2 s01 = __fadd2_rn(lq[0], lq[1]), s23 = __fadd2_rn(lq[2], lq[3]);
+          l_run += (s01.x + s01.y) + (s23.x + s23.y);
+        }
         tmem_st32(ts, sr[0]);
         tmem_st32(ts + 32, sr[1]);
         tmem_st_wait();
