@@ -235,6 +235,24 @@ def test_hybrid_engine_tensor_prefill_matches_oracle(cfg):
                                                       (128, 28, 4, 4096, 0, 1), (128, 4, 2, 1500, 0, 12), (64, 4, 2, 900, 70, 12),
                                                       (128, 2, 1, 2048, 0, 40)])
 def test_flash_attention_matches_fp32_reference(D, nq, nkv, T, pos0, qscale):
+    _flash_case(D, nq, nkv, T, pos0, qscale)
+
+
+@pytest.mark.parametrize("D,nq,nkv,T,pos0,qscale", [(128, 4, 2, 700, 0, 1), (64, 4, 2, 300, 70, 12), (128, 2, 1, 1024, 0, 40)])
+def test_flash_attention_one_tile_kernel_on_long_passes(D, nq, nkv, T, pos0, qscale):
+    """`adamk_prefill_attention_set_kernel(1)`: the one-tile kernel (two softmax warpgroups per q row) is what short passes
+    use; forced onto longer ones it must agree with the same reference (ring wrap-around, lazy rescale)."""
+    from paper_2605_11581_b200.prefill import _lib
+
+    lib = _lib()
+    lib.adamk_prefill_attention_set_kernel(1)
+    try:
+        _flash_case(D, nq, nkv, T, pos0, qscale)
+    finally:
+        lib.adamk_prefill_attention_set_kernel(0)
+
+
+def _flash_case(D, nq, nkv, T, pos0, qscale):
     """csrc/prefill_attn.cu (tcgen05 QK^T and PV, softmax out of tensor memory) against a plain fp32 causal attention on
     the same bf16 q / k / v: GQA group sizes 1-7, ragged last tiles, a single row, chunked prefill (pos0 > 0), the
     Qwen2.5-7B shape at 4096 tokens.  ``qscale`` > 1 sharpens the scores (maxima that keep growing by many powers of two
