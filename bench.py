@@ -62,7 +62,8 @@ def measured_peak() -> tuple[float, str]:
 
 
 class ClockSampler:
-    """nvidia-smi clock / throttle sampling during the timed region."""
+    """SM clock / throttle-reason sampling during the timed region: NVML from a thread (first sample taken
+    synchronously, so a short region is never left without one), `nvidia-smi -lms` as the fallback."""
 
     QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -70,8 +71,45 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index, self.rows, self.proc = index, [], None
+        self.sm, self.mx, self.flags, self._stop, self._thread, self._nvml = [], None, set(), False, None, None
+
+    def _sample_nvml(self):
+        nv, h = self._nvml
+        self.sm.append(int(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+        r = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h) if hasattr(nv, "nvmlDeviceGetCurrentClocksEventReasons")
+                else nv.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+        for name, bit in (("hw_slowdown", 0x8), ("sw_power_cap", 0x4), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40)):
+            if r & bit:
+                self.flags.add(name)
 
     def start(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            # CUDA_VISIBLE_DEVICES may renumber the devices: address the GPU by the UUID torch reports
+            uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+            try:
+                h = nv.nvmlDeviceGetHandleByUUID(("GPU-" + uuid).encode())
+            except Exception:
+                h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self._nvml = (nv, h)
+            self.mx = int(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._sample_nvml()
+
+            def loop():
+                while not self._stop:
+                    try:
+                        self._sample_nvml()
+                    except Exception:
+                        break
+                    time.sleep(0.02)
+
+            self._thread = threading.Thread(target=loop, daemon=True)
+            self._thread.start()
+            return
+        except Exception:
+            self._nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
@@ -85,6 +123,17 @@ class ClockSampler:
             self.rows.append([c.strip() for c in line.split(",")])
 
     def stop(self) -> dict:
+        if self._nvml is not None:
+            try:
+                self._sample_nvml()              # one more, still under load
+            except Exception:
+                pass
+            self._stop = True
+            if self._thread is not None:
+                self._thread.join(timeout=1.0)
+            sm = sorted(self.sm)
+            return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": self.mx, "reasons": sorted(self.flags),
+                    "samples": len(sm), "source": "nvml"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.15)
@@ -94,7 +143,7 @@ class ClockSampler:
         reasons = sorted({n for r in self.rows if len(r) >= 6 for n, v in zip(names, r[2:6]) if v.startswith("Active")})
         mx = [int(r[1]) for r in self.rows if len(r) > 1 and r[1].isdigit()]
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(sm)}
+                "reasons": reasons, "samples": len(sm), "source": "nvidia-smi"}
 
 
 def cpu_decode_sample(cfg, weights, prompt, n_steps: int, warmup: int = 2) -> dict:
