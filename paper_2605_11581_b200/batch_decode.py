@@ -100,6 +100,7 @@ class BatchedDecoder:
         self.logits = torch.empty(B, cfg.vocab, dtype=f32, device=dev)
         ws = self.lib.adamk_batch_attention_workspace(B, nq, D, max_ctx)
         self.attn_ws = torch.empty(ws // 4, dtype=f32, device=dev)
+        self.argmax_ws = torch.zeros(self.lib.adamk_batch_argmax_workspace(B), dtype=torch.uint8, device=dev)   # zero once; the kernel re-arms it
         self._graph = None
         self.launches_per_step = 0
         self.steps = 0
@@ -174,8 +175,8 @@ class BatchedDecoder:
                                           _ptr(self.logits), self.logits.numel(), st))
         gemm(self.xp, self.lm_head, self.logits, epilogue=EPI_ATOMIC)
         adv = auto_advance
-        _ok(lib.adamk_batch_argmax(_ptr(self.logits), B, cfg.vocab, _ptr(self.next_token), _ptr(self.tokens) if adv else None,
-                                   _ptr(self.positions) if adv else None, st))
+        _ok(lib.adamk_batch_argmax_sliced(_ptr(self.logits), B, cfg.vocab, _ptr(self.argmax_ws), _ptr(self.next_token),
+                                          _ptr(self.tokens) if adv else None, _ptr(self.positions) if adv else None, st))
         return n + 4
 
     def capture(self) -> None:

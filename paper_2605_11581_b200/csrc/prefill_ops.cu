@@ -448,6 +448,61 @@ __global__ void batch_argmax_kernel(const float* __restrict__ logits, int V, int
   }
 }
 
+// The same pick with every row cut into kArgmaxSlices slices (grid (slices, B)): a row of 150 K logits scanned by ONE
+// CTA took 73 us -- a whole GEMM's worth of a decode step.  Each CTA leaves (value, index) of its slice in `scratch`
+// [B][slices]; the last CTA of a row to finish (a counter per row, zero before the first call and reset by that CTA)
+// reduces the slices in slice order, so ties still go to the lowest index.
+constexpr int kArgmaxSlices = 64;
+__global__ void batch_argmax_sliced_kernel(const float* __restrict__ logits, int V, unsigned long long* __restrict__ scratch,
+                                           int32_t* __restrict__ next, int32_t* tokens, int32_t* positions) {
+  griddep_sync();
+  const int b = blockIdx.y, sl = blockIdx.x, S = gridDim.x;
+  const int per = (V + S - 1) / S, lo = sl * per, hi = min(V, lo + per);
+  const float* row = logits + (long long)b * V;
+  float best = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const float v = row[i];
+    if (v > best) { best = v; idx = i; }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  __shared__ int last;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > best || (ov == best && oi < idx)) { best = ov; idx = oi; }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sv[warp] = best; si[warp] = idx; }
+  __syncthreads();
+  unsigned long long* part = scratch + (long long)b * (S + 1);   // S partial records, then the row's counter
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (blockDim.x >> 5); ++w)
+      if (sv[w] > best || (sv[w] == best && si[w] < idx)) { best = sv[w]; idx = si[w]; }
+    part[sl] = ((unsigned long long)__float_as_uint(best) << 32) | (unsigned)idx;
+    __threadfence();
+    last = atomicAdd(reinterpret_cast<unsigned*>(part + S), 1u) == (unsigned)(S - 1);
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  best = -INFINITY;
+  idx = 0x7fffffff;
+  for (int k = 0; k < S; ++k) {
+    const unsigned long long rec = *reinterpret_cast<volatile unsigned long long*>(part + k);
+    const float v = __uint_as_float((unsigned)(rec >> 32));
+    const int i = (int)(unsigned)rec;
+    if (v > best || (v == best && i < idx)) { best = v; idx = i; }
+  }
+  if (idx < 0 || idx >= V) idx = 0;   // a row of NaN / -inf has no maximum: a valid token id, not the sentinel
+  next[b] = idx;
+  if (tokens != nullptr) tokens[b] = idx;
+  if (positions != nullptr) positions[b] += 1;
+  *reinterpret_cast<unsigned*>(part + S) = 0u;   // ready for the next step
+}
+
 // act planes [P][B][I] = split(silu(gate) * up) from gu fp32 [B][2 I] whose columns interleave gate and up in blocks of
 // `block` features (the layout of the fused-SwiGLU GEMM weight).  grid (feature blocks, tokens).
 __global__ void swiglu_split_kernel(const float* __restrict__ gu, int I, int block, __nv_bfloat16* __restrict__ planes, long long plane_stride,
@@ -600,6 +655,16 @@ int adamk_batch_swiglu_split(const float* gu, int B, int I, int block, void* pla
   if (gu == nullptr || planes == nullptr || B <= 0 || I <= 0 || block <= 0 || I % block || (parts < 1 || parts > 3)) return ADAMK_PF_E_INVALID;
   pfo::launch(pfo::swiglu_split_kernel, dim3(dim3((I + 511) / 512, B)), dim3(512), 0, static_cast<cudaStream_t>(stream), gu, I, block, static_cast<__nv_bfloat16*>(planes), (long long)B * I, parts);
   return pfo::done("batch swiglu");
+}
+
+size_t adamk_batch_argmax_workspace(int B) { return B > 0 ? (size_t)B * (pfo::kArgmaxSlices + 1) * sizeof(unsigned long long) : 0; }
+
+int adamk_batch_argmax_sliced(const float* logits, int B, int V, void* scratch, int32_t* next, int32_t* tokens, int32_t* positions,
+                              adamk_pf_stream stream) {
+  if (logits == nullptr || next == nullptr || scratch == nullptr || B <= 0 || V <= 0) return ADAMK_PF_E_INVALID;
+  pfo::launch(pfo::batch_argmax_sliced_kernel, dim3(pfo::kArgmaxSlices, B), dim3(256), 0, static_cast<cudaStream_t>(stream), logits, V,
+              static_cast<unsigned long long*>(scratch), next, tokens, positions);
+  return pfo::done("batch argmax (sliced)");
 }
 
 int adamk_batch_argmax(const float* logits, int B, int V, int32_t* next, int32_t* tokens, int32_t* positions, adamk_pf_stream stream) {

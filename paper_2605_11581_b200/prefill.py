@@ -34,7 +34,7 @@ GU_BLOCK = 128   # features per gate / up block of the interleaved weight = half
 PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_prefill_set_walk", "adamk_prefill_set_trace", "adamk_prefill_prefetch_next",
                    "adamk_prefill_gemm_plan", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
                    "adamk_prefill_split", "adamk_prefill_rope_store", "adamk_batch_rope_store", "adamk_batch_attention_workspace",
-                   "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split", "adamk_batch_embed",
+                   "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_argmax_sliced", "adamk_batch_argmax_workspace", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split", "adamk_batch_embed",
                    "adamk_prefill_attention", "adamk_prefill_vt", "adamk_prefill_attention_last_error", "adamk_prefill_attention_set_kernel",
                    "adamk_prefill", "adamk_prefill_workspace_bytes", "adamk_prefill_pass_last_error")
 
@@ -88,6 +88,9 @@ def _lib():
         lib.adamk_batch_attention_workspace.restype = C.c_size_t
         lib.adamk_batch_attention.argtypes = [vp, vp, vp, vp, i, i, i, i, i, ll, vp, vp, i, vp]
         lib.adamk_batch_argmax.argtypes = [vp, i, i, vp, vp, vp, vp]
+        lib.adamk_batch_argmax_sliced.argtypes = [vp, i, i, vp, vp, vp, vp, vp]
+        lib.adamk_batch_argmax_workspace.argtypes = [i]
+        lib.adamk_batch_argmax_workspace.restype = C.c_size_t
         lib.adamk_batch_swiglu_split.argtypes = [vp, i, i, i, vp, i, vp]
         lib.adamk_batch_rmsnorm_split.argtypes = [vp, vp, f, i, i, vp, i, vp, ll, vp]
         _declared = True

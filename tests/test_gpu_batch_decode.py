@@ -81,6 +81,25 @@ def test_row_operators():
     P._ok(lib.adamk_batch_argmax(P._ptr(logits), 4, V, P._ptr(nxt), P._ptr(toks), P._ptr(pos), P._stream()))
     assert nxt.tolist() == logits.argmax(dim=1).tolist() and nxt[1].item() == 77 and nxt[2].item() == V - 1
     assert toks.tolist() == nxt.tolist() and pos.tolist() == [6, 7, 8, 9]
+    # the sliced pick (64 CTAs per row): same answers, the scratch re-arms itself, NaN rows give a valid id
+    for V2, rows in ((3000, 4), (151936, 3), (70, 2)):
+        lg = torch.randn(rows, V2, device="cuda", generator=g)
+        lg[0, 5] = lg[0, V2 - 1] = 99.0                    # tie across slices: the lowest index wins
+        if rows > 2:
+            lg[2] = float("nan")
+        ws = torch.zeros(lib.adamk_batch_argmax_workspace(rows), dtype=torch.uint8, device="cuda")
+        nxt2 = torch.full((rows,), -1, dtype=torch.int32, device="cuda")
+        toks2 = torch.zeros(rows, dtype=torch.int32, device="cuda")
+        pos2 = torch.arange(rows, dtype=torch.int32, device="cuda")
+        for rep in range(3):
+            P._ok(lib.adamk_batch_argmax_sliced(P._ptr(lg), rows, V2, P._ptr(ws), P._ptr(nxt2), P._ptr(toks2), P._ptr(pos2), P._stream()))
+        torch.cuda.synchronize()
+        want2 = lg.argmax(dim=1).tolist()
+        assert nxt2[0].item() == 5 and nxt2[1].item() == want2[1]
+        if rows > 2:
+            assert nxt2[2].item() == 0
+        assert toks2.tolist() == nxt2.tolist() and pos2.tolist() == [r + 3 for r in range(rows)]
+        assert (ws.view(torch.int64).view(rows, -1)[:, -1] == 0).all()      # counters back at zero
 
 
 def _run_parity(cfg, B, steps, oracle_cache, max_ctx=320, seed=11):
