@@ -98,12 +98,15 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bflo
 
 // planes[p][t][:] = split(h[t] * rsqrt(mean(h[t]^2) + eps) * gain)
 __global__ void rmsnorm_split_kernel(const float* __restrict__ h, const __nv_bfloat16* __restrict__ gain, float eps, int H,
-                                     __nv_bfloat16* __restrict__ planes, long long plane_stride, int parts, float4* zero, long long zero_n4) {
+                                     __nv_bfloat16* __restrict__ planes, long long plane_stride, int parts, float4* zero, long long zero_n4,
+                                     int rows) {
   griddep_sync();
   __shared__ float red[32];
   const long long t = blockIdx.x;
-  // batched decode: clear the fp32 targets of the atomic GEMMs that follow (saves a memset launch per layer)
+  // batched decode: clear the fp32 targets of the atomic GEMMs that follow (saves a memset launch per layer).  The grid
+  // may hold more CTAs than rows: a handful of rows would otherwise clear megabytes (the logits) by themselves.
   for (long long i = t * blockDim.x + threadIdx.x; i < zero_n4; i += (long long)gridDim.x * blockDim.x) zero[i] = make_float4(0, 0, 0, 0);
+  if (t >= rows) return;
   const float* row = h + t * H;
   float ss = 0.f;
   for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
@@ -546,7 +549,7 @@ int adamk_batch_embed(const int32_t* tokens, int T, const void* embed, int H, in
 int adamk_prefill_rmsnorm_split(const float* h, const void* gain, float eps, int T, int H, void* planes, int parts, adamk_pf_stream stream) {
   if (h == nullptr || gain == nullptr || planes == nullptr || T <= 0 || H <= 0 || H % 4 || (parts < 1 || parts > 3)) return ADAMK_PF_E_INVALID;
   pfo::launch(pfo::rmsnorm_split_kernel, dim3(T), dim3(256), 0, static_cast<cudaStream_t>(stream), h, static_cast<const __nv_bfloat16*>(gain), eps, H,
-                                                                             static_cast<__nv_bfloat16*>(planes), (long long)T * H, parts, nullptr, 0);
+                                                                             static_cast<__nv_bfloat16*>(planes), (long long)T * H, parts, nullptr, 0, T);
   return pfo::done("prefill rmsnorm");
 }
 
@@ -555,9 +558,13 @@ int adamk_batch_rmsnorm_split(const float* h, const void* gain, float eps, int B
   if (h == nullptr || gain == nullptr || planes == nullptr || B <= 0 || H <= 0 || H % 4 || (parts < 1 || parts > 3) || zero_n % 4 ||
       (reinterpret_cast<uintptr_t>(zero) & 15))
     return ADAMK_PF_E_INVALID;
-  pfo::launch(pfo::rmsnorm_split_kernel, dim3(B), dim3(256), 0, static_cast<cudaStream_t>(stream), h, static_cast<const __nv_bfloat16*>(gain), eps, H,
+  // one CTA per row, plus CTAs that only clear: ~16 KB of the zeroed region per CTA, at most one CTA per SM
+  long long grid = (zero != nullptr ? zero_n * 4 / 16384 : 0);
+  grid = grid > 148 ? 148 : grid;
+  grid = grid < B ? B : grid;
+  pfo::launch(pfo::rmsnorm_split_kernel, dim3((unsigned)grid), dim3(256), 0, static_cast<cudaStream_t>(stream), h, static_cast<const __nv_bfloat16*>(gain), eps, H,
                                                                              static_cast<__nv_bfloat16*>(planes), (long long)B * H, parts,
-                                                                             reinterpret_cast<float4*>(zero), zero_n / 4);
+                                                                             reinterpret_cast<float4*>(zero), zero_n / 4, B);
   return pfo::done("batch rmsnorm");
 }
 
