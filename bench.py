@@ -5,7 +5,7 @@
 
 A *step* is one decode step (one token) of BASELINE.json configs[1]:
 Qwen2.5-1.5B, random-init bf16, batch 1, after a 512-token prompt; K steps are
-timed after W warm-up steps (defaults 128 / 8).  One JSON line is printed by
+timed after W warm-up steps (defaults 128 / 16).  One JSON line is printed by
 rank 0:
 
   value      whole-job decode tokens/s with token/position state resident in HBM
@@ -398,7 +398,7 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=128)
-    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=16)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--model", default="qwen2.5-1.5b")
     ap.add_argument("--cpu-steps", type=int, default=48, help="decode steps of the bounded CPU-baseline sample")

@@ -274,16 +274,22 @@ class MegaKernelPlugin:
         if self._host_io is None:
             self._host_io = torch.zeros(3, dtype=torch.int32).pin_memory()
             self._host_np = self._host_io.numpy()
+            self._host_args = {}
         io = self._host_np
         io[0], io[1] = token, position
-        base = self._host_io.data_ptr()
-        _check(self.lib, self.lib.adamk_decode_step_host(
-            self._h, C.c_void_p(base), C.c_void_p(base + 4), 1,
-            C.c_void_p(self.tokens.data_ptr()), C.c_void_p(self.positions.data_ptr()),
-            C.c_void_p(self.k_cache.data_ptr()), C.c_void_p(self.v_cache.data_ptr()),
-            C.c_void_p(self.workspace.data_ptr()),
-            C.c_void_p(self.logits.data_ptr()) if want_logits else None,
-            C.c_void_p(self.next_token.data_ptr()), C.c_void_p(base + 8), self._stream_ptr()))
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        key = (bool(want_logits), stream)
+        args = self._host_args.get(key)
+        if args is None:        # every argument but the token and the position is fixed: converted once per (logits, stream)
+            base = self._host_io.data_ptr()
+            args = (self._h, C.c_void_p(base), C.c_void_p(base + 4), 1,
+                    C.c_void_p(self.tokens.data_ptr()), C.c_void_p(self.positions.data_ptr()),
+                    C.c_void_p(self.k_cache.data_ptr()), C.c_void_p(self.v_cache.data_ptr()),
+                    C.c_void_p(self.workspace.data_ptr()),
+                    C.c_void_p(self.logits.data_ptr()) if want_logits else None,
+                    C.c_void_p(self.next_token.data_ptr()), C.c_void_p(base + 8), C.c_void_p(stream))
+            self._host_args[key] = args
+        _check(self.lib, self.lib.adamk_decode_step_host(*args))
         self.launches += 1
         return int(io[2])
 
