@@ -44,7 +44,12 @@ const char* adamk_prefill_last_error(void);
 
 /* Launch the operators below with programmatic dependent launch (stream serialization attribute): each kernel's
  * prologue overlaps the previous kernel's tail and `griddepcontrol.wait` orders the data.  Process-wide, off by
- * default; the batched decode step (dozens of ~10 us kernels per layer) turns it on. */
+ * default; the batched decode step (dozens of ~10 us kernels per layer) turns it on.
+ *   0 = off; 1 = on; 2 = on, and every GEMM issues the WEIGHT boxes of its first pass over the shared-memory ring
+ *   ahead of the wait (the weight is constant data: only token rows, bias and outputs are ordered behind the previous
+ *   kernel) -- the batched decode default; 3 = 2 + the next k blocks of the CTA's weight share requested into L2
+ *   (measured slower than 2; kept for A/B, tools/batch_pdl_ab.py).  Modes 2 / 3 require that no kernel in the stream
+ *   writes a GEMM's weight operand. */
 void adamk_prefill_set_pdl(int on);
 
 /* Tile walk order of adamk_prefill_gemm, process-wide: -1 (default) = chosen per call -- tile column fastest when the

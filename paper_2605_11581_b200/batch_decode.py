@@ -45,7 +45,7 @@ class _SequenceCache:
 
 class BatchedDecoder:
     def __init__(self, cfg: ModelConfig, weights: DecoderWeights, batch: int, max_ctx: int, device: int = 0, planes: int | None = None,
-                 pdl: bool = False, l2_prefetch: bool = False):
+                 pdl: int = 2, l2_prefetch: bool = False):
         if not torch.cuda.is_available():
             raise AdamkError(-102, "no CUDA device: batched decode has no CPU fallback")
         if not 1 <= batch <= 128:
@@ -61,7 +61,10 @@ class BatchedDecoder:
         # every GEMM pulls the next GEMM's weight into L2 while it waits for its own (measured: -3.6 % step time on
         # Qwen2.5-1.5B at batch 8, +9 % on Qwen2.5-7B whose GEMMs are already bandwidth-bound; off by default)
         self.l2_prefetch = bool(l2_prefetch)
-        self.pdl = bool(pdl)            # programmatic dependent launch between the step's kernels (measured: no gain)
+        # programmatic dependent launch between the step's kernels (adamk_prefill_set_pdl): 1 = prologues overlap the previous
+        # kernel's tail (-3.6 % step time at batch 8), 2 = also the first ring pass of every GEMM's weights issued ahead of
+        # griddepcontrol.wait (-6.6 % at batch 8, -5 % at 16, +-0 at 64; profiles/r02_batch_pdl_ab.txt)
+        self.pdl = int(pdl)
         dev = self.device = torch.device("cuda", device)
         cos, sin = rope_table(cfg, max_ctx)
         self._rope = (cos.to(dev), sin.to(dev))

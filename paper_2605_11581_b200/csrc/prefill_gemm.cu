@@ -105,6 +105,11 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 }
 // Programmatic dependent launch: let the next kernel of the stream start its prologue now, and wait for the previous
 // kernel's results before touching global memory (both are no-ops for a launch without the attribute).
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {   // box -> L2 only
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y)
+               : "memory");
+}
+constexpr int kEarlyL2Blocks = 96;   // k blocks per CTA requested into L2 ahead of griddepcontrol.wait (8-32 KB each)
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -156,6 +161,7 @@ struct GemmArgs {
   int n_tiles_n;        // tile columns
   int stacked;          // EPI_ATOMIC with parts * T <= 128: the planes are consecutive rows of ONE token tile, K is walked
                         // once (the weight is read once), accumulator row r adds into output row r % T
+  int w_early;          // programmatic dependent launch: first ring pass of weight boxes issued ahead of griddepcontrol.wait
 };
 
 constexpr int BOXN = 64;            // weight rows per TMA box: the slice granularity of a tile
@@ -382,6 +388,35 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the weight operand is constant data, so the producer lane fills the (empty) ring
+  // with the weight boxes of its first kStages k blocks BEFORE waiting for the previous kernel; only the token
+  // rows, the accumulator targets and the bias wait.  A decode-sized launch otherwise spends 2.8-3.8 us on its
+  // first operands from cold HBM (tools/gemm_trace.py) with nothing in flight.
+  const bool producer = warp == 0 && lane == 0;
+  int pre = 0;   // ring stages whose weight boxes (and transaction count) were issued ahead of the wait
+  if (producer && g.w_early) {
+    int ahead = 0;   // k blocks past the ring whose weight boxes were requested into L2 (w_early >= 2)
+    const int ahead_max = g.w_early >= 2 ? kEarlyL2Blocks : 0;
+    for (int idx = blockIdx.x; idx < n_work && (pre < S::kStages || ahead < ahead_max); idx += gridDim.x) {
+      const Item it = decode_item<BN>(idx, g, m_tiles, kb_per_part);
+      const int boxes = it.w / BOXN;
+      const int n_kb = it.kb_len * (g.stacked ? 1 : g.parts);
+      for (int kb = 0; kb < n_kb && (pre < S::kStages || ahead < ahead_max); ++kb) {
+        const int part = kb / it.kb_len, k0 = (it.kb_lo + kb - part * it.kb_len) * BK;
+        if (pre < S::kStages) {
+          uint8_t* sa = smem + pre * S::kStage;
+          mbar_expect_tx(&full[pre], S::kStageA + boxes * BOXN * BK * 2);
+          for (int j = 0; j < boxes; ++j)
+            tma_load_2d(&map_w, &full[pre], sa + S::kStageA + j * (BOXN * BK * 2), k0, box_row<BN, EPI>(it, j));
+          ++pre;
+        } else {
+          if (part == 0 || g.stacked)   // the planes of an unstacked pass walk the same weight again
+            for (int j = 0; j < boxes; ++j) tma_prefetch_2d(&map_w, k0, box_row<BN, EPI>(it, j));
+          ++ahead;
+        }
+      }
+    }
+  }
   griddep_wait();   // everything above overlapped the previous kernel's tail
   if (threadIdx.x == 0) PF_STAMP(1);
 
@@ -389,19 +424,24 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int issued = 0;
       for (int idx = blockIdx.x; idx < n_work; idx += gridDim.x) {
         const Item it = decode_item<BN>(idx, g, m_tiles, kb_per_part);
         const int boxes = it.w / BOXN;
         const uint32_t bytes = S::kStageA + boxes * BOXN * BK * 2;
         const int n_kb = it.kb_len * (g.stacked ? 1 : g.parts);
-        for (int kb = 0; kb < n_kb; ++kb) {
+        for (int kb = 0; kb < n_kb; ++kb, ++issued) {
           const int part = kb / it.kb_len, k0 = (it.kb_lo + kb - part * it.kb_len) * BK;
-          mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStage;
-          mbar_expect_tx(&full[stage], bytes);
-          tma_load_2d(&map_x, &full[stage], sa, k0, part * g.T + it.m0);
-          for (int j = 0; j < boxes; ++j)
-            tma_load_2d(&map_w, &full[stage], sa + S::kStageA + j * (BOXN * BK * 2), k0, box_row<BN, EPI>(it, j));
+          if (issued < pre) {   // first pass over the ring: the weights are already on their way
+            tma_load_2d(&map_x, &full[stage], sa, k0, part * g.T + it.m0);
+          } else {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], bytes);
+            tma_load_2d(&map_x, &full[stage], sa, k0, part * g.T + it.m0);
+            for (int j = 0; j < boxes; ++j)
+              tma_load_2d(&map_w, &full[stage], sa + S::kStageA + j * (BOXN * BK * 2), k0, box_row<BN, EPI>(it, j));
+          }
           if (++stage == S::kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -823,6 +863,7 @@ static void apply_plan(GemmArgs& g, const Plan& p) {
   g.ksplit = p.ksplit;
   g.kb_per_split = p.kb_per_split;
   g.stacked = p.stacked;
+  g.w_early = g_pdl >= 2 ? g_pdl - 1 : 0;
 }
 
 template <int BN, int EPI>
@@ -899,7 +940,7 @@ extern "C" {
 const char* adamk_prefill_last_error(void) { return pf::g_err; }
 
 void adamk_prefill_set_walk(int mode) { pf::g_walk = mode < 0 ? -1 : (mode ? 1 : 0); }
-void adamk_prefill_set_pdl(int on) { pf::g_pdl = on ? 1 : 0; }
+void adamk_prefill_set_pdl(int on) { pf::g_pdl = on < 0 ? 0 : (on > 3 ? 3 : on); }
 
 void adamk_prefill_prefetch_next(const void* ptr, long long bytes) {
   pf::g_pf_ptr = static_cast<const uint8_t*>(ptr);

@@ -205,6 +205,34 @@ def test_gemm_hints_do_not_change_results():
     assert (outs[0] - outs[1]).abs().max().item() <= 1e-5      # fp32 atomics: order-dependent last bits only
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_weights_ahead_of_the_dependency_wait(mode):
+    """adamk_prefill_set_pdl modes: a producer kernel rewrites the token planes and clears the target right before
+    every GEMM of a chain (as the decode step's row kernels do); with the weight boxes of the first ring pass issued
+    ahead of griddepcontrol.wait (2) and the L2 requests past the ring (3) each GEMM must still see the planes of ITS
+    producer.  K = 8960 walks the ring many times, K = 256 leaves ring stages unused."""
+    from paper_2605_11581_b200 import prefill as P
+
+    lib = P._lib()
+    g = torch.Generator(device="cuda").manual_seed(17 + mode)
+    for K, N in ((8960, 1536), (256, 2048), (1536, 17920)):
+        w = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+        xs = [torch.randn(8, K, device="cuda", generator=g) for _ in range(6)]
+        planes = torch.zeros(3, 8, K, device="cuda", dtype=torch.bfloat16)
+        outs = [torch.zeros(8, N, device="cuda") for _ in xs]
+        lib.adamk_prefill_set_pdl(mode)
+        try:
+            for x, out in zip(xs, outs):    # split -> GEMM -> split -> GEMM ...: own kernels only, all with the attribute
+                P._ok(lib.adamk_prefill_split(P._ptr(x), x.numel(), P._ptr(planes), 3, P._stream()))
+                P.gemm(planes, w, out, epilogue=P.EPI_ATOMIC)
+        finally:
+            lib.adamk_prefill_set_pdl(0)
+        torch.cuda.synchronize()
+        for x, out in zip(xs, outs):
+            want = x.double() @ w.double().T
+            assert (out.double() - want).abs().max().item() <= 4e-5 * want.abs().max().item(), (mode, K, N)
+
+
 def test_full_size_qwen25_1p5b_prefill_and_batched_decode():
     """BASELINE.json configs[1] dimensions end to end on the tensor-core path: three prompts (64, 1 and 23 tokens)
     cached by the tcgen05 Prefill, then batched decode steps whose 151 936 logits per sequence are compared with the
