@@ -172,6 +172,12 @@ int adamk_decode_step_host(adamk_handle h, const int32_t* token_ids_host, const 
  * Fills `info` (8 ints: code, sm, task, tag seen, tag expected, detail, thread, -) if not NULL. */
 int adamk_device_status(adamk_handle h, int32_t* info);
 
+/* Re-arm a handle whose last step REJECTED its input (code 4: a position outside [0, max_ctx) or a token id outside
+ * the vocabulary, read from the device state another component advances).  Such a step leaves every CTA before it
+ * touches the cache, the workspace or the epoch, and does not trap: the context stays usable and, after this call,
+ * so is the handle.  Watchdog codes (1, 2, 3, 5) trap the kernel; for those this returns ADAMK_E_DEVICE. */
+int adamk_clear_device_status(adamk_handle h);
+
 /* Optional per-task timeline (the device analogue of the reference's
  * chrome_trace_events, /root/reference/pkg/src/mkplan/simulator.py:381-411):
  * when a device buffer of adamk_trace_bytes() is set, consumer thread 0 of every

@@ -315,6 +315,18 @@ __device__ __noinline__ void dev_fail(const KParams& p, int code, int task, int 
   __trap();
 }
 
+// A rejected input (DE_BAD_POS): recorded, not trapped -- every CTA reads the same token / position and leaves before
+// touching any state, so the context stays usable and adamk_clear_device_status() re-arms the handle.
+__device__ __noinline__ void dev_report(const KParams& p, int code, int task, int a, int b, int c) {
+  volatile int* s = p.status;
+  if (s) {
+    s[1] = blockIdx.x; s[2] = task; s[3] = a; s[4] = b; s[5] = c; s[6] = threadIdx.x;
+    __threadfence_system();
+    s[0] = code;
+    __threadfence_system();
+  }
+}
+
 __device__ __noinline__ void mbar_wait_slow(const KParams& p, uint32_t bar, uint32_t parity, int code, int task) {
   const long long t0 = clock64();
   // the Loader's waits (EMPTY / INFLIGHT) time out later than the consumers': the first report names the root cause
@@ -2024,7 +2036,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       int lpos = 0;
       if (!p.probe) {
         lpos = __ldcg(p.positions);
-        if (lpos < 0 || lpos >= p.max_ctx) return;  // the consumers report the error
+        const int ltok = __ldcg(p.tokens);
+        if (lpos < 0 || lpos >= p.max_ctx || ltok < 0 || ltok >= p.V * p.tp_size) return;  // the consumers report the error
       }
       // While the ring is full (consumers waiting on another SM) the Loader keeps HBM busy by
       // prefetching its own upcoming weight stages into L2, up to pf_window bytes past the ring.
@@ -2180,8 +2193,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
     pos = __ldcg(p.positions);
     c.epoch = ld_relaxed_u32(p.sync);
     if (pos < 0 || pos >= p.max_ctx || tok < 0 || tok >= p.V * p.tp_size) {
-      if (c.ctid == 0) dev_fail(p, DE_BAD_POS, -1, pos, tok, p.max_ctx);
-      return;
+      if (c.ctid == 0 && blockIdx.x == 0) dev_report(p, DE_BAD_POS, -1, pos, tok, p.max_ctx);
+      return;   // uniformly: same words read by every CTA, nothing published, no epoch bump
     }
   }
   for (int ti = tb; ti < te; ++ti) {
@@ -2529,6 +2542,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   const Task* tasks = reinterpret_cast<const Task*>(tt + kHeaderInts + h->n_sms + 1);
   if (sm_begin[0] != 0 || sm_begin[h->n_sms] != h->n_tasks) return bad("sm_begin does not cover the task list");
   size_t wbytes = 0;
+  int lm_seen = 0;
   for (int s = 0; s < h->n_sms; ++s)
     if (sm_begin[s] > sm_begin[s + 1]) return bad("sm_begin not monotone");
   const int qkv_rows = (d.n_q_heads + 2 * d.n_kv_heads) * d.head_dim;
@@ -2568,6 +2582,7 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
       continue;
     }
     if (t.type < T_QKV || t.type > T_LMHEAD) return bad("unknown task type");
+    if (t.type == T_LMHEAD) ++lm_seen;
     if (t.b > 0xffff || t.rt > 0xffff || t.kchunks > 0xffff || t.ktc > 0xffff || t.n_tiles > 0xffff || t.n_ktiles > 0xffff)
       return bad("task field exceeds the packed 16-bit range");
     int n_rows = 0, K = 0;
@@ -2600,6 +2615,9 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
     const size_t off = (size_t)(uint32_t)t.w_off * 16;
     wbytes = std::max(wbytes, off + task_stream_bytes(t));
   }
+  // lm_finish() publishes the token and bumps the epoch when its counter reaches n_lm_tasks - 1: a header that
+  // disagrees with the table would hang the step until the watchdog or end it early
+  if (lm_seen != h->n_lm_tasks) return bad("n_lm_tasks in the header differs from the number of LM-head tasks");
   h->packed_weight_bytes = align_up(wbytes, 256);
   // fp32 parameter tail
   h->fp_ln1 = 0; h->fp_ln2 = d.hidden; h->fp_bias = 2 * d.hidden; h->fp_qn = h->fp_bias + qkv_rows;
@@ -2919,6 +2937,15 @@ int adamk_set_trace(adamk_handle h, void* trace_buf) {
 }
 
 size_t adamk_trace_bytes(adamk_handle h) { return h ? (size_t)h->n_tasks * 8 * sizeof(unsigned long long) : 0; }
+
+int adamk_clear_device_status(adamk_handle h) {
+  if (!h) return fail(ADAMK_E_INVALID, "NULL handle");
+  const int code = h->status_host[0];
+  if (code == 0) return ADAMK_OK;
+  if (code != DE_BAD_POS) return fail(ADAMK_E_DEVICE, "the recorded device error trapped the kernel: the CUDA context is lost");
+  memset(h->status_host, 0, 64);
+  return ADAMK_OK;
+}
 
 int adamk_device_status(adamk_handle h, int32_t* info) {
   if (!h) return fail(ADAMK_E_INVALID, "NULL handle");

@@ -219,6 +219,39 @@ def test_error_paths():
     plug.close()
 
 
+def test_rejected_position_does_not_cost_the_context():
+    """A position at max_ctx or a token outside the vocabulary (device state another component advances) is REPORTED
+    (device code 4) without a trap: the free-running loop's step past the cache leaves cache, workspace and epoch
+    alone, later calls fail with the device-error code until `adamk_clear_device_status`, and after it the same
+    handle produces the oracle's logits again (adamk.cu bad-position path)."""
+    from paper_2605_11581_b200.plugin import AdamkError
+
+    cfg, max_ctx = TINY, 24
+    _, ref, plug = _setup(cfg, SCHEDS["c7f"], max_ctx=max_ctx)
+    g = torch.Generator().manual_seed(9)
+    prompt = torch.randint(0, cfg.vocab, (max_ctx,), generator=g).tolist()
+    for pos, tok in enumerate(prompt[:-1]):
+        out = plug.decode_step(tok, pos, want_logits=True)
+        want = ref.step(tok, pos)
+    plug.check()
+    good = out.logits.clone()
+    np.testing.assert_allclose(good.cpu().numpy().reshape(-1), want.numpy().reshape(-1), atol=2e-3, rtol=0)
+    k_before = plug.k_cache.clone()
+    for bad_tok, bad_pos in ((prompt[-1], max_ctx), (prompt[-1], -1), (cfg.vocab, 3), (-2, 3)):
+        plug.set_state(bad_tok, bad_pos)
+        plug.enqueue(want_logits=True, auto_advance=True)
+        with pytest.raises(AdamkError, match="device error 4"):
+            plug.check()
+        with pytest.raises(AdamkError):      # the handle stays closed until the caller acknowledges
+            plug.enqueue()
+        plug.clear_rejected_input()
+        assert int(plug.positions.item()) == bad_pos and torch.equal(plug.k_cache, k_before)
+    out = plug.decode_step(prompt[-2], max_ctx - 2, want_logits=True)     # same step as before the rejections
+    plug.check()
+    assert torch.equal(out.logits, good)
+    plug.close()
+
+
 def test_hybrid_engine_generate_matches_oracle():
     """Engine hook: prefill (decode-path backend) then a device-resident decode loop."""
     from oracle.decode_ref import RefDecoder

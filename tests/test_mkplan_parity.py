@@ -85,6 +85,28 @@ def test_threads_do_not_change_the_trace(tmp_path):
     assert a == b == (G / "s01.trace").read_bytes()
 
 
+@pytest.mark.parametrize("case", [c for c in MANIFEST["searches"] if c["name"] in ("s02", "s05", "s08")],
+                         ids=lambda c: c["name"])
+def test_worker_processes_do_not_change_the_trace(case, monkeypatch):
+    """MK_PLANNER_PROCS: base simulations and improvement passes in forked workers (what makes a full-dimension
+    search practical) -- the golden bytes at the golden budget, and the sequential bytes at budgets that run out inside
+    the base simulations, between a gap fill and its role rebalance, and one short of everything."""
+    inp = G / "inputs"
+    texts = [(inp / f"graph_{case['graph']}.json").read_text(), (inp / f"hw_{case['hw']}.json").read_text(),
+             (inp / f"space_{case['space']}.json").read_text()]
+    monkeypatch.setenv("MK_PLANNER_PROCS", "3")
+    full = search.run_search(*texts, budget=case["budget"])
+    assert search.serialize_trace(full) == (G / f"{case['name']}.trace").read_bytes()
+    kept, simulated = full.stats["kept"], full.stats["simulated"]
+    for budget in sorted({max(1, kept // 2), kept + 1, kept + 2, kept + 7, max(1, simulated - 1)}):
+        if budget >= case["budget"]:
+            continue
+        monkeypatch.setenv("MK_PLANNER_PROCS", "3")
+        forked = search.serialize_trace(search.run_search(*texts, budget=budget))
+        monkeypatch.setenv("MK_PLANNER_PROCS", "0")
+        assert forked == search.serialize_trace(search.run_search(*texts, budget=budget, parallel=1)), budget
+
+
 def test_round_trip_rebuild_and_compare():
     inp = G / "inputs"
     data = (G / "s07.trace").read_bytes()
