@@ -94,7 +94,10 @@ const char* adamk_last_error(void);
  * table blob (task_table.py: header, per-SM ranges, 64-byte task records).
  * The table is validated against the description and the device, then copied
  * to the GPU.  tp_rank/tp_size select the tensor-parallel shard (1 GPU: 0/1;
- * tp_size 2, 4 or 8 otherwise). */
+ * tp_size 2, 4 or 8 otherwise).  The handle belongs to the CUDA device that is
+ * current at this call: every buffer and stream later passed with it must live
+ * on that device, and a step may be issued from a thread whose current device
+ * differs (the library switches for the launch and switches back). */
 int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task_table_bytes,
                  int tp_rank, int tp_size, adamk_handle* out);
 void adamk_destroy(adamk_handle h);

@@ -2443,6 +2443,7 @@ struct AdamkHandle_ {
   AdamkModelDesc desc{};
   int n_sms = 0, C = 0, n_stage = 0, stage_bytes = 0, n_tasks = 0, batch = 0, inflight = 0;
   int attn_chunks = 0, attn_min_chunk = 0, scratch_bytes = 0, n_lm_tasks = 0, poll_sleep_ns = 0, task_cache_bytes = 0, pf_window_kb = 0, pace = 0, poll_inflight = 0, fuse_down = 0, w4a16 = 0;
+  int device = 0, dev_sms = 0;     // the device current at adamk_create owns the handle
   const unsigned* d_sm_stream = nullptr;
   size_t packed_weight_bytes = 0;  // matrix streams only
   size_t fparam_floats = 0;
@@ -2495,6 +2496,11 @@ int adamk_create(const AdamkModelDesc* desc, const void* task_table, size_t task
   auto h = new AdamkHandle_();
   h->desc = *desc;
   h->tp_rank = tp_rank; h->tp_size = tp_size;
+  if (cudaGetDevice(&h->device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&h->dev_sms, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess) {
+    delete h;
+    return fail(ADAMK_E_CUDA, "no current CUDA device");
+  }
   h->n_sms = tt[2]; h->C = tt[3]; h->n_stage = tt[4]; h->stage_bytes = tt[5]; h->n_tasks = tt[6]; h->batch = tt[7];
   h->inflight = tt[8]; h->attn_chunks = tt[9]; h->attn_min_chunk = tt[10]; h->scratch_bytes = tt[11];
   h->n_lm_tasks = tt[12]; h->poll_sleep_ns = tt[14] & 0xffff; h->stream_down = !((tt[14] >> 16) & 1); h->pf_window_kb = tt[15] & 0xffff; h->pace = (tt[15] >> 16) & 0x7fff; h->poll_inflight = (tt[14] >> 20) & 0xf; h->fuse_down = (tt[14] >> 24) & 1; h->w4a16 = (tt[14] >> 26) & 1;
@@ -2862,10 +2868,16 @@ static int fill_params(adamk_handle h, KParams& p, void* workspace) {
 }
 
 static int launch(adamk_handle h, const KParams& p, cudaStream_t stream) {
-  int dev = 0, sms = 0;
-  CUDA_TRY(cudaGetDevice(&dev));
-  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  if (sms < h->n_sms) return fail(ADAMK_E_INVALID, "task table was built for more SMs than this device has");
+  // The handle belongs to the device that was current at adamk_create (its task table, status block and SM count):
+  // a caller whose thread has another device current is switched for the launch and switched back.
+  if (h->dev_sms < h->n_sms) return fail(ADAMK_E_INVALID, "task table was built for more SMs than this device has");
+  int cur = 0;
+  CUDA_TRY(cudaGetDevice(&cur));
+  struct DeviceGuard {
+    int back;
+    ~DeviceGuard() { if (back >= 0) cudaSetDevice(back); }
+  } guard{cur != h->device ? cur : -1};
+  if (cur != h->device) CUDA_TRY(cudaSetDevice(h->device));
   void* args[] = {(void*)&p};
   // cooperative launch: all CTAs must be co-resident (they poll each other's outputs)
   const bool tp = h->tp_size > 1;

@@ -157,7 +157,8 @@ __global__ void rope_store_kernel(const RopeArgs a) {
   if (pos < 0 || pos >= a.max_ctx) return;   // a sequence past its cache: nothing is written (no out-of-bounds K / V / table access)
   __nv_bfloat16* k_cache = a.k_cache + t * a.seq_stride;
   __nv_bfloat16* v_cache = a.v_cache + t * a.seq_stride;
-  for (int hd = threadIdx.x >> 5; hd < heads; hd += nw) {
+  // gridDim.y spreads the heads of a token over CTAs (batched decode: a few tokens, latency- not work-bound)
+  for (int hd = blockIdx.y * nw + (threadIdx.x >> 5); hd < heads; hd += nw * gridDim.y) {
     const float* x = row + hd * a.D;
     if (hd >= a.n_q + a.n_kv) {   // value head: plain bf16 store
       __nv_bfloat16* dst = v_cache + ((long long)(hd - a.n_q - a.n_kv) * a.max_ctx + pos) * a.D;
@@ -597,7 +598,8 @@ int adamk_batch_rope_store(const float* qkv, int B, int n_q, int n_kv, int D, co
   pfo::RopeArgs a{qkv, static_cast<const __nv_bfloat16*>(q_gain), static_cast<const __nv_bfloat16*>(k_gain), cos, sin, q_out,
                   static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), B, n_q, n_kv, D, max_ctx, 0, 0, eps,
                   positions, seq_stride};
-  pfo::launch(pfo::rope_store_kernel, dim3(B), dim3(256), 0, static_cast<cudaStream_t>(stream), a);
+  // one head per warp, two warps per CTA: 8 sequences x 16 heads are 64 CTAs instead of 8
+  pfo::launch(pfo::rope_store_kernel, dim3(B, (n_q + 2 * n_kv + 1) / 2), dim3(64), 0, static_cast<cudaStream_t>(stream), a);
   return pfo::done("batch rope");
 }
 
