@@ -52,6 +52,12 @@ const char* adamk_prefill_last_error(void);
  *   writes a GEMM's weight operand. */
 void adamk_prefill_set_pdl(int on);
 
+/* Decode-sized ATOMIC calls whose stacked planes hold at most 32 tokens each (batch <= 32): plane p is placed in rows
+ * [32 p, 32 p + T) of the 128-row token tile (a 3-D tensor map of the token operand), so that every plane's accumulator
+ * rows sit in their own tensor-memory lane quarter and one epilogue warp per plane sends the atomics instead of one
+ * warp for all planes.  Process-wide, on by default; 0 restores consecutive rows (A/B). */
+void adamk_prefill_set_plane_quarters(int on);
+
 /* Tile walk order of adamk_prefill_gemm, process-wide: -1 (default) = chosen per call -- tile column fastest when the
  * activation operand is larger than the weight and the weight fits L2 (the down projection of a long prompt), token
  * block fastest otherwise; 0 / 1 force one of them (A/B measurements, tools/ncu_prefill.py). */

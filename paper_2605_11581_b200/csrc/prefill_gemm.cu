@@ -76,6 +76,14 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Shared-memory matrix descriptor of a K-major tile stored as rows of 128 bytes with the 128-byte swizzle
 // (what the TMA box above writes): 8-row groups 1024 bytes apart (stride byte offset), descriptor version 1.
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
@@ -161,6 +169,9 @@ struct GemmArgs {
   int n_tiles_n;        // tile columns
   int stacked;          // EPI_ATOMIC with parts * T <= 128: the planes are consecutive rows of ONE token tile, K is walked
                         // once (the weight is read once), accumulator row r adds into output row r % T
+                        // 2 = the same with plane p at rows [32 p, 32 p + T) (T <= 32; 3-D tensor map of the token
+                        // operand): output row r % 32, every plane's rows in their own tensor-memory lane quarter
+  int quarters;         // host: this call's token map is the 3-D plane map (apply_plan turns stacked into 2)
   int w_early;          // programmatic dependent launch: first ring pass of weight boxes issued ahead of griddepcontrol.wait
 };
 
@@ -270,13 +281,15 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, uint32_t t_addr
     // atomics: summing them in the patch first was measured slower (2.55 vs 2.31 ms per batch-8 step).
     const int n0 = n_blk * BN + sub * w;
     float* out = static_cast<float*>(g.out);
-    const int live = min(32, (g.stacked ? g.parts * g.T : g.T) - row0);   // rows of this patch that hold data
+    // rows of this patch that hold data (stacked == 2: plane q sits in rows [32 q, 32 q + T), one TMEM lane quarter and
+    // therefore one epilogue warp per plane instead of one warp for all of them)
+    const int live = g.stacked == 2 ? min(32, g.T) : min(32, (g.stacked ? g.parts * g.T : g.T) - row0);
     const int n_it = (live + 3) >> 2;
     long long roff[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int row = row0 + i * 4 + sub_row;
-      roff[i] = (i * 4 + sub_row < live) ? (long long)(g.stacked ? row % g.T : row) * g.ldo : -1;
+      roff[i] = (i * 4 + sub_row < live) ? (long long)(g.stacked == 2 ? (row & 31) : g.stacked ? row % g.T : row) * g.ldo : -1;
     }
 #pragma unroll 1
     for (int c = 0; c < w; c += 64) {   // two tensor-memory loads in flight per wait (w is a multiple of 64)
@@ -434,11 +447,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
           const int part = kb / it.kb_len, k0 = (it.kb_lo + kb - part * it.kb_len) * BK;
           uint8_t* sa = smem + stage * S::kStage;
           if (issued < pre) {   // first pass over the ring: the weights are already on their way
-            tma_load_2d(&map_x, &full[stage], sa, k0, part * g.T + it.m0);
+            if (g.stacked == 2) tma_load_3d(&map_x, &full[stage], sa, k0, 0, 0);
+            else tma_load_2d(&map_x, &full[stage], sa, k0, part * g.T + it.m0);
           } else {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_expect_tx(&full[stage], bytes);
-            tma_load_2d(&map_x, &full[stage], sa, k0, part * g.T + it.m0);
+            if (g.stacked == 2) tma_load_3d(&map_x, &full[stage], sa, k0, 0, 0);   // plane p -> rows [32 p, 32 p + T)
+            else tma_load_2d(&map_x, &full[stage], sa, k0, part * g.T + it.m0);
             for (int j = 0; j < boxes; ++j)
               tma_load_2d(&map_w, &full[stage], sa + S::kStageA + j * (BOXN * BK * 2), k0, box_row<BN, EPI>(it, j));
           }
@@ -500,7 +515,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
       tc_fence_after();
       if (n == 0 && quarter == 0 && lane == 0) PF_STAMP(6);
       const uint32_t t_addr = tmem_base + as * BN + (uint32_t(quarter * 32) << 16);
-      const int rows_live = (EPI == ADAMK_PF_EPI_ATOMIC && g.stacked) ? g.parts * g.T : g.T;
+      const int rows_live = (EPI == ADAMK_PF_EPI_ATOMIC && g.stacked) ? (g.stacked == 2 ? g.parts * 32 : g.parts * g.T) : g.T;
       if (row0 < rows_live)   // decode-sized T: most warps own no live row and only hand the accumulator back
         epilogue_tile<BN, EPI>(g, t_addr, patch, row0, it.n_blk, it.sub, it.w, lane, sub_row, cg, it.kb_lo == 0);
       tc_fence_before();
@@ -773,6 +788,29 @@ static bool make_map(CUtensorMap* m, const void* base, long long rows, long long
   return true;
 }
 
+// The token operand of a stacked decode-sized call as bf16 [parts][T][cols]: box [4 planes][32 rows][64 columns], so
+// that plane p lands in rows [32 p, 32 p + T) of the 128-row tile (rows and planes outside the tensor are zero filled).
+static bool make_map_planes(CUtensorMap* m, const void* base, int parts, long long T, long long cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) {
+    snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled is not available from this driver");
+    return false;
+  }
+  cuuint64_t dims[3] = {cuuint64_t(cols), cuuint64_t(T), cuuint64_t(parts)};
+  cuuint64_t strides[2] = {cuuint64_t(cols) * 2, cuuint64_t(T) * cuuint64_t(cols) * 2};
+  cuuint32_t box[3] = {cuuint32_t(BK), 32, 4};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled (planes) failed with %d (parts %d T %lld cols %lld)", int(r), parts, T, cols);
+    return false;
+  }
+  return true;
+}
+
+static int g_quarters = 1;   // adamk_prefill_set_plane_quarters()
+
 // How one GEMM call is cut into work: tile shape, work items (whole tiles + column slices of the last wave), split-K.
 // Pure host arithmetic (adamk_prefill_gemm_plan exposes it; tests/test_prefill_plan.py checks it without a GPU).
 struct Plan {
@@ -862,7 +900,7 @@ static void apply_plan(GemmArgs& g, const Plan& p) {
   g.n_items = p.n_items;
   g.ksplit = p.ksplit;
   g.kb_per_split = p.kb_per_split;
-  g.stacked = p.stacked;
+  g.stacked = (p.stacked && g.quarters) ? 2 : p.stacked;
   g.w_early = g_pdl >= 2 ? g_pdl - 1 : 0;
 }
 
@@ -940,6 +978,7 @@ extern "C" {
 const char* adamk_prefill_last_error(void) { return pf::g_err; }
 
 void adamk_prefill_set_walk(int mode) { pf::g_walk = mode < 0 ? -1 : (mode ? 1 : 0); }
+void adamk_prefill_set_plane_quarters(int on) { pf::g_quarters = on ? 1 : 0; }
 void adamk_prefill_set_pdl(int on) { pf::g_pdl = on < 0 ? 0 : (on > 3 ? 3 : on); }
 
 void adamk_prefill_prefetch_next(const void* ptr, long long bytes) {
@@ -1012,8 +1051,14 @@ int adamk_prefill_gemm(const void* x_planes, int parts, int T, int K, const void
   }
   const Plan plan = plan_gemm(T, N, K, parts, epilogue, tile_n, n_sms);
   CUtensorMap mx, mw;
-  if (!make_map(&mx, x_planes, (long long)parts * T, K, BM) || !make_map(&mw, w, N, K, BOXN)) return ADAMK_PF_E_CUDA;
+  // a stacked decode-sized call with several planes of at most 32 tokens: one tensor-memory lane quarter per plane
+  const bool quarters = g_quarters && plan.stacked && plan.tile != ADAMK_PF_TILE_PAIR && epilogue == ADAMK_PF_EPI_ATOMIC && T <= 32 &&
+                        parts >= 2 && parts <= 4;
+  if (!(quarters ? make_map_planes(&mx, x_planes, parts, T, K) : make_map(&mx, x_planes, (long long)parts * T, K, BM)) ||
+      !make_map(&mw, w, N, K, BOXN))
+    return ADAMK_PF_E_CUDA;
   GemmArgs g{T, N, K, parts, ldo, bias, out, parts_out, part_stride, 0, 1, 0, 1, 0, g_pf_ptr, g_pf_bytes, g_trace, 0};
+  g.quarters = quarters ? 1 : 0;
   g_pf_ptr = nullptr;
   g_pf_bytes = 0;
   {

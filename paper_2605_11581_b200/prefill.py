@@ -31,7 +31,7 @@ TILE_AUTO, TILE_128, TILE_256, TILE_PAIR = 0, 128, 256, 512   # include/adamk_pr
 PREFETCH_MAX_BYTES = 64 << 20   # L2 prefetch hint cap (half of the 126 MB L2)
 GU_BLOCK = 128   # features per gate / up block of the interleaved weight = half of a 256-wide GEMM tile
 
-PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_prefill_set_walk", "adamk_prefill_set_trace", "adamk_prefill_prefetch_next",
+PREFILL_EXPORTS = ("adamk_prefill_last_error", "adamk_prefill_set_pdl", "adamk_prefill_set_plane_quarters", "adamk_prefill_set_walk", "adamk_prefill_set_trace", "adamk_prefill_prefetch_next",
                    "adamk_prefill_gemm_plan", "adamk_prefill_gemm", "adamk_prefill_embed", "adamk_prefill_rmsnorm_split",
                    "adamk_prefill_split", "adamk_prefill_rope_store", "adamk_batch_rope_store", "adamk_batch_attention_workspace",
                    "adamk_batch_attention", "adamk_batch_argmax", "adamk_batch_argmax_sliced", "adamk_batch_argmax_workspace", "adamk_batch_swiglu_split", "adamk_batch_rmsnorm_split", "adamk_batch_embed",
@@ -61,6 +61,8 @@ def _lib():
         lib.adamk_prefill_last_error.restype = C.c_char_p
         lib.adamk_prefill_set_pdl.argtypes = [i]
         lib.adamk_prefill_set_pdl.restype = None
+        lib.adamk_prefill_set_plane_quarters.argtypes = [i]
+        lib.adamk_prefill_set_plane_quarters.restype = None
         lib.adamk_prefill_set_walk.argtypes = [i]
         lib.adamk_prefill_set_walk.restype = None
         lib.adamk_prefill_set_trace.argtypes = [vp]
