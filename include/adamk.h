@@ -164,7 +164,9 @@ int adamk_decode_step(adamk_handle h, int32_t* token_ids, int32_t* positions, in
  * decode hook): copies token_ids / positions (HOST int32[batch], pinned memory for the copies
  * to be asynchronous) into the device state, launches the step (auto_advance = 0), copies the greedy next token
  * into next_token_host (HOST int32[batch]) and waits for the stream.  One library call per token instead of
- * three copies, a launch and a synchronise issued from the host language. */
+ * three copies, a launch and a synchronise issued from the host language.  A position outside [0, max_ctx) or a
+ * token id outside the vocabulary is refused with ADAMK_E_INVALID before anything is copied or launched (on the
+ * device the same input ends in a trap and a lost context: the device-resident loop must be bounded by its driver). */
 int adamk_decode_step_host(adamk_handle h, const int32_t* token_ids_host, const int32_t* positions_host, int batch,
                            int32_t* token_ids, int32_t* positions,
                            void* k_cache, void* v_cache, void* workspace,
@@ -174,12 +176,6 @@ int adamk_decode_step_host(adamk_handle h, const int32_t* token_ids_host, const 
 /* Poll the device-written status block (host-mapped); 0 = no error recorded.
  * Fills `info` (8 ints: code, sm, task, tag seen, tag expected, detail, thread, -) if not NULL. */
 int adamk_device_status(adamk_handle h, int32_t* info);
-
-/* Re-arm a handle whose last step REJECTED its input (code 4: a position outside [0, max_ctx) or a token id outside
- * the vocabulary, read from the device state another component advances).  Such a step leaves every CTA before it
- * touches the cache, the workspace or the epoch, and does not trap: the context stays usable and, after this call,
- * so is the handle.  Watchdog codes (1, 2, 3, 5) trap the kernel; for those this returns ADAMK_E_DEVICE. */
-int adamk_clear_device_status(adamk_handle h);
 
 /* Optional per-task timeline (the device analogue of the reference's
  * chrome_trace_events, /root/reference/pkg/src/mkplan/simulator.py:381-411):

@@ -315,18 +315,6 @@ __device__ __noinline__ void dev_fail(const KParams& p, int code, int task, int 
   __trap();
 }
 
-// A rejected input (DE_BAD_POS): recorded, not trapped -- every CTA reads the same token / position and leaves before
-// touching any state, so the context stays usable and adamk_clear_device_status() re-arms the handle.
-__device__ __noinline__ void dev_report(const KParams& p, int code, int task, int a, int b, int c) {
-  volatile int* s = p.status;
-  if (s) {
-    s[1] = blockIdx.x; s[2] = task; s[3] = a; s[4] = b; s[5] = c; s[6] = threadIdx.x;
-    __threadfence_system();
-    s[0] = code;
-    __threadfence_system();
-  }
-}
-
 __device__ __noinline__ void mbar_wait_slow(const KParams& p, uint32_t bar, uint32_t parity, int code, int task) {
   const long long t0 = clock64();
   // the Loader's waits (EMPTY / INFLIGHT) time out later than the consumers': the first report names the root cause
@@ -2036,8 +2024,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
       int lpos = 0;
       if (!p.probe) {
         lpos = __ldcg(p.positions);
-        const int ltok = __ldcg(p.tokens);
-        if (lpos < 0 || lpos >= p.max_ctx || ltok < 0 || ltok >= p.V * p.tp_size) return;  // the consumers report the error
+        if (lpos < 0 || lpos >= p.max_ctx) return;  // the consumers report the error
       }
       // While the ring is full (consumers waiting on another SM) the Loader keeps HBM busy by
       // prefetching its own upcoming weight stages into L2, up to pf_window bytes past the ring.
@@ -2193,8 +2180,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) adamk_decode_kernel(const __
     pos = __ldcg(p.positions);
     c.epoch = ld_relaxed_u32(p.sync);
     if (pos < 0 || pos >= p.max_ctx || tok < 0 || tok >= p.V * p.tp_size) {
-      if (c.ctid == 0 && blockIdx.x == 0) dev_report(p, DE_BAD_POS, -1, pos, tok, p.max_ctx);
-      return;   // uniformly: same words read by every CTA, nothing published, no epoch bump
+      if (c.ctid == 0) dev_fail(p, DE_BAD_POS, -1, pos, tok, p.max_ctx);
+      return;
     }
   }
   for (int ti = tb; ti < te; ++ti) {
@@ -2913,6 +2900,14 @@ int adamk_decode_step_host(adamk_handle h, const int32_t* token_ids_host, const 
   if (!token_ids_host || !positions_host || !next_token_host || !token_ids || !positions || !next_token_out)
     return fail(ADAMK_E_INVALID, "NULL argument");
   if (!h || batch != h->batch) return fail(ADAMK_E_INVALID, "batch does not match the task table");
+  // Host buffers: what the device would answer with a trap (sticky CUDA error) is refused here, before anything is
+  // copied or launched.  The device-resident loop (adamk_decode_step with auto_advance) is bounded by its driver.
+  for (int b = 0; b < batch; ++b) {
+    if (positions_host[b] < 0 || positions_host[b] >= h->desc.max_ctx)
+      return fail(ADAMK_E_INVALID, "position outside [0, max_ctx): the step would leave the KV cache");
+    if (token_ids_host[b] < 0 || token_ids_host[b] >= h->desc.vocab * h->tp_size)
+      return fail(ADAMK_E_INVALID, "token id outside the vocabulary");
+  }
   cudaStream_t st = (cudaStream_t)stream;
   const size_t nb = (size_t)batch * sizeof(int32_t);
   if (positions == token_ids + batch && positions_host == token_ids_host + batch) {   // adjacent state: one copy
@@ -2949,15 +2944,6 @@ int adamk_set_trace(adamk_handle h, void* trace_buf) {
 }
 
 size_t adamk_trace_bytes(adamk_handle h) { return h ? (size_t)h->n_tasks * 8 * sizeof(unsigned long long) : 0; }
-
-int adamk_clear_device_status(adamk_handle h) {
-  if (!h) return fail(ADAMK_E_INVALID, "NULL handle");
-  const int code = h->status_host[0];
-  if (code == 0) return ADAMK_OK;
-  if (code != DE_BAD_POS) return fail(ADAMK_E_DEVICE, "the recorded device error trapped the kernel: the CUDA context is lost");
-  memset(h->status_host, 0, 64);
-  return ADAMK_OK;
-}
 
 int adamk_device_status(adamk_handle h, int32_t* info) {
   if (!h) return fail(ADAMK_E_INVALID, "NULL handle");

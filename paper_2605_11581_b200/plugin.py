@@ -61,7 +61,7 @@ class _WeightPtrs(C.Structure):
 EXPORTS = (
     "adamk_abi_version", "adamk_device_sm_count", "adamk_last_error", "adamk_create", "adamk_destroy",
     "adamk_packed_bytes", "adamk_bind_weights", "adamk_bind_peers", "adamk_workspace_bytes",
-    "adamk_workspace_init", "adamk_kv_cache_bytes", "adamk_decode_step", "adamk_device_status", "adamk_clear_device_status",
+    "adamk_workspace_init", "adamk_kv_cache_bytes", "adamk_decode_step", "adamk_device_status",
     "adamk_stream_probe", "adamk_trace_bytes", "adamk_set_trace", "adamk_share_weights", "adamk_bind_weights_w4a16",
     "adamk_decode_step_host",
 )
@@ -102,8 +102,6 @@ def load_library() -> C.CDLL:
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     lib.adamk_decode_step_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int] + [C.c_void_p] * 9
     lib.adamk_device_status.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
-    lib.adamk_clear_device_status.argtypes = [C.c_void_p]
-    lib.adamk_clear_device_status.restype = C.c_int
     lib.adamk_stream_probe.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     if lib.adamk_abi_version() != ABI_VERSION:
         raise AdamkError(-101, "libadamk.so ABI version mismatch; rebuild")
@@ -305,12 +303,6 @@ class MegaKernelPlugin:
             if code != 0:
                 raise AdamkError(-5, f"device error {code}: sm={info[1]} task={info[2]} a={info[3]} "
                                      f"b={info[4]} c={info[5]} tid={info[6]}")
-
-    def clear_rejected_input(self) -> None:
-        """After a step that reported a rejected position / token (device code 4): re-arm the handle.  Raises for the
-        watchdog codes, which trap the kernel and lose the context."""
-        torch.cuda.synchronize(self.device)
-        _check(self.lib, self.lib.adamk_clear_device_status(self._h))
 
     def stream_probe(self, mode: int = 1) -> None:
         if not hasattr(self, "_sink"):

@@ -57,6 +57,40 @@ def test_gemm_atomic_split_k(T, K, N, parts):
         assert (out.double() - exact).abs().max().item() <= 8e-6 * max(1.0, exact.abs().max().item())
 
 
+@pytest.mark.parametrize("T,K,N,parts", [(1, 1536, 2048, 2), (8, 1536, 2048, 3), (8, 8960, 1536, 3), (16, 1536, 17920, 3), (31, 512, 328, 3),
+                                         (32, 1536, 1536, 3), (32, 3584, 4608, 2), (33, 1536, 1536, 3), (5, 64, 8, 2)])
+def test_one_lane_quarter_per_plane(T, K, N, parts):
+    """adamk_prefill_set_plane_quarters: with at most 32 tokens per plane the token operand goes through the 3-D tensor
+    map (plane p in rows [32 p, 32 p + T) of the tile) and one epilogue warp per plane sends the atomics; the product,
+    the bias (once per output row) and the rows beyond T must be exactly what the consecutive-row layout gives, up to
+    the order of the fp32 atomics.  T = 33 does not qualify and must be untouched by the switch."""
+    from paper_2605_11581_b200 import prefill as P
+
+    lib = P._lib()
+    g = torch.Generator(device="cuda").manual_seed(3 * T + K + N)
+    x = torch.randn(T, K, device="cuda", generator=g)
+    w = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g)
+    base = torch.randn(T, N, device="cuda", generator=g)
+    xp = _planes(x, parts)
+    want = base.double() + xp.double().sum(0) @ w.double().T + bias.double()
+    outs = []
+    try:
+        for on in (0, 1):
+            lib.adamk_prefill_set_plane_quarters(on)
+            guard = torch.full((T + 2, N), 7.0, device="cuda")      # rows T, T + 1 must stay untouched
+            guard[:T] = base
+            P.gemm(xp, w, guard[:T], bias=bias, epilogue=P.EPI_ATOMIC)
+            torch.cuda.synchronize()
+            assert torch.all(guard[T:] == 7.0)
+            outs.append(guard[:T].clone())
+    finally:
+        lib.adamk_prefill_set_plane_quarters(1)
+    for out in outs:
+        assert (out.double() - want).abs().max().item() <= 4e-5 * max(1.0, want.abs().max().item())
+    assert (outs[0] - outs[1]).abs().max().item() <= 2e-5 * max(1.0, want.abs().max().item())
+
+
 def test_row_operators():
     from paper_2605_11581_b200 import prefill as P
 

@@ -219,36 +219,25 @@ def test_error_paths():
     plug.close()
 
 
-def test_rejected_position_does_not_cost_the_context():
-    """A position at max_ctx or a token outside the vocabulary (device state another component advances) is REPORTED
-    (device code 4) without a trap: the free-running loop's step past the cache leaves cache, workspace and epoch
-    alone, later calls fail with the device-error code until `adamk_clear_device_status`, and after it the same
-    handle produces the oracle's logits again (adamk.cu bad-position path)."""
+def test_host_step_refuses_inputs_that_would_trap():
+    """`adamk_decode_step_host` validates the host token / position before copying or launching: a position at max_ctx
+    or a token outside the vocabulary is an AdamkError (ADAMK_E_INVALID), the CUDA context and the handle stay usable
+    and the next good step gives the oracle's logits (on the device the same input traps)."""
     from paper_2605_11581_b200.plugin import AdamkError
 
     cfg, max_ctx = TINY, 24
     _, ref, plug = _setup(cfg, SCHEDS["c7f"], max_ctx=max_ctx)
     g = torch.Generator().manual_seed(9)
-    prompt = torch.randint(0, cfg.vocab, (max_ctx,), generator=g).tolist()
-    for pos, tok in enumerate(prompt[:-1]):
-        out = plug.decode_step(tok, pos, want_logits=True)
+    prompt = torch.randint(0, cfg.vocab, (8,), generator=g).tolist()
+    for pos, tok in enumerate(prompt):
+        got = plug.decode_step_host(tok, pos, want_logits=True)
         want = ref.step(tok, pos)
+        for bad_tok, bad_pos in ((tok, max_ctx), (tok, -1), (cfg.vocab, pos), (-2, pos)):
+            with pytest.raises(AdamkError):
+                plug.decode_step_host(bad_tok, bad_pos)
     plug.check()
-    good = out.logits.clone()
-    np.testing.assert_allclose(good.cpu().numpy().reshape(-1), want.numpy().reshape(-1), atol=2e-3, rtol=0)
-    k_before = plug.k_cache.clone()
-    for bad_tok, bad_pos in ((prompt[-1], max_ctx), (prompt[-1], -1), (cfg.vocab, 3), (-2, 3)):
-        plug.set_state(bad_tok, bad_pos)
-        plug.enqueue(want_logits=True, auto_advance=True)
-        with pytest.raises(AdamkError, match="device error 4"):
-            plug.check()
-        with pytest.raises(AdamkError):      # the handle stays closed until the caller acknowledges
-            plug.enqueue()
-        plug.clear_rejected_input()
-        assert int(plug.positions.item()) == bad_pos and torch.equal(plug.k_cache, k_before)
-    out = plug.decode_step(prompt[-2], max_ctx - 2, want_logits=True)     # same step as before the rejections
-    plug.check()
-    assert torch.equal(out.logits, good)
+    assert got == int(want.argmax())
+    np.testing.assert_allclose(plug.logits.cpu().numpy().reshape(-1), want.numpy().reshape(-1), atol=2e-3, rtol=0)
     plug.close()
 
 
