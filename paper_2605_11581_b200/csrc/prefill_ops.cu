@@ -386,22 +386,28 @@ batch_attn_partial_kernel(const float* __restrict__ q, const __nv_bfloat16* __re
   }
 }
 
-// grid (n_q, B): merge the live splits and emit the attention output as bf16 planes [P][B][n_q * D].
+// grid (n_q, B), 4 D threads: merge the live splits and emit the attention output as bf16 planes [P][B][n_q * D].
+// The kernel is a chain of dependent L2 round trips, not work: thread group q = tid / D takes the splits
+// s = 8 (q + 4 k) .. + 7 (eight loads in flight each), so a 2K context is two round trips instead of five, and the four
+// partial (numerator, denominator) pairs meet in shared memory in a fixed order.
+constexpr int kMergeGroups = 4;
 template <int D>
-__global__ void batch_attn_merge_kernel(const float* __restrict__ part, const int32_t* __restrict__ positions, __nv_bfloat16* __restrict__ planes,
-                                        int B, int n_q, int splits, int parts) {
+__global__ void __launch_bounds__(kMergeGroups * D)
+batch_attn_merge_kernel(const float* __restrict__ part, const int32_t* __restrict__ positions, __nv_bfloat16* __restrict__ planes,
+                        int B, int n_q, int splits, int parts) {
   griddep_sync();
-  const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
+  const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x % D, q = threadIdx.x / D;
   const int live = min(max((positions[b] + kAttnChunk) / kAttnChunk, 1), splits);   // ceil((pos + 1) / chunk), inside the records that exist
   const float* src = part + ((long long)b * n_q + h) * splits * (D + 2);
   // the splits' maxima through shared memory (one load each, all in flight), then the weighted sums eight splits at a time
   extern __shared__ float m_s[];
-  for (int s = d; s < live; s += D) m_s[s] = src[s * (D + 2) + D];
+  __shared__ float num_s[kMergeGroups][D], den_s[kMergeGroups];
+  for (int s = threadIdx.x; s < live; s += kMergeGroups * D) m_s[s] = src[s * (D + 2) + D];
   __syncthreads();
   float M = -INFINITY;
   for (int s = 0; s < live; ++s) M = fmaxf(M, m_s[s]);
   float num = 0.f, den = 0.f;
-  for (int s0 = 0; s0 < live; s0 += 8) {
+  for (int s0 = 8 * q; s0 < live; s0 += 8 * kMergeGroups) {
     float ov[8], lv[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -416,8 +422,18 @@ __global__ void batch_attn_merge_kernel(const float* __restrict__ part, const in
       den = fmaf(w, lv[u], den);
     }
   }
-  const long long o = (long long)b * n_q * D + h * D + d;
-  put_split(planes + o, (long long)B * n_q * D, parts, num / den);
+  num_s[q][d] = num;
+  if (d == 0) den_s[q] = den;
+  __syncthreads();
+  if (q == 0) {
+#pragma unroll
+    for (int g = 1; g < kMergeGroups; ++g) {
+      num += num_s[g][d];
+      den += den_s[g];
+    }
+    const long long o = (long long)b * n_q * D + h * D + d;
+    put_split(planes + o, (long long)B * n_q * D, parts, num / den);
+  }
 }
 
 // grid B: greedy pick (lowest index on ties), written to next[b]; tokens / positions advanced in place when asked.
@@ -639,7 +655,7 @@ int adamk_batch_attention(const float* q, const void* k_cache, const void* v_cac
       case 8: ADAMK_ATTN_CASE(128, 8); break;
       default: ok = false;
     }
-    if (ok) pfo::launch(pfo::batch_attn_merge_kernel<128>, dim3(mgrid), dim3(128), splits * sizeof(float), s, workspace, positions, planes, B, n_q, splits, parts);
+    if (ok) pfo::launch(pfo::batch_attn_merge_kernel<128>, dim3(mgrid), dim3(pfo::kMergeGroups * 128), splits * sizeof(float), s, workspace, positions, planes, B, n_q, splits, parts);
   } else {
     switch (G) {
       case 1: ADAMK_ATTN_CASE(64, 1); break;
@@ -650,7 +666,7 @@ int adamk_batch_attention(const float* q, const void* k_cache, const void* v_cac
       case 8: ADAMK_ATTN_CASE(64, 8); break;
       default: ok = false;
     }
-    if (ok) pfo::launch(pfo::batch_attn_merge_kernel<64>, dim3(mgrid), dim3(64), splits * sizeof(float), s, workspace, positions, planes, B, n_q, splits, parts);
+    if (ok) pfo::launch(pfo::batch_attn_merge_kernel<64>, dim3(mgrid), dim3(pfo::kMergeGroups * 64), splits * sizeof(float), s, workspace, positions, planes, B, n_q, splits, parts);
   }
 #undef ADAMK_ATTN_CASE
   if (!ok) {
