@@ -97,25 +97,53 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bflo
 }
 
 // planes[p][t][:] = split(h[t] * rsqrt(mean(h[t]^2) + eps) * gain)
+constexpr int kNormKeep = 4;   // float4 pieces of a row a thread keeps in registers (256 threads: rows up to 4096 wide)
 __global__ void rmsnorm_split_kernel(const float* __restrict__ h, const __nv_bfloat16* __restrict__ gain, float eps, int H,
                                      __nv_bfloat16* __restrict__ planes, long long plane_stride, int parts, float4* zero, long long zero_n4,
                                      int rows) {
-  griddep_sync();
-  __shared__ float red[32];
+  // The kernel is a chain of L2 round trips between two GEMMs.  The gain is constant data: it is requested ahead of
+  // griddepcontrol.wait (under the previous kernel's tail), and the row stays in registers between the two passes.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long t = blockIdx.x;
+  const int step = blockDim.x * 4;
+  uint2 gk[kNormKeep];
+#pragma unroll
+  for (int n = 0; n < kNormKeep; ++n) {
+    const int i = threadIdx.x * 4 + n * step;
+    gk[n] = (t < rows && i < H) ? *reinterpret_cast<const uint2*>(gain + i) : make_uint2(0, 0);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __shared__ float red[32];
   // batched decode: clear the fp32 targets of the atomic GEMMs that follow (saves a memset launch per layer).  The grid
   // may hold more CTAs than rows: a handful of rows would otherwise clear megabytes (the logits) by themselves.
   for (long long i = t * blockDim.x + threadIdx.x; i < zero_n4; i += (long long)gridDim.x * blockDim.x) zero[i] = make_float4(0, 0, 0, 0);
   if (t >= rows) return;
   const float* row = h + t * H;
+  float4 vk[kNormKeep];
   float ss = 0.f;
-  for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
+#pragma unroll
+  for (int n = 0; n < kNormKeep; ++n) {
+    const int i = threadIdx.x * 4 + n * step;
+    vk[n] = i < H ? *reinterpret_cast<const float4*>(row + i) : make_float4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int n = 0; n < kNormKeep; ++n) ss += vk[n].x * vk[n].x + vk[n].y * vk[n].y + vk[n].z * vk[n].z + vk[n].w * vk[n].w;
+  for (int i = threadIdx.x * 4 + kNormKeep * step; i < H; i += step) {   // rows wider than the register window
     const float4 v = *reinterpret_cast<const float4*>(row + i);
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   const float inv = rsqrtf(block_sum(ss, red) / float(H) + eps);
   __nv_bfloat16* hi = planes + t * H;
-  for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
+#pragma unroll
+  for (int n = 0; n < kNormKeep; ++n) {
+    const int i = threadIdx.x * 4 + n * step;
+    if (i < H) {
+      const float x[4] = {vk[n].x * inv * __uint_as_float(gk[n].x << 16), vk[n].y * inv * __uint_as_float(gk[n].x & 0xffff0000u),
+                          vk[n].z * inv * __uint_as_float(gk[n].y << 16), vk[n].w * inv * __uint_as_float(gk[n].y & 0xffff0000u)};
+      put_split4(hi + i, plane_stride, parts, x);
+    }
+  }
+  for (int i = threadIdx.x * 4 + kNormKeep * step; i < H; i += step) {
     const float4 v = *reinterpret_cast<const float4*>(row + i);
     const uint2 graw = *reinterpret_cast<const uint2*>(gain + i);
     const float x[4] = {v.x * inv * __uint_as_float(graw.x << 16), v.y * inv * __uint_as_float(graw.x & 0xffff0000u),
